@@ -1,0 +1,265 @@
+/*
+ * gps.h -- C ABI of libgps.so, the B200 (sm_100a) implementation of the per-frame
+ * Gaussian-Plus-SDF mapping step of GPS-SLAM (arXiv 2509.11574).
+ *
+ * Citations: "P:n" = /root/reference/PAPER.md line n (section / equation named beside it);
+ * readings of points the paper leaves silent are numbered R-* in DESIGN.md §3.
+ *
+ * The paper states the problem as (Sec. 3.2.1 "SDF fusion"): "Given the k-th frame ...
+ * an RGB image C_k and a depth map D_k ... with the intrinsic camera parameters ... using the
+ * estimated camera pose T_{g,k} ... update the SDF and color values in a global hash table;
+ * afterwards the raycast is performed", then render with Eqs. 1-4 (Sec. 3.1) and
+ * optimise with the L1 loss of Eq. 7 using Adam (App. C).
+ * The four hot entry points are gps_fuse, gps_raycast, gps_render and gps_refine_step.
+ *
+ * General conventions (apply to every function below)
+ *  - Every pointer is a DEVICE pointer unless marked (host).  Device buffers are caller-owned,
+ *    contiguous, 16-byte aligned, and must stay alive until the stream work completes.
+ *  - `stream` is a cudaStream_t passed as an opaque pointer (NULL = legacy default stream).
+ *    All calls enqueue work on `stream` and return without synchronising, except the ones
+ *    whose name ends in _sync.
+ *  - Argument validation is synchronous and happens before any launch: a bad argument returns
+ *    GPS_ERR_INVALID_ARG and enqueues nothing.  Data invalidity is NOT an error: zero depth,
+ *    ray misses, culled Gaussians and an empty loss mask are ordinary data.
+ *  - CUDA launch failures return GPS_ERR_CUDA; gps_last_error() then holds a thread-local
+ *    message.  No C++ exception ever crosses this ABI.
+ *  - The library never allocates device memory on the hot path: the volume is allocated once
+ *    by gps_volume_create, everything else is caller-provided (workspace sizes come from the
+ *    *_workspace_size queries).
+ *  - Pixel (u,v) has integer coordinates at its centre; camera point X projects to
+ *    (fx*X.x/X.z + cx, fy*X.y/X.z + cy) (R-PIX).  Poses are camera->world, R row-major
+ *    (R-POSE); world->camera is X = R^T (P - t).
+ */
+#ifndef GPS_H_
+#define GPS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GPS_ABI_VERSION 1
+
+typedef void* gps_stream_t; /* a cudaStream_t */
+
+typedef enum {
+  GPS_OK = 0,
+  GPS_ERR_INVALID_ARG = 1,         /* synchronous argument check failed; nothing enqueued      */
+  GPS_ERR_OUT_OF_BLOCKS = 2,       /* a previous gps_fuse exceeded max_blocks (sticky)         */
+  GPS_ERR_WORKSPACE_TOO_SMALL = 3, /* ws_bytes below the *_workspace_size query                */
+  GPS_ERR_CUDA = 4,                /* CUDA runtime error; see gps_last_error()                 */
+  GPS_ERR_OOM = 5                  /* gps_volume_create could not allocate                     */
+} gps_status;
+
+/* Pinhole intrinsics shared by the depth and colour images (R-PIX).  width,height in pixels. */
+typedef struct {
+  float fx, fy, cx, cy;
+  int32_t width, height;
+} gps_intrinsics;
+
+/* Camera->world rigid transform T_{g,k}.  World point P = R * X_cam + t.             */
+typedef struct {
+  float R[9]; /* row-major */
+  float t[3];
+} gps_pose;
+
+/* ------------------------------------------------------------------------------------------
+ * Voxel-block hash volume ("update the SDF and color values in a global hash table";
+ * voxel contents P:60: truncated signed distance d(p) and colour c(p)).
+ * Library-owned and opaque.  Voxel (i,j,k) sits at world (i,j,k)*voxel_size; block b holds
+ * voxels 8b..8b+7 per axis (R-VOX).  A voxel is 8 bytes {f32 tsdf in [-1,1] (1 == mu);
+ * u8 r,g,b; u8 w}; a new block starts as tsdf = 1, rgb = 0, w = 0.
+ * ------------------------------------------------------------------------------------------ */
+typedef struct {
+  float voxel_size; /* metres; paper: 0.005                                          */
+  float mu;         /* truncation distance, metres; reading R-MU: 4*voxel_size = 0.02         */
+  int32_t w_max;    /* weight cap, 1..255; reading R-WMAX: 100                                */
+  float depth_min;  /* valid depth / ray range lower bound, metres (R-DEPTH: 0.1)             */
+  float depth_max;  /* valid depth / ray range upper bound, metres (R-DEPTH: 10)              */
+  int64_t max_blocks; /* block budget (>= 1); exceeding it is GPS_ERR_OUT_OF_BLOCKS          */
+  int64_t hash_slots; /* open-addressing slots, power of two, >= 2*max_blocks recommended   */
+} gps_volume_config;
+
+typedef struct gps_volume gps_volume;
+
+/* Allocates the hash table and block pool on the current device and initialises them on
+ * `stream`.  *out receives the handle (host).  Returns GPS_ERR_OOM if allocation fails.       */
+gps_status gps_volume_create(const gps_volume_config* cfg /*host*/, gps_stream_t stream,
+                             gps_volume** out /*host*/);
+/* Frees everything.  The caller must ensure no work on the volume is pending.               */
+void gps_volume_destroy(gps_volume* vol);
+/* Empties the volume (all blocks free, overflow flag cleared, frame counter reset).          */
+gps_status gps_volume_reset(gps_volume* vol, gps_stream_t stream);
+/* Synchronises `stream`, then reports the number of allocated blocks (may exceed the budget
+ * when an overflow happened), the budget, and the number of blocks marked visible by the last
+ * gps_fuse.  Any pointer may be NULL.  Returns GPS_ERR_OUT_OF_BLOCKS if overflow happened.   */
+gps_status gps_volume_stats_sync(gps_volume* vol, gps_stream_t stream, int64_t* n_blocks /*host*/,
+                                 int64_t* budget /*host*/, int64_t* n_visible /*host*/);
+
+/* gps_fuse -- Sec. 3.2.1 "SDF fusion", voxel data P:60.
+ * (1) Allocation: every valid depth pixel (depth/depth_scale in [depth_min, depth_max]) is
+ *     back-projected; its band [X(1-mu/|X|), X(1+mu/|X|)] is sampled at 5 equispaced points,
+ *     each transformed by the pose and mapped to block floor(W/(8*voxel_size)); every such
+ *     block is inserted into the hash (R-BAND) and marked visible for this frame.
+ * (2) Integration: every voxel of every visible block is projected to its nearest pixel; with
+ *     eta = depth - z: skipped if eta < -mu, else s = min(1, eta/mu),
+ *     tsdf <- (tsdf*w + s)/(w+1), rgb <- integer rounded running mean, w <- min(w+1, w_max)
+ *     (R-INT).  Allocation and tsdf use the prescribed fp32 sequences of DESIGN.md §4 (no FMA
+ *     contraction) so that they are bit-reproducible.
+ * depth: u16[height*width] row-major; metres = depth/depth_scale; 0 = invalid.
+ * rgba:  u8[height*width*4] row-major RGBA, colour in [0,255] (alpha ignored).
+ * Block-budget overflow is detected on device: the blocks that fit are integrated, a sticky
+ * flag is set, and the NEXT call on this volume (or gps_volume_stats_sync) returns
+ * GPS_ERR_OUT_OF_BLOCKS.  Must not run concurrently with any other call on the same volume.  */
+gps_status gps_fuse(gps_volume* vol, const gps_intrinsics* K /*host*/, const gps_pose* T /*host*/,
+                    const uint16_t* depth, float depth_scale, const uint8_t* rgba,
+                    gps_stream_t stream);
+
+/* gps_raycast -- Sec. 3.1 first pass: per-pixel march to the zero crossing, C_t by
+ * trilinear interpolation of the eight neighbouring voxels' colours, D_t by projecting V*.
+ * Reading R-RAY: unit ray from the camera centre; samples t_j = depth_min + j*voxel_size,
+ * j = 0..J, J = floor((double)(depth_max-depth_min)/(double)voxel_size); a sample is valid iff
+ * all 8 trilinear corners are allocated with w > 0; the first valid sample with tsdf <= 0 whose
+ * predecessor is valid and > 0 gives t* by linear interpolation; otherwise a miss.
+ * Unallocated blocks are skipped without changing the result.
+ * depth_out:  f32[height*width], camera z of V* in metres; 0 = miss.
+ * color_out:  f32[height*width*3], RGB in [0,1]; 0 on a miss.
+ * vertex_out: nullable f32[height*width*3], V* in world metres; 0 on a miss.                 */
+gps_status gps_raycast(const gps_volume* vol, const gps_intrinsics* K /*host*/,
+                       const gps_pose* T /*host*/, float* depth_out, float* color_out,
+                       float* vertex_out, gps_stream_t stream);
+
+/* ------------------------------------------------------------------------------------------
+ * Gaussians ("G = {p_i, sigma_i, r_i, s_i, SH_i} ... following 3DGS").  Caller-owned SoA,
+ * each array 16-byte aligned:
+ *   xyz[n*3] world position; log_scale[n*3] (s = exp); rot[n*4] quaternion (w,x,y,z),
+ *   normalised inside the forward pass (R-QUAT); opacity_raw[n] (sigma = sigmoid);
+ *   sh[n*(deg+1)^2*3] coefficient-major RGB triples (coefficient l,m of Gaussian i, channel c at
+ *   sh[(i*(deg+1)^2 + lm)*3 + c]).  sh_degree in {0,1,2,3} (R-SH: 3 for benchmarks).
+ * ------------------------------------------------------------------------------------------ */
+typedef struct {
+  int64_t n;
+  int32_t sh_degree;
+  float* xyz;
+  float* log_scale;
+  float* rot;
+  float* opacity_raw;
+  float* sh;
+} gps_gaussians;
+
+/* Rasteriser settings.  Defaults in brackets are the readings of DESIGN.md §3.            */
+typedef struct {
+  float eps_depth;  /* epsilon of Eqs. 1-2, metres [0.02] (R-EPS)                  */
+  float alpha_min;  /* alpha clamp of Eq. 3 text [1/255]                              */
+  float near_z;     /* Gaussians with camera z <= near_z are culled [0.2] (R-NEAR)           */
+  float lowpass;    /* added to the Sigma_2D diagonal, px^2 [0.3] (R-LOWPASS)                */
+  int32_t tile;     /* 8 or 16: tile edge in pixels (accelerator only: output independent)   */
+  int32_t tile_depth_precull; /* 0|1: drop list entries behind every pixel of the tile     */
+  int64_t max_pairs; /* capacity of the (tile,Gaussian) pair list; 0 = 32*n + 65536         */
+} gps_render_config;
+
+size_t gps_render_workspace_size(int64_t n, const gps_intrinsics* K /*host*/,
+                                 const gps_render_config* cfg /*host*/);
+
+/* gps_render -- Sec. 3.1 second pass: Eqs. 1-3 with the 3-sigma footprint reading
+ * (R-FOOT), composite Eq. 4 with W_t = 1:
+ *   C* = (C_t + C_G)/(1 + W_G).
+ * sdf_depth f32[H*W] (0 = miss: no depth test, R-MISS), sdf_color f32[H*W*3] in [0,1].
+ * out_color f32[H*W*3] = C*, out_weight f32[H*W] = W_G.
+ * target_rgba (nullable) u8[H*W*4] and loss_out (nullable device f32 scalar, needs target):
+ * loss_out <- the mean L1 of Eq. 7 over the mask {D_t > 0 or W_G > 0} (R-L1).
+ * ws: caller-provided device workspace of >= gps_render_workspace_size() bytes; it also keeps
+ * the tile lists of the last render for gps_debug_render_lists_sync.                         */
+gps_status gps_render(const gps_gaussians* g /*host struct, device arrays*/,
+                      const gps_intrinsics* K /*host*/, const gps_pose* T /*host*/,
+                      const float* sdf_depth, const float* sdf_color, const uint8_t* target_rgba,
+                      const gps_render_config* cfg /*host*/, void* ws, size_t ws_bytes,
+                      float* out_color, float* out_weight, float* loss_out, gps_stream_t stream);
+
+/* Adam (torch formula, "Libtorch"; per-group learning rates of App. C).        */
+typedef struct {
+  float lr_xyz;     /* 1.6e-4 */
+  float lr_sh0;     /* 2.5e-3 */
+  float lr_shrest;  /* 5e-4   */
+  float lr_opacity; /* 5e-2   */
+  float lr_scale;   /* 5e-3   */
+  float lr_rot;     /* 1e-3   */
+  float beta1;      /* 0.9    (R-ADAM) */
+  float beta2;      /* 0.999  */
+  float eps;        /* 1e-15  */
+} gps_adam_config;
+
+/* First and second moments, same shape (n, sh_degree) as the parameters; `step` is the number
+ * of Adam steps taken so far (host-side; incremented by gps_refine_step / gps_adam_step).     */
+typedef struct {
+  gps_gaussians m;
+  gps_gaussians v;
+  int64_t step;
+} gps_adam_state;
+
+/* One training view: pose, intrinsics, its cached SDF render ("recording the
+ * SDF-rendered color images and depth maps to avoid repeated raycast") and the target C_k.    */
+typedef struct {
+  gps_intrinsics K;
+  gps_pose T;
+  const float* sdf_depth;     /* f32[H*W]   */
+  const float* sdf_color;     /* f32[H*W*3] */
+  const uint8_t* target_rgba; /* u8[H*W*4]  */
+} gps_view;
+
+size_t gps_refine_workspace_size(int64_t n, const gps_intrinsics* K /*host, largest view*/,
+                                 const gps_render_config* cfg /*host*/, int32_t n_views);
+
+/* gps_refine_step -- one Gaussian optimisation iteration (Eq. 7):
+ * for each view: render (as gps_render) -> L1 loss and its gradient -> exact analytic backward
+ * to every raw parameter (R-GRAD); gradients of all views are summed; then one dense Adam
+ * update of every Gaussian (R-ADAM), state->step incremented on the host.
+ * loss_out (nullable device f32 scalar) <- sum over views of the per-view mean L1.
+ * grad_out (nullable; test hook) <- the summed raw-parameter gradient used by Adam, in the
+ * parameter SoA layout (n and sh_degree must equal g's).                                      */
+gps_status gps_refine_step(gps_gaussians* g, gps_adam_state* state /*host struct*/,
+                           const gps_view* views /*host array*/, int32_t n_views,
+                           const gps_render_config* rcfg /*host*/,
+                           const gps_adam_config* acfg /*host*/, void* ws, size_t ws_bytes,
+                           float* loss_out, const gps_gaussians* grad_out, gps_stream_t stream);
+
+/* gps_adam_step -- the Adam update of gps_refine_step alone, on caller-given gradients
+ * `grad` (parameter SoA layout).  Used to test the optimiser on identical gradients.          */
+gps_status gps_adam_step(gps_gaussians* g, gps_adam_state* state /*host struct*/,
+                         const gps_gaussians* grad, const gps_adam_config* acfg /*host*/,
+                         gps_stream_t stream);
+
+/* Synchronises `stream` and reports the pair count K of the last render held in `ws`, the pair
+ * capacity, and the number of Gaussians that survived culling.  Returns
+ * GPS_ERR_WORKSPACE_TOO_SMALL if K exceeded the capacity (that render dropped pairs).        */
+gps_status gps_render_stats_sync(const void* ws, gps_stream_t stream, int64_t* n_pairs /*host*/,
+                                 int64_t* capacity /*host*/, int64_t* n_visible /*host*/);
+
+/* ---- test / debug hooks (synchronise; never on the timed path) --------------------------- */
+
+/* Copies up to `cap` allocated blocks (any order): coords i32[cap*3], and if voxels != NULL
+ * their 512 voxels each (8-byte voxels, voxel (i,j,k) of a block at index i + 8j + 64k).
+ * *n (host) receives the number of allocated, backed blocks (may exceed cap).                */
+gps_status gps_debug_export_blocks_sync(const gps_volume* vol, gps_stream_t stream,
+                                        int32_t* coords, void* voxels, int64_t cap,
+                                        int64_t* n /*host*/);
+/* Copies the block coords marked visible by the last gps_fuse (any order).                  */
+gps_status gps_debug_export_visible_sync(const gps_volume* vol, gps_stream_t stream,
+                                         int32_t* coords, int64_t cap, int64_t* n /*host*/);
+/* Copies the per-tile Gaussian lists of the last render in `ws`: values u32[cap] (Gaussian
+ * indices, concatenated tile lists in tile-id order, each ascending by (depth bits, index)),
+ * ranges u32[2*n_tiles] ([start,end) per tile, row-major tile ids).  *K (host) = total pairs.
+ * With tile_depth_precull the ranges are the truncated ones.                                  */
+gps_status gps_debug_render_lists_sync(const void* ws, gps_stream_t stream, uint32_t* values,
+                                       int64_t cap, uint32_t* ranges, int64_t* K /*host*/);
+
+const char* gps_status_string(gps_status s);
+const char* gps_last_error(void); /* thread-local; "" if none */
+int gps_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GPS_H_ */
