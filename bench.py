@@ -1,0 +1,383 @@
+#!/usr/bin/env python3
+"""Benchmark of the GPS-SLAM mapping step on B200 (BASELINE.json metric: mapping frames/sec at
+1280x720, fuse + raycast + refine; HBM GB/s per kernel).
+
+One timed *step* = one delta_k interval of the paper's schedule on synthetic
+Azure-Kinect-shaped input (config cfg4, BASELINE.json configs[3]): 10 frames x (gps_fuse +
+gps_raycast), then at the round frame the 6 selected views are raycast once and 20
+single-view gps_refine_step iterations run (reading R-VIEW) over 200k Gaussians (SH degree 3).
+That covers every row of SURVEY §8(a).  value = frames / second (whole job, max over ranks).
+
+    python bench.py [--gpus N --steps K --warmup W]           # our CUDA path
+    python bench.py --impl reference ...                       # the CPU oracle arm
+Multi-GPU (torchrun): one independent sequence per rank, no data-path collective ("weak").
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg4")
+    ap.add_argument("--history", type=int, default=60, help="frames fused before warm-up (untimed)")
+    ap.add_argument("--gaussians", type=int, default=0, help="override N (0 = config)")
+    ap.add_argument("--sh-degree", type=int, default=3)
+    ap.add_argument("--tile", type=int, default=16)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=20.0, help="budget of the cpu_baseline sample")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------------------------
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class Clocks:
+    """nvidia-smi sampling of SM clocks and throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.p = None
+        self.path = os.path.join("/tmp", f"gps_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.f = open(self.path, "w")
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-i", str(self.idx), "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.p.terminate()
+        self.p.wait()
+        self.f.close()
+        rows = [l.strip().split(", ") for l in open(self.path) if l.strip()]
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[1]))
+                mx = float(r[2])
+                for nm, v in zip(names, r[5:9]):
+                    if v.strip() == "Active":
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                continue
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (copy, best of 10)"
+    except Exception:
+        return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+# ----------------------------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import gps_synth as S
+    import paper_2509_11574_b200 as G
+    from paper_2509_11574_b200 import _native as N
+    from paper_2509_11574_b200.pipeline import MappingPipeline
+
+    cfg = S.get_config(args.config)
+    if ws > 1:  # config 5: an independent sequence (different room and path) per GPU
+        cfg = S.get_config(args.config, seed=40 + rank)
+    dk = 10
+    n_frames = args.history + dk * (args.warmup + args.steps)
+    if not args.no_e2e:
+        n_frames += dk * args.steps
+    t0 = time.time()
+    scene = S.make_scene(cfg)
+    dc = S.pixel_rays(cfg, "cuda")
+    poses = S.trajectory(cfg, n_frames)
+    frames = []
+    for k in range(n_frames):
+        fr = S.render_frame(cfg, scene, *poses[k], k=k, device="cuda", dc=dc)
+        frames.append((fr.depth.contiguous(), fr.rgba.contiguous(), fr.R, fr.t))
+    del dc
+    n_g = args.gaussians or cfg.n_gaussians
+    gd = S.make_gaussians(cfg, n=n_g, sh_degree=args.sh_degree)
+    t_setup = time.time() - t0
+    cam = G.Camera(cfg.fx, cfg.fy, cfg.cx, cfg.cy, cfg.width, cfg.height)
+    vol = G.Volume(voxel_size=cfg.voxel_size, max_blocks=cfg.max_blocks, hash_slots=cfg.hash_slots)
+    g = G.Gaussians.from_dict(gd)
+    pipe = MappingPipeline(cam, g, vol, cfg.depth_scale, G.RenderConfig(tile=args.tile), seed=rank)
+    k = 0
+    for _ in range(args.history):  # build a steady-state volume (untimed, no rounds)
+        d, c, R, t = frames[k]
+        pipe.process_frame(k, d, c, R, t, refine=False)
+        k += 1
+
+    def run_steps(n_steps, host=None):
+        nonlocal k
+        for _ in range(n_steps):
+            for _ in range(dk):
+                if host is None:
+                    d, c, R, t = frames[k]
+                else:
+                    d, c = host[k]
+                    R, t = frames[k][2], frames[k][3]
+                pipe.process_frame(k, d, c, R, t)
+                k += 1
+            if host is not None:  # the step's result read back (D2H) on the stream
+                host["loss"][host["i"]].copy_(pipe.last_loss, non_blocking=True)
+                host["i"] += 1
+
+    # align so that every step ends with its round frame (k % 10 == 0 after the step's 10 frames)
+    while (k + dk - 1) % dk != 0:
+        d, c, R, t = frames[k]
+        pipe.process_frame(k, d, c, R, t, refine=False)
+        k += 1
+    run_steps(args.warmup)
+    torch.cuda.synchronize()
+    st = vol.stats()
+    if st["status"] != "GPS_OK":
+        raise RuntimeError(f"volume overflow during warm-up: {st}")
+    # ---------------- timed region (device-resident inputs) ----------------
+    clocks = Clocks(local)
+    stream = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    N._lib.gps_profile_enable(1)
+    ev0.record(stream)
+    run_steps(args.steps)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    prof = read_profile(N)
+    N._lib.gps_profile_enable(0)
+    rstats = pipe.ras.stats()
+    vstats = vol.stats()
+    ms_max = ms
+    if ws > 1:
+        tt = torch.tensor([ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms_max = float(tt.item())
+    frames_timed = args.steps * dk
+    value = frames_timed * ws / (ms_max / 1000.0)
+    # ---------------- end-to-end leg: host (pinned) frames, result read back ----------------
+    e2e = None
+    if not args.no_e2e:
+        host = {}
+        for j in range(k, k + dk * args.steps):
+            host[j] = (frames[j][0].cpu().pin_memory(), frames[j][1].cpu().pin_memory())
+        host["loss"] = [torch.empty(1, dtype=torch.float32).pin_memory() for _ in range(args.steps)]
+        host["i"] = 0
+        h2d = dk * (frames[k][0].numel() * 2 + frames[k][1].numel())
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        run_steps(args.steps, host)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1)
+        if ws > 1:
+            tt = torch.tensor([ems], device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ems = float(tt.item())
+        e2e = {"value": round(frames_timed * ws / (ems / 1000.0), 2), "unit": "frames/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 4,
+               "ms_per_step": round(ems / args.steps, 4),
+               "path": "MappingPipeline.process_frame with pinned-host depth/RGBA (H2D on the stream) + loss D2H"}
+    if ws > 1:
+        dist.barrier()
+    if rank != 0:
+        dist.destroy_process_group()
+        return None
+    # ---------------- roofline of the dominant kernel ----------------
+    peak, peak_src = peaks()
+    P = 11 + 3 * (args.sh_degree + 1) ** 2
+    per_launch = {}
+    # algorithmic bytes per launch: dense Adam reads p, m, v and the 2D gradient,
+    # writes p, m, v: 24 P + 48 B per Gaussian
+    per_launch["k_grad_adam"] = n_g * (24 * P + 48)
+    # integration reads + writes every voxel of every visible block: 16 B x 512 x B_vis
+    vis_total = vstats.get("visible_total", 0)
+    if prof["k_integrate"]["launches"]:
+        per_launch["k_integrate"] = 16 * 512 * vis_total / prof["k_integrate"]["launches"]
+    step_ms = ms / args.steps
+    dominant = max((kk for kk in prof if kk != "memset"), key=lambda kk: prof[kk]["ms"])
+    roof_k = dominant if dominant in per_launch else max(per_launch, key=lambda kk: prof[kk]["ms"])
+    avg = prof[roof_k]["ms"] / max(prof[roof_k]["launches"], 1)
+    achieved = per_launch[roof_k] / (avg / 1000.0) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            traffic = json.load(f).get(roof_k)
+    except Exception:
+        pass
+    roof = {"kernel": roof_k, "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
+            "algorithmic_bytes_per_launch": int(per_launch[roof_k]), "avg_launch_ms": round(avg, 5)}
+    shares = {kk: {"ms_per_step": round(v["ms"] / args.steps, 4), "launches_per_step": v["launches"] / args.steps,
+                   "share": round(v["ms"] / max(ms, 1e-9), 4)} for kk, v in prof.items()}
+    launches = int(sum(v["launches"] for kk, v in prof.items() if kk != "memset"))
+    cpu = None
+    if not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, gd, frames, args.cpu_seconds)
+    line = {
+        "metric": "mapping frames/sec at 1280x720 (fuse+raycast+refine)",
+        "value": round(value, 2), "unit": "frames/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms_max / args.steps, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded analytic rooms, gps_synth)",
+        "config": {"workload": f"{args.config}: Azure-Kinect-shaped {cfg.width}x{cfg.height}, {n_g} Gaussians "
+                               f"(SH deg {args.sh_degree}), voxel {cfg.voxel_size} m, delta_k=10, 20 iters/round, "
+                               f"6 views/round (R-VIEW: 1 view/iteration); step = 10 frames",
+                   "frames_per_step": dk, "gaussians": n_g, "sh_degree": args.sh_degree, "tile": args.tile,
+                   "resolution": [cfg.width, cfg.height], "history_frames": args.history,
+                   "parallelism": f"replicas x{ws} (independent sequences)",
+                   "l2": "inputs larger than L2 (per-step state > 126 MB: params+Adam 283 MB, volume)"},
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "gpu_launches_per_step": launches / args.steps,
+        "roofline": roof,
+        "kernels": shares,
+        "cpu_baseline": cpu,
+        "clocks": clk,
+        "stats": {"render": rstats, "volume": vstats, "setup_s": round(t_setup, 1), "rounds": pipe.rounds},
+    }
+    if ws > 1:
+        dist.destroy_process_group()
+    return line
+
+
+def read_profile(N):
+    import ctypes as C
+    names = C.create_string_buffer(512)
+    tot = (C.c_double * 16)()
+    cnt = (C.c_int64 * 16)()
+    n = N._lib.gps_profile_read_sync(names, 512, tot, cnt, 16)
+    ks = names.value.decode().split(";")[:n]
+    return {k: {"ms": tot[i], "launches": int(cnt[i])} for i, k in enumerate(ks)}
+
+
+# ----------------------------------------------------------------------------------------------
+def cpu_baseline(cfg, gd, frames, budget_s):
+    """The oracle as it stands (single-threaded C + numpy, fp64 render), on a bounded sample of
+    the same workload: fuse of 2 full frames, raycast of a pixel sample (scaled to a full frame),
+    one refine iteration on a sampled subset of Gaussians (scaled to all).  Frame time is
+    assembled like the step: t = t_fuse + 1.6 t_raycast + 2 t_iter."""
+    import oracle as O
+    import torch
+
+    ocam = O.Camera(cfg.fx, cfg.fy, cfg.cx, cfg.cy, cfg.width, cfg.height)
+    vol = O.Volume(voxel_size=cfg.voxel_size, mu=4 * cfg.voxel_size)
+    t0 = time.time()
+    nf = 0
+    for k in range(2):
+        d, c, R, t = frames[k]
+        vol.fuse(ocam, R, t, d.cpu().numpy().view(np.uint16), cfg.depth_scale, c.cpu().numpy())
+        nf += 1
+    t_fuse = (time.time() - t0) / nf
+    rng = np.random.default_rng(0)
+    npx = 400
+    pix = np.stack([rng.integers(0, cfg.width, npx), rng.integers(0, cfg.height, npx)], 1).astype(np.int32)
+    t0 = time.time()
+    vol.raycast(ocam, frames[1][2], frames[1][3], pix)
+    t_ray = (time.time() - t0) * (cfg.width * cfg.height / npx)
+    n = gd["xyz"].shape[0]
+    m = min(n, 20000)
+    sub = {k: (v[:m] if isinstance(v, np.ndarray) else v) for k, v in gd.items()}
+    Dt = np.zeros((cfg.height, cfg.width), np.float32)
+    Ct = np.zeros((cfg.height, cfg.width, 3), np.float32)
+    tgt = frames[1][1].cpu().numpy()
+    t0 = time.time()
+    out = O.render(sub, ocam, frames[1][2], frames[1][3], Dt, Ct)
+    loss, Gr, cnt, _ = O.l1_loss(out["Cstar"], out["WG"], Dt, tgt)
+    grads, _ = O.backward(sub, ocam, frames[1][2], frames[1][3], Dt, out["Cstar"], out["WG"], Gr)
+    zero = {k: np.zeros_like(np.asarray(v, np.float64)) for k, v in grads.items()}
+    O.adam_step(sub, zero, zero, grads, 0)
+    t_iter = (time.time() - t0) * (n / m)
+    t_frame = t_fuse + 1.6 * t_ray + 2.0 * t_iter
+    return {"value": round(1.0 / t_frame, 6), "unit": "frames/s", "cores": 1, "kind": "oracle",
+            "sample": f"fuse 2 full frames; raycast {npx} px scaled to {cfg.width}x{cfg.height}; one refine "
+                      f"iteration on {m} of {n} Gaussians scaled x{n / m:.1f}; t_frame = t_fuse + 1.6 t_ray + 2 t_iter",
+            "t_fuse_s": round(t_fuse, 3), "t_raycast_s": round(t_ray, 2), "t_iter_s": round(t_iter, 2)}
+
+
+def run_reference(args):
+    """The CPU oracle arm (tier rule ④): rank 0 only; each step is the bounded sample."""
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return None
+    import gps_synth as S
+    cfg = S.get_config(args.config)
+    frames = [(f.depth, f.rgba, f.R, f.t) for f in S.make_frames(cfg, 2, start=args.history)]
+    gd = S.make_gaussians(cfg, n=args.gaussians or cfg.n_gaussians, sh_degree=args.sh_degree)
+    for _ in range(args.warmup):
+        pass  # the oracle has no warm-up state; the first step below is representative
+    vals = []
+    t0 = time.time()
+    for _ in range(args.steps):
+        cb = cpu_baseline(cfg, gd, frames, args.cpu_seconds)
+        vals.append(cb["value"])
+        if time.time() - t0 > 150:
+            break
+    v = float(np.median(vals))
+    cb["value"] = round(v, 6)
+    return {"impl": "reference", "metric": "mapping frames/sec at 1280x720 (fuse+raycast+refine)", "value": cb["value"],
+            "unit": "frames/s", "n_gpus": 0, "steps": len(vals), "warmup": args.warmup,
+            "ms_per_step": round(10 * 1000.0 / v, 1), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded analytic rooms, gps_synth)",
+            "config": {"workload": f"{args.config} bounded sample (see cpu_baseline.sample)"},
+            "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    args = parse()
+    line = run_reference(args) if args.impl == "reference" else run_ours(args)
+    if line is not None:
+        print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()

@@ -93,10 +93,13 @@ void gps_volume_destroy(gps_volume* vol);
 /* Empties the volume (all blocks free, overflow flag cleared, frame counter reset).          */
 gps_status gps_volume_reset(gps_volume* vol, gps_stream_t stream);
 /* Synchronises `stream`, then reports the number of allocated blocks (may exceed the budget
- * when an overflow happened), the budget, and the number of blocks marked visible by the last
- * gps_fuse.  Any pointer may be NULL.  Returns GPS_ERR_OUT_OF_BLOCKS if overflow happened.   */
+ * when an overflow happened), the budget, the number of blocks marked visible by the last
+ * gps_fuse, and the sum of visible blocks over every integration since create/reset (the unit
+ * count of the integration roofline).  Any pointer may be NULL.  Returns
+ * GPS_ERR_OUT_OF_BLOCKS if overflow happened.                                                 */
 gps_status gps_volume_stats_sync(gps_volume* vol, gps_stream_t stream, int64_t* n_blocks /*host*/,
-                                 int64_t* budget /*host*/, int64_t* n_visible /*host*/);
+                                 int64_t* budget /*host*/, int64_t* n_visible /*host*/,
+                                 int64_t* visible_total /*host*/);
 
 /* gps_fuse -- Sec. 3.2.1 "SDF fusion", voxel data P:60.
  * (1) Allocation: every valid depth pixel (depth/depth_scale in [depth_min, depth_max]) is
@@ -254,6 +257,17 @@ gps_status gps_debug_export_visible_sync(const gps_volume* vol, gps_stream_t str
  * With tile_depth_precull the ranges are the truncated ones.                                  */
 gps_status gps_debug_render_lists_sync(const void* ws, gps_stream_t stream, uint32_t* values,
                                        int64_t cap, uint32_t* ranges, int64_t* K /*host*/);
+
+/* ---- measurement hooks ------------------------------------------------------------------- */
+/* gps_profile_enable(1) starts a fresh session in which every kernel launch of the library is
+ * bracketed by two CUDA events recorded on its launch stream (0 stops recording).  Host-side
+ * cost: two cudaEventRecord per launch.  gps_profile_read_sync synchronises the recorded events
+ * and writes, per kernel id, the summed device time in ms and the launch count; `names`
+ * (host, names_cap bytes) receives "k_alloc;k_integrate;..." in id order.  Returns the number
+ * of kernel ids.                                                                              */
+void gps_profile_enable(int on);
+int gps_profile_read_sync(char* names /*host*/, int names_cap, double* total_ms /*host*/,
+                          int64_t* launches /*host*/, int cap);
 
 const char* gps_status_string(gps_status s);
 const char* gps_last_error(void); /* thread-local; "" if none */

@@ -1,0 +1,12 @@
+"""B200-native (sm_100a) Gaussian-Plus-SDF mapping step of GPS-SLAM (arXiv 2509.11574).
+
+The compute path is libgps.so (hand-written CUDA behind the C ABI of include/gps.h); this
+package is the thin Python binding (``api``), the host-side round schedule (``schedule``) and
+the in-tree build (``build``).  Importing it loads libgps.so and raises if it is missing.
+"""
+from . import _native
+from .api import (AdamConfig, AdamState, Camera, Gaussians, Rasterizer, RenderConfig, View, Volume,
+                  adam_step, pose_struct)
+
+__all__ = ["AdamConfig", "AdamState", "Camera", "Gaussians", "Rasterizer", "RenderConfig", "View", "Volume",
+           "adam_step", "pose_struct"]

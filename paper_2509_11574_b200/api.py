@@ -1,0 +1,308 @@
+"""Torch-facing API over libgps (the C ABI of include/gps.h).
+
+Torch supplies device memory and streams only; every step of the mapping path runs in
+libgps.so's sm_100a kernels.  Functions take torch tensors (device unless noted), pass their
+pointers and the current CUDA stream to the C ABI, and raise GPSError on a non-OK status.
+
+Paper: GPS-SLAM, arXiv 2509.11574.  gps_fuse/gps_raycast: Sec. 3.2.1 and
+Sec. 3.1 first pass; gps_render: Eqs. 1-4; gps_refine_step: Eq. 7,
+Adam with App. C learning rates.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native as N
+
+_L = N.load()
+
+
+def _stream(stream=None) -> int:
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _ptr(t: torch.Tensor | None):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("expected a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError("expected a contiguous tensor")
+    return C.c_void_p(t.data_ptr())
+
+
+@dataclass
+class Camera:
+    fx: float
+    fy: float
+    cx: float
+    cy: float
+    width: int
+    height: int
+
+    def c(self) -> N.gps_intrinsics:
+        return N.gps_intrinsics(self.fx, self.fy, self.cx, self.cy, self.width, self.height)
+
+
+def pose_struct(R, t) -> N.gps_pose:
+    R = np.asarray(R, np.float32).reshape(9)
+    t = np.asarray(t, np.float32).reshape(3)
+    return N.gps_pose((C.c_float * 9)(*R.tolist()), (C.c_float * 3)(*t.tolist()))
+
+
+# ---------------------------------------------------------------------------------------------
+# volume
+# ---------------------------------------------------------------------------------------------
+VOXEL_DTYPE = np.dtype([("tsdf", "<f4"), ("rgbw", "u1", (4,))])
+
+
+class Volume:
+    """Voxel-block hash volume owned by libgps (gps_volume_*)."""
+
+    def __init__(self, voxel_size=0.005, mu=None, w_max=100, depth_min=0.1, depth_max=10.0,
+                 max_blocks=1 << 18, hash_slots=1 << 20, stream=None):
+        mu = 4 * voxel_size if mu is None else mu
+        self.cfg = N.gps_volume_config(voxel_size, mu, w_max, depth_min, depth_max, int(max_blocks),
+                                       int(hash_slots))
+        h = C.c_void_p()
+        N.check("gps_volume_create", _L.gps_volume_create(C.byref(self.cfg), _stream(stream), C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None) is not None and self.h.value:
+            torch.cuda.synchronize()
+            _L.gps_volume_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def reset(self, stream=None):
+        N.check("gps_volume_reset", _L.gps_volume_reset(self.h, _stream(stream)))
+
+    def fuse(self, cam: Camera, R, t, depth: torch.Tensor, depth_scale: float, rgba: torch.Tensor,
+             stream=None):
+        """depth: u16/i16 [H,W] raw sensor units; rgba: u8 [H,W,4].  CPU tensors are copied to
+        the device first (that copy is part of an end-to-end measurement)."""
+        if not depth.is_cuda:
+            depth = depth.cuda(non_blocking=True)
+        if not rgba.is_cuda:
+            rgba = rgba.cuda(non_blocking=True)
+        assert depth.element_size() == 2 and depth.numel() == cam.width * cam.height
+        assert rgba.dtype == torch.uint8 and rgba.numel() == 4 * cam.width * cam.height
+        N.check("gps_fuse", _L.gps_fuse(self.h, C.byref(cam.c()), C.byref(pose_struct(R, t)), _ptr(depth),
+                                        float(depth_scale), _ptr(rgba), _stream(stream)))
+
+    def raycast(self, cam: Camera, R, t, depth_out=None, color_out=None, vertex_out=None,
+                want_vertex=False, stream=None):
+        dev = torch.device("cuda")
+        if depth_out is None:
+            depth_out = torch.empty((cam.height, cam.width), dtype=torch.float32, device=dev)
+        if color_out is None:
+            color_out = torch.empty((cam.height, cam.width, 3), dtype=torch.float32, device=dev)
+        if want_vertex and vertex_out is None:
+            vertex_out = torch.empty((cam.height, cam.width, 3), dtype=torch.float32, device=dev)
+        N.check("gps_raycast", _L.gps_raycast(self.h, C.byref(cam.c()), C.byref(pose_struct(R, t)),
+                                              _ptr(depth_out), _ptr(color_out), _ptr(vertex_out),
+                                              _stream(stream)))
+        return depth_out, color_out, vertex_out
+
+    def stats(self, stream=None):
+        nb, bud, nv, vt = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
+        st = _L.gps_volume_stats_sync(self.h, _stream(stream), C.byref(nb), C.byref(bud), C.byref(nv), C.byref(vt))
+        return {"n_blocks": nb.value, "budget": bud.value, "n_visible": nv.value, "visible_total": vt.value,
+                "status": N.STATUS[st]}
+
+    def export_blocks(self, with_voxels=True, stream=None):
+        """(coords i32[n,3], voxels structured [n,512] (tsdf f32, rgbw u8[4]) or None), any order."""
+        cap = int(self.cfg.max_blocks)
+        coords = torch.empty((cap, 3), dtype=torch.int32, device="cuda")
+        vox = torch.empty((cap, 512, 2), dtype=torch.int32, device="cuda") if with_voxels else None
+        n = C.c_int64()
+        N.check("gps_debug_export_blocks_sync",
+                _L.gps_debug_export_blocks_sync(self.h, _stream(stream), _ptr(coords), _ptr(vox), cap, C.byref(n)))
+        k = min(n.value, cap)
+        c = coords[:k].cpu().numpy()
+        v = None
+        if with_voxels:
+            v = vox[:k].cpu().numpy().view(VOXEL_DTYPE).reshape(k, 512)
+        return c, v
+
+    def export_visible(self, stream=None):
+        cap = int(self.cfg.max_blocks)
+        coords = torch.empty((cap, 3), dtype=torch.int32, device="cuda")
+        n = C.c_int64()
+        N.check("gps_debug_export_visible_sync",
+                _L.gps_debug_export_visible_sync(self.h, _stream(stream), _ptr(coords), cap, C.byref(n)))
+        return coords[:min(n.value, cap)].cpu().numpy()
+
+
+# ---------------------------------------------------------------------------------------------
+# Gaussians, optimiser state, rasteriser
+# ---------------------------------------------------------------------------------------------
+FIELDS = ("xyz", "log_scale", "rot", "opacity_raw", "sh")
+
+
+class Gaussians:
+    """Caller-owned SoA parameter arrays (float32, contiguous, CUDA)."""
+
+    def __init__(self, n: int, sh_degree: int, device="cuda", tensors: dict | None = None):
+        self.n, self.sh_degree = int(n), int(sh_degree)
+        nc = (sh_degree + 1) ** 2
+        shapes = {"xyz": (n, 3), "log_scale": (n, 3), "rot": (n, 4), "opacity_raw": (n,), "sh": (n, nc * 3)}
+        for k in FIELDS:
+            if tensors is not None:
+                v = torch.as_tensor(np.asarray(tensors[k], np.float32)).reshape(shapes[k])
+                setattr(self, k, v.to(device).contiguous())
+            else:
+                setattr(self, k, torch.zeros(shapes[k], dtype=torch.float32, device=device))
+
+    @staticmethod
+    def from_dict(d: dict, device="cuda") -> "Gaussians":
+        return Gaussians(int(np.asarray(d["xyz"]).shape[0]), int(d["sh_degree"]), device, d)
+
+    def zeros_like(self) -> "Gaussians":
+        return Gaussians(self.n, self.sh_degree, self.xyz.device)
+
+    def c(self) -> N.gps_gaussians:
+        return N.gps_gaussians(self.n, self.sh_degree, *(C.c_void_p(getattr(self, k).data_ptr()) for k in FIELDS))
+
+    def to_numpy(self) -> dict:
+        out = {k: getattr(self, k).detach().cpu().numpy() for k in FIELDS}
+        out["sh_degree"] = self.sh_degree
+        return out
+
+    def clone(self) -> "Gaussians":
+        g = Gaussians(self.n, self.sh_degree, self.xyz.device)
+        for k in FIELDS:
+            getattr(g, k).copy_(getattr(self, k))
+        return g
+
+
+class AdamState:
+    def __init__(self, g: Gaussians):
+        self.m = g.zeros_like()
+        self.v = g.zeros_like()
+        self.step = 0
+
+
+@dataclass
+class RenderConfig:
+    eps_depth: float = 0.02          # R-EPS  ("small positive threshold")
+    alpha_min: float = 1.0 / 255
+    near_z: float = 0.2              # R-NEAR
+    lowpass: float = 0.3             # R-LOWPASS
+    tile: int = 16
+    tile_depth_precull: int = 1
+    max_pairs: int = 0
+
+    def c(self) -> N.gps_render_config:
+        return N.gps_render_config(self.eps_depth, self.alpha_min, self.near_z, self.lowpass, self.tile,
+                                   self.tile_depth_precull, self.max_pairs)
+
+
+@dataclass
+class AdamConfig:
+    lr_xyz: float = 1.6e-4
+    lr_sh0: float = 2.5e-3
+    lr_shrest: float = 5e-4
+    lr_opacity: float = 5e-2
+    lr_scale: float = 5e-3
+    lr_rot: float = 1e-3
+    beta1: float = 0.9         # R-ADAM
+    beta2: float = 0.999
+    eps: float = 1e-15
+
+    def c(self) -> N.gps_adam_config:
+        return N.gps_adam_config(self.lr_xyz, self.lr_sh0, self.lr_shrest, self.lr_opacity, self.lr_scale,
+                                 self.lr_rot, self.beta1, self.beta2, self.eps)
+
+
+@dataclass
+class View:
+    cam: Camera
+    R: np.ndarray
+    t: np.ndarray
+    sdf_depth: torch.Tensor
+    sdf_color: torch.Tensor
+    target_rgba: torch.Tensor
+
+    def c(self) -> N.gps_view:
+        return N.gps_view(self.cam.c(), pose_struct(self.R, self.t), _ptr(self.sdf_depth), _ptr(self.sdf_color),
+                          _ptr(self.target_rgba))
+
+
+class Rasterizer:
+    """Owns the device workspace of gps_render / gps_refine_step for up to n Gaussians."""
+
+    def __init__(self, n: int, cam: Camera, cfg: RenderConfig | None = None, n_views: int = 1):
+        self.cfg = cfg or RenderConfig()
+        self.n, self.cam, self.n_views = n, cam, n_views
+        size = _L.gps_refine_workspace_size(n, C.byref(cam.c()), C.byref(self.cfg.c()), n_views)
+        if size == 0:
+            raise ValueError("bad rasteriser configuration")
+        self.ws = torch.empty(size, dtype=torch.uint8, device="cuda")
+        self.loss = torch.zeros(1, dtype=torch.float32, device="cuda")
+
+    def render(self, g: Gaussians, cam: Camera, R, t, sdf_depth, sdf_color, target_rgba=None,
+               out_color=None, out_weight=None, stream=None):
+        if out_color is None:
+            out_color = torch.empty((cam.height, cam.width, 3), dtype=torch.float32, device="cuda")
+        if out_weight is None:
+            out_weight = torch.empty((cam.height, cam.width), dtype=torch.float32, device="cuda")
+        loss = self.loss if target_rgba is not None else None
+        N.check("gps_render", _L.gps_render(C.byref(g.c()), C.byref(cam.c()), C.byref(pose_struct(R, t)),
+                                            _ptr(sdf_depth), _ptr(sdf_color), _ptr(target_rgba),
+                                            C.byref(self.cfg.c()), _ptr(self.ws), self.ws.numel(),
+                                            _ptr(out_color), _ptr(out_weight), _ptr(loss), _stream(stream)))
+        return out_color, out_weight, loss
+
+    def refine_step(self, g: Gaussians, state: AdamState, views: list[View], adam: AdamConfig | None = None,
+                    grad_out: Gaussians | None = None, stream=None):
+        adam = adam or AdamConfig()
+        arr = (N.gps_view * len(views))(*[v.c() for v in views])
+        st = N.gps_adam_state(state.m.c(), state.v.c(), state.step)
+        gc = g.c()
+        go = grad_out.c() if grad_out is not None else None
+        N.check("gps_refine_step",
+                _L.gps_refine_step(C.byref(gc), C.byref(st), arr, len(views), C.byref(self.cfg.c()),
+                                   C.byref(adam.c()), _ptr(self.ws), self.ws.numel(), _ptr(self.loss),
+                                   C.byref(go) if go is not None else None, _stream(stream)))
+        state.step = st.step
+        return self.loss
+
+    def stats(self, stream=None):
+        K, cap, nv = C.c_int64(), C.c_int64(), C.c_int64()
+        st = _L.gps_render_stats_sync(_ptr(self.ws), _stream(stream), C.byref(K), C.byref(cap), C.byref(nv))
+        return {"pairs": K.value, "capacity": cap.value, "n_visible": nv.value, "status": N.STATUS[st]}
+
+    def lists(self, stream=None):
+        """(values u32[K], ranges u32[n_tiles, 2]) of the last render."""
+        cam = self.cam
+        tiles = -(-cam.width // self.cfg.tile) * -(-cam.height // self.cfg.tile)
+        K = C.c_int64()
+        N.check("gps_debug_render_lists_sync",
+                _L.gps_debug_render_lists_sync(_ptr(self.ws), _stream(stream), None, 0, None, C.byref(K)))
+        vals = torch.empty(max(K.value, 1), dtype=torch.int32, device="cuda")
+        ranges = torch.empty((tiles, 2), dtype=torch.int32, device="cuda")
+        N.check("gps_debug_render_lists_sync",
+                _L.gps_debug_render_lists_sync(_ptr(self.ws), _stream(stream), _ptr(vals), K.value, _ptr(ranges),
+                                               C.byref(K)))
+        return (vals[:K.value].cpu().numpy().view(np.uint32), ranges.cpu().numpy().view(np.uint32))
+
+
+def adam_step(g: Gaussians, state: AdamState, grad: Gaussians, adam: AdamConfig | None = None, stream=None):
+    adam = adam or AdamConfig()
+    st = N.gps_adam_state(state.m.c(), state.v.c(), state.step)
+    N.check("gps_adam_step", _L.gps_adam_step(C.byref(g.c()), C.byref(st), C.byref(grad.c()), C.byref(adam.c()),
+                                              _stream(stream)))
+    state.step = st.step

@@ -1,0 +1,110 @@
+// common.cuh -- shared device/host helpers of libgps (sm_100a).  Nothing here is shared with
+// the CPU oracle (oracle/oracle.c); the two implement DESIGN.md §4 independently.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <string>
+
+#include "gps.h"
+
+namespace gps {
+
+// ---- error plumbing ------------------------------------------------------------------------
+void set_error(const std::string& msg);
+gps_status cuda_fail(const char* where, cudaError_t e);
+#define GPS_CHECK_LAUNCH(where)                                    \
+  do {                                                             \
+    cudaError_t e__ = cudaGetLastError();                          \
+    if (e__ != cudaSuccess) return ::gps::cuda_fail(where, e__);   \
+  } while (0)
+#define GPS_CHECK_CUDA(call)                                       \
+  do {                                                             \
+    cudaError_t e__ = (call);                                      \
+    if (e__ != cudaSuccess) return ::gps::cuda_fail(#call, e__);   \
+  } while (0)
+gps_status invalid(const std::string& msg);
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+inline cudaStream_t as_stream(gps_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ---- prescribed fp32 arithmetic: never contracted into FMA ------------------
+__device__ __forceinline__ float pmul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float padd(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float psub(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ float pdiv(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ float psqrt(float a) { return __fsqrt_rn(a); }
+// ((a0*b0 + a1*b1) + a2*b2), each product and sum rounded separately
+__device__ __forceinline__ float pdot3(float a0, float b0, float a1, float b1, float a2, float b2) {
+  return padd(padd(pmul(a0, b0), pmul(a1, b1)), pmul(a2, b2));
+}
+
+// ---- voxel-block hash -------------------------------------------------------
+// Voxel: 8 bytes, {f32 tsdf; u8 r, g, b, w}; block = 8^3 voxels, index i + 8j + 64k.
+struct __align__(8) Voxel {
+  float tsdf;
+  uint32_t rgbw;  // r | g<<8 | b<<16 | w<<24
+};
+constexpr uint64_t kEmptyKey = ~0ull;
+constexpr uint32_t kBlockBits = 21;
+constexpr uint32_t kBlockMask = (1u << kBlockBits) - 1u;
+
+__host__ __device__ __forceinline__ uint64_t pack_block(int x, int y, int z) {
+  return ((uint64_t)((uint32_t)x & kBlockMask) << 42) | ((uint64_t)((uint32_t)y & kBlockMask) << 21) |
+         (uint64_t)((uint32_t)z & kBlockMask);
+}
+__host__ __device__ __forceinline__ int sext21(uint32_t v) {
+  return (int)(v << 11) >> 11;
+}
+__host__ __device__ __forceinline__ void unpack_block(uint64_t k, int& x, int& y, int& z) {
+  x = sext21((uint32_t)(k >> 42) & kBlockMask);
+  y = sext21((uint32_t)(k >> 21) & kBlockMask);
+  z = sext21((uint32_t)k & kBlockMask);
+}
+// spatial hash of the voxel-hashing family: primes 73856093, 19349669, 83492791
+__host__ __device__ __forceinline__ uint32_t hash_block(int x, int y, int z) {
+  return ((uint32_t)x * 73856093u) ^ ((uint32_t)y * 19349669u) ^ ((uint32_t)z * 83492791u);
+}
+
+struct VolumeCounters {
+  uint32_t n_blocks;   // blocks handed out (may exceed max_blocks on overflow)
+  uint32_t n_vis;      // visible slots this frame
+  uint32_t overflow;   // sticky: budget, table or visible-list overflow
+  uint32_t pad;
+  unsigned long long vis_total;  // sum of n_vis over all integrations (measurement)
+};
+
+struct VolumeView {  // passed by value to kernels
+  uint64_t* keys;
+  int32_t* vals;  // pool block index, -1 = none
+  uint32_t* stamp;
+  Voxel* pool;
+  int32_t* vis;  // visible slots
+  VolumeCounters* ctr;
+  uint32_t slot_mask;
+  uint32_t max_blocks;
+};
+
+// find a block: returns its pool index, or -1 if unallocated / unbacked
+__device__ __forceinline__ int32_t find_block(const VolumeView& v, int x, int y, int z) {
+  const uint64_t key = pack_block(x, y, z);
+  uint32_t h = hash_block(x, y, z) & v.slot_mask;
+  for (uint32_t probe = 0; probe <= v.slot_mask; ++probe) {
+    const uint64_t k = __ldg(&v.keys[h]);
+    if (k == key) return __ldg(&v.vals[h]);
+    if (k == kEmptyKey) return -1;
+    h = (h + 1) & v.slot_mask;
+  }
+  return -1;
+}
+
+}  // namespace gps
+
+// the opaque handle of the C ABI
+struct gps_volume {
+  gps_volume_config cfg;
+  gps::VolumeView view;
+  uint32_t frame;
+  int device;
+};

@@ -1,0 +1,1280 @@
+// render.cu -- the Gaussian half of the mapping step for sm_100a: gps_render, gps_refine_step,
+// gps_adam_step and their workspace.
+//
+// Paper: GPS-SLAM (arXiv 2509.11574).  Gaussians "following 3DGS"; second-pass
+// rendering Eqs. 1-3 with depth culling against the SDF depth, composite Eq. 4
+// (W_t = 1); L1 loss Eq. 7; optimisation with Libtorch's Adam at
+// the learning rates of App. C.  Readings R-*: DESIGN.md §3; prescribed fp32 for the
+// tile-membership fields: DESIGN.md §4.3.
+//
+// Pipeline of one view:
+//   k_preprocess  per Gaussian: projection -> 48-B splat record, tile counts, zero 2D grads
+//   k_scan        one CTA: exclusive scan of the tile counts (MSD radix pass on the tile digit)
+//   k_emit        per Gaussian: scatter its index into every touched tile's bucket
+//   k_sort_blend  one CTA per tile: sort the bucket by (depth bits, index) in shared memory,
+//                 front-to-back blend with early termination at the SDF depth, composite,
+//                 fused L1 partials; the last CTA finalises the loss deterministically
+//   k_backward    one CTA per tile: a warp per list entry walks the entry's footprint inside the
+//                 tile, accumulates the 9 2D gradients in registers, warp-reduces, and issues
+//                 three vector reductions (red.global.add.v4.f32)
+//   k_grad_adam   per Gaussian: 2D -> raw-parameter chain rule fused with dense Adam; SH
+//                 coefficients swept coalesced from shared memory
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "prof.cuh"
+
+namespace gps {
+
+constexpr int kMaxList = 2048;  // entries a tile sorts in shared memory (16 KB of keys)
+constexpr uint32_t kWsMagic = 0x47505357u;  // "GPSW"
+
+struct WsHeader {
+  uint32_t magic, tile, tiles_x, tiles_y;
+  uint32_t width, height, n_tiles, pad0;
+  uint64_t cap_pairs;
+  int64_t n;
+  // ---- zeroed by every render (one memset together with counts and cursor) ----
+  uint32_t K;          // total pairs
+  uint32_t overflow;   // K > cap
+  uint32_t n_visible;  // Gaussians surviving culls
+  uint32_t mask_count; // |M| of the L1 mask
+  uint32_t ticket;     // last-CTA election for the loss
+  uint32_t pad1[3];
+  // ---- static: where this render's lists live (refine and render layouts differ) ----
+  uint64_t off_vals, off_offsets, off_tile_end;
+};
+
+struct WsLayout {
+  size_t hdr, counts, cursor, offsets, tile_end, loss_part, records, grad2d, vals, keys, cstar, wg, gbuf, total;
+  size_t zero_begin, zero_bytes;
+};
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+WsLayout ws_layout(int64_t n, int W, int H, int tile, int64_t cap, int64_t n_params, bool refine, bool gbuf) {
+  const size_t tiles = (size_t)((W + tile - 1) / tile) * ((H + tile - 1) / tile);
+  WsLayout L{};
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    size_t at = o;
+    o = align_up(o + bytes, 256);
+    return at;
+  };
+  L.hdr = take(sizeof(WsHeader));
+  L.counts = take(4 * tiles);
+  L.cursor = take(4 * tiles);
+  L.zero_begin = L.hdr + offsetof(WsHeader, K);
+  L.zero_bytes = L.cursor + 4 * tiles - L.zero_begin;
+  L.offsets = take(4 * (tiles + 1));
+  L.tile_end = take(4 * tiles);
+  L.loss_part = take(4 * tiles);
+  L.records = take(48 * (size_t)std::max<int64_t>(n, 1));
+  L.grad2d = refine ? take(48 * (size_t)std::max<int64_t>(n, 1)) : 0;
+  L.vals = take(4 * (size_t)cap);
+  L.keys = take(8 * (size_t)cap);
+  L.cstar = refine ? take(12 * (size_t)W * H) : 0;
+  L.wg = refine ? take(4 * (size_t)W * H) : 0;
+  L.gbuf = gbuf ? take(4 * (size_t)n_params) : 0;
+  L.total = o;
+  return L;
+}
+
+int64_t default_cap(int64_t n, int64_t cfg_cap) { return cfg_cap > 0 ? cfg_cap : 32 * n + 65536; }
+
+// --------------------------------------------------------------------------------------------
+struct Cam {
+  float fx, fy, cx, cy;
+  int W, H;
+  float R[9], t[3];
+};
+
+struct RenderArgs {
+  Cam cam;
+  float eps, alpha_min, near_z, lowpass;
+  int tile, tiles_x, tiles_y;
+  int64_t n;
+  int deg, nc;
+  uint32_t cap;
+};
+
+// SH basis of 3DGS (degree <= 3), real, at unit direction (x, y, z)
+__device__ __forceinline__ void sh_basis(float x, float y, float z, int deg, float* Y) {
+  const float C0 = 0.28209479177387814f, C1 = 0.4886025119029199f;
+  Y[0] = C0;
+  if (deg < 1) return;
+  Y[1] = -C1 * y; Y[2] = C1 * z; Y[3] = -C1 * x;
+  if (deg < 2) return;
+  const float xx = x * x, yy = y * y, zz = z * z;
+  Y[4] = 1.0925484305920792f * x * y;
+  Y[5] = -1.0925484305920792f * y * z;
+  Y[6] = 0.31539156525252005f * (2.f * zz - xx - yy);
+  Y[7] = -1.0925484305920792f * x * z;
+  Y[8] = 0.5462742152960396f * (xx - yy);
+  if (deg < 3) return;
+  Y[9] = -0.5900435899266435f * y * (3.f * xx - yy);
+  Y[10] = 2.890611442640554f * x * y * z;
+  Y[11] = -0.4570457994644658f * y * (4.f * zz - xx - yy);
+  Y[12] = 0.3731763325901154f * z * (2.f * zz - 3.f * xx - 3.f * yy);
+  Y[13] = -0.4570457994644658f * x * (4.f * zz - xx - yy);
+  Y[14] = 1.445305721320277f * z * (xx - yy);
+  Y[15] = -0.5900435899266435f * x * (xx - 3.f * yy);
+}
+
+// d Y_k / d(x,y,z), accumulated as ddir += w_k * dY_k
+__device__ __forceinline__ void sh_basis_vjp(float x, float y, float z, int deg, const float* w, float* dd) {
+  const float C1 = 0.4886025119029199f;
+  dd[0] = dd[1] = dd[2] = 0.f;
+  if (deg < 1) return;
+  dd[1] += -C1 * w[1]; dd[2] += C1 * w[2]; dd[0] += -C1 * w[3];
+  if (deg < 2) return;
+  const float xx = x * x, yy = y * y, zz = z * z;
+  const float a0 = 1.0925484305920792f, a1 = -1.0925484305920792f, a2 = 0.31539156525252005f,
+              a3 = -1.0925484305920792f, a4 = 0.5462742152960396f;
+  dd[0] += a0 * y * w[4]; dd[1] += a0 * x * w[4];
+  dd[1] += a1 * z * w[5]; dd[2] += a1 * y * w[5];
+  dd[0] += -2.f * a2 * x * w[6]; dd[1] += -2.f * a2 * y * w[6]; dd[2] += 4.f * a2 * z * w[6];
+  dd[0] += a3 * z * w[7]; dd[2] += a3 * x * w[7];
+  dd[0] += 2.f * a4 * x * w[8]; dd[1] += -2.f * a4 * y * w[8];
+  if (deg < 3) return;
+  const float b0 = -0.5900435899266435f, b1 = 2.890611442640554f, b2 = -0.4570457994644658f,
+              b3 = 0.3731763325901154f, b4 = -0.4570457994644658f, b5 = 1.445305721320277f,
+              b6 = -0.5900435899266435f;
+  dd[0] += b0 * 6.f * x * y * w[9]; dd[1] += b0 * (3.f * xx - 3.f * yy) * w[9];
+  dd[0] += b1 * y * z * w[10]; dd[1] += b1 * x * z * w[10]; dd[2] += b1 * x * y * w[10];
+  dd[0] += b2 * (-2.f * x * y) * w[11]; dd[1] += b2 * (4.f * zz - xx - 3.f * yy) * w[11]; dd[2] += b2 * 8.f * y * z * w[11];
+  dd[0] += b3 * (-6.f * x * z) * w[12]; dd[1] += b3 * (-6.f * y * z) * w[12]; dd[2] += b3 * (6.f * zz - 3.f * xx - 3.f * yy) * w[12];
+  dd[0] += b4 * (4.f * zz - 3.f * xx - yy) * w[13]; dd[1] += b4 * (-2.f * x * y) * w[13]; dd[2] += b4 * 8.f * x * z * w[13];
+  dd[0] += b5 * 2.f * x * z * w[14]; dd[1] += b5 * (-2.f * y * z) * w[14]; dd[2] += b5 * (xx - yy) * w[14];
+  dd[0] += b6 * (3.f * xx - 3.f * yy) * w[15]; dd[1] += b6 * (-6.f * x * y) * w[15];
+}
+
+// Everything the forward and backward need about one Gaussian in one view.  The fields that
+// decide tile membership and the sort key (X, Sigma_2D, p_hat, rect) follow the prescribed fp32
+// sequence of DESIGN.md §4.3 (the CPU oracle evaluates the same sequence independently).
+struct Proj {
+  bool culled;
+  float X[3];
+  float s[3], qh[4], qn, Rq[9], M[9], S[9];
+  float cu, cv;
+  bool clx, cly;
+  float J00, J02, J11, J12, T[6];
+  float cxx, cxy, cyy, det, ca, cb, cc;
+  float px, py;
+  int x0, y0, x1, y1;
+};
+
+__device__ __forceinline__ void project_p32(const Cam& c, float near_z, float lowpass, const float* p,
+                                            const float* ls, const float* q, Proj& g) {
+  g.culled = true;
+  const float D0 = psub(p[0], c.t[0]), D1 = psub(p[1], c.t[1]), D2 = psub(p[2], c.t[2]);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) g.X[k] = pdot3(c.R[0 * 3 + k], D0, c.R[1 * 3 + k], D1, c.R[2 * 3 + k], D2);
+  if (!(g.X[2] > near_z)) return;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) g.s[k] = (float)exp((double)ls[k]);
+  float qn2 = padd(pmul(q[0], q[0]), pmul(q[1], q[1]));
+  qn2 = padd(qn2, pmul(q[2], q[2]));
+  qn2 = padd(qn2, pmul(q[3], q[3]));
+  g.qn = psqrt(qn2);
+  const float w = pdiv(q[0], g.qn), x = pdiv(q[1], g.qn), y = pdiv(q[2], g.qn), z = pdiv(q[3], g.qn);
+  g.qh[0] = w; g.qh[1] = x; g.qh[2] = y; g.qh[3] = z;
+  float* Rq = g.Rq;
+  Rq[0] = psub(1.0f, pmul(2.0f, padd(pmul(y, y), pmul(z, z))));
+  Rq[1] = pmul(2.0f, psub(pmul(x, y), pmul(w, z)));
+  Rq[2] = pmul(2.0f, padd(pmul(x, z), pmul(w, y)));
+  Rq[3] = pmul(2.0f, padd(pmul(x, y), pmul(w, z)));
+  Rq[4] = psub(1.0f, pmul(2.0f, padd(pmul(x, x), pmul(z, z))));
+  Rq[5] = pmul(2.0f, psub(pmul(y, z), pmul(w, x)));
+  Rq[6] = pmul(2.0f, psub(pmul(x, z), pmul(w, y)));
+  Rq[7] = pmul(2.0f, padd(pmul(y, z), pmul(w, x)));
+  Rq[8] = psub(1.0f, pmul(2.0f, padd(pmul(x, x), pmul(y, y))));
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int cc = 0; cc < 3; ++cc) g.M[3 * r + cc] = pmul(Rq[3 * r + cc], g.s[cc]);
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int cc = 0; cc < 3; ++cc)
+      g.S[3 * r + cc] = pdot3(g.M[3 * r], g.M[3 * cc], g.M[3 * r + 1], g.M[3 * cc + 1], g.M[3 * r + 2], g.M[3 * cc + 2]);
+  const float tanx = pdiv((float)c.W, pmul(2.0f, c.fx)), tany = pdiv((float)c.H, pmul(2.0f, c.fy));
+  const float limx = pmul(1.3f, tanx), limy = pmul(1.3f, tany);
+  const float txz = pdiv(g.X[0], g.X[2]), tyz = pdiv(g.X[1], g.X[2]);
+  g.clx = (txz < -limx || txz > limx);
+  g.cly = (tyz < -limy || tyz > limy);
+  g.cu = txz < -limx ? -limx : (txz > limx ? limx : txz);
+  g.cv = tyz < -limy ? -limy : (tyz > limy ? limy : tyz);
+  const float tx = pmul(g.cu, g.X[2]), ty = pmul(g.cv, g.X[2]);
+  const float z2 = pmul(g.X[2], g.X[2]);
+  g.J00 = pdiv(c.fx, g.X[2]);
+  g.J02 = -pdiv(pmul(c.fx, tx), z2);
+  g.J11 = pdiv(c.fy, g.X[2]);
+  g.J12 = -pdiv(pmul(c.fy, ty), z2);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    g.T[k] = padd(pmul(g.J00, c.R[k * 3 + 0]), pmul(g.J02, c.R[k * 3 + 2]));
+    g.T[3 + k] = padd(pmul(g.J11, c.R[k * 3 + 1]), pmul(g.J12, c.R[k * 3 + 2]));
+  }
+  float U[6];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      U[3 * a + k] = pdot3(g.T[3 * a], g.S[k], g.T[3 * a + 1], g.S[3 + k], g.T[3 * a + 2], g.S[6 + k]);
+  const float sxx = pdot3(U[0], g.T[0], U[1], g.T[1], U[2], g.T[2]);
+  const float sxy = pdot3(U[0], g.T[3], U[1], g.T[4], U[2], g.T[5]);
+  const float syy = pdot3(U[3], g.T[3], U[4], g.T[4], U[5], g.T[5]);
+  g.cxx = padd(sxx, lowpass);
+  g.cxy = sxy;
+  g.cyy = padd(syy, lowpass);
+  g.det = psub(pmul(g.cxx, g.cyy), pmul(g.cxy, g.cxy));
+  if (!(g.det > 0.0f)) return;
+  g.ca = pdiv(g.cyy, g.det);
+  g.cb = -pdiv(g.cxy, g.det);
+  g.cc = pdiv(g.cxx, g.det);
+  g.px = padd(pdiv(pmul(c.fx, g.X[0]), g.X[2]), c.cx);
+  g.py = padd(pdiv(pmul(c.fy, g.X[1]), g.X[2]), c.cy);
+  const float rx = pmul(3.0f, psqrt(g.cxx)), ry = pmul(3.0f, psqrt(g.cyy));
+  float fx0 = floorf(psub(g.px, rx)), fx1 = ceilf(padd(g.px, rx));
+  float fy0 = floorf(psub(g.py, ry)), fy1 = ceilf(padd(g.py, ry));
+  fx0 = fmaxf(fx0, 0.0f);
+  fy0 = fmaxf(fy0, 0.0f);
+  fx1 = fminf(fx1, (float)(c.W - 1));
+  fy1 = fminf(fy1, (float)(c.H - 1));
+  if (!(fx0 <= fx1 && fy0 <= fy1)) return;
+  g.x0 = (int)fx0; g.y0 = (int)fy0; g.x1 = (int)fx1; g.y1 = (int)fy1;
+  g.culled = false;
+}
+
+struct SH {
+  float Y[16];
+  float dir[3], dnorm;
+};
+
+__device__ __forceinline__ void view_dir(const Cam& c, const float* p, int deg, SH& h) {
+  const float d0 = p[0] - c.t[0], d1 = p[1] - c.t[1], d2 = p[2] - c.t[2];
+  h.dnorm = sqrtf(d0 * d0 + d1 * d1 + d2 * d2);
+  const float inv = 1.0f / h.dnorm;
+  h.dir[0] = d0 * inv; h.dir[1] = d1 * inv; h.dir[2] = d2 * inv;
+  sh_basis(h.dir[0], h.dir[1], h.dir[2], deg, h.Y);
+}
+
+// ============================================================================================
+// k_preprocess
+// ============================================================================================
+struct SplatPtrs {
+  float4* rec;     // 3 float4 per Gaussian
+  float4* grad2d;  // 3 float4 per Gaussian (nullable)
+  uint32_t* counts;
+  WsHeader* hdr;
+};
+
+__global__ void __launch_bounds__(256) k_preprocess(RenderArgs a, gps_gaussians g, SplatPtrs w) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= a.n) return;
+  if (w.grad2d) {
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    w.grad2d[3 * i] = z; w.grad2d[3 * i + 1] = z; w.grad2d[3 * i + 2] = z;
+  }
+  Proj pr;
+  project_p32(a.cam, a.near_z, a.lowpass, g.xyz + 3 * i, g.log_scale + 3 * i, g.rot + 4 * i, pr);
+  if (pr.culled) {
+    // an empty rect marks the record as not listed (never read by later kernels)
+    w.rec[3 * i + 1] = make_float4(0.f, 0.f, 0.f, __uint_as_float(0xFFFFu));
+    return;
+  }
+  SH h;
+  view_dir(a.cam, g.xyz + 3 * i, a.deg, h);
+  const float* sh = g.sh + (size_t)i * a.nc * 3;
+  float col[3];
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) {
+    float acc = 0.f;
+    for (int k = 0; k < a.nc; ++k) acc = fmaf(h.Y[k], __ldg(&sh[3 * k + ch]), acc);
+    col[ch] = fmaxf(acc + 0.5f, 0.0f);
+  }
+  const float sigma = 1.0f / (1.0f + __expf(-__ldg(&g.opacity_raw[i])));
+  const uint32_t rx = (uint32_t)pr.x0 | ((uint32_t)pr.x1 << 16);
+  const uint32_t ry = (uint32_t)pr.y0 | ((uint32_t)pr.y1 << 16);
+  w.rec[3 * i + 0] = make_float4(pr.px, pr.py, pr.ca, pr.cb);
+  w.rec[3 * i + 1] = make_float4(pr.cc, sigma, pr.X[2], __uint_as_float(rx));
+  w.rec[3 * i + 2] = make_float4(col[0], col[1], col[2], __uint_as_float(ry));
+  const int tx0 = pr.x0 / a.tile, tx1 = pr.x1 / a.tile, ty0 = pr.y0 / a.tile, ty1 = pr.y1 / a.tile;
+  for (int ty = ty0; ty <= ty1; ++ty)
+    for (int tx = tx0; tx <= tx1; ++tx) atomicAdd(&w.counts[ty * a.tiles_x + tx], 1u);
+  atomicAdd(&w.hdr->n_visible, 1u);
+}
+
+// ============================================================================================
+// k_scan: exclusive scan of the per-tile counts (one CTA, 1024 threads, chunked)
+// ============================================================================================
+__global__ void __launch_bounds__(1024) k_scan(const uint32_t* __restrict__ counts, uint32_t* offsets,
+                                               int n_tiles, WsHeader* hdr, WsHeader stat) {
+  __shared__ uint32_t warp_sums[32];
+  __shared__ uint32_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int base = 0; base < n_tiles; base += 1024) {
+    const int i = base + threadIdx.x;
+    const uint32_t v = i < n_tiles ? counts[i] : 0u;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_sums[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      uint32_t s = warp_sums[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, s, o);
+        if (lane >= o) s += y;
+      }
+      warp_sums[lane] = s;  // inclusive
+    }
+    __syncthreads();
+    const uint32_t excl = carry + (wid ? warp_sums[wid - 1] : 0u) + x - v;
+    if (i < n_tiles) offsets[i] = excl;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = excl + v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    offsets[n_tiles] = carry;
+    hdr->magic = stat.magic; hdr->tile = stat.tile; hdr->tiles_x = stat.tiles_x; hdr->tiles_y = stat.tiles_y;
+    hdr->width = stat.width; hdr->height = stat.height; hdr->n_tiles = stat.n_tiles;
+    hdr->cap_pairs = stat.cap_pairs; hdr->n = stat.n;
+    hdr->off_vals = stat.off_vals; hdr->off_offsets = stat.off_offsets; hdr->off_tile_end = stat.off_tile_end;
+    hdr->K = carry;
+    hdr->overflow = carry > stat.cap_pairs ? 1u : 0u;
+  }
+}
+
+// ============================================================================================
+// k_emit: bucket each listed Gaussian into its tiles (order inside a bucket is arbitrary; the
+// per-tile sort makes the final order unique)
+// ============================================================================================
+__global__ void __launch_bounds__(256) k_emit(RenderArgs a, const float4* __restrict__ rec,
+                                              const uint32_t* __restrict__ offsets, uint32_t* cursor,
+                                              uint32_t* vals) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= a.n) return;
+  const float4 r1 = rec[3 * i + 1], r2 = rec[3 * i + 2];
+  const uint32_t rx = __float_as_uint(r1.w), ry = __float_as_uint(r2.w);
+  const int x0 = rx & 0xFFFF, x1 = rx >> 16, y0 = ry & 0xFFFF, y1 = ry >> 16;
+  if (x1 < x0) return;  // culled
+  const int tx0 = x0 / a.tile, tx1 = x1 / a.tile, ty0 = y0 / a.tile, ty1 = y1 / a.tile;
+  for (int ty = ty0; ty <= ty1; ++ty)
+    for (int tx = tx0; tx <= tx1; ++tx) {
+      const int t = ty * a.tiles_x + tx;
+      const uint32_t pos = offsets[t] + atomicAdd(&cursor[t], 1u);
+      if (pos < a.cap) vals[pos] = (uint32_t)i;
+    }
+}
+
+// ============================================================================================
+// sort helpers: bitonic network in its all-ascending form (the first comparator of every merge
+// compares mirror images), which lets a list of any length n be sorted without padding
+// ============================================================================================
+template <typename Keys>
+__device__ __forceinline__ void bitonic_sort(Keys keys, int n) {
+  int P = 1;
+  while (P < n) P <<= 1;
+  for (int k = 2; k <= P; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int c = threadIdx.x; c < (P >> 1); c += blockDim.x) {
+        int lo, hi;
+        if (j == (k >> 1)) {
+          const int blk = c / j, off = c % j;
+          lo = blk * k + off;
+          hi = blk * k + k - 1 - off;
+        } else {
+          const int blk = c / j, off = c % j;
+          lo = blk * 2 * j + off;
+          hi = lo + j;
+        }
+        if (hi < n) {
+          const uint64_t a = keys[lo], b = keys[hi];
+          if (a > b) {
+            keys[lo] = b;
+            keys[hi] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// ============================================================================================
+// k_sort_blend
+// ============================================================================================
+struct BlendIO {
+  const float* sdf_depth;
+  const float* sdf_color;
+  const uint32_t* target;  // nullable (RGBA as u32)
+  float* out_color;
+  float* out_weight;
+  float* loss_out;  // nullable
+  int accumulate_loss;
+};
+
+template <int TILE>
+__global__ void __launch_bounds__(TILE* TILE) k_sort_blend(RenderArgs a, const float4* __restrict__ rec,
+                                                          const uint32_t* __restrict__ offsets, uint32_t* vals,
+                                                          uint64_t* gkeys, uint32_t* tile_end, float* loss_part,
+                                                          WsHeader* hdr, BlendIO io, int precull) {
+  constexpr int NT = TILE * TILE;
+  __shared__ uint64_t skeys[kMaxList];
+  __shared__ float4 s0[NT], s1[NT], s2[NT];
+  __shared__ float red[NT / 32 + 1];
+  __shared__ uint32_t redi[NT / 32 + 1];
+  const int t = blockIdx.x;
+  const int tx = t % a.tiles_x, ty = t / a.tiles_x;
+  const uint32_t start = min(offsets[t], a.cap);
+  const uint32_t end = min(offsets[t + 1], a.cap);
+  const int n = (int)(end - start);
+  // ---- per-tile sort by (depth bits, index) ----
+  if (n <= kMaxList) {
+    for (int e = threadIdx.x; e < n; e += NT) {
+      const uint32_t idx = vals[start + e];
+      const float d = rec[3 * idx + 1].z;
+      skeys[e] = ((uint64_t)__float_as_uint(d) << 32) | idx;
+    }
+    __syncthreads();
+    bitonic_sort(skeys, n);
+    for (int e = threadIdx.x; e < n; e += NT) vals[start + e] = (uint32_t)skeys[e];
+  } else {
+    uint64_t* gk = gkeys + start;
+    for (int e = threadIdx.x; e < n; e += NT) {
+      const uint32_t idx = vals[start + e];
+      gk[e] = ((uint64_t)__float_as_uint(rec[3 * idx + 1].z) << 32) | idx;
+    }
+    __syncthreads();
+    bitonic_sort(gk, n);
+    for (int e = threadIdx.x; e < n; e += NT) vals[start + e] = (uint32_t)gk[e];
+  }
+  __syncthreads();
+  // ---- pixel state ----
+  const int lx = threadIdx.x % TILE, ly = threadIdx.x / TILE;
+  const int x = tx * TILE + lx, y = ty * TILE + ly;
+  const bool inside = x < a.cam.W && y < a.cam.H;
+  const size_t pix = inside ? (size_t)y * a.cam.W + x : 0;
+  const float D = inside ? io.sdf_depth[pix] : 0.f;
+  const float lim = D > 0.f ? D + a.eps : INFINITY;  // R-MISS: no depth test on an SDF miss
+  const float fx = (float)x, fy = (float)y;
+  // optional pre-cull: entries at or behind every pixel's limit cannot contribute in this tile
+  int n_eff = n;
+  if (precull) {
+    float m = inside ? lim : -INFINITY;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      float mm = red[0];
+      for (int k = 1; k < NT / 32 + (NT % 32 ? 1 : 0); ++k) mm = fmaxf(mm, red[k]);
+      red[NT / 32] = mm;
+    }
+    __syncthreads();
+    const float tmax = red[NT / 32];
+    if (tmax < INFINITY) {  // binary search: first entry with d >= tmax
+      int lo = 0, hi = n;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        const float d = rec[3 * vals[start + mid] + 1].z;
+        if (d >= tmax) hi = mid; else lo = mid + 1;
+      }
+      n_eff = lo;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) tile_end[t] = start + n_eff;
+  // ---- front-to-back blend, Eqs. 1-3, early termination at the SDF depth ----
+  float W = 0.f, C0 = 0.f, C1 = 0.f, C2 = 0.f;
+  bool done = !inside;
+  for (int base = 0; base < n_eff; base += NT) {
+    const int cnt = min(NT, n_eff - base);
+    __syncthreads();
+    if (threadIdx.x < cnt) {
+      const uint32_t idx = vals[start + base + threadIdx.x];
+      s0[threadIdx.x] = rec[3 * idx];
+      s1[threadIdx.x] = rec[3 * idx + 1];
+      s2[threadIdx.x] = rec[3 * idx + 2];
+    }
+    __syncthreads();
+    if (!done) {
+      for (int k = 0; k < cnt; ++k) {
+        const float4 r1 = s1[k];
+        if (!(r1.z < lim)) {  // sorted by depth: every later entry fails Eq. 1's indicator too
+          done = true;
+          break;
+        }
+        const float4 r0 = s0[k];
+        const float dx = fx - r0.x, dy = fy - r0.y;
+        const float q = r0.z * dx * dx + 2.f * r0.w * dx * dy + r1.x * dy * dy;
+        if (q > 9.f) continue;  // outside the 3-sigma ellipse (R-FOOT)
+        const float al = r1.y * __expf(-0.5f * q);
+        if (al < a.alpha_min) continue;  // P:90 clamp
+        const float4 r2 = s2[k];
+        W += al;
+        C0 = fmaf(al, r2.x, C0);
+        C1 = fmaf(al, r2.y, C1);
+        C2 = fmaf(al, r2.z, C2);
+      }
+    }
+    if (__syncthreads_count(!done) == 0) break;
+  }
+  // ---- Eq. 4 composite with W_t = 1, fused L1 ----
+  float l1 = 0.f;
+  uint32_t inmask = 0;
+  if (inside) {
+    const float inv = 1.0f / (1.0f + W);
+    const float ct0 = io.sdf_color[3 * pix], ct1 = io.sdf_color[3 * pix + 1], ct2 = io.sdf_color[3 * pix + 2];
+    const float o0 = (ct0 + C0) * inv, o1 = (ct1 + C1) * inv, o2 = (ct2 + C2) * inv;
+    io.out_color[3 * pix] = W > 0.f ? o0 : ct0;
+    io.out_color[3 * pix + 1] = W > 0.f ? o1 : ct1;
+    io.out_color[3 * pix + 2] = W > 0.f ? o2 : ct2;
+    io.out_weight[pix] = W;
+    if (io.target && (D > 0.f || W > 0.f)) {
+      const uint32_t c = io.target[pix];
+      const float k0 = (float)(c & 0xFFu) * (1.f / 255.f), k1 = (float)((c >> 8) & 0xFFu) * (1.f / 255.f),
+                  k2 = (float)((c >> 16) & 0xFFu) * (1.f / 255.f);
+      const float r0 = W > 0.f ? o0 : ct0, r1 = W > 0.f ? o1 : ct1, r2 = W > 0.f ? o2 : ct2;
+      l1 = fabsf(r0 - k0) + fabsf(r1 - k1) + fabsf(r2 - k2);
+      inmask = 1;
+    }
+  }
+  if (!io.target) return;
+  // deterministic CTA reduction (fixed shuffle tree + fixed smem order)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    l1 += __shfl_xor_sync(0xFFFFFFFFu, l1, o);
+    inmask += __shfl_xor_sync(0xFFFFFFFFu, inmask, o);
+  }
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) {
+    red[threadIdx.x >> 5] = l1;
+    redi[threadIdx.x >> 5] = inmask;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float s = 0.f;
+    uint32_t m = 0;
+    for (int k = 0; k < (NT + 31) / 32; ++k) {
+      s += red[k];
+      m += redi[k];
+    }
+    loss_part[t] = s;
+    if (m) atomicAdd(&hdr->mask_count, m);
+    __threadfence();
+    const uint32_t ticket = atomicAdd(&hdr->ticket, 1u);
+    redi[0] = ticket == (uint32_t)(gridDim.x - 1) ? 1u : 0u;
+  }
+  __syncthreads();
+  if (redi[0] == 0u) return;
+  // last CTA: sum the tile partials in tile order (fixed tree) -> mean L1 (R-L1)
+  __threadfence();
+  float s = 0.f;
+  for (int k = threadIdx.x; k < (int)gridDim.x; k += NT) s += *(volatile float*)&loss_part[k];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float tot = 0.f;
+    for (int k = 0; k < (NT + 31) / 32; ++k) tot += red[k];
+    const uint32_t m = *(volatile uint32_t*)&hdr->mask_count;
+    const float lv = m ? tot / (3.0f * (float)m) : 0.0f;
+    if (io.loss_out) *io.loss_out = io.accumulate_loss ? *io.loss_out + lv : lv;
+    hdr->ticket = 0u;
+  }
+}
+
+// ============================================================================================
+// k_backward: exact gradient of the L1 loss w.r.t. each listed Gaussian's 2D quantities
+// (p_hat, conic, sigma, colour), R-GRAD.  Order of entries is irrelevant (no transmittance);
+// each tile list is walked back to front.
+// ============================================================================================
+__device__ __forceinline__ void red_add_v4(float4* addr, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
+               : "memory");
+}
+
+template <int TILE>
+__global__ void __launch_bounds__(256) k_backward(RenderArgs a, const float4* __restrict__ rec,
+                                                  const uint32_t* __restrict__ offsets,
+                                                  const uint32_t* __restrict__ vals,
+                                                  const uint32_t* __restrict__ tile_end,
+                                                  const float* __restrict__ sdf_depth,
+                                                  const float* __restrict__ cstar, const float* __restrict__ wg,
+                                                  const uint32_t* __restrict__ target, const WsHeader* hdr,
+                                                  float4* grad2d) {
+  constexpr int NP = TILE * TILE;
+  __shared__ float sg0[NP], sg1[NP], sg2[NP], ss[NP], slim[NP];
+  const int t = blockIdx.x;
+  const int tx = t % a.tiles_x, ty = t / a.tiles_x;
+  const uint32_t m = hdr->mask_count;
+  const float inv3m = m ? 1.0f / (3.0f * (float)m) : 0.0f;
+  for (int p = threadIdx.x; p < NP; p += blockDim.x) {
+    const int x = tx * TILE + p % TILE, y = ty * TILE + p / TILE;
+    float g0 = 0.f, g1 = 0.f, g2 = 0.f, s = 0.f, lim = -INFINITY;  // -inf: no pair passes
+    if (x < a.cam.W && y < a.cam.H && m) {
+      const size_t pix = (size_t)y * a.cam.W + x;
+      const float D = sdf_depth[pix], Wp = wg[pix];
+      if (D > 0.f || Wp > 0.f) {
+        const float A = 1.0f / (1.0f + Wp);
+        const uint32_t c = target[pix];
+        const float c0 = cstar[3 * pix], c1 = cstar[3 * pix + 1], c2 = cstar[3 * pix + 2];
+        const float d0 = c0 - (float)(c & 0xFFu) * (1.f / 255.f);
+        const float d1 = c1 - (float)((c >> 8) & 0xFFu) * (1.f / 255.f);
+        const float d2 = c2 - (float)((c >> 16) & 0xFFu) * (1.f / 255.f);
+        // dL/dC* = sign(C* - C_k) / (3|M|), sign(0) = 0
+        g0 = (d0 > 0.f ? inv3m : (d0 < 0.f ? -inv3m : 0.f)) * A;
+        g1 = (d1 > 0.f ? inv3m : (d1 < 0.f ? -inv3m : 0.f)) * A;
+        g2 = (d2 > 0.f ? inv3m : (d2 < 0.f ? -inv3m : 0.f)) * A;
+        s = g0 * c0 + g1 * c1 + g2 * c2;  // A * sum_ch g_ch C*_ch
+        lim = D > 0.f ? D + a.eps : INFINITY;
+      }
+    }
+    sg0[p] = g0; sg1[p] = g1; sg2[p] = g2; ss[p] = s; slim[p] = lim;
+  }
+  __syncthreads();
+  if (!m) return;
+  const uint32_t start = min(offsets[t], a.cap);
+  const uint32_t end = min(tile_end[t], a.cap);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int tx0 = tx * TILE, ty0 = ty * TILE;
+  for (int e = (int)end - 1 - warp; e >= (int)start; e -= nw) {
+    const uint32_t idx = vals[e];
+    const float4 r0 = rec[3 * idx], r1 = rec[3 * idx + 1], r2 = rec[3 * idx + 2];
+    const uint32_t rx = __float_as_uint(r1.w), ry = __float_as_uint(r2.w);
+    const int x0 = max((int)(rx & 0xFFFF), tx0), x1 = min((int)(rx >> 16), tx0 + TILE - 1);
+    const int y0 = max((int)(ry & 0xFFFF), ty0), y1 = min((int)(ry >> 16), ty0 + TILE - 1);
+    const int wx = x1 - x0 + 1, cnt = wx * (y1 - y0 + 1);
+    float dpx = 0.f, dpy = 0.f, da = 0.f, db = 0.f, dc = 0.f, dsig = 0.f, dr = 0.f, dg = 0.f, dbl = 0.f;
+    bool any = false;
+    for (int k = lane; k < cnt; k += 32) {
+      const int x = x0 + k % wx, y = y0 + k / wx;
+      const int p = (y - ty0) * TILE + (x - tx0);
+      if (!(r1.z < slim[p])) continue;  // Eq. 1 indicator (and inactive pixels)
+      const float dx = (float)x - r0.x, dy = (float)y - r0.y;
+      const float q = r0.z * dx * dx + 2.f * r0.w * dx * dy + r1.x * dy * dy;
+      if (q > 9.f) continue;
+      const float ex = __expf(-0.5f * q);
+      const float al = r1.y * ex;
+      if (al < a.alpha_min) continue;
+      const float gA0 = sg0[p], gA1 = sg1[p], gA2 = sg2[p];
+      // dL/dalpha = A * sum_ch g_ch (c_ch - C*_ch)
+      const float dal = gA0 * r2.x + gA1 * r2.y + gA2 * r2.z - ss[p];
+      dr = fmaf(gA0, al, dr);
+      dg = fmaf(gA1, al, dg);
+      dbl = fmaf(gA2, al, dbl);
+      dsig = fmaf(dal, ex, dsig);
+      const float dpow = -al * dal;
+      da = fmaf(dpow * 0.5f, dx * dx, da);
+      db = fmaf(dpow, dx * dy, db);
+      dc = fmaf(dpow * 0.5f, dy * dy, dc);
+      dpx = fmaf(-dpow, r0.z * dx + r0.w * dy, dpx);
+      dpy = fmaf(-dpow, r0.w * dx + r1.x * dy, dpy);
+      any = true;
+    }
+    if (!__any_sync(0xFFFFFFFFu, any)) continue;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      dpx += __shfl_xor_sync(0xFFFFFFFFu, dpx, o);
+      dpy += __shfl_xor_sync(0xFFFFFFFFu, dpy, o);
+      da += __shfl_xor_sync(0xFFFFFFFFu, da, o);
+      db += __shfl_xor_sync(0xFFFFFFFFu, db, o);
+      dc += __shfl_xor_sync(0xFFFFFFFFu, dc, o);
+      dsig += __shfl_xor_sync(0xFFFFFFFFu, dsig, o);
+      dr += __shfl_xor_sync(0xFFFFFFFFu, dr, o);
+      dg += __shfl_xor_sync(0xFFFFFFFFu, dg, o);
+      dbl += __shfl_xor_sync(0xFFFFFFFFu, dbl, o);
+    }
+    if (lane == 0) {
+      red_add_v4(grad2d + 3 * idx, dpx, dpy, da, db);
+      red_add_v4(grad2d + 3 * idx + 1, dc, dsig, dr, dg);
+      atomicAdd(reinterpret_cast<float*>(grad2d + 3 * idx + 2), dbl);
+    }
+  }
+}
+
+// ============================================================================================
+// k_grad_adam: raw-parameter gradient (R-GRAD chain rule) fused with dense Adam (R-ADAM)
+// ============================================================================================
+struct AdamArgs {
+  float b1, b2, eps;
+  float step_xyz, step_ls, step_rot, step_op, step_sh0, step_shr;  // lr / (1 - b1^t)
+  float inv_sqrt_bc2;                                               // 1 / sqrt(1 - b2^t)
+};
+
+enum { kModeFinal = 0, kModeAccum = 1, kModeExternal = 2 };
+
+__device__ __forceinline__ void adam1(float& p, float& m, float& v, float g, float step, const AdamArgs& ad) {
+  m = ad.b1 * m + (1.0f - ad.b1) * g;
+  v = ad.b2 * v + (1.0f - ad.b2) * g * g;
+  p -= step * m / (sqrtf(v) * ad.inv_sqrt_bc2 + ad.eps);
+}
+
+constexpr int kAdamThreads = 128;
+
+template <int MODE>
+__global__ void __launch_bounds__(kAdamThreads) k_grad_adam(RenderArgs a, gps_gaussians g, gps_gaussians gm,
+                                                            gps_gaussians gv, const float4* __restrict__ grad2d,
+                                                            gps_gaussians gbuf, int has_gbuf, gps_gaussians gout,
+                                                            int has_gout, AdamArgs ad) {
+  __shared__ float sY[kAdamThreads][16];
+  __shared__ float sdc[kAdamThreads][3];
+  const int64_t i0 = (int64_t)blockIdx.x * kAdamThreads;
+  const int64_t i = i0 + threadIdx.x;
+  const int nc = a.nc;
+  if (i < a.n) {
+    float gx[3] = {0, 0, 0}, gls[3] = {0, 0, 0}, gq[4] = {0, 0, 0, 0}, gop = 0.f;
+    float dcol[3] = {0, 0, 0};
+    float Y[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) Y[k] = 0.f;
+    if (MODE != kModeExternal) {
+      const float4 q0 = grad2d[3 * i], q1 = grad2d[3 * i + 1], q2 = grad2d[3 * i + 2];
+      const float dpx = q0.x, dpy = q0.y, da = q0.z, db = q0.w, dcc = q1.x, dsig = q1.y;
+      dcol[0] = q1.z; dcol[1] = q1.w; dcol[2] = q2.x;
+      const bool nz = (dpx != 0.f) | (dpy != 0.f) | (da != 0.f) | (db != 0.f) | (dcc != 0.f) | (dsig != 0.f) |
+                      (dcol[0] != 0.f) | (dcol[1] != 0.f) | (dcol[2] != 0.f);
+      if (nz) {
+        const float* p = g.xyz + 3 * i;
+        Proj pr;
+        project_p32(a.cam, a.near_z, a.lowpass, p, g.log_scale + 3 * i, g.rot + 4 * i, pr);
+        SH h;
+        view_dir(a.cam, p, a.deg, h);
+#pragma unroll
+        for (int k = 0; k < 16; ++k) Y[k] = k < nc ? h.Y[k] : 0.f;
+        const float* sh = g.sh + (size_t)i * nc * 3;
+        // opacity: sigma = sigmoid(o)
+        const float sig = 1.0f / (1.0f + __expf(-g.opacity_raw[i]));
+        gop = dsig * sig * (1.f - sig);
+        // colour -> SH and view direction (clamped channels get zero gradient)
+        float w[16];
+        float ddir[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {
+          float acc = 0.f;
+          for (int k = 0; k < nc; ++k) acc = fmaf(h.Y[k], sh[3 * k + ch], acc);
+          if (acc + 0.5f < 0.f) dcol[ch] = 0.f;
+        }
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+          w[k] = k < nc ? dcol[0] * sh[3 * k] + dcol[1] * sh[3 * k + 1] + dcol[2] * sh[3 * k + 2] : 0.f;
+        sh_basis_vjp(h.dir[0], h.dir[1], h.dir[2], a.deg, w, ddir);
+        const float dd = ddir[0] * h.dir[0] + ddir[1] * h.dir[1] + ddir[2] * h.dir[2];
+        const float invn = 1.f / h.dnorm;
+#pragma unroll
+        for (int e = 0; e < 3; ++e) gx[e] += (ddir[e] - h.dir[e] * dd) * invn;
+        // conic (a, b, c) -> Sigma_2D (cxx, cxy, cyy)
+        const float det = pr.det, id = 1.f / det, id2 = id * id;
+        const float cxx = pr.cxx, cxy = pr.cxy, cyy = pr.cyy;
+        const float dcxx = da * (-cyy * cyy * id2) + db * (cxy * cyy * id2) + dcc * (id - cxx * cyy * id2);
+        const float dcyy = da * (id - cyy * cxx * id2) + db * (cxy * cxx * id2) + dcc * (-cxx * cxx * id2);
+        const float dcxy = da * (2.f * cyy * cxy * id2) + db * (-id - 2.f * cxy * cxy * id2) + dcc * (2.f * cxx * cxy * id2);
+        // Sigma_2D = T S T^T + lowpass I
+        const float* T0 = pr.T;
+        const float* T1 = pr.T + 3;
+        float ST0[3], ST1[3];
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+          ST0[r] = pr.S[3 * r] * T0[0] + pr.S[3 * r + 1] * T0[1] + pr.S[3 * r + 2] * T0[2];
+          ST1[r] = pr.S[3 * r] * T1[0] + pr.S[3 * r + 1] * T1[1] + pr.S[3 * r + 2] * T1[2];
+        }
+        float dS[9], dT0[3], dT1[3];
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+#pragma unroll
+          for (int k = 0; k < 3; ++k) dS[3 * j + k] = dcxx * T0[j] * T0[k] + dcxy * T0[j] * T1[k] + dcyy * T1[j] * T1[k];
+          dT0[j] = 2.f * dcxx * ST0[j] + dcxy * ST1[j];
+          dT1[j] = dcxy * ST0[j] + 2.f * dcyy * ST1[j];
+        }
+        // T = J Wc  (Wc[r][c] = R[c][r])
+        float dJ00 = 0.f, dJ02 = 0.f, dJ11 = 0.f, dJ12 = 0.f;
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          dJ00 += dT0[j] * a.cam.R[j * 3 + 0];
+          dJ02 += dT0[j] * a.cam.R[j * 3 + 2];
+          dJ11 += dT1[j] * a.cam.R[j * 3 + 1];
+          dJ12 += dT1[j] * a.cam.R[j * 3 + 2];
+        }
+        const float z = pr.X[2], iz = 1.f / z, iz2 = iz * iz;
+        const float fx = a.cam.fx, fy = a.cam.fy;
+        float dX[3] = {0.f, 0.f, 0.f};
+        dX[2] += dJ00 * (-fx * iz2) + dJ11 * (-fy * iz2);
+        const float dcu_dx = pr.clx ? 0.f : iz, dcu_dz = pr.clx ? 0.f : -pr.X[0] * iz2;
+        const float dcv_dy = pr.cly ? 0.f : iz, dcv_dz = pr.cly ? 0.f : -pr.X[1] * iz2;
+        dX[0] += dJ02 * (-fx * iz) * dcu_dx;
+        dX[2] += dJ02 * (fx * pr.cu * iz2 - fx * iz * dcu_dz);
+        dX[1] += dJ12 * (-fy * iz) * dcv_dy;
+        dX[2] += dJ12 * (fy * pr.cv * iz2 - fy * iz * dcv_dz);
+        dX[0] += dpx * fx * iz;
+        dX[1] += dpy * fy * iz;
+        dX[2] += dpx * (-fx * pr.X[0] * iz2) + dpy * (-fy * pr.X[1] * iz2);
+#pragma unroll
+        for (int r = 0; r < 3; ++r) gx[r] += a.cam.R[3 * r] * dX[0] + a.cam.R[3 * r + 1] * dX[1] + a.cam.R[3 * r + 2] * dX[2];
+        // S = M M^T, M = Rq diag(s)
+        float dRq[9];
+#pragma unroll
+        for (int l = 0; l < 3; ++l) {
+          float ds = 0.f;
+#pragma unroll
+          for (int j = 0; j < 3; ++j) {
+            float dM = 0.f;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) dM += (dS[3 * j + k] + dS[3 * k + j]) * pr.M[3 * k + l];
+            dRq[3 * j + l] = dM * pr.s[l];
+            ds += dM * pr.Rq[3 * j + l];
+          }
+          gls[l] = ds * pr.s[l];
+        }
+        const float qw = pr.qh[0], qx = pr.qh[1], qy = pr.qh[2], qz = pr.qh[3];
+        float dqh[4];
+        dqh[0] = dRq[1] * (-2.f * qz) + dRq[2] * (2.f * qy) + dRq[3] * (2.f * qz) + dRq[5] * (-2.f * qx) +
+                 dRq[6] * (-2.f * qy) + dRq[7] * (2.f * qx);
+        dqh[1] = dRq[1] * (2.f * qy) + dRq[2] * (2.f * qz) + dRq[3] * (2.f * qy) + dRq[4] * (-4.f * qx) +
+                 dRq[5] * (-2.f * qw) + dRq[6] * (2.f * qz) + dRq[7] * (2.f * qw) + dRq[8] * (-4.f * qx);
+        dqh[2] = dRq[0] * (-4.f * qy) + dRq[1] * (2.f * qx) + dRq[2] * (2.f * qw) + dRq[3] * (2.f * qx) +
+                 dRq[5] * (2.f * qz) + dRq[6] * (-2.f * qw) + dRq[7] * (2.f * qz) + dRq[8] * (-4.f * qy);
+        dqh[3] = dRq[0] * (-4.f * qz) + dRq[1] * (-2.f * qw) + dRq[2] * (2.f * qx) + dRq[3] * (2.f * qw) +
+                 dRq[4] * (-4.f * qz) + dRq[5] * (2.f * qy) + dRq[6] * (2.f * qx) + dRq[7] * (2.f * qy);
+        const float dot = dqh[0] * qw + dqh[1] * qx + dqh[2] * qy + dqh[3] * qz;
+        const float iqn = 1.f / pr.qn;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) gq[k] = (dqh[k] - pr.qh[k] * dot) * iqn;
+      } else {
+        dcol[0] = dcol[1] = dcol[2] = 0.f;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        gx[k] = gbuf.xyz[3 * i + k];
+        gls[k] = gbuf.log_scale[3 * i + k];
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) gq[k] = gbuf.rot[4 * i + k];
+      gop = gbuf.opacity_raw[i];
+    }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) sY[threadIdx.x][k] = Y[k];
+    sdc[threadIdx.x][0] = dcol[0]; sdc[threadIdx.x][1] = dcol[1]; sdc[threadIdx.x][2] = dcol[2];
+    if (MODE == kModeAccum) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        gbuf.xyz[3 * i + k] += gx[k];
+        gbuf.log_scale[3 * i + k] += gls[k];
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) gbuf.rot[4 * i + k] += gq[k];
+      gbuf.opacity_raw[i] += gop;
+    } else {
+      if (MODE == kModeFinal && has_gbuf) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          gx[k] += gbuf.xyz[3 * i + k];
+          gls[k] += gbuf.log_scale[3 * i + k];
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) gq[k] += gbuf.rot[4 * i + k];
+        gop += gbuf.opacity_raw[i];
+      }
+      if (has_gout) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          gout.xyz[3 * i + k] = gx[k];
+          gout.log_scale[3 * i + k] = gls[k];
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) gout.rot[4 * i + k] = gq[k];
+        gout.opacity_raw[i] = gop;
+      }
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        adam1(g.xyz[3 * i + k], gm.xyz[3 * i + k], gv.xyz[3 * i + k], gx[k], ad.step_xyz, ad);
+        adam1(g.log_scale[3 * i + k], gm.log_scale[3 * i + k], gv.log_scale[3 * i + k], gls[k], ad.step_ls, ad);
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) adam1(g.rot[4 * i + k], gm.rot[4 * i + k], gv.rot[4 * i + k], gq[k], ad.step_rot, ad);
+      adam1(g.opacity_raw[i], gm.opacity_raw[i], gv.opacity_raw[i], gop, ad.step_op, ad);
+    }
+  }
+  __syncthreads();
+  // ---- SH coefficients: coalesced sweep over this CTA's contiguous block ----
+  const int64_t nG = min((int64_t)kAdamThreads, a.n - i0);
+  if (nG <= 0) return;
+  const int per = nc * 3;
+  const int64_t base = i0 * per;
+  const int total = (int)(nG * per);
+  for (int e = threadIdx.x; e < total; e += kAdamThreads) {
+    const int gi = e / per, r = e - gi * per, k = r / 3, ch = r - 3 * k;
+    float grad = MODE == kModeExternal ? gbuf.sh[base + e] : sY[gi][k] * sdc[gi][ch];
+    if (MODE == kModeAccum) {
+      gbuf.sh[base + e] += grad;
+      continue;
+    }
+    if (MODE == kModeFinal && has_gbuf) grad += gbuf.sh[base + e];
+    if (has_gout) gout.sh[base + e] = grad;
+    adam1(g.sh[base + e], gm.sh[base + e], gv.sh[base + e], grad, k == 0 ? ad.step_sh0 : ad.step_shr, ad);
+  }
+}
+
+}  // namespace gps
+
+using namespace gps;
+
+namespace {
+
+bool valid_K(const gps_intrinsics* K) {
+  return K && K->width > 0 && K->height > 0 && K->fx > 0 && K->fy > 0 && K->width <= 65535 && K->height <= 65535;
+}
+
+gps_status check_gaussians(const gps_gaussians* g, const char* who) {
+  if (!g) return invalid(std::string(who) + ": null Gaussians");
+  if (g->n < 0 || g->n > 0x7FFFFFFFll) return invalid(std::string(who) + ": bad Gaussian count");
+  if (g->sh_degree < 0 || g->sh_degree > 3) return invalid(std::string(who) + ": sh_degree must be 0..3");
+  if (g->n > 0 && (!g->xyz || !g->log_scale || !g->rot || !g->opacity_raw || !g->sh))
+    return invalid(std::string(who) + ": null Gaussian array");
+  if (g->n > 0 && (!aligned16(g->xyz) || !aligned16(g->log_scale) || !aligned16(g->rot) ||
+                   !aligned16(g->opacity_raw) || !aligned16(g->sh)))
+    return invalid(std::string(who) + ": Gaussian arrays must be 16-byte aligned");
+  return GPS_OK;
+}
+
+bool same_shape(const gps_gaussians* a, const gps_gaussians* b) { return a->n == b->n && a->sh_degree == b->sh_degree; }
+
+RenderArgs make_args(const gps_gaussians* g, const gps_intrinsics* K, const gps_pose* T, const gps_render_config* c,
+                     int64_t cap) {
+  RenderArgs a;
+  a.cam.fx = K->fx; a.cam.fy = K->fy; a.cam.cx = K->cx; a.cam.cy = K->cy; a.cam.W = K->width; a.cam.H = K->height;
+  for (int i = 0; i < 9; ++i) a.cam.R[i] = T->R[i];
+  for (int i = 0; i < 3; ++i) a.cam.t[i] = T->t[i];
+  a.eps = c->eps_depth; a.alpha_min = c->alpha_min; a.near_z = c->near_z; a.lowpass = c->lowpass;
+  a.tile = c->tile;
+  a.tiles_x = (K->width + c->tile - 1) / c->tile;
+  a.tiles_y = (K->height + c->tile - 1) / c->tile;
+  a.n = g->n;
+  a.deg = g->sh_degree;
+  a.nc = (g->sh_degree + 1) * (g->sh_degree + 1);
+  a.cap = (uint32_t)std::min<int64_t>(cap, 0xFFFFFFFFll);
+  return a;
+}
+
+gps_gaussians slice_params(const gps_gaussians* g, float* base) {
+  // a gps_gaussians view over one dense float buffer laid out group after group
+  gps_gaussians o = *g;
+  const int64_t n = g->n;
+  o.xyz = base;
+  o.log_scale = base + 3 * n;
+  o.rot = base + 6 * n;
+  o.opacity_raw = base + 10 * n;
+  o.sh = base + align_up(11 * n, 4);
+  return o;
+}
+int64_t gbuf_floats(const gps_gaussians* g) {
+  return (int64_t)align_up(11 * g->n, 4) + 3 * g->n * (g->sh_degree + 1) * (g->sh_degree + 1);
+}
+
+struct View1 {
+  const gps_intrinsics* K;
+  const gps_pose* T;
+  const float* sdf_depth;
+  const float* sdf_color;
+  const uint8_t* target;
+};
+
+// forward of one view: preprocess .. sort_blend.  ws must follow ws_layout(refine).
+gps_status forward_view(const gps_gaussians* g, const View1& v, const gps_render_config* c, char* ws,
+                        const WsLayout& L, int64_t cap, float* out_color, float* out_weight, float* loss_out,
+                        int accumulate_loss, bool zero_grad2d, cudaStream_t s) {
+  RenderArgs a = make_args(g, v.K, v.T, c, cap);
+  WsHeader* hdr = reinterpret_cast<WsHeader*>(ws + L.hdr);
+  {
+    GPS_PROF(K_MEMSET, s);
+    GPS_CHECK_CUDA(cudaMemsetAsync(ws + L.zero_begin, 0, L.zero_bytes, s));
+  }
+  SplatPtrs sp;
+  sp.rec = reinterpret_cast<float4*>(ws + L.records);
+  sp.grad2d = zero_grad2d ? reinterpret_cast<float4*>(ws + L.grad2d) : nullptr;
+  sp.counts = reinterpret_cast<uint32_t*>(ws + L.counts);
+  sp.hdr = hdr;
+  const int n_tiles = a.tiles_x * a.tiles_y;
+  if (g->n > 0) {
+    GPS_PROF(K_PREPROCESS, s);
+    k_preprocess<<<(unsigned)((g->n + 255) / 256), 256, 0, s>>>(a, *g, sp);
+    GPS_CHECK_LAUNCH("k_preprocess");
+  }
+  WsHeader stat{};
+  stat.magic = kWsMagic; stat.tile = a.tile; stat.tiles_x = a.tiles_x; stat.tiles_y = a.tiles_y;
+  stat.width = a.cam.W; stat.height = a.cam.H; stat.n_tiles = n_tiles; stat.cap_pairs = a.cap; stat.n = g->n;
+  stat.off_vals = L.vals; stat.off_offsets = L.offsets; stat.off_tile_end = L.tile_end;
+  uint32_t* offsets = reinterpret_cast<uint32_t*>(ws + L.offsets);
+  {
+    GPS_PROF(K_SCAN, s);
+    k_scan<<<1, 1024, 0, s>>>(sp.counts, offsets, n_tiles, hdr, stat);
+  }
+  GPS_CHECK_LAUNCH("k_scan");
+  uint32_t* vals = reinterpret_cast<uint32_t*>(ws + L.vals);
+  if (g->n > 0) {
+    GPS_PROF(K_EMIT, s);
+    k_emit<<<(unsigned)((g->n + 255) / 256), 256, 0, s>>>(a, sp.rec, offsets,
+                                                          reinterpret_cast<uint32_t*>(ws + L.cursor), vals);
+    GPS_CHECK_LAUNCH("k_emit");
+  }
+  BlendIO io;
+  io.sdf_depth = v.sdf_depth;
+  io.sdf_color = v.sdf_color;
+  io.target = reinterpret_cast<const uint32_t*>(v.target);
+  io.out_color = out_color;
+  io.out_weight = out_weight;
+  io.loss_out = loss_out;
+  io.accumulate_loss = accumulate_loss;
+  uint64_t* gk = reinterpret_cast<uint64_t*>(ws + L.keys);
+  uint32_t* tend = reinterpret_cast<uint32_t*>(ws + L.tile_end);
+  float* lp = reinterpret_cast<float*>(ws + L.loss_part);
+  {
+  GPS_PROF(K_SORT_BLEND, s);
+  if (a.tile == 16)
+    k_sort_blend<16><<<n_tiles, 256, 0, s>>>(a, sp.rec, offsets, vals, gk, tend, lp, hdr, io, c->tile_depth_precull);
+  else
+    k_sort_blend<8><<<n_tiles, 64, 0, s>>>(a, sp.rec, offsets, vals, gk, tend, lp, hdr, io, c->tile_depth_precull);
+  }
+  GPS_CHECK_LAUNCH("k_sort_blend");
+  return GPS_OK;
+}
+
+gps_status check_render_cfg(const gps_render_config* c) {
+  if (!c) return invalid("null render config");
+  if (c->tile != 8 && c->tile != 16) return invalid("render config: tile must be 8 or 16");
+  if (!(c->eps_depth >= 0) || !(c->alpha_min >= 0) || !(c->lowpass >= 0)) return invalid("render config: bad value");
+  if (c->max_pairs < 0 || c->max_pairs > 0xFFFFFFFFll) return invalid("render config: bad max_pairs");
+  return GPS_OK;
+}
+
+AdamArgs make_adam(const gps_adam_config* c, int64_t step) {
+  AdamArgs a;
+  const double t = (double)step;
+  const double bc1 = 1.0 - std::pow((double)c->beta1, t), bc2 = 1.0 - std::pow((double)c->beta2, t);
+  a.b1 = c->beta1; a.b2 = c->beta2; a.eps = c->eps;
+  a.step_xyz = (float)(c->lr_xyz / bc1);
+  a.step_ls = (float)(c->lr_scale / bc1);
+  a.step_rot = (float)(c->lr_rot / bc1);
+  a.step_op = (float)(c->lr_opacity / bc1);
+  a.step_sh0 = (float)(c->lr_sh0 / bc1);
+  a.step_shr = (float)(c->lr_shrest / bc1);
+  a.inv_sqrt_bc2 = (float)(1.0 / std::sqrt(bc2));
+  return a;
+}
+
+gps_status check_adam_state(const gps_gaussians* g, const gps_adam_state* st) {
+  if (!st) return invalid("null Adam state");
+  if (!same_shape(g, &st->m) || !same_shape(g, &st->v)) return invalid("Adam state shape differs from the parameters");
+  gps_status r = check_gaussians(&st->m, "adam m");
+  if (r != GPS_OK) return r;
+  return check_gaussians(&st->v, "adam v");
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t gps_render_workspace_size(int64_t n, const gps_intrinsics* K, const gps_render_config* cfg) {
+  if (!valid_K(K) || !cfg || (cfg->tile != 8 && cfg->tile != 16) || n < 0) return 0;
+  return ws_layout(n, K->width, K->height, cfg->tile, default_cap(n, cfg->max_pairs), 0, false, false).total;
+}
+
+size_t gps_refine_workspace_size(int64_t n, const gps_intrinsics* K, const gps_render_config* cfg, int32_t n_views) {
+  if (!valid_K(K) || !cfg || (cfg->tile != 8 && cfg->tile != 16) || n < 0 || n_views < 1) return 0;
+  gps_gaussians dummy{};
+  dummy.n = n;
+  dummy.sh_degree = 3;  // size for the largest degree
+  return ws_layout(n, K->width, K->height, cfg->tile, default_cap(n, cfg->max_pairs), gbuf_floats(&dummy), true,
+                   n_views > 1)
+      .total;
+}
+
+gps_status gps_render(const gps_gaussians* g, const gps_intrinsics* K, const gps_pose* T, const float* sdf_depth,
+                      const float* sdf_color, const uint8_t* target_rgba, const gps_render_config* cfg, void* ws,
+                      size_t ws_bytes, float* out_color, float* out_weight, float* loss_out, gps_stream_t stream) {
+  gps_status st = check_gaussians(g, "gps_render");
+  if (st != GPS_OK) return st;
+  if ((st = check_render_cfg(cfg)) != GPS_OK) return st;
+  if (!valid_K(K) || !T || !sdf_depth || !sdf_color || !ws || !out_color || !out_weight)
+    return invalid("gps_render: null or bad argument");
+  if (loss_out && !target_rgba) return invalid("gps_render: loss_out needs target_rgba");
+  if (target_rgba && (reinterpret_cast<uintptr_t>(target_rgba) & 3u)) return invalid("gps_render: target must be 4-byte aligned");
+  const int64_t cap = default_cap(g->n, cfg->max_pairs);
+  const WsLayout L = ws_layout(g->n, K->width, K->height, cfg->tile, cap, 0, false, false);
+  if (ws_bytes < L.total) {
+    set_error("gps_render: workspace too small");
+    return GPS_ERR_WORKSPACE_TOO_SMALL;
+  }
+  if (!aligned16(ws)) return invalid("gps_render: workspace must be 16-byte aligned");
+  View1 v{K, T, sdf_depth, sdf_color, target_rgba};
+  return forward_view(g, v, cfg, static_cast<char*>(ws), L, cap, out_color, out_weight, loss_out, 0, false,
+                      as_stream(stream));
+}
+
+gps_status gps_refine_step(gps_gaussians* g, gps_adam_state* state, const gps_view* views, int32_t n_views,
+                           const gps_render_config* rcfg, const gps_adam_config* acfg, void* ws, size_t ws_bytes,
+                           float* loss_out, const gps_gaussians* grad_out, gps_stream_t stream) {
+  gps_status st = check_gaussians(g, "gps_refine_step");
+  if (st != GPS_OK) return st;
+  if ((st = check_render_cfg(rcfg)) != GPS_OK) return st;
+  if ((st = check_adam_state(g, state)) != GPS_OK) return st;
+  if (!views || n_views < 1 || !acfg || !ws) return invalid("gps_refine_step: bad argument");
+  if (grad_out) {
+    if (!same_shape(g, grad_out)) return invalid("gps_refine_step: grad_out shape differs");
+    if ((st = check_gaussians(grad_out, "grad_out")) != GPS_OK) return st;
+  }
+  int maxW = 0, maxH = 0;
+  for (int v = 0; v < n_views; ++v) {
+    const gps_view& vw = views[v];
+    if (!valid_K(&vw.K) || !vw.sdf_depth || !vw.sdf_color || !vw.target_rgba)
+      return invalid("gps_refine_step: bad view " + std::to_string(v));
+    if (reinterpret_cast<uintptr_t>(vw.target_rgba) & 3u) return invalid("gps_refine_step: target must be 4-byte aligned");
+    maxW = std::max(maxW, vw.K.width);
+    maxH = std::max(maxH, vw.K.height);
+  }
+  if (!aligned16(ws)) return invalid("gps_refine_step: workspace must be 16-byte aligned");
+  const int64_t cap = default_cap(g->n, rcfg->max_pairs);
+  gps_gaussians dummy{};
+  dummy.n = g->n;
+  dummy.sh_degree = 3;
+  const WsLayout L = ws_layout(g->n, maxW, maxH, rcfg->tile, cap, gbuf_floats(&dummy), true, n_views > 1);
+  if (ws_bytes < L.total) {
+    set_error("gps_refine_step: workspace too small");
+    return GPS_ERR_WORKSPACE_TOO_SMALL;
+  }
+  cudaStream_t s = as_stream(stream);
+  char* w = static_cast<char*>(ws);
+  WsHeader* hdr = reinterpret_cast<WsHeader*>(w + L.hdr);
+  float4* grad2d = reinterpret_cast<float4*>(w + L.grad2d);
+  float* cstar = reinterpret_cast<float*>(w + L.cstar);
+  float* wg = reinterpret_cast<float*>(w + L.wg);
+  gps_gaussians gb = n_views > 1 ? slice_params(g, reinterpret_cast<float*>(w + L.gbuf)) : gps_gaussians{};
+  if (n_views > 1)
+    GPS_CHECK_CUDA(cudaMemsetAsync(w + L.gbuf, 0, sizeof(float) * gbuf_floats(g), s));
+  if (loss_out) GPS_CHECK_CUDA(cudaMemsetAsync(loss_out, 0, sizeof(float), s));
+  AdamArgs ad = make_adam(acfg, state->step + 1);
+  const gps_gaussians gout = grad_out ? *grad_out : gps_gaussians{};
+  for (int v = 0; v < n_views; ++v) {
+    const gps_view& vw = views[v];
+    View1 v1{&vw.K, &vw.T, vw.sdf_depth, vw.sdf_color, vw.target_rgba};
+    st = forward_view(g, v1, rcfg, w, L, cap, cstar, wg, loss_out, 1, true, s);
+    if (st != GPS_OK) return st;
+    RenderArgs a = make_args(g, &vw.K, &vw.T, rcfg, cap);
+    const int n_tiles = a.tiles_x * a.tiles_y;
+    const uint32_t* offsets = reinterpret_cast<const uint32_t*>(w + L.offsets);
+    const uint32_t* vals = reinterpret_cast<const uint32_t*>(w + L.vals);
+    const uint32_t* tend = reinterpret_cast<const uint32_t*>(w + L.tile_end);
+    const float4* rec = reinterpret_cast<const float4*>(w + L.records);
+    const uint32_t* tgt = reinterpret_cast<const uint32_t*>(vw.target_rgba);
+    {
+    GPS_PROF(K_BACKWARD, s);
+    if (rcfg->tile == 16)
+      k_backward<16><<<n_tiles, 256, 0, s>>>(a, rec, offsets, vals, tend, vw.sdf_depth, cstar, wg, tgt, hdr, grad2d);
+    else
+      k_backward<8><<<n_tiles, 256, 0, s>>>(a, rec, offsets, vals, tend, vw.sdf_depth, cstar, wg, tgt, hdr, grad2d);
+    }
+    GPS_CHECK_LAUNCH("k_backward");
+    if (g->n > 0) {
+      const unsigned grid = (unsigned)((g->n + kAdamThreads - 1) / kAdamThreads);
+      GPS_PROF(K_GRAD_ADAM, s);
+      if (v < n_views - 1)
+        k_grad_adam<kModeAccum><<<grid, kAdamThreads, 0, s>>>(a, *g, state->m, state->v, grad2d, gb, 1, gout, 0, ad);
+      else
+        k_grad_adam<kModeFinal><<<grid, kAdamThreads, 0, s>>>(a, *g, state->m, state->v, grad2d, gb, n_views > 1,
+                                                               gout, grad_out != nullptr, ad);
+      GPS_CHECK_LAUNCH("k_grad_adam");
+    }
+  }
+  state->step += 1;
+  return GPS_OK;
+}
+
+gps_status gps_adam_step(gps_gaussians* g, gps_adam_state* state, const gps_gaussians* grad,
+                         const gps_adam_config* acfg, gps_stream_t stream) {
+  gps_status st = check_gaussians(g, "gps_adam_step");
+  if (st != GPS_OK) return st;
+  if ((st = check_adam_state(g, state)) != GPS_OK) return st;
+  if (!grad || !acfg || !same_shape(g, grad)) return invalid("gps_adam_step: bad gradient argument");
+  if ((st = check_gaussians(grad, "grad")) != GPS_OK) return st;
+  AdamArgs ad = make_adam(acfg, state->step + 1);
+  RenderArgs a{};
+  a.n = g->n;
+  a.deg = g->sh_degree;
+  a.nc = (g->sh_degree + 1) * (g->sh_degree + 1);
+  if (g->n > 0) {
+    const unsigned grid = (unsigned)((g->n + kAdamThreads - 1) / kAdamThreads);
+    k_grad_adam<kModeExternal><<<grid, kAdamThreads, 0, as_stream(stream)>>>(a, *g, state->m, state->v, nullptr, *grad,
+                                                                             1, gps_gaussians{}, 0, ad);
+    GPS_CHECK_LAUNCH("k_grad_adam");
+  }
+  state->step += 1;
+  return GPS_OK;
+}
+
+gps_status gps_render_stats_sync(const void* ws, gps_stream_t stream, int64_t* n_pairs, int64_t* capacity,
+                                 int64_t* n_visible) {
+  if (!ws) return invalid("gps_render_stats_sync: null workspace");
+  WsHeader h;
+  GPS_CHECK_CUDA(cudaMemcpyAsync(&h, ws, sizeof(h), cudaMemcpyDeviceToHost, as_stream(stream)));
+  GPS_CHECK_CUDA(cudaStreamSynchronize(as_stream(stream)));
+  if (h.magic != kWsMagic) return invalid("gps_render_stats_sync: workspace holds no render");
+  if (n_pairs) *n_pairs = h.K;
+  if (capacity) *capacity = (int64_t)h.cap_pairs;
+  if (n_visible) *n_visible = h.n_visible;
+  if (h.overflow) {
+    set_error("render pair list overflow: " + std::to_string(h.K) + " pairs > capacity " + std::to_string(h.cap_pairs));
+    return GPS_ERR_WORKSPACE_TOO_SMALL;
+  }
+  return GPS_OK;
+}
+
+gps_status gps_debug_render_lists_sync(const void* ws, gps_stream_t stream, uint32_t* values, int64_t cap,
+                                       uint32_t* ranges, int64_t* K) {
+  if (!ws || !K) return invalid("gps_debug_render_lists_sync: null argument");
+  cudaStream_t s = as_stream(stream);
+  WsHeader h;
+  GPS_CHECK_CUDA(cudaMemcpyAsync(&h, ws, sizeof(h), cudaMemcpyDeviceToHost, s));
+  GPS_CHECK_CUDA(cudaStreamSynchronize(s));
+  if (h.magic != kWsMagic) return invalid("gps_debug_render_lists_sync: workspace holds no render");
+  const char* w = static_cast<const char*>(ws);
+  *K = h.K;
+  if (values) {
+    const int64_t cnt = std::min<int64_t>({cap, (int64_t)h.K, (int64_t)h.cap_pairs});
+    GPS_CHECK_CUDA(cudaMemcpyAsync(values, w + h.off_vals, 4 * cnt, cudaMemcpyDeviceToDevice, s));
+  }
+  if (ranges) {
+    // ranges[2t] = offsets[t], ranges[2t+1] = tile_end[t]
+    std::vector<uint32_t> off(h.n_tiles + 1), te(h.n_tiles);
+    GPS_CHECK_CUDA(cudaMemcpyAsync(off.data(), w + h.off_offsets, 4 * (h.n_tiles + 1), cudaMemcpyDeviceToHost, s));
+    GPS_CHECK_CUDA(cudaMemcpyAsync(te.data(), w + h.off_tile_end, 4 * h.n_tiles, cudaMemcpyDeviceToHost, s));
+    GPS_CHECK_CUDA(cudaStreamSynchronize(s));
+    std::vector<uint32_t> r(2 * h.n_tiles);
+    for (uint32_t t = 0; t < h.n_tiles; ++t) {
+      r[2 * t] = off[t];
+      r[2 * t + 1] = te[t];
+    }
+    GPS_CHECK_CUDA(cudaMemcpyAsync(ranges, r.data(), 4 * r.size(), cudaMemcpyHostToDevice, s));
+  }
+  GPS_CHECK_CUDA(cudaStreamSynchronize(s));
+  return GPS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,646 @@
+// volume.cu -- voxel-block hash volume: gps_volume_*, gps_fuse (allocation + integration) and
+// gps_raycast for sm_100a.
+//
+// Paper: GPS-SLAM (arXiv 2509.11574) Sec. 3.2.1 "SDF fusion", PAPER.md P:106 ("Following
+// InfiniTAM ... we perform standard SDF fusion to update the SDF and color values in a global
+// hash table. Afterwards, the raycast is performed"), voxel contents P:60, raycast P:70-73.
+// Readings R-BAND, R-INT, R-RAY and the prescribed fp32 sequences: DESIGN.md §3-§4.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "common.cuh"
+#include "prof.cuh"
+
+namespace gps {
+
+// ============================================================================================
+// allocation: one CTA per 32x32 pixel patch, 256 threads x 4 pixels (one 8-byte depth load
+// each); band blocks are de-duplicated in a CTA-local shared-memory hash set before any
+// global hash traffic (hundreds of pixels share a block).
+// ============================================================================================
+constexpr int kAllocPatch = 32;
+constexpr int kSmemSet = 2048;
+
+struct FuseParams {
+  float fx, fy, cx, cy;
+  int W, H;
+  float R[9], t[3];
+  float scale, mu, voxel, bs, dmin, dmax;
+  int wmax;
+};
+
+__device__ __forceinline__ void mark_visible(const VolumeView& v, uint32_t slot, uint32_t frame,
+                                             uint32_t* d_flag) {
+  if (v.stamp[slot] == frame) return;
+  if (atomicExch(&v.stamp[slot], frame) == frame) return;
+  const uint32_t idx = atomicAdd(&v.ctr->n_vis, 1u);
+  if (idx < v.max_blocks) {
+    v.vis[idx] = (int32_t)slot;
+  } else {
+    v.ctr->overflow = 1u;
+    *(volatile uint32_t*)d_flag = 1u;
+  }
+}
+
+__device__ void global_insert(const VolumeView& v, uint64_t key, uint32_t frame, uint32_t* d_flag) {
+  int x, y, z;
+  unpack_block(key, x, y, z);
+  uint32_t h = hash_block(x, y, z) & v.slot_mask;
+  for (uint32_t probe = 0; probe <= v.slot_mask; ++probe) {
+    uint64_t k = *(volatile uint64_t*)&v.keys[h];
+    if (k == key) {
+      mark_visible(v, h, frame, d_flag);
+      return;
+    }
+    if (k == kEmptyKey) {
+      const unsigned long long old = atomicCAS((unsigned long long*)&v.keys[h], (unsigned long long)kEmptyKey,
+                                               (unsigned long long)key);
+      if (old == kEmptyKey) {
+        const uint32_t b = atomicAdd(&v.ctr->n_blocks, 1u);
+        if (b < v.max_blocks) {
+          v.vals[h] = (int32_t)b;  // the pool block was initialised empty at create/reset
+        } else {
+          v.ctr->overflow = 1u;
+          *(volatile uint32_t*)d_flag = 1u;
+        }
+        mark_visible(v, h, frame, d_flag);
+        return;
+      }
+      if (old == key) {
+        mark_visible(v, h, frame, d_flag);
+        return;
+      }
+    }
+    h = (h + 1) & v.slot_mask;
+  }
+  v.ctr->overflow = 1u;  // table full
+  *(volatile uint32_t*)d_flag = 1u;
+}
+
+__device__ __forceinline__ void set_insert(unsigned long long* set, uint64_t key, const VolumeView& v,
+                                           uint32_t frame, uint32_t* d_flag) {
+  int x, y, z;
+  unpack_block(key, x, y, z);
+  uint32_t h = hash_block(x, y, z) & (kSmemSet - 1);
+  for (int probe = 0; probe < kSmemSet; ++probe) {
+    const unsigned long long old = atomicCAS(&set[h], (unsigned long long)kEmptyKey, (unsigned long long)key);
+    if (old == kEmptyKey || old == key) return;
+    h = (h + 1) & (kSmemSet - 1);
+  }
+  global_insert(v, key, frame, d_flag);  // CTA set full: go straight to the global table
+}
+
+// R-BAND for one pixel: the prescribed fp32 sequence of DESIGN.md §4.1, then every block of the
+// axis-aligned boxes spanned by consecutive samples' blocks.
+__device__ __forceinline__ void pixel_blocks(const FuseParams& p, int u, int vv, uint16_t raw,
+                                             unsigned long long* set, const VolumeView& v,
+                                             uint32_t frame, uint32_t* d_flag) {
+  const float d = pdiv((float)raw, p.scale);
+  if (!(d >= p.dmin && d <= p.dmax)) return;
+  const float xn = pdiv(psub((float)u, p.cx), p.fx);
+  const float yn = pdiv(psub((float)vv, p.cy), p.fy);
+  const float X[3] = {pmul(xn, d), pmul(yn, d), d};
+  float n2 = padd(pmul(X[0], X[0]), pmul(X[1], X[1]));
+  n2 = padd(n2, pmul(X[2], X[2]));
+  const float q = pdiv(p.mu, psqrt(n2));
+  const float a = psub(1.0f, q), b = padd(1.0f, q);
+  float A[3], B[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    A[k] = pmul(X[k], a);
+    B[k] = pmul(X[k], b);
+  }
+  int blk[5][3];
+#pragma unroll
+  for (int s = 0; s < 5; ++s) {
+    const float f = (float)s * 0.25f;
+    float Q[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) Q[k] = padd(A[k], pmul(psub(B[k], A[k]), f));
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const float Wr = padd(pdot3(p.R[3 * r + 0], Q[0], p.R[3 * r + 1], Q[1], p.R[3 * r + 2], Q[2]), p.t[r]);
+      blk[s][r] = (int)floorf(pdiv(Wr, p.bs));
+    }
+  }
+  uint64_t last = kEmptyKey;
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    const int x0 = min(blk[s][0], blk[s + 1][0]), x1 = max(blk[s][0], blk[s + 1][0]);
+    const int y0 = min(blk[s][1], blk[s + 1][1]), y1 = max(blk[s][1], blk[s + 1][1]);
+    const int z0 = min(blk[s][2], blk[s + 1][2]), z1 = max(blk[s][2], blk[s + 1][2]);
+    for (int z = z0; z <= z1; ++z)
+      for (int y = y0; y <= y1; ++y)
+        for (int x = x0; x <= x1; ++x) {
+          const uint64_t key = pack_block(x, y, z);
+          if (key != last) set_insert(set, key, v, frame, d_flag);
+          last = key;
+        }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_alloc(VolumeView v, FuseParams p,
+                                               const uint16_t* __restrict__ depth, uint32_t frame,
+                                               uint32_t* d_flag) {
+  __shared__ unsigned long long set[kSmemSet];
+  for (int i = threadIdx.x; i < kSmemSet; i += blockDim.x) set[i] = kEmptyKey;
+  __syncthreads();
+  const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;
+  const int y = blockIdx.y * kAllocPatch + ty;
+  const int x0 = blockIdx.x * kAllocPatch + tx * 4;
+  if (y < p.H && x0 < p.W) {
+    const uint16_t* row = depth + (size_t)y * p.W;
+    uint16_t d4[4] = {0, 0, 0, 0};
+    if (x0 + 3 < p.W && ((reinterpret_cast<uintptr_t>(row + x0) & 7u) == 0)) {
+      const ushort4 q = *reinterpret_cast<const ushort4*>(row + x0);  // coalesced 8-byte load
+      d4[0] = q.x; d4[1] = q.y; d4[2] = q.z; d4[3] = q.w;
+    } else {
+      for (int k = 0; k < 4; ++k)
+        if (x0 + k < p.W) d4[k] = row[x0 + k];
+    }
+#pragma unroll 1
+    for (int k = 0; k < 4; ++k)
+      if (x0 + k < p.W && d4[k] != 0) pixel_blocks(p, x0 + k, y, d4[k], set, v, frame, d_flag);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kSmemSet; i += blockDim.x) {
+    const uint64_t key = set[i];
+    if (key != kEmptyKey) global_insert(v, key, frame, d_flag);
+  }
+}
+
+// ============================================================================================
+// integration (R-INT): grid-stride over the visible list; one CTA per block, 256 threads x 2
+// adjacent voxels (one 16-byte load/store each).  Prescribed fp32, DESIGN.md §4.2.
+// ============================================================================================
+__device__ __forceinline__ void integrate_voxel(const FuseParams& p, int gx, int gy, int gz, Voxel& vx,
+                                                const uint16_t* __restrict__ depth,
+                                                const uint32_t* __restrict__ rgba) {
+  const float P0 = pmul((float)gx, p.voxel), P1 = pmul((float)gy, p.voxel), P2 = pmul((float)gz, p.voxel);
+  const float D0 = psub(P0, p.t[0]), D1 = psub(P1, p.t[1]), D2 = psub(P2, p.t[2]);
+  const float X0 = pdot3(p.R[0], D0, p.R[3], D1, p.R[6], D2);
+  const float X1 = pdot3(p.R[1], D0, p.R[4], D1, p.R[7], D2);
+  const float X2 = pdot3(p.R[2], D0, p.R[5], D1, p.R[8], D2);
+  if (!(X2 > 0.0f)) return;
+  const float uf = padd(pdiv(pmul(p.fx, X0), X2), p.cx);
+  const float vf = padd(pdiv(pmul(p.fy, X1), X2), p.cy);
+  const float ur = floorf(padd(uf, 0.5f)), vr = floorf(padd(vf, 0.5f));
+  if (!(ur >= 0.0f && ur <= (float)(p.W - 1) && vr >= 0.0f && vr <= (float)(p.H - 1))) return;
+  const size_t pix = (size_t)vr * p.W + (size_t)ur;
+  const float d = pdiv((float)__ldg(&depth[pix]), p.scale);
+  if (!(d >= p.dmin && d <= p.dmax)) return;
+  const float eta = psub(d, X2);
+  if (eta < -p.mu) return;
+  float s = pdiv(eta, p.mu);
+  if (s > 1.0f) s = 1.0f;
+  const uint32_t cw = vx.rgbw;
+  const int w = (int)(cw >> 24);
+  const float wf = (float)w;
+  vx.tsdf = pdiv(padd(pmul(vx.tsdf, wf), s), padd(wf, 1.0f));
+  const uint32_t c = __ldg(&rgba[pix]);
+  const int w1 = w + 1, half = w1 >> 1;
+  uint32_t out = 0;
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) {
+    const int old = (int)((cw >> (8 * ch)) & 0xFFu);
+    const int x8 = (int)((c >> (8 * ch)) & 0xFFu);
+    out |= (uint32_t)((old * w + x8 + half) / w1) << (8 * ch);
+  }
+  out |= (uint32_t)min(w1, p.wmax) << 24;
+  vx.rgbw = out;
+}
+
+__global__ void __launch_bounds__(256) k_integrate(VolumeView v, FuseParams p,
+                                                   const uint16_t* __restrict__ depth,
+                                                   const uint32_t* __restrict__ rgba) {
+  const uint32_t nvis = min(*(volatile uint32_t*)&v.ctr->n_vis, v.max_blocks);
+  if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&v.ctr->vis_total, (unsigned long long)nvis);
+  const int e = 2 * threadIdx.x;  // voxel pair (e, e+1): same j,k; i even
+  const int li = e & 7, lj = (e >> 3) & 7, lk = e >> 6;
+  for (uint32_t q = blockIdx.x; q < nvis; q += gridDim.x) {
+    const int32_t slot = v.vis[q];
+    const int32_t b = v.vals[slot];
+    if (b < 0) continue;
+    int bx, by, bz;
+    unpack_block(v.keys[slot], bx, by, bz);
+    float4* ptr = reinterpret_cast<float4*>(v.pool + (size_t)b * 512 + e);
+    float4 raw = *ptr;
+    Voxel v0{raw.x, __float_as_uint(raw.y)}, v1{raw.z, __float_as_uint(raw.w)};
+    const int gx = bx * 8 + li, gy = by * 8 + lj, gz = bz * 8 + lk;
+    integrate_voxel(p, gx, gy, gz, v0, depth, rgba);
+    integrate_voxel(p, gx + 1, gy, gz, v1, depth, rgba);
+    *ptr = make_float4(v0.tsdf, __uint_as_float(v0.rgbw), v1.tsdf, __uint_as_float(v1.rgbw));
+  }
+}
+
+__global__ void k_reset_frame(VolumeCounters* ctr) { ctr->n_vis = 0u; }
+
+__global__ void k_fill_pool(Voxel* pool, size_t n) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    pool[i].tsdf = 1.0f;
+    pool[i].rgbw = 0u;
+  }
+}
+
+__global__ void k_fill_u64(uint64_t* p, size_t n, uint64_t val) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += stride) p[i] = val;
+}
+
+// ============================================================================================
+// raycast (R-RAY): one thread per pixel, 16x16 CTAs.  Fixed grid t_j = dmin + j*voxel; a sample
+// is valid iff its 8 trilinear corners are allocated with w > 0.  When the base corner's block is
+// unallocated the march jumps to the block's exit (result-preserving).
+// ============================================================================================
+struct RayParams {
+  float fx, fy, cx, cy;
+  int W, H;
+  float R[9], t[3];
+  float voxel, inv_voxel, dmin;
+  int J;  // last grid index
+};
+
+struct BlockCache {
+  int x, y, z;
+  int32_t b;
+};
+
+__device__ __forceinline__ int32_t cached_find(const VolumeView& v, BlockCache& c, int x, int y, int z) {
+  if (x == c.x && y == c.y && z == c.z) return c.b;
+  c.x = x; c.y = y; c.z = z;
+  c.b = find_block(v, x, y, z);
+  return c.b;
+}
+
+// trilinear tsdf (and colour) at voxel-unit position p; returns validity
+template <bool kColor>
+__device__ __forceinline__ bool trilinear(const VolumeView& v, BlockCache& c0, BlockCache& c1, float px,
+                                          float py, float pz, float& f, float* col) {
+  const float fx = floorf(px), fy = floorf(py), fz = floorf(pz);
+  const int gx = (int)fx, gy = (int)fy, gz = (int)fz;
+  const float ax = px - fx, ay = py - fy, az = pz - fz;
+  float acc = 0.f, c[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+  for (int corner = 0; corner < 8; ++corner) {
+    const int dx = corner & 1, dy = (corner >> 1) & 1, dz = (corner >> 2) & 1;
+    const int cx = gx + dx, cy = gy + dy, cz = gz + dz;
+    const int bx = cx >> 3, by = cy >> 3, bz = cz >> 3;
+    const int32_t b = (corner == 0) ? cached_find(v, c0, bx, by, bz)
+                                    : ((bx == c0.x && by == c0.y && bz == c0.z) ? c0.b : cached_find(v, c1, bx, by, bz));
+    if (b < 0) return false;
+    const int idx = (cx & 7) + 8 * (cy & 7) + 64 * (cz & 7);
+    const Voxel vx = v.pool[(size_t)b * 512 + idx];
+    if ((vx.rgbw >> 24) == 0u) return false;
+    const float w = (dx ? ax : 1.f - ax) * (dy ? ay : 1.f - ay) * (dz ? az : 1.f - az);
+    acc = fmaf(w, vx.tsdf, acc);
+    if (kColor) {
+      c[0] = fmaf(w, (float)(vx.rgbw & 0xFFu), c[0]);
+      c[1] = fmaf(w, (float)((vx.rgbw >> 8) & 0xFFu), c[1]);
+      c[2] = fmaf(w, (float)((vx.rgbw >> 16) & 0xFFu), c[2]);
+    }
+  }
+  f = acc;
+  if (kColor) {
+    col[0] = c[0]; col[1] = c[1]; col[2] = c[2];
+  }
+  return true;
+}
+
+__global__ void __launch_bounds__(256) k_raycast(VolumeView v, RayParams p, float* __restrict__ depth_out,
+                                                 float* __restrict__ color_out,
+                                                 float* __restrict__ vertex_out) {
+  const int u = blockIdx.x * 16 + (threadIdx.x & 15);
+  const int vv = blockIdx.y * 16 + (threadIdx.x >> 4);
+  if (u >= p.W || vv >= p.H) return;
+  const float dcx = (u - p.cx) / p.fx, dcy = (vv - p.cy) / p.fy;
+  const float nrm = sqrtf(dcx * dcx + dcy * dcy + 1.0f);
+  const float inv = 1.0f / nrm;
+  const float dhx = dcx * inv, dhy = dcy * inv, dhz = inv;
+  const float rx = p.R[0] * dhx + p.R[1] * dhy + p.R[2] * dhz;
+  const float ry = p.R[3] * dhx + p.R[4] * dhy + p.R[5] * dhz;
+  const float rz = p.R[6] * dhx + p.R[7] * dhy + p.R[8] * dhz;
+  // ray in voxel units: p(t) = o/v + t * r/v
+  const float ox = p.t[0] * p.inv_voxel, oy = p.t[1] * p.inv_voxel, oz = p.t[2] * p.inv_voxel;
+  const float qx = rx * p.inv_voxel, qy = ry * p.inv_voxel, qz = rz * p.inv_voxel;
+  // reciprocal ray components for block exits (in voxel units per metre of t)
+  const float iqx = qx != 0.f ? 1.f / qx : INFINITY;
+  const float iqy = qy != 0.f ? 1.f / qy : INFINITY;
+  const float iqz = qz != 0.f ? 1.f / qz : INFINITY;
+  BlockCache c0{INT_MIN, INT_MIN, INT_MIN, -1}, c1{INT_MIN, INT_MIN, INT_MIN, -1};
+  bool prev_valid = false, hit = false;
+  float prev_f = 0.f, tstar = 0.f;
+  int j = 0;
+  while (j <= p.J) {
+    const float t = p.dmin + (float)j * p.voxel;
+    const float px = fmaf(t, qx, ox), py = fmaf(t, qy, oy), pz = fmaf(t, qz, oz);
+    const int bx = (int)floorf(px) >> 3, by = (int)floorf(py) >> 3, bz = (int)floorf(pz) >> 3;
+    if (cached_find(v, c0, bx, by, bz) < 0) {
+      // skip to the exit of this unallocated block (all its samples are invalid)
+      const float ex = qx != 0.f ? ((qx > 0.f ? (float)(bx + 1) : (float)bx) * 8.f - ox) * iqx : INFINITY;
+      const float ey = qy != 0.f ? ((qy > 0.f ? (float)(by + 1) : (float)by) * 8.f - oy) * iqy : INFINITY;
+      const float ez = qz != 0.f ? ((qz > 0.f ? (float)(bz + 1) : (float)bz) * 8.f - oz) * iqz : INFINITY;
+      const float texit = fminf(ex, fminf(ey, ez));
+      // first grid index at or past the exit, minus a 0.01-step margin against fp32 error
+      const float jn = ceilf((texit - p.dmin) / p.voxel - 0.01f);
+      j = max(j + 1, (jn <= (float)(p.J + 1)) ? (int)jn : p.J + 1);
+      prev_valid = false;
+      continue;
+    }
+    float f;
+    const bool valid = trilinear<false>(v, c0, c1, px, py, pz, f, nullptr);
+    if (j >= 1 && valid && f <= 0.f) {
+      if (prev_valid && prev_f > 0.f) {
+        tstar = (p.dmin + (float)(j - 1) * p.voxel) + p.voxel * prev_f / (prev_f - f);
+        hit = true;
+      }
+      break;
+    }
+    prev_valid = valid;
+    prev_f = f;
+    ++j;
+  }
+  float D = 0.f, col[3] = {0.f, 0.f, 0.f}, V[3] = {0.f, 0.f, 0.f};
+  if (hit) {
+    V[0] = p.t[0] + tstar * rx;
+    V[1] = p.t[1] + tstar * ry;
+    V[2] = p.t[2] + tstar * rz;
+    float fd;
+    if (trilinear<true>(v, c0, c1, V[0] * p.inv_voxel, V[1] * p.inv_voxel, V[2] * p.inv_voxel, fd, col)) {
+      D = tstar * inv;
+      col[0] *= (1.f / 255.f); col[1] *= (1.f / 255.f); col[2] *= (1.f / 255.f);
+    } else {
+      col[0] = col[1] = col[2] = 0.f;
+      V[0] = V[1] = V[2] = 0.f;
+    }
+  }
+  const size_t pix = (size_t)vv * p.W + u;
+  depth_out[pix] = D;
+  color_out[3 * pix + 0] = col[0];
+  color_out[3 * pix + 1] = col[1];
+  color_out[3 * pix + 2] = col[2];
+  if (vertex_out) {
+    vertex_out[3 * pix + 0] = V[0];
+    vertex_out[3 * pix + 1] = V[1];
+    vertex_out[3 * pix + 2] = V[2];
+  }
+}
+
+// ---- debug export ----------------------------------------------------------------------------
+__global__ void k_export_blocks(VolumeView v, int32_t* coords, Voxel* voxels, uint32_t cap,
+                                uint32_t* count) {
+  const uint32_t slots = v.slot_mask + 1;
+  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < slots; s += gridDim.x * blockDim.x) {
+    const uint64_t k = v.keys[s];
+    if (k == kEmptyKey || v.vals[s] < 0) continue;
+    const uint32_t i = atomicAdd(count, 1u);
+    if (i >= cap) continue;
+    int x, y, z;
+    unpack_block(k, x, y, z);
+    coords[3 * i] = x; coords[3 * i + 1] = y; coords[3 * i + 2] = z;
+    if (voxels) {
+      const Voxel* src = v.pool + (size_t)v.vals[s] * 512;
+      for (int e = 0; e < 512; ++e) voxels[(size_t)i * 512 + e] = src[e];
+    }
+  }
+}
+
+__global__ void k_export_visible(VolumeView v, int32_t* coords, uint32_t cap, uint32_t* count) {
+  const uint32_t nvis = min(v.ctr->n_vis, v.max_blocks);
+  for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < nvis; q += gridDim.x * blockDim.x) {
+    const int32_t slot = v.vis[q];
+    if (v.vals[slot] < 0) continue;
+    const uint32_t i = atomicAdd(count, 1u);
+    if (i >= cap) continue;
+    int x, y, z;
+    unpack_block(v.keys[slot], x, y, z);
+    coords[3 * i] = x; coords[3 * i + 1] = y; coords[3 * i + 2] = z;
+  }
+}
+
+// host-mapped sticky overflow flags, one per volume (index by the volume's flag pointer)
+struct HostFlag {
+  uint32_t* host;
+  uint32_t* dev;
+};
+
+}  // namespace gps
+
+using namespace gps;
+
+namespace {
+// the flag lives right after the public struct
+struct VolumeImpl : gps_volume {
+  HostFlag flag;
+};
+
+gps_status check_sticky(const gps_volume* vol) {
+  const VolumeImpl* v = static_cast<const VolumeImpl*>(vol);
+  if (*(volatile uint32_t*)v->flag.host) {
+    set_error("volume block budget / hash table exceeded by an earlier gps_fuse");
+    return GPS_ERR_OUT_OF_BLOCKS;
+  }
+  return GPS_OK;
+}
+
+gps_status fill_volume(VolumeImpl* v, cudaStream_t s) {
+  const gps_volume_config& c = v->cfg;
+  k_fill_u64<<<592, 256, 0, s>>>(v->view.keys, (size_t)c.hash_slots, kEmptyKey);
+  GPS_CHECK_LAUNCH("k_fill_u64");
+  GPS_CHECK_CUDA(cudaMemsetAsync(v->view.vals, 0xFF, sizeof(int32_t) * c.hash_slots, s));
+  GPS_CHECK_CUDA(cudaMemsetAsync(v->view.stamp, 0xFF, sizeof(uint32_t) * c.hash_slots, s));
+  k_fill_pool<<<1184, 256, 0, s>>>(v->view.pool, (size_t)c.max_blocks * 512);
+  GPS_CHECK_LAUNCH("k_fill_pool");
+  GPS_CHECK_CUDA(cudaMemsetAsync(v->view.ctr, 0, sizeof(VolumeCounters), s));
+  *(volatile uint32_t*)v->flag.host = 0u;
+  v->frame = 0;
+  return GPS_OK;
+}
+
+bool valid_intrinsics(const gps_intrinsics* K) {
+  return K && K->width > 0 && K->height > 0 && K->fx > 0 && K->fy > 0 && std::isfinite(K->cx) &&
+         std::isfinite(K->cy) && K->width <= 65535 && K->height <= 65535;
+}
+}  // namespace
+
+extern "C" {
+
+gps_status gps_volume_create(const gps_volume_config* cfg, gps_stream_t stream, gps_volume** out) {
+  if (!cfg || !out) return invalid("gps_volume_create: null argument");
+  *out = nullptr;
+  if (!(cfg->voxel_size > 0) || !(cfg->mu > 0) || cfg->w_max < 1 || cfg->w_max > 255 ||
+      !(cfg->depth_min >= 0) || !(cfg->depth_max > cfg->depth_min) || cfg->max_blocks < 1 ||
+      cfg->max_blocks > (1ll << 30) || cfg->hash_slots < 2 || (cfg->hash_slots & (cfg->hash_slots - 1)) ||
+      cfg->hash_slots > (1ll << 31))
+    return invalid("gps_volume_create: bad config (voxel_size, mu > 0; 1 <= w_max <= 255; "
+                   "depth_max > depth_min; hash_slots a power of two)");
+  VolumeImpl* v = new VolumeImpl();
+  v->cfg = *cfg;
+  cudaGetDevice(&v->device);
+  const size_t slots = (size_t)cfg->hash_slots, nb = (size_t)cfg->max_blocks;
+  bool ok = cudaMalloc(&v->view.keys, sizeof(uint64_t) * slots) == cudaSuccess &&
+            cudaMalloc(&v->view.vals, sizeof(int32_t) * slots) == cudaSuccess &&
+            cudaMalloc(&v->view.stamp, sizeof(uint32_t) * slots) == cudaSuccess &&
+            cudaMalloc(&v->view.pool, sizeof(Voxel) * 512 * nb) == cudaSuccess &&
+            cudaMalloc(&v->view.vis, sizeof(int32_t) * nb) == cudaSuccess &&
+            cudaMalloc(&v->view.ctr, sizeof(VolumeCounters)) == cudaSuccess &&
+            cudaHostAlloc(&v->flag.host, sizeof(uint32_t), cudaHostAllocMapped) == cudaSuccess &&
+            cudaHostGetDevicePointer(&v->flag.dev, v->flag.host, 0) == cudaSuccess;
+  if (!ok) {
+    cudaGetLastError();
+    set_error("gps_volume_create: out of device memory");
+    gps_volume_destroy(v);
+    return GPS_ERR_OOM;
+  }
+  v->view.slot_mask = (uint32_t)(slots - 1);
+  v->view.max_blocks = (uint32_t)nb;
+  gps_status st = fill_volume(v, as_stream(stream));
+  if (st != GPS_OK) {
+    gps_volume_destroy(v);
+    return st;
+  }
+  *out = v;
+  return GPS_OK;
+}
+
+void gps_volume_destroy(gps_volume* vol) {
+  if (!vol) return;
+  VolumeImpl* v = static_cast<VolumeImpl*>(vol);
+  cudaFree(v->view.keys);
+  cudaFree(v->view.vals);
+  cudaFree(v->view.stamp);
+  cudaFree(v->view.pool);
+  cudaFree(v->view.vis);
+  cudaFree(v->view.ctr);
+  if (v->flag.host) cudaFreeHost(v->flag.host);
+  delete v;
+}
+
+gps_status gps_volume_reset(gps_volume* vol, gps_stream_t stream) {
+  if (!vol) return invalid("gps_volume_reset: null volume");
+  return fill_volume(static_cast<VolumeImpl*>(vol), as_stream(stream));
+}
+
+gps_status gps_volume_stats_sync(gps_volume* vol, gps_stream_t stream, int64_t* n_blocks, int64_t* budget,
+                                 int64_t* n_visible, int64_t* visible_total) {
+  if (!vol) return invalid("gps_volume_stats_sync: null volume");
+  VolumeImpl* v = static_cast<VolumeImpl*>(vol);
+  VolumeCounters c;
+  GPS_CHECK_CUDA(cudaMemcpyAsync(&c, v->view.ctr, sizeof(c), cudaMemcpyDeviceToHost, as_stream(stream)));
+  GPS_CHECK_CUDA(cudaStreamSynchronize(as_stream(stream)));
+  if (n_blocks) *n_blocks = c.n_blocks;
+  if (budget) *budget = v->cfg.max_blocks;
+  if (n_visible) *n_visible = std::min<int64_t>(c.n_vis, v->cfg.max_blocks);
+  if (visible_total) *visible_total = (int64_t)c.vis_total;
+  if (c.overflow || *(volatile uint32_t*)v->flag.host) {
+    set_error("volume block budget exceeded: budget " + std::to_string(v->cfg.max_blocks));
+    return GPS_ERR_OUT_OF_BLOCKS;
+  }
+  return GPS_OK;
+}
+
+gps_status gps_fuse(gps_volume* vol, const gps_intrinsics* K, const gps_pose* T, const uint16_t* depth,
+                    float depth_scale, const uint8_t* rgba, gps_stream_t stream) {
+  if (!vol || !T || !depth || !rgba) return invalid("gps_fuse: null argument");
+  if (!valid_intrinsics(K)) return invalid("gps_fuse: bad intrinsics");
+  if (!(depth_scale > 0)) return invalid("gps_fuse: depth_scale must be > 0");
+  if ((reinterpret_cast<uintptr_t>(rgba) & 3u) != 0) return invalid("gps_fuse: rgba must be 4-byte aligned");
+  if ((reinterpret_cast<uintptr_t>(depth) & 1u) != 0) return invalid("gps_fuse: depth must be 2-byte aligned");
+  gps_status st = check_sticky(vol);
+  if (st != GPS_OK) return st;
+  VolumeImpl* v = static_cast<VolumeImpl*>(vol);
+  cudaStream_t s = as_stream(stream);
+  FuseParams p;
+  p.fx = K->fx; p.fy = K->fy; p.cx = K->cx; p.cy = K->cy; p.W = K->width; p.H = K->height;
+  for (int i = 0; i < 9; ++i) p.R[i] = T->R[i];
+  for (int i = 0; i < 3; ++i) p.t[i] = T->t[i];
+  p.scale = depth_scale;
+  p.mu = v->cfg.mu;
+  p.voxel = v->cfg.voxel_size;
+  p.bs = 8.0f * v->cfg.voxel_size;
+  p.dmin = v->cfg.depth_min;
+  p.dmax = v->cfg.depth_max;
+  p.wmax = v->cfg.w_max;
+  const uint32_t frame = v->frame++;
+  k_reset_frame<<<1, 1, 0, s>>>(v->view.ctr);
+  GPS_CHECK_LAUNCH("k_reset_frame");
+  dim3 ga((p.W + kAllocPatch - 1) / kAllocPatch, (p.H + kAllocPatch - 1) / kAllocPatch);
+  {
+    GPS_PROF(K_ALLOC, s);
+    k_alloc<<<ga, 256, 0, s>>>(v->view, p, depth, frame, v->flag.dev);
+  }
+  GPS_CHECK_LAUNCH("k_alloc");
+  // persistent-style grid: 148 SMs x 8 resident 256-thread CTAs, striding over the visible list
+  {
+    GPS_PROF(K_INTEGRATE, s);
+    k_integrate<<<148 * 8, 256, 0, s>>>(v->view, p, depth, reinterpret_cast<const uint32_t*>(rgba));
+  }
+  GPS_CHECK_LAUNCH("k_integrate");
+  return GPS_OK;
+}
+
+gps_status gps_raycast(const gps_volume* vol, const gps_intrinsics* K, const gps_pose* T, float* depth_out,
+                       float* color_out, float* vertex_out, gps_stream_t stream) {
+  if (!vol || !T || !depth_out || !color_out) return invalid("gps_raycast: null argument");
+  if (!valid_intrinsics(K)) return invalid("gps_raycast: bad intrinsics");
+  gps_status st = check_sticky(vol);
+  if (st != GPS_OK) return st;
+  const VolumeImpl* v = static_cast<const VolumeImpl*>(vol);
+  RayParams p;
+  p.fx = K->fx; p.fy = K->fy; p.cx = K->cx; p.cy = K->cy; p.W = K->width; p.H = K->height;
+  for (int i = 0; i < 9; ++i) p.R[i] = T->R[i];
+  for (int i = 0; i < 3; ++i) p.t[i] = T->t[i];
+  p.voxel = v->cfg.voxel_size;
+  p.inv_voxel = 1.0f / v->cfg.voxel_size;
+  p.dmin = v->cfg.depth_min;
+  p.J = (int)std::floor(((double)v->cfg.depth_max - (double)v->cfg.depth_min) / (double)v->cfg.voxel_size);
+  dim3 g((p.W + 15) / 16, (p.H + 15) / 16);
+  {
+    GPS_PROF(K_RAYCAST, as_stream(stream));
+    k_raycast<<<g, 256, 0, as_stream(stream)>>>(v->view, p, depth_out, color_out, vertex_out);
+  }
+  GPS_CHECK_LAUNCH("k_raycast");
+  return GPS_OK;
+}
+
+gps_status gps_debug_export_blocks_sync(const gps_volume* vol, gps_stream_t stream, int32_t* coords, void* voxels,
+                                        int64_t cap, int64_t* n) {
+  if (!vol || !coords || !n || cap < 0) return invalid("gps_debug_export_blocks_sync: bad argument");
+  const VolumeImpl* v = static_cast<const VolumeImpl*>(vol);
+  cudaStream_t s = as_stream(stream);
+  uint32_t* cnt = nullptr;
+  GPS_CHECK_CUDA(cudaMallocAsync(&cnt, sizeof(uint32_t), s));
+  GPS_CHECK_CUDA(cudaMemsetAsync(cnt, 0, sizeof(uint32_t), s));
+  k_export_blocks<<<256, 256, 0, s>>>(v->view, coords, reinterpret_cast<Voxel*>(voxels),
+                                      (uint32_t)std::min<int64_t>(cap, 0xFFFFFFFFll), cnt);
+  GPS_CHECK_LAUNCH("k_export_blocks");
+  uint32_t h = 0;
+  GPS_CHECK_CUDA(cudaMemcpyAsync(&h, cnt, sizeof(h), cudaMemcpyDeviceToHost, s));
+  GPS_CHECK_CUDA(cudaFreeAsync(cnt, s));
+  GPS_CHECK_CUDA(cudaStreamSynchronize(s));
+  *n = h;
+  return GPS_OK;
+}
+
+gps_status gps_debug_export_visible_sync(const gps_volume* vol, gps_stream_t stream, int32_t* coords, int64_t cap,
+                                         int64_t* n) {
+  if (!vol || !coords || !n || cap < 0) return invalid("gps_debug_export_visible_sync: bad argument");
+  const VolumeImpl* v = static_cast<const VolumeImpl*>(vol);
+  cudaStream_t s = as_stream(stream);
+  uint32_t* cnt = nullptr;
+  GPS_CHECK_CUDA(cudaMallocAsync(&cnt, sizeof(uint32_t), s));
+  GPS_CHECK_CUDA(cudaMemsetAsync(cnt, 0, sizeof(uint32_t), s));
+  k_export_visible<<<256, 256, 0, s>>>(v->view, coords, (uint32_t)std::min<int64_t>(cap, 0xFFFFFFFFll), cnt);
+  GPS_CHECK_LAUNCH("k_export_visible");
+  uint32_t h = 0;
+  GPS_CHECK_CUDA(cudaMemcpyAsync(&h, cnt, sizeof(h), cudaMemcpyDeviceToHost, s));
+  GPS_CHECK_CUDA(cudaFreeAsync(cnt, s));
+  GPS_CHECK_CUDA(cudaStreamSynchronize(s));
+  *n = h;
+  return GPS_OK;
+}
+
+}  // extern "C"

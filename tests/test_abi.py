@@ -1,0 +1,41 @@
+"""CPU checks of the boundary: libgps.so (built for sm_100a) loads without a GPU, exports every
+function include/gps.h declares, and its binding declares the same set.  No compute calls."""
+import ctypes
+import subprocess
+
+import pytest
+
+from paper_2509_11574_b200 import _native as N
+
+
+def test_header_declares_the_four_hot_calls():
+    syms = N.declared_symbols()
+    for s in ("gps_fuse", "gps_raycast", "gps_render", "gps_refine_step"):
+        assert s in syms
+
+
+def test_library_exports_every_declared_symbol():
+    lib = N.load()
+    for s in N.declared_symbols():
+        assert hasattr(lib, s), s
+    assert set(N.PROTOTYPES) == set(N.declared_symbols())
+    assert lib.gps_abi_version() == 1
+    assert lib.gps_status_string(2) == b"GPS_ERR_OUT_OF_BLOCKS"
+
+
+def test_library_is_sm100a_code():
+    out = subprocess.run(["cuobjdump", "--list-elf", N.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_argument_validation_is_synchronous_and_needs_no_gpu():
+    lib = N.load()
+    cfg = N.gps_volume_config(0.005, 0.02, 300, 0.1, 10.0, 16, 1000)  # w_max > 255, slots not 2^k
+    h = ctypes.c_void_p()
+    assert lib.gps_volume_create(ctypes.byref(cfg), None, ctypes.byref(h)) == 1
+    assert b"bad config" in lib.gps_last_error()
+    rc = N.gps_render_config(0.02, 1 / 255, 0.2, 0.3, 12, 0, 0)  # tile must be 8 or 16
+    K = N.gps_intrinsics(60, 60, 31.5, 23.5, 64, 48)
+    assert lib.gps_render_workspace_size(10, ctypes.byref(K), ctypes.byref(rc)) == 0
+    rc.tile = 16
+    assert lib.gps_render_workspace_size(10, ctypes.byref(K), ctypes.byref(rc)) > 0

@@ -1,0 +1,213 @@
+"""GPU parity of gps_render / gps_refine_step / gps_adam_step against the CPU oracle
+(SURVEY §8(c) O5-O10).  Inputs are seeded (gps_synth): analytic-scene D_t/C_t stand-ins, so the
+render stage is compared without consuming any CUDA output.
+
+Bars: tile lists bit-exact (both sides bin the prescribed-fp32 projection fields);
+C* within 1e-3 absolute and W_G within 1e-3 relative on unambiguous pixels; loss within 1e-5
+relative; raw-parameter gradients within 1e-3 relative with the floor tau = 1e-3 max|g| per block
+(Gaussians touching an ambiguous decision excluded and counted); Adam within 1e-6 relative on
+identical gradients.  PAPER.md Eqs. 1-4, Eq. 7."""
+import numpy as np
+import pytest
+import torch
+
+import gps_synth as S
+import oracle as O
+from tests import gpu_helpers as H
+
+pytestmark = pytest.mark.gpu
+
+GROUPS = ("xyz", "log_scale", "rot", "opacity_raw", "sh")
+
+
+def setup(cfg_name="cfg1", start=0, n=None):
+    import paper_2509_11574_b200 as G
+    cfg = S.get_config(cfg_name)
+    fr = H.frames(cfg, 1, start=start)[0]
+    gd = S.make_gaussians(cfg, n=n, frames=[fr] if cfg_name == "cfg1" else None)
+    Dt, Ct = S.sdf_stage_inputs(cfg, fr, seed=start)
+    tgt = S.target_rgba(cfg, fr)
+    gcam, ocam = H.cams(cfg)
+    dev = dict(Dt=torch.from_numpy(Dt).cuda(), Ct=torch.from_numpy(Ct).cuda(), tgt=tgt.cuda().contiguous())
+    return G, cfg, fr, gd, Dt, Ct, tgt.numpy(), gcam, ocam, dev
+
+
+def gpu_render(G, gd, gcam, fr, dev, tile=16, precull=0, target=True):
+    g = G.Gaussians.from_dict(gd)
+    ras = G.Rasterizer(g.n, gcam, G.RenderConfig(tile=tile, tile_depth_precull=precull))
+    Cs, W, loss = ras.render(g, gcam, fr.R, fr.t, dev["Dt"], dev["Ct"], dev["tgt"] if target else None)
+    torch.cuda.synchronize()
+    return ras, Cs.cpu().numpy(), W.cpu().numpy(), (loss.item() if loss is not None else None)
+
+
+def check_forward(out, Cs, W, max_amb_frac):
+    ok = ~out["amb"]
+    assert (~ok).mean() <= max_amb_frac, f"{(~ok).sum()} ambiguous pixels"
+    assert np.max(np.abs(Cs[ok] - out["Cstar"][ok])) <= 1e-3
+    assert np.all(np.abs(W[ok] - out["WG"][ok]) <= 1e-3 * out["WG"][ok] + 1e-6)
+    assert out["WG"].max() > 0.5
+
+
+@pytest.mark.parametrize("tile", [16, 8])
+def test_render_cfg1_matches_oracle_and_lists_bit_exact(tile):
+    G, cfg, fr, gd, Dt, Ct, tgt, gcam, ocam, dev = setup()
+    ras, Cs, W, loss = gpu_render(G, gd, gcam, fr, dev, tile=tile, precull=0)
+    out = O.render(gd, ocam, fr.R, fr.t, Dt, Ct)
+    check_forward(out, Cs, W, 0.02)
+    ol, _, cnt, _ = O.l1_loss(out["Cstar"], out["WG"], Dt, tgt)
+    assert abs(loss - ol) <= 1e-5 * ol
+    # tile lists: bit-exact against the oracle's binning of its own P32 projection
+    rect, depth, culled = O.project_p32(gd, ocam, fr.R, fr.t, O.RenderCfg())
+    ov, orng = O.tile_lists(rect, depth, culled, cfg.width, cfg.height, tile)
+    gv, grng = ras.lists()
+    assert np.array_equal(grng, orng)
+    assert np.array_equal(gv, ov)
+    st = ras.stats()
+    assert st["pairs"] == len(ov) and st["n_visible"] == int((culled == 0).sum()) and st["status"] == "GPS_OK"
+
+
+def test_precull_and_early_exit_do_not_change_the_image():
+    """Early termination at the SDF depth and the tile pre-cull skip only entries that add exact
+    zeros (lists are depth-sorted), so the image is bitwise unchanged; the
+    truncated lists are prefixes of the full ones.  Rendering is deterministic."""
+    G, cfg, fr, gd, Dt, Ct, tgt, gcam, ocam, dev = setup()
+    ras0, C0, W0, l0 = gpu_render(G, gd, gcam, fr, dev, precull=0)
+    v0, r0 = ras0.lists()
+    ras1, C1, W1, l1 = gpu_render(G, gd, gcam, fr, dev, precull=1)
+    v1, r1 = ras1.lists()
+    assert np.array_equal(C0, C1) and np.array_equal(W0, W1) and l0 == l1
+    assert np.array_equal(r0[:, 0], r1[:, 0]) and np.all(r1[:, 1] <= r0[:, 1])
+    for t in range(len(r0)):
+        assert np.array_equal(v1[r1[t, 0]:r1[t, 1]], v0[r0[t, 0]:r0[t, 0] + (r1[t, 1] - r1[t, 0])])
+    _, C2, W2, l2 = gpu_render(G, gd, gcam, fr, dev, precull=1)
+    assert np.array_equal(C1, C2) and np.array_equal(W1, W2) and l1 == l2
+
+
+def test_zero_gaussians_compose_identity():
+    """AC1: with no Gaussians C* = C_t bitwise and W_G = 0."""
+    G, cfg, fr, gd, Dt, Ct, tgt, gcam, ocam, dev = setup()
+    g0 = {k: (v[:0] if isinstance(v, np.ndarray) else v) for k, v in gd.items()}
+    _, Cs, W, _ = gpu_render(G, g0, gcam, fr, dev)
+    assert np.array_equal(Cs, Ct) and np.all(W == 0)
+
+
+@pytest.mark.slow
+def test_render_full_size_cfg4():
+    G, cfg, fr, gd, Dt, Ct, tgt, gcam, ocam, dev = setup("cfg4", start=300)
+    ras, Cs, W, loss = gpu_render(G, gd, gcam, fr, dev, precull=1)
+    out = O.render(gd, ocam, fr.R, fr.t, Dt, Ct)
+    check_forward(out, Cs, W, 1e-3)
+    ol = O.l1_loss(out["Cstar"], out["WG"], Dt, tgt)[0]
+    assert abs(loss - ol) <= 1e-5 * ol
+
+
+# ---------------------------------------------------------------------------------------------
+def oracle_grads(gd, ocam, R, t, Dt, Ct, tgt):
+    out = O.render(gd, ocam, R, t, Dt, Ct)
+    loss, G, cnt, samb = O.l1_loss(out["Cstar"], out["WG"], Dt, tgt)
+    grads, gamb = O.backward(gd, ocam, R, t, Dt, out["Cstar"], out["WG"], G, pix_amb=out["amb"] | samb)
+    return loss, grads, gamb
+
+
+def compare_grads(gg, ref, gamb, min_checked=50):
+    keep = ~gamb
+    assert keep.sum() >= min_checked
+    for k in GROUPS:
+        a = gg[k].reshape(len(keep), -1)[keep]
+        b = ref[k].reshape(len(keep), -1)[keep]
+        tau = 1e-3 * np.max(np.abs(b))
+        assert tau > 0, k
+        err = np.abs(a - b) / np.maximum(np.abs(b), tau)
+        assert err.max() <= 1e-3, (k, float(err.max()))
+
+
+def test_refine_gradients_and_adam_cfg1():
+    G, cfg, fr, gd, Dt, Ct, tgt, gcam, ocam, dev = setup()
+    g = G.Gaussians.from_dict(gd)
+    p0 = g.to_numpy()
+    st = G.AdamState(g)
+    gout = g.zeros_like()
+    ras = G.Rasterizer(g.n, gcam, G.RenderConfig())
+    view = G.View(gcam, fr.R, fr.t, dev["Dt"], dev["Ct"], dev["tgt"])
+    loss = ras.refine_step(g, st, [view], grad_out=gout).item()
+    assert st.step == 1
+    oloss, ref, gamb = oracle_grads(gd, ocam, fr.R, fr.t, Dt, Ct, tgt)
+    assert abs(loss - oloss) <= 1e-5 * oloss
+    gg = gout.to_numpy()
+    compare_grads(gg, ref, gamb)
+    # Adam step 1: p1 = p0 - lr g/(|g| + eps): equal to the oracle's update of the oracle gradient
+    # wherever |g| is above the per-block floor (sign-like below it: may differ by 2 lr)
+    m0 = {k: np.zeros_like(np.asarray(p0[k], np.float64)) for k in GROUPS}
+    P1, _, _ = O.adam_step(p0, m0, m0, ref, 0)
+    p1 = g.to_numpy()
+    for k in GROUPS:
+        b = ref[k].reshape(len(gamb), -1)
+        sel = (np.abs(b) > 1e-2 * np.max(np.abs(b))) & ~gamb[:, None]
+        a1 = p1[k].reshape(len(gamb), -1)[sel]
+        e1 = P1[k].reshape(len(gamb), -1)[sel]
+        assert np.max(np.abs(a1 - e1)) <= 1e-6 * np.max(np.abs(e1)) + 1e-7, k
+
+
+def test_adam_step_identical_gradients():
+    """O10: given identical gradients the device Adam equals the oracle's (3 steps)."""
+    import paper_2509_11574_b200 as G
+    rng = np.random.default_rng(3)
+    gd = S.random_gaussians(777, 3, rng)
+    g = G.Gaussians.from_dict(gd)
+    st = G.AdamState(g)
+    P = {k: np.asarray(gd[k], np.float64) for k in GROUPS}
+    M = {k: np.zeros_like(v) for k, v in P.items()}
+    V = {k: np.zeros_like(v) for k, v in P.items()}
+    for step in range(3):
+        gr = {k: (rng.normal(size=np.shape(gd[k])) * 10.0 ** rng.uniform(-6, 0)).astype(np.float32) for k in GROUPS}
+        G.adam_step(g, st, G.Gaussians.from_dict({**gr, "sh_degree": 3}))
+        P, M, V = O.adam_step(P, M, V, {k: np.asarray(v, np.float64) for k, v in gr.items()}, step)
+    torch.cuda.synchronize()
+    got = g.to_numpy()
+    for k in GROUPS:
+        err = np.abs(got[k] - P[k]) / np.maximum(np.abs(P[k]), 1e-3)
+        assert err.max() <= 1e-6, (k, err.max())
+    assert st.step == 3
+
+
+def test_refine_two_views_sums_gradients():
+    """n_views = 2 (SPEC's all-views variant): gradients and losses of the views add."""
+    G, cfg, fr, gd, Dt, Ct, tgt, gcam, ocam, dev = setup()
+    R2 = np.asarray(fr.R, np.float32)
+    t2 = (np.asarray(fr.t) + np.array([0.004, -0.003, 0.0])).astype(np.float32)
+    g = G.Gaussians.from_dict(gd)
+    st = G.AdamState(g)
+    gout = g.zeros_like()
+    ras = G.Rasterizer(g.n, gcam, G.RenderConfig(), n_views=2)
+    views = [G.View(gcam, fr.R, fr.t, dev["Dt"], dev["Ct"], dev["tgt"]),
+             G.View(gcam, R2, t2, dev["Dt"], dev["Ct"], dev["tgt"])]
+    loss = ras.refine_step(g, st, views, grad_out=gout).item()
+    l1, r1, a1 = oracle_grads(gd, ocam, fr.R, fr.t, Dt, Ct, tgt)
+    l2, r2, a2 = oracle_grads(gd, ocam, R2, t2, Dt, Ct, tgt)
+    assert abs(loss - (l1 + l2)) <= 1e-5 * (l1 + l2)
+    compare_grads(gout.to_numpy(), {k: r1[k] + r2[k] for k in GROUPS}, a1 | a2)
+
+
+def test_refinement_reduces_the_loss():
+    """20 iterations on one view lower the L1 loss (SPEC S:336 monotone toy fit)."""
+    G, cfg, fr, gd, Dt, Ct, tgt, gcam, ocam, dev = setup()
+    g = G.Gaussians.from_dict(gd)
+    st = G.AdamState(g)
+    ras = G.Rasterizer(g.n, gcam, G.RenderConfig())
+    view = G.View(gcam, fr.R, fr.t, dev["Dt"], dev["Ct"], dev["tgt"])
+    losses = [ras.refine_step(g, st, [view]).item() for _ in range(20)]
+    assert losses[-1] < losses[0] * 0.98
+
+
+@pytest.mark.slow
+def test_refine_gradients_full_size_cfg4():
+    G, cfg, fr, gd, Dt, Ct, tgt, gcam, ocam, dev = setup("cfg4", start=300)
+    g = G.Gaussians.from_dict(gd)
+    st = G.AdamState(g)
+    gout = g.zeros_like()
+    ras = G.Rasterizer(g.n, gcam, G.RenderConfig())
+    view = G.View(gcam, fr.R, fr.t, dev["Dt"], dev["Ct"], dev["tgt"])
+    loss = ras.refine_step(g, st, [view], grad_out=gout).item()
+    oloss, ref, gamb = oracle_grads(gd, ocam, fr.R, fr.t, Dt, Ct, tgt)
+    assert abs(loss - oloss) <= 1e-5 * oloss
+    compare_grads(gout.to_numpy(), ref, gamb, min_checked=10000)
