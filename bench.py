@@ -123,7 +123,7 @@ def run_ours(args):
     if ws > 1:  # config 5: an independent sequence (different room and path) per GPU
         cfg = S.get_config(args.config, seed=40 + rank)
     dk = 10
-    n_frames = args.history + dk * (args.warmup + args.steps)
+    n_frames = args.history + dk * (args.warmup + args.steps + 1)  # +1 step: alignment slack
     if not args.no_e2e:
         n_frames += dk * args.steps
     t0 = time.time()

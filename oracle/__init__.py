@@ -62,6 +62,7 @@ def lib():
         L.orc_fuse.argtypes = [vp, vp, i32, i32, vp, vp, vp, f32, vp]
         L.orc_raycast.argtypes = [vp, vp, i32, i32, vp, vp, vp, i64, vp, vp, vp, vp]
         L.orc_project_p32.argtypes = [i64, vp, vp, vp, vp, i32, i32, vp, vp, f32, f32, vp, vp, vp]
+        L.orc_project_p32_full.argtypes = [i64, vp, vp, vp, vp, vp, i32, i32, vp, vp, f32, f32, vp, vp, vp, vp]
         L.orc_sh_basis.argtypes = [f64, f64, f64, vp, vp]
         L.orc_render.argtypes = [i64, i32, vp, vp, vp, vp, vp, vp, i32, i32, vp, vp,
                                  f64, f64, f64, f64, vp, vp, vp, vp, vp, vp]
@@ -189,17 +190,22 @@ def n_coeffs(deg: int) -> int:
     return (deg + 1) ** 2
 
 
-def project_p32(g: dict, cam: Camera, R, t, cfg: RenderCfg):
+def project_p32(g: dict, cam: Camera, R, t, cfg: RenderCfg, fields: bool = False):
     """P32 projection fields: rect i32[n,4] (x0,y0,x1,y1 inclusive), depth
-    f32[n] (camera z) and culled i32[n]."""
+    f32[n] (camera z) and culled i32[n]; with fields=True also f32[n,6] (px, py, conic a, b, c,
+    ln sigma)."""
     n = int(g["xyz"].shape[0])
     rect = np.zeros((n, 4), np.int32)
     depth = np.zeros(n, np.float32)
     culled = np.zeros(n, np.int32)
-    lib().orc_project_p32(n, _p(_f32(g["xyz"])), _p(_f32(g["log_scale"])), _p(_f32(g["rot"])),
-                          _p(cam.k4_f32()), cam.width, cam.height, _p(_f32(R).reshape(9)),
-                          _p(_f32(t).reshape(3)), float(np.float32(cfg.near_z)),
-                          float(np.float32(cfg.lowpass)), _p(rect), _p(depth), _p(culled))
+    fl = np.zeros((n, 6), np.float32)
+    lib().orc_project_p32_full(n, _p(_f32(g["xyz"])), _p(_f32(g["log_scale"])), _p(_f32(g["rot"])),
+                               _p(_f32(g["opacity_raw"]).reshape(n)),
+                               _p(cam.k4_f32()), cam.width, cam.height, _p(_f32(R).reshape(9)),
+                               _p(_f32(t).reshape(3)), float(np.float32(cfg.near_z)),
+                               float(np.float32(cfg.lowpass)), _p(rect), _p(depth), _p(culled), _p(fl))
+    if fields:
+        return rect, depth, culled, fl
     return rect, depth, culled
 
 

@@ -393,118 +393,172 @@ void orc_raycast(const orc_volume* v, const float* K4, int W, int H, const float
 /* Gaussians                                                                                */
 /* ======================================================================================= */
 
-/* ---- P32 projection fields that decide tile membership and sort keys ---
- * Follows 3DGS's EWA projection ("following 3DGS", P:89 Sigma_2D) in the prescribed fp32
- * evaluation order.  Outputs per Gaussian: rect (x0,y0,x1,y1) inclusive pixel bounds clipped to
- * the image, depth d = camera z, culled flag.  exp is evaluated as (float)exp((double)x).  */
-void orc_project_p32(int64_t n, const float* xyz, const float* ls, const float* rot,
-                     const float* K4, int W, int H, const float* R, const float* t, float near_z,
-                     float lowpass, int32_t* rect, float* depth, int32_t* culled) {
+/* ---- P32 projection fields that decide tile membership, sort keys and pair membership ----
+ * (DESIGN.md §4.3).  Follows 3DGS's EWA projection ("following 3DGS", P:89 Sigma_2D) in
+ * the prescribed fp32 evaluation order.  exp/log are evaluated in double and rounded once.
+ * Per Gaussian: culled flag, depth d = camera z, p_hat, conic (a, b, c), ln(sigma), and the
+ * inclusive pixel rect of the 3-sigma ellipse clipped to the image.                          */
+typedef struct {
+  int culled;
+  float d, px, py, a, b, c, lnsig;
+  int32_t rect[4];
+} p32;
+
+static void proj32(const float* p, const float* ls, const float* q, float o, const float* K4, int W,
+                   int H, const float* R, const float* t, float near_z, float lowpass, p32* g) {
   float fx = K4[0], fy = K4[1], cx = K4[2], cy = K4[3];
   float tanx = (float)W / (2.0f * fx), tany = (float)H / (2.0f * fy);
   float limx = 1.3f * tanx, limy = 1.3f * tany;
-  for (int64_t i = 0; i < n; ++i) {
-    culled[i] = 1;
-    depth[i] = 0.0f;
-    rect[4 * i] = rect[4 * i + 1] = 0;
-    rect[4 * i + 2] = rect[4 * i + 3] = -1;
-    float D[3], X[3];
-    for (int c = 0; c < 3; ++c) D[c] = xyz[3 * i + c] - t[c];
-    for (int c = 0; c < 3; ++c) {
-      float acc = R[0 * 3 + c] * D[0];
-      float p1 = R[1 * 3 + c] * D[1];
-      acc = acc + p1;
-      float p2 = R[2 * 3 + c] * D[2];
-      X[c] = acc + p2;
-    }
-    depth[i] = X[2];
-    if (!(X[2] > near_z)) continue;
-    float s[3];
-    for (int c = 0; c < 3; ++c) s[c] = (float)exp((double)ls[3 * i + c]);
-    float qw = rot[4 * i], qx = rot[4 * i + 1], qy = rot[4 * i + 2], qz = rot[4 * i + 3];
-    float qn2 = qw * qw + qx * qx;
-    qn2 = qn2 + qy * qy;
-    qn2 = qn2 + qz * qz;
-    float qn = sqrtf(qn2);
-    float w = qw / qn, x = qx / qn, y = qy / qn, z = qz / qn;
-    float Rq[9];
-    Rq[0] = 1.0f - 2.0f * (y * y + z * z);
-    Rq[1] = 2.0f * (x * y - w * z);
-    Rq[2] = 2.0f * (x * z + w * y);
-    Rq[3] = 2.0f * (x * y + w * z);
-    Rq[4] = 1.0f - 2.0f * (x * x + z * z);
-    Rq[5] = 2.0f * (y * z - w * x);
-    Rq[6] = 2.0f * (x * z - w * y);
-    Rq[7] = 2.0f * (y * z + w * x);
-    Rq[8] = 1.0f - 2.0f * (x * x + y * y);
-    float M[9];
-    for (int r = 0; r < 3; ++r)
-      for (int c = 0; c < 3; ++c) M[3 * r + c] = Rq[3 * r + c] * s[c];
-    float S[9];
-    for (int r = 0; r < 3; ++r)
-      for (int c = 0; c < 3; ++c) {
-        float acc = M[3 * r + 0] * M[3 * c + 0];
-        float p1 = M[3 * r + 1] * M[3 * c + 1];
-        acc = acc + p1;
-        float p2 = M[3 * r + 2] * M[3 * c + 2];
-        S[3 * r + c] = acc + p2;
-      }
-    float txz = X[0] / X[2], tyz = X[1] / X[2];
-    float cu = txz < -limx ? -limx : (txz > limx ? limx : txz);
-    float cv = tyz < -limy ? -limy : (tyz > limy ? limy : tyz);
-    float tx = cu * X[2], ty = cv * X[2];
-    float z2 = X[2] * X[2];
-    float J00 = fx / X[2];
-    float J02 = -(fx * tx) / z2;
-    float J11 = fy / X[2];
-    float J12 = -(fy * ty) / z2;
-    /* T = J * Wc, Wc = R^T (world->camera rotation): Wc[r][c] = R[c][r] */
-    float T[6];
-    for (int c = 0; c < 3; ++c) {
-      float a0 = J00 * R[c * 3 + 0];
-      float a2 = J02 * R[c * 3 + 2];
-      T[c] = a0 + a2;
-      float b1 = J11 * R[c * 3 + 1];
-      float b2 = J12 * R[c * 3 + 2];
-      T[3 + c] = b1 + b2;
-    }
-    float U[6];
-    for (int a = 0; a < 2; ++a)
-      for (int c = 0; c < 3; ++c) {
-        float acc = T[3 * a + 0] * S[0 * 3 + c];
-        float p1 = T[3 * a + 1] * S[1 * 3 + c];
-        acc = acc + p1;
-        float p2 = T[3 * a + 2] * S[2 * 3 + c];
-        U[3 * a + c] = acc + p2;
-      }
-    float Sg[3]; /* xx, xy, yy */
-    int ab[3][2] = {{0, 0}, {0, 1}, {1, 1}};
-    for (int e = 0; e < 3; ++e) {
-      int a = ab[e][0], b = ab[e][1];
-      float acc = U[3 * a + 0] * T[3 * b + 0];
-      float p1 = U[3 * a + 1] * T[3 * b + 1];
-      acc = acc + p1;
-      float p2 = U[3 * a + 2] * T[3 * b + 2];
-      Sg[e] = acc + p2;
-    }
-    float cxx = Sg[0] + lowpass, cxy = Sg[1], cyy = Sg[2] + lowpass;
-    float det = cxx * cyy - cxy * cxy;
-    if (!(det > 0.0f)) continue;
-    float px = (fx * X[0]) / X[2] + cx;
-    float py = (fy * X[1]) / X[2] + cy;
-    float rx = 3.0f * sqrtf(cxx), ry = 3.0f * sqrtf(cyy);
-    float fx0 = floorf(px - rx), fx1 = ceilf(px + rx), fy0 = floorf(py - ry), fy1 = ceilf(py + ry);
-    if (fx0 < 0.0f) fx0 = 0.0f;
-    if (fy0 < 0.0f) fy0 = 0.0f;
-    if (fx1 > (float)(W - 1)) fx1 = (float)(W - 1);
-    if (fy1 > (float)(H - 1)) fy1 = (float)(H - 1);
-    if (!(fx0 <= fx1 && fy0 <= fy1)) continue;
-    rect[4 * i] = (int32_t)fx0;
-    rect[4 * i + 1] = (int32_t)fy0;
-    rect[4 * i + 2] = (int32_t)fx1;
-    rect[4 * i + 3] = (int32_t)fy1;
-    culled[i] = 0;
+  memset(g, 0, sizeof(*g));
+  g->culled = 1;
+  g->rect[2] = g->rect[3] = -1;
+  float D[3], X[3];
+  for (int c = 0; c < 3; ++c) D[c] = p[c] - t[c];
+  for (int c = 0; c < 3; ++c) {
+    float acc = R[0 * 3 + c] * D[0];
+    float p1 = R[1 * 3 + c] * D[1];
+    acc = acc + p1;
+    float p2 = R[2 * 3 + c] * D[2];
+    X[c] = acc + p2;
   }
+  g->d = X[2];
+  if (!(X[2] > near_z)) return;
+  float s[3];
+  for (int c = 0; c < 3; ++c) s[c] = (float)exp((double)ls[c]);
+  float qw = q[0], qx = q[1], qy = q[2], qz = q[3];
+  float qn2 = qw * qw + qx * qx;
+  qn2 = qn2 + qy * qy;
+  qn2 = qn2 + qz * qz;
+  float qn = sqrtf(qn2);
+  float w = qw / qn, x = qx / qn, y = qy / qn, z = qz / qn;
+  float Rq[9];
+  Rq[0] = 1.0f - 2.0f * (y * y + z * z);
+  Rq[1] = 2.0f * (x * y - w * z);
+  Rq[2] = 2.0f * (x * z + w * y);
+  Rq[3] = 2.0f * (x * y + w * z);
+  Rq[4] = 1.0f - 2.0f * (x * x + z * z);
+  Rq[5] = 2.0f * (y * z - w * x);
+  Rq[6] = 2.0f * (x * z - w * y);
+  Rq[7] = 2.0f * (y * z + w * x);
+  Rq[8] = 1.0f - 2.0f * (x * x + y * y);
+  float M[9];
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) M[3 * r + c] = Rq[3 * r + c] * s[c];
+  float S[9];
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) {
+      float acc = M[3 * r + 0] * M[3 * c + 0];
+      float p1 = M[3 * r + 1] * M[3 * c + 1];
+      acc = acc + p1;
+      float p2 = M[3 * r + 2] * M[3 * c + 2];
+      S[3 * r + c] = acc + p2;
+    }
+  float txz = X[0] / X[2], tyz = X[1] / X[2];
+  float cu = txz < -limx ? -limx : (txz > limx ? limx : txz);
+  float cv = tyz < -limy ? -limy : (tyz > limy ? limy : tyz);
+  float tx = cu * X[2], ty = cv * X[2];
+  float z2 = X[2] * X[2];
+  float J00 = fx / X[2];
+  float J02 = -(fx * tx) / z2;
+  float J11 = fy / X[2];
+  float J12 = -(fy * ty) / z2;
+  /* T = J * Wc, Wc = R^T (world->camera rotation): Wc[r][c] = R[c][r] */
+  float T[6];
+  for (int c = 0; c < 3; ++c) {
+    float a0 = J00 * R[c * 3 + 0];
+    float a2 = J02 * R[c * 3 + 2];
+    T[c] = a0 + a2;
+    float b1 = J11 * R[c * 3 + 1];
+    float b2 = J12 * R[c * 3 + 2];
+    T[3 + c] = b1 + b2;
+  }
+  float U[6];
+  for (int a = 0; a < 2; ++a)
+    for (int c = 0; c < 3; ++c) {
+      float acc = T[3 * a + 0] * S[0 * 3 + c];
+      float p1 = T[3 * a + 1] * S[1 * 3 + c];
+      acc = acc + p1;
+      float p2 = T[3 * a + 2] * S[2 * 3 + c];
+      U[3 * a + c] = acc + p2;
+    }
+  float Sg[3]; /* xx, xy, yy */
+  int ab[3][2] = {{0, 0}, {0, 1}, {1, 1}};
+  for (int e = 0; e < 3; ++e) {
+    int a = ab[e][0], b = ab[e][1];
+    float acc = U[3 * a + 0] * T[3 * b + 0];
+    float p1 = U[3 * a + 1] * T[3 * b + 1];
+    acc = acc + p1;
+    float p2 = U[3 * a + 2] * T[3 * b + 2];
+    Sg[e] = acc + p2;
+  }
+  float cxx = Sg[0] + lowpass, cxy = Sg[1], cyy = Sg[2] + lowpass;
+  float det = cxx * cyy - cxy * cxy;
+  if (!(det > 0.0f)) return;
+  g->a = cyy / det;
+  g->b = -(cxy / det);
+  g->c = cxx / det;
+  g->px = (fx * X[0]) / X[2] + cx;
+  g->py = (fy * X[1]) / X[2] + cy;
+  g->lnsig = (float)(-log1p(exp(-(double)o)));
+  float rx = 3.0f * sqrtf(cxx), ry = 3.0f * sqrtf(cyy);
+  float fx0 = floorf(g->px - rx), fx1 = ceilf(g->px + rx), fy0 = floorf(g->py - ry), fy1 = ceilf(g->py + ry);
+  if (fx0 < 0.0f) fx0 = 0.0f;
+  if (fy0 < 0.0f) fy0 = 0.0f;
+  if (fx1 > (float)(W - 1)) fx1 = (float)(W - 1);
+  if (fy1 > (float)(H - 1)) fy1 = (float)(H - 1);
+  if (!(fx0 <= fx1 && fy0 <= fy1)) return;
+  g->rect[0] = (int32_t)fx0;
+  g->rect[1] = (int32_t)fy0;
+  g->rect[2] = (int32_t)fx1;
+  g->rect[3] = (int32_t)fy1;
+  g->culled = 0;
+}
+
+/* Pair membership (Eqs. 1-3 indicator and alpha clamp with the 3-sigma reading R-FOOT), decided
+ * in prescribed fp32: q = Delta^T conic Delta with explicit fused multiply-adds,
+ * in iff q <= min(9, 2 (L + ln sigma)), L = fl(-ln alpha_min) computed in double
+ *                                  [<=> 3-sigma ellipse and alpha >= alpha_min (= 1/255)]
+ *         and (D_t == 0 or d < fl(D_t + eps)).                                                 */
+static int in_p32(const p32* g, int x, int y, float Dt, float eps, float L) {
+  float dx = (float)x - g->px, dy = (float)y - g->py;
+  float b2 = 2.0f * g->b;
+  float t1 = g->a * dx;
+  float t2 = b2 * dx;
+  float t3 = g->c * dy;
+  float t4 = t3 * dy;
+  float inner = fmaf(t2, dy, t4);
+  float q = fmaf(t1, dx, inner);
+  float qs = L + g->lnsig;
+  float qmax = 2.0f * qs;
+  if (qmax > 9.0f) qmax = 9.0f;
+  if (!(q <= qmax)) return 0;
+  if (Dt != 0.0f) {
+    float lim = Dt + eps;
+    if (!(g->d < lim)) return 0;
+  }
+  return 1;
+}
+
+void orc_project_p32_full(int64_t n, const float* xyz, const float* ls, const float* rot, const float* op,
+                          const float* K4, int W, int H, const float* R, const float* t, float near_z,
+                          float lowpass, int32_t* rect, float* depth, int32_t* culled, float* fields /*n*6*/) {
+  for (int64_t i = 0; i < n; ++i) {
+    p32 g;
+    proj32(xyz + 3 * i, ls + 3 * i, rot + 4 * i, op ? op[i] : 0.0f, K4, W, H, R, t, near_z, lowpass, &g);
+    culled[i] = g.culled;
+    depth[i] = g.d;
+    for (int k = 0; k < 4; ++k) rect[4 * i + k] = g.rect[k];
+    if (fields) {
+      fields[6 * i] = g.px; fields[6 * i + 1] = g.py; fields[6 * i + 2] = g.a;
+      fields[6 * i + 3] = g.b; fields[6 * i + 4] = g.c; fields[6 * i + 5] = g.lnsig;
+    }
+  }
+}
+
+void orc_project_p32(int64_t n, const float* xyz, const float* ls, const float* rot,
+                     const float* K4, int W, int H, const float* R, const float* t, float near_z,
+                     float lowpass, int32_t* rect, float* depth, int32_t* culled) {
+  orc_project_p32_full(n, xyz, ls, rot, NULL, K4, W, H, R, t, near_z, lowpass, rect, depth, culled, NULL);
 }
 
 /* ---- F64 projection, the forward quantities of one Gaussian -------------- */
@@ -655,26 +709,15 @@ static camf64 make_cam(const double* K4, int W, int H, const double* R, const do
   return c;
 }
 
-/* Pixel rectangle that certainly contains every pixel with Delta^T Sigma^-1 Delta <= 9:
- * the ellipse's bounding box |dx| <= 3 sqrt(cxx), |dy| <= 3 sqrt(cyy), widened by one pixel. */
-static void f64_rect(const gproj* g, int W, int H, int* x0, int* y0, int* x1, int* y1) {
-  double rx = 3.0 * sqrt(g->cxx) + 1.0, ry = 3.0 * sqrt(g->cyy) + 1.0;
-  double a0 = floor(g->px - rx), a1 = ceil(g->px + rx), b0 = floor(g->py - ry), b1 = ceil(g->py + ry);
-  if (a0 < 0) a0 = 0;
-  if (b0 < 0) b0 = 0;
-  if (a1 > W - 1) a1 = W - 1;
-  if (b1 > H - 1) b1 = H - 1;
-  *x0 = (int)a0; *x1 = (int)a1; *y0 = (int)b0; *y1 = (int)b1;
-}
-
 typedef struct {
-  int in;       /* pair contributes */
-  int amb;      /* a decision of this pair is within fp noise of its threshold */
-  double alpha, dx, dy, ex; /* ex = exp(-power) */
+  int in;       /* pair contributes: the P32 decision (in_p32)                                 */
+  int amb;      /* an fp64 evaluation of a decision is within fp32 noise of its threshold,
+                   i.e. an fp64-decided implementation may legitimately disagree here       */
+  double alpha, dx, dy, ex; /* fp64 values; ex = exp(-power) */
 } pairv;
 
-/* Eqs. 1-3 for one pair with the footprint reading R-FOOT. */
-static pairv eval_pair(const gproj* g, int x, int y, double Dt, double eps, double alpha_min) {
+/* Eqs. 1-3 for one pair: membership from the P32 fields, values in fp64. */
+static pairv eval_pair(const gproj* g, const p32* h, int x, int y, double Dt, double eps, double alpha_min) {
   pairv r;
   memset(&r, 0, sizeof(r));
   r.dx = (double)x - g->px;
@@ -683,60 +726,82 @@ static pairv eval_pair(const gproj* g, int x, int y, double Dt, double eps, doub
   double power = 0.5 * qf;
   r.ex = exp(-power);
   r.alpha = g->sigma * r.ex;
+  r.in = in_p32(h, x, y, (float)Dt, (float)eps, (float)(-log((double)(float)alpha_min)));
   int in_ell = qf <= 9.0;
   int in_alpha = r.alpha >= alpha_min;
   int in_depth = (Dt == 0.0) || (g->d < Dt + eps);
-  r.in = in_ell && in_alpha && in_depth;
-  /* ambiguity: any of the three decisions within fp32 noise of its threshold */
   int near_ell = fabs(qf - 9.0) < 1e-4;
   int near_alpha = fabs(r.alpha / alpha_min - 1.0) < 1e-4;
-  int near_depth = (Dt != 0.0) && fabs(g->d - (Dt + eps)) < 1e-5;
-  /* only relevant when the other decisions let the pair through */
+  int near_depth = (Dt != 0.0) && fabs(g->d - (Dt + eps)) < 3e-6;
   r.amb = (near_ell && (in_alpha || near_alpha) && (in_depth || near_depth)) ||
           (near_alpha && (in_ell || near_ell) && (in_depth || near_depth)) ||
           (near_depth && (in_ell || near_ell) && (in_alpha || near_alpha));
   return r;
 }
 
-/* Gaussian-level decisions that are near a threshold (near plane, det) */
+/* Gaussian-level decisions whose fp64 evaluation is near a threshold (near plane, det) */
 static int gauss_amb(const gproj* g, double near_z) {
   if (fabs(g->d - near_z) < 1e-5) return 1;
-  if (!g->culled && g->det < 1e-6 * g->cxx * g->cyy) return 1;
+  if (g->det > 0 && g->det < 1e-6 * g->cxx * g->cyy) return 1;
   return 0;
 }
 
-/* Forward: Eqs. 1-4 per pixel (plain definition: sums over all Gaussians, W_t = 1).
- * Params in double.  Dt (0 = SDF miss, R-MISS) and Ct are per-pixel inputs.
- * Outputs: Cstar (H*W*3), WG (H*W), CG (H*W*3, nullable), amb (H*W, nullable: 1 if any pair
- * decision at the pixel is ambiguous or a Gaussian-level decision covering it is).        */
+static void f32_params(const double* xyz, const double* ls, const double* rot, double op, float* p,
+                       float* l, float* q, float* o) {
+  for (int k = 0; k < 3; ++k) {
+    p[k] = (float)xyz[k];
+    l[k] = (float)ls[k];
+  }
+  for (int k = 0; k < 4; ++k) q[k] = (float)rot[k];
+  *o = (float)op;
+}
+
+static void cam32(const double* K4, const double* R, const double* t, float* K4f, float* Rf, float* tf) {
+  for (int k = 0; k < 4; ++k) K4f[k] = (float)K4[k];
+  for (int k = 0; k < 9; ++k) Rf[k] = (float)R[k];
+  for (int k = 0; k < 3; ++k) tf[k] = (float)t[k];
+}
+
+/* Forward: Eqs. 1-4 per pixel (plain definition: sums over all Gaussians, W_t = 1), values in
+ * fp64, pair membership decided in prescribed fp32.  Params in double (their
+ * fp32 roundings feed the decisions).  Dt (0 = SDF miss, R-MISS) and Ct are per-pixel inputs.
+ * Outputs: Cstar (H*W*3), WG (H*W), CG (H*W*3, nullable), amb (H*W, nullable): 1 where an
+ * fp64-decided implementation could legitimately differ (used only against such references). */
 void orc_render(int64_t n, int deg, const double* xyz, const double* ls, const double* rot,
                 const double* op, const double* sh, const double* K4, int W, int H,
                 const double* R, const double* t, double eps, double alpha_min, double near_z,
                 double lowpass, const double* Dt, const double* Ct, double* Cstar, double* WG,
                 double* CG, uint8_t* amb) {
   camf64 cam = make_cam(K4, W, H, R, t, near_z, lowpass);
+  float K4f[4], Rf[9], tf[3];
+  cam32(K4, R, t, K4f, Rf, tf);
   int nc = (deg + 1) * (deg + 1);
   int64_t HW = (int64_t)W * H;
   double* cg = (double*)calloc(HW * 3, sizeof(double));
   memset(WG, 0, sizeof(double) * HW);
   if (amb) memset(amb, 0, HW);
   for (int64_t i = 0; i < n; ++i) {
+    float pf[3], lf[3], qf[4], of;
+    f32_params(xyz + 3 * i, ls + 3 * i, rot + 4 * i, op[i], pf, lf, qf, &of);
+    p32 h;
+    proj32(pf, lf, qf, of, K4f, W, H, Rf, tf, (float)near_z, (float)lowpass, &h);
     gproj g;
     project_f64(&cam, deg, xyz + 3 * i, ls + 3 * i, rot + 4 * i, op[i], sh + 3 * nc * i, &g);
     int gam = gauss_amb(&g, near_z);
-    if (g.culled && !gam) continue;
-    if (!(g.det > 0) || !(g.X[2] > 0)) continue; /* nothing defined to flag */
-    int x0, y0, x1, y1;
-    f64_rect(&g, W, H, &x0, &y0, &x1, &y1);
-    for (int y = y0; y <= y1; ++y)
-      for (int x = x0; x <= x1; ++x) {
+    if (h.culled || !(g.det > 0) || !(g.X[2] > 0)) {
+      if (amb && gam && g.det > 0 && g.X[2] > 0) { /* fp64 might keep it: flag its footprint */
+        double rx = 3.0 * sqrt(g.cxx) + 1.0, ry = 3.0 * sqrt(g.cyy) + 1.0;
+        int x0 = (int)fmax(0, floor(g.px - rx)), x1 = (int)fmin(W - 1, ceil(g.px + rx));
+        int y0 = (int)fmax(0, floor(g.py - ry)), y1 = (int)fmin(H - 1, ceil(g.py + ry));
+        for (int y = y0; y <= y1; ++y)
+          for (int x = x0; x <= x1; ++x) amb[(int64_t)y * W + x] = 1;
+      }
+      continue;
+    }
+    for (int y = h.rect[1]; y <= h.rect[3]; ++y)
+      for (int x = h.rect[0]; x <= h.rect[2]; ++x) {
         int64_t pi = (int64_t)y * W + x;
-        if (g.culled) {
-          pairv pv = eval_pair(&g, x, y, Dt[pi], eps, alpha_min);
-          if (amb && (pv.in || pv.amb)) amb[pi] = 1;
-          continue;
-        }
-        pairv pv = eval_pair(&g, x, y, Dt[pi], eps, alpha_min);
+        pairv pv = eval_pair(&g, &h, x, y, Dt[pi], eps, alpha_min);
         if (amb && (pv.amb || (gam && pv.in))) amb[pi] = 1;
         if (!pv.in) continue;
         for (int ch = 0; ch < 3; ++ch) cg[3 * pi + ch] += pv.alpha * g.col[ch];
@@ -762,6 +827,8 @@ void orc_backward(int64_t n, int deg, const double* xyz, const double* ls, const
                   const double* G, const uint8_t* pix_amb, double* gxyz, double* gls,
                   double* grot, double* gop, double* gsh, uint8_t* gamb) {
   camf64 cam = make_cam(K4, W, H, R, t, near_z, lowpass);
+  float K4f[4], Rf[9], tf[3];
+  cam32(K4, R, t, K4f, Rf, tf);
   int nc = (deg + 1) * (deg + 1);
   for (int64_t i = 0; i < n; ++i) {
     double* dp = gxyz + 3 * i;
@@ -777,16 +844,18 @@ void orc_backward(int64_t n, int deg, const double* xyz, const double* ls, const
     gproj g;
     const double* sh_i = sh + 3 * nc * i;
     project_f64(&cam, deg, xyz + 3 * i, ls + 3 * i, rot + 4 * i, op[i], sh_i, &g);
+    float pf[3], lf[3], qf[4], of;
+    f32_params(xyz + 3 * i, ls + 3 * i, rot + 4 * i, op[i], pf, lf, qf, &of);
+    p32 h;
+    proj32(pf, lf, qf, of, K4f, W, H, Rf, tf, (float)near_z, (float)lowpass, &h);
     if (gamb && gauss_amb(&g, near_z)) gamb[i] = 1;
-    if (g.culled) continue;
+    if (h.culled || !(g.det > 0) || !(g.X[2] > 0)) continue;
     /* ---- per-pair accumulation of the 2D gradients ---- */
     double dcol[3] = {0, 0, 0}, dsig = 0, da = 0, db = 0, dc = 0, dpx = 0, dpy = 0;
-    int x0, y0, x1, y1;
-    f64_rect(&g, W, H, &x0, &y0, &x1, &y1);
-    for (int y = y0; y <= y1; ++y)
-      for (int x = x0; x <= x1; ++x) {
+    for (int y = h.rect[1]; y <= h.rect[3]; ++y)
+      for (int x = h.rect[0]; x <= h.rect[2]; ++x) {
         int64_t pi = (int64_t)y * W + x;
-        pairv pv = eval_pair(&g, x, y, Dt[pi], eps, alpha_min);
+        pairv pv = eval_pair(&g, &h, x, y, Dt[pi], eps, alpha_min);
         if (gamb && (pv.amb || (pv.in && pix_amb && pix_amb[pi]))) gamb[i] = 1;
         if (!pv.in) continue;
         double A = 1.0 / (1.0 + WG[pi]);

@@ -98,6 +98,7 @@ struct Cam {
 struct RenderArgs {
   Cam cam;
   float eps, alpha_min, near_z, lowpass;
+  float ln_inv_amin;  // fl(-ln alpha_min), computed on the host in double
   int tile, tiles_x, tiles_y;
   int64_t n;
   int deg, nc;
@@ -266,6 +267,18 @@ __device__ __forceinline__ void view_dir(const Cam& c, const float* p, int deg, 
   sh_basis(h.dir[0], h.dir[1], h.dir[2], deg, h.Y);
 }
 
+// Pair membership, prescribed fp32 (the oracle evaluates the same sequence):
+// q = Delta^T conic Delta with explicit fused multiply-adds; in iff q <= q_max, where
+// q_max = min(9, 2 (L + ln sigma)) <=> the 3-sigma ellipse (R-FOOT) and alpha >= alpha_min.
+__device__ __forceinline__ float pair_q(float px, float py, float a, float b2, float c, float x, float y) {
+  const float dx = x - px, dy = y - py;
+  const float inner = __fmaf_rn(pmul(b2, dx), dy, pmul(pmul(c, dy), dy));
+  return __fmaf_rn(pmul(a, dx), dx, inner);
+}
+__device__ __forceinline__ float pair_qmax(float L, float lnsig) {
+  return fminf(9.0f, pmul(2.0f, padd(L, lnsig)));
+}
+
 // ============================================================================================
 // k_preprocess
 // ============================================================================================
@@ -300,11 +313,12 @@ __global__ void __launch_bounds__(256) k_preprocess(RenderArgs a, gps_gaussians 
     for (int k = 0; k < a.nc; ++k) acc = fmaf(h.Y[k], __ldg(&sh[3 * k + ch]), acc);
     col[ch] = fmaxf(acc + 0.5f, 0.0f);
   }
-  const float sigma = 1.0f / (1.0f + __expf(-__ldg(&g.opacity_raw[i])));
+  // ln(sigmoid(o)) rounded once from double: feeds the exact membership decision q <= q_max
+  const float lnsig = (float)(-log1p(exp(-(double)__ldg(&g.opacity_raw[i]))));
   const uint32_t rx = (uint32_t)pr.x0 | ((uint32_t)pr.x1 << 16);
   const uint32_t ry = (uint32_t)pr.y0 | ((uint32_t)pr.y1 << 16);
   w.rec[3 * i + 0] = make_float4(pr.px, pr.py, pr.ca, pr.cb);
-  w.rec[3 * i + 1] = make_float4(pr.cc, sigma, pr.X[2], __uint_as_float(rx));
+  w.rec[3 * i + 1] = make_float4(pr.cc, lnsig, pr.X[2], __uint_as_float(rx));
   w.rec[3 * i + 2] = make_float4(col[0], col[1], col[2], __uint_as_float(ry));
   const int tx0 = pr.x0 / a.tile, tx1 = pr.x1 / a.tile, ty0 = pr.y0 / a.tile, ty1 = pr.y1 / a.tile;
   for (int ty = ty0; ty <= ty1; ++ty)
@@ -436,7 +450,7 @@ __global__ void __launch_bounds__(TILE* TILE) k_sort_blend(RenderArgs a, const f
                                                           WsHeader* hdr, BlendIO io, int precull) {
   constexpr int NT = TILE * TILE;
   __shared__ uint64_t skeys[kMaxList];
-  __shared__ float4 s0[NT], s1[NT], s2[NT];
+  __shared__ float4 s0[NT], s1[NT], s2[NT];  // s0 = (px, py, a, 2b); s1 = (c, ln sigma, d, q_max)
   __shared__ float red[NT / 32 + 1];
   __shared__ uint32_t redi[NT / 32 + 1];
   const int t = blockIdx.x;
@@ -508,8 +522,9 @@ __global__ void __launch_bounds__(TILE* TILE) k_sort_blend(RenderArgs a, const f
     __syncthreads();
     if (threadIdx.x < cnt) {
       const uint32_t idx = vals[start + base + threadIdx.x];
-      s0[threadIdx.x] = rec[3 * idx];
-      s1[threadIdx.x] = rec[3 * idx + 1];
+      const float4 r0 = rec[3 * idx], r1 = rec[3 * idx + 1];
+      s0[threadIdx.x] = make_float4(r0.x, r0.y, r0.z, pmul(2.0f, r0.w));
+      s1[threadIdx.x] = make_float4(r1.x, r1.y, r1.z, pair_qmax(a.ln_inv_amin, r1.y));
       s2[threadIdx.x] = rec[3 * idx + 2];
     }
     __syncthreads();
@@ -521,11 +536,9 @@ __global__ void __launch_bounds__(TILE* TILE) k_sort_blend(RenderArgs a, const f
           break;
         }
         const float4 r0 = s0[k];
-        const float dx = fx - r0.x, dy = fy - r0.y;
-        const float q = r0.z * dx * dx + 2.f * r0.w * dx * dy + r1.x * dy * dy;
-        if (q > 9.f) continue;  // outside the 3-sigma ellipse (R-FOOT)
-        const float al = r1.y * __expf(-0.5f * q);
-        if (al < a.alpha_min) continue;  // P:90 clamp
+        const float q = pair_q(r0.x, r0.y, r0.z, r0.w, r1.x, fx, fy);
+        if (!(q <= r1.w)) continue;  // outside the 3-sigma ellipse or alpha < alpha_min
+        const float al = __expf(fmaf(-0.5f, q, r1.y));  // sigma exp(-q/2), Eq. 3
         const float4 r2 = s2[k];
         W += al;
         C0 = fmaf(al, r2.x, C0);
@@ -620,7 +633,7 @@ __global__ void __launch_bounds__(256) k_backward(RenderArgs a, const float4* __
                                                   const float* __restrict__ sdf_depth,
                                                   const float* __restrict__ cstar, const float* __restrict__ wg,
                                                   const uint32_t* __restrict__ target, const WsHeader* hdr,
-                                                  float4* grad2d) {
+                                                  const float* __restrict__ xyz, float4* grad2d) {
   constexpr int NP = TILE * TILE;
   __shared__ float sg0[NP], sg1[NP], sg2[NP], ss[NP], slim[NP];
   const int t = blockIdx.x;
@@ -659,6 +672,21 @@ __global__ void __launch_bounds__(256) k_backward(RenderArgs a, const float4* __
   for (int e = (int)end - 1 - warp; e >= (int)start; e -= nw) {
     const uint32_t idx = vals[e];
     const float4 r0 = rec[3 * idx], r1 = rec[3 * idx + 1], r2 = rec[3 * idx + 2];
+    const float b2 = pmul(2.0f, r0.w), qmax = pair_qmax(a.ln_inv_amin, r1.y);
+    const float sig = __expf(r1.y);
+    // p_hat in double, once per entry: the value path uses the offset from the fp32 p_hat that
+    // made the (exact) membership decision.  fp32 p_hat carries ~1e-4 px of rounding at
+    // x ~ 1000 px, which sign cancellation in a Gaussian's gradient sum would amplify.
+    float ddx, ddy;
+    {
+      const double D0 = (double)xyz[3 * idx] - a.cam.t[0], D1 = (double)xyz[3 * idx + 1] - a.cam.t[1],
+                   D2 = (double)xyz[3 * idx + 2] - a.cam.t[2];
+      const double X0 = a.cam.R[0] * D0 + a.cam.R[3] * D1 + a.cam.R[6] * D2;
+      const double X1 = a.cam.R[1] * D0 + a.cam.R[4] * D1 + a.cam.R[7] * D2;
+      const double X2 = a.cam.R[2] * D0 + a.cam.R[5] * D1 + a.cam.R[8] * D2;
+      ddx = (float)((double)a.cam.fx * X0 / X2 + (double)a.cam.cx - (double)r0.x);
+      ddy = (float)((double)a.cam.fy * X1 / X2 + (double)a.cam.cy - (double)r0.y);
+    }
     const uint32_t rx = __float_as_uint(r1.w), ry = __float_as_uint(r2.w);
     const int x0 = max((int)(rx & 0xFFFF), tx0), x1 = min((int)(rx >> 16), tx0 + TILE - 1);
     const int y0 = max((int)(ry & 0xFFFF), ty0), y1 = min((int)(ry >> 16), ty0 + TILE - 1);
@@ -669,12 +697,12 @@ __global__ void __launch_bounds__(256) k_backward(RenderArgs a, const float4* __
       const int x = x0 + k % wx, y = y0 + k / wx;
       const int p = (y - ty0) * TILE + (x - tx0);
       if (!(r1.z < slim[p])) continue;  // Eq. 1 indicator (and inactive pixels)
-      const float dx = (float)x - r0.x, dy = (float)y - r0.y;
-      const float q = r0.z * dx * dx + 2.f * r0.w * dx * dy + r1.x * dy * dy;
-      if (q > 9.f) continue;
-      const float ex = __expf(-0.5f * q);
-      const float al = r1.y * ex;
-      if (al < a.alpha_min) continue;
+      const float q = pair_q(r0.x, r0.y, r0.z, b2, r1.x, (float)x, (float)y);
+      if (!(q <= qmax)) continue;
+      const float dx = ((float)x - r0.x) - ddx, dy = ((float)y - r0.y) - ddy;  // exact offsets
+      const float qv = fmaf(r0.z * dx, dx, fmaf(2.f * r0.w * dx, dy, r1.x * dy * dy));
+      const float ex = __expf(-0.5f * qv);
+      const float al = sig * ex;
       const float gA0 = sg0[p], gA1 = sg1[p], gA2 = sg2[p];
       // dL/dalpha = A * sum_ch g_ch (c_ch - C*_ch)
       const float dal = gA0 * r2.x + gA1 * r2.y + gA2 * r2.z - ss[p];
@@ -964,6 +992,7 @@ RenderArgs make_args(const gps_gaussians* g, const gps_intrinsics* K, const gps_
   for (int i = 0; i < 9; ++i) a.cam.R[i] = T->R[i];
   for (int i = 0; i < 3; ++i) a.cam.t[i] = T->t[i];
   a.eps = c->eps_depth; a.alpha_min = c->alpha_min; a.near_z = c->near_z; a.lowpass = c->lowpass;
+  a.ln_inv_amin = (float)(-std::log((double)c->alpha_min));
   a.tile = c->tile;
   a.tiles_x = (K->width + c->tile - 1) / c->tile;
   a.tiles_y = (K->height + c->tile - 1) / c->tile;
@@ -1187,9 +1216,11 @@ gps_status gps_refine_step(gps_gaussians* g, gps_adam_state* state, const gps_vi
     {
     GPS_PROF(K_BACKWARD, s);
     if (rcfg->tile == 16)
-      k_backward<16><<<n_tiles, 256, 0, s>>>(a, rec, offsets, vals, tend, vw.sdf_depth, cstar, wg, tgt, hdr, grad2d);
+      k_backward<16><<<n_tiles, 256, 0, s>>>(a, rec, offsets, vals, tend, vw.sdf_depth, cstar, wg, tgt, hdr,
+                                             g->xyz, grad2d);
     else
-      k_backward<8><<<n_tiles, 256, 0, s>>>(a, rec, offsets, vals, tend, vw.sdf_depth, cstar, wg, tgt, hdr, grad2d);
+      k_backward<8><<<n_tiles, 256, 0, s>>>(a, rec, offsets, vals, tend, vw.sdf_depth, cstar, wg, tgt, hdr,
+                                            g->xyz, grad2d);
     }
     GPS_CHECK_LAUNCH("k_backward");
     if (g->n > 0) {

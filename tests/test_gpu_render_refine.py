@@ -40,11 +40,12 @@ def gpu_render(G, gd, gcam, fr, dev, tile=16, precull=0, target=True):
     return ras, Cs.cpu().numpy(), W.cpu().numpy(), (loss.item() if loss is not None else None)
 
 
-def check_forward(out, Cs, W, max_amb_frac):
-    ok = ~out["amb"]
-    assert (~ok).mean() <= max_amb_frac, f"{(~ok).sum()} ambiguous pixels"
-    assert np.max(np.abs(Cs[ok] - out["Cstar"][ok])) <= 1e-3
-    assert np.all(np.abs(W[ok] - out["WG"][ok]) <= 1e-3 * out["WG"][ok] + 1e-6)
+def check_forward(out, Cs, W):
+    """Pair membership is decided bit-identically on both sides, so every
+    pixel is compared: C* within 1e-3 absolute, W_G within 1e-3 relative."""
+    assert np.max(np.abs(Cs - out["Cstar"])) <= 1e-3
+    assert np.all(np.abs(W - out["WG"]) <= 1e-3 * out["WG"] + 1e-6)
+    assert np.all((W > 0) == (out["WG"] > 0))
     assert out["WG"].max() > 0.5
 
 
@@ -53,7 +54,7 @@ def test_render_cfg1_matches_oracle_and_lists_bit_exact(tile):
     G, cfg, fr, gd, Dt, Ct, tgt, gcam, ocam, dev = setup()
     ras, Cs, W, loss = gpu_render(G, gd, gcam, fr, dev, tile=tile, precull=0)
     out = O.render(gd, ocam, fr.R, fr.t, Dt, Ct)
-    check_forward(out, Cs, W, 0.02)
+    check_forward(out, Cs, W)
     ol, _, cnt, _ = O.l1_loss(out["Cstar"], out["WG"], Dt, tgt)
     assert abs(loss - ol) <= 1e-5 * ol
     # tile lists: bit-exact against the oracle's binning of its own P32 projection
@@ -96,7 +97,7 @@ def test_render_full_size_cfg4():
     G, cfg, fr, gd, Dt, Ct, tgt, gcam, ocam, dev = setup("cfg4", start=300)
     ras, Cs, W, loss = gpu_render(G, gd, gcam, fr, dev, precull=1)
     out = O.render(gd, ocam, fr.R, fr.t, Dt, Ct)
-    check_forward(out, Cs, W, 1e-3)
+    check_forward(out, Cs, W)
     ol = O.l1_loss(out["Cstar"], out["WG"], Dt, tgt)[0]
     assert abs(loss - ol) <= 1e-5 * ol
 
@@ -105,7 +106,8 @@ def test_render_full_size_cfg4():
 def oracle_grads(gd, ocam, R, t, Dt, Ct, tgt):
     out = O.render(gd, ocam, R, t, Dt, Ct)
     loss, G, cnt, samb = O.l1_loss(out["Cstar"], out["WG"], Dt, tgt)
-    grads, gamb = O.backward(gd, ocam, R, t, Dt, out["Cstar"], out["WG"], G, pix_amb=out["amb"] | samb)
+    # only sign(C* - C_k) ties (|C* - C_k| < 1e-5) can legitimately differ: membership is exact
+    grads, gamb = O.backward(gd, ocam, R, t, Dt, out["Cstar"], out["WG"], G, pix_amb=samb)
     return loss, grads, gamb
 
 
@@ -164,9 +166,12 @@ def test_adam_step_identical_gradients():
         P, M, V = O.adam_step(P, M, V, {k: np.asarray(v, np.float64) for k, v in gr.items()}, step)
     torch.cuda.synchronize()
     got = g.to_numpy()
+    lr = {"xyz": 1.6e-4, "log_scale": 5e-3, "rot": 1e-3, "opacity_raw": 5e-2, "sh": 2.5e-3}
     for k in GROUPS:
-        err = np.abs(got[k] - P[k]) / np.maximum(np.abs(P[k]), 1e-3)
-        assert err.max() <= 1e-6, (k, err.max())
+        # 1e-6 relative, plus fp32 rounding of the three updates (absolute, ~ lr)
+        Pk = np.asarray(P[k]).reshape(got[k].shape)
+        err = np.abs(got[k] - Pk) - 1e-6 * np.abs(Pk)
+        assert err.max() <= 1e-6 * 3 * lr[k], (k, err.max())
     assert st.step == 3
 
 
@@ -210,4 +215,9 @@ def test_refine_gradients_full_size_cfg4():
     loss = ras.refine_step(g, st, [view], grad_out=gout).item()
     oloss, ref, gamb = oracle_grads(gd, ocam, fr.R, fr.t, Dt, Ct, tgt)
     assert abs(loss - oloss) <= 1e-5 * oloss
-    compare_grads(gout.to_numpy(), ref, gamb, min_checked=10000)
+    got = gout.to_numpy()
+    import os
+    if os.path.isdir("gpurun_out"):  # diagnostics for offline analysis
+        np.savez_compressed("gpurun_out/cfg4_grads.npz", **{k: np.asarray(got[k], np.float32)[:, :12]
+                                                            if k == "sh" else got[k] for k in GROUPS})
+    compare_grads(got, ref, gamb, min_checked=10000)
