@@ -113,10 +113,11 @@ static int64_t band_blocks(const float* K4, int W, int H, const float* R, const 
                            float dmin, float dmax, int32_t* out /* W*H*32*3 */) {
   int64_t m = 0;
   float bs = 8.0f * voxel;
+  float inv_scale = 1.0f / scale;
   float fx = K4[0], fy = K4[1], cx = K4[2], cy = K4[3];
   for (int v = 0; v < H; ++v) {
     for (int u = 0; u < W; ++u) {
-      float d = (float)depth[(int64_t)v * W + u] / scale;
+      float d = (float)depth[(int64_t)v * W + u] * inv_scale;
       if (!(d >= dmin && d <= dmax)) continue;
       float xn = ((float)u - cx) / fx;
       float yn = ((float)v - cy) / fy;
@@ -215,6 +216,7 @@ static void integrate_block(orc_volume* v, int64_t bi, const float* K4, int W, i
                             const uint8_t* rgba) {
   const int32_t* bc = v->coords + 3 * bi;
   float fx = K4[0], fy = K4[1], cx = K4[2], cy = K4[3];
+  float inv_scale = 1.0f / scale, inv_mu = 1.0f / v->mu;
   for (int k = 0; k < 8; ++k)
     for (int j = 0; j < 8; ++j)
       for (int i = 0; i < 8; ++i) {
@@ -232,20 +234,21 @@ static void integrate_block(orc_volume* v, int64_t bi, const float* K4, int W, i
           X[c] = acc + p2;
         }
         if (!(X[2] > 0.0f)) continue;
+        float iz = 1.0f / X[2];
         float ux = fx * X[0];
-        float uf = ux / X[2];
+        float uf = ux * iz;
         uf = uf + cx;
         float vy = fy * X[1];
-        float vf = vy / X[2];
+        float vf = vy * iz;
         vf = vf + cy;
         float ur = floorf(uf + 0.5f), vr = floorf(vf + 0.5f);
         if (!(ur >= 0.0f && ur <= (float)(W - 1) && vr >= 0.0f && vr <= (float)(H - 1))) continue;
         int64_t pix = (int64_t)vr * W + (int64_t)ur;
-        float d = (float)depth[pix] / scale;
+        float d = (float)depth[pix] * inv_scale;
         if (!(d >= v->dmin && d <= v->dmax)) continue;
         float eta = d - X[2];
         if (eta < -v->mu) continue;
-        float s = eta / v->mu;
+        float s = eta * inv_mu;
         if (s > 1.0f) s = 1.0f;
         int idx = i + 8 * j + 64 * k;
         float* ts = v->tsdf + 512 * bi + idx;
@@ -255,7 +258,8 @@ static void integrate_block(orc_volume* v, int64_t bi, const float* K4, int W, i
         float num = (*ts) * wf;
         num = num + s;
         float den = wf + 1.0f;
-        *ts = num / den;
+        float rden = 1.0f / den;
+        *ts = num * rden;
         for (int c = 0; c < 3; ++c) { /* exact rational mean, round half up (R-INT) */
           int x8 = rgba[4 * pix + c];
           cw[c] = (uint8_t)((cw[c] * w + x8 + (w + 1) / 2) / (w + 1));

@@ -71,7 +71,7 @@ struct VolumeCounters {
   uint32_t n_blocks;   // blocks handed out (may exceed max_blocks on overflow)
   uint32_t n_vis;      // visible slots this frame
   uint32_t overflow;   // sticky: budget, table or visible-list overflow
-  uint32_t pad;
+  uint32_t n_prev;     // n_blocks before the current frame's allocation
   unsigned long long vis_total;  // sum of n_vis over all integrations (measurement)
 };
 
@@ -81,6 +81,9 @@ struct VolumeView {  // passed by value to kernels
   uint32_t* stamp;
   Voxel* pool;
   int32_t* vis;  // visible slots
+  uint64_t* bkeys;  // pool block index -> packed block key (for passes over all blocks)
+  int32_t* nbr;     // pool block index -> 8 pool indices of the blocks at +(dx,dy,dz), dx,dy,dz in
+                    // {0,1}, entry k = dx | dy<<1 | dz<<2 (entry 0 = itself; -1 = unallocated)
   VolumeCounters* ctr;
   uint32_t slot_mask;
   uint32_t max_blocks;

@@ -29,6 +29,7 @@ struct FuseParams {
   int W, H;
   float R[9], t[3];
   float scale, mu, voxel, bs, dmin, dmax;
+  float inv_scale, inv_mu;  // fl(1/depth_scale), fl(1/mu): host fp32 divisions
   int wmax;
 };
 
@@ -61,6 +62,7 @@ __device__ void global_insert(const VolumeView& v, uint64_t key, uint32_t frame,
       if (old == kEmptyKey) {
         const uint32_t b = atomicAdd(&v.ctr->n_blocks, 1u);
         if (b < v.max_blocks) {
+          v.bkeys[b] = key;
           v.vals[h] = (int32_t)b;  // the pool block was initialised empty at create/reset
         } else {
           v.ctr->overflow = 1u;
@@ -98,7 +100,7 @@ __device__ __forceinline__ void set_insert(unsigned long long* set, uint64_t key
 __device__ __forceinline__ void pixel_blocks(const FuseParams& p, int u, int vv, uint16_t raw,
                                              unsigned long long* set, const VolumeView& v,
                                              uint32_t frame, uint32_t* d_flag) {
-  const float d = pdiv((float)raw, p.scale);
+  const float d = pmul((float)raw, p.inv_scale);
   if (!(d >= p.dmin && d <= p.dmax)) return;
   const float xn = pdiv(psub((float)u, p.cx), p.fx);
   const float yn = pdiv(psub((float)vv, p.cy), p.fy);
@@ -176,46 +178,61 @@ __global__ void __launch_bounds__(256) k_alloc(VolumeView v, FuseParams p,
 // integration (R-INT): grid-stride over the visible list; one CTA per block, 256 threads x 2
 // adjacent voxels (one 16-byte load/store each).  Prescribed fp32, DESIGN.md §4.2.
 // ============================================================================================
-__device__ __forceinline__ void integrate_voxel(const FuseParams& p, int gx, int gy, int gz, Voxel& vx,
-                                                const uint16_t* __restrict__ depth,
-                                                const uint32_t* __restrict__ rgba) {
+// geometry of one voxel (prescribed fp32): whether it is updated, its pixel and
+// the truncated sample s.  Needs no voxel data, so skipped voxels cost no memory traffic.
+__device__ __forceinline__ bool voxel_sample(const FuseParams& p, int gx, int gy, int gz,
+                                             const uint16_t* __restrict__ depth, uint32_t& pix, float& s) {
   const float P0 = pmul((float)gx, p.voxel), P1 = pmul((float)gy, p.voxel), P2 = pmul((float)gz, p.voxel);
   const float D0 = psub(P0, p.t[0]), D1 = psub(P1, p.t[1]), D2 = psub(P2, p.t[2]);
   const float X0 = pdot3(p.R[0], D0, p.R[3], D1, p.R[6], D2);
   const float X1 = pdot3(p.R[1], D0, p.R[4], D1, p.R[7], D2);
   const float X2 = pdot3(p.R[2], D0, p.R[5], D1, p.R[8], D2);
-  if (!(X2 > 0.0f)) return;
-  const float uf = padd(pdiv(pmul(p.fx, X0), X2), p.cx);
-  const float vf = padd(pdiv(pmul(p.fy, X1), X2), p.cy);
+  if (!(X2 > 0.0f)) return false;
+  const float iz = __frcp_rn(X2);
+  const float uf = padd(pmul(pmul(p.fx, X0), iz), p.cx);
+  const float vf = padd(pmul(pmul(p.fy, X1), iz), p.cy);
   const float ur = floorf(padd(uf, 0.5f)), vr = floorf(padd(vf, 0.5f));
-  if (!(ur >= 0.0f && ur <= (float)(p.W - 1) && vr >= 0.0f && vr <= (float)(p.H - 1))) return;
-  const size_t pix = (size_t)vr * p.W + (size_t)ur;
-  const float d = pdiv((float)__ldg(&depth[pix]), p.scale);
-  if (!(d >= p.dmin && d <= p.dmax)) return;
+  if (!(ur >= 0.0f && ur <= (float)(p.W - 1) && vr >= 0.0f && vr <= (float)(p.H - 1))) return false;
+  pix = (uint32_t)vr * (uint32_t)p.W + (uint32_t)ur;
+  const float d = pmul((float)__ldg(&depth[pix]), p.inv_scale);
+  if (!(d >= p.dmin && d <= p.dmax)) return false;
   const float eta = psub(d, X2);
-  if (eta < -p.mu) return;
-  float s = pdiv(eta, p.mu);
-  if (s > 1.0f) s = 1.0f;
-  const uint32_t cw = vx.rgbw;
-  const int w = (int)(cw >> 24);
+  if (eta < -p.mu) return false;
+  s = fminf(pmul(eta, p.inv_mu), 1.0f);
+  return true;
+}
+
+// running means (R-INT): tsdf in prescribed fp32 with a correctly rounded reciprocal of (w+1);
+// colour as the exact rational mean with round-half-up, the division by w+1 done as a
+// multiply-high by ceil(2^32/(w+1)) (exact for numerators < 2^17 and w+1 <= 256)
+__device__ __forceinline__ uint2 voxel_update(float tsdf, uint32_t cw, float s, uint32_t c, int wmax,
+                                              const uint32_t* __restrict__ smagic) {
+  const uint32_t w = cw >> 24;
   const float wf = (float)w;
-  vx.tsdf = pdiv(padd(pmul(vx.tsdf, wf), s), padd(wf, 1.0f));
-  const uint32_t c = __ldg(&rgba[pix]);
-  const int w1 = w + 1, half = w1 >> 1;
-  uint32_t out = 0;
+  const float t = pmul(padd(pmul(tsdf, wf), s), __frcp_rn(padd(wf, 1.0f)));
+  const uint32_t w1 = w + 1, half = w1 >> 1, magic = smagic[w];
+  uint32_t out;
+  if (w == 0) {
+    out = c & 0x00FFFFFFu;  // first observation: the mean is the sample (2^32/1 has no u32 magic)
+  } else {
+    out = 0;
 #pragma unroll
-  for (int ch = 0; ch < 3; ++ch) {
-    const int old = (int)((cw >> (8 * ch)) & 0xFFu);
-    const int x8 = (int)((c >> (8 * ch)) & 0xFFu);
-    out |= (uint32_t)((old * w + x8 + half) / w1) << (8 * ch);
+    for (int ch = 0; ch < 3; ++ch) {
+      const uint32_t old = (cw >> (8 * ch)) & 0xFFu, x8 = (c >> (8 * ch)) & 0xFFu;
+      out |= __umulhi(old * w + x8 + half, magic) << (8 * ch);
+    }
   }
-  out |= (uint32_t)min(w1, p.wmax) << 24;
-  vx.rgbw = out;
+  out |= min(w1, (uint32_t)wmax) << 24;
+  return make_uint2(__float_as_uint(t), out);
 }
 
 __global__ void __launch_bounds__(256) k_integrate(VolumeView v, FuseParams p,
                                                    const uint16_t* __restrict__ depth,
                                                    const uint32_t* __restrict__ rgba) {
+  __shared__ uint32_t smagic[256];
+  // smagic[w] = ceil(2^32 / (w+1)) for w >= 1 (w = 0 is special-cased in voxel_update)
+  for (int d = threadIdx.x; d < 256; d += blockDim.x) smagic[d] = 0xFFFFFFFFu / (uint32_t)(d + 1) + 1u;
+  __syncthreads();
   const uint32_t nvis = min(*(volatile uint32_t*)&v.ctr->n_vis, v.max_blocks);
   if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&v.ctr->vis_total, (unsigned long long)nvis);
   const int e = 2 * threadIdx.x;  // voxel pair (e, e+1): same j,k; i even
@@ -226,17 +243,53 @@ __global__ void __launch_bounds__(256) k_integrate(VolumeView v, FuseParams p,
     if (b < 0) continue;
     int bx, by, bz;
     unpack_block(v.keys[slot], bx, by, bz);
+    const int gx = bx * 8 + li, gy = by * 8 + lj, gz = bz * 8 + lk;
+    uint32_t pix0 = 0, pix1 = 0;
+    float s0 = 0.f, s1 = 0.f;
+    const bool u0 = voxel_sample(p, gx, gy, gz, depth, pix0, s0);
+    const bool u1 = voxel_sample(p, gx + 1, gy, gz, depth, pix1, s1);
+    if (!(u0 | u1)) continue;  // neither voxel observed: no load, no store
     float4* ptr = reinterpret_cast<float4*>(v.pool + (size_t)b * 512 + e);
     float4 raw = *ptr;
-    Voxel v0{raw.x, __float_as_uint(raw.y)}, v1{raw.z, __float_as_uint(raw.w)};
-    const int gx = bx * 8 + li, gy = by * 8 + lj, gz = bz * 8 + lk;
-    integrate_voxel(p, gx, gy, gz, v0, depth, rgba);
-    integrate_voxel(p, gx + 1, gy, gz, v1, depth, rgba);
-    *ptr = make_float4(v0.tsdf, __uint_as_float(v0.rgbw), v1.tsdf, __uint_as_float(v1.rgbw));
+    if (u0) {
+      const uint2 r = voxel_update(raw.x, __float_as_uint(raw.y), s0, __ldg(&rgba[pix0]), p.wmax, smagic);
+      raw.x = __uint_as_float(r.x);
+      raw.y = __uint_as_float(r.y);
+    }
+    if (u1) {
+      const uint2 r = voxel_update(raw.z, __float_as_uint(raw.w), s1, __ldg(&rgba[pix1]), p.wmax, smagic);
+      raw.z = __uint_as_float(r.x);
+      raw.w = __uint_as_float(r.y);
+    }
+    *ptr = raw;
   }
 }
 
-__global__ void k_reset_frame(VolumeCounters* ctr) { ctr->n_vis = 0u; }
+__global__ void k_reset_frame(VolumeCounters* ctr) {
+  ctr->n_vis = 0u;
+  ctr->n_prev = ctr->n_blocks;
+}
+
+// --------------------------------------------------------------------------------------------
+// k_link: neighbour table of the blocks allocated this frame.  Each new block b looks up its 7
+// +neighbours and writes itself into the table of each existing -neighbour; every (block, entry)
+// pair has exactly one writer value, so the concurrent updates cannot conflict.
+// --------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_link(VolumeView v) {
+  const uint32_t lo = min(v.ctr->n_prev, v.max_blocks), hi = min(v.ctr->n_blocks, v.max_blocks);
+  for (uint32_t b = lo + blockIdx.x * blockDim.x + threadIdx.x; b < hi; b += gridDim.x * blockDim.x) {
+    int x, y, z;
+    unpack_block(v.bkeys[b], x, y, z);
+    v.nbr[8 * (size_t)b] = (int32_t)b;
+#pragma unroll
+    for (int k = 1; k < 8; ++k) {
+      const int dx = k & 1, dy = (k >> 1) & 1, dz = (k >> 2) & 1;
+      v.nbr[8 * (size_t)b + k] = find_block(v, x + dx, y + dy, z + dz);
+      const int32_t m = find_block(v, x - dx, y - dy, z - dz);
+      if (m >= 0) v.nbr[8 * (size_t)m + k] = (int32_t)b;
+    }
+  }
+}
 
 __global__ void k_fill_pool(Voxel* pool, size_t n) {
   const size_t stride = (size_t)gridDim.x * blockDim.x;
@@ -264,6 +317,77 @@ struct RayParams {
   int J;  // last grid index
 };
 
+// --------------------------------------------------------------------------------------------
+// Range image: for every 16x16-pixel tile, [t_min, t_max] over ALL allocated blocks whose
+// projection can cover a pixel of the tile.  A sample's base-corner block must be allocated for
+// the sample to be valid, and the sample lies in that block's box extended by one voxel on the
+// + side; every such box meets the ray of the sample's pixel, so no valid sample of a ray lies
+// outside its tile's range: starting the march at t_min and stopping at t_max is
+// result-preserving.
+// --------------------------------------------------------------------------------------------
+constexpr int kRangeTile = 16;
+constexpr int kMaxRangeTiles = 256 * 256;  // images up to 4096 x 4096 use the range image
+
+__global__ void __launch_bounds__(256) k_range(VolumeView v, RayParams p, uint32_t* tmin, uint32_t* tmax,
+                                               int tiles_x, int tiles_y) {
+  const uint32_t nb = min(*(volatile uint32_t*)&v.ctr->n_blocks, v.max_blocks);
+  for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += gridDim.x * blockDim.x) {
+    int bx, by, bz;
+    unpack_block(v.bkeys[b], bx, by, bz);
+    const float s = 8.0f * p.voxel;
+    const float lo[3] = {bx * s, by * s, bz * s};
+    const float hi[3] = {lo[0] + 9.0f * p.voxel, lo[1] + 9.0f * p.voxel, lo[2] + 9.0f * p.voxel};
+    // distance from the camera centre to the box, and to its farthest corner
+    float d2min = 0.f, d2max = 0.f;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const float o = p.t[k];
+      const float dn = o < lo[k] ? lo[k] - o : (o > hi[k] ? o - hi[k] : 0.f);
+      const float df = fmaxf(fabsf(o - lo[k]), fabsf(o - hi[k]));
+      d2min += dn * dn;
+      d2max += df * df;
+    }
+    const float t0 = sqrtf(d2min) * 0.9999f, t1 = sqrtf(d2max) * 1.0001f + 1e-4f;
+    // projected footprint (bbox of the 8 projected corners if all are in front of the camera)
+    float umin = INFINITY, umax = -INFINITY, vmin = INFINITY, vmax = -INFINITY;
+    bool all_front = true, any_front = false;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const float P0 = (c & 1 ? hi[0] : lo[0]) - p.t[0];
+      const float P1 = (c & 2 ? hi[1] : lo[1]) - p.t[1];
+      const float P2 = (c & 4 ? hi[2] : lo[2]) - p.t[2];
+      const float X = p.R[0] * P0 + p.R[3] * P1 + p.R[6] * P2;
+      const float Y = p.R[1] * P0 + p.R[4] * P1 + p.R[7] * P2;
+      const float Z = p.R[2] * P0 + p.R[5] * P1 + p.R[8] * P2;
+      if (Z > 1e-3f) {
+        any_front = true;
+        const float iz = 1.0f / Z;
+        const float u = p.fx * X * iz + p.cx, w = p.fy * Y * iz + p.cy;
+        umin = fminf(umin, u); umax = fmaxf(umax, u);
+        vmin = fminf(vmin, w); vmax = fmaxf(vmax, w);
+      } else {
+        all_front = false;
+      }
+    }
+    if (!any_front) continue;  // entirely behind the camera plane: no ray meets it
+    int tx0 = 0, tx1 = tiles_x - 1, ty0 = 0, ty1 = tiles_y - 1;
+    if (all_front) {
+      if (umax < -1.f || vmax < -1.f || umin > p.W || vmin > p.H) continue;
+      tx0 = max(0, (int)floorf((umin - 1.f) / kRangeTile));
+      tx1 = min(tiles_x - 1, (int)floorf((umax + 1.f) / kRangeTile));
+      ty0 = max(0, (int)floorf((vmin - 1.f) / kRangeTile));
+      ty1 = min(tiles_y - 1, (int)floorf((vmax + 1.f) / kRangeTile));
+    }
+    const uint32_t a0 = __float_as_uint(t0), a1 = __float_as_uint(t1);
+    for (int ty = ty0; ty <= ty1; ++ty)
+      for (int tx = tx0; tx <= tx1; ++tx) {
+        const int t = ty * tiles_x + tx;
+        if (tmin[t] > a0) atomicMin(&tmin[t], a0);
+        if (tmax[t] < a1) atomicMax(&tmax[t], a1);
+      }
+  }
+}
+
 struct BlockCache {
   int x, y, z;
   int32_t b;
@@ -278,29 +402,51 @@ __device__ __forceinline__ int32_t cached_find(const VolumeView& v, BlockCache& 
 
 // trilinear tsdf (and colour) at voxel-unit position p; returns validity
 template <bool kColor>
-__device__ __forceinline__ bool trilinear(const VolumeView& v, BlockCache& c0, BlockCache& c1, float px,
-                                          float py, float pz, float& f, float* col) {
+__device__ __forceinline__ bool trilinear(const VolumeView& v, BlockCache& c0, float px, float py, float pz,
+                                          float& f, float* col) {
   const float fx = floorf(px), fy = floorf(py), fz = floorf(pz);
   const int gx = (int)fx, gy = (int)fy, gz = (int)fz;
   const float ax = px - fx, ay = py - fy, az = pz - fz;
+  const int32_t b0 = cached_find(v, c0, gx >> 3, gy >> 3, gz >> 3);
+  if (b0 < 0) return false;
+  const int lx = gx & 7, ly = gy & 7, lz = gz & 7;
+  const bool nx = lx == 7, ny = ly == 7, nz = lz == 7;
+  Voxel vx[8];
+  if (!(nx | ny | nz)) {
+    // fast path: all 8 corners in the base voxel's block (67% of samples)
+    const Voxel* base = v.pool + (size_t)b0 * 512 + (lx + 8 * ly + 64 * lz);
+#pragma unroll
+    for (int corner = 0; corner < 8; ++corner)
+      vx[corner] = base[(corner & 1) + 8 * ((corner >> 1) & 1) + 64 * ((corner >> 2) & 1)];
+  } else {
+    // corners across a block face: the +neighbour table (one 32-byte load) replaces hash probes
+    const int4 n0 = reinterpret_cast<const int4*>(v.nbr)[2 * (size_t)b0];
+    const int4 n1 = reinterpret_cast<const int4*>(v.nbr)[2 * (size_t)b0 + 1];
+#pragma unroll
+    for (int corner = 0; corner < 8; ++corner) {
+      const int dx = corner & 1, dy = (corner >> 1) & 1, dz = (corner >> 2) & 1;
+      const bool sx = dx && nx, sy = dy && ny, sz = dz && nz;
+      const int32_t b = sz ? (sy ? (sx ? n1.w : n1.z) : (sx ? n1.y : n1.x))
+                           : (sy ? (sx ? n0.w : n0.z) : (sx ? n0.y : n0.x));
+      if (b < 0) return false;
+      const int idx = ((lx + dx) & 7) + 8 * ((ly + dy) & 7) + 64 * ((lz + dz) & 7);
+      vx[corner] = v.pool[(size_t)b * 512 + idx];
+    }
+  }
+  uint32_t wmin = 0xFFu;
+#pragma unroll
+  for (int corner = 0; corner < 8; ++corner) wmin = min(wmin, vx[corner].rgbw >> 24);
+  if (wmin == 0u) return false;
   float acc = 0.f, c[3] = {0.f, 0.f, 0.f};
 #pragma unroll
   for (int corner = 0; corner < 8; ++corner) {
     const int dx = corner & 1, dy = (corner >> 1) & 1, dz = (corner >> 2) & 1;
-    const int cx = gx + dx, cy = gy + dy, cz = gz + dz;
-    const int bx = cx >> 3, by = cy >> 3, bz = cz >> 3;
-    const int32_t b = (corner == 0) ? cached_find(v, c0, bx, by, bz)
-                                    : ((bx == c0.x && by == c0.y && bz == c0.z) ? c0.b : cached_find(v, c1, bx, by, bz));
-    if (b < 0) return false;
-    const int idx = (cx & 7) + 8 * (cy & 7) + 64 * (cz & 7);
-    const Voxel vx = v.pool[(size_t)b * 512 + idx];
-    if ((vx.rgbw >> 24) == 0u) return false;
     const float w = (dx ? ax : 1.f - ax) * (dy ? ay : 1.f - ay) * (dz ? az : 1.f - az);
-    acc = fmaf(w, vx.tsdf, acc);
+    acc = fmaf(w, vx[corner].tsdf, acc);
     if (kColor) {
-      c[0] = fmaf(w, (float)(vx.rgbw & 0xFFu), c[0]);
-      c[1] = fmaf(w, (float)((vx.rgbw >> 8) & 0xFFu), c[1]);
-      c[2] = fmaf(w, (float)((vx.rgbw >> 16) & 0xFFu), c[2]);
+      c[0] = fmaf(w, (float)(vx[corner].rgbw & 0xFFu), c[0]);
+      c[1] = fmaf(w, (float)((vx[corner].rgbw >> 8) & 0xFFu), c[1]);
+      c[2] = fmaf(w, (float)((vx[corner].rgbw >> 16) & 0xFFu), c[2]);
     }
   }
   f = acc;
@@ -312,10 +458,26 @@ __device__ __forceinline__ bool trilinear(const VolumeView& v, BlockCache& c0, B
 
 __global__ void __launch_bounds__(256) k_raycast(VolumeView v, RayParams p, float* __restrict__ depth_out,
                                                  float* __restrict__ color_out,
-                                                 float* __restrict__ vertex_out) {
+                                                 float* __restrict__ vertex_out,
+                                                 const uint32_t* __restrict__ tmin,
+                                                 const uint32_t* __restrict__ tmax) {
   const int u = blockIdx.x * 16 + (threadIdx.x & 15);
   const int vv = blockIdx.y * 16 + (threadIdx.x >> 4);
   if (u >= p.W || vv >= p.H) return;
+  int jstart = 0, jend = p.J;
+  if (tmin) {  // the tile's range image entry (CTA == 16x16 range tile)
+    const int tile = blockIdx.y * gridDim.x + blockIdx.x;
+    const uint32_t a0 = tmin[tile], a1 = tmax[tile];
+    if (a0 == 0xFFFFFFFFu) {
+      jend = -1;  // no allocated block can meet any ray of this tile: miss
+    } else {
+      const float t0 = __uint_as_float(a0), t1 = __uint_as_float(a1);
+      const float js = floorf((t0 - p.dmin) / p.voxel) - 1.0f;
+      const float je = ceilf((t1 - p.dmin) / p.voxel) + 1.0f;
+      jstart = js <= 0.f ? 0 : (js >= (float)p.J ? p.J : (int)js);
+      jend = je >= (float)p.J ? p.J : (je < 0.f ? -1 : (int)je);
+    }
+  }
   const float dcx = (u - p.cx) / p.fx, dcy = (vv - p.cy) / p.fy;
   const float nrm = sqrtf(dcx * dcx + dcy * dcy + 1.0f);
   const float inv = 1.0f / nrm;
@@ -330,11 +492,11 @@ __global__ void __launch_bounds__(256) k_raycast(VolumeView v, RayParams p, floa
   const float iqx = qx != 0.f ? 1.f / qx : INFINITY;
   const float iqy = qy != 0.f ? 1.f / qy : INFINITY;
   const float iqz = qz != 0.f ? 1.f / qz : INFINITY;
-  BlockCache c0{INT_MIN, INT_MIN, INT_MIN, -1}, c1{INT_MIN, INT_MIN, INT_MIN, -1};
+  BlockCache c0{INT_MIN, INT_MIN, INT_MIN, -1};
   bool prev_valid = false, hit = false;
   float prev_f = 0.f, tstar = 0.f;
-  int j = 0;
-  while (j <= p.J) {
+  int j = jstart;  // samples before jstart (and after jend) meet no allocated block: invalid
+  while (j <= jend) {
     const float t = p.dmin + (float)j * p.voxel;
     const float px = fmaf(t, qx, ox), py = fmaf(t, qy, oy), pz = fmaf(t, qz, oz);
     const int bx = (int)floorf(px) >> 3, by = (int)floorf(py) >> 3, bz = (int)floorf(pz) >> 3;
@@ -351,7 +513,7 @@ __global__ void __launch_bounds__(256) k_raycast(VolumeView v, RayParams p, floa
       continue;
     }
     float f;
-    const bool valid = trilinear<false>(v, c0, c1, px, py, pz, f, nullptr);
+    const bool valid = trilinear<false>(v, c0, px, py, pz, f, nullptr);
     if (j >= 1 && valid && f <= 0.f) {
       if (prev_valid && prev_f > 0.f) {
         tstar = (p.dmin + (float)(j - 1) * p.voxel) + p.voxel * prev_f / (prev_f - f);
@@ -369,7 +531,7 @@ __global__ void __launch_bounds__(256) k_raycast(VolumeView v, RayParams p, floa
     V[1] = p.t[1] + tstar * ry;
     V[2] = p.t[2] + tstar * rz;
     float fd;
-    if (trilinear<true>(v, c0, c1, V[0] * p.inv_voxel, V[1] * p.inv_voxel, V[2] * p.inv_voxel, fd, col)) {
+    if (trilinear<true>(v, c0, V[0] * p.inv_voxel, V[1] * p.inv_voxel, V[2] * p.inv_voxel, fd, col)) {
       D = tstar * inv;
       col[0] *= (1.f / 255.f); col[1] *= (1.f / 255.f); col[2] *= (1.f / 255.f);
     } else {
@@ -435,6 +597,7 @@ namespace {
 // the flag lives right after the public struct
 struct VolumeImpl : gps_volume {
   HostFlag flag;
+  uint32_t* range;  // 2 x kMaxRangeTiles: range image of the raycast (t_min, t_max bits)
 };
 
 gps_status check_sticky(const gps_volume* vol) {
@@ -486,6 +649,9 @@ gps_status gps_volume_create(const gps_volume_config* cfg, gps_stream_t stream, 
             cudaMalloc(&v->view.stamp, sizeof(uint32_t) * slots) == cudaSuccess &&
             cudaMalloc(&v->view.pool, sizeof(Voxel) * 512 * nb) == cudaSuccess &&
             cudaMalloc(&v->view.vis, sizeof(int32_t) * nb) == cudaSuccess &&
+            cudaMalloc(&v->view.bkeys, sizeof(uint64_t) * nb) == cudaSuccess &&
+            cudaMalloc(&v->view.nbr, sizeof(int32_t) * 8 * nb) == cudaSuccess &&
+            cudaMalloc(&v->range, sizeof(uint32_t) * 2 * kMaxRangeTiles) == cudaSuccess &&
             cudaMalloc(&v->view.ctr, sizeof(VolumeCounters)) == cudaSuccess &&
             cudaHostAlloc(&v->flag.host, sizeof(uint32_t), cudaHostAllocMapped) == cudaSuccess &&
             cudaHostGetDevicePointer(&v->flag.dev, v->flag.host, 0) == cudaSuccess;
@@ -514,6 +680,9 @@ void gps_volume_destroy(gps_volume* vol) {
   cudaFree(v->view.stamp);
   cudaFree(v->view.pool);
   cudaFree(v->view.vis);
+  cudaFree(v->view.bkeys);
+  cudaFree(v->view.nbr);
+  cudaFree(v->range);
   cudaFree(v->view.ctr);
   if (v->flag.host) cudaFreeHost(v->flag.host);
   delete v;
@@ -559,6 +728,8 @@ gps_status gps_fuse(gps_volume* vol, const gps_intrinsics* K, const gps_pose* T,
   for (int i = 0; i < 3; ++i) p.t[i] = T->t[i];
   p.scale = depth_scale;
   p.mu = v->cfg.mu;
+  p.inv_scale = 1.0f / depth_scale;
+  p.inv_mu = 1.0f / v->cfg.mu;
   p.voxel = v->cfg.voxel_size;
   p.bs = 8.0f * v->cfg.voxel_size;
   p.dmin = v->cfg.depth_min;
@@ -573,6 +744,11 @@ gps_status gps_fuse(gps_volume* vol, const gps_intrinsics* K, const gps_pose* T,
     k_alloc<<<ga, 256, 0, s>>>(v->view, p, depth, frame, v->flag.dev);
   }
   GPS_CHECK_LAUNCH("k_alloc");
+  {
+    GPS_PROF(K_LINK, s);
+    k_link<<<148, 256, 0, s>>>(v->view);
+  }
+  GPS_CHECK_LAUNCH("k_link");
   // persistent-style grid: 148 SMs x 8 resident 256-thread CTAs, striding over the visible list
   {
     GPS_PROF(K_INTEGRATE, s);
@@ -598,9 +774,24 @@ gps_status gps_raycast(const gps_volume* vol, const gps_intrinsics* K, const gps
   p.dmin = v->cfg.depth_min;
   p.J = (int)std::floor(((double)v->cfg.depth_max - (double)v->cfg.depth_min) / (double)v->cfg.voxel_size);
   dim3 g((p.W + 15) / 16, (p.H + 15) / 16);
+  cudaStream_t s = as_stream(stream);
+  const int ntiles = (int)(g.x * g.y);
+  uint32_t* tmin = nullptr;
+  uint32_t* tmax = nullptr;
+  if (ntiles <= kMaxRangeTiles) {
+    tmin = v->range;
+    tmax = v->range + kMaxRangeTiles;
+    GPS_CHECK_CUDA(cudaMemsetAsync(tmin, 0xFF, sizeof(uint32_t) * ntiles, s));
+    GPS_CHECK_CUDA(cudaMemsetAsync(tmax, 0x00, sizeof(uint32_t) * ntiles, s));
+    {
+      GPS_PROF(K_RANGE, s);
+      k_range<<<148 * 4, 256, 0, s>>>(v->view, p, tmin, tmax, (int)g.x, (int)g.y);
+    }
+    GPS_CHECK_LAUNCH("k_range");
+  }
   {
-    GPS_PROF(K_RAYCAST, as_stream(stream));
-    k_raycast<<<g, 256, 0, as_stream(stream)>>>(v->view, p, depth_out, color_out, vertex_out);
+    GPS_PROF(K_RAYCAST, s);
+    k_raycast<<<g, 256, 0, s>>>(v->view, p, depth_out, color_out, vertex_out, tmin, tmax);
   }
   GPS_CHECK_LAUNCH("k_raycast");
   return GPS_OK;

@@ -39,3 +39,15 @@ def test_argument_validation_is_synchronous_and_needs_no_gpu():
     assert lib.gps_render_workspace_size(10, ctypes.byref(K), ctypes.byref(rc)) == 0
     rc.tile = 16
     assert lib.gps_render_workspace_size(10, ctypes.byref(K), ctypes.byref(rc)) > 0
+
+
+def test_colour_mean_magic_division_is_exact():
+    """k_integrate divides the colour running-mean numerator (<= 255*255 + 255 + 128) by w+1
+    (1..256) as a multiply-high by ceil(2^32/(w+1)); exhaustively equal to integer division, so
+    the colour stays bit-exact with the oracle's plain division (R-INT)."""
+    import numpy as np
+    n = np.arange(0, 255 * 255 + 255 + 129, dtype=np.uint64)
+    for d in range(2, 257):  # d = w + 1; w = 0 copies the sample instead (M would be 2^32)
+        M32 = np.uint32((np.uint32(0xFFFFFFFF) // np.uint32(d)) + np.uint32(1))  # u32 as on device
+        assert int(M32) == -(-(1 << 32) // d)
+        assert np.array_equal((n * np.uint64(M32)) >> np.uint64(32), n // np.uint64(d)), d

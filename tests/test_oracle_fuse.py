@@ -170,8 +170,10 @@ def test_first_observation_copies_sample():
     sel = (np.abs(P[..., 0]) < 1e-9) & (np.abs(P[..., 1]) < 1e-9) & (cw[..., 3] == 1)
     assert sel.sum() >= 5
     z = P[..., 2][sel].astype(np.float32)
-    expect = np.minimum(np.float32(1.0), (np.float32(0.3) - z) / np.float32(MU))
-    assert np.max(np.abs(ts[sel] - expect)) <= 1e-6
+    # the sample s of DESIGN.md §4.2: d = raw * fl(1/scale), s = min(1, (d - z) * fl(1/mu))
+    d = np.float32(3000) * (np.float32(1.0) / np.float32(1e4))
+    expect = np.minimum(np.float32(1.0), (d - z) * (np.float32(1.0) / np.float32(MU)))
+    assert np.max(np.abs(ts[sel] - expect)) == 0.0
 
 
 def test_budget_overflow_flag():
