@@ -180,6 +180,7 @@ def run_ours(args):
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    upd0 = vol.stats()["updated_total"]
     clocks.start()
     N._lib.gps_profile_enable(1)
     ev0.record(stream)
@@ -236,13 +237,14 @@ def run_ours(args):
     peak, peak_src = peaks()
     P = 11 + 3 * (args.sh_degree + 1) ** 2
     per_launch = {}
-    # algorithmic bytes per launch: dense Adam reads p, m, v and the 2D gradient,
-    # writes p, m, v: 24 P + 48 B per Gaussian
-    per_launch["k_grad_adam"] = n_g * (24 * P + 48)
-    # integration reads + writes every voxel of every visible block: 16 B x 512 x B_vis
-    vis_total = vstats.get("visible_total", 0)
+    # algorithmic bytes per launch: dense Adam reads and writes p, m, v (24 P B per
+    # Gaussian) and reads each Gaussian's gradient record + flag (132 B)
+    per_launch["k_adam"] = n_g * (24 * P + 132)
+    # integration reads + writes each voxel it updates (eta >= -mu): 16 B per updated voxel,
+    # counted on device over the timed region (updated_total delta)
     if prof["k_integrate"]["launches"]:
-        per_launch["k_integrate"] = 16 * 512 * vis_total / prof["k_integrate"]["launches"]
+        upd = vstats["updated_total"] - upd0
+        per_launch["k_integrate"] = 16 * upd / prof["k_integrate"]["launches"]
     step_ms = ms / args.steps
     dominant = max((kk for kk in prof if kk != "memset"), key=lambda kk: prof[kk]["ms"])
     roof_k = dominant if dominant in per_launch else max(per_launch, key=lambda kk: prof[kk]["ms"])

@@ -94,12 +94,13 @@ void gps_volume_destroy(gps_volume* vol);
 gps_status gps_volume_reset(gps_volume* vol, gps_stream_t stream);
 /* Synchronises `stream`, then reports the number of allocated blocks (may exceed the budget
  * when an overflow happened), the budget, the number of blocks marked visible by the last
- * gps_fuse, and the sum of visible blocks over every integration since create/reset (the unit
- * count of the integration roofline).  Any pointer may be NULL.  Returns
+ * gps_fuse, the sum of visible blocks over every integration since create/reset, and the sum
+ * of voxels actually updated (eta >= -mu) over those integrations (the integration roofline's
+ * unit count: 16 bytes each).  Any pointer may be NULL.  Returns
  * GPS_ERR_OUT_OF_BLOCKS if overflow happened.                                                 */
 gps_status gps_volume_stats_sync(gps_volume* vol, gps_stream_t stream, int64_t* n_blocks /*host*/,
                                  int64_t* budget /*host*/, int64_t* n_visible /*host*/,
-                                 int64_t* visible_total /*host*/);
+                                 int64_t* visible_total /*host*/, int64_t* updated_total /*host*/);
 
 /* gps_fuse -- Sec. 3.2.1 "SDF fusion", voxel data P:60.
  * (1) Allocation: every valid depth pixel (depth/depth_scale in [depth_min, depth_max]) is

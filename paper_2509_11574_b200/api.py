@@ -117,10 +117,11 @@ class Volume:
         return depth_out, color_out, vertex_out
 
     def stats(self, stream=None):
-        nb, bud, nv, vt = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
-        st = _L.gps_volume_stats_sync(self.h, _stream(stream), C.byref(nb), C.byref(bud), C.byref(nv), C.byref(vt))
+        nb, bud, nv, vt, ut = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
+        st = _L.gps_volume_stats_sync(self.h, _stream(stream), C.byref(nb), C.byref(bud), C.byref(nv), C.byref(vt),
+                                      C.byref(ut))
         return {"n_blocks": nb.value, "budget": bud.value, "n_visible": nv.value, "visible_total": vt.value,
-                "status": N.STATUS[st]}
+                "updated_total": ut.value, "status": N.STATUS[st]}
 
     def export_blocks(self, with_voxels=True, stream=None):
         """(coords i32[n,3], voxels structured [n,512] (tsdf f32, rgbw u8[4]) or None), any order."""

@@ -73,6 +73,7 @@ struct VolumeCounters {
   uint32_t overflow;   // sticky: budget, table or visible-list overflow
   uint32_t n_prev;     // n_blocks before the current frame's allocation
   unsigned long long vis_total;  // sum of n_vis over all integrations (measurement)
+  unsigned long long upd_total;  // voxels updated over all integrations (measurement)
 };
 
 struct VolumeView {  // passed by value to kernels

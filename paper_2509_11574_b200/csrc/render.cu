@@ -17,8 +17,9 @@
 //   k_backward    one CTA per tile: a warp per list entry walks the entry's footprint inside the
 //                 tile, accumulates the 9 2D gradients in registers, warp-reduces, and issues
 //                 three vector reductions (red.global.add.v4.f32)
-//   k_grad_adam   per Gaussian: 2D -> raw-parameter chain rule fused with dense Adam; SH
-//                 coefficients swept coalesced from shared memory
+//   k_chain       per Gaussian with a gradient: 2D -> raw-parameter chain rule into a 128-B
+//                 record (11 raw gradients, clamped colour gradient, SH basis)
+//   k_adam        dense Adam streamed over float4 units of every parameter array
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -52,7 +53,7 @@ struct WsHeader {
 };
 
 struct WsLayout {
-  size_t hdr, counts, cursor, offsets, tile_end, loss_part, records, grad2d, vals, keys, cstar, wg, gbuf, total;
+  size_t hdr, counts, cursor, offsets, tile_end, loss_part, records, grad2d, rec3, vals, keys, cstar, wg, gbuf, total;
   size_t zero_begin, zero_bytes;
 };
 
@@ -77,6 +78,7 @@ WsLayout ws_layout(int64_t n, int W, int H, int tile, int64_t cap, int64_t n_par
   L.loss_part = take(4 * tiles);
   L.records = take(48 * (size_t)std::max<int64_t>(n, 1));
   L.grad2d = refine ? take(48 * (size_t)std::max<int64_t>(n, 1)) : 0;
+  L.rec3 = refine ? take(128 * (size_t)std::max<int64_t>(n, 1)) : 0;
   L.vals = take(4 * (size_t)cap);
   L.keys = take(8 * (size_t)cap);
   L.cstar = refine ? take(12 * (size_t)W * H) : 0;
@@ -748,39 +750,19 @@ struct AdamArgs {
   float inv_sqrt_bc2;                                               // 1 / sqrt(1 - b2^t)
 };
 
-enum { kModeFinal = 0, kModeAccum = 1, kModeExternal = 2 };
 
-__device__ __forceinline__ void adam1(float& p, float& m, float& v, float g, float step, const AdamArgs& ad) {
-  m = ad.b1 * m + (1.0f - ad.b1) * g;
-  v = ad.b2 * v + (1.0f - ad.b2) * g * g;
-  p -= step * m / (sqrtf(v) * ad.inv_sqrt_bc2 + ad.eps);
-}
+constexpr int kChainThreads = 128;
+constexpr int kAdamThreads = 256;
 
-constexpr int kAdamThreads = 128;
-
-template <int MODE>
-__global__ void __launch_bounds__(kAdamThreads) k_grad_adam(RenderArgs a, gps_gaussians g, gps_gaussians gm,
-                                                            gps_gaussians gv, const float4* __restrict__ grad2d,
-                                                            gps_gaussians gbuf, int has_gbuf, gps_gaussians gout,
-                                                            int has_gout, AdamArgs ad) {
-  __shared__ float sY[kAdamThreads][16];
-  __shared__ float sdc[kAdamThreads][3];
-  const int64_t i0 = (int64_t)blockIdx.x * kAdamThreads;
-  const int64_t i = i0 + threadIdx.x;
+// Raw-parameter gradient of one Gaussian from its 2D gradients (R-GRAD chain rule).  Outputs
+// gx[3], gls[3], gq[4], gop, dcol[3] (clamped channels zeroed) and the SH basis Y[16] at the view
+// direction (the SH gradient is Y[k] * dcol[ch]).
+__device__ __forceinline__ void chain3d(const RenderArgs& a, const gps_gaussians& g, int64_t i, float dpx, float dpy,
+                                        float da, float db, float dcc, float dsig, float* dcol, float* gx,
+                                        float* gls, float* gq, float& gop, float* Y) {
   const int nc = a.nc;
-  if (i < a.n) {
-    float gx[3] = {0, 0, 0}, gls[3] = {0, 0, 0}, gq[4] = {0, 0, 0, 0}, gop = 0.f;
-    float dcol[3] = {0, 0, 0};
-    float Y[16];
 #pragma unroll
-    for (int k = 0; k < 16; ++k) Y[k] = 0.f;
-    if (MODE != kModeExternal) {
-      const float4 q0 = grad2d[3 * i], q1 = grad2d[3 * i + 1], q2 = grad2d[3 * i + 2];
-      const float dpx = q0.x, dpy = q0.y, da = q0.z, db = q0.w, dcc = q1.x, dsig = q1.y;
-      dcol[0] = q1.z; dcol[1] = q1.w; dcol[2] = q2.x;
-      const bool nz = (dpx != 0.f) | (dpy != 0.f) | (da != 0.f) | (db != 0.f) | (dcc != 0.f) | (dsig != 0.f) |
-                      (dcol[0] != 0.f) | (dcol[1] != 0.f) | (dcol[2] != 0.f);
-      if (nz) {
+  for (int k = 0; k < 3; ++k) gx[k] = gls[k] = 0.f;
         const float* p = g.xyz + 3 * i;
         Proj pr;
         project_p32(a.cam, a.near_z, a.lowpass, p, g.log_scale + 3 * i, g.rot + 4 * i, pr);
@@ -885,79 +867,151 @@ __global__ void __launch_bounds__(kAdamThreads) k_grad_adam(RenderArgs a, gps_ga
         const float iqn = 1.f / pr.qn;
 #pragma unroll
         for (int k = 0; k < 4; ++k) gq[k] = (dqh[k] - pr.qh[k] * dot) * iqn;
-      } else {
-        dcol[0] = dcol[1] = dcol[2] = 0.f;
-      }
-    } else {
+}
+
+// k_chain: one thread per Gaussian with a non-zero 2D gradient.  ACCUM = 0 writes the 128-byte
+// gradient record {gx, gls, gq, gop, dcol, Y[16]} and flags it in the (per-iteration zeroed) 2D
+// gradient slot; ACCUM = 1 adds the dense raw gradient into gbuf (multi-view rounds).
+template <int ACCUM>
+__global__ void __launch_bounds__(kChainThreads) k_chain(RenderArgs a, gps_gaussians g, float4* grad2d,
+                                                         float4* rec3, gps_gaussians gbuf) {
+  const int64_t i = blockIdx.x * (int64_t)kChainThreads + threadIdx.x;
+  if (i >= a.n) return;
+  const float4 q0 = grad2d[3 * i], q1 = grad2d[3 * i + 1], q2 = grad2d[3 * i + 2];
+  float dcol[3] = {q1.z, q1.w, q2.x};
+  const bool nz = (q0.x != 0.f) | (q0.y != 0.f) | (q0.z != 0.f) | (q0.w != 0.f) | (q1.x != 0.f) | (q1.y != 0.f) |
+                  (dcol[0] != 0.f) | (dcol[1] != 0.f) | (dcol[2] != 0.f);
+  if (!nz) return;
+  float gx[3], gls[3], gq[4], gop, Y[16];
+  chain3d(a, g, i, q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, dcol, gx, gls, gq, gop, Y);
+  if (ACCUM) {
 #pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        gx[k] = gbuf.xyz[3 * i + k];
-        gls[k] = gbuf.log_scale[3 * i + k];
-      }
-#pragma unroll
-      for (int k = 0; k < 4; ++k) gq[k] = gbuf.rot[4 * i + k];
-      gop = gbuf.opacity_raw[i];
+    for (int k = 0; k < 3; ++k) {
+      gbuf.xyz[3 * i + k] += gx[k];
+      gbuf.log_scale[3 * i + k] += gls[k];
     }
 #pragma unroll
-    for (int k = 0; k < 16; ++k) sY[threadIdx.x][k] = Y[k];
-    sdc[threadIdx.x][0] = dcol[0]; sdc[threadIdx.x][1] = dcol[1]; sdc[threadIdx.x][2] = dcol[2];
-    if (MODE == kModeAccum) {
+    for (int k = 0; k < 4; ++k) gbuf.rot[4 * i + k] += gq[k];
+    gbuf.opacity_raw[i] += gop;
+    float* sh = gbuf.sh + (size_t)i * a.nc * 3;
+    for (int k = 0; k < a.nc; ++k)
 #pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        gbuf.xyz[3 * i + k] += gx[k];
-        gbuf.log_scale[3 * i + k] += gls[k];
-      }
-#pragma unroll
-      for (int k = 0; k < 4; ++k) gbuf.rot[4 * i + k] += gq[k];
-      gbuf.opacity_raw[i] += gop;
-    } else {
-      if (MODE == kModeFinal && has_gbuf) {
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-          gx[k] += gbuf.xyz[3 * i + k];
-          gls[k] += gbuf.log_scale[3 * i + k];
-        }
-#pragma unroll
-        for (int k = 0; k < 4; ++k) gq[k] += gbuf.rot[4 * i + k];
-        gop += gbuf.opacity_raw[i];
-      }
-      if (has_gout) {
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-          gout.xyz[3 * i + k] = gx[k];
-          gout.log_scale[3 * i + k] = gls[k];
-        }
-#pragma unroll
-        for (int k = 0; k < 4; ++k) gout.rot[4 * i + k] = gq[k];
-        gout.opacity_raw[i] = gop;
-      }
-#pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        adam1(g.xyz[3 * i + k], gm.xyz[3 * i + k], gv.xyz[3 * i + k], gx[k], ad.step_xyz, ad);
-        adam1(g.log_scale[3 * i + k], gm.log_scale[3 * i + k], gv.log_scale[3 * i + k], gls[k], ad.step_ls, ad);
-      }
-#pragma unroll
-      for (int k = 0; k < 4; ++k) adam1(g.rot[4 * i + k], gm.rot[4 * i + k], gv.rot[4 * i + k], gq[k], ad.step_rot, ad);
-      adam1(g.opacity_raw[i], gm.opacity_raw[i], gv.opacity_raw[i], gop, ad.step_op, ad);
+      for (int ch = 0; ch < 3; ++ch) sh[3 * k + ch] += Y[k] * dcol[ch];
+    return;
+  }
+  float4* r = rec3 + 8 * i;
+  r[0] = make_float4(gx[0], gx[1], gx[2], gls[0]);
+  r[1] = make_float4(gls[1], gls[2], gq[0], gq[1]);
+  r[2] = make_float4(gq[2], gq[3], gop, dcol[0]);
+  r[3] = make_float4(dcol[1], dcol[2], 0.f, 0.f);
+  r[4] = make_float4(Y[0], Y[1], Y[2], Y[3]);
+  r[5] = make_float4(Y[4], Y[5], Y[6], Y[7]);
+  r[6] = make_float4(Y[8], Y[9], Y[10], Y[11]);
+  r[7] = make_float4(Y[12], Y[13], Y[14], Y[15]);
+  grad2d[3 * i + 2].y = 1.0f;  // record valid for this iteration (the slot is re-zeroed by k_preprocess)
+}
+
+// k_adam: dense Adam (R-ADAM) streamed over float4 units of every parameter array (all five SoA
+// groups in one flattened index space).  Gradients: external arrays (gps_adam_step), or the
+// flagged k_chain record (0 if unflagged) plus an optional dense multi-view accumulator.
+struct AdamSrc {
+  const float4* grad2d;  // flags (nullable in external mode)
+  const float* rec3;     // 32 floats per Gaussian
+  gps_gaussians gbuf;    // dense accumulator or external gradient (nullable pointers)
+  int has_gbuf, external;
+  gps_gaussians gout;
+  int has_gout;
+};
+
+__device__ __forceinline__ float chain_grad(const AdamSrc& s, int group, uint32_t gi, int comp) {
+  if (!(s.grad2d[3 * gi + 2].y != 0.f)) return 0.f;
+  const float* r = s.rec3 + 32 * gi;
+  switch (group) {
+    case 0: return r[comp];           // xyz
+    case 1: return r[3 + comp];       // log_scale
+    case 2: return r[6 + comp];       // rot
+    case 3: return r[10];             // opacity
+    default: {                        // sh: Y[k] * dcol[ch]
+      const int k = comp / 3, ch = comp - 3 * k;
+      return r[16 + k] * r[11 + ch];
     }
   }
-  __syncthreads();
-  // ---- SH coefficients: coalesced sweep over this CTA's contiguous block ----
-  const int64_t nG = min((int64_t)kAdamThreads, a.n - i0);
-  if (nG <= 0) return;
-  const int per = nc * 3;
-  const int64_t base = i0 * per;
-  const int total = (int)(nG * per);
-  for (int e = threadIdx.x; e < total; e += kAdamThreads) {
-    const int gi = e / per, r = e - gi * per, k = r / 3, ch = r - 3 * k;
-    float grad = MODE == kModeExternal ? gbuf.sh[base + e] : sY[gi][k] * sdc[gi][ch];
-    if (MODE == kModeAccum) {
-      gbuf.sh[base + e] += grad;
-      continue;
+}
+
+__global__ void __launch_bounds__(kAdamThreads) k_adam(RenderArgs a, gps_gaussians g, gps_gaussians gm, gps_gaussians gv,
+                                                       AdamSrc src, AdamArgs ad) {
+  // 32-bit element indices: n * 3 (deg+1)^2 < 2^31 is checked on the host
+  const uint32_t n = (uint32_t)a.n, nsh = 3u * (uint32_t)a.nc;
+  const uint32_t u1 = (3u * n + 3u) / 4u, u2 = u1 + (3u * n + 3u) / 4u, u3 = u2 + n, u4 = u3 + (n + 3u) / 4u,
+                 u5 = u4 + (nsh * n + 3u) / 4u;
+  for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < u5; u += gridDim.x * blockDim.x) {
+    const int grp = (u >= u1) + (u >= u2) + (u >= u3) + (u >= u4);
+    float *P, *M, *V, *E, *O;
+    float step;
+    uint32_t len, dim, base;
+    switch (grp) {
+      case 0: P = g.xyz; M = gm.xyz; V = gv.xyz; E = src.gbuf.xyz; O = src.gout.xyz; step = ad.step_xyz;
+              len = 3u * n; dim = 3u; base = 0u; break;
+      case 1: P = g.log_scale; M = gm.log_scale; V = gv.log_scale; E = src.gbuf.log_scale; O = src.gout.log_scale;
+              step = ad.step_ls; len = 3u * n; dim = 3u; base = u1; break;
+      case 2: P = g.rot; M = gm.rot; V = gv.rot; E = src.gbuf.rot; O = src.gout.rot; step = ad.step_rot;
+              len = 4u * n; dim = 4u; base = u2; break;
+      case 3: P = g.opacity_raw; M = gm.opacity_raw; V = gv.opacity_raw; E = src.gbuf.opacity_raw;
+              O = src.gout.opacity_raw; step = ad.step_op; len = n; dim = 1u; base = u3; break;
+      default: P = g.sh; M = gm.sh; V = gv.sh; E = src.gbuf.sh; O = src.gout.sh; step = ad.step_shr;
+               len = nsh * n; dim = nsh; base = u4; break;
     }
-    if (MODE == kModeFinal && has_gbuf) grad += gbuf.sh[base + e];
-    if (has_gout) gout.sh[base + e] = grad;
-    adam1(g.sh[base + e], gm.sh[base + e], gv.sh[base + e], grad, k == 0 ? ad.step_sh0 : ad.step_shr, ad);
+    const uint32_t e0 = 4u * (u - base);
+    const uint32_t cnt = min(4u, len - e0);
+    float p[4], m[4], v[4];
+    if (cnt == 4u) {
+      const float4 p4 = *reinterpret_cast<const float4*>(P + e0), m4 = *reinterpret_cast<const float4*>(M + e0),
+                   v4 = *reinterpret_cast<const float4*>(V + e0);
+      p[0] = p4.x; p[1] = p4.y; p[2] = p4.z; p[3] = p4.w;
+      m[0] = m4.x; m[1] = m4.y; m[2] = m4.z; m[3] = m4.w;
+      v[0] = v4.x; v[1] = v4.y; v[2] = v4.z; v[3] = v4.w;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        p[k] = (uint32_t)k < cnt ? P[e0 + k] : 0.f;
+        m[k] = (uint32_t)k < cnt ? M[e0 + k] : 0.f;
+        v[k] = (uint32_t)k < cnt ? V[e0 + k] : 0.f;
+      }
+    }
+    uint32_t gi = e0 / dim, comp = e0 - gi * dim;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t e = e0 + k;
+      float gk = 0.f;
+      if ((uint32_t)k < cnt) {
+        if (src.external) {
+          gk = E[e];
+        } else {
+          gk = chain_grad(src, grp, gi, (int)comp);
+          if (src.has_gbuf) gk += E[e];
+        }
+        if (src.has_gout) O[e] = gk;
+      }
+      const float st = (grp == 4 && comp < 3u) ? ad.step_sh0 : step;
+      m[k] = ad.b1 * m[k] + (1.0f - ad.b1) * gk;
+      v[k] = ad.b2 * v[k] + (1.0f - ad.b2) * gk * gk;
+      p[k] -= st * m[k] / (sqrtf(v[k]) * ad.inv_sqrt_bc2 + ad.eps);
+      if (++comp == dim) {  // next element: advance (gaussian, component) without a division
+        comp = 0u;
+        ++gi;
+      }
+    }
+    if (cnt == 4u) {
+      *reinterpret_cast<float4*>(P + e0) = make_float4(p[0], p[1], p[2], p[3]);
+      *reinterpret_cast<float4*>(M + e0) = make_float4(m[0], m[1], m[2], m[3]);
+      *reinterpret_cast<float4*>(V + e0) = make_float4(v[0], v[1], v[2], v[3]);
+    } else {
+      for (uint32_t k = 0; k < cnt; ++k) {
+        P[e0 + k] = p[k];
+        M[e0 + k] = m[k];
+        V[e0 + k] = v[k];
+      }
+    }
   }
 }
 
@@ -973,7 +1027,7 @@ bool valid_K(const gps_intrinsics* K) {
 
 gps_status check_gaussians(const gps_gaussians* g, const char* who) {
   if (!g) return invalid(std::string(who) + ": null Gaussians");
-  if (g->n < 0 || g->n > 0x7FFFFFFFll) return invalid(std::string(who) + ": bad Gaussian count");
+  if (g->n < 0 || g->n > (1ll << 25)) return invalid(std::string(who) + ": Gaussian count must be <= 2^25");
   if (g->sh_degree < 0 || g->sh_degree > 3) return invalid(std::string(who) + ": sh_degree must be 0..3");
   if (g->n > 0 && (!g->xyz || !g->log_scale || !g->rot || !g->opacity_raw || !g->sh))
     return invalid(std::string(who) + ": null Gaussian array");
@@ -1224,15 +1278,29 @@ gps_status gps_refine_step(gps_gaussians* g, gps_adam_state* state, const gps_vi
     }
     GPS_CHECK_LAUNCH("k_backward");
     if (g->n > 0) {
-      const unsigned grid = (unsigned)((g->n + kAdamThreads - 1) / kAdamThreads);
-      GPS_PROF(K_GRAD_ADAM, s);
+      const unsigned cgrid = (unsigned)((g->n + kChainThreads - 1) / kChainThreads);
+      float4* rec3 = reinterpret_cast<float4*>(w + L.rec3);
+      GPS_PROF(K_CHAIN, s);
       if (v < n_views - 1)
-        k_grad_adam<kModeAccum><<<grid, kAdamThreads, 0, s>>>(a, *g, state->m, state->v, grad2d, gb, 1, gout, 0, ad);
+        k_chain<1><<<cgrid, kChainThreads, 0, s>>>(a, *g, grad2d, rec3, gb);
       else
-        k_grad_adam<kModeFinal><<<grid, kAdamThreads, 0, s>>>(a, *g, state->m, state->v, grad2d, gb, n_views > 1,
-                                                               gout, grad_out != nullptr, ad);
-      GPS_CHECK_LAUNCH("k_grad_adam");
+        k_chain<0><<<cgrid, kChainThreads, 0, s>>>(a, *g, grad2d, rec3, gb);
+      GPS_CHECK_LAUNCH("k_chain");
     }
+  }
+  if (g->n > 0) {
+    RenderArgs a = make_args(g, &views[0].K, &views[0].T, rcfg, cap);
+    AdamSrc src{};
+    src.grad2d = grad2d;
+    src.rec3 = reinterpret_cast<const float*>(w + L.rec3);
+    src.gbuf = gb;
+    src.has_gbuf = n_views > 1;
+    src.external = 0;
+    src.gout = grad_out ? *grad_out : gps_gaussians{};
+    src.has_gout = grad_out != nullptr;
+    GPS_PROF(K_GRAD_ADAM, s);
+    k_adam<<<148 * 8, kAdamThreads, 0, s>>>(a, *g, state->m, state->v, src, ad);
+    GPS_CHECK_LAUNCH("k_adam");
   }
   state->step += 1;
   return GPS_OK;
@@ -1251,10 +1319,12 @@ gps_status gps_adam_step(gps_gaussians* g, gps_adam_state* state, const gps_gaus
   a.deg = g->sh_degree;
   a.nc = (g->sh_degree + 1) * (g->sh_degree + 1);
   if (g->n > 0) {
-    const unsigned grid = (unsigned)((g->n + kAdamThreads - 1) / kAdamThreads);
-    k_grad_adam<kModeExternal><<<grid, kAdamThreads, 0, as_stream(stream)>>>(a, *g, state->m, state->v, nullptr, *grad,
-                                                                             1, gps_gaussians{}, 0, ad);
-    GPS_CHECK_LAUNCH("k_grad_adam");
+    AdamSrc src{};
+    src.gbuf = *grad;
+    src.external = 1;
+    GPS_PROF(K_GRAD_ADAM, as_stream(stream));
+    k_adam<<<148 * 8, kAdamThreads, 0, as_stream(stream)>>>(a, *g, state->m, state->v, src, ad);
+    GPS_CHECK_LAUNCH("k_adam");
   }
   state->step += 1;
   return GPS_OK;

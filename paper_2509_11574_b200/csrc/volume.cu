@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -237,10 +238,12 @@ __global__ void __launch_bounds__(256) k_integrate(VolumeView v, FuseParams p,
   if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&v.ctr->vis_total, (unsigned long long)nvis);
   const int e = 2 * threadIdx.x;  // voxel pair (e, e+1): same j,k; i even
   const int li = e & 7, lj = (e >> 3) & 7, lk = e >> 6;
+  __shared__ uint32_t scnt[8];
+  uint32_t n_upd = 0;
   for (uint32_t q = blockIdx.x; q < nvis; q += gridDim.x) {
     const int32_t slot = v.vis[q];
     const int32_t b = v.vals[slot];
-    if (b < 0) continue;
+    if (b < 0) continue;  // uniform across the CTA
     int bx, by, bz;
     unpack_block(v.keys[slot], bx, by, bz);
     const int gx = bx * 8 + li, gy = by * 8 + lj, gz = bz * 8 + lk;
@@ -248,20 +251,31 @@ __global__ void __launch_bounds__(256) k_integrate(VolumeView v, FuseParams p,
     float s0 = 0.f, s1 = 0.f;
     const bool u0 = voxel_sample(p, gx, gy, gz, depth, pix0, s0);
     const bool u1 = voxel_sample(p, gx + 1, gy, gz, depth, pix1, s1);
-    if (!(u0 | u1)) continue;  // neither voxel observed: no load, no store
-    float4* ptr = reinterpret_cast<float4*>(v.pool + (size_t)b * 512 + e);
-    float4 raw = *ptr;
-    if (u0) {
-      const uint2 r = voxel_update(raw.x, __float_as_uint(raw.y), s0, __ldg(&rgba[pix0]), p.wmax, smagic);
-      raw.x = __uint_as_float(r.x);
-      raw.y = __uint_as_float(r.y);
+    if (u0 | u1) {  // a voxel pair nobody observes costs no load and no store
+      float4* ptr = reinterpret_cast<float4*>(v.pool + (size_t)b * 512 + e);
+      float4 raw = *ptr;
+      if (u0) {
+        const uint2 r = voxel_update(raw.x, __float_as_uint(raw.y), s0, __ldg(&rgba[pix0]), p.wmax, smagic);
+        raw.x = __uint_as_float(r.x);
+        raw.y = __uint_as_float(r.y);
+      }
+      if (u1) {
+        const uint2 r = voxel_update(raw.z, __float_as_uint(raw.w), s1, __ldg(&rgba[pix1]), p.wmax, smagic);
+        raw.z = __uint_as_float(r.x);
+        raw.w = __uint_as_float(r.y);
+      }
+      *ptr = raw;
+      n_upd += (uint32_t)u0 + (uint32_t)u1;
     }
-    if (u1) {
-      const uint2 r = voxel_update(raw.z, __float_as_uint(raw.w), s1, __ldg(&rgba[pix1]), p.wmax, smagic);
-      raw.z = __uint_as_float(r.x);
-      raw.w = __uint_as_float(r.y);
-    }
-    *ptr = raw;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) n_upd += __shfl_xor_sync(0xFFFFFFFFu, n_upd, o);
+  if ((threadIdx.x & 31) == 0) scnt[threadIdx.x >> 5] = n_upd;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long s = 0;
+    for (int k = 0; k < 8; ++k) s += scnt[k];
+    if (s) atomicAdd(&v.ctr->upd_total, s);
   }
 }
 
@@ -411,51 +425,46 @@ __device__ __forceinline__ bool trilinear(const VolumeView& v, BlockCache& c0, f
   if (b0 < 0) return false;
   const int lx = gx & 7, ly = gy & 7, lz = gz & 7;
   const bool nx = lx == 7, ny = ly == 7, nz = lz == 7;
+  // one branch-free path for every sample: the base block's +neighbour row (one 32-byte load,
+  // L1-resident along a ray) supplies the block of each corner; corners inside the base block
+  // select b0 itself (entry 0)
+  const int4 n0 = reinterpret_cast<const int4*>(v.nbr)[2 * (size_t)b0];
+  const int4 n1 = reinterpret_cast<const int4*>(v.nbr)[2 * (size_t)b0 + 1];
   Voxel vx[8];
-  if (!(nx | ny | nz)) {
-    // fast path: all 8 corners in the base voxel's block (67% of samples)
-    const Voxel* base = v.pool + (size_t)b0 * 512 + (lx + 8 * ly + 64 * lz);
-#pragma unroll
-    for (int corner = 0; corner < 8; ++corner)
-      vx[corner] = base[(corner & 1) + 8 * ((corner >> 1) & 1) + 64 * ((corner >> 2) & 1)];
-  } else {
-    // corners across a block face: the +neighbour table (one 32-byte load) replaces hash probes
-    const int4 n0 = reinterpret_cast<const int4*>(v.nbr)[2 * (size_t)b0];
-    const int4 n1 = reinterpret_cast<const int4*>(v.nbr)[2 * (size_t)b0 + 1];
-#pragma unroll
-    for (int corner = 0; corner < 8; ++corner) {
-      const int dx = corner & 1, dy = (corner >> 1) & 1, dz = (corner >> 2) & 1;
-      const bool sx = dx && nx, sy = dy && ny, sz = dz && nz;
-      const int32_t b = sz ? (sy ? (sx ? n1.w : n1.z) : (sx ? n1.y : n1.x))
-                           : (sy ? (sx ? n0.w : n0.z) : (sx ? n0.y : n0.x));
-      if (b < 0) return false;
-      const int idx = ((lx + dx) & 7) + 8 * ((ly + dy) & 7) + 64 * ((lz + dz) & 7);
-      vx[corner] = v.pool[(size_t)b * 512 + idx];
-    }
-  }
-  uint32_t wmin = 0xFFu;
-#pragma unroll
-  for (int corner = 0; corner < 8; ++corner) wmin = min(wmin, vx[corner].rgbw >> 24);
-  if (wmin == 0u) return false;
-  float acc = 0.f, c[3] = {0.f, 0.f, 0.f};
+  bool ok = true;
 #pragma unroll
   for (int corner = 0; corner < 8; ++corner) {
     const int dx = corner & 1, dy = (corner >> 1) & 1, dz = (corner >> 2) & 1;
-    const float w = (dx ? ax : 1.f - ax) * (dy ? ay : 1.f - ay) * (dz ? az : 1.f - az);
-    acc = fmaf(w, vx[corner].tsdf, acc);
-    if (kColor) {
-      c[0] = fmaf(w, (float)(vx[corner].rgbw & 0xFFu), c[0]);
-      c[1] = fmaf(w, (float)((vx[corner].rgbw >> 8) & 0xFFu), c[1]);
-      c[2] = fmaf(w, (float)((vx[corner].rgbw >> 16) & 0xFFu), c[2]);
-    }
+    const bool sx = dx && nx, sy = dy && ny, sz = dz && nz;
+    const int32_t b = sz ? (sy ? (sx ? n1.w : n1.z) : (sx ? n1.y : n1.x))
+                         : (sy ? (sx ? n0.w : n0.z) : (sx ? n0.y : b0));
+    ok &= b >= 0;
+    const int idx = ((lx + dx) & 7) + 8 * ((ly + dy) & 7) + 64 * ((lz + dz) & 7);
+    vx[corner] = v.pool[(size_t)max(b, 0) * 512 + idx];
   }
-  f = acc;
+  uint32_t wmin = vx[0].rgbw;
+#pragma unroll
+  for (int corner = 1; corner < 8; ++corner) wmin = min(wmin, vx[corner].rgbw);
+  if (!ok || (wmin >> 24) == 0u) return false;  // an unallocated corner, or w = 0
+  // trilinear as nested lerps (x, then y, then z)
+  auto lerp = [](float a, float b, float t) { return fmaf(t, b - a, a); };
+  const float x00 = lerp(vx[0].tsdf, vx[1].tsdf, ax), x10 = lerp(vx[2].tsdf, vx[3].tsdf, ax);
+  const float x01 = lerp(vx[4].tsdf, vx[5].tsdf, ax), x11 = lerp(vx[6].tsdf, vx[7].tsdf, ax);
+  f = lerp(lerp(x00, x10, ay), lerp(x01, x11, ay), az);
   if (kColor) {
-    col[0] = c[0]; col[1] = c[1]; col[2] = c[2];
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+      float c[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) c[k] = (float)((vx[k].rgbw >> (8 * ch)) & 0xFFu);
+      col[ch] = lerp(lerp(lerp(c[0], c[1], ax), lerp(c[2], c[3], ax), ay),
+                     lerp(lerp(c[4], c[5], ax), lerp(c[6], c[7], ax), ay), az);
+    }
   }
   return true;
 }
 
+template <int kDebug>
 __global__ void __launch_bounds__(256) k_raycast(VolumeView v, RayParams p, float* __restrict__ depth_out,
                                                  float* __restrict__ color_out,
                                                  float* __restrict__ vertex_out,
@@ -496,7 +505,9 @@ __global__ void __launch_bounds__(256) k_raycast(VolumeView v, RayParams p, floa
   bool prev_valid = false, hit = false;
   float prev_f = 0.f, tstar = 0.f;
   int j = jstart;  // samples before jstart (and after jend) meet no allocated block: invalid
+  int n_iter = 0, n_skip = 0, n_invalid = 0;
   while (j <= jend) {
+    if (kDebug) ++n_iter;
     const float t = p.dmin + (float)j * p.voxel;
     const float px = fmaf(t, qx, ox), py = fmaf(t, qy, oy), pz = fmaf(t, qz, oz);
     const int bx = (int)floorf(px) >> 3, by = (int)floorf(py) >> 3, bz = (int)floorf(pz) >> 3;
@@ -510,10 +521,12 @@ __global__ void __launch_bounds__(256) k_raycast(VolumeView v, RayParams p, floa
       const float jn = ceilf((texit - p.dmin) / p.voxel - 0.01f);
       j = max(j + 1, (jn <= (float)(p.J + 1)) ? (int)jn : p.J + 1);
       prev_valid = false;
+      if (kDebug) ++n_skip;
       continue;
     }
     float f;
     const bool valid = trilinear<false>(v, c0, px, py, pz, f, nullptr);
+    if (kDebug && !valid) ++n_invalid;
     if (j >= 1 && valid && f <= 0.f) {
       if (prev_valid && prev_f > 0.f) {
         tstar = (p.dmin + (float)(j - 1) * p.voxel) + p.voxel * prev_f / (prev_f - f);
@@ -544,7 +557,11 @@ __global__ void __launch_bounds__(256) k_raycast(VolumeView v, RayParams p, floa
   color_out[3 * pix + 0] = col[0];
   color_out[3 * pix + 1] = col[1];
   color_out[3 * pix + 2] = col[2];
-  if (vertex_out) {
+  if (kDebug) {  // diagnostics (GPS_RAYCAST_DEBUG=1): loop iterations, block skips, invalid samples
+    vertex_out[3 * pix + 0] = (float)n_iter;
+    vertex_out[3 * pix + 1] = (float)n_skip;
+    vertex_out[3 * pix + 2] = (float)n_invalid;
+  } else if (vertex_out) {
     vertex_out[3 * pix + 0] = V[0];
     vertex_out[3 * pix + 1] = V[1];
     vertex_out[3 * pix + 2] = V[2];
@@ -694,7 +711,7 @@ gps_status gps_volume_reset(gps_volume* vol, gps_stream_t stream) {
 }
 
 gps_status gps_volume_stats_sync(gps_volume* vol, gps_stream_t stream, int64_t* n_blocks, int64_t* budget,
-                                 int64_t* n_visible, int64_t* visible_total) {
+                                 int64_t* n_visible, int64_t* visible_total, int64_t* updated_total) {
   if (!vol) return invalid("gps_volume_stats_sync: null volume");
   VolumeImpl* v = static_cast<VolumeImpl*>(vol);
   VolumeCounters c;
@@ -704,6 +721,7 @@ gps_status gps_volume_stats_sync(gps_volume* vol, gps_stream_t stream, int64_t* 
   if (budget) *budget = v->cfg.max_blocks;
   if (n_visible) *n_visible = std::min<int64_t>(c.n_vis, v->cfg.max_blocks);
   if (visible_total) *visible_total = (int64_t)c.vis_total;
+  if (updated_total) *updated_total = (int64_t)c.upd_total;
   if (c.overflow || *(volatile uint32_t*)v->flag.host) {
     set_error("volume block budget exceeded: budget " + std::to_string(v->cfg.max_blocks));
     return GPS_ERR_OUT_OF_BLOCKS;
@@ -791,7 +809,11 @@ gps_status gps_raycast(const gps_volume* vol, const gps_intrinsics* K, const gps
   }
   {
     GPS_PROF(K_RAYCAST, s);
-    k_raycast<<<g, 256, 0, s>>>(v->view, p, depth_out, color_out, vertex_out, tmin, tmax);
+    static const bool dbg = getenv("GPS_RAYCAST_DEBUG") != nullptr;
+    if (dbg && vertex_out)
+      k_raycast<1><<<g, 256, 0, s>>>(v->view, p, depth_out, color_out, vertex_out, tmin, tmax);
+    else
+      k_raycast<0><<<g, 256, 0, s>>>(v->view, p, depth_out, color_out, vertex_out, tmin, tmax);
   }
   GPS_CHECK_LAUNCH("k_raycast");
   return GPS_OK;
