@@ -76,7 +76,7 @@ WsLayout ws_layout(int64_t n, int W, int H, int tile, int64_t cap, int64_t n_par
   L.offsets = take(4 * (tiles + 1));
   L.tile_end = take(4 * tiles);
   L.loss_part = take(4 * tiles);
-  L.records = take(48 * (size_t)std::max<int64_t>(n, 1));
+  L.records = take(64 * (size_t)std::max<int64_t>(n, 1));
   L.grad2d = refine ? take(48 * (size_t)std::max<int64_t>(n, 1)) : 0;
   L.rec3 = refine ? take(128 * (size_t)std::max<int64_t>(n, 1)) : 0;
   L.vals = take(4 * (size_t)cap);
@@ -285,7 +285,7 @@ __device__ __forceinline__ float pair_qmax(float L, float lnsig) {
 // k_preprocess
 // ============================================================================================
 struct SplatPtrs {
-  float4* rec;     // 3 float4 per Gaussian
+  float4* rec;     // 4 float4 per Gaussian
   float4* grad2d;  // 3 float4 per Gaussian (nullable)
   uint32_t* counts;
   WsHeader* hdr;
@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(256) k_preprocess(RenderArgs a, gps_gaussians 
   project_p32(a.cam, a.near_z, a.lowpass, g.xyz + 3 * i, g.log_scale + 3 * i, g.rot + 4 * i, pr);
   if (pr.culled) {
     // an empty rect marks the record as not listed (never read by later kernels)
-    w.rec[3 * i + 1] = make_float4(0.f, 0.f, 0.f, __uint_as_float(0xFFFFu));
+    w.rec[4 * i + 1] = make_float4(0.f, 0.f, 0.f, __uint_as_float(0xFFFFu));
     return;
   }
   SH h;
@@ -319,9 +319,23 @@ __global__ void __launch_bounds__(256) k_preprocess(RenderArgs a, gps_gaussians 
   const float lnsig = (float)(-log1p(exp(-(double)__ldg(&g.opacity_raw[i]))));
   const uint32_t rx = (uint32_t)pr.x0 | ((uint32_t)pr.x1 << 16);
   const uint32_t ry = (uint32_t)pr.y0 | ((uint32_t)pr.y1 << 16);
-  w.rec[3 * i + 0] = make_float4(pr.px, pr.py, pr.ca, pr.cb);
-  w.rec[3 * i + 1] = make_float4(pr.cc, lnsig, pr.X[2], __uint_as_float(rx));
-  w.rec[3 * i + 2] = make_float4(col[0], col[1], col[2], __uint_as_float(ry));
+  // p_hat in double: the backward's value path uses the offset of the exact centre from the
+  // fp32 p_hat that makes the (exact) membership decisions -- fp32 p_hat carries ~1e-4 px of
+  // rounding at x ~ 1000 px, which sign cancellation in a Gaussian's gradient sum would amplify
+  float ddx, ddy;
+  {
+    const double D0 = (double)g.xyz[3 * i] - a.cam.t[0], D1 = (double)g.xyz[3 * i + 1] - a.cam.t[1],
+                 D2 = (double)g.xyz[3 * i + 2] - a.cam.t[2];
+    const double X0 = a.cam.R[0] * D0 + a.cam.R[3] * D1 + a.cam.R[6] * D2;
+    const double X1 = a.cam.R[1] * D0 + a.cam.R[4] * D1 + a.cam.R[7] * D2;
+    const double iz = 1.0 / (a.cam.R[2] * D0 + a.cam.R[5] * D1 + a.cam.R[8] * D2);
+    ddx = (float)((double)a.cam.fx * X0 * iz + (double)a.cam.cx - (double)pr.px);
+    ddy = (float)((double)a.cam.fy * X1 * iz + (double)a.cam.cy - (double)pr.py);
+  }
+  w.rec[4 * i + 0] = make_float4(pr.px, pr.py, pr.ca, pr.cb);
+  w.rec[4 * i + 1] = make_float4(pr.cc, lnsig, pr.X[2], __uint_as_float(rx));
+  w.rec[4 * i + 2] = make_float4(col[0], col[1], col[2], __uint_as_float(ry));
+  w.rec[4 * i + 3] = make_float4(ddx, ddy, 0.f, 0.f);
   const int tx0 = pr.x0 / a.tile, tx1 = pr.x1 / a.tile, ty0 = pr.y0 / a.tile, ty1 = pr.y1 / a.tile;
   for (int ty = ty0; ty <= ty1; ++ty)
     for (int tx = tx0; tx <= tx1; ++tx) atomicAdd(&w.counts[ty * a.tiles_x + tx], 1u);
@@ -385,7 +399,7 @@ __global__ void __launch_bounds__(256) k_emit(RenderArgs a, const float4* __rest
                                               uint32_t* vals) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= a.n) return;
-  const float4 r1 = rec[3 * i + 1], r2 = rec[3 * i + 2];
+  const float4 r1 = rec[4 * i + 1], r2 = rec[4 * i + 2];
   const uint32_t rx = __float_as_uint(r1.w), ry = __float_as_uint(r2.w);
   const int x0 = rx & 0xFFFF, x1 = rx >> 16, y0 = ry & 0xFFFF, y1 = ry >> 16;
   if (x1 < x0) return;  // culled
@@ -464,7 +478,7 @@ __global__ void __launch_bounds__(TILE* TILE) k_sort_blend(RenderArgs a, const f
   if (n <= kMaxList) {
     for (int e = threadIdx.x; e < n; e += NT) {
       const uint32_t idx = vals[start + e];
-      const float d = rec[3 * idx + 1].z;
+      const float d = rec[4 * idx + 1].z;
       skeys[e] = ((uint64_t)__float_as_uint(d) << 32) | idx;
     }
     __syncthreads();
@@ -474,7 +488,7 @@ __global__ void __launch_bounds__(TILE* TILE) k_sort_blend(RenderArgs a, const f
     uint64_t* gk = gkeys + start;
     for (int e = threadIdx.x; e < n; e += NT) {
       const uint32_t idx = vals[start + e];
-      gk[e] = ((uint64_t)__float_as_uint(rec[3 * idx + 1].z) << 32) | idx;
+      gk[e] = ((uint64_t)__float_as_uint(rec[4 * idx + 1].z) << 32) | idx;
     }
     __syncthreads();
     bitonic_sort(gk, n);
@@ -508,7 +522,7 @@ __global__ void __launch_bounds__(TILE* TILE) k_sort_blend(RenderArgs a, const f
       int lo = 0, hi = n;
       while (lo < hi) {
         const int mid = (lo + hi) >> 1;
-        const float d = rec[3 * vals[start + mid] + 1].z;
+        const float d = rec[4 * vals[start + mid] + 1].z;
         if (d >= tmax) hi = mid; else lo = mid + 1;
       }
       n_eff = lo;
@@ -524,10 +538,10 @@ __global__ void __launch_bounds__(TILE* TILE) k_sort_blend(RenderArgs a, const f
     __syncthreads();
     if (threadIdx.x < cnt) {
       const uint32_t idx = vals[start + base + threadIdx.x];
-      const float4 r0 = rec[3 * idx], r1 = rec[3 * idx + 1];
+      const float4 r0 = rec[4 * idx], r1 = rec[4 * idx + 1];
       s0[threadIdx.x] = make_float4(r0.x, r0.y, r0.z, pmul(2.0f, r0.w));
       s1[threadIdx.x] = make_float4(r1.x, r1.y, r1.z, pair_qmax(a.ln_inv_amin, r1.y));
-      s2[threadIdx.x] = rec[3 * idx + 2];
+      s2[threadIdx.x] = rec[4 * idx + 2];
     }
     __syncthreads();
     if (!done) {
@@ -627,6 +641,19 @@ __device__ __forceinline__ void red_add_v4(float4* addr, float a, float b, float
                : "memory");
 }
 
+// one reduce-scatter level: lanes with `mask` set keep the upper half of their NIN values and
+// send the lower half to the partner, which keeps the lower half (padding counts as zero)
+template <int NIN, int NKEEP>
+__device__ __forceinline__ void rs_level(const float* x, float* y, int lane, int mask) {
+  const bool up = lane & mask;
+#pragma unroll
+  for (int k = 0; k < NKEEP; ++k) {
+    const float hi = (NKEEP + k < NIN) ? x[NKEEP + k] : 0.f;
+    const float lo = x[k];
+    y[k] = (up ? hi : lo) + __shfl_xor_sync(0xFFFFFFFFu, up ? lo : hi, mask);
+  }
+}
+
 template <int TILE>
 __global__ void __launch_bounds__(256) k_backward(RenderArgs a, const float4* __restrict__ rec,
                                                   const uint32_t* __restrict__ offsets,
@@ -635,7 +662,7 @@ __global__ void __launch_bounds__(256) k_backward(RenderArgs a, const float4* __
                                                   const float* __restrict__ sdf_depth,
                                                   const float* __restrict__ cstar, const float* __restrict__ wg,
                                                   const uint32_t* __restrict__ target, const WsHeader* hdr,
-                                                  const float* __restrict__ xyz, float4* grad2d) {
+                                                  float* grad2d) {
   constexpr int NP = TILE * TILE;
   __shared__ float sg0[NP], sg1[NP], sg2[NP], ss[NP], slim[NP];
   const int t = blockIdx.x;
@@ -671,73 +698,66 @@ __global__ void __launch_bounds__(256) k_backward(RenderArgs a, const float4* __
   const uint32_t end = min(tile_end[t], a.cap);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int tx0 = tx * TILE, ty0 = ty * TILE;
+  // the lane that ends up holding each reduced value (reduce-scatter below), and which value
+  int vidx;
+  {
+    const int b4 = (lane >> 4) & 1, b3 = (lane >> 3) & 1, b2 = (lane >> 2) & 1, b1 = (lane >> 1) & 1;
+    const int kc = b1;
+    const int kb = b2 ? (2 + kc < 3 ? 2 + kc : -1) : kc;
+    const int ka = kb < 0 ? -1 : (b3 ? (3 + kb < 5 ? 3 + kb : -1) : kb);
+    vidx = (ka < 0 || (lane & 1)) ? -1 : (b4 ? (ka < 4 ? 5 + ka : -1) : ka);
+  }
   for (int e = (int)end - 1 - warp; e >= (int)start; e -= nw) {
     const uint32_t idx = vals[e];
-    const float4 r0 = rec[3 * idx], r1 = rec[3 * idx + 1], r2 = rec[3 * idx + 2];
+    const float4 r0 = rec[4 * idx], r1 = rec[4 * idx + 1], r2 = rec[4 * idx + 2], r3 = rec[4 * idx + 3];
     const float b2 = pmul(2.0f, r0.w), qmax = pair_qmax(a.ln_inv_amin, r1.y);
     const float sig = __expf(r1.y);
-    // p_hat in double, once per entry: the value path uses the offset from the fp32 p_hat that
-    // made the (exact) membership decision.  fp32 p_hat carries ~1e-4 px of rounding at
-    // x ~ 1000 px, which sign cancellation in a Gaussian's gradient sum would amplify.
-    float ddx, ddy;
-    {
-      const double D0 = (double)xyz[3 * idx] - a.cam.t[0], D1 = (double)xyz[3 * idx + 1] - a.cam.t[1],
-                   D2 = (double)xyz[3 * idx + 2] - a.cam.t[2];
-      const double X0 = a.cam.R[0] * D0 + a.cam.R[3] * D1 + a.cam.R[6] * D2;
-      const double X1 = a.cam.R[1] * D0 + a.cam.R[4] * D1 + a.cam.R[7] * D2;
-      const double X2 = a.cam.R[2] * D0 + a.cam.R[5] * D1 + a.cam.R[8] * D2;
-      ddx = (float)((double)a.cam.fx * X0 / X2 + (double)a.cam.cx - (double)r0.x);
-      ddy = (float)((double)a.cam.fy * X1 / X2 + (double)a.cam.cy - (double)r0.y);
-    }
     const uint32_t rx = __float_as_uint(r1.w), ry = __float_as_uint(r2.w);
     const int x0 = max((int)(rx & 0xFFFF), tx0), x1 = min((int)(rx >> 16), tx0 + TILE - 1);
     const int y0 = max((int)(ry & 0xFFFF), ty0), y1 = min((int)(ry >> 16), ty0 + TILE - 1);
     const int wx = x1 - x0 + 1, cnt = wx * (y1 - y0 + 1);
-    float dpx = 0.f, dpy = 0.f, da = 0.f, db = 0.f, dc = 0.f, dsig = 0.f, dr = 0.f, dg = 0.f, dbl = 0.f;
+    // k / wx for k < 256, wx <= 16 as a multiply-high (exact; tests/test_abi.py)
+    const uint32_t magic = (65536u + (uint32_t)wx - 1u) / (uint32_t)wx;
+    float acc[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) acc[k] = 0.f;
     bool any = false;
     for (int k = lane; k < cnt; k += 32) {
-      const int x = x0 + k % wx, y = y0 + k / wx;
+      const int row = (int)(((uint32_t)k * magic) >> 16);
+      const int x = x0 + (k - row * wx), y = y0 + row;
       const int p = (y - ty0) * TILE + (x - tx0);
       if (!(r1.z < slim[p])) continue;  // Eq. 1 indicator (and inactive pixels)
       const float q = pair_q(r0.x, r0.y, r0.z, b2, r1.x, (float)x, (float)y);
       if (!(q <= qmax)) continue;
-      const float dx = ((float)x - r0.x) - ddx, dy = ((float)y - r0.y) - ddy;  // exact offsets
+      const float dx = ((float)x - r0.x) - r3.x, dy = ((float)y - r0.y) - r3.y;  // exact offsets
       const float qv = fmaf(r0.z * dx, dx, fmaf(2.f * r0.w * dx, dy, r1.x * dy * dy));
       const float ex = __expf(-0.5f * qv);
       const float al = sig * ex;
       const float gA0 = sg0[p], gA1 = sg1[p], gA2 = sg2[p];
       // dL/dalpha = A * sum_ch g_ch (c_ch - C*_ch)
       const float dal = gA0 * r2.x + gA1 * r2.y + gA2 * r2.z - ss[p];
-      dr = fmaf(gA0, al, dr);
-      dg = fmaf(gA1, al, dg);
-      dbl = fmaf(gA2, al, dbl);
-      dsig = fmaf(dal, ex, dsig);
       const float dpow = -al * dal;
-      da = fmaf(dpow * 0.5f, dx * dx, da);
-      db = fmaf(dpow, dx * dy, db);
-      dc = fmaf(dpow * 0.5f, dy * dy, dc);
-      dpx = fmaf(-dpow, r0.z * dx + r0.w * dy, dpx);
-      dpy = fmaf(-dpow, r0.w * dx + r1.x * dy, dpy);
+      acc[0] = fmaf(-dpow, r0.z * dx + r0.w * dy, acc[0]);  // p_hat x
+      acc[1] = fmaf(-dpow, r0.w * dx + r1.x * dy, acc[1]);  // p_hat y
+      acc[2] = fmaf(dpow * 0.5f, dx * dx, acc[2]);           // conic a
+      acc[3] = fmaf(dpow, dx * dy, acc[3]);                  // conic b
+      acc[4] = fmaf(dpow * 0.5f, dy * dy, acc[4]);           // conic c
+      acc[5] = fmaf(dal, ex, acc[5]);                        // sigma
+      acc[6] = fmaf(gA0, al, acc[6]);                        // colour r, g, b
+      acc[7] = fmaf(gA1, al, acc[7]);
+      acc[8] = fmaf(gA2, al, acc[8]);
       any = true;
     }
     if (!__any_sync(0xFFFFFFFFu, any)) continue;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      dpx += __shfl_xor_sync(0xFFFFFFFFu, dpx, o);
-      dpy += __shfl_xor_sync(0xFFFFFFFFu, dpy, o);
-      da += __shfl_xor_sync(0xFFFFFFFFu, da, o);
-      db += __shfl_xor_sync(0xFFFFFFFFu, db, o);
-      dc += __shfl_xor_sync(0xFFFFFFFFu, dc, o);
-      dsig += __shfl_xor_sync(0xFFFFFFFFu, dsig, o);
-      dr += __shfl_xor_sync(0xFFFFFFFFu, dr, o);
-      dg += __shfl_xor_sync(0xFFFFFFFFu, dg, o);
-      dbl += __shfl_xor_sync(0xFFFFFFFFu, dbl, o);
-    }
-    if (lane == 0) {
-      red_add_v4(grad2d + 3 * idx, dpx, dpy, da, db);
-      red_add_v4(grad2d + 3 * idx + 1, dc, dsig, dr, dg);
-      atomicAdd(reinterpret_cast<float*>(grad2d + 3 * idx + 2), dbl);
-    }
+    // warp reduce-scatter: 12 shuffles instead of 45; value k ends on one even lane
+    float l1[5], l2[3], l3[2], l4[1];
+    rs_level<9, 5>(acc, l1, lane, 16);
+    rs_level<5, 3>(l1, l2, lane, 8);
+    rs_level<3, 2>(l2, l3, lane, 4);
+    rs_level<2, 1>(l3, l4, lane, 2);
+    const float tot = l4[0] + __shfl_xor_sync(0xFFFFFFFFu, l4[0], 1);
+    // 2D gradient slot layout: [px, py, a, b | c, sigma, r, g | b, flag, -, -]
+    if (vidx >= 0) atomicAdd(grad2d + 12 * (size_t)idx + vidx, tot);
   }
 }
 
@@ -1271,10 +1291,10 @@ gps_status gps_refine_step(gps_gaussians* g, gps_adam_state* state, const gps_vi
     GPS_PROF(K_BACKWARD, s);
     if (rcfg->tile == 16)
       k_backward<16><<<n_tiles, 256, 0, s>>>(a, rec, offsets, vals, tend, vw.sdf_depth, cstar, wg, tgt, hdr,
-                                             g->xyz, grad2d);
+                                             reinterpret_cast<float*>(grad2d));
     else
       k_backward<8><<<n_tiles, 256, 0, s>>>(a, rec, offsets, vals, tend, vw.sdf_depth, cstar, wg, tgt, hdr,
-                                            g->xyz, grad2d);
+                                            reinterpret_cast<float*>(grad2d));
     }
     GPS_CHECK_LAUNCH("k_backward");
     if (g->n > 0) {

@@ -328,6 +328,7 @@ struct RayParams {
   int W, H;
   float R[9], t[3];
   float voxel, inv_voxel, dmin;
+  float zc;  // smallest camera z of any ray sample: dmin * min over pixels of the unit ray's z
   int J;  // last grid index
 };
 
@@ -362,36 +363,47 @@ __global__ void __launch_bounds__(256) k_range(VolumeView v, RayParams p, uint32
       d2max += df * df;
     }
     const float t0 = sqrtf(d2min) * 0.9999f, t1 = sqrtf(d2max) * 1.0001f + 1e-4f;
-    // projected footprint (bbox of the 8 projected corners if all are in front of the camera)
-    float umin = INFINITY, umax = -INFINITY, vmin = INFINITY, vmax = -INFINITY;
-    bool all_front = true, any_front = false;
+    // projected footprint of the box clipped to z >= zc (no ray sample has camera z < zc): the
+    // bbox of the projections of its corners in front and of its edges' crossings of z = zc
+    float C[8][3];
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       const float P0 = (c & 1 ? hi[0] : lo[0]) - p.t[0];
       const float P1 = (c & 2 ? hi[1] : lo[1]) - p.t[1];
       const float P2 = (c & 4 ? hi[2] : lo[2]) - p.t[2];
-      const float X = p.R[0] * P0 + p.R[3] * P1 + p.R[6] * P2;
-      const float Y = p.R[1] * P0 + p.R[4] * P1 + p.R[7] * P2;
-      const float Z = p.R[2] * P0 + p.R[5] * P1 + p.R[8] * P2;
-      if (Z > 1e-3f) {
-        any_front = true;
-        const float iz = 1.0f / Z;
-        const float u = p.fx * X * iz + p.cx, w = p.fy * Y * iz + p.cy;
-        umin = fminf(umin, u); umax = fmaxf(umax, u);
-        vmin = fminf(vmin, w); vmax = fmaxf(vmax, w);
-      } else {
-        all_front = false;
+      C[c][0] = p.R[0] * P0 + p.R[3] * P1 + p.R[6] * P2;
+      C[c][1] = p.R[1] * P0 + p.R[4] * P1 + p.R[7] * P2;
+      C[c][2] = p.R[2] * P0 + p.R[5] * P1 + p.R[8] * P2;
+    }
+    float umin = INFINITY, umax = -INFINITY, vmin = INFINITY, vmax = -INFINITY;
+    const float zc = p.zc;
+    auto add = [&](float X, float Y, float Z) {
+      const float iz = 1.0f / Z;
+      const float u = p.fx * X * iz + p.cx, w = p.fy * Y * iz + p.cy;
+      umin = fminf(umin, u); umax = fmaxf(umax, u);
+      vmin = fminf(vmin, w); vmax = fmaxf(vmax, w);
+    };
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      if (C[c][2] >= zc) add(C[c][0], C[c][1], C[c][2]);
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+#pragma unroll
+      for (int bit = 1; bit < 8; bit <<= 1) {
+        const int d = c | bit;
+        if (d == c) continue;  // each edge once (c has the bit clear)
+        const float za = C[c][2], zb = C[d][2];
+        if ((za < zc) != (zb < zc)) {
+          const float s = (zc - za) / (zb - za);
+          add(C[c][0] + s * (C[d][0] - C[c][0]), C[c][1] + s * (C[d][1] - C[c][1]), zc);
+        }
       }
-    }
-    if (!any_front) continue;  // entirely behind the camera plane: no ray meets it
-    int tx0 = 0, tx1 = tiles_x - 1, ty0 = 0, ty1 = tiles_y - 1;
-    if (all_front) {
-      if (umax < -1.f || vmax < -1.f || umin > p.W || vmin > p.H) continue;
-      tx0 = max(0, (int)floorf((umin - 1.f) / kRangeTile));
-      tx1 = min(tiles_x - 1, (int)floorf((umax + 1.f) / kRangeTile));
-      ty0 = max(0, (int)floorf((vmin - 1.f) / kRangeTile));
-      ty1 = min(tiles_y - 1, (int)floorf((vmax + 1.f) / kRangeTile));
-    }
+    if (!(umin <= umax)) continue;  // entirely nearer than any sample: no ray meets it
+    if (umax < -1.f || vmax < -1.f || umin > p.W || vmin > p.H) continue;
+    const int tx0 = max(0, (int)floorf((fmaxf(umin, -2.f) - 1.f) / kRangeTile));
+    const int tx1 = min(tiles_x - 1, (int)floorf((fminf(umax, (float)p.W + 2.f) + 1.f) / kRangeTile));
+    const int ty0 = max(0, (int)floorf((fmaxf(vmin, -2.f) - 1.f) / kRangeTile));
+    const int ty1 = min(tiles_y - 1, (int)floorf((fminf(vmax, (float)p.H + 2.f) + 1.f) / kRangeTile));
     const uint32_t a0 = __float_as_uint(t0), a1 = __float_as_uint(t1);
     for (int ty = ty0; ty <= ty1; ++ty)
       for (int tx = tx0; tx <= tx1; ++tx) {
@@ -791,6 +803,12 @@ gps_status gps_raycast(const gps_volume* vol, const gps_intrinsics* K, const gps
   p.inv_voxel = 1.0f / v->cfg.voxel_size;
   p.dmin = v->cfg.depth_min;
   p.J = (int)std::floor(((double)v->cfg.depth_max - (double)v->cfg.depth_min) / (double)v->cfg.voxel_size);
+  {
+    // the unit ray's z is smallest at an image corner; 0.99 keeps the bound conservative in fp32
+    const double ex = std::max(std::fabs(0.0 - K->cx), std::fabs((double)(K->width - 1) - K->cx)) / K->fx;
+    const double ey = std::max(std::fabs(0.0 - K->cy), std::fabs((double)(K->height - 1) - K->cy)) / K->fy;
+    p.zc = (float)(0.99 * (double)v->cfg.depth_min / std::sqrt(1.0 + ex * ex + ey * ey));
+  }
   dim3 g((p.W + 15) / 16, (p.H + 15) / 16);
   cudaStream_t s = as_stream(stream);
   const int ntiles = (int)(g.x * g.y);

@@ -51,3 +51,12 @@ def test_colour_mean_magic_division_is_exact():
         M32 = np.uint32((np.uint32(0xFFFFFFFF) // np.uint32(d)) + np.uint32(1))  # u32 as on device
         assert int(M32) == -(-(1 << 32) // d)
         assert np.array_equal((n * np.uint64(M32)) >> np.uint64(32), n // np.uint64(d)), d
+
+
+def test_footprint_walk_division_is_exact():
+    """k_backward maps lane index k < 256 of a w <= 16 wide footprint to (k / w, k % w) with
+    (k * ceil(2^16 / w)) >> 16; exhaustively exact."""
+    for w in range(1, 17):
+        magic = (65536 + w - 1) // w
+        for k in range(256):
+            assert (k * magic) >> 16 == k // w, (w, k)
