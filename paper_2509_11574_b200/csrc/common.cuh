@@ -40,8 +40,11 @@ __device__ __forceinline__ float pdot3(float a0, float b0, float a1, float b1, f
   return padd(padd(pmul(a0, b0), pmul(a1, b1)), pmul(a2, b2));
 }
 
-// ---- voxel-block hash -------------------------------------------------------
-// Voxel: 8 bytes, {f32 tsdf; u8 r, g, b, w}; block = 8^3 voxels, index i + 8j + 64k.
+// ---- voxel-block hash ----------------------------------------------------------
+// Voxel: {f32 tsdf; u8 r, g, b, w}, block = 8^3 voxels, index i + 8j + 64k.  In HBM the pool is
+// two planes: tsdf[block][512] (4 B; an unobserved voxel (w = 0) holds a quiet NaN, so the march
+// reads only this plane and "valid" is "not NaN") and rgbw[block][512] (4 B).  Voxel is the
+// interleaved form used by the debug export (NaN shown as the R-VOX initial tsdf 1).
 struct __align__(8) Voxel {
   float tsdf;
   uint32_t rgbw;  // r | g<<8 | b<<16 | w<<24
@@ -80,7 +83,8 @@ struct VolumeView {  // passed by value to kernels
   uint64_t* keys;
   int32_t* vals;  // pool block index, -1 = none
   uint32_t* stamp;
-  Voxel* pool;
+  float* tsdf;     // pool plane: tsdf[b * 512 + idx], NaN = unobserved
+  uint32_t* rgbw;  // pool plane: r | g<<8 | b<<16 | w<<24
   int32_t* vis;  // visible slots
   uint64_t* bkeys;  // pool block index -> packed block key (for passes over all blocks)
   int32_t* nbr;     // pool block index -> 8 pool indices of the blocks at +(dx,dy,dz), dx,dy,dz in

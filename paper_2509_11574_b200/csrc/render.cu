@@ -531,6 +531,8 @@ __global__ void __launch_bounds__(TILE* TILE) k_sort_blend(RenderArgs a, const f
   }
   if (threadIdx.x == 0) tile_end[t] = start + n_eff;
   // ---- front-to-back blend, Eqs. 1-3, early termination at the SDF depth ----
+  constexpr int kWarpRows = 32 / TILE;  // pixel rows covered by one warp
+  const int wy0 = ty * TILE + (threadIdx.x >> 5) * kWarpRows, wy1 = wy0 + kWarpRows - 1;
   float W = 0.f, C0 = 0.f, C1 = 0.f, C2 = 0.f;
   bool done = !inside;
   for (int base = 0; base < n_eff; base += NT) {
@@ -546,6 +548,9 @@ __global__ void __launch_bounds__(TILE* TILE) k_sort_blend(RenderArgs a, const f
     __syncthreads();
     if (!done) {
       for (int k = 0; k < cnt; ++k) {
+        // warp-uniform row cull: the warp's pixels are rows [wy0, wy0 + rows) of the image
+        const uint32_t ry = __float_as_uint(s2[k].w);
+        if ((int)(ry >> 16) < wy0 || (int)(ry & 0xFFFFu) > wy1) continue;
         const float4 r1 = s1[k];
         if (!(r1.z < lim)) {  // sorted by depth: every later entry fails Eq. 1's indicator too
           done = true;

@@ -210,7 +210,8 @@ __device__ __forceinline__ uint2 voxel_update(float tsdf, uint32_t cw, float s, 
                                               const uint32_t* __restrict__ smagic) {
   const uint32_t w = cw >> 24;
   const float wf = (float)w;
-  const float t = pmul(padd(pmul(tsdf, wf), s), __frcp_rn(padd(wf, 1.0f)));
+  // w = 0: the stored NaN stands for the initial tsdf 1, and (1*0 + s) * (1/1) = s exactly
+  const float t = w == 0 ? s : pmul(padd(pmul(tsdf, wf), s), __frcp_rn(padd(wf, 1.0f)));
   const uint32_t w1 = w + 1, half = w1 >> 1, magic = smagic[w];
   uint32_t out;
   if (w == 0) {
@@ -252,19 +253,22 @@ __global__ void __launch_bounds__(256) k_integrate(VolumeView v, FuseParams p,
     const bool u0 = voxel_sample(p, gx, gy, gz, depth, pix0, s0);
     const bool u1 = voxel_sample(p, gx + 1, gy, gz, depth, pix1, s1);
     if (u0 | u1) {  // a voxel pair nobody observes costs no load and no store
-      float4* ptr = reinterpret_cast<float4*>(v.pool + (size_t)b * 512 + e);
-      float4 raw = *ptr;
+      float2* tp = reinterpret_cast<float2*>(v.tsdf + (size_t)b * 512 + e);
+      uint2* cp = reinterpret_cast<uint2*>(v.rgbw + (size_t)b * 512 + e);
+      float2 ts = *tp;
+      uint2 cw = *cp;
       if (u0) {
-        const uint2 r = voxel_update(raw.x, __float_as_uint(raw.y), s0, __ldg(&rgba[pix0]), p.wmax, smagic);
-        raw.x = __uint_as_float(r.x);
-        raw.y = __uint_as_float(r.y);
+        const uint2 r = voxel_update(ts.x, cw.x, s0, __ldg(&rgba[pix0]), p.wmax, smagic);
+        ts.x = __uint_as_float(r.x);
+        cw.x = r.y;
       }
       if (u1) {
-        const uint2 r = voxel_update(raw.z, __float_as_uint(raw.w), s1, __ldg(&rgba[pix1]), p.wmax, smagic);
-        raw.z = __uint_as_float(r.x);
-        raw.w = __uint_as_float(r.y);
+        const uint2 r = voxel_update(ts.y, cw.y, s1, __ldg(&rgba[pix1]), p.wmax, smagic);
+        ts.y = __uint_as_float(r.x);
+        cw.y = r.y;
       }
-      *ptr = raw;
+      *tp = ts;
+      *cp = cw;
       n_upd += (uint32_t)u0 + (uint32_t)u1;
     }
   }
@@ -305,11 +309,11 @@ __global__ void __launch_bounds__(256) k_link(VolumeView v) {
   }
 }
 
-__global__ void k_fill_pool(Voxel* pool, size_t n) {
+__global__ void k_fill_pool(float* tsdf, uint32_t* rgbw, size_t n) {
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += stride) {
-    pool[i].tsdf = 1.0f;
-    pool[i].rgbw = 0u;
+    tsdf[i] = __uint_as_float(0x7FC00000u);  // unobserved (R-VOX initial tsdf 1, w = 0)
+    rgbw[i] = 0u;
   }
 }
 
@@ -442,7 +446,8 @@ __device__ __forceinline__ bool trilinear(const VolumeView& v, BlockCache& c0, f
   // select b0 itself (entry 0)
   const int4 n0 = reinterpret_cast<const int4*>(v.nbr)[2 * (size_t)b0];
   const int4 n1 = reinterpret_cast<const int4*>(v.nbr)[2 * (size_t)b0 + 1];
-  Voxel vx[8];
+  float tv[8];
+  size_t addr[8];
   bool ok = true;
 #pragma unroll
   for (int corner = 0; corner < 8; ++corner) {
@@ -452,23 +457,28 @@ __device__ __forceinline__ bool trilinear(const VolumeView& v, BlockCache& c0, f
                          : (sy ? (sx ? n0.w : n0.z) : (sx ? n0.y : b0));
     ok &= b >= 0;
     const int idx = ((lx + dx) & 7) + 8 * ((ly + dy) & 7) + 64 * ((lz + dz) & 7);
-    vx[corner] = v.pool[(size_t)max(b, 0) * 512 + idx];
+    addr[corner] = (size_t)max(b, 0) * 512 + idx;
+    tv[corner] = v.tsdf[addr[corner]];
   }
-  uint32_t wmin = vx[0].rgbw;
+  // an unallocated corner, or an unobserved one (NaN): the sample is invalid
+  float chk = tv[0];
 #pragma unroll
-  for (int corner = 1; corner < 8; ++corner) wmin = min(wmin, vx[corner].rgbw);
-  if (!ok || (wmin >> 24) == 0u) return false;  // an unallocated corner, or w = 0
+  for (int corner = 1; corner < 8; ++corner) chk += tv[corner];
+  if (!ok || isnan(chk)) return false;
   // trilinear as nested lerps (x, then y, then z)
   auto lerp = [](float a, float b, float t) { return fmaf(t, b - a, a); };
-  const float x00 = lerp(vx[0].tsdf, vx[1].tsdf, ax), x10 = lerp(vx[2].tsdf, vx[3].tsdf, ax);
-  const float x01 = lerp(vx[4].tsdf, vx[5].tsdf, ax), x11 = lerp(vx[6].tsdf, vx[7].tsdf, ax);
+  const float x00 = lerp(tv[0], tv[1], ax), x10 = lerp(tv[2], tv[3], ax);
+  const float x01 = lerp(tv[4], tv[5], ax), x11 = lerp(tv[6], tv[7], ax);
   f = lerp(lerp(x00, x10, ay), lerp(x01, x11, ay), az);
   if (kColor) {
+    uint32_t cw[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) cw[k] = v.rgbw[addr[k]];
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch) {
       float c[8];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) c[k] = (float)((vx[k].rgbw >> (8 * ch)) & 0xFFu);
+      for (int k = 0; k < 8; ++k) c[k] = (float)((cw[k] >> (8 * ch)) & 0xFFu);
       col[ch] = lerp(lerp(lerp(c[0], c[1], ax), lerp(c[2], c[3], ax), ay),
                      lerp(lerp(c[4], c[5], ax), lerp(c[6], c[7], ax), ay), az);
     }
@@ -593,8 +603,11 @@ __global__ void k_export_blocks(VolumeView v, int32_t* coords, Voxel* voxels, ui
     unpack_block(k, x, y, z);
     coords[3 * i] = x; coords[3 * i + 1] = y; coords[3 * i + 2] = z;
     if (voxels) {
-      const Voxel* src = v.pool + (size_t)v.vals[s] * 512;
-      for (int e = 0; e < 512; ++e) voxels[(size_t)i * 512 + e] = src[e];
+      const size_t base = (size_t)v.vals[s] * 512;
+      for (int e = 0; e < 512; ++e) {
+        const float t = v.tsdf[base + e];
+        voxels[(size_t)i * 512 + e] = Voxel{isnan(t) ? 1.0f : t, v.rgbw[base + e]};
+      }
     }
   }
 }
@@ -644,7 +657,7 @@ gps_status fill_volume(VolumeImpl* v, cudaStream_t s) {
   GPS_CHECK_LAUNCH("k_fill_u64");
   GPS_CHECK_CUDA(cudaMemsetAsync(v->view.vals, 0xFF, sizeof(int32_t) * c.hash_slots, s));
   GPS_CHECK_CUDA(cudaMemsetAsync(v->view.stamp, 0xFF, sizeof(uint32_t) * c.hash_slots, s));
-  k_fill_pool<<<1184, 256, 0, s>>>(v->view.pool, (size_t)c.max_blocks * 512);
+  k_fill_pool<<<1184, 256, 0, s>>>(v->view.tsdf, v->view.rgbw, (size_t)c.max_blocks * 512);
   GPS_CHECK_LAUNCH("k_fill_pool");
   GPS_CHECK_CUDA(cudaMemsetAsync(v->view.ctr, 0, sizeof(VolumeCounters), s));
   *(volatile uint32_t*)v->flag.host = 0u;
@@ -676,7 +689,8 @@ gps_status gps_volume_create(const gps_volume_config* cfg, gps_stream_t stream, 
   bool ok = cudaMalloc(&v->view.keys, sizeof(uint64_t) * slots) == cudaSuccess &&
             cudaMalloc(&v->view.vals, sizeof(int32_t) * slots) == cudaSuccess &&
             cudaMalloc(&v->view.stamp, sizeof(uint32_t) * slots) == cudaSuccess &&
-            cudaMalloc(&v->view.pool, sizeof(Voxel) * 512 * nb) == cudaSuccess &&
+            cudaMalloc(&v->view.tsdf, sizeof(float) * 512 * nb) == cudaSuccess &&
+            cudaMalloc(&v->view.rgbw, sizeof(uint32_t) * 512 * nb) == cudaSuccess &&
             cudaMalloc(&v->view.vis, sizeof(int32_t) * nb) == cudaSuccess &&
             cudaMalloc(&v->view.bkeys, sizeof(uint64_t) * nb) == cudaSuccess &&
             cudaMalloc(&v->view.nbr, sizeof(int32_t) * 8 * nb) == cudaSuccess &&
@@ -707,7 +721,8 @@ void gps_volume_destroy(gps_volume* vol) {
   cudaFree(v->view.keys);
   cudaFree(v->view.vals);
   cudaFree(v->view.stamp);
-  cudaFree(v->view.pool);
+  cudaFree(v->view.tsdf);
+  cudaFree(v->view.rgbw);
   cudaFree(v->view.vis);
   cudaFree(v->view.bkeys);
   cudaFree(v->view.nbr);
