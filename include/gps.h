@@ -249,6 +249,12 @@ gps_status gps_render_stats_sync(const void* ws, gps_stream_t stream, int64_t* n
 gps_status gps_debug_export_blocks_sync(const gps_volume* vol, gps_stream_t stream,
                                         int32_t* coords, void* voxels, int64_t cap,
                                         int64_t* n /*host*/);
+/* Runs gps_raycast for (K, T) into temporary buffers while marking every tsdf voxel the march
+ * reads; *unique_voxels (host) = their number.  Measures the raycast roofline's unit count
+ * (4 bytes per unique voxel read + 16 bytes of output per pixel).  Allocates; debug only.     */
+gps_status gps_debug_raycast_footprint_sync(const gps_volume* vol, const gps_intrinsics* K /*host*/,
+                                            const gps_pose* T /*host*/, gps_stream_t stream,
+                                            int64_t* unique_voxels /*host*/);
 /* Copies the block coords marked visible by the last gps_fuse (any order).                  */
 gps_status gps_debug_export_visible_sync(const gps_volume* vol, gps_stream_t stream,
                                          int32_t* coords, int64_t cap, int64_t* n /*host*/);

@@ -85,6 +85,7 @@ PROTOTYPES = {
     "gps_render_stats_sync": (gps_status, [vp, gps_stream_t, P(i64), P(i64), P(i64)]),
     "gps_debug_export_blocks_sync": (gps_status, [vp, gps_stream_t, vp, vp, i64, P(i64)]),
     "gps_debug_export_visible_sync": (gps_status, [vp, gps_stream_t, vp, i64, P(i64)]),
+    "gps_debug_raycast_footprint_sync": (gps_status, [vp, P(gps_intrinsics), P(gps_pose), gps_stream_t, P(i64)]),
     "gps_debug_render_lists_sync": (gps_status, [vp, gps_stream_t, vp, i64, vp, P(i64)]),
     "gps_profile_enable": (None, [C.c_int]),
     "gps_profile_read_sync": (C.c_int, [C.c_char_p, C.c_int, P(C.c_double), P(i64), C.c_int]),

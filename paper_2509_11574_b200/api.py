@@ -138,6 +138,14 @@ class Volume:
             v = vox[:k].cpu().numpy().view(VOXEL_DTYPE).reshape(k, 512)
         return c, v
 
+    def raycast_footprint(self, cam: Camera, R, t, stream=None) -> int:
+        """Number of distinct tsdf voxels a raycast from (R, t) reads (debug; synchronises)."""
+        n = C.c_int64()
+        N.check("gps_debug_raycast_footprint_sync",
+                _L.gps_debug_raycast_footprint_sync(self.h, C.byref(cam.c()), C.byref(pose_struct(R, t)),
+                                                   _stream(stream), C.byref(n)))
+        return n.value
+
     def export_visible(self, stream=None):
         cap = int(self.cfg.max_blocks)
         coords = torch.empty((cap, 3), dtype=torch.int32, device="cuda")

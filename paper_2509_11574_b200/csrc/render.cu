@@ -418,19 +418,23 @@ __global__ void __launch_bounds__(256) k_emit(RenderArgs a, const float4* __rest
 // ============================================================================================
 template <typename Keys>
 __device__ __forceinline__ void bitonic_sort(Keys keys, int n) {
-  int P = 1;
-  while (P < n) P <<= 1;
-  for (int k = 2; k <= P; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
+  int P = 1, lgP = 0;
+  while (P < n) {
+    P <<= 1;
+    ++lgP;
+  }
+  for (int lk = 1; lk <= lgP; ++lk) {
+    const int k = 1 << lk;
+    for (int lj = lk - 1; lj >= 0; --lj) {
+      const int j = 1 << lj;  // powers of two: block/offset by shift and mask
       for (int c = threadIdx.x; c < (P >> 1); c += blockDim.x) {
+        const int blk = c >> lj, off = c & (j - 1);
         int lo, hi;
-        if (j == (k >> 1)) {
-          const int blk = c / j, off = c % j;
-          lo = blk * k + off;
-          hi = blk * k + k - 1 - off;
+        if (lj == lk - 1) {
+          lo = (blk << lk) + off;
+          hi = (blk << lk) + k - 1 - off;
         } else {
-          const int blk = c / j, off = c % j;
-          lo = blk * 2 * j + off;
+          lo = (blk << (lj + 1)) + off;
           hi = lo + j;
         }
         if (hi < n) {

@@ -431,9 +431,9 @@ __device__ __forceinline__ int32_t cached_find(const VolumeView& v, BlockCache& 
 }
 
 // trilinear tsdf (and colour) at voxel-unit position p; returns validity
-template <bool kColor>
+template <bool kColor, bool kFoot = false>
 __device__ __forceinline__ bool trilinear(const VolumeView& v, BlockCache& c0, float px, float py, float pz,
-                                          float& f, float* col) {
+                                          float& f, float* col, uint32_t* footprint = nullptr) {
   const float fx = floorf(px), fy = floorf(py), fz = floorf(pz);
   const int gx = (int)fx, gy = (int)fy, gz = (int)fz;
   const float ax = px - fx, ay = py - fy, az = pz - fz;
@@ -459,6 +459,7 @@ __device__ __forceinline__ bool trilinear(const VolumeView& v, BlockCache& c0, f
     const int idx = ((lx + dx) & 7) + 8 * ((ly + dy) & 7) + 64 * ((lz + dz) & 7);
     addr[corner] = (size_t)max(b, 0) * 512 + idx;
     tv[corner] = v.tsdf[addr[corner]];
+    if (kFoot && b >= 0) atomicOr(&footprint[addr[corner] >> 5], 1u << (addr[corner] & 31));
   }
   // an unallocated corner, or an unobserved one (NaN): the sample is invalid
   float chk = tv[0];
@@ -486,12 +487,15 @@ __device__ __forceinline__ bool trilinear(const VolumeView& v, BlockCache& c0, f
   return true;
 }
 
+// kDebug: 0 = production; 1 = per-pixel march statistics in vertex_out; 2 = mark every tsdf voxel
+// the march reads in `footprint` (the raycast roofline's unique-voxel count)
 template <int kDebug>
 __global__ void __launch_bounds__(256) k_raycast(VolumeView v, RayParams p, float* __restrict__ depth_out,
                                                  float* __restrict__ color_out,
                                                  float* __restrict__ vertex_out,
                                                  const uint32_t* __restrict__ tmin,
-                                                 const uint32_t* __restrict__ tmax) {
+                                                 const uint32_t* __restrict__ tmax,
+                                                 uint32_t* footprint = nullptr) {
   const int u = blockIdx.x * 16 + (threadIdx.x & 15);
   const int vv = blockIdx.y * 16 + (threadIdx.x >> 4);
   if (u >= p.W || vv >= p.H) return;
@@ -547,7 +551,7 @@ __global__ void __launch_bounds__(256) k_raycast(VolumeView v, RayParams p, floa
       continue;
     }
     float f;
-    const bool valid = trilinear<false>(v, c0, px, py, pz, f, nullptr);
+    const bool valid = trilinear<false, kDebug == 2>(v, c0, px, py, pz, f, nullptr, footprint);
     if (kDebug && !valid) ++n_invalid;
     if (j >= 1 && valid && f <= 0.f) {
       if (prev_valid && prev_f > 0.f) {
@@ -579,7 +583,7 @@ __global__ void __launch_bounds__(256) k_raycast(VolumeView v, RayParams p, floa
   color_out[3 * pix + 0] = col[0];
   color_out[3 * pix + 1] = col[1];
   color_out[3 * pix + 2] = col[2];
-  if (kDebug) {  // diagnostics (GPS_RAYCAST_DEBUG=1): loop iterations, block skips, invalid samples
+  if (kDebug == 1) {  // diagnostics (GPS_RAYCAST_DEBUG=1): loop iterations, block skips, invalid samples
     vertex_out[3 * pix + 0] = (float)n_iter;
     vertex_out[3 * pix + 1] = (float)n_skip;
     vertex_out[3 * pix + 2] = (float)n_invalid;
@@ -588,6 +592,15 @@ __global__ void __launch_bounds__(256) k_raycast(VolumeView v, RayParams p, floa
     vertex_out[3 * pix + 1] = V[1];
     vertex_out[3 * pix + 2] = V[2];
   }
+}
+
+__global__ void k_popcount(const uint32_t* __restrict__ words, size_t n, unsigned long long* total) {
+  unsigned long long s = 0;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    s += __popc(words[i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
+  if ((threadIdx.x & 31) == 0 && s) atomicAdd(total, s);
 }
 
 // ---- debug export ----------------------------------------------------------------------------
@@ -803,12 +816,8 @@ gps_status gps_fuse(gps_volume* vol, const gps_intrinsics* K, const gps_pose* T,
   return GPS_OK;
 }
 
-gps_status gps_raycast(const gps_volume* vol, const gps_intrinsics* K, const gps_pose* T, float* depth_out,
-                       float* color_out, float* vertex_out, gps_stream_t stream) {
-  if (!vol || !T || !depth_out || !color_out) return invalid("gps_raycast: null argument");
-  if (!valid_intrinsics(K)) return invalid("gps_raycast: bad intrinsics");
-  gps_status st = check_sticky(vol);
-  if (st != GPS_OK) return st;
+static gps_status raycast_impl(const gps_volume* vol, const gps_intrinsics* K, const gps_pose* T, float* depth_out,
+                               float* color_out, float* vertex_out, uint32_t* footprint, gps_stream_t stream) {
   const VolumeImpl* v = static_cast<const VolumeImpl*>(vol);
   RayParams p;
   p.fx = K->fx; p.fy = K->fy; p.cx = K->cx; p.cy = K->cy; p.W = K->width; p.H = K->height;
@@ -843,12 +852,52 @@ gps_status gps_raycast(const gps_volume* vol, const gps_intrinsics* K, const gps
   {
     GPS_PROF(K_RAYCAST, s);
     static const bool dbg = getenv("GPS_RAYCAST_DEBUG") != nullptr;
-    if (dbg && vertex_out)
+    if (footprint)
+      k_raycast<2><<<g, 256, 0, s>>>(v->view, p, depth_out, color_out, nullptr, tmin, tmax, footprint);
+    else if (dbg && vertex_out)
       k_raycast<1><<<g, 256, 0, s>>>(v->view, p, depth_out, color_out, vertex_out, tmin, tmax);
     else
       k_raycast<0><<<g, 256, 0, s>>>(v->view, p, depth_out, color_out, vertex_out, tmin, tmax);
   }
   GPS_CHECK_LAUNCH("k_raycast");
+  return GPS_OK;
+}
+
+gps_status gps_raycast(const gps_volume* vol, const gps_intrinsics* K, const gps_pose* T, float* depth_out,
+                       float* color_out, float* vertex_out, gps_stream_t stream) {
+  if (!vol || !T || !depth_out || !color_out) return invalid("gps_raycast: null argument");
+  if (!valid_intrinsics(K)) return invalid("gps_raycast: bad intrinsics");
+  gps_status st = check_sticky(vol);
+  if (st != GPS_OK) return st;
+  return raycast_impl(vol, K, T, depth_out, color_out, vertex_out, nullptr, stream);
+}
+
+gps_status gps_debug_raycast_footprint_sync(const gps_volume* vol, const gps_intrinsics* K, const gps_pose* T,
+                                            gps_stream_t stream, int64_t* unique_voxels) {
+  if (!vol || !T || !unique_voxels || !valid_intrinsics(K)) return invalid("gps_debug_raycast_footprint_sync: bad argument");
+  const VolumeImpl* v = static_cast<const VolumeImpl*>(vol);
+  cudaStream_t s = as_stream(stream);
+  const size_t words = ((size_t)v->cfg.max_blocks * 512 + 31) / 32;
+  const size_t px = (size_t)K->width * K->height;
+  uint32_t* bm = nullptr;
+  float* buf = nullptr;
+  unsigned long long* cnt = nullptr;
+  GPS_CHECK_CUDA(cudaMallocAsync(&bm, words * 4, s));
+  GPS_CHECK_CUDA(cudaMallocAsync(&buf, px * 16, s));
+  GPS_CHECK_CUDA(cudaMallocAsync(&cnt, 8, s));
+  GPS_CHECK_CUDA(cudaMemsetAsync(bm, 0, words * 4, s));
+  GPS_CHECK_CUDA(cudaMemsetAsync(cnt, 0, 8, s));
+  gps_status st = raycast_impl(vol, K, T, buf, buf + px, nullptr, bm, stream);
+  if (st != GPS_OK) return st;
+  k_popcount<<<592, 256, 0, s>>>(bm, words, cnt);
+  GPS_CHECK_LAUNCH("k_popcount");
+  unsigned long long h = 0;
+  GPS_CHECK_CUDA(cudaMemcpyAsync(&h, cnt, 8, cudaMemcpyDeviceToHost, s));
+  GPS_CHECK_CUDA(cudaFreeAsync(bm, s));
+  GPS_CHECK_CUDA(cudaFreeAsync(buf, s));
+  GPS_CHECK_CUDA(cudaFreeAsync(cnt, s));
+  GPS_CHECK_CUDA(cudaStreamSynchronize(s));
+  *unique_voxels = (int64_t)h;
   return GPS_OK;
 }
 
