@@ -54,6 +54,29 @@ def dist_env():
     return ws, rank, local
 
 
+def rank_config(name: str, rank: int, world: int):
+    """Config 5: with several GPUs every rank maps its own independent sequence
+    (seed 40 + rank: a different room and trajectory); a single GPU runs the config's own seed."""
+    import gps_synth as S
+    return S.get_config(name, seed=40 + rank) if world > 1 else S.get_config(name)
+
+
+def max_over_ranks(ms: float, device) -> float:
+    """The job's time is the slowest rank's device time (all_reduce MAX; a no-op on one rank)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return ms
+    t = torch.tensor([ms], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def job_rate(units_per_rank: int, world: int, ms_max: float) -> float:
+    """Whole-job throughput: units processed by all ranks / the slowest rank's time."""
+    return units_per_rank * world / (ms_max / 1000.0)
+
+
 class Clocks:
     """nvidia-smi sampling of SM clocks and throttle reasons during the timed region."""
 
@@ -120,9 +143,7 @@ def run_ours(args):
     from paper_2509_11574_b200 import _native as N
     from paper_2509_11574_b200.pipeline import MappingPipeline
 
-    cfg = S.get_config(args.config)
-    if ws > 1:  # config 5: an independent sequence (different room and path) per GPU
-        cfg = S.get_config(args.config, seed=40 + rank)
+    cfg = rank_config(args.config, rank, ws)
     dk = 10
     n_frames = args.history + dk * (args.warmup + args.steps + 1)  # +1 step: alignment slack
     if not args.no_e2e:
@@ -199,13 +220,9 @@ def run_ours(args):
     N._lib.gps_profile_enable(0)
     rstats = pipe.ras.stats()
     vstats = vol.stats()
-    ms_max = ms
-    if ws > 1:
-        tt = torch.tensor([ms], device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms_max = float(tt.item())
+    ms_max = max_over_ranks(ms, "cuda")
     frames_timed = args.steps * dk
-    value = frames_timed * ws / (ms_max / 1000.0)
+    value = job_rate(frames_timed, ws, ms_max)
     # ---------------- end-to-end leg: host (pinned) frames, result read back ----------------
     e2e = None
     if not args.no_e2e:
@@ -223,12 +240,8 @@ def run_ours(args):
         run_steps(args.steps, host)
         e1.record(stream)
         torch.cuda.synchronize()
-        ems = e0.elapsed_time(e1)
-        if ws > 1:
-            tt = torch.tensor([ems], device="cuda")
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            ems = float(tt.item())
-        e2e = {"value": round(frames_timed * ws / (ems / 1000.0), 2), "unit": "frames/s",
+        ems = max_over_ranks(e0.elapsed_time(e1), "cuda")
+        e2e = {"value": round(job_rate(frames_timed, ws, ems), 2), "unit": "frames/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 4,
                "ms_per_step": round(ems / args.steps, 4),
                "path": "MappingPipeline.process_frame with pinned-host depth/RGBA (H2D on the stream) + loss D2H"}
@@ -287,13 +300,7 @@ def run_ours(args):
         "value": round(value, 2), "unit": "frames/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(ms_max / args.steps, 4), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded analytic rooms, gps_synth)",
-        "config": {"workload": f"{args.config}: Azure-Kinect-shaped {cfg.width}x{cfg.height}, {n_g} Gaussians "
-                               f"(SH deg {args.sh_degree}), voxel {cfg.voxel_size} m, delta_k=10, 20 iters/round, "
-                               f"6 views/round (R-VIEW: 1 view/iteration); step = 10 frames",
-                   "frames_per_step": dk, "gaussians": n_g, "sh_degree": args.sh_degree, "tile": args.tile,
-                   "resolution": [cfg.width, cfg.height], "history_frames": args.history,
-                   "parallelism": f"replicas x{ws} (independent sequences)",
-                   "l2": "inputs larger than L2 (per-step state > 126 MB: params+Adam 283 MB, volume)"},
+        "config": workload_config(args, cfg, n_g, ws),
         "e2e": e2e,
         "gpu_launches": launches,
         "gpu_launches_per_step": launches / args.steps,
@@ -306,6 +313,16 @@ def run_ours(args):
     if ws > 1:
         dist.destroy_process_group()
     return line
+
+
+def workload_config(args, cfg, n_g, ws):
+    return {"workload": f"{args.config}: {cfg.width}x{cfg.height} synthetic RGB-D ({cfg.name}), {n_g} Gaussians "
+                        f"(SH deg {args.sh_degree}), voxel {cfg.voxel_size} m, delta_k=10, 20 iters/round, "
+                        f"6 views/round (R-VIEW: 1 view/iteration); step = 10 frames",
+            "frames_per_step": 10, "gaussians": n_g, "sh_degree": args.sh_degree, "tile": args.tile,
+            "resolution": [cfg.width, cfg.height], "history_frames": args.history,
+            "parallelism": f"replicas x{ws} (independent sequences)",
+            "l2": "inputs larger than L2 (per-step state > 126 MB: params+Adam 283 MB, volume)"}
 
 
 def read_profile(N):
@@ -386,7 +403,8 @@ def run_reference(args):
             "unit": "frames/s", "n_gpus": 0, "steps": len(vals), "warmup": args.warmup,
             "ms_per_step": round(10 * 1000.0 / v, 1), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded analytic rooms, gps_synth)",
-            "config": {"workload": f"{args.config} bounded sample (see cpu_baseline.sample)"},
+            "config": dict(workload_config(args, cfg, gd["xyz"].shape[0], 1),
+                           reference="the CPU oracle timed on a bounded sample of this workload (cpu_baseline.sample)"),
             "cpu_baseline": cb,
             "e2e": {"value": cb["value"], "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 

@@ -53,7 +53,8 @@ struct WsHeader {
 };
 
 struct WsLayout {
-  size_t hdr, counts, cursor, offsets, tile_end, loss_part, records, grad2d, rec3, vals, keys, cstar, wg, gbuf, total;
+  size_t hdr, counts, cursor, bigcounts, offsets, tile_end, loss_part, records, ranks, grad2d, rec3, vals, keys, cstar, wg,
+      gbuf, total;
   size_t zero_begin, zero_bytes;
 };
 
@@ -69,14 +70,16 @@ WsLayout ws_layout(int64_t n, int W, int H, int tile, int64_t cap, int64_t n_par
     return at;
   };
   L.hdr = take(sizeof(WsHeader));
-  L.counts = take(4 * tiles);
-  L.cursor = take(4 * tiles);
+  L.counts = take(4 * tiles);     // per tile: entries of Gaussians spanning <= 4 tiles
+  L.cursor = take(4 * tiles);     // per tile: scatter cursor of the others
+  L.bigcounts = take(4 * tiles);  // per tile: entries of Gaussians spanning > 4 tiles
   L.zero_begin = L.hdr + offsetof(WsHeader, K);
-  L.zero_bytes = L.cursor + 4 * tiles - L.zero_begin;
+  L.zero_bytes = L.bigcounts + 4 * tiles - L.zero_begin;
   L.offsets = take(4 * (tiles + 1));
   L.tile_end = take(4 * tiles);
   L.loss_part = take(4 * tiles);
   L.records = take(64 * (size_t)std::max<int64_t>(n, 1));
+  L.ranks = take(16 * (size_t)std::max<int64_t>(n, 1));
   L.grad2d = refine ? take(48 * (size_t)std::max<int64_t>(n, 1)) : 0;
   L.rec3 = refine ? take(128 * (size_t)std::max<int64_t>(n, 1)) : 0;
   L.vals = take(4 * (size_t)cap);
@@ -286,6 +289,8 @@ __device__ __forceinline__ float pair_qmax(float L, float lnsig) {
 // ============================================================================================
 struct SplatPtrs {
   float4* rec;     // 4 float4 per Gaussian
+  uint4* ranks;    // per Gaussian: its rank inside each of its (<= 4) tile buckets
+  uint32_t* bigcounts;
   float4* grad2d;  // 3 float4 per Gaussian (nullable)
   uint32_t* counts;
   WsHeader* hdr;
@@ -337,15 +342,26 @@ __global__ void __launch_bounds__(256) k_preprocess(RenderArgs a, gps_gaussians 
   w.rec[4 * i + 2] = make_float4(col[0], col[1], col[2], __uint_as_float(ry));
   w.rec[4 * i + 3] = make_float4(ddx, ddy, 0.f, 0.f);
   const int tx0 = pr.x0 / a.tile, tx1 = pr.x1 / a.tile, ty0 = pr.y0 / a.tile, ty1 = pr.y1 / a.tile;
-  for (int ty = ty0; ty <= ty1; ++ty)
-    for (int tx = tx0; tx <= tx1; ++tx) atomicAdd(&w.counts[ty * a.tiles_x + tx], 1u);
+  if ((tx1 - tx0 + 1) * (ty1 - ty0 + 1) <= 4) {
+    // the count atomic's old value is this Gaussian's slot inside the tile bucket: k_emit
+    // scatters without atomics
+    uint32_t rk[4] = {0u, 0u, 0u, 0u};
+    int k = 0;
+    for (int ty = ty0; ty <= ty1; ++ty)
+      for (int tx = tx0; tx <= tx1; ++tx) rk[k++] = atomicAdd(&w.counts[ty * a.tiles_x + tx], 1u);
+    w.ranks[i] = make_uint4(rk[0], rk[1], rk[2], rk[3]);
+  } else {
+    for (int ty = ty0; ty <= ty1; ++ty)
+      for (int tx = tx0; tx <= tx1; ++tx) atomicAdd(&w.bigcounts[ty * a.tiles_x + tx], 1u);
+  }
   atomicAdd(&w.hdr->n_visible, 1u);
 }
 
 // ============================================================================================
 // k_scan: exclusive scan of the per-tile counts (one CTA, 1024 threads, chunked)
 // ============================================================================================
-__global__ void __launch_bounds__(1024) k_scan(const uint32_t* __restrict__ counts, uint32_t* offsets,
+__global__ void __launch_bounds__(1024) k_scan(const uint32_t* __restrict__ counts,
+                                               const uint32_t* __restrict__ bigcounts, uint32_t* offsets,
                                                int n_tiles, WsHeader* hdr, WsHeader stat) {
   __shared__ uint32_t warp_sums[32];
   __shared__ uint32_t carry;
@@ -354,7 +370,7 @@ __global__ void __launch_bounds__(1024) k_scan(const uint32_t* __restrict__ coun
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (int base = 0; base < n_tiles; base += 1024) {
     const int i = base + threadIdx.x;
-    const uint32_t v = i < n_tiles ? counts[i] : 0u;
+    const uint32_t v = i < n_tiles ? counts[i] + bigcounts[i] : 0u;
     uint32_t x = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -395,6 +411,8 @@ __global__ void __launch_bounds__(1024) k_scan(const uint32_t* __restrict__ coun
 // per-tile sort makes the final order unique)
 // ============================================================================================
 __global__ void __launch_bounds__(256) k_emit(RenderArgs a, const float4* __restrict__ rec,
+                                              const uint4* __restrict__ ranks,
+                                              const uint32_t* __restrict__ counts,
                                               const uint32_t* __restrict__ offsets, uint32_t* cursor,
                                               uint32_t* vals) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -404,12 +422,23 @@ __global__ void __launch_bounds__(256) k_emit(RenderArgs a, const float4* __rest
   const int x0 = rx & 0xFFFF, x1 = rx >> 16, y0 = ry & 0xFFFF, y1 = ry >> 16;
   if (x1 < x0) return;  // culled
   const int tx0 = x0 / a.tile, tx1 = x1 / a.tile, ty0 = y0 / a.tile, ty1 = y1 / a.tile;
-  for (int ty = ty0; ty <= ty1; ++ty)
-    for (int tx = tx0; tx <= tx1; ++tx) {
-      const int t = ty * a.tiles_x + tx;
-      const uint32_t pos = offsets[t] + atomicAdd(&cursor[t], 1u);
-      if (pos < a.cap) vals[pos] = (uint32_t)i;
-    }
+  if ((tx1 - tx0 + 1) * (ty1 - ty0 + 1) <= 4) {
+    const uint4 r4 = ranks[i];
+    const uint32_t rk[4] = {r4.x, r4.y, r4.z, r4.w};
+    int k = 0;
+    for (int ty = ty0; ty <= ty1; ++ty)
+      for (int tx = tx0; tx <= tx1; ++tx) {
+        const uint32_t pos = offsets[ty * a.tiles_x + tx] + rk[k++];
+        if (pos < a.cap) vals[pos] = (uint32_t)i;
+      }
+  } else {  // large footprints: after the ranked entries of each tile, by an atomic cursor
+    for (int ty = ty0; ty <= ty1; ++ty)
+      for (int tx = tx0; tx <= tx1; ++tx) {
+        const int t = ty * a.tiles_x + tx;
+        const uint32_t pos = offsets[t] + counts[t] + atomicAdd(&cursor[t], 1u);
+        if (pos < a.cap) vals[pos] = (uint32_t)i;
+      }
+  }
 }
 
 // ============================================================================================
@@ -1123,6 +1152,8 @@ gps_status forward_view(const gps_gaussians* g, const View1& v, const gps_render
   sp.rec = reinterpret_cast<float4*>(ws + L.records);
   sp.grad2d = zero_grad2d ? reinterpret_cast<float4*>(ws + L.grad2d) : nullptr;
   sp.counts = reinterpret_cast<uint32_t*>(ws + L.counts);
+  sp.ranks = reinterpret_cast<uint4*>(ws + L.ranks);
+  sp.bigcounts = reinterpret_cast<uint32_t*>(ws + L.bigcounts);
   sp.hdr = hdr;
   const int n_tiles = a.tiles_x * a.tiles_y;
   if (g->n > 0) {
@@ -1137,13 +1168,13 @@ gps_status forward_view(const gps_gaussians* g, const View1& v, const gps_render
   uint32_t* offsets = reinterpret_cast<uint32_t*>(ws + L.offsets);
   {
     GPS_PROF(K_SCAN, s);
-    k_scan<<<1, 1024, 0, s>>>(sp.counts, offsets, n_tiles, hdr, stat);
+    k_scan<<<1, 1024, 0, s>>>(sp.counts, sp.bigcounts, offsets, n_tiles, hdr, stat);
   }
   GPS_CHECK_LAUNCH("k_scan");
   uint32_t* vals = reinterpret_cast<uint32_t*>(ws + L.vals);
   if (g->n > 0) {
     GPS_PROF(K_EMIT, s);
-    k_emit<<<(unsigned)((g->n + 255) / 256), 256, 0, s>>>(a, sp.rec, offsets,
+    k_emit<<<(unsigned)((g->n + 255) / 256), 256, 0, s>>>(a, sp.rec, sp.ranks, sp.counts, offsets,
                                                           reinterpret_cast<uint32_t*>(ws + L.cursor), vals);
     GPS_CHECK_LAUNCH("k_emit");
   }
