@@ -161,7 +161,8 @@ def run_ours(args):
     gd = S.make_gaussians(cfg, n=n_g, sh_degree=args.sh_degree)
     t_setup = time.time() - t0
     cam = G.Camera(cfg.fx, cfg.fy, cfg.cx, cfg.cy, cfg.width, cfg.height)
-    vol = G.Volume(voxel_size=cfg.voxel_size, max_blocks=cfg.max_blocks, hash_slots=cfg.hash_slots)
+    vol = G.Volume(voxel_size=cfg.voxel_size, max_blocks=cfg.max_blocks, hash_slots=cfg.hash_slots,
+                   dense_bounds=S.scene_bounds(cfg))
     g = G.Gaussians.from_dict(gd)
     pipe = MappingPipeline(cam, g, vol, cfg.depth_scale, G.RenderConfig(tile=args.tile), seed=rank)
     k = 0

@@ -73,6 +73,14 @@ CONFIGS = {
 }
 
 
+def scene_bounds(cfg: "SynthConfig", margin: float = 0.5):
+    """Axis-aligned bounds (metres) that contain the scene, for the optional dense block grid."""
+    if cfg.scene == "plane_sphere":
+        return ((-0.5, -0.5, -0.1), (0.5, 0.5, 0.6))
+    X, Y, Z = cfg.room
+    return ((-margin, -margin, -margin), (X + margin, Y + margin, Z + margin))
+
+
 def get_config(name: str, **over) -> SynthConfig:
     import dataclasses
     return dataclasses.replace(CONFIGS[name], **over)

@@ -80,6 +80,12 @@ typedef struct {
   float depth_max;  /* valid depth / ray range upper bound, metres (R-DEPTH: 10)              */
   int64_t max_blocks; /* block budget (>= 1); exceeding it is GPS_ERR_OUT_OF_BLOCKS          */
   int64_t hash_slots; /* open-addressing slots, power of two, >= 2*max_blocks recommended   */
+  /* Optional dense block-index grid (an accelerator; results do not depend on it): blocks with
+   * coordinates in [dense_origin, dense_origin + dense_dims) are also indexed by a direct array
+   * (4 bytes per cell) so the raycast looks them up with one load instead of hash probing.
+   * dense_dims all zero = disabled.  Coordinates in blocks (8 * voxel_size metres).            */
+  int32_t dense_origin[3];
+  int32_t dense_dims[3];
 } gps_volume_config;
 
 typedef struct gps_volume gps_volume;

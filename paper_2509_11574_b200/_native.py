@@ -33,7 +33,7 @@ class gps_pose(C.Structure):
 class gps_volume_config(C.Structure):
     _fields_ = [("voxel_size", C.c_float), ("mu", C.c_float), ("w_max", C.c_int32),
                 ("depth_min", C.c_float), ("depth_max", C.c_float), ("max_blocks", C.c_int64),
-                ("hash_slots", C.c_int64)]
+                ("hash_slots", C.c_int64), ("dense_origin", C.c_int32 * 3), ("dense_dims", C.c_int32 * 3)]
 
 
 class gps_gaussians(C.Structure):

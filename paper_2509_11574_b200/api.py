@@ -66,10 +66,18 @@ class Volume:
     """Voxel-block hash volume owned by libgps (gps_volume_*)."""
 
     def __init__(self, voxel_size=0.005, mu=None, w_max=100, depth_min=0.1, depth_max=10.0,
-                 max_blocks=1 << 18, hash_slots=1 << 20, stream=None):
+                 max_blocks=1 << 18, hash_slots=1 << 20, dense_bounds=None, stream=None):
+        """dense_bounds: optional ((x0, y0, z0), (x1, y1, z1)) in metres covered by the dense
+        block-index grid (an accelerator for the raycast; results do not depend on it)."""
         mu = 4 * voxel_size if mu is None else mu
+        org, dims = (0, 0, 0), (0, 0, 0)
+        if dense_bounds is not None:
+            bs = 8 * voxel_size
+            lo = [int(np.floor(c / bs)) - 1 for c in dense_bounds[0]]
+            hi = [int(np.ceil(c / bs)) + 1 for c in dense_bounds[1]]
+            org, dims = tuple(lo), tuple(h - l for l, h in zip(lo, hi))
         self.cfg = N.gps_volume_config(voxel_size, mu, w_max, depth_min, depth_max, int(max_blocks),
-                                       int(hash_slots))
+                                       int(hash_slots), (C.c_int32 * 3)(*org), (C.c_int32 * 3)(*dims))
         h = C.c_void_p()
         N.check("gps_volume_create", _L.gps_volume_create(C.byref(self.cfg), _stream(stream), C.byref(h)))
         self.h = h

@@ -92,6 +92,8 @@ struct VolumeView {  // passed by value to kernels
   VolumeCounters* ctr;
   uint32_t slot_mask;
   uint32_t max_blocks;
+  int32_t* grid;  // optional dense block-index grid (nullable), -1 = unallocated
+  int gox, goy, goz, gdx, gdy, gdz;
 };
 
 // find a block: returns its pool index, or -1 if unallocated / unbacked
@@ -105,6 +107,14 @@ __device__ __forceinline__ int32_t find_block(const VolumeView& v, int x, int y,
     h = (h + 1) & v.slot_mask;
   }
   return -1;
+}
+
+// pool index of a block, through the dense grid when the block lies inside it
+__device__ __forceinline__ int32_t find_block_fast(const VolumeView& v, int x, int y, int z) {
+  const unsigned ix = (unsigned)(x - v.gox), iy = (unsigned)(y - v.goy), iz = (unsigned)(z - v.goz);
+  if (v.grid && ix < (unsigned)v.gdx && iy < (unsigned)v.gdy && iz < (unsigned)v.gdz)
+    return __ldg(&v.grid[((size_t)iz * v.gdy + iy) * v.gdx + ix]);
+  return find_block(v, x, y, z);
 }
 
 }  // namespace gps

@@ -65,6 +65,9 @@ __device__ void global_insert(const VolumeView& v, uint64_t key, uint32_t frame,
         if (b < v.max_blocks) {
           v.bkeys[b] = key;
           v.vals[h] = (int32_t)b;  // the pool block was initialised empty at create/reset
+          const unsigned ix = (unsigned)(x - v.gox), iy = (unsigned)(y - v.goy), iz = (unsigned)(z - v.goz);
+          if (v.grid && ix < (unsigned)v.gdx && iy < (unsigned)v.gdy && iz < (unsigned)v.gdz)
+            v.grid[((size_t)iz * v.gdy + iy) * v.gdx + ix] = (int32_t)b;
         } else {
           v.ctr->overflow = 1u;
           *(volatile uint32_t*)d_flag = 1u;
@@ -302,8 +305,8 @@ __global__ void __launch_bounds__(256) k_link(VolumeView v) {
 #pragma unroll
     for (int k = 1; k < 8; ++k) {
       const int dx = k & 1, dy = (k >> 1) & 1, dz = (k >> 2) & 1;
-      v.nbr[8 * (size_t)b + k] = find_block(v, x + dx, y + dy, z + dz);
-      const int32_t m = find_block(v, x - dx, y - dy, z - dz);
+      v.nbr[8 * (size_t)b + k] = find_block_fast(v, x + dx, y + dy, z + dz);
+      const int32_t m = find_block_fast(v, x - dx, y - dy, z - dz);
       if (m >= 0) v.nbr[8 * (size_t)m + k] = (int32_t)b;
     }
   }
@@ -426,7 +429,7 @@ struct BlockCache {
 __device__ __forceinline__ int32_t cached_find(const VolumeView& v, BlockCache& c, int x, int y, int z) {
   if (x == c.x && y == c.y && z == c.z) return c.b;
   c.x = x; c.y = y; c.z = z;
-  c.b = find_block(v, x, y, z);
+  c.b = find_block_fast(v, x, y, z);
   return c.b;
 }
 
@@ -673,6 +676,9 @@ gps_status fill_volume(VolumeImpl* v, cudaStream_t s) {
   k_fill_pool<<<1184, 256, 0, s>>>(v->view.tsdf, v->view.rgbw, (size_t)c.max_blocks * 512);
   GPS_CHECK_LAUNCH("k_fill_pool");
   GPS_CHECK_CUDA(cudaMemsetAsync(v->view.ctr, 0, sizeof(VolumeCounters), s));
+  if (v->view.grid)
+    GPS_CHECK_CUDA(cudaMemsetAsync(v->view.grid, 0xFF,
+                                   sizeof(int32_t) * (size_t)v->view.gdx * v->view.gdy * v->view.gdz, s));
   *(volatile uint32_t*)v->flag.host = 0u;
   v->frame = 0;
   return GPS_OK;
@@ -692,7 +698,8 @@ gps_status gps_volume_create(const gps_volume_config* cfg, gps_stream_t stream, 
   if (!(cfg->voxel_size > 0) || !(cfg->mu > 0) || cfg->w_max < 1 || cfg->w_max > 255 ||
       !(cfg->depth_min >= 0) || !(cfg->depth_max > cfg->depth_min) || cfg->max_blocks < 1 ||
       cfg->max_blocks > (1ll << 30) || cfg->hash_slots < 2 || (cfg->hash_slots & (cfg->hash_slots - 1)) ||
-      cfg->hash_slots > (1ll << 31))
+      cfg->hash_slots > (1ll << 31) || cfg->dense_dims[0] < 0 || cfg->dense_dims[1] < 0 || cfg->dense_dims[2] < 0 ||
+      (double)cfg->dense_dims[0] * cfg->dense_dims[1] * cfg->dense_dims[2] > (double)(1ll << 30))
     return invalid("gps_volume_create: bad config (voxel_size, mu > 0; 1 <= w_max <= 255; "
                    "depth_max > depth_min; hash_slots a power of two)");
   VolumeImpl* v = new VolumeImpl();
@@ -719,6 +726,20 @@ gps_status gps_volume_create(const gps_volume_config* cfg, gps_stream_t stream, 
   }
   v->view.slot_mask = (uint32_t)(slots - 1);
   v->view.max_blocks = (uint32_t)nb;
+  v->view.grid = nullptr;
+  v->view.gox = cfg->dense_origin[0]; v->view.goy = cfg->dense_origin[1]; v->view.goz = cfg->dense_origin[2];
+  v->view.gdx = cfg->dense_dims[0]; v->view.gdy = cfg->dense_dims[1]; v->view.gdz = cfg->dense_dims[2];
+  const size_t gcells = (size_t)std::max(0, v->view.gdx) * std::max(0, v->view.gdy) * std::max(0, v->view.gdz);
+  if (gcells > 0) {
+    if (cudaMalloc(&v->view.grid, sizeof(int32_t) * gcells) != cudaSuccess) {
+      cudaGetLastError();
+      set_error("gps_volume_create: out of device memory (dense grid)");
+      gps_volume_destroy(v);
+      return GPS_ERR_OOM;
+    }
+  } else {
+    v->view.gdx = v->view.gdy = v->view.gdz = 0;
+  }
   gps_status st = fill_volume(v, as_stream(stream));
   if (st != GPS_OK) {
     gps_volume_destroy(v);
@@ -739,6 +760,7 @@ void gps_volume_destroy(gps_volume* vol) {
   cudaFree(v->view.vis);
   cudaFree(v->view.bkeys);
   cudaFree(v->view.nbr);
+  if (v->view.grid) cudaFree(v->view.grid);
   cudaFree(v->range);
   cudaFree(v->view.ctr);
   if (v->flag.host) cudaFreeHost(v->flag.host);

@@ -132,3 +132,24 @@ def test_raycast_empty_volume_misses():
     vol = H.gpu_volume(cfg)
     D, C, _ = vol.raycast(gcam, np.eye(3), np.zeros(3))
     assert torch.all(D == 0) and torch.all(C == 0)
+
+
+def test_dense_grid_changes_nothing():
+    """The dense block-index grid only accelerates lookups: allocation, integration and raycast
+    are bitwise identical with and without it (cfg2 prefix, raycast from an unfused pose)."""
+    cfg = S.get_config("cfg2")
+    frs = H.frames(cfg, 3)
+    a = H.gpu_volume(cfg)
+    b = H.gpu_volume(cfg, dense_bounds=S.scene_bounds(cfg))
+    gcam, _ = H.cams(cfg)
+    for fr in frs:
+        d, c = H.to_dev(fr)
+        a.fuse(gcam, fr.R, fr.t, d, cfg.depth_scale, c)
+        b.fuse(gcam, fr.R, fr.t, d, cfg.depth_scale, c)
+    ca, va = H.sorted_blocks(*a.export_blocks())
+    cb, vb = H.sorted_blocks(*b.export_blocks())
+    assert np.array_equal(ca, cb) and np.array_equal(va.view(np.uint8), vb.view(np.uint8))
+    R, t = S.trajectory(cfg, 1, start=5)[0]
+    Da, Ca, _ = a.raycast(gcam, R, t)
+    Db, Cb, _ = b.raycast(gcam, R, t)
+    assert torch.equal(Da, Db) and torch.equal(Ca, Cb)

@@ -32,7 +32,8 @@ def main():
     poses = S.trajectory(cfg, args.history + args.iters + 1)
     frames = [S.render_frame(cfg, scene, *poses[k], k=k, device="cuda", dc=dc) for k in range(len(poses))]
     cam = G.Camera(cfg.fx, cfg.fy, cfg.cx, cfg.cy, cfg.width, cfg.height)
-    vol = G.Volume(voxel_size=cfg.voxel_size, max_blocks=cfg.max_blocks, hash_slots=cfg.hash_slots)
+    vol = G.Volume(voxel_size=cfg.voxel_size, max_blocks=cfg.max_blocks, hash_slots=cfg.hash_slots,
+                   dense_bounds=None if os.environ.get("GPS_NO_GRID") else S.scene_bounds(cfg))
     for k in range(args.history):
         f = frames[k]
         vol.fuse(cam, f.R, f.t, f.depth, cfg.depth_scale, f.rgba)
