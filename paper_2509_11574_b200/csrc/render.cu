@@ -53,8 +53,8 @@ struct WsHeader {
 };
 
 struct WsLayout {
-  size_t hdr, counts, cursor, bigcounts, offsets, tile_end, loss_part, records, ranks, grad2d, rec3, vals, keys, cstar, wg,
-      gbuf, total;
+  size_t hdr, counts, cursor, bigcounts, offsets, tile_end, loss_part, records, ranks, grad2d, rec3, cgj, vals, keys,
+      cstar, wg, gbuf, total;
   size_t zero_begin, zero_bytes;
 };
 
@@ -82,6 +82,7 @@ WsLayout ws_layout(int64_t n, int W, int H, int tile, int64_t cap, int64_t n_par
   L.ranks = take(16 * (size_t)std::max<int64_t>(n, 1));
   L.grad2d = refine ? take(48 * (size_t)std::max<int64_t>(n, 1)) : 0;
   L.rec3 = refine ? take(128 * (size_t)std::max<int64_t>(n, 1)) : 0;
+  L.cgj = refine ? take(48 * (size_t)std::max<int64_t>(n, 1)) : 0;
   L.vals = take(4 * (size_t)cap);
   L.keys = take(8 * (size_t)cap);
   L.cstar = refine ? take(12 * (size_t)W * H) : 0;
@@ -292,6 +293,7 @@ struct SplatPtrs {
   uint4* ranks;    // per Gaussian: its rank inside each of its (<= 4) tile buckets
   uint32_t* bigcounts;
   float4* grad2d;  // 3 float4 per Gaussian (nullable)
+  float4* cgj;     // 3 float4 per Gaussian: colour/direction Jacobian + clamp bits (refine only)
   uint32_t* counts;
   WsHeader* hdr;
 };
@@ -314,11 +316,27 @@ __global__ void __launch_bounds__(256) k_preprocess(RenderArgs a, gps_gaussians 
   view_dir(a.cam, g.xyz + 3 * i, a.deg, h);
   const float* sh = g.sh + (size_t)i * a.nc * 3;
   float col[3];
+  uint32_t clamp = 0u;
 #pragma unroll
   for (int ch = 0; ch < 3; ++ch) {
     float acc = 0.f;
     for (int k = 0; k < a.nc; ++k) acc = fmaf(h.Y[k], __ldg(&sh[3 * k + ch]), acc);
     col[ch] = fmaxf(acc + 0.5f, 0.0f);
+    if (acc + 0.5f < 0.f) clamp |= 1u << ch;
+  }
+  if (w.cgj) {
+    // d colour_ch / d dir_e for the backward's view-direction term (the chain then needs no SH)
+    float Gc[9];
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+      float wk[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) wk[k] = k < a.nc ? __ldg(&sh[3 * k + ch]) : 0.f;
+      sh_basis_vjp(h.dir[0], h.dir[1], h.dir[2], a.deg, wk, Gc + 3 * ch);
+    }
+    w.cgj[3 * i] = make_float4(Gc[0], Gc[1], Gc[2], Gc[3]);
+    w.cgj[3 * i + 1] = make_float4(Gc[4], Gc[5], Gc[6], Gc[7]);
+    w.cgj[3 * i + 2] = make_float4(Gc[8], __uint_as_float(clamp), 0.f, 0.f);
   }
   // ln(sigmoid(o)) rounded once from double: feeds the exact membership decision q <= q_max
   const float lnsig = (float)(-log1p(exp(-(double)__ldg(&g.opacity_raw[i]))));
@@ -817,7 +835,7 @@ constexpr int kAdamThreads = 256;
 // direction (the SH gradient is Y[k] * dcol[ch]).
 __device__ __forceinline__ void chain3d(const RenderArgs& a, const gps_gaussians& g, int64_t i, float dpx, float dpy,
                                         float da, float db, float dcc, float dsig, float* dcol, float* gx,
-                                        float* gls, float* gq, float& gop, float* Y) {
+                                        float* gls, float* gq, float& gop, float* Y, const float4* __restrict__ cgj) {
   const int nc = a.nc;
 #pragma unroll
   for (int k = 0; k < 3; ++k) gx[k] = gls[k] = 0.f;
@@ -828,23 +846,20 @@ __device__ __forceinline__ void chain3d(const RenderArgs& a, const gps_gaussians
         view_dir(a.cam, p, a.deg, h);
 #pragma unroll
         for (int k = 0; k < 16; ++k) Y[k] = k < nc ? h.Y[k] : 0.f;
-        const float* sh = g.sh + (size_t)i * nc * 3;
         // opacity: sigma = sigmoid(o)
         const float sig = 1.0f / (1.0f + __expf(-g.opacity_raw[i]));
         gop = dsig * sig * (1.f - sig);
-        // colour -> SH and view direction (clamped channels get zero gradient)
-        float w[16];
-        float ddir[3] = {0.f, 0.f, 0.f};
+        // colour -> view direction through the Jacobian Gc[ch][e] = sum_k SH_k,ch dY_k/d dir_e and
+        // the clamp bits that k_preprocess stored (clamped channels get zero gradient)
+        const float4 c0 = cgj[3 * i], c1 = cgj[3 * i + 1], c2 = cgj[3 * i + 2];
+        const uint32_t clamp = __float_as_uint(c2.y);
 #pragma unroll
-        for (int ch = 0; ch < 3; ++ch) {
-          float acc = 0.f;
-          for (int k = 0; k < nc; ++k) acc = fmaf(h.Y[k], sh[3 * k + ch], acc);
-          if (acc + 0.5f < 0.f) dcol[ch] = 0.f;
-        }
+        for (int ch = 0; ch < 3; ++ch)
+          if (clamp & (1u << ch)) dcol[ch] = 0.f;
+        const float Gc[9] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w, c2.x};
+        float ddir[3];
 #pragma unroll
-        for (int k = 0; k < 16; ++k)
-          w[k] = k < nc ? dcol[0] * sh[3 * k] + dcol[1] * sh[3 * k + 1] + dcol[2] * sh[3 * k + 2] : 0.f;
-        sh_basis_vjp(h.dir[0], h.dir[1], h.dir[2], a.deg, w, ddir);
+        for (int e = 0; e < 3; ++e) ddir[e] = dcol[0] * Gc[e] + dcol[1] * Gc[3 + e] + dcol[2] * Gc[6 + e];
         const float dd = ddir[0] * h.dir[0] + ddir[1] * h.dir[1] + ddir[2] * h.dir[2];
         const float invn = 1.f / h.dnorm;
 #pragma unroll
@@ -932,7 +947,8 @@ __device__ __forceinline__ void chain3d(const RenderArgs& a, const gps_gaussians
 // gradient slot; ACCUM = 1 adds the dense raw gradient into gbuf (multi-view rounds).
 template <int ACCUM>
 __global__ void __launch_bounds__(kChainThreads) k_chain(RenderArgs a, gps_gaussians g, float4* grad2d,
-                                                         float4* rec3, gps_gaussians gbuf) {
+                                                         float4* rec3, gps_gaussians gbuf,
+                                                         const float4* __restrict__ cgj) {
   const int64_t i = blockIdx.x * (int64_t)kChainThreads + threadIdx.x;
   if (i >= a.n) return;
   const float4 q0 = grad2d[3 * i], q1 = grad2d[3 * i + 1], q2 = grad2d[3 * i + 2];
@@ -941,7 +957,7 @@ __global__ void __launch_bounds__(kChainThreads) k_chain(RenderArgs a, gps_gauss
                   (dcol[0] != 0.f) | (dcol[1] != 0.f) | (dcol[2] != 0.f);
   if (!nz) return;
   float gx[3], gls[3], gq[4], gop, Y[16];
-  chain3d(a, g, i, q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, dcol, gx, gls, gq, gop, Y);
+  chain3d(a, g, i, q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, dcol, gx, gls, gq, gop, Y, cgj);
   if (ACCUM) {
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
@@ -1002,7 +1018,9 @@ __global__ void __launch_bounds__(kAdamThreads) k_adam(RenderArgs a, gps_gaussia
   const uint32_t n = (uint32_t)a.n, nsh = 3u * (uint32_t)a.nc;
   const uint32_t u1 = (3u * n + 3u) / 4u, u2 = u1 + (3u * n + 3u) / 4u, u3 = u2 + n, u4 = u3 + (n + 3u) / 4u,
                  u5 = u4 + (nsh * n + 3u) / 4u;
-  for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < u5; u += gridDim.x * blockDim.x) {
+  const uint32_t stride = gridDim.x * blockDim.x;
+#pragma unroll 2
+  for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < u5; u += stride) {
     const int grp = (u >= u1) + (u >= u2) + (u >= u3) + (u >= u4);
     float *P, *M, *V, *E, *O;
     float step;
@@ -1151,6 +1169,7 @@ gps_status forward_view(const gps_gaussians* g, const View1& v, const gps_render
   SplatPtrs sp;
   sp.rec = reinterpret_cast<float4*>(ws + L.records);
   sp.grad2d = zero_grad2d ? reinterpret_cast<float4*>(ws + L.grad2d) : nullptr;
+  sp.cgj = zero_grad2d ? reinterpret_cast<float4*>(ws + L.cgj) : nullptr;
   sp.counts = reinterpret_cast<uint32_t*>(ws + L.counts);
   sp.ranks = reinterpret_cast<uint4*>(ws + L.ranks);
   sp.bigcounts = reinterpret_cast<uint32_t*>(ws + L.bigcounts);
@@ -1341,10 +1360,11 @@ gps_status gps_refine_step(gps_gaussians* g, gps_adam_state* state, const gps_vi
       const unsigned cgrid = (unsigned)((g->n + kChainThreads - 1) / kChainThreads);
       float4* rec3 = reinterpret_cast<float4*>(w + L.rec3);
       GPS_PROF(K_CHAIN, s);
+      const float4* cgj = reinterpret_cast<const float4*>(w + L.cgj);
       if (v < n_views - 1)
-        k_chain<1><<<cgrid, kChainThreads, 0, s>>>(a, *g, grad2d, rec3, gb);
+        k_chain<1><<<cgrid, kChainThreads, 0, s>>>(a, *g, grad2d, rec3, gb, cgj);
       else
-        k_chain<0><<<cgrid, kChainThreads, 0, s>>>(a, *g, grad2d, rec3, gb);
+        k_chain<0><<<cgrid, kChainThreads, 0, s>>>(a, *g, grad2d, rec3, gb, cgj);
       GPS_CHECK_LAUNCH("k_chain");
     }
   }

@@ -40,6 +40,7 @@ class MappingPipeline:
         self.view_color = [torch.empty((H, W, 3), dtype=torch.float32, device=dev) for _ in range(nv)]
         self.frames = {}          # frame id -> (rgba device tensor, R, t) for keyframes and the interval
         self.interval = []
+        self.last_frame = None
         self.last_loss = None
         self.rounds = 0
         self.iterations_run = 0
@@ -52,6 +53,7 @@ class MappingPipeline:
         rgba = self._device(rgba)
         self.vol.fuse(self.cam, R, t, depth, self.depth_scale, rgba)
         self.vol.raycast(self.cam, R, t, self.depth, self.color)
+        self.last_frame = k
         is_kf = self.kf.offer(k, R, t)
         self.interval.append(k)
         self.frames[k] = (rgba, np.asarray(R, np.float32), np.asarray(t, np.float32))
@@ -70,6 +72,10 @@ class MappingPipeline:
         views = []
         for j, f in enumerate(views_ids):
             rgba, R, t = self.frames[f]
+            if f == self.last_frame:
+                # the frame just fused was raycast against this very volume: same result
+                views.append(A.View(self.cam, R, t, self.depth, self.color, rgba))
+                continue
             self.vol.raycast(self.cam, R, t, self.view_depth[j], self.view_color[j])
             views.append(A.View(self.cam, R, t, self.view_depth[j], self.view_color[j], rgba))
         for i in range(self.iterations):
