@@ -98,6 +98,11 @@ gps_status gps_volume_create(const gps_volume_config* cfg /*host*/, gps_stream_t
 void gps_volume_destroy(gps_volume* vol);
 /* Empties the volume (all blocks free, overflow flag cleared, frame counter reset).          */
 gps_status gps_volume_reset(gps_volume* vol, gps_stream_t stream);
+/* Copies the complete state of `src` into `dst` (device to device, on `stream`): hash, blocks,
+ * neighbour table, dense grid, counters and the sticky overflow flag.  Both volumes must have
+ * been created with identical configs.  A snapshot for concurrent readers (the Gaussian thread
+ * of P:116 reads a volume snapshot) or for replaying a sequence window.                      */
+gps_status gps_volume_copy(gps_volume* dst, const gps_volume* src, gps_stream_t stream);
 /* Synchronises `stream`, then reports the number of allocated blocks (may exceed the budget
  * when an overflow happened), the budget, the number of blocks marked visible by the last
  * gps_fuse, the sum of visible blocks over every integration since create/reset, and the sum

@@ -70,6 +70,7 @@ PROTOTYPES = {
     "gps_volume_create": (gps_status, [P(gps_volume_config), gps_stream_t, P(vp)]),
     "gps_volume_destroy": (None, [vp]),
     "gps_volume_reset": (gps_status, [vp, gps_stream_t]),
+    "gps_volume_copy": (gps_status, [vp, vp, gps_stream_t]),
     "gps_volume_stats_sync": (gps_status, [vp, gps_stream_t, P(i64), P(i64), P(i64), P(i64), P(i64)]),
     "gps_fuse": (gps_status, [vp, P(gps_intrinsics), P(gps_pose), vp, f32, vp, gps_stream_t]),
     "gps_raycast": (gps_status, [vp, P(gps_intrinsics), P(gps_pose), vp, vp, vp, gps_stream_t]),

@@ -97,6 +97,19 @@ class Volume:
     def reset(self, stream=None):
         N.check("gps_volume_reset", _L.gps_volume_reset(self.h, _stream(stream)))
 
+    def copy_from(self, other: "Volume", stream=None):
+        """Device-to-device copy of another volume's complete state (identical configs)."""
+        N.check("gps_volume_copy", _L.gps_volume_copy(self.h, other.h, _stream(stream)))
+
+    def clone(self, stream=None) -> "Volume":
+        v = Volume.__new__(Volume)
+        v.cfg = N.gps_volume_config.from_buffer_copy(self.cfg)
+        h = C.c_void_p()
+        N.check("gps_volume_create", _L.gps_volume_create(C.byref(v.cfg), _stream(stream), C.byref(h)))
+        v.h = h
+        v.copy_from(self, stream)
+        return v
+
     def fuse(self, cam: Camera, R, t, depth: torch.Tensor, depth_scale: float, rgba: torch.Tensor,
              stream=None):
         """depth: u16/i16 [H,W] raw sensor units; rgba: u8 [H,W,4].  CPU tensors are copied to

@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "common.cuh"
@@ -765,6 +766,31 @@ void gps_volume_destroy(gps_volume* vol) {
   cudaFree(v->view.ctr);
   if (v->flag.host) cudaFreeHost(v->flag.host);
   delete v;
+}
+
+gps_status gps_volume_copy(gps_volume* dst, const gps_volume* src, gps_stream_t stream) {
+  if (!dst || !src) return invalid("gps_volume_copy: null volume");
+  if (std::memcmp(&dst->cfg, &src->cfg, sizeof(gps_volume_config)) != 0)
+    return invalid("gps_volume_copy: volumes have different configs");
+  VolumeImpl* d = static_cast<VolumeImpl*>(dst);
+  const VolumeImpl* s = static_cast<const VolumeImpl*>(src);
+  cudaStream_t st = as_stream(stream);
+  const size_t slots = (size_t)s->cfg.hash_slots, nb = (size_t)s->cfg.max_blocks;
+  auto cp = [&](void* a, const void* b, size_t bytes) { return cudaMemcpyAsync(a, b, bytes, cudaMemcpyDeviceToDevice, st); };
+  GPS_CHECK_CUDA(cp(d->view.keys, s->view.keys, 8 * slots));
+  GPS_CHECK_CUDA(cp(d->view.vals, s->view.vals, 4 * slots));
+  GPS_CHECK_CUDA(cp(d->view.stamp, s->view.stamp, 4 * slots));
+  GPS_CHECK_CUDA(cp(d->view.tsdf, s->view.tsdf, 4 * 512 * nb));
+  GPS_CHECK_CUDA(cp(d->view.rgbw, s->view.rgbw, 4 * 512 * nb));
+  GPS_CHECK_CUDA(cp(d->view.vis, s->view.vis, 4 * nb));
+  GPS_CHECK_CUDA(cp(d->view.bkeys, s->view.bkeys, 8 * nb));
+  GPS_CHECK_CUDA(cp(d->view.nbr, s->view.nbr, 32 * nb));
+  GPS_CHECK_CUDA(cp(d->view.ctr, s->view.ctr, sizeof(VolumeCounters)));
+  if (s->view.grid)
+    GPS_CHECK_CUDA(cp(d->view.grid, s->view.grid, 4 * (size_t)s->view.gdx * s->view.gdy * s->view.gdz));
+  d->frame = s->frame;
+  *(volatile uint32_t*)d->flag.host = *(volatile uint32_t*)s->flag.host;
+  return GPS_OK;
 }
 
 gps_status gps_volume_reset(gps_volume* vol, gps_stream_t stream) {

@@ -42,11 +42,23 @@ class MappingPipeline:
         self.interval = []
         self.last_frame = None
         self.last_loss = None
+        self.copy_stream = torch.cuda.Stream()
         self.rounds = 0
         self.iterations_run = 0
 
     def _device(self, x: torch.Tensor) -> torch.Tensor:
-        return x if x.is_cuda else x.to("cuda", non_blocking=True)
+        """Host frames are uploaded on a dedicated copy stream (pinned memory -> async), so frame
+        k+1's upload overlaps frame k's kernels; the compute stream waits on an event."""
+        if x.is_cuda:
+            return x
+        compute = torch.cuda.current_stream()
+        with torch.cuda.stream(self.copy_stream):
+            d = x.to("cuda", non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(self.copy_stream)
+        compute.wait_event(ev)
+        d.record_stream(compute)
+        return d
 
     def process_frame(self, k: int, depth: torch.Tensor, rgba: torch.Tensor, R, t, refine: bool = True):
         depth = self._device(depth)
@@ -66,6 +78,28 @@ class MappingPipeline:
         for f in [f for f in self.frames if f not in keep]:
             del self.frames[f]
         return is_kf
+
+    def snapshot(self):
+        """Complete mapping state (device copies of the volume, Gaussians and Adam moments, plus
+        the host bookkeeping) for replaying a window of the sequence."""
+        import copy
+        return {"vol": self.vol.clone(), "g": self.g.clone(), "m": self.state.m.clone(), "v": self.state.v.clone(),
+                "step": self.state.step, "kf": (list(self.kf.keyframes), copy.deepcopy(self.kf._last)),
+                "frames": dict(self.frames), "interval": list(self.interval), "last_frame": self.last_frame,
+                "rng": copy.deepcopy(self.rng.bit_generator.state), "rounds": self.rounds,
+                "iterations_run": self.iterations_run}
+
+    def restore(self, s):
+        self.vol.copy_from(s["vol"])
+        for k in A.FIELDS:
+            getattr(self.g, k).copy_(getattr(s["g"], k))
+            getattr(self.state.m, k).copy_(getattr(s["m"], k))
+            getattr(self.state.v, k).copy_(getattr(s["v"], k))
+        self.state.step = s["step"]
+        self.kf.keyframes, self.kf._last = list(s["kf"][0]), s["kf"][1]
+        self.frames, self.interval, self.last_frame = dict(s["frames"]), list(s["interval"]), s["last_frame"]
+        self.rng.bit_generator.state = s["rng"]
+        self.rounds, self.iterations_run = s["rounds"], s["iterations_run"]
 
     def refine_round(self):
         views_ids = Sch.select_views(self.kf.keyframes, self.interval, self.rng, self.n_global, self.n_local)
