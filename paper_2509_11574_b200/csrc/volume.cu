@@ -245,29 +245,46 @@ __global__ void __launch_bounds__(256) k_integrate(VolumeView v, FuseParams p,
   const int li = e & 7, lj = (e >> 3) & 7, lk = e >> 6;
   __shared__ uint32_t scnt[8];
   uint32_t n_upd = 0;
-  for (uint32_t q = blockIdx.x; q < nvis; q += gridDim.x) {
+  // software pipeline over the CTA's blocks: the next block's (pool index, key) are loaded while
+  // the current one is integrated, and the voxel pair is loaded alongside the depth gather
+  uint32_t q = blockIdx.x;
+  int32_t b_next = -1;
+  uint64_t key_next = 0;
+  if (q < nvis) {
     const int32_t slot = v.vis[q];
-    const int32_t b = v.vals[slot];
+    b_next = v.vals[slot];
+    key_next = v.keys[slot];
+  }
+  for (; q < nvis; q += gridDim.x) {
+    const int32_t b = b_next;
+    const uint64_t key = key_next;
+    const uint32_t qn = q + gridDim.x;
+    if (qn < nvis) {
+      const int32_t slot = v.vis[qn];
+      b_next = v.vals[slot];
+      key_next = v.keys[slot];
+    }
     if (b < 0) continue;  // uniform across the CTA
     int bx, by, bz;
-    unpack_block(v.keys[slot], bx, by, bz);
+    unpack_block(key, bx, by, bz);
+    float2* tp = reinterpret_cast<float2*>(v.tsdf + (size_t)b * 512 + e);
+    uint2* cp = reinterpret_cast<uint2*>(v.rgbw + (size_t)b * 512 + e);
+    float2 ts = *tp;  // speculative: off the dependent chain (bandwidth is not the limit here)
+    uint2 cw = *cp;
     const int gx = bx * 8 + li, gy = by * 8 + lj, gz = bz * 8 + lk;
     uint32_t pix0 = 0, pix1 = 0;
     float s0 = 0.f, s1 = 0.f;
     const bool u0 = voxel_sample(p, gx, gy, gz, depth, pix0, s0);
     const bool u1 = voxel_sample(p, gx + 1, gy, gz, depth, pix1, s1);
-    if (u0 | u1) {  // a voxel pair nobody observes costs no load and no store
-      float2* tp = reinterpret_cast<float2*>(v.tsdf + (size_t)b * 512 + e);
-      uint2* cp = reinterpret_cast<uint2*>(v.rgbw + (size_t)b * 512 + e);
-      float2 ts = *tp;
-      uint2 cw = *cp;
+    if (u0 | u1) {
+      const uint32_t c0 = u0 ? __ldg(&rgba[pix0]) : 0u, c1 = u1 ? __ldg(&rgba[pix1]) : 0u;
       if (u0) {
-        const uint2 r = voxel_update(ts.x, cw.x, s0, __ldg(&rgba[pix0]), p.wmax, smagic);
+        const uint2 r = voxel_update(ts.x, cw.x, s0, c0, p.wmax, smagic);
         ts.x = __uint_as_float(r.x);
         cw.x = r.y;
       }
       if (u1) {
-        const uint2 r = voxel_update(ts.y, cw.y, s1, __ldg(&rgba[pix1]), p.wmax, smagic);
+        const uint2 r = voxel_update(ts.y, cw.y, s1, c1, p.wmax, smagic);
         ts.y = __uint_as_float(r.x);
         cw.y = r.y;
       }
@@ -425,12 +442,17 @@ __global__ void __launch_bounds__(256) k_range(VolumeView v, RayParams p, uint32
 struct BlockCache {
   int x, y, z;
   int32_t b;
+  int4 n0, n1;  // the block's +neighbour row, loaded once per block entry
 };
 
 __device__ __forceinline__ int32_t cached_find(const VolumeView& v, BlockCache& c, int x, int y, int z) {
   if (x == c.x && y == c.y && z == c.z) return c.b;
   c.x = x; c.y = y; c.z = z;
   c.b = find_block_fast(v, x, y, z);
+  if (c.b >= 0) {
+    c.n0 = __ldg(reinterpret_cast<const int4*>(v.nbr) + 2 * (size_t)c.b);
+    c.n1 = __ldg(reinterpret_cast<const int4*>(v.nbr) + 2 * (size_t)c.b + 1);
+  }
   return c.b;
 }
 
@@ -448,8 +470,7 @@ __device__ __forceinline__ bool trilinear(const VolumeView& v, BlockCache& c0, f
   // one branch-free path for every sample: the base block's +neighbour row (one 32-byte load,
   // L1-resident along a ray) supplies the block of each corner; corners inside the base block
   // select b0 itself (entry 0)
-  const int4 n0 = reinterpret_cast<const int4*>(v.nbr)[2 * (size_t)b0];
-  const int4 n1 = reinterpret_cast<const int4*>(v.nbr)[2 * (size_t)b0 + 1];
+  const int4 n0 = c0.n0, n1 = c0.n1;
   float tv[8];
   size_t addr[8];
   bool ok = true;
@@ -531,7 +552,7 @@ __global__ void __launch_bounds__(256) k_raycast(VolumeView v, RayParams p, floa
   const float iqx = qx != 0.f ? 1.f / qx : INFINITY;
   const float iqy = qy != 0.f ? 1.f / qy : INFINITY;
   const float iqz = qz != 0.f ? 1.f / qz : INFINITY;
-  BlockCache c0{INT_MIN, INT_MIN, INT_MIN, -1};
+  BlockCache c0{INT_MIN, INT_MIN, INT_MIN, -1, make_int4(-1, -1, -1, -1), make_int4(-1, -1, -1, -1)};
   bool prev_valid = false, hit = false;
   float prev_f = 0.f, tstar = 0.f;
   int j = jstart;  // samples before jstart (and after jend) meet no allocated block: invalid
