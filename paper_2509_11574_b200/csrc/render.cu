@@ -833,113 +833,171 @@ constexpr int kAdamThreads = 256;
 // Raw-parameter gradient of one Gaussian from its 2D gradients (R-GRAD chain rule).  Outputs
 // gx[3], gls[3], gq[4], gop, dcol[3] (clamped channels zeroed) and the SH basis Y[16] at the view
 // direction (the SH gradient is Y[k] * dcol[ch]).
+// fp64 re-projection for the backward chain only (forward membership stays P32):
+// Sigma_2D can be ill-conditioned (thin, anisotropic Gaussians), and the conic-inverse VJP scales
+// fp32 rounding by cond(Sigma_2D)^2; B200's FP64 rate makes this per-Gaussian step cheap.
+struct ProjD {
+  double X[3], s[3], qh[4], qn, Rq[9], M[9], S[9], cu, cv, T[6], cxx, cxy, cyy, det;
+  bool clx, cly;
+};
+
+__device__ __forceinline__ void project_f64(const Cam& c, float lowpass, const float* p, const float* ls,
+                                            const float* q, ProjD& g) {
+  const double D0 = (double)p[0] - c.t[0], D1 = (double)p[1] - c.t[1], D2 = (double)p[2] - c.t[2];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) g.X[k] = (double)c.R[k] * D0 + (double)c.R[3 + k] * D1 + (double)c.R[6 + k] * D2;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) g.s[k] = exp((double)ls[k]);
+  const double q0 = q[0], q1 = q[1], q2 = q[2], q3 = q[3];
+  g.qn = sqrt(q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
+  const double iq = 1.0 / g.qn;
+  const double w = q0 * iq, x = q1 * iq, y = q2 * iq, z = q3 * iq;
+  g.qh[0] = w; g.qh[1] = x; g.qh[2] = y; g.qh[3] = z;
+  double* Rq = g.Rq;
+  Rq[0] = 1.0 - 2.0 * (y * y + z * z); Rq[1] = 2.0 * (x * y - w * z); Rq[2] = 2.0 * (x * z + w * y);
+  Rq[3] = 2.0 * (x * y + w * z); Rq[4] = 1.0 - 2.0 * (x * x + z * z); Rq[5] = 2.0 * (y * z - w * x);
+  Rq[6] = 2.0 * (x * z - w * y); Rq[7] = 2.0 * (y * z + w * x); Rq[8] = 1.0 - 2.0 * (x * x + y * y);
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int cc = 0; cc < 3; ++cc) g.M[3 * r + cc] = Rq[3 * r + cc] * g.s[cc];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int cc = 0; cc < 3; ++cc)
+      g.S[3 * r + cc] = g.M[3 * r] * g.M[3 * cc] + g.M[3 * r + 1] * g.M[3 * cc + 1] + g.M[3 * r + 2] * g.M[3 * cc + 2];
+  const double limx = 1.3 * ((double)c.W / (2.0 * c.fx)), limy = 1.3 * ((double)c.H / (2.0 * c.fy));
+  const double txz = g.X[0] / g.X[2], tyz = g.X[1] / g.X[2];
+  g.clx = (txz < -limx || txz > limx);
+  g.cly = (tyz < -limy || tyz > limy);
+  g.cu = txz < -limx ? -limx : (txz > limx ? limx : txz);
+  g.cv = tyz < -limy ? -limy : (tyz > limy ? limy : tyz);
+  const double iz = 1.0 / g.X[2];
+  const double J00 = c.fx * iz, J02 = -c.fx * g.cu * iz, J11 = c.fy * iz, J12 = -c.fy * g.cv * iz;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    g.T[k] = J00 * c.R[k * 3 + 0] + J02 * c.R[k * 3 + 2];
+    g.T[3 + k] = J11 * c.R[k * 3 + 1] + J12 * c.R[k * 3 + 2];
+  }
+  double U[6];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      U[3 * a + k] = g.T[3 * a] * g.S[k] + g.T[3 * a + 1] * g.S[3 + k] + g.T[3 * a + 2] * g.S[6 + k];
+  g.cxx = U[0] * g.T[0] + U[1] * g.T[1] + U[2] * g.T[2] + lowpass;
+  g.cxy = U[0] * g.T[3] + U[1] * g.T[4] + U[2] * g.T[5];
+  g.cyy = U[3] * g.T[3] + U[4] * g.T[4] + U[5] * g.T[5] + lowpass;
+  g.det = g.cxx * g.cyy - g.cxy * g.cxy;
+}
+
 __device__ __forceinline__ void chain3d(const RenderArgs& a, const gps_gaussians& g, int64_t i, float dpx, float dpy,
                                         float da, float db, float dcc, float dsig, float* dcol, float* gx,
                                         float* gls, float* gq, float& gop, float* Y, const float4* __restrict__ cgj) {
   const int nc = a.nc;
+  const float* p = g.xyz + 3 * i;
+  ProjD pr;
+  project_f64(a.cam, a.lowpass, p, g.log_scale + 3 * i, g.rot + 4 * i, pr);
+  SH h;
+  view_dir(a.cam, p, a.deg, h);
 #pragma unroll
-  for (int k = 0; k < 3; ++k) gx[k] = gls[k] = 0.f;
-        const float* p = g.xyz + 3 * i;
-        Proj pr;
-        project_p32(a.cam, a.near_z, a.lowpass, p, g.log_scale + 3 * i, g.rot + 4 * i, pr);
-        SH h;
-        view_dir(a.cam, p, a.deg, h);
+  for (int k = 0; k < 16; ++k) Y[k] = k < nc ? h.Y[k] : 0.f;
+  // opacity: sigma = sigmoid(o)
+  const float sig = 1.0f / (1.0f + __expf(-g.opacity_raw[i]));
+  gop = dsig * sig * (1.f - sig);
+  // colour -> view direction through the Jacobian Gc[ch][e] = sum_k SH_k,ch dY_k/d dir_e and
+  // the clamp bits that k_preprocess stored (clamped channels get zero gradient)
+  const float4 c0 = cgj[3 * i], c1 = cgj[3 * i + 1], c2 = cgj[3 * i + 2];
+  const uint32_t clamp = __float_as_uint(c2.y);
 #pragma unroll
-        for (int k = 0; k < 16; ++k) Y[k] = k < nc ? h.Y[k] : 0.f;
-        // opacity: sigma = sigmoid(o)
-        const float sig = 1.0f / (1.0f + __expf(-g.opacity_raw[i]));
-        gop = dsig * sig * (1.f - sig);
-        // colour -> view direction through the Jacobian Gc[ch][e] = sum_k SH_k,ch dY_k/d dir_e and
-        // the clamp bits that k_preprocess stored (clamped channels get zero gradient)
-        const float4 c0 = cgj[3 * i], c1 = cgj[3 * i + 1], c2 = cgj[3 * i + 2];
-        const uint32_t clamp = __float_as_uint(c2.y);
+  for (int ch = 0; ch < 3; ++ch)
+    if (clamp & (1u << ch)) dcol[ch] = 0.f;
+  const float Gc[9] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w, c2.x};
+  float ddir[3];
 #pragma unroll
-        for (int ch = 0; ch < 3; ++ch)
-          if (clamp & (1u << ch)) dcol[ch] = 0.f;
-        const float Gc[9] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w, c2.x};
-        float ddir[3];
+  for (int e = 0; e < 3; ++e) ddir[e] = dcol[0] * Gc[e] + dcol[1] * Gc[3 + e] + dcol[2] * Gc[6 + e];
+  const float dd = ddir[0] * h.dir[0] + ddir[1] * h.dir[1] + ddir[2] * h.dir[2];
+  const float invn = 1.f / h.dnorm;
+  double gxd[3];
 #pragma unroll
-        for (int e = 0; e < 3; ++e) ddir[e] = dcol[0] * Gc[e] + dcol[1] * Gc[3 + e] + dcol[2] * Gc[6 + e];
-        const float dd = ddir[0] * h.dir[0] + ddir[1] * h.dir[1] + ddir[2] * h.dir[2];
-        const float invn = 1.f / h.dnorm;
+  for (int e = 0; e < 3; ++e) gxd[e] = (double)((ddir[e] - h.dir[e] * dd) * invn);
+  // conic (a, b, c) -> Sigma_2D (cxx, cxy, cyy)
+  const double id = 1.0 / pr.det, id2 = id * id;
+  const double cxx = pr.cxx, cxy = pr.cxy, cyy = pr.cyy;
+  const double dcxx = da * (-cyy * cyy * id2) + db * (cxy * cyy * id2) + dcc * (id - cxx * cyy * id2);
+  const double dcyy = da * (id - cyy * cxx * id2) + db * (cxy * cxx * id2) + dcc * (-cxx * cxx * id2);
+  const double dcxy = da * (2.0 * cyy * cxy * id2) + db * (-id - 2.0 * cxy * cxy * id2) + dcc * (2.0 * cxx * cxy * id2);
+  // Sigma_2D = T S T^T + lowpass I
+  const double* T0 = pr.T;
+  const double* T1 = pr.T + 3;
+  double ST0[3], ST1[3];
 #pragma unroll
-        for (int e = 0; e < 3; ++e) gx[e] += (ddir[e] - h.dir[e] * dd) * invn;
-        // conic (a, b, c) -> Sigma_2D (cxx, cxy, cyy)
-        const float det = pr.det, id = 1.f / det, id2 = id * id;
-        const float cxx = pr.cxx, cxy = pr.cxy, cyy = pr.cyy;
-        const float dcxx = da * (-cyy * cyy * id2) + db * (cxy * cyy * id2) + dcc * (id - cxx * cyy * id2);
-        const float dcyy = da * (id - cyy * cxx * id2) + db * (cxy * cxx * id2) + dcc * (-cxx * cxx * id2);
-        const float dcxy = da * (2.f * cyy * cxy * id2) + db * (-id - 2.f * cxy * cxy * id2) + dcc * (2.f * cxx * cxy * id2);
-        // Sigma_2D = T S T^T + lowpass I
-        const float* T0 = pr.T;
-        const float* T1 = pr.T + 3;
-        float ST0[3], ST1[3];
+  for (int r = 0; r < 3; ++r) {
+    ST0[r] = pr.S[3 * r] * T0[0] + pr.S[3 * r + 1] * T0[1] + pr.S[3 * r + 2] * T0[2];
+    ST1[r] = pr.S[3 * r] * T1[0] + pr.S[3 * r + 1] * T1[1] + pr.S[3 * r + 2] * T1[2];
+  }
+  double dS[9], dT0[3], dT1[3];
 #pragma unroll
-        for (int r = 0; r < 3; ++r) {
-          ST0[r] = pr.S[3 * r] * T0[0] + pr.S[3 * r + 1] * T0[1] + pr.S[3 * r + 2] * T0[2];
-          ST1[r] = pr.S[3 * r] * T1[0] + pr.S[3 * r + 1] * T1[1] + pr.S[3 * r + 2] * T1[2];
-        }
-        float dS[9], dT0[3], dT1[3];
+  for (int j = 0; j < 3; ++j) {
 #pragma unroll
-        for (int j = 0; j < 3; ++j) {
+    for (int k = 0; k < 3; ++k) dS[3 * j + k] = dcxx * T0[j] * T0[k] + dcxy * T0[j] * T1[k] + dcyy * T1[j] * T1[k];
+    dT0[j] = 2.0 * dcxx * ST0[j] + dcxy * ST1[j];
+    dT1[j] = dcxy * ST0[j] + 2.0 * dcyy * ST1[j];
+  }
+  // T = J Wc  (Wc[r][c] = R[c][r])
+  double dJ00 = 0.0, dJ02 = 0.0, dJ11 = 0.0, dJ12 = 0.0;
 #pragma unroll
-          for (int k = 0; k < 3; ++k) dS[3 * j + k] = dcxx * T0[j] * T0[k] + dcxy * T0[j] * T1[k] + dcyy * T1[j] * T1[k];
-          dT0[j] = 2.f * dcxx * ST0[j] + dcxy * ST1[j];
-          dT1[j] = dcxy * ST0[j] + 2.f * dcyy * ST1[j];
-        }
-        // T = J Wc  (Wc[r][c] = R[c][r])
-        float dJ00 = 0.f, dJ02 = 0.f, dJ11 = 0.f, dJ12 = 0.f;
+  for (int j = 0; j < 3; ++j) {
+    dJ00 += dT0[j] * a.cam.R[j * 3 + 0];
+    dJ02 += dT0[j] * a.cam.R[j * 3 + 2];
+    dJ11 += dT1[j] * a.cam.R[j * 3 + 1];
+    dJ12 += dT1[j] * a.cam.R[j * 3 + 2];
+  }
+  const double z = pr.X[2], iz = 1.0 / z, iz2 = iz * iz;
+  const double fx = a.cam.fx, fy = a.cam.fy;
+  double dX[3] = {0.0, 0.0, 0.0};
+  dX[2] += dJ00 * (-fx * iz2) + dJ11 * (-fy * iz2);
+  const double dcu_dx = pr.clx ? 0.0 : iz, dcu_dz = pr.clx ? 0.0 : -pr.X[0] * iz2;
+  const double dcv_dy = pr.cly ? 0.0 : iz, dcv_dz = pr.cly ? 0.0 : -pr.X[1] * iz2;
+  dX[0] += dJ02 * (-fx * iz) * dcu_dx;
+  dX[2] += dJ02 * (fx * pr.cu * iz2 - fx * iz * dcu_dz);
+  dX[1] += dJ12 * (-fy * iz) * dcv_dy;
+  dX[2] += dJ12 * (fy * pr.cv * iz2 - fy * iz * dcv_dz);
+  dX[0] += dpx * fx * iz;
+  dX[1] += dpy * fy * iz;
+  dX[2] += dpx * (-fx * pr.X[0] * iz2) + dpy * (-fy * pr.X[1] * iz2);
 #pragma unroll
-        for (int j = 0; j < 3; ++j) {
-          dJ00 += dT0[j] * a.cam.R[j * 3 + 0];
-          dJ02 += dT0[j] * a.cam.R[j * 3 + 2];
-          dJ11 += dT1[j] * a.cam.R[j * 3 + 1];
-          dJ12 += dT1[j] * a.cam.R[j * 3 + 2];
-        }
-        const float z = pr.X[2], iz = 1.f / z, iz2 = iz * iz;
-        const float fx = a.cam.fx, fy = a.cam.fy;
-        float dX[3] = {0.f, 0.f, 0.f};
-        dX[2] += dJ00 * (-fx * iz2) + dJ11 * (-fy * iz2);
-        const float dcu_dx = pr.clx ? 0.f : iz, dcu_dz = pr.clx ? 0.f : -pr.X[0] * iz2;
-        const float dcv_dy = pr.cly ? 0.f : iz, dcv_dz = pr.cly ? 0.f : -pr.X[1] * iz2;
-        dX[0] += dJ02 * (-fx * iz) * dcu_dx;
-        dX[2] += dJ02 * (fx * pr.cu * iz2 - fx * iz * dcu_dz);
-        dX[1] += dJ12 * (-fy * iz) * dcv_dy;
-        dX[2] += dJ12 * (fy * pr.cv * iz2 - fy * iz * dcv_dz);
-        dX[0] += dpx * fx * iz;
-        dX[1] += dpy * fy * iz;
-        dX[2] += dpx * (-fx * pr.X[0] * iz2) + dpy * (-fy * pr.X[1] * iz2);
+  for (int r = 0; r < 3; ++r)
+    gx[r] = (float)(gxd[r] + a.cam.R[3 * r] * dX[0] + a.cam.R[3 * r + 1] * dX[1] + a.cam.R[3 * r + 2] * dX[2]);
+  // S = M M^T, M = Rq diag(s)
+  double dRq[9];
 #pragma unroll
-        for (int r = 0; r < 3; ++r) gx[r] += a.cam.R[3 * r] * dX[0] + a.cam.R[3 * r + 1] * dX[1] + a.cam.R[3 * r + 2] * dX[2];
-        // S = M M^T, M = Rq diag(s)
-        float dRq[9];
+  for (int l = 0; l < 3; ++l) {
+    double ds = 0.0;
 #pragma unroll
-        for (int l = 0; l < 3; ++l) {
-          float ds = 0.f;
+    for (int j = 0; j < 3; ++j) {
+      double dM = 0.0;
 #pragma unroll
-          for (int j = 0; j < 3; ++j) {
-            float dM = 0.f;
+      for (int k = 0; k < 3; ++k) dM += (dS[3 * j + k] + dS[3 * k + j]) * pr.M[3 * k + l];
+      dRq[3 * j + l] = dM * pr.s[l];
+      ds += dM * pr.Rq[3 * j + l];
+    }
+    gls[l] = (float)(ds * pr.s[l]);
+  }
+  const double qw = pr.qh[0], qx = pr.qh[1], qy = pr.qh[2], qz = pr.qh[3];
+  double dqh[4];
+  dqh[0] = dRq[1] * (-2.0 * qz) + dRq[2] * (2.0 * qy) + dRq[3] * (2.0 * qz) + dRq[5] * (-2.0 * qx) +
+           dRq[6] * (-2.0 * qy) + dRq[7] * (2.0 * qx);
+  dqh[1] = dRq[1] * (2.0 * qy) + dRq[2] * (2.0 * qz) + dRq[3] * (2.0 * qy) + dRq[4] * (-4.0 * qx) +
+           dRq[5] * (-2.0 * qw) + dRq[6] * (2.0 * qz) + dRq[7] * (2.0 * qw) + dRq[8] * (-4.0 * qx);
+  dqh[2] = dRq[0] * (-4.0 * qy) + dRq[1] * (2.0 * qx) + dRq[2] * (2.0 * qw) + dRq[3] * (2.0 * qx) +
+           dRq[5] * (2.0 * qz) + dRq[6] * (-2.0 * qw) + dRq[7] * (2.0 * qz) + dRq[8] * (-4.0 * qy);
+  dqh[3] = dRq[0] * (-4.0 * qz) + dRq[1] * (-2.0 * qw) + dRq[2] * (2.0 * qx) + dRq[3] * (2.0 * qw) +
+           dRq[4] * (-4.0 * qz) + dRq[5] * (2.0 * qy) + dRq[6] * (2.0 * qx) + dRq[7] * (2.0 * qy);
+  const double dot = dqh[0] * qw + dqh[1] * qx + dqh[2] * qy + dqh[3] * qz;
+  const double iqn = 1.0 / pr.qn;
 #pragma unroll
-            for (int k = 0; k < 3; ++k) dM += (dS[3 * j + k] + dS[3 * k + j]) * pr.M[3 * k + l];
-            dRq[3 * j + l] = dM * pr.s[l];
-            ds += dM * pr.Rq[3 * j + l];
-          }
-          gls[l] = ds * pr.s[l];
-        }
-        const float qw = pr.qh[0], qx = pr.qh[1], qy = pr.qh[2], qz = pr.qh[3];
-        float dqh[4];
-        dqh[0] = dRq[1] * (-2.f * qz) + dRq[2] * (2.f * qy) + dRq[3] * (2.f * qz) + dRq[5] * (-2.f * qx) +
-                 dRq[6] * (-2.f * qy) + dRq[7] * (2.f * qx);
-        dqh[1] = dRq[1] * (2.f * qy) + dRq[2] * (2.f * qz) + dRq[3] * (2.f * qy) + dRq[4] * (-4.f * qx) +
-                 dRq[5] * (-2.f * qw) + dRq[6] * (2.f * qz) + dRq[7] * (2.f * qw) + dRq[8] * (-4.f * qx);
-        dqh[2] = dRq[0] * (-4.f * qy) + dRq[1] * (2.f * qx) + dRq[2] * (2.f * qw) + dRq[3] * (2.f * qx) +
-                 dRq[5] * (2.f * qz) + dRq[6] * (-2.f * qw) + dRq[7] * (2.f * qz) + dRq[8] * (-4.f * qy);
-        dqh[3] = dRq[0] * (-4.f * qz) + dRq[1] * (-2.f * qw) + dRq[2] * (2.f * qx) + dRq[3] * (2.f * qw) +
-                 dRq[4] * (-4.f * qz) + dRq[5] * (2.f * qy) + dRq[6] * (2.f * qx) + dRq[7] * (2.f * qy);
-        const float dot = dqh[0] * qw + dqh[1] * qx + dqh[2] * qy + dqh[3] * qz;
-        const float iqn = 1.f / pr.qn;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) gq[k] = (dqh[k] - pr.qh[k] * dot) * iqn;
+  for (int k = 0; k < 4; ++k) gq[k] = (float)((dqh[k] - pr.qh[k] * dot) * iqn);
 }
 
 // k_chain: one thread per Gaussian with a non-zero 2D gradient.  ACCUM = 0 writes the 128-byte
