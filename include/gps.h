@@ -260,6 +260,10 @@ gps_status gps_render_stats_sync(const void* ws, gps_stream_t stream, int64_t* n
 gps_status gps_debug_export_blocks_sync(const gps_volume* vol, gps_stream_t stream,
                                         int32_t* coords, void* voxels, int64_t cap,
                                         int64_t* n /*host*/);
+/* Checks the tsdf apron invariant (every block's + face copy equals its owner
+ * voxel, NaN where the owning block is unallocated) over all allocated blocks, looking owners up
+ * in the hash table; *n_bad (host) = number of apron cells that differ.  Debug only.        */
+gps_status gps_debug_apron_check_sync(const gps_volume* vol, gps_stream_t stream, int64_t* n_bad /*host*/);
 /* Runs gps_raycast for (K, T) into temporary buffers while marking every tsdf voxel the march
  * reads; *unique_voxels (host) = their number.  Measures the raycast roofline's unit count
  * (4 bytes per unique voxel read + 16 bytes of output per pixel).  Allocates; debug only.     */

@@ -86,6 +86,7 @@ PROTOTYPES = {
     "gps_render_stats_sync": (gps_status, [vp, gps_stream_t, P(i64), P(i64), P(i64)]),
     "gps_debug_export_blocks_sync": (gps_status, [vp, gps_stream_t, vp, vp, i64, P(i64)]),
     "gps_debug_export_visible_sync": (gps_status, [vp, gps_stream_t, vp, i64, P(i64)]),
+    "gps_debug_apron_check_sync": (gps_status, [vp, gps_stream_t, P(i64)]),
     "gps_debug_raycast_footprint_sync": (gps_status, [vp, P(gps_intrinsics), P(gps_pose), gps_stream_t, P(i64)]),
     "gps_debug_render_lists_sync": (gps_status, [vp, gps_stream_t, vp, i64, vp, P(i64)]),
     "gps_profile_enable": (None, [C.c_int]),

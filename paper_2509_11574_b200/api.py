@@ -159,6 +159,13 @@ class Volume:
             v = vox[:k].cpu().numpy().view(VOXEL_DTYPE).reshape(k, 512)
         return c, v
 
+    def apron_mismatches(self, stream=None) -> int:
+        """Apron cells (the + face copies of the tsdf plane) that differ from their owner voxels;
+        0 after every fuse (debug; synchronises)."""
+        n = C.c_int64()
+        N.check("gps_debug_apron_check_sync", _L.gps_debug_apron_check_sync(self.h, _stream(stream), C.byref(n)))
+        return n.value
+
     def raycast_footprint(self, cam: Camera, R, t, stream=None) -> int:
         """Number of distinct tsdf voxels a raycast from (R, t) reads (debug; synchronises)."""
         n = C.c_int64()

@@ -79,16 +79,26 @@ struct VolumeCounters {
   unsigned long long upd_total;  // voxels updated over all integrations (measurement)
 };
 
+// tsdf plane layout of one block: 9 planes x 9 rows x 10 floats (x, y, z in [0, 8], x = 9 is
+// padding that keeps even-x voxel pairs 8-byte aligned).  The 8 trilinear corners of any sample
+// whose base voxel lies in the block are then at constant offsets from one address.
+constexpr int kTsdfSY = 10, kTsdfSZ = 90, kTsdfBlock = 810;
+__host__ __device__ __forceinline__ int tsdf_index(int x, int y, int z) { return x + kTsdfSY * y + kTsdfSZ * z; }
+
 struct VolumeView {  // passed by value to kernels
   uint64_t* keys;
   int32_t* vals;  // pool block index, -1 = none
   uint32_t* stamp;
-  float* tsdf;     // pool plane: tsdf[b * 512 + idx], NaN = unobserved
+  float* tsdf;     // pool plane: tsdf[b * kTsdfBlock + tsdf_index(x, y, z)], NaN = unobserved;
+                   // x, y, z in [0, 8]: the + faces (coordinate 8) are an apron copy of the
+                   // +neighbours' voxels (NaN where the neighbour is unallocated), kept exact by
+                   // k_apron after every integration
   uint32_t* rgbw;  // pool plane: r | g<<8 | b<<16 | w<<24
   int32_t* vis;  // visible slots
   uint64_t* bkeys;  // pool block index -> packed block key (for passes over all blocks)
   int32_t* nbr;     // pool block index -> 8 pool indices of the blocks at +(dx,dy,dz), dx,dy,dz in
                     // {0,1}, entry k = dx | dy<<1 | dz<<2 (entry 0 = itself; -1 = unallocated)
+  int32_t* nbrm;    // the same for the blocks at -(dx,dy,dz): whose aprons a block's voxels feed
   VolumeCounters* ctr;
   uint32_t slot_mask;
   uint32_t max_blocks;
@@ -113,7 +123,7 @@ __device__ __forceinline__ int32_t find_block(const VolumeView& v, int x, int y,
 __device__ __forceinline__ int32_t find_block_fast(const VolumeView& v, int x, int y, int z) {
   const unsigned ix = (unsigned)(x - v.gox), iy = (unsigned)(y - v.goy), iz = (unsigned)(z - v.goz);
   if (v.grid && ix < (unsigned)v.gdx && iy < (unsigned)v.gdy && iz < (unsigned)v.gdz)
-    return __ldg(&v.grid[((size_t)iz * v.gdy + iy) * v.gdx + ix]);
+    return __ldg(&v.grid[(iz * (unsigned)v.gdy + iy) * (unsigned)v.gdx + ix]);  // <= 2^30 cells (validated)
   return find_block(v, x, y, z);
 }
 

@@ -265,9 +265,12 @@ __global__ void __launch_bounds__(256) k_integrate(VolumeView v, FuseParams p,
       key_next = v.keys[slot];
     }
     if (b < 0) continue;  // uniform across the CTA
+    // the -neighbour row for the apron push, loaded here so its latency overlaps the gather
+    const int4 m0 = __ldg(reinterpret_cast<const int4*>(v.nbrm) + 2 * (size_t)b);
+    const int4 m1 = __ldg(reinterpret_cast<const int4*>(v.nbrm) + 2 * (size_t)b + 1);
     int bx, by, bz;
     unpack_block(key, bx, by, bz);
-    float2* tp = reinterpret_cast<float2*>(v.tsdf + (size_t)b * 512 + e);
+    float2* tp = reinterpret_cast<float2*>(v.tsdf + (size_t)b * kTsdfBlock + tsdf_index(li, lj, lk));
     uint2* cp = reinterpret_cast<uint2*>(v.rgbw + (size_t)b * 512 + e);
     float2 ts = *tp;  // speculative: off the dependent chain (bandwidth is not the limit here)
     uint2 cw = *cp;
@@ -291,6 +294,19 @@ __global__ void __launch_bounds__(256) k_integrate(VolumeView v, FuseParams p,
       *tp = ts;
       *cp = cw;
       n_upd += (uint32_t)u0 + (uint32_t)u1;
+      // apron push: an updated voxel with a coordinate 0 is an apron cell of the -neighbours
+      // across those faces (k_link's comment)
+      const int zyz = (lj == 0 ? 2 : 0) | (lk == 0 ? 4 : 0);
+      if (zyz | (li == 0)) {
+        const int32_t mm[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
+#pragma unroll
+        for (int k = 1; k < 8; ++k) {
+          if (mm[k] < 0) continue;
+          float* dst = v.tsdf + (size_t)mm[k] * kTsdfBlock + tsdf_index(li + 8 * (k & 1), lj + 8 * ((k >> 1) & 1), lk + 8 * (k >> 2));
+          if (u0 && (k & ~(zyz | (li == 0 ? 1 : 0))) == 0) dst[0] = ts.x;
+          if (u1 && (k & ~zyz) == 0) dst[1] = ts.y;   // voxel li+1 >= 1: never on the x face
+        }
+      }
     }
   }
 #pragma unroll
@@ -310,32 +326,63 @@ __global__ void k_reset_frame(VolumeCounters* ctr) {
 }
 
 // --------------------------------------------------------------------------------------------
-// k_link: neighbour table of the blocks allocated this frame.  Each new block b looks up its 7
-// +neighbours and writes itself into the table of each existing -neighbour; every (block, entry)
-// pair has exactly one writer value, so the concurrent updates cannot conflict.
+// k_link (one warp per block allocated this frame, before k_integrate):
+//  * neighbour tables: the new block b looks up its 7 +neighbours and 7 -neighbours and writes
+//    itself into the opposite table of each existing one; every (block, entry) has exactly one
+//    writer value, so concurrent updates cannot conflict;
+//  * apron pull: b's 217 apron cells (a coordinate equal to 8) take the current voxels of the
+//    +neighbours that own them (NaN where unallocated).  k_integrate then pushes every voxel it
+//    updates into the aprons of its -neighbours, so after each fuse every apron equals its
+//    owners: an apron changes only when its owner voxel is updated (pushed) or when its block is
+//    new (pulled here, before this frame's integration).
 // --------------------------------------------------------------------------------------------
+__device__ __forceinline__ void apron_cell(int c, int& x, int& y, int& z) {
+  // the x = 8 face (81 cells), the y = 8 face without x = 8 (72), the z = 8 face without both (64)
+  if (c < 81) { x = 8; y = c % 9; z = c / 9; }
+  else if (c < 153) { x = (c - 81) % 8; y = 8; z = (c - 81) / 8; }
+  else { x = (c - 153) % 8; y = (c - 153) / 8; z = 8; }
+}
+
 __global__ void __launch_bounds__(256) k_link(VolumeView v) {
   const uint32_t lo = min(v.ctr->n_prev, v.max_blocks), hi = min(v.ctr->n_blocks, v.max_blocks);
-  for (uint32_t b = lo + blockIdx.x * blockDim.x + threadIdx.x; b < hi; b += gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t b = lo + warp; b < hi; b += nwarps) {
     int x, y, z;
     unpack_block(v.bkeys[b], x, y, z);
-    v.nbr[8 * (size_t)b] = (int32_t)b;
-#pragma unroll
-    for (int k = 1; k < 8; ++k) {
+    int32_t mine = (int32_t)b;  // lanes 0-7: +neighbour k; lanes 8-15: -neighbour k - 8
+    if (lane < 16) {
+      const int k = lane & 7, sg = lane < 8 ? 1 : -1;
       const int dx = k & 1, dy = (k >> 1) & 1, dz = (k >> 2) & 1;
-      v.nbr[8 * (size_t)b + k] = find_block_fast(v, x + dx, y + dy, z + dz);
-      const int32_t m = find_block_fast(v, x - dx, y - dy, z - dz);
-      if (m >= 0) v.nbr[8 * (size_t)m + k] = (int32_t)b;
+      if (k) {
+        mine = find_block_fast(v, x + sg * dx, y + sg * dy, z + sg * dz);
+        // the existing neighbour's opposite table gets b
+        if (mine >= 0) (lane < 8 ? v.nbrm : v.nbr)[8 * (size_t)mine + k] = (int32_t)b;
+      }
+      (lane < 8 ? v.nbr : v.nbrm)[8 * (size_t)b + k] = mine;
+    }
+    int32_t nb[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) nb[k] = __shfl_sync(0xFFFFFFFFu, mine, k);
+    float* base = v.tsdf + (size_t)b * kTsdfBlock;
+    for (int c = lane; c < 217; c += 32) {
+      int ax, ay, az;
+      apron_cell(c, ax, ay, az);
+      const int k = (ax >> 3) | ((ay >> 3) << 1) | ((az >> 3) << 2);
+      int32_t o = -1;
+#pragma unroll
+      for (int q = 1; q < 8; ++q) o = q == k ? nb[q] : o;
+      base[tsdf_index(ax, ay, az)] = o >= 0 ? v.tsdf[(size_t)o * kTsdfBlock + tsdf_index(ax & 7, ay & 7, az & 7)]
+                                            : __uint_as_float(0x7FC00000u);
     }
   }
 }
 
-__global__ void k_fill_pool(float* tsdf, uint32_t* rgbw, size_t n) {
+__global__ void k_fill_pool(float* tsdf, uint32_t* rgbw, size_t nb) {
   const size_t stride = (size_t)gridDim.x * blockDim.x;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += stride) {
-    tsdf[i] = __uint_as_float(0x7FC00000u);  // unobserved (R-VOX initial tsdf 1, w = 0)
-    rgbw[i] = 0u;
-  }
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nb * kTsdfBlock; i += stride)
+    tsdf[i] = __uint_as_float(0x7FC00000u);  // unobserved (R-VOX initial tsdf 1, w = 0); apron: no owner
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nb * 512; i += stride) rgbw[i] = 0u;
 }
 
 __global__ void k_fill_u64(uint64_t* p, size_t n, uint64_t val) {
@@ -442,72 +489,82 @@ __global__ void __launch_bounds__(256) k_range(VolumeView v, RayParams p, uint32
 struct BlockCache {
   int x, y, z;
   int32_t b;
-  int4 n0, n1;  // the block's +neighbour row, loaded once per block entry
 };
 
 __device__ __forceinline__ int32_t cached_find(const VolumeView& v, BlockCache& c, int x, int y, int z) {
   if (x == c.x && y == c.y && z == c.z) return c.b;
   c.x = x; c.y = y; c.z = z;
   c.b = find_block_fast(v, x, y, z);
-  if (c.b >= 0) {
-    c.n0 = __ldg(reinterpret_cast<const int4*>(v.nbr) + 2 * (size_t)c.b);
-    c.n1 = __ldg(reinterpret_cast<const int4*>(v.nbr) + 2 * (size_t)c.b + 1);
-  }
   return c.b;
 }
 
-// trilinear tsdf (and colour) at voxel-unit position p; returns validity
-template <bool kColor, bool kFoot = false>
-__device__ __forceinline__ bool trilinear(const VolumeView& v, BlockCache& c0, float px, float py, float pz,
-                                          float& f, float* col, uint32_t* footprint = nullptr) {
+// trilinear as nested lerps (x, then y, then z) of corners numbered dx | dy<<1 | dz<<2
+__device__ __forceinline__ float lerp3(const float* c, float ax, float ay, float az) {
+  auto lerp = [](float a, float b, float t) { return fmaf(t, b - a, a); };
+  const float x00 = lerp(c[0], c[1], ax), x10 = lerp(c[2], c[3], ax);
+  const float x01 = lerp(c[4], c[5], ax), x11 = lerp(c[6], c[7], ax);
+  return lerp(lerp(x00, x10, ay), lerp(x01, x11, ay), az);
+}
+
+// entry k (= dx | dy<<1 | dz<<2) of a block's +neighbour row (n0 = entries 0-3, n1 = 4-7), by
+// selects (a dynamically indexed array would live in local memory)
+__device__ __forceinline__ int32_t nbr_entry(int32_t b0, int4 n0, int4 n1, int k) {
+  return (k & 4) ? ((k & 2) ? ((k & 1) ? n1.w : n1.z) : ((k & 1) ? n1.y : n1.x))
+                 : ((k & 2) ? ((k & 1) ? n0.w : n0.z) : ((k & 1) ? n0.y : b0));
+}
+
+// footprint diagnostic: mark the owner voxel (512-voxel numbering) of each of the 8 corners of the
+// sample whose base voxel is (lx, ly, lz) in block b0
+__device__ __forceinline__ void mark_footprint(const VolumeView& v, int32_t b0, int lx, int ly, int lz,
+                                               uint32_t* footprint) {
+  const int4 n0 = __ldg(reinterpret_cast<const int4*>(v.nbr) + 2 * (size_t)b0);
+  const int4 n1 = __ldg(reinterpret_cast<const int4*>(v.nbr) + 2 * (size_t)b0 + 1);
+#pragma unroll
+  for (int corner = 0; corner < 8; ++corner) {
+    const int dx = corner & 1, dy = (corner >> 1) & 1, dz = (corner >> 2) & 1;
+    const int k = (dx && lx == 7) | ((dy && ly == 7) << 1) | ((dz && lz == 7) << 2);
+    const int32_t b = nbr_entry(b0, n0, n1, k);
+    if (b < 0) continue;
+    const size_t a = (size_t)b * 512 + ((lx + dx) & 7) + 8 * ((ly + dy) & 7) + 64 * ((lz + dz) & 7);
+    atomicOr(&footprint[a >> 5], 1u << (a & 31));
+  }
+}
+
+// tsdf and colour at voxel-unit position p (the hit point); returns validity.  The tsdf corners
+// come from the apron layout, the colour corners from their owner voxels via the +neighbour row.
+__device__ __forceinline__ bool trilinear_color(const VolumeView& v, BlockCache& c0, float px, float py, float pz,
+                                                float& f, float* col) {
   const float fx = floorf(px), fy = floorf(py), fz = floorf(pz);
   const int gx = (int)fx, gy = (int)fy, gz = (int)fz;
   const float ax = px - fx, ay = py - fy, az = pz - fz;
   const int32_t b0 = cached_find(v, c0, gx >> 3, gy >> 3, gz >> 3);
   if (b0 < 0) return false;
   const int lx = gx & 7, ly = gy & 7, lz = gz & 7;
-  const bool nx = lx == 7, ny = ly == 7, nz = lz == 7;
-  // one branch-free path for every sample: the base block's +neighbour row (one 32-byte load,
-  // L1-resident along a ray) supplies the block of each corner; corners inside the base block
-  // select b0 itself (entry 0)
-  const int4 n0 = c0.n0, n1 = c0.n1;
+  const float* tb = v.tsdf + (size_t)b0 * kTsdfBlock + tsdf_index(lx, ly, lz);
   float tv[8];
-  size_t addr[8];
-  bool ok = true;
 #pragma unroll
-  for (int corner = 0; corner < 8; ++corner) {
-    const int dx = corner & 1, dy = (corner >> 1) & 1, dz = (corner >> 2) & 1;
-    const bool sx = dx && nx, sy = dy && ny, sz = dz && nz;
-    const int32_t b = sz ? (sy ? (sx ? n1.w : n1.z) : (sx ? n1.y : n1.x))
-                         : (sy ? (sx ? n0.w : n0.z) : (sx ? n0.y : b0));
-    ok &= b >= 0;
-    const int idx = ((lx + dx) & 7) + 8 * ((ly + dy) & 7) + 64 * ((lz + dz) & 7);
-    addr[corner] = (size_t)max(b, 0) * 512 + idx;
-    tv[corner] = v.tsdf[addr[corner]];
-    if (kFoot && b >= 0) atomicOr(&footprint[addr[corner] >> 5], 1u << (addr[corner] & 31));
-  }
-  // an unallocated corner, or an unobserved one (NaN): the sample is invalid
+  for (int corner = 0; corner < 8; ++corner) tv[corner] = tb[tsdf_index(corner & 1, (corner >> 1) & 1, (corner >> 2) & 1)];
   float chk = tv[0];
 #pragma unroll
   for (int corner = 1; corner < 8; ++corner) chk += tv[corner];
-  if (!ok || isnan(chk)) return false;
-  // trilinear as nested lerps (x, then y, then z)
-  auto lerp = [](float a, float b, float t) { return fmaf(t, b - a, a); };
-  const float x00 = lerp(tv[0], tv[1], ax), x10 = lerp(tv[2], tv[3], ax);
-  const float x01 = lerp(tv[4], tv[5], ax), x11 = lerp(tv[6], tv[7], ax);
-  f = lerp(lerp(x00, x10, ay), lerp(x01, x11, ay), az);
-  if (kColor) {
-    uint32_t cw[8];
+  if (isnan(chk)) return false;  // an unallocated or unobserved corner
+  f = lerp3(tv, ax, ay, az);
+  const int4 n0 = __ldg(reinterpret_cast<const int4*>(v.nbr) + 2 * (size_t)b0);
+  const int4 n1 = __ldg(reinterpret_cast<const int4*>(v.nbr) + 2 * (size_t)b0 + 1);
+  uint32_t cw[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) cw[k] = v.rgbw[addr[k]];
+  for (int corner = 0; corner < 8; ++corner) {
+    const int dx = corner & 1, dy = (corner >> 1) & 1, dz = (corner >> 2) & 1;
+    const int k = (dx && lx == 7) | ((dy && ly == 7) << 1) | ((dz && lz == 7) << 2);
+    // every corner's block is allocated here (its tsdf apron entry is not NaN)
+    cw[corner] = v.rgbw[(size_t)nbr_entry(b0, n0, n1, k) * 512 + ((lx + dx) & 7) + 8 * ((ly + dy) & 7) + 64 * ((lz + dz) & 7)];
+  }
 #pragma unroll
-    for (int ch = 0; ch < 3; ++ch) {
-      float c[8];
+  for (int ch = 0; ch < 3; ++ch) {
+    float c[8];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) c[k] = (float)((cw[k] >> (8 * ch)) & 0xFFu);
-      col[ch] = lerp(lerp(lerp(c[0], c[1], ax), lerp(c[2], c[3], ax), ay),
-                     lerp(lerp(c[4], c[5], ax), lerp(c[6], c[7], ax), ay), az);
-    }
+    for (int k = 0; k < 8; ++k) c[k] = (float)((cw[k] >> (8 * ch)) & 0xFFu);
+    col[ch] = lerp3(c, ax, ay, az);
   }
   return true;
 }
@@ -552,17 +609,29 @@ __global__ void __launch_bounds__(256) k_raycast(VolumeView v, RayParams p, floa
   const float iqx = qx != 0.f ? 1.f / qx : INFINITY;
   const float iqy = qy != 0.f ? 1.f / qy : INFINITY;
   const float iqz = qz != 0.f ? 1.f / qz : INFINITY;
-  BlockCache c0{INT_MIN, INT_MIN, INT_MIN, -1, make_int4(-1, -1, -1, -1), make_int4(-1, -1, -1, -1)};
+  BlockCache c0{INT_MIN, INT_MIN, INT_MIN, -1};
   bool prev_valid = false, hit = false;
   float prev_f = 0.f, tstar = 0.f;
   int j = jstart;  // samples before jstart (and after jend) meet no allocated block: invalid
   int n_iter = 0, n_skip = 0, n_invalid = 0;
+  // one structured body per grid index (the block lookup, then either the skip or the sample), so
+  // the warp reconverges every iteration
   while (j <= jend) {
     if (kDebug) ++n_iter;
     const float t = p.dmin + (float)j * p.voxel;
     const float px = fmaf(t, qx, ox), py = fmaf(t, qy, oy), pz = fmaf(t, qz, oz);
-    const int bx = (int)floorf(px) >> 3, by = (int)floorf(py) >> 3, bz = (int)floorf(pz) >> 3;
-    if (cached_find(v, c0, bx, by, bz) < 0) {
+    const float fx = floorf(px), fy = floorf(py), fz = floorf(pz);
+    const int gx = (int)fx, gy = (int)fy, gz = (int)fz;
+    const int bx = gx >> 3, by = gy >> 3, bz = gz >> 3;
+    // inside the dense grid the lookup is one cached load, done by every lane every step (no
+    // divergent cache-miss path); outside it (or without a grid) through the per-ray block cache
+    const unsigned ix = (unsigned)(bx - v.gox), iy = (unsigned)(by - v.goy), iz = (unsigned)(bz - v.goz);
+    int32_t b0;
+    if (v.grid && ix < (unsigned)v.gdx && iy < (unsigned)v.gdy && iz < (unsigned)v.gdz)
+      b0 = __ldg(&v.grid[(iz * (unsigned)v.gdy + iy) * (unsigned)v.gdx + ix]);
+    else
+      b0 = cached_find(v, c0, bx, by, bz);
+    if (b0 < 0) {
       // skip to the exit of this unallocated block (all its samples are invalid)
       const float ex = qx != 0.f ? ((qx > 0.f ? (float)(bx + 1) : (float)bx) * 8.f - ox) * iqx : INFINITY;
       const float ey = qy != 0.f ? ((qy > 0.f ? (float)(by + 1) : (float)by) * 8.f - oy) * iqy : INFINITY;
@@ -573,21 +642,31 @@ __global__ void __launch_bounds__(256) k_raycast(VolumeView v, RayParams p, floa
       j = max(j + 1, (jn <= (float)(p.J + 1)) ? (int)jn : p.J + 1);
       prev_valid = false;
       if (kDebug) ++n_skip;
-      continue;
-    }
-    float f;
-    const bool valid = trilinear<false, kDebug == 2>(v, c0, px, py, pz, f, nullptr, footprint);
-    if (kDebug && !valid) ++n_invalid;
-    if (j >= 1 && valid && f <= 0.f) {
-      if (prev_valid && prev_f > 0.f) {
-        tstar = (p.dmin + (float)(j - 1) * p.voxel) + p.voxel * prev_f / (prev_f - f);
-        hit = true;
+    } else {
+      // the 8 corners at constant offsets in the apron layout (NaN: unallocated or unobserved)
+      const float* tb = v.tsdf + (size_t)b0 * kTsdfBlock + tsdf_index(gx & 7, gy & 7, gz & 7);
+      float tv[8];
+#pragma unroll
+      for (int corner = 0; corner < 8; ++corner)
+        tv[corner] = tb[tsdf_index(corner & 1, (corner >> 1) & 1, (corner >> 2) & 1)];
+      if (kDebug == 2) mark_footprint(v, b0, gx & 7, gy & 7, gz & 7, footprint);
+      float chk = tv[0];
+#pragma unroll
+      for (int corner = 1; corner < 8; ++corner) chk += tv[corner];
+      const bool valid = !isnan(chk);
+      const float f = lerp3(tv, px - fx, py - fy, pz - fz);
+      if (kDebug && !valid) ++n_invalid;
+      if (j >= 1 && valid && f <= 0.f) {
+        if (prev_valid && prev_f > 0.f) {
+          tstar = (p.dmin + (float)(j - 1) * p.voxel) + p.voxel * prev_f / (prev_f - f);
+          hit = true;
+        }
+        break;
       }
-      break;
+      prev_valid = valid;
+      prev_f = f;
+      ++j;
     }
-    prev_valid = valid;
-    prev_f = f;
-    ++j;
   }
   float D = 0.f, col[3] = {0.f, 0.f, 0.f}, V[3] = {0.f, 0.f, 0.f};
   if (hit) {
@@ -595,7 +674,7 @@ __global__ void __launch_bounds__(256) k_raycast(VolumeView v, RayParams p, floa
     V[1] = p.t[1] + tstar * ry;
     V[2] = p.t[2] + tstar * rz;
     float fd;
-    if (trilinear<true>(v, c0, V[0] * p.inv_voxel, V[1] * p.inv_voxel, V[2] * p.inv_voxel, fd, col)) {
+    if (trilinear_color(v, c0, V[0] * p.inv_voxel, V[1] * p.inv_voxel, V[2] * p.inv_voxel, fd, col)) {
       D = tstar * inv;
       col[0] *= (1.f / 255.f); col[1] *= (1.f / 255.f); col[2] *= (1.f / 255.f);
     } else {
@@ -616,6 +695,21 @@ __global__ void __launch_bounds__(256) k_raycast(VolumeView v, RayParams p, floa
     vertex_out[3 * pix + 0] = V[0];
     vertex_out[3 * pix + 1] = V[1];
     vertex_out[3 * pix + 2] = V[2];
+  }
+}
+
+__global__ void k_apron_check(VolumeView v, unsigned long long* bad) {
+  const uint32_t nb = min(v.ctr->n_blocks, v.max_blocks);
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < (size_t)nb * 217; i += (size_t)gridDim.x * blockDim.x) {
+    const uint32_t b = (uint32_t)(i / 217);
+    int x, y, z;
+    apron_cell((int)(i % 217), x, y, z);
+    int bx, by, bz;
+    unpack_block(v.bkeys[b], bx, by, bz);
+    const int32_t o = find_block(v, bx + (x >> 3), by + (y >> 3), bz + (z >> 3));
+    const float want = o >= 0 ? v.tsdf[(size_t)o * kTsdfBlock + tsdf_index(x & 7, y & 7, z & 7)] : __uint_as_float(0x7FC00000u);
+    const float got = v.tsdf[(size_t)b * kTsdfBlock + tsdf_index(x, y, z)];
+    if (!((isnan(want) && isnan(got)) || __float_as_uint(want) == __float_as_uint(got))) atomicAdd(bad, 1ull);
   }
 }
 
@@ -641,10 +735,10 @@ __global__ void k_export_blocks(VolumeView v, int32_t* coords, Voxel* voxels, ui
     unpack_block(k, x, y, z);
     coords[3 * i] = x; coords[3 * i + 1] = y; coords[3 * i + 2] = z;
     if (voxels) {
-      const size_t base = (size_t)v.vals[s] * 512;
+      const size_t b = (size_t)v.vals[s];
       for (int e = 0; e < 512; ++e) {
-        const float t = v.tsdf[base + e];
-        voxels[(size_t)i * 512 + e] = Voxel{isnan(t) ? 1.0f : t, v.rgbw[base + e]};
+        const float t = v.tsdf[b * kTsdfBlock + tsdf_index(e & 7, (e >> 3) & 7, e >> 6)];
+        voxels[(size_t)i * 512 + e] = Voxel{isnan(t) ? 1.0f : t, v.rgbw[b * 512 + e]};
       }
     }
   }
@@ -695,7 +789,7 @@ gps_status fill_volume(VolumeImpl* v, cudaStream_t s) {
   GPS_CHECK_LAUNCH("k_fill_u64");
   GPS_CHECK_CUDA(cudaMemsetAsync(v->view.vals, 0xFF, sizeof(int32_t) * c.hash_slots, s));
   GPS_CHECK_CUDA(cudaMemsetAsync(v->view.stamp, 0xFF, sizeof(uint32_t) * c.hash_slots, s));
-  k_fill_pool<<<1184, 256, 0, s>>>(v->view.tsdf, v->view.rgbw, (size_t)c.max_blocks * 512);
+  k_fill_pool<<<1184, 256, 0, s>>>(v->view.tsdf, v->view.rgbw, (size_t)c.max_blocks);
   GPS_CHECK_LAUNCH("k_fill_pool");
   GPS_CHECK_CUDA(cudaMemsetAsync(v->view.ctr, 0, sizeof(VolumeCounters), s));
   if (v->view.grid)
@@ -731,11 +825,12 @@ gps_status gps_volume_create(const gps_volume_config* cfg, gps_stream_t stream, 
   bool ok = cudaMalloc(&v->view.keys, sizeof(uint64_t) * slots) == cudaSuccess &&
             cudaMalloc(&v->view.vals, sizeof(int32_t) * slots) == cudaSuccess &&
             cudaMalloc(&v->view.stamp, sizeof(uint32_t) * slots) == cudaSuccess &&
-            cudaMalloc(&v->view.tsdf, sizeof(float) * 512 * nb) == cudaSuccess &&
+            cudaMalloc(&v->view.tsdf, sizeof(float) * kTsdfBlock * nb) == cudaSuccess &&
             cudaMalloc(&v->view.rgbw, sizeof(uint32_t) * 512 * nb) == cudaSuccess &&
             cudaMalloc(&v->view.vis, sizeof(int32_t) * nb) == cudaSuccess &&
             cudaMalloc(&v->view.bkeys, sizeof(uint64_t) * nb) == cudaSuccess &&
             cudaMalloc(&v->view.nbr, sizeof(int32_t) * 8 * nb) == cudaSuccess &&
+            cudaMalloc(&v->view.nbrm, sizeof(int32_t) * 8 * nb) == cudaSuccess &&
             cudaMalloc(&v->range, sizeof(uint32_t) * 2 * kMaxRangeTiles) == cudaSuccess &&
             cudaMalloc(&v->view.ctr, sizeof(VolumeCounters)) == cudaSuccess &&
             cudaHostAlloc(&v->flag.host, sizeof(uint32_t), cudaHostAllocMapped) == cudaSuccess &&
@@ -782,6 +877,7 @@ void gps_volume_destroy(gps_volume* vol) {
   cudaFree(v->view.vis);
   cudaFree(v->view.bkeys);
   cudaFree(v->view.nbr);
+  cudaFree(v->view.nbrm);
   if (v->view.grid) cudaFree(v->view.grid);
   cudaFree(v->range);
   cudaFree(v->view.ctr);
@@ -801,11 +897,12 @@ gps_status gps_volume_copy(gps_volume* dst, const gps_volume* src, gps_stream_t 
   GPS_CHECK_CUDA(cp(d->view.keys, s->view.keys, 8 * slots));
   GPS_CHECK_CUDA(cp(d->view.vals, s->view.vals, 4 * slots));
   GPS_CHECK_CUDA(cp(d->view.stamp, s->view.stamp, 4 * slots));
-  GPS_CHECK_CUDA(cp(d->view.tsdf, s->view.tsdf, 4 * 512 * nb));
+  GPS_CHECK_CUDA(cp(d->view.tsdf, s->view.tsdf, 4 * kTsdfBlock * nb));
   GPS_CHECK_CUDA(cp(d->view.rgbw, s->view.rgbw, 4 * 512 * nb));
   GPS_CHECK_CUDA(cp(d->view.vis, s->view.vis, 4 * nb));
   GPS_CHECK_CUDA(cp(d->view.bkeys, s->view.bkeys, 8 * nb));
   GPS_CHECK_CUDA(cp(d->view.nbr, s->view.nbr, 32 * nb));
+  GPS_CHECK_CUDA(cp(d->view.nbrm, s->view.nbrm, 32 * nb));
   GPS_CHECK_CUDA(cp(d->view.ctr, s->view.ctr, sizeof(VolumeCounters)));
   if (s->view.grid)
     GPS_CHECK_CUDA(cp(d->view.grid, s->view.grid, 4 * (size_t)s->view.gdx * s->view.gdy * s->view.gdz));
@@ -939,6 +1036,23 @@ gps_status gps_raycast(const gps_volume* vol, const gps_intrinsics* K, const gps
   gps_status st = check_sticky(vol);
   if (st != GPS_OK) return st;
   return raycast_impl(vol, K, T, depth_out, color_out, vertex_out, nullptr, stream);
+}
+
+gps_status gps_debug_apron_check_sync(const gps_volume* vol, gps_stream_t stream, int64_t* n_bad) {
+  if (!vol || !n_bad) return invalid("gps_debug_apron_check_sync: bad argument");
+  const VolumeImpl* v = static_cast<const VolumeImpl*>(vol);
+  cudaStream_t s = as_stream(stream);
+  unsigned long long* cnt = nullptr;
+  GPS_CHECK_CUDA(cudaMallocAsync(&cnt, 8, s));
+  GPS_CHECK_CUDA(cudaMemsetAsync(cnt, 0, 8, s));
+  k_apron_check<<<592, 256, 0, s>>>(v->view, cnt);
+  GPS_CHECK_LAUNCH("k_apron_check");
+  unsigned long long h = 0;
+  GPS_CHECK_CUDA(cudaMemcpyAsync(&h, cnt, 8, cudaMemcpyDeviceToHost, s));
+  GPS_CHECK_CUDA(cudaFreeAsync(cnt, s));
+  GPS_CHECK_CUDA(cudaStreamSynchronize(s));
+  *n_bad = (int64_t)h;
+  return GPS_OK;
 }
 
 gps_status gps_debug_raycast_footprint_sync(const gps_volume* vol, const gps_intrinsics* K, const gps_pose* T,

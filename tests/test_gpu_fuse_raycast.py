@@ -27,6 +27,18 @@ def compare_volumes(gvol, ovol, expect_min_blocks=1):
     return int((dt == 0).mean() * 100), len(oc)
 
 
+def test_apron_invariant_over_a_sequence():
+    """The tsdf plane's + face copies equal their owner voxels after every fuse (new blocks next
+    to old ones, blocks re-observed, blocks not visible this frame): cfg2, 6 frames."""
+    cfg = S.get_config("cfg2")
+    gcam, _ = H.cams(cfg)
+    vol = H.gpu_volume(cfg)
+    for fr in H.frames(cfg, 6):
+        d, c = H.to_dev(fr)
+        vol.fuse(gcam, fr.R, fr.t, d, cfg.depth_scale, c)
+        assert vol.apron_mismatches() == 0
+
+
 def test_fuse_cfg1_bit_exact():
     cfg = S.get_config("cfg1")
     frs = H.frames(cfg, 1)
