@@ -281,6 +281,28 @@ __device__ __forceinline__ float pair_q(float px, float py, float a, float b2, f
   const float inner = __fmaf_rn(pmul(b2, dx), dy, pmul(pmul(c, dy), dy));
   return __fmaf_rn(pmul(a, dx), dx, inner);
 }
+// Conservative test: can any pixel (x, y), x in [xa, xb], y in [ya, yb] (integers), pass the
+// prescribed-fp32 membership pair_q(...) <= qmax?  Per row, the x-interval of the ellipse
+// a dx^2 + 2b dx dy + c dy^2 <= qmax is centre px + m, half-width sqrt(m^2 - t); it is widened
+// by 1e-5 of the magnitudes of its terms (about 100x the fp32 rounding of either computation)
+// so that it only ever rejects strips no pixel of which passes.  Never decides membership.
+__device__ __forceinline__ bool ellipse_meets_strip(float px, float py, float a, float b2, float c, float qmax,
+                                                    int xa, int xb, int ya, int yb) {
+  const float ia = 1.0f / a, hb = 0.5f * b2;
+  for (int y = ya; y <= yb; ++y) {
+    const float dy = (float)y - py;
+    const float m = -hb * dy * ia;
+    const float cq = c * dy * dy;
+    const float t = (cq - qmax) * ia;
+    const float r2 = m * m - t;
+    const float marg = 1e-5f * (m * m + (cq + qmax) * ia) + 1e-4f;
+    if (r2 + marg < 0.f) continue;
+    const float h = sqrtf(r2 + marg) + 1e-3f;
+    if (px + m - h <= (float)xb && px + m + h >= (float)xa) return true;
+  }
+  return false;
+}
+
 __device__ __forceinline__ float pair_qmax(float L, float lnsig) {
   return fminf(9.0f, pmul(2.0f, padd(L, lnsig)));
 }
@@ -582,10 +604,18 @@ __global__ void __launch_bounds__(TILE* TILE) k_sort_blend(RenderArgs a, const f
   }
   if (threadIdx.x == 0) tile_end[t] = start + n_eff;
   // ---- front-to-back blend, Eqs. 1-3, early termination at the SDF depth ----
+  // Each warp compacts the staged batch 32 entries at a time: lane j tests entry j against the
+  // warp's rows and the warp's deepest pixel limit, a ballot keeps the survivors, and the warp
+  // walks only those in list order.  Every pixel still sees exactly the entries it saw before,
+  // in the same order, so W and C are bitwise unchanged.
   constexpr int kWarpRows = 32 / TILE;  // pixel rows covered by one warp
+  const int lane = threadIdx.x & 31;
   const int wy0 = ty * TILE + (threadIdx.x >> 5) * kWarpRows, wy1 = wy0 + kWarpRows - 1;
+  float wlim = inside ? lim : -INFINITY;  // the warp's largest limit: entries at or behind it
+#pragma unroll                            // contribute to none of its pixels (lists are sorted)
+  for (int o = 16; o > 0; o >>= 1) wlim = fmaxf(wlim, __shfl_xor_sync(0xFFFFFFFFu, wlim, o));
   float W = 0.f, C0 = 0.f, C1 = 0.f, C2 = 0.f;
-  bool done = !inside;
+  bool wdone = !(wlim > -INFINITY);  // warp-uniform
   for (int base = 0; base < n_eff; base += NT) {
     const int cnt = min(NT, n_eff - base);
     __syncthreads();
@@ -597,28 +627,42 @@ __global__ void __launch_bounds__(TILE* TILE) k_sort_blend(RenderArgs a, const f
       s2[threadIdx.x] = rec[4 * idx + 2];
     }
     __syncthreads();
-    if (!done) {
-      for (int k = 0; k < cnt; ++k) {
-        // warp-uniform row cull: the warp's pixels are rows [wy0, wy0 + rows) of the image
+    for (int kb = 0; kb < cnt && !wdone; kb += 32) {
+      const int k = kb + lane;
+      bool live = false, stop = false;
+      if (k < cnt) {
+        stop = !(s1[k].z < wlim);
         const uint32_t ry = __float_as_uint(s2[k].w);
-        if ((int)(ry >> 16) < wy0 || (int)(ry & 0xFFFFu) > wy1) continue;
-        const float4 r1 = s1[k];
-        if (!(r1.z < lim)) {  // sorted by depth: every later entry fails Eq. 1's indicator too
-          done = true;
-          break;
+        live = !stop && (int)(ry >> 16) >= wy0 && (int)(ry & 0xFFFFu) <= wy1;
+        if (live) {  // the ellipse itself must meet the warp's pixel strip
+          const float4 e0 = s0[k];
+          live = ellipse_meets_strip(e0.x, e0.y, e0.z, e0.w, s1[k].x, s1[k].w, tx * TILE, tx * TILE + TILE - 1,
+                                     wy0, wy1);
         }
-        const float4 r0 = s0[k];
+      }
+      uint32_t lm = __ballot_sync(0xFFFFFFFFu, live);
+      const uint32_t sm = __ballot_sync(0xFFFFFFFFu, stop);
+      if (sm) {
+        lm &= (1u << (__ffs(sm) - 1)) - 1u;  // survivors before the first stop
+        wdone = true;
+      }
+      while (lm) {
+        const int kk = kb + __ffs(lm) - 1;
+        lm &= lm - 1u;
+        const float4 r1 = s1[kk];
+        if (!(r1.z < lim)) continue;  // Eq. 1's indicator for this pixel
+        const float4 r0 = s0[kk];
         const float q = pair_q(r0.x, r0.y, r0.z, r0.w, r1.x, fx, fy);
         if (!(q <= r1.w)) continue;  // outside the 3-sigma ellipse or alpha < alpha_min
         const float al = __expf(fmaf(-0.5f, q, r1.y));  // sigma exp(-q/2), Eq. 3
-        const float4 r2 = s2[k];
+        const float4 r2 = s2[kk];
         W += al;
         C0 = fmaf(al, r2.x, C0);
         C1 = fmaf(al, r2.y, C1);
         C2 = fmaf(al, r2.z, C2);
       }
     }
-    if (__syncthreads_count(!done) == 0) break;
+    if (__syncthreads_count(!wdone) == 0) break;
   }
   // ---- Eq. 4 composite with W_t = 1, fused L1 ----
   float l1 = 0.f;
@@ -763,12 +807,29 @@ __global__ void __launch_bounds__(256) k_backward(RenderArgs a, const float4* __
     const int ka = kb < 0 ? -1 : (b3 ? (3 + kb < 5 ? 3 + kb : -1) : kb);
     vidx = (ka < 0 || (lane & 1)) ? -1 : (b4 ? (ka < 4 ? 5 + ka : -1) : ka);
   }
-  for (int e = (int)end - 1 - warp; e >= (int)start; e -= nw) {
-    const uint32_t idx = vals[e];
-    const float4 r0 = rec[4 * idx], r1 = rec[4 * idx + 1], r2 = rec[4 * idx + 2], r3 = rec[4 * idx + 3];
-    const float b2 = pmul(2.0f, r0.w), qmax = pair_qmax(a.ln_inv_amin, r1.y);
-    const float sig = __expf(r1.y);
-    const uint32_t rx = __float_as_uint(r1.w), ry = __float_as_uint(r2.w);
+  // entries are staged 256 at a time into shared memory by the whole CTA (independent loads),
+  // then each warp takes entries j = warp, warp + nw, ... of the batch
+  __shared__ float4 se0[256], se1[256], se2[256], se3[256];
+  __shared__ uint32_t sidx[256];
+  for (uint32_t base = start; base < end; base += 256) {
+    const int cnt_e = (int)min(256u, end - base);
+    __syncthreads();
+    for (int j = threadIdx.x; j < cnt_e; j += blockDim.x) {
+      const uint32_t id = vals[base + j];
+      sidx[j] = id;
+      const float4 q0 = rec[4 * id], q1 = rec[4 * id + 1], q2 = rec[4 * id + 2], q3 = rec[4 * id + 3];
+      se0[j] = q0;
+      se1[j] = make_float4(q1.x, q1.y, q1.z, pair_qmax(a.ln_inv_amin, q1.y));
+      se2[j] = make_float4(q2.x, q2.y, q2.z, __expf(q1.y));
+      se3[j] = make_float4(q3.x, q3.y, q1.w, q2.w);  // exact offsets, packed rect x / y ranges
+    }
+    __syncthreads();
+  for (int j = warp; j < cnt_e; j += nw) {
+    const uint32_t idx = sidx[j];
+    const float4 r0 = se0[j], r1 = se1[j], r2 = se2[j], r3 = se3[j];
+    const float b2 = pmul(2.0f, r0.w), qmax = r1.w;
+    const float sig = r2.w;
+    const uint32_t rx = __float_as_uint(r3.z), ry = __float_as_uint(r3.w);
     const int x0 = max((int)(rx & 0xFFFF), tx0), x1 = min((int)(rx >> 16), tx0 + TILE - 1);
     const int y0 = max((int)(ry & 0xFFFF), ty0), y1 = min((int)(ry >> 16), ty0 + TILE - 1);
     const int wx = x1 - x0 + 1, cnt = wx * (y1 - y0 + 1);
@@ -814,6 +875,7 @@ __global__ void __launch_bounds__(256) k_backward(RenderArgs a, const float4* __
     const float tot = l4[0] + __shfl_xor_sync(0xFFFFFFFFu, l4[0], 1);
     // 2D gradient slot layout: [px, py, a, b | c, sigma, r, g | b, flag, -, -]
     if (vidx >= 0) atomicAdd(grad2d + 12 * (size_t)idx + vidx, tot);
+  }
   }
 }
 
