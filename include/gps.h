@@ -262,7 +262,9 @@ gps_status gps_debug_export_blocks_sync(const gps_volume* vol, gps_stream_t stre
                                         int64_t* n /*host*/);
 /* Checks the tsdf apron invariant (every block's + face copy equals its owner
  * voxel, NaN where the owning block is unallocated) over all allocated blocks, looking owners up
- * in the hash table; *n_bad (host) = number of apron cells that differ.  Debug only.        */
+ * in the hash table, and the raycast's per-block count of cells <= 0 (DESIGN.md §4.4 (iii))
+ * against a recount; *n_bad (host) = apron cells that differ + blocks whose count is wrong.
+ * Debug only.                                                                               */
 gps_status gps_debug_apron_check_sync(const gps_volume* vol, gps_stream_t stream, int64_t* n_bad /*host*/);
 /* Runs gps_raycast for (K, T) into temporary buffers while marking every tsdf voxel the march
  * reads; *unique_voxels (host) = their number.  Measures the raycast roofline's unit count

@@ -99,6 +99,11 @@ struct VolumeView {  // passed by value to kernels
   int32_t* nbr;     // pool block index -> 8 pool indices of the blocks at +(dx,dy,dz), dx,dy,dz in
                     // {0,1}, entry k = dx | dy<<1 | dz<<2 (entry 0 = itself; -1 = unallocated)
   int32_t* nbrm;    // the same for the blocks at -(dx,dy,dz): whose aprons a block's voxels feed
+  int32_t* negcnt;  // pool block index -> number of cells of its tsdf plane (own voxels + apron)
+                    // holding a value <= 0 (NaN never counts); kept exact by k_link (apron pull)
+                    // and k_integrate (sign transitions of updated voxels and their apron pushes).
+                    // 0 means every valid trilinear sample based in the block is > 0, so the
+                    // raycast cannot find a +->- bracket there (DESIGN.md §4.4 (iii))
   VolumeCounters* ctr;
   uint32_t slot_mask;
   uint32_t max_blocks;

@@ -279,8 +279,10 @@ __global__ void __launch_bounds__(256) k_integrate(VolumeView v, FuseParams p,
     float s0 = 0.f, s1 = 0.f;
     const bool u0 = voxel_sample(p, gx, gy, gz, depth, pix0, s0);
     const bool u1 = voxel_sample(p, gx + 1, gy, gz, depth, pix1, s1);
+    int dneg0 = 0, dneg1 = 0;  // change of the "tsdf <= 0" indicator of each voxel (NaN: false)
     if (u0 | u1) {
       const uint32_t c0 = u0 ? __ldg(&rgba[pix0]) : 0u, c1 = u1 ? __ldg(&rgba[pix1]) : 0u;
+      const float old0 = ts.x, old1 = ts.y;
       if (u0) {
         const uint2 r = voxel_update(ts.x, cw.x, s0, c0, p.wmax, smagic);
         ts.x = __uint_as_float(r.x);
@@ -291,6 +293,8 @@ __global__ void __launch_bounds__(256) k_integrate(VolumeView v, FuseParams p,
         ts.y = __uint_as_float(r.x);
         cw.y = r.y;
       }
+      dneg0 = u0 ? (int)(ts.x <= 0.f) - (int)(old0 <= 0.f) : 0;
+      dneg1 = u1 ? (int)(ts.y <= 0.f) - (int)(old1 <= 0.f) : 0;
       *tp = ts;
       *cp = cw;
       n_upd += (uint32_t)u0 + (uint32_t)u1;
@@ -303,11 +307,19 @@ __global__ void __launch_bounds__(256) k_integrate(VolumeView v, FuseParams p,
         for (int k = 1; k < 8; ++k) {
           if (mm[k] < 0) continue;
           float* dst = v.tsdf + (size_t)mm[k] * kTsdfBlock + tsdf_index(li + 8 * (k & 1), lj + 8 * ((k >> 1) & 1), lk + 8 * (k >> 2));
-          if (u0 && (k & ~(zyz | (li == 0 ? 1 : 0))) == 0) dst[0] = ts.x;
-          if (u1 && (k & ~zyz) == 0) dst[1] = ts.y;   // voxel li+1 >= 1: never on the x face
+          const bool p0 = u0 && (k & ~(zyz | (li == 0 ? 1 : 0))) == 0;
+          const bool p1 = u1 && (k & ~zyz) == 0;  // voxel li+1 >= 1: never on the x face
+          if (p0) dst[0] = ts.x;
+          if (p1) dst[1] = ts.y;
+          // the apron cell held the owner's old value: same indicator change (rare: sign flips)
+          const int dn = (p0 ? dneg0 : 0) + (p1 ? dneg1 : 0);
+          if (dn) atomicAdd(&v.negcnt[mm[k]], dn);
         }
       }
     }
+    // the block's own cells: one warp-aggregated update (b is CTA-uniform, all lanes reach here)
+    const int dsum = __reduce_add_sync(0xFFFFFFFFu, dneg0 + dneg1);
+    if ((threadIdx.x & 31) == 0 && dsum) atomicAdd(&v.negcnt[b], dsum);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) n_upd += __shfl_xor_sync(0xFFFFFFFFu, n_upd, o);
@@ -365,6 +377,7 @@ __global__ void __launch_bounds__(256) k_link(VolumeView v) {
 #pragma unroll
     for (int k = 0; k < 8; ++k) nb[k] = __shfl_sync(0xFFFFFFFFu, mine, k);
     float* base = v.tsdf + (size_t)b * kTsdfBlock;
+    int nneg = 0;  // the new block's own voxels are unobserved: its count is its apron's
     for (int c = lane; c < 217; c += 32) {
       int ax, ay, az;
       apron_cell(c, ax, ay, az);
@@ -372,9 +385,13 @@ __global__ void __launch_bounds__(256) k_link(VolumeView v) {
       int32_t o = -1;
 #pragma unroll
       for (int q = 1; q < 8; ++q) o = q == k ? nb[q] : o;
-      base[tsdf_index(ax, ay, az)] = o >= 0 ? v.tsdf[(size_t)o * kTsdfBlock + tsdf_index(ax & 7, ay & 7, az & 7)]
-                                            : __uint_as_float(0x7FC00000u);
+      const float val = o >= 0 ? v.tsdf[(size_t)o * kTsdfBlock + tsdf_index(ax & 7, ay & 7, az & 7)]
+                               : __uint_as_float(0x7FC00000u);
+      base[tsdf_index(ax, ay, az)] = val;
+      nneg += (int)(val <= 0.f);
     }
+    nneg = __reduce_add_sync(0xFFFFFFFFu, nneg);
+    if (lane == 0) v.negcnt[b] = nneg;
   }
 }
 
@@ -610,6 +627,8 @@ __global__ void __launch_bounds__(256) k_raycast(VolumeView v, RayParams p, floa
   const float iqy = qy != 0.f ? 1.f / qy : INFINITY;
   const float iqz = qz != 0.f ? 1.f / qz : INFINITY;
   BlockCache c0{INT_MIN, INT_MIN, INT_MIN, -1};
+  int32_t pb = -1;    // the last allocated block the march entered, and whether its tsdf plane
+  bool ppos = false;  // holds no value <= 0 (negcnt == 0; cleared once its samples are skipped)
   bool prev_valid = false, hit = false;
   float prev_f = 0.f, tstar = 0.f;
   int j = jstart;  // samples before jstart (and after jend) meet no allocated block: invalid
@@ -631,16 +650,29 @@ __global__ void __launch_bounds__(256) k_raycast(VolumeView v, RayParams p, floa
       b0 = __ldg(&v.grid[(iz * (unsigned)v.gdy + iy) * (unsigned)v.gdx + ix]);
     else
       b0 = cached_find(v, c0, bx, by, bz);
-    if (b0 < 0) {
-      // skip to the exit of this unallocated block (all its samples are invalid)
+    if (b0 >= 0 && b0 != pb) {
+      pb = b0;
+      ppos = __ldg(&v.negcnt[b0]) == 0;
+    }
+    if (b0 < 0 || ppos) {
+      // exit of this block: first grid index at or past it, minus a 0.01-step margin against
+      // fp32 error (so jn never exceeds the true first index of the next block)
       const float ex = qx != 0.f ? ((qx > 0.f ? (float)(bx + 1) : (float)bx) * 8.f - ox) * iqx : INFINITY;
       const float ey = qy != 0.f ? ((qy > 0.f ? (float)(by + 1) : (float)by) * 8.f - oy) * iqy : INFINITY;
       const float ez = qz != 0.f ? ((qz > 0.f ? (float)(bz + 1) : (float)bz) * 8.f - oz) * iqz : INFINITY;
       const float texit = fminf(ex, fminf(ey, ez));
-      // first grid index at or past the exit, minus a 0.01-step margin against fp32 error
       const float jn = ceilf((texit - p.dmin) / p.voxel - 0.01f);
-      j = max(j + 1, (jn <= (float)(p.J + 1)) ? (int)jn : p.J + 1);
-      prev_valid = false;
+      const int jnext = (jn <= (float)(p.J + 1)) ? (int)jn : p.J + 1;
+      if (b0 < 0) {  // unallocated: all its samples are invalid
+        j = max(j + 1, jnext);
+        prev_valid = false;
+      } else {
+        // all-positive block: no sample based in it can end the march (a valid sample is a convex
+        // combination of > 0 corners), so only its last sample matters -- as the predecessor of
+        // the next block's first.  Jump there and evaluate it normally.
+        ppos = false;
+        j = max(j, jnext - 1);
+      }
       if (kDebug) ++n_skip;
     } else {
       // the 8 corners at constant offsets in the apron layout (NaN: unallocated or unobserved)
@@ -710,6 +742,19 @@ __global__ void k_apron_check(VolumeView v, unsigned long long* bad) {
     const float want = o >= 0 ? v.tsdf[(size_t)o * kTsdfBlock + tsdf_index(x & 7, y & 7, z & 7)] : __uint_as_float(0x7FC00000u);
     const float got = v.tsdf[(size_t)b * kTsdfBlock + tsdf_index(x, y, z)];
     if (!((isnan(want) && isnan(got)) || __float_as_uint(want) == __float_as_uint(got))) atomicAdd(bad, 1ull);
+  }
+}
+
+// negcnt invariant: recount the <= 0 cells of each allocated block's plane (own + apron)
+__global__ void k_negcnt_check(VolumeView v, unsigned long long* bad) {
+  const uint32_t nb = min(v.ctr->n_blocks, v.max_blocks);
+  const int lane = threadIdx.x & 31;
+  for (uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < nb; b += (gridDim.x * blockDim.x) >> 5) {
+    int n = 0;
+    for (int c = lane; c < 729; c += 32)
+      n += (int)(v.tsdf[(size_t)b * kTsdfBlock + tsdf_index(c % 9, (c / 9) % 9, c / 81)] <= 0.f);
+    n = __reduce_add_sync(0xFFFFFFFFu, n);
+    if (lane == 0 && n != v.negcnt[b]) atomicAdd(bad, 1ull);
   }
 }
 
@@ -791,6 +836,7 @@ gps_status fill_volume(VolumeImpl* v, cudaStream_t s) {
   GPS_CHECK_CUDA(cudaMemsetAsync(v->view.stamp, 0xFF, sizeof(uint32_t) * c.hash_slots, s));
   k_fill_pool<<<1184, 256, 0, s>>>(v->view.tsdf, v->view.rgbw, (size_t)c.max_blocks);
   GPS_CHECK_LAUNCH("k_fill_pool");
+  GPS_CHECK_CUDA(cudaMemsetAsync(v->view.negcnt, 0, sizeof(int32_t) * c.max_blocks, s));
   GPS_CHECK_CUDA(cudaMemsetAsync(v->view.ctr, 0, sizeof(VolumeCounters), s));
   if (v->view.grid)
     GPS_CHECK_CUDA(cudaMemsetAsync(v->view.grid, 0xFF,
@@ -831,6 +877,7 @@ gps_status gps_volume_create(const gps_volume_config* cfg, gps_stream_t stream, 
             cudaMalloc(&v->view.bkeys, sizeof(uint64_t) * nb) == cudaSuccess &&
             cudaMalloc(&v->view.nbr, sizeof(int32_t) * 8 * nb) == cudaSuccess &&
             cudaMalloc(&v->view.nbrm, sizeof(int32_t) * 8 * nb) == cudaSuccess &&
+            cudaMalloc(&v->view.negcnt, sizeof(int32_t) * nb) == cudaSuccess &&
             cudaMalloc(&v->range, sizeof(uint32_t) * 2 * kMaxRangeTiles) == cudaSuccess &&
             cudaMalloc(&v->view.ctr, sizeof(VolumeCounters)) == cudaSuccess &&
             cudaHostAlloc(&v->flag.host, sizeof(uint32_t), cudaHostAllocMapped) == cudaSuccess &&
@@ -878,6 +925,7 @@ void gps_volume_destroy(gps_volume* vol) {
   cudaFree(v->view.bkeys);
   cudaFree(v->view.nbr);
   cudaFree(v->view.nbrm);
+  cudaFree(v->view.negcnt);
   if (v->view.grid) cudaFree(v->view.grid);
   cudaFree(v->range);
   cudaFree(v->view.ctr);
@@ -903,6 +951,7 @@ gps_status gps_volume_copy(gps_volume* dst, const gps_volume* src, gps_stream_t 
   GPS_CHECK_CUDA(cp(d->view.bkeys, s->view.bkeys, 8 * nb));
   GPS_CHECK_CUDA(cp(d->view.nbr, s->view.nbr, 32 * nb));
   GPS_CHECK_CUDA(cp(d->view.nbrm, s->view.nbrm, 32 * nb));
+  GPS_CHECK_CUDA(cp(d->view.negcnt, s->view.negcnt, 4 * nb));
   GPS_CHECK_CUDA(cp(d->view.ctr, s->view.ctr, sizeof(VolumeCounters)));
   if (s->view.grid)
     GPS_CHECK_CUDA(cp(d->view.grid, s->view.grid, 4 * (size_t)s->view.gdx * s->view.gdy * s->view.gdz));
@@ -1047,6 +1096,8 @@ gps_status gps_debug_apron_check_sync(const gps_volume* vol, gps_stream_t stream
   GPS_CHECK_CUDA(cudaMemsetAsync(cnt, 0, 8, s));
   k_apron_check<<<592, 256, 0, s>>>(v->view, cnt);
   GPS_CHECK_LAUNCH("k_apron_check");
+  k_negcnt_check<<<592, 256, 0, s>>>(v->view, cnt);
+  GPS_CHECK_LAUNCH("k_negcnt_check");
   unsigned long long h = 0;
   GPS_CHECK_CUDA(cudaMemcpyAsync(&h, cnt, 8, cudaMemcpyDeviceToHost, s));
   GPS_CHECK_CUDA(cudaFreeAsync(cnt, s));
