@@ -320,9 +320,37 @@ struct SplatPtrs {
   WsHeader* hdr;
 };
 
+__device__ __forceinline__ void preprocess_one(const RenderArgs& a, const gps_gaussians& g, const SplatPtrs& w,
+                                               int64_t i, int (&trect)[4]);
+
+// Per Gaussian: the projection and record (preprocess_one), then, warp-cooperatively, the tile
+// counts of footprints spanning more than 4 tiles (one lane per tile instead of a serial loop)
+// and one aggregated n_visible update per warp.
 __global__ void __launch_bounds__(256) k_preprocess(RenderArgs a, gps_gaussians g, SplatPtrs w) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= a.n) return;
+  int tr[4] = {1, 0, 0, 0};  // tile rect tx0, tx1, ty0, ty1 of a listed Gaussian (tx0 > tx1: none)
+  if (i < a.n) preprocess_one(a, g, w, i, tr);
+  const bool listed = tr[0] <= tr[1];
+  const bool big = listed && (tr[1] - tr[0] + 1) * (tr[3] - tr[2] + 1) > 4;
+  const uint32_t lm = __ballot_sync(0xFFFFFFFFu, listed);
+  const int lane = threadIdx.x & 31;
+  if (lane == 0 && lm) atomicAdd(&w.hdr->n_visible, (uint32_t)__popc(lm));
+  uint32_t bm = __ballot_sync(0xFFFFFFFFu, big);
+  while (bm) {
+    const int src = __ffs(bm) - 1;
+    bm &= bm - 1u;
+    const int tx0 = __shfl_sync(0xFFFFFFFFu, tr[0], src), tx1 = __shfl_sync(0xFFFFFFFFu, tr[1], src);
+    const int ty0 = __shfl_sync(0xFFFFFFFFu, tr[2], src), ty1 = __shfl_sync(0xFFFFFFFFu, tr[3], src);
+    const int wx = tx1 - tx0 + 1, cnt = wx * (ty1 - ty0 + 1);
+    for (int k = lane; k < cnt; k += 32) {
+      const int ty = ty0 + k / wx, tx = tx0 + k % wx;
+      atomicAdd(&w.bigcounts[ty * a.tiles_x + tx], 1u);
+    }
+  }
+}
+
+__device__ __forceinline__ void preprocess_one(const RenderArgs& a, const gps_gaussians& g, const SplatPtrs& w,
+                                               int64_t i, int (&trect)[4]) {
   if (w.grad2d) {
     const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
     w.grad2d[3 * i] = z; w.grad2d[3 * i + 1] = z; w.grad2d[3 * i + 2] = z;
@@ -382,6 +410,7 @@ __global__ void __launch_bounds__(256) k_preprocess(RenderArgs a, gps_gaussians 
   w.rec[4 * i + 2] = make_float4(col[0], col[1], col[2], __uint_as_float(ry));
   w.rec[4 * i + 3] = make_float4(ddx, ddy, 0.f, 0.f);
   const int tx0 = pr.x0 / a.tile, tx1 = pr.x1 / a.tile, ty0 = pr.y0 / a.tile, ty1 = pr.y1 / a.tile;
+  trect[0] = tx0; trect[1] = tx1; trect[2] = ty0; trect[3] = ty1;
   if ((tx1 - tx0 + 1) * (ty1 - ty0 + 1) <= 4) {
     // the count atomic's old value is this Gaussian's slot inside the tile bucket: k_emit
     // scatters without atomics
@@ -390,11 +419,7 @@ __global__ void __launch_bounds__(256) k_preprocess(RenderArgs a, gps_gaussians 
     for (int ty = ty0; ty <= ty1; ++ty)
       for (int tx = tx0; tx <= tx1; ++tx) rk[k++] = atomicAdd(&w.counts[ty * a.tiles_x + tx], 1u);
     w.ranks[i] = make_uint4(rk[0], rk[1], rk[2], rk[3]);
-  } else {
-    for (int ty = ty0; ty <= ty1; ++ty)
-      for (int tx = tx0; tx <= tx1; ++tx) atomicAdd(&w.bigcounts[ty * a.tiles_x + tx], 1u);
   }
-  atomicAdd(&w.hdr->n_visible, 1u);
 }
 
 // ============================================================================================
@@ -456,13 +481,18 @@ __global__ void __launch_bounds__(256) k_emit(RenderArgs a, const float4* __rest
                                               const uint32_t* __restrict__ offsets, uint32_t* cursor,
                                               uint32_t* vals) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= a.n) return;
-  const float4 r1 = rec[4 * i + 1], r2 = rec[4 * i + 2];
-  const uint32_t rx = __float_as_uint(r1.w), ry = __float_as_uint(r2.w);
-  const int x0 = rx & 0xFFFF, x1 = rx >> 16, y0 = ry & 0xFFFF, y1 = ry >> 16;
-  if (x1 < x0) return;  // culled
-  const int tx0 = x0 / a.tile, tx1 = x1 / a.tile, ty0 = y0 / a.tile, ty1 = y1 / a.tile;
-  if ((tx1 - tx0 + 1) * (ty1 - ty0 + 1) <= 4) {
+  int tx0 = 1, tx1 = 0, ty0 = 0, ty1 = 0;
+  if (i < a.n) {
+    const float4 r1 = rec[4 * i + 1], r2 = rec[4 * i + 2];
+    const uint32_t rx = __float_as_uint(r1.w), ry = __float_as_uint(r2.w);
+    const int x0 = rx & 0xFFFF, x1 = rx >> 16, y0 = ry & 0xFFFF, y1 = ry >> 16;
+    if (x0 <= x1) {  // else culled
+      tx0 = x0 / a.tile; tx1 = x1 / a.tile; ty0 = y0 / a.tile; ty1 = y1 / a.tile;
+    }
+  }
+  const bool listed = tx0 <= tx1;
+  const bool big = listed && (tx1 - tx0 + 1) * (ty1 - ty0 + 1) > 4;
+  if (listed && !big) {
     const uint4 r4 = ranks[i];
     const uint32_t rk[4] = {r4.x, r4.y, r4.z, r4.w};
     int k = 0;
@@ -471,13 +501,24 @@ __global__ void __launch_bounds__(256) k_emit(RenderArgs a, const float4* __rest
         const uint32_t pos = offsets[ty * a.tiles_x + tx] + rk[k++];
         if (pos < a.cap) vals[pos] = (uint32_t)i;
       }
-  } else {  // large footprints: after the ranked entries of each tile, by an atomic cursor
-    for (int ty = ty0; ty <= ty1; ++ty)
-      for (int tx = tx0; tx <= tx1; ++tx) {
-        const int t = ty * a.tiles_x + tx;
-        const uint32_t pos = offsets[t] + counts[t] + atomicAdd(&cursor[t], 1u);
-        if (pos < a.cap) vals[pos] = (uint32_t)i;
-      }
+  }
+  // large footprints: after the ranked entries of each tile, by an atomic cursor -- the warp
+  // takes them one at a time, a lane per tile, so a footprint of T tiles costs ceil(T/32)
+  // atomic round trips instead of T serial ones
+  const int lane = threadIdx.x & 31;
+  uint32_t bm = __ballot_sync(0xFFFFFFFFu, big);
+  while (bm) {
+    const int src = __ffs(bm) - 1;
+    bm &= bm - 1u;
+    const int sx0 = __shfl_sync(0xFFFFFFFFu, tx0, src), sx1 = __shfl_sync(0xFFFFFFFFu, tx1, src);
+    const int sy0 = __shfl_sync(0xFFFFFFFFu, ty0, src), sy1 = __shfl_sync(0xFFFFFFFFu, ty1, src);
+    const uint32_t gi = (uint32_t)__shfl_sync(0xFFFFFFFFu, (uint32_t)i, src);
+    const int wx = sx1 - sx0 + 1, cnt = wx * (sy1 - sy0 + 1);
+    for (int k = lane; k < cnt; k += 32) {
+      const int t = (sy0 + k / wx) * a.tiles_x + sx0 + k % wx;
+      const uint32_t pos = offsets[t] + counts[t] + atomicAdd(&cursor[t], 1u);
+      if (pos < a.cap) vals[pos] = gi;
+    }
   }
 }
 

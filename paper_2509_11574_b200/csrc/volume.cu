@@ -307,19 +307,29 @@ __global__ void __launch_bounds__(256) k_integrate(VolumeView v, FuseParams p,
         for (int k = 1; k < 8; ++k) {
           if (mm[k] < 0) continue;
           float* dst = v.tsdf + (size_t)mm[k] * kTsdfBlock + tsdf_index(li + 8 * (k & 1), lj + 8 * ((k >> 1) & 1), lk + 8 * (k >> 2));
-          const bool p0 = u0 && (k & ~(zyz | (li == 0 ? 1 : 0))) == 0;
-          const bool p1 = u1 && (k & ~zyz) == 0;  // voxel li+1 >= 1: never on the x face
-          if (p0) dst[0] = ts.x;
-          if (p1) dst[1] = ts.y;
-          // the apron cell held the owner's old value: same indicator change (rare: sign flips)
-          const int dn = (p0 ? dneg0 : 0) + (p1 ? dneg1 : 0);
-          if (dn) atomicAdd(&v.negcnt[mm[k]], dn);
+          if (u0 && (k & ~(zyz | (li == 0 ? 1 : 0))) == 0) dst[0] = ts.x;
+          if (u1 && (k & ~zyz) == 0) dst[1] = ts.y;   // voxel li+1 >= 1: never on the x face
         }
       }
     }
-    // the block's own cells: one warp-aggregated update (b is CTA-uniform, all lanes reach here)
-    const int dsum = __reduce_add_sync(0xFFFFFFFFu, dneg0 + dneg1);
-    if ((threadIdx.x & 31) == 0 && dsum) atomicAdd(&v.negcnt[b], dsum);
+    // negcnt: the indicator changes of this warp's voxels, for the block itself and (the apron
+    // cell held the owner's old value) for every -neighbour whose apron they feed.  Sign flips
+    // are rare, so the warp first checks for any (b and the -neighbour row are CTA-uniform).
+    if (__any_sync(0xFFFFFFFFu, (dneg0 | dneg1) != 0)) {
+      const int lane = threadIdx.x & 31;
+      const int dsum = __reduce_add_sync(0xFFFFFFFFu, dneg0 + dneg1);
+      if (lane == 0 && dsum) atomicAdd(&v.negcnt[b], dsum);
+      const int zyz = (lj == 0 ? 2 : 0) | (lk == 0 ? 4 : 0) | (li == 0 ? 1 : 0);
+      const int32_t mm[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
+#pragma unroll
+      for (int k = 1; k < 8; ++k) {
+        // voxel li feeds -neighbour k iff k's axes are among its zero coordinates; li + 1 never
+        // lies on the x face
+        const int dn = ((k & ~zyz) == 0 ? dneg0 : 0) + ((k & ~(zyz & 6)) == 0 ? dneg1 : 0);
+        const int dk = __reduce_add_sync(0xFFFFFFFFu, dn);
+        if (lane == 0 && dk && mm[k] >= 0) atomicAdd(&v.negcnt[mm[k]], dk);
+      }
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) n_upd += __shfl_xor_sync(0xFFFFFFFFu, n_upd, o);
@@ -588,8 +598,8 @@ __device__ __forceinline__ bool trilinear_color(const VolumeView& v, BlockCache&
 
 // kDebug: 0 = production; 1 = per-pixel march statistics in vertex_out; 2 = mark every tsdf voxel
 // the march reads in `footprint` (the raycast roofline's unique-voxel count)
-template <int kDebug>
-__global__ void __launch_bounds__(256) k_raycast(VolumeView v, RayParams p, float* __restrict__ depth_out,
+template <int kDebug, int kMinCtas = 6>
+__global__ void __launch_bounds__(256, kMinCtas) k_raycast(VolumeView v, RayParams p, float* __restrict__ depth_out,
                                                  float* __restrict__ color_out,
                                                  float* __restrict__ vertex_out,
                                                  const uint32_t* __restrict__ tmin,
@@ -1071,8 +1081,17 @@ static gps_status raycast_impl(const gps_volume* vol, const gps_intrinsics* K, c
       k_raycast<2><<<g, 256, 0, s>>>(v->view, p, depth_out, color_out, nullptr, tmin, tmax, footprint);
     else if (dbg && vertex_out)
       k_raycast<1><<<g, 256, 0, s>>>(v->view, p, depth_out, color_out, vertex_out, tmin, tmax);
-    else
-      k_raycast<0><<<g, 256, 0, s>>>(v->view, p, depth_out, color_out, vertex_out, tmin, tmax);
+    else {
+      // occupancy variants for tuning (GPS_RAYCAST_CTAS = resident CTAs per SM the register
+      // budget targets; default 6 = 40 registers, no spills)
+      static const int ctas = getenv("GPS_RAYCAST_CTAS") ? atoi(getenv("GPS_RAYCAST_CTAS")) : 6;
+      if (ctas == 8)
+        k_raycast<0, 8><<<g, 256, 0, s>>>(v->view, p, depth_out, color_out, vertex_out, tmin, tmax);
+      else if (ctas == 4)
+        k_raycast<0, 4><<<g, 256, 0, s>>>(v->view, p, depth_out, color_out, vertex_out, tmin, tmax);
+      else
+        k_raycast<0, 6><<<g, 256, 0, s>>>(v->view, p, depth_out, color_out, vertex_out, tmin, tmax);
+    }
   }
   GPS_CHECK_LAUNCH("k_raycast");
   return GPS_OK;

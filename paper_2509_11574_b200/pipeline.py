@@ -3,9 +3,10 @@ once, then `iterations` refine steps), driving libgps through the C ABI.
 
 PAPER.md P:106 (per-frame fusion then raycast), P:138 (views raycast once per round)
 (every 10 frames, 20 iterations), P:129 (keyframes).  Readings R-VIEW, R-VIEWS (schedule.py).
-All compute is in libgps's kernels on one CUDA stream; this class only sequences calls and keeps
-the device buffers.  Frames may be device tensors, or host tensors (copied in on the stream --
-that is the end-to-end path).
+All compute is in libgps's kernels (fusion and raycasts on the caller's stream, refinement on a
+second stream when overlap=True); this class only sequences calls and keeps the device buffers.
+Frames may be device tensors, or host tensors (copied in on a copy stream -- that is the
+end-to-end path).
 """
 from __future__ import annotations
 
@@ -17,10 +18,20 @@ from . import schedule as Sch
 
 
 class MappingPipeline:
+    """overlap=True runs each round's refinement on a second stream while the following frames
+    are fused and raycast on the caller's stream -- the paper's two parallel threads (P:116,
+    "the SDF ... and the 3D Gaussian ... are executed in parallel").  The data dependencies are
+    those of the serial schedule: a round reads only its views' raycasts (taken at the round
+    frame), its targets and the Gaussians, none of which the fusion stream writes; view
+    buffers are double-buffered across rounds, and a round's buffer set is reused only after the
+    refinement that read it (two rounds earlier) has finished.  join() makes the caller's stream
+    wait for the refinement stream."""
+
     def __init__(self, cam: A.Camera, gaussians: A.Gaussians, volume: A.Volume, depth_scale: float,
                  render_cfg: A.RenderConfig | None = None, adam_cfg: A.AdamConfig | None = None,
                  delta_k: int = Sch.DELTA_K, iterations: int = Sch.ITERATIONS,
-                 n_global: int = Sch.N_GLOBAL, n_local: int = Sch.N_LOCAL, seed: int = 0):
+                 n_global: int = Sch.N_GLOBAL, n_local: int = Sch.N_LOCAL, seed: int = 0,
+                 overlap: bool = True):
         self.cam, self.g, self.vol = cam, gaussians, volume
         self.depth_scale = float(depth_scale)
         self.rcfg = render_cfg or A.RenderConfig()
@@ -33,16 +44,25 @@ class MappingPipeline:
         self.rng = np.random.default_rng(seed)
         H, W = cam.height, cam.width
         dev = torch.device("cuda")
-        self.depth = torch.empty((H, W), dtype=torch.float32, device=dev)   # D_t of the last frame
-        self.color = torch.empty((H, W, 3), dtype=torch.float32, device=dev)
+        # D_t / C_t of the last frame (aliases a view buffer when that frame is a round view)
+        self._fdepth = torch.empty((H, W), dtype=torch.float32, device=dev)
+        self._fcolor = torch.empty((H, W, 3), dtype=torch.float32, device=dev)
+        self.depth, self.color = self._fdepth, self._fcolor
         nv = n_global + n_local
-        self.view_depth = [torch.empty((H, W), dtype=torch.float32, device=dev) for _ in range(nv)]
-        self.view_color = [torch.empty((H, W, 3), dtype=torch.float32, device=dev) for _ in range(nv)]
+        nsets = 2
+        self.view_depth = [[torch.empty((H, W), dtype=torch.float32, device=dev) for _ in range(nv)]
+                           for _ in range(nsets)]
+        self.view_color = [[torch.empty((H, W, 3), dtype=torch.float32, device=dev) for _ in range(nv)]
+                           for _ in range(nsets)]
         self.frames = {}          # frame id -> (rgba device tensor, R, t) for keyframes and the interval
         self.interval = []
         self.last_frame = None
         self.last_loss = None
         self.copy_stream = torch.cuda.Stream()
+        self.overlap = overlap  # may be switched between rounds
+        self.refine_stream = torch.cuda.Stream()
+        self._set_free = [None] * nsets   # event: the refinement that last read buffer set s is done
+        self._refine_done = None
         self.rounds = 0
         self.iterations_run = 0
 
@@ -64,13 +84,24 @@ class MappingPipeline:
         depth = self._device(depth)
         rgba = self._device(rgba)
         self.vol.fuse(self.cam, R, t, depth, self.depth_scale, rgba)
-        self.vol.raycast(self.cam, R, t, self.depth, self.color)
         self.last_frame = k
         is_kf = self.kf.offer(k, R, t)
         self.interval.append(k)
         self.frames[k] = (rgba, np.asarray(R, np.float32), np.asarray(t, np.float32))
-        if refine and Sch.is_round_frame(k, self.delta_k):
-            self.refine_round()
+        round_now = refine and Sch.is_round_frame(k, self.delta_k)
+        views_ids = None
+        self.depth, self.color = self._fdepth, self._fcolor
+        if round_now:
+            views_ids = Sch.select_views(self.kf.keyframes, self.interval, self.rng, self.n_global, self.n_local)
+            s = self.rounds % len(self.view_depth)
+            self._wait_set(s)
+            if k in views_ids:
+                # the frame just fused is a view: its per-frame raycast is the view's
+                j = views_ids.index(k)
+                self.depth, self.color = self.view_depth[s][j], self.view_color[s][j]
+        self.vol.raycast(self.cam, R, t, self.depth, self.color)
+        if round_now:
+            self._refine_round(views_ids)
         if len(self.interval) >= self.delta_k or Sch.is_round_frame(k, self.delta_k):
             self.interval = []
         # keep device frames only for keyframes and the current interval
@@ -79,10 +110,29 @@ class MappingPipeline:
             del self.frames[f]
         return is_kf
 
+    def _wait_set(self, s: int):
+        ev = self._set_free[s]
+        if ev is not None:
+            torch.cuda.current_stream().wait_event(ev)
+
+    def join(self, stream=None):
+        """Order `stream` (default: the current stream) after all refinement issued so far."""
+        if self._refine_done is not None:
+            (stream or torch.cuda.current_stream()).wait_event(self._refine_done)
+
+    def loss_to(self, dst: torch.Tensor):
+        """Asynchronous copy of the last refinement loss into dst (e.g. pinned host memory),
+        ordered on the refinement stream so the fusion stream never waits for it."""
+        if self.last_loss is None:
+            return
+        with torch.cuda.stream(self.refine_stream if self.overlap else torch.cuda.current_stream()):
+            dst.copy_(self.last_loss, non_blocking=True)
+
     def snapshot(self):
         """Complete mapping state (device copies of the volume, Gaussians and Adam moments, plus
         the host bookkeeping) for replaying a window of the sequence."""
         import copy
+        self.join()
         return {"vol": self.vol.clone(), "g": self.g.clone(), "m": self.state.m.clone(), "v": self.state.v.clone(),
                 "step": self.state.step, "kf": (list(self.kf.keyframes), copy.deepcopy(self.kf._last)),
                 "frames": dict(self.frames), "interval": list(self.interval), "last_frame": self.last_frame,
@@ -90,6 +140,7 @@ class MappingPipeline:
                 "iterations_run": self.iterations_run}
 
     def restore(self, s):
+        self.join()
         self.vol.copy_from(s["vol"])
         for k in A.FIELDS:
             getattr(self.g, k).copy_(getattr(s["g"], k))
@@ -100,21 +151,44 @@ class MappingPipeline:
         self.frames, self.interval, self.last_frame = dict(s["frames"]), list(s["interval"]), s["last_frame"]
         self.rng.bit_generator.state = s["rng"]
         self.rounds, self.iterations_run = s["rounds"], s["iterations_run"]
+        if True:  # the refinement stream must see the restored state
+            ev = torch.cuda.Event()
+            ev.record(torch.cuda.current_stream())
+            self.refine_stream.wait_event(ev)
 
     def refine_round(self):
+        """A round at the current point of the sequence (views chosen now; the last frame's
+        raycast is recomputed into the round's buffers)."""
         views_ids = Sch.select_views(self.kf.keyframes, self.interval, self.rng, self.n_global, self.n_local)
+        self._wait_set(self.rounds % len(self.view_depth))
+        return self._refine_round(views_ids, reuse_last=False)
+
+    def _refine_round(self, views_ids, reuse_last: bool = True):
+        s = self.rounds % len(self.view_depth)
         views = []
         for j, f in enumerate(views_ids):
             rgba, R, t = self.frames[f]
-            if f == self.last_frame:
-                # the frame just fused was raycast against this very volume: same result
-                views.append(A.View(self.cam, R, t, self.depth, self.color, rgba))
-                continue
-            self.vol.raycast(self.cam, R, t, self.view_depth[j], self.view_color[j])
-            views.append(A.View(self.cam, R, t, self.view_depth[j], self.view_color[j], rgba))
-        for i in range(self.iterations):
-            v = views[Sch.view_for_iteration(i, len(views))]
-            self.last_loss = self.ras.refine_step(self.g, self.state, [v], self.adam)
+            if not (reuse_last and f == self.last_frame):
+                self.vol.raycast(self.cam, R, t, self.view_depth[s][j], self.view_color[s][j])
+            views.append(A.View(self.cam, R, t, self.view_depth[s][j], self.view_color[s][j], rgba))
+        if self.overlap:
+            ready = torch.cuda.Event()
+            ready.record(torch.cuda.current_stream())
+            rs = self.refine_stream
+            rs.wait_event(ready)
+            for v in views:
+                v.target_rgba.record_stream(rs)
+        else:
+            rs = torch.cuda.current_stream()
+            self.join(rs)  # after any refinement still running from an overlapped round
+        with torch.cuda.stream(rs):
+            for i in range(self.iterations):
+                v = views[Sch.view_for_iteration(i, len(views))]
+                self.last_loss = self.ras.refine_step(self.g, self.state, [v], self.adam, stream=rs)
+            done = torch.cuda.Event()
+            done.record(rs)
+        self._set_free[s] = done
+        self._refine_done = done
         self.rounds += 1
         self.iterations_run += self.iterations
         return views_ids
