@@ -39,6 +39,8 @@ def parse():
     ap.add_argument("--gaussians", type=int, default=0, help="override N (0 = config)")
     ap.add_argument("--sh-degree", type=int, default=3)
     ap.add_argument("--tile", type=int, default=16)
+    ap.add_argument("--sort-free", action="store_true",
+                    help="the paper's sort-free renderer (P:99-100) instead of the depth-sorted tile lists")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-profile", action="store_true", help="time without the per-launch event profiler")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -164,7 +166,8 @@ def run_ours(args):
     vol = G.Volume(voxel_size=cfg.voxel_size, max_blocks=cfg.max_blocks, hash_slots=cfg.hash_slots,
                    dense_bounds=S.scene_bounds(cfg))
     g = G.Gaussians.from_dict(gd)
-    pipe = MappingPipeline(cam, g, vol, cfg.depth_scale, G.RenderConfig(tile=args.tile), seed=rank,
+    rcfg = G.RenderConfig(tile=args.tile, sort_free=int(args.sort_free))
+    pipe = MappingPipeline(cam, g, vol, cfg.depth_scale, rcfg, seed=rank,
                            overlap=not args.no_overlap)
     k = 0
     for _ in range(args.history):  # build a steady-state volume (untimed, no rounds)
@@ -350,6 +353,7 @@ def workload_config(args, cfg, n_g, ws):
                         f"(SH deg {args.sh_degree}), voxel {cfg.voxel_size} m, delta_k=10, 20 iters/round, "
                         f"6 views/round (R-VIEW: 1 view/iteration); step = 10 frames",
             "frames_per_step": 10, "gaussians": n_g, "sh_degree": args.sh_degree, "tile": args.tile,
+            "renderer": "sort-free (P:99-100)" if args.sort_free else "depth-sorted tile lists",
             "resolution": [cfg.width, cfg.height], "history_frames": args.history,
             "parallelism": f"replicas x{ws} (independent sequences)",
             "streams": "fusion+raycast on one stream, refinement rounds on a second (P:116)"

@@ -173,6 +173,12 @@ typedef struct {
   int32_t tile;     /* 8 or 16: tile edge in pixels (accelerator only: output independent)   */
   int32_t tile_depth_precull; /* 0|1: drop list entries behind every pixel of the tile     */
   int64_t max_pairs; /* capacity of the (tile,Gaussian) pair list; 0 = 32*n + 65536         */
+  int32_t sort_free; /* 0: depth-sorted tile lists, each pixel stops at its first entry at or
+                      *    behind D_t + eps (sorted);
+                      * 1: the paper's sort-free rendering (Table 7): lists
+                      *    stay unsorted -- Eqs. 1-2 are order-free sums -- and every entry is
+                      *    depth-tested; same C*, W_G up to fp32 summation order               */
+  int32_t reserved;  /* 0                                                                     */
 } gps_render_config;
 
 size_t gps_render_workspace_size(int64_t n, const gps_intrinsics* K /*host*/,
@@ -262,7 +268,7 @@ gps_status gps_debug_export_blocks_sync(const gps_volume* vol, gps_stream_t stre
                                         int64_t* n /*host*/);
 /* Checks the tsdf apron invariant (every block's + face copy equals its owner
  * voxel, NaN where the owning block is unallocated) over all allocated blocks, looking owners up
- * in the hash table, and the raycast's per-block count of cells <= 0 (DESIGN.md §4.4 (iii))
+ * in the hash table, and the raycast's per-sub-block counts of cells <= 0 (DESIGN.md §4.4 (iii))
  * against a recount; *n_bad (host) = apron cells that differ + blocks whose count is wrong.
  * Debug only.                                                                               */
 gps_status gps_debug_apron_check_sync(const gps_volume* vol, gps_stream_t stream, int64_t* n_bad /*host*/);

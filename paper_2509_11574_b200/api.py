@@ -241,10 +241,11 @@ class RenderConfig:
     tile: int = 16
     tile_depth_precull: int = 1
     max_pairs: int = 0
+    sort_free: int = 0               # 1: the paper's sort-free rendering
 
     def c(self) -> N.gps_render_config:
         return N.gps_render_config(self.eps_depth, self.alpha_min, self.near_z, self.lowpass, self.tile,
-                                   self.tile_depth_precull, self.max_pairs)
+                                   self.tile_depth_precull, self.max_pairs, self.sort_free, 0)
 
 
 @dataclass

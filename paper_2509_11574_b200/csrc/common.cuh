@@ -79,11 +79,16 @@ struct VolumeCounters {
   unsigned long long upd_total;  // voxels updated over all integrations (measurement)
 };
 
-// tsdf plane layout of one block: 9 planes x 9 rows x 10 floats (x, y, z in [0, 8], x = 9 is
-// padding that keeps even-x voxel pairs 8-byte aligned).  The 8 trilinear corners of any sample
-// whose base voxel lies in the block are then at constant offsets from one address.
-constexpr int kTsdfSY = 10, kTsdfSZ = 90, kTsdfBlock = 810;
-__host__ __device__ __forceinline__ int tsdf_index(int x, int y, int z) { return x + kTsdfSY * y + kTsdfSZ * z; }
+// tsdf plane layout of one block (cells x, y, z in [0, 8]; a coordinate 8 is the apron copy of a
+// +neighbour's voxel): the cells with x < 8 as 9 planes x 9 rows of 8 floats -- every row is one
+// 32-byte sector (the block stride, 736 floats, is a whole number of sectors) -- then the x = 8
+// face, 9 x 9 floats, then 7 floats of padding.  The trilinear corners of a sample based at
+// (lx, ly, lz) are at constant offsets {0, 8, 72, 80} from its base cell, and its x + 1 corners
+// at the same offsets from lx + 1 (lx < 7) or at {0, 1, 9, 10} from face cell (ly, lz) (lx = 7).
+constexpr int kTsdfSY = 8, kTsdfSZ = 72, kTsdfFace = 648, kTsdfBlock = 736;
+__host__ __device__ __forceinline__ int tsdf_index(int x, int y, int z) {
+  return x < 8 ? x + kTsdfSY * y + kTsdfSZ * z : kTsdfFace + y + 9 * z;
+}
 
 struct VolumeView {  // passed by value to kernels
   uint64_t* keys;
@@ -99,17 +104,30 @@ struct VolumeView {  // passed by value to kernels
   int32_t* nbr;     // pool block index -> 8 pool indices of the blocks at +(dx,dy,dz), dx,dy,dz in
                     // {0,1}, entry k = dx | dy<<1 | dz<<2 (entry 0 = itself; -1 = unallocated)
   int32_t* nbrm;    // the same for the blocks at -(dx,dy,dz): whose aprons a block's voxels feed
-  int32_t* negcnt;  // pool block index -> number of cells of its tsdf plane (own voxels + apron)
-                    // holding a value <= 0 (NaN never counts); kept exact by k_link (apron pull)
-                    // and k_integrate (sign transitions of updated voxels and their apron pushes).
-                    // 0 means every valid trilinear sample based in the block is > 0, so the
-                    // raycast cannot find a +->- bracket there (DESIGN.md §4.4 (iii))
+  uint64_t* subneg;  // pool block index -> for each 4^3 sub-block s (byte s = sx + 2sy + 4sz),
+                     // the number of cells of its 5^3 corner region in the tsdf plane (cells
+                     // [4sx, 4sx + 4] x ..., apron included) holding a value <= 0 (NaN never
+                     // counts); kept exact by k_link (apron pull) and k_integrate (sign changes of
+                     // updated voxels and their apron pushes).  A zero byte means every valid
+                     // trilinear sample based in the sub-block is > 0, so the raycast cannot find
+                     // a +->- bracket there (DESIGN.md §4.4 (iii))
   VolumeCounters* ctr;
   uint32_t slot_mask;
   uint32_t max_blocks;
   int32_t* grid;  // optional dense block-index grid (nullable), -1 = unallocated
   int gox, goy, goz, gdx, gdy, gdz;
 };
+
+// subneg bytes (one bit per sub-block, as 1 << 8s) whose 5^3 corner region holds plane cell
+// (x, y, z), x, y, z in [0, 8]: along each axis cell 4 is shared by sub-blocks 0 and 1
+__host__ __device__ __forceinline__ uint64_t cell_subs(int x, int y, int z) {
+  const int mx = x == 4 ? 3 : (x < 4 ? 1 : 2), my = y == 4 ? 3 : (y < 4 ? 1 : 2), mz = z == 4 ? 3 : (z < 4 ? 1 : 2);
+  uint64_t w = 0;
+#pragma unroll
+  for (int s = 0; s < 8; ++s)
+    if (((mx >> (s & 1)) & (my >> ((s >> 1) & 1)) & (mz >> (s >> 2))) & 1) w |= 1ull << (8 * s);
+  return w;
+}
 
 // find a block: returns its pool index, or -1 if unallocated / unbacked
 __device__ __forceinline__ int32_t find_block(const VolumeView& v, int x, int y, int z) {

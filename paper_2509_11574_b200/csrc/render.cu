@@ -365,12 +365,29 @@ __device__ __forceinline__ void preprocess_one(const RenderArgs& a, const gps_ga
   SH h;
   view_dir(a.cam, g.xyz + 3 * i, a.deg, h);
   const float* sh = g.sh + (size_t)i * a.nc * 3;
+  // all of the Gaussian's SH coefficients in flight at once (fully unrolled; twelve 16-byte
+  // loads at degree 3, whose 192-byte rows are 16-byte aligned), instead of one dependent load
+  // per coefficient
+  const int nsh = 3 * a.nc;
+  float shv[48];
+  if (nsh == 48) {
+#pragma unroll
+    for (int j = 0; j < 12; ++j) {
+      const float4 q = __ldg(reinterpret_cast<const float4*>(sh) + j);
+      shv[4 * j] = q.x; shv[4 * j + 1] = q.y; shv[4 * j + 2] = q.z; shv[4 * j + 3] = q.w;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 48; ++j) shv[j] = j < nsh ? __ldg(sh + j) : 0.f;
+  }
   float col[3];
   uint32_t clamp = 0u;
 #pragma unroll
   for (int ch = 0; ch < 3; ++ch) {
     float acc = 0.f;
-    for (int k = 0; k < a.nc; ++k) acc = fmaf(h.Y[k], __ldg(&sh[3 * k + ch]), acc);
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+      if (k < a.nc) acc = fmaf(h.Y[k], shv[3 * k + ch], acc);
     col[ch] = fmaxf(acc + 0.5f, 0.0f);
     if (acc + 0.5f < 0.f) clamp |= 1u << ch;
   }
@@ -381,7 +398,7 @@ __device__ __forceinline__ void preprocess_one(const RenderArgs& a, const gps_ga
     for (int ch = 0; ch < 3; ++ch) {
       float wk[16];
 #pragma unroll
-      for (int k = 0; k < 16; ++k) wk[k] = k < a.nc ? __ldg(&sh[3 * k + ch]) : 0.f;
+      for (int k = 0; k < 16; ++k) wk[k] = shv[3 * k + ch];  // zero beyond the degree
       sh_basis_vjp(h.dir[0], h.dir[1], h.dir[2], a.deg, wk, Gc + 3 * ch);
     }
     w.cgj[3 * i] = make_float4(Gc[0], Gc[1], Gc[2], Gc[3]);
@@ -423,7 +440,8 @@ __device__ __forceinline__ void preprocess_one(const RenderArgs& a, const gps_ga
 }
 
 // ============================================================================================
-// k_scan: exclusive scan of the per-tile counts (one CTA, 1024 threads, chunked)
+// k_scan: exclusive scan of the per-tile counts (one CTA, 1024 threads x 4 consecutive tiles
+// per pass: one pass up to 4096 tiles, i.e. 1280x720 at 16x16)
 // ============================================================================================
 __global__ void __launch_bounds__(1024) k_scan(const uint32_t* __restrict__ counts,
                                                const uint32_t* __restrict__ bigcounts, uint32_t* offsets,
@@ -433,9 +451,12 @@ __global__ void __launch_bounds__(1024) k_scan(const uint32_t* __restrict__ coun
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int base = 0; base < n_tiles; base += 1024) {
-    const int i = base + threadIdx.x;
-    const uint32_t v = i < n_tiles ? counts[i] + bigcounts[i] : 0u;
+  for (int base = 0; base < n_tiles; base += 4096) {
+    const int i0 = base + 4 * threadIdx.x;
+    uint32_t c[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) c[k] = i0 + k < n_tiles ? counts[i0 + k] + bigcounts[i0 + k] : 0u;
+    const uint32_t v = c[0] + c[1] + c[2] + c[3];
     uint32_t x = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -445,19 +466,23 @@ __global__ void __launch_bounds__(1024) k_scan(const uint32_t* __restrict__ coun
     if (lane == 31) warp_sums[wid] = x;
     __syncthreads();
     if (wid == 0) {
-      uint32_t s = warp_sums[lane];
+      uint32_t sw = warp_sums[lane];
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, s, o);
-        if (lane >= o) s += y;
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, sw, o);
+        if (lane >= o) sw += y;
       }
-      warp_sums[lane] = s;  // inclusive
+      warp_sums[lane] = sw;  // inclusive
     }
     __syncthreads();
-    const uint32_t excl = carry + (wid ? warp_sums[wid - 1] : 0u) + x - v;
-    if (i < n_tiles) offsets[i] = excl;
+    uint32_t excl = carry + (wid ? warp_sums[wid - 1] : 0u) + x - v;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (i0 + k < n_tiles) offsets[i0 + k] = excl;
+      excl += c[k];
+    }
     __syncthreads();
-    if (threadIdx.x == 1023) carry = excl + v;
+    if (threadIdx.x == 1023) carry = excl;
     __syncthreads();
   }
   if (threadIdx.x == 0) {
@@ -573,7 +598,7 @@ struct BlendIO {
   int accumulate_loss;
 };
 
-template <int TILE>
+template <int TILE, bool SORTED>
 __global__ void __launch_bounds__(TILE* TILE) k_sort_blend(RenderArgs a, const float4* __restrict__ rec,
                                                           const uint32_t* __restrict__ offsets, uint32_t* vals,
                                                           uint64_t* gkeys, uint32_t* tile_end, float* loss_part,
@@ -588,8 +613,26 @@ __global__ void __launch_bounds__(TILE* TILE) k_sort_blend(RenderArgs a, const f
   const uint32_t start = min(offsets[t], a.cap);
   const uint32_t end = min(offsets[t + 1], a.cap);
   const int n = (int)(end - start);
-  // ---- per-tile sort by (depth bits, index) ----
-  if (n <= kMaxList) {
+  // ---- per-tile sort by (depth bits, index) (sort-free: the list stays in bucket order) ----
+  if (!SORTED) {
+  } else if (n <= NT) {
+    // short list (the common case): rank sort -- each key's rank is the number of smaller keys
+    // (keys are unique: the index is in the low word), two barriers instead of a bitonic network
+    uint64_t key = ~0ull;
+    if ((int)threadIdx.x < n) {
+      const uint32_t idx = vals[start + threadIdx.x];
+      key = ((uint64_t)__float_as_uint(rec[4 * idx + 1].z) << 32) | idx;
+      skeys[threadIdx.x] = key;
+    }
+    __syncthreads();
+    int rank = 0;
+    for (int j = 0; j < n; ++j) rank += skeys[j] < key;  // broadcast reads
+    __syncthreads();
+    if ((int)threadIdx.x < n) {
+      skeys[rank] = key;
+      vals[start + rank] = (uint32_t)key;
+    }
+  } else if (n <= kMaxList) {
     for (int e = threadIdx.x; e < n; e += NT) {
       const uint32_t idx = vals[start + e];
       const float d = rec[4 * idx + 1].z;
@@ -619,7 +662,7 @@ __global__ void __launch_bounds__(TILE* TILE) k_sort_blend(RenderArgs a, const f
   const float fx = (float)x, fy = (float)y;
   // optional pre-cull: entries at or behind every pixel's limit cannot contribute in this tile
   int n_eff = n;
-  if (precull) {
+  if (SORTED && precull) {
     float m = inside ? lim : -INFINITY;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
@@ -636,7 +679,7 @@ __global__ void __launch_bounds__(TILE* TILE) k_sort_blend(RenderArgs a, const f
       int lo = 0, hi = n;
       while (lo < hi) {
         const int mid = (lo + hi) >> 1;
-        const float d = rec[4 * vals[start + mid] + 1].z;
+        const float d = n <= kMaxList ? __uint_as_float((uint32_t)(skeys[mid] >> 32)) : rec[4 * vals[start + mid] + 1].z;
         if (d >= tmax) hi = mid; else lo = mid + 1;
       }
       n_eff = lo;
@@ -672,9 +715,12 @@ __global__ void __launch_bounds__(TILE* TILE) k_sort_blend(RenderArgs a, const f
       const int k = kb + lane;
       bool live = false, stop = false;
       if (k < cnt) {
-        stop = !(s1[k].z < wlim);
+        // sorted: the first entry at or behind the warp's deepest limit ends the warp's list;
+        // sort-free: such an entry is only skipped
+        const bool behind = !(s1[k].z < wlim);
+        stop = SORTED && behind;
         const uint32_t ry = __float_as_uint(s2[k].w);
-        live = !stop && (int)(ry >> 16) >= wy0 && (int)(ry & 0xFFFFu) <= wy1;
+        live = !behind && (int)(ry >> 16) >= wy0 && (int)(ry & 0xFFFFu) <= wy1;
         if (live) {  // the ellipse itself must meet the warp's pixel strip
           const float4 e0 = s0[k];
           live = ellipse_meets_strip(e0.x, e0.y, e0.z, e0.w, s1[k].x, s1[k].w, tx * TILE, tx * TILE + TILE - 1,
@@ -795,18 +841,16 @@ __device__ __forceinline__ void rs_level(const float* x, float* y, int lane, int
   }
 }
 
+// Per-pixel state of the backward for tile t (R-GRAD, Eq. 7 P:140 with Eq. 4): for a
+// pixel of the loss mask, (g0, g1, g2) = A dL/dC*_ch with A = 1 / (1 + W_G) and s = sum_ch g_ch C*_ch
+// (so dL/dalpha_i = sum_ch g_ch c_i,ch - s), and lim = D_t + eps (inf on an SDF miss); -inf for
+// pixels outside the image or the mask (no pair passes).
 template <int TILE>
-__global__ void __launch_bounds__(256) k_backward(RenderArgs a, const float4* __restrict__ rec,
-                                                  const uint32_t* __restrict__ offsets,
-                                                  const uint32_t* __restrict__ vals,
-                                                  const uint32_t* __restrict__ tile_end,
-                                                  const float* __restrict__ sdf_depth,
-                                                  const float* __restrict__ cstar, const float* __restrict__ wg,
-                                                  const uint32_t* __restrict__ target, const WsHeader* hdr,
-                                                  float* grad2d) {
+__device__ __forceinline__ uint32_t backward_pixel_state(const RenderArgs& a, int t, const float* __restrict__ sdf_depth,
+                                                         const float* __restrict__ cstar, const float* __restrict__ wg,
+                                                         const uint32_t* __restrict__ target, const WsHeader* hdr,
+                                                         float4* sgs, float* slim) {
   constexpr int NP = TILE * TILE;
-  __shared__ float sg0[NP], sg1[NP], sg2[NP], ss[NP], slim[NP];
-  const int t = blockIdx.x;
   const int tx = t % a.tiles_x, ty = t / a.tiles_x;
   const uint32_t m = hdr->mask_count;
   const float inv3m = m ? 1.0f / (3.0f * (float)m) : 0.0f;
@@ -831,8 +875,29 @@ __global__ void __launch_bounds__(256) k_backward(RenderArgs a, const float4* __
         lim = D > 0.f ? D + a.eps : INFINITY;
       }
     }
-    sg0[p] = g0; sg1[p] = g1; sg2[p] = g2; ss[p] = s; slim[p] = lim;
+    sgs[p] = make_float4(g0, g1, g2, s);
+    slim[p] = lim;
   }
+  return m;
+}
+
+template <int TILE>
+__global__ void __launch_bounds__(256) k_backward(RenderArgs a, const float4* __restrict__ rec,
+                                                  const uint32_t* __restrict__ offsets,
+                                                  const uint32_t* __restrict__ vals,
+                                                  const uint32_t* __restrict__ tile_end,
+                                                  const float* __restrict__ sdf_depth,
+                                                  const float* __restrict__ cstar, const float* __restrict__ wg,
+                                                  const uint32_t* __restrict__ target, const WsHeader* hdr,
+                                                  float* grad2d) {
+  constexpr int NP = TILE * TILE;
+  __shared__ float4 sgs[NP];  // per pixel (g0, g1, g2, s): A * dL/dC*_ch and A * sum_ch g_ch C*_ch
+  __shared__ float slim[NP];
+  __shared__ uint32_t smagic[TILE + 1];  // ceil(65536 / w), w = 1..TILE
+  if (threadIdx.x <= TILE) smagic[threadIdx.x] = threadIdx.x ? (65536u + threadIdx.x - 1u) / threadIdx.x : 0u;
+  const int t = blockIdx.x;
+  const int tx = t % a.tiles_x, ty = t / a.tiles_x;
+  const uint32_t m = backward_pixel_state<TILE>(a, t, sdf_depth, cstar, wg, target, hdr, sgs, slim);
   __syncthreads();
   if (!m) return;
   const uint32_t start = min(offsets[t], a.cap);
@@ -875,7 +940,7 @@ __global__ void __launch_bounds__(256) k_backward(RenderArgs a, const float4* __
     const int y0 = max((int)(ry & 0xFFFF), ty0), y1 = min((int)(ry >> 16), ty0 + TILE - 1);
     const int wx = x1 - x0 + 1, cnt = wx * (y1 - y0 + 1);
     // k / wx for k < 256, wx <= 16 as a multiply-high (exact; tests/test_abi.py)
-    const uint32_t magic = (65536u + (uint32_t)wx - 1u) / (uint32_t)wx;
+    const uint32_t magic = smagic[wx];
     float acc[9];
 #pragma unroll
     for (int k = 0; k < 9; ++k) acc[k] = 0.f;
@@ -891,9 +956,10 @@ __global__ void __launch_bounds__(256) k_backward(RenderArgs a, const float4* __
       const float qv = fmaf(r0.z * dx, dx, fmaf(2.f * r0.w * dx, dy, r1.x * dy * dy));
       const float ex = __expf(-0.5f * qv);
       const float al = sig * ex;
-      const float gA0 = sg0[p], gA1 = sg1[p], gA2 = sg2[p];
+      const float4 gs = sgs[p];
+      const float gA0 = gs.x, gA1 = gs.y, gA2 = gs.z;
       // dL/dalpha = A * sum_ch g_ch (c_ch - C*_ch)
-      const float dal = gA0 * r2.x + gA1 * r2.y + gA2 * r2.z - ss[p];
+      const float dal = gA0 * r2.x + gA1 * r2.y + gA2 * r2.z - gs.w;
       const float dpow = -al * dal;
       acc[0] = fmaf(-dpow, r0.z * dx + r0.w * dy, acc[0]);  // p_hat x
       acc[1] = fmaf(-dpow, r0.w * dx + r1.x * dy, acc[1]);  // p_hat y
@@ -917,6 +983,137 @@ __global__ void __launch_bounds__(256) k_backward(RenderArgs a, const float4* __
     // 2D gradient slot layout: [px, py, a, b | c, sigma, r, g | b, flag, -, -]
     if (vidx >= 0) atomicAdd(grad2d + 12 * (size_t)idx + vidx, tot);
   }
+  }
+}
+
+// --------------------------------------------------------------------------------------------
+// k_backward_items: the same gradient, computed per (entry, pixel group) instead of per entry.
+// The paper launches threads per Gaussian, each accumulating its gradient in registers, with
+// Gaussians split into fixed-size pixel groups so that all threads do the same number of
+// iterations (App. B).  Here, per tile: each listed entry's footprint inside the
+// tile (rect x tile, row-major) is cut into groups of kGroupPx pixels; one THREAD takes one
+// group, walks its pixels against the tile's pixel state in shared memory, keeps the 9 partial
+// sums in registers and issues 3 vector reductions -- no warp reduction and no idle lanes on
+// small footprints.
+// --------------------------------------------------------------------------------------------
+constexpr int kGroupPx = 32;
+
+template <int TILE>
+__global__ void __launch_bounds__(256) k_backward_items(RenderArgs a, const float4* __restrict__ rec,
+                                                        const uint32_t* __restrict__ offsets,
+                                                        const uint32_t* __restrict__ vals,
+                                                        const uint32_t* __restrict__ tile_end,
+                                                        const float* __restrict__ sdf_depth,
+                                                        const float* __restrict__ cstar, const float* __restrict__ wg,
+                                                        const uint32_t* __restrict__ target, const WsHeader* hdr,
+                                                        float* grad2d) {
+  constexpr int NP = TILE * TILE;
+  __shared__ float4 sgs[NP];
+  __shared__ float slim[NP];
+  __shared__ uint32_t smagic[TILE + 1];  // ceil(65536 / w), w = 1..TILE
+  if (threadIdx.x <= TILE) smagic[threadIdx.x] = threadIdx.x ? (65536u + threadIdx.x - 1u) / threadIdx.x : 0u;
+  const int t = blockIdx.x;
+  const int tx = t % a.tiles_x, ty = t / a.tiles_x;
+  const uint32_t m = backward_pixel_state<TILE>(a, t, sdf_depth, cstar, wg, target, hdr, sgs, slim);
+  __syncthreads();
+  if (!m) return;
+  const uint32_t start = min(offsets[t], a.cap);
+  const uint32_t end = min(tile_end[t], a.cap);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int tx0 = tx * TILE, ty0 = ty * TILE;
+  __shared__ float4 se0[256], se1[256], se2[256], se3[256];
+  __shared__ int4 sgeo[256];    // per entry: x0, y0, wx, cnt of rect x tile
+  __shared__ uint32_t sidx[256];
+  __shared__ int sitem[256];    // exclusive offsets of the entries' groups
+  __shared__ int swarp[8];
+  for (uint32_t base = start; base < end; base += 256) {
+    const int cnt_e = (int)min(256u, end - base);
+    __syncthreads();
+    int ng = 0;
+    const int j = threadIdx.x;
+    if (j < cnt_e) {
+      const uint32_t id = vals[base + j];
+      sidx[j] = id;
+      const float4 q0 = rec[4 * id], q1 = rec[4 * id + 1], q2 = rec[4 * id + 2], q3 = rec[4 * id + 3];
+      se0[j] = make_float4(q0.x, q0.y, q0.z, pmul(2.0f, q0.w));  // (px, py, a, 2b)
+      se1[j] = make_float4(q1.x, q0.w, q1.z, pair_qmax(a.ln_inv_amin, q1.y));  // (c, b, d, q_max)
+      se2[j] = make_float4(q2.x, q2.y, q2.z, __expf(q1.y));  // (r, g, b, sigma)
+      se3[j] = make_float4(q3.x, q3.y, 0.f, 0.f);  // exact centre offsets
+      const uint32_t rx = __float_as_uint(q1.w), ry = __float_as_uint(q2.w);
+      const int x0 = max((int)(rx & 0xFFFF), tx0), x1 = min((int)(rx >> 16), tx0 + TILE - 1);
+      const int y0 = max((int)(ry & 0xFFFF), ty0), y1 = min((int)(ry >> 16), ty0 + TILE - 1);
+      const int wx = x1 - x0 + 1, cnt = wx * (y1 - y0 + 1);
+      sgeo[j] = make_int4(x0, y0, wx, cnt);
+      ng = (cnt + kGroupPx - 1) / kGroupPx;
+    }
+    // exclusive scan of the group counts over the batch
+    int incl = ng;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if (lane == 31) swarp[warp] = incl;
+    __syncthreads();
+    int woff = 0, total = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      const int v = swarp[w];
+      woff += w < warp ? v : 0;
+      total += v;
+    }
+    sitem[j] = woff + incl - ng;
+    __syncthreads();
+    for (int it = threadIdx.x; it < total; it += blockDim.x) {
+      // the entry owning group `it`: the last entry whose first group is <= it
+      int lo = 0, hi = cnt_e - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (sitem[mid] <= it) lo = mid; else hi = mid - 1;
+      }
+      const int e = lo;
+      const int4 geo = sgeo[e];
+      const float4 r0 = se0[e], r1 = se1[e], r2 = se2[e], r3 = se3[e];
+      const uint32_t magic = smagic[geo.z];
+      const int k0 = (it - sitem[e]) * kGroupPx, k1 = min(geo.w, k0 + kGroupPx);
+      float acc[9];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) acc[k] = 0.f;
+      bool any = false;
+      for (int k = k0; k < k1; ++k) {
+        const int row = (int)(((uint32_t)k * magic) >> 16);
+        const int x = geo.x + (k - row * geo.z), y = geo.y + row;
+        const int p = (y - ty0) * TILE + (x - tx0);
+        if (!(r1.z < slim[p])) continue;  // Eq. 1 indicator (and inactive pixels)
+        const float q = pair_q(r0.x, r0.y, r0.z, r0.w, r1.x, (float)x, (float)y);
+        if (!(q <= r1.w)) continue;
+        const float dx = ((float)x - r0.x) - r3.x, dy = ((float)y - r0.y) - r3.y;  // exact offsets
+        const float qv = fmaf(r0.z * dx, dx, fmaf(2.f * r1.y * dx, dy, r1.x * dy * dy));
+        const float ex = __expf(-0.5f * qv);
+        const float al = r2.w * ex;
+        const float4 gs = sgs[p];
+        // dL/dalpha = A * sum_ch g_ch (c_ch - C*_ch)
+        const float dal = gs.x * r2.x + gs.y * r2.y + gs.z * r2.z - gs.w;
+        const float dpow = -al * dal;
+        acc[0] = fmaf(-dpow, r0.z * dx + r1.y * dy, acc[0]);  // p_hat x
+        acc[1] = fmaf(-dpow, r1.y * dx + r1.x * dy, acc[1]);  // p_hat y
+        acc[2] = fmaf(dpow * 0.5f, dx * dx, acc[2]);           // conic a
+        acc[3] = fmaf(dpow, dx * dy, acc[3]);                  // conic b
+        acc[4] = fmaf(dpow * 0.5f, dy * dy, acc[4]);           // conic c
+        acc[5] = fmaf(dal, ex, acc[5]);                        // sigma
+        acc[6] = fmaf(gs.x, al, acc[6]);                       // colour r, g, b
+        acc[7] = fmaf(gs.y, al, acc[7]);
+        acc[8] = fmaf(gs.z, al, acc[8]);
+        any = true;
+      }
+      if (any) {
+        // 2D gradient slot layout: [px, py, a, b | c, sigma, r, g | b, flag, -, -]
+        float* gp = grad2d + 12 * (size_t)sidx[e];
+        red_add_v4(reinterpret_cast<float4*>(gp), acc[0], acc[1], acc[2], acc[3]);
+        red_add_v4(reinterpret_cast<float4*>(gp + 4), acc[4], acc[5], acc[6], acc[7]);
+        atomicAdd(gp + 8, acc[8]);
+      }
+    }
   }
 }
 
@@ -1158,96 +1355,124 @@ struct AdamSrc {
   int has_gout;
 };
 
-__device__ __forceinline__ float chain_grad(const AdamSrc& s, int group, uint32_t gi, int comp) {
-  if (!(s.grad2d[3 * gi + 2].y != 0.f)) return 0.f;
-  const float* r = s.rec3 + 32 * gi;
-  switch (group) {
-    case 0: return r[comp];           // xyz
-    case 1: return r[3 + comp];       // log_scale
-    case 2: return r[6 + comp];       // rot
-    case 3: return r[10];             // opacity
-    default: {                        // sh: Y[k] * dcol[ch]
-      const int k = comp / 3, ch = comp - 3 * k;
-      return r[16 + k] * r[11 + ch];
+// One float4 unit of one parameter group per thread, one CTA per chunk of kAdamThreads units;
+// each group's unit range is padded to whole chunks, so the group -- hence the floats per
+// Gaussian DIM, the step size and the gradient source -- is a compile-time constant inside a
+// CTA.  Every load of a unit (p, m, v, the gradient flag and record entries) is independent and
+// issued before any is used: one memory latency per unit, and ~10 resident CTAs per SM keep
+// enough bytes in flight for HBM.  The update divides and takes the square root with the
+// approximate MUFU forms (relative error ~2^-22 on the step, far inside R-ADAM's 1e-6).
+constexpr uint32_t kAdamChunk = kAdamThreads;
+
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float r;
+  asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+template <int GRP, int DIM>
+__device__ __forceinline__ void adam_unit(float* __restrict__ P, float* __restrict__ M, float* __restrict__ V,
+                                          const float* __restrict__ E, float* __restrict__ O, uint32_t len,
+                                          uint32_t u, const AdamSrc& src, const AdamArgs& ad, float step) {
+  const uint32_t e0 = 4u * u;
+  if (e0 >= len) return;
+  const uint32_t cnt = min(4u, len - e0);
+  const float* __restrict__ rec3 = src.rec3;
+  const float4* __restrict__ flags = src.grad2d;
+  float p[4], m[4], v[4], fl[4], ra[4], rb[4], ex[4];
+  if (cnt == 4u) {
+    const float4 p4 = *reinterpret_cast<const float4*>(P + e0), m4 = *reinterpret_cast<const float4*>(M + e0),
+                 v4 = *reinterpret_cast<const float4*>(V + e0);
+    p[0] = p4.x; p[1] = p4.y; p[2] = p4.z; p[3] = p4.w;
+    m[0] = m4.x; m[1] = m4.y; m[2] = m4.z; m[3] = m4.w;
+    v[0] = v4.x; v[1] = v4.y; v[2] = v4.z; v[3] = v4.w;
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      p[k] = (uint32_t)k < cnt ? P[e0 + k] : 0.f;
+      m[k] = (uint32_t)k < cnt ? M[e0 + k] : 0.f;
+      v[k] = (uint32_t)k < cnt ? V[e0 + k] : 0.f;
     }
   }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const uint32_t e = e0 + min((uint32_t)k, cnt - 1u), gi = e / DIM, comp = e - gi * DIM;  // DIM: constant
+    fl[k] = 0.f; ra[k] = 0.f; rb[k] = 1.f; ex[k] = 0.f;
+    if (src.external) {
+      ex[k] = E[e];
+    } else {
+      fl[k] = flags[3 * gi + 2].y;  // k_chain's record is valid this iteration
+      const float* r = rec3 + 32 * gi;
+      if (GRP == 0) ra[k] = r[comp];
+      else if (GRP == 1) ra[k] = r[3 + comp];
+      else if (GRP == 2) ra[k] = r[6 + comp];
+      else if (GRP == 3) ra[k] = r[10];
+      else { ra[k] = r[16 + comp / 3]; rb[k] = r[11 + comp % 3]; }  // sh: Y[k] * dcol[ch]
+      if (src.has_gbuf) ex[k] = E[e];
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    float gr;
+    if (src.external) {
+      gr = ex[k];
+    } else {
+      gr = fl[k] != 0.f ? (GRP == 4 ? ra[k] * rb[k] : ra[k]) : 0.f;
+      if (src.has_gbuf) gr += ex[k];
+    }
+    if (src.has_gout && (uint32_t)k < cnt) O[e0 + k] = gr;
+    const uint32_t comp = (e0 + k) % DIM;
+    const float st = (GRP == 4 && comp < 3u) ? ad.step_sh0 : step;
+    m[k] = ad.b1 * m[k] + (1.0f - ad.b1) * gr;
+    v[k] = ad.b2 * v[k] + (1.0f - ad.b2) * gr * gr;
+    p[k] -= __fdividef(st * m[k], sqrt_approx(v[k]) * ad.inv_sqrt_bc2 + ad.eps);
+  }
+  if (cnt == 4u) {
+    *reinterpret_cast<float4*>(P + e0) = make_float4(p[0], p[1], p[2], p[3]);
+    *reinterpret_cast<float4*>(M + e0) = make_float4(m[0], m[1], m[2], m[3]);
+    *reinterpret_cast<float4*>(V + e0) = make_float4(v[0], v[1], v[2], v[3]);
+  } else {
+    for (uint32_t k = 0; k < cnt; ++k) {
+      P[e0 + k] = p[k];
+      M[e0 + k] = m[k];
+      V[e0 + k] = v[k];
+    }
+  }
+}
+
+__host__ __device__ __forceinline__ uint32_t adam_chunks(uint32_t len) {
+  return ((len + 3u) / 4u + kAdamChunk - 1u) / kAdamChunk;
+}
+__host__ __device__ __forceinline__ uint32_t adam_total_chunks(uint32_t n, uint32_t nsh) {
+  return 2u * adam_chunks(3u * n) + adam_chunks(4u * n) + adam_chunks(n) + adam_chunks(nsh * n);
 }
 
 __global__ void __launch_bounds__(kAdamThreads) k_adam(RenderArgs a, gps_gaussians g, gps_gaussians gm, gps_gaussians gv,
                                                        AdamSrc src, AdamArgs ad) {
   // 32-bit element indices: n * 3 (deg+1)^2 < 2^31 is checked on the host
   const uint32_t n = (uint32_t)a.n, nsh = 3u * (uint32_t)a.nc;
-  const uint32_t u1 = (3u * n + 3u) / 4u, u2 = u1 + (3u * n + 3u) / 4u, u3 = u2 + n, u4 = u3 + (n + 3u) / 4u,
-                 u5 = u4 + (nsh * n + 3u) / 4u;
-  const uint32_t stride = gridDim.x * blockDim.x;
-#pragma unroll 2
-  for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < u5; u += stride) {
-    const int grp = (u >= u1) + (u >= u2) + (u >= u3) + (u >= u4);
-    float *P, *M, *V, *E, *O;
-    float step;
-    uint32_t len, dim, base;
-    switch (grp) {
-      case 0: P = g.xyz; M = gm.xyz; V = gv.xyz; E = src.gbuf.xyz; O = src.gout.xyz; step = ad.step_xyz;
-              len = 3u * n; dim = 3u; base = 0u; break;
-      case 1: P = g.log_scale; M = gm.log_scale; V = gv.log_scale; E = src.gbuf.log_scale; O = src.gout.log_scale;
-              step = ad.step_ls; len = 3u * n; dim = 3u; base = u1; break;
-      case 2: P = g.rot; M = gm.rot; V = gv.rot; E = src.gbuf.rot; O = src.gout.rot; step = ad.step_rot;
-              len = 4u * n; dim = 4u; base = u2; break;
-      case 3: P = g.opacity_raw; M = gm.opacity_raw; V = gv.opacity_raw; E = src.gbuf.opacity_raw;
-              O = src.gout.opacity_raw; step = ad.step_op; len = n; dim = 1u; base = u3; break;
-      default: P = g.sh; M = gm.sh; V = gv.sh; E = src.gbuf.sh; O = src.gout.sh; step = ad.step_shr;
-               len = nsh * n; dim = nsh; base = u4; break;
-    }
-    const uint32_t e0 = 4u * (u - base);
-    const uint32_t cnt = min(4u, len - e0);
-    float p[4], m[4], v[4];
-    if (cnt == 4u) {
-      const float4 p4 = *reinterpret_cast<const float4*>(P + e0), m4 = *reinterpret_cast<const float4*>(M + e0),
-                   v4 = *reinterpret_cast<const float4*>(V + e0);
-      p[0] = p4.x; p[1] = p4.y; p[2] = p4.z; p[3] = p4.w;
-      m[0] = m4.x; m[1] = m4.y; m[2] = m4.z; m[3] = m4.w;
-      v[0] = v4.x; v[1] = v4.y; v[2] = v4.z; v[3] = v4.w;
-    } else {
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        p[k] = (uint32_t)k < cnt ? P[e0 + k] : 0.f;
-        m[k] = (uint32_t)k < cnt ? M[e0 + k] : 0.f;
-        v[k] = (uint32_t)k < cnt ? V[e0 + k] : 0.f;
-      }
-    }
-    uint32_t gi = e0 / dim, comp = e0 - gi * dim;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const uint32_t e = e0 + k;
-      float gk = 0.f;
-      if ((uint32_t)k < cnt) {
-        if (src.external) {
-          gk = E[e];
-        } else {
-          gk = chain_grad(src, grp, gi, (int)comp);
-          if (src.has_gbuf) gk += E[e];
-        }
-        if (src.has_gout) O[e] = gk;
-      }
-      const float st = (grp == 4 && comp < 3u) ? ad.step_sh0 : step;
-      m[k] = ad.b1 * m[k] + (1.0f - ad.b1) * gk;
-      v[k] = ad.b2 * v[k] + (1.0f - ad.b2) * gk * gk;
-      p[k] -= st * m[k] / (sqrtf(v[k]) * ad.inv_sqrt_bc2 + ad.eps);
-      if (++comp == dim) {  // next element: advance (gaussian, component) without a division
-        comp = 0u;
-        ++gi;
-      }
-    }
-    if (cnt == 4u) {
-      *reinterpret_cast<float4*>(P + e0) = make_float4(p[0], p[1], p[2], p[3]);
-      *reinterpret_cast<float4*>(M + e0) = make_float4(m[0], m[1], m[2], m[3]);
-      *reinterpret_cast<float4*>(V + e0) = make_float4(v[0], v[1], v[2], v[3]);
-    } else {
-      for (uint32_t k = 0; k < cnt; ++k) {
-        P[e0 + k] = p[k];
-        M[e0 + k] = m[k];
-        V[e0 + k] = v[k];
-      }
+  const uint32_t c1 = adam_chunks(3u * n), c2 = c1 + adam_chunks(3u * n), c3 = c2 + adam_chunks(4u * n),
+                 c4 = c3 + adam_chunks(n);
+  const uint32_t c = blockIdx.x;  // CTA-uniform group
+  if (c < c1) {
+    adam_unit<0, 3>(g.xyz, gm.xyz, gv.xyz, src.gbuf.xyz, src.gout.xyz, 3u * n, c * kAdamChunk + threadIdx.x, src, ad,
+                    ad.step_xyz);
+  } else if (c < c2) {
+    adam_unit<1, 3>(g.log_scale, gm.log_scale, gv.log_scale, src.gbuf.log_scale, src.gout.log_scale, 3u * n,
+                    (c - c1) * kAdamChunk + threadIdx.x, src, ad, ad.step_ls);
+  } else if (c < c3) {
+    adam_unit<2, 4>(g.rot, gm.rot, gv.rot, src.gbuf.rot, src.gout.rot, 4u * n, (c - c2) * kAdamChunk + threadIdx.x,
+                    src, ad, ad.step_rot);
+  } else if (c < c4) {
+    adam_unit<3, 1>(g.opacity_raw, gm.opacity_raw, gv.opacity_raw, src.gbuf.opacity_raw, src.gout.opacity_raw, n,
+                    (c - c3) * kAdamChunk + threadIdx.x, src, ad, ad.step_op);
+  } else {
+    const uint32_t u = (c - c4) * kAdamChunk + threadIdx.x;
+    switch (nsh) {
+      case 3: adam_unit<4, 3>(g.sh, gm.sh, gv.sh, src.gbuf.sh, src.gout.sh, nsh * n, u, src, ad, ad.step_shr); break;
+      case 12: adam_unit<4, 12>(g.sh, gm.sh, gv.sh, src.gbuf.sh, src.gout.sh, nsh * n, u, src, ad, ad.step_shr); break;
+      case 27: adam_unit<4, 27>(g.sh, gm.sh, gv.sh, src.gbuf.sh, src.gout.sh, nsh * n, u, src, ad, ad.step_shr); break;
+      default: adam_unit<4, 48>(g.sh, gm.sh, gv.sh, src.gbuf.sh, src.gout.sh, nsh * n, u, src, ad, ad.step_shr); break;
     }
   }
 }
@@ -1371,10 +1596,16 @@ gps_status forward_view(const gps_gaussians* g, const View1& v, const gps_render
   float* lp = reinterpret_cast<float*>(ws + L.loss_part);
   {
   GPS_PROF(K_SORT_BLEND, s);
-  if (a.tile == 16)
-    k_sort_blend<16><<<n_tiles, 256, 0, s>>>(a, sp.rec, offsets, vals, gk, tend, lp, hdr, io, c->tile_depth_precull);
-  else
-    k_sort_blend<8><<<n_tiles, 64, 0, s>>>(a, sp.rec, offsets, vals, gk, tend, lp, hdr, io, c->tile_depth_precull);
+  if (c->sort_free) {
+    if (a.tile == 16)
+      k_sort_blend<16, false><<<n_tiles, 256, 0, s>>>(a, sp.rec, offsets, vals, gk, tend, lp, hdr, io, 0);
+    else
+      k_sort_blend<8, false><<<n_tiles, 64, 0, s>>>(a, sp.rec, offsets, vals, gk, tend, lp, hdr, io, 0);
+  } else if (a.tile == 16) {
+    k_sort_blend<16, true><<<n_tiles, 256, 0, s>>>(a, sp.rec, offsets, vals, gk, tend, lp, hdr, io, c->tile_depth_precull);
+  } else {
+    k_sort_blend<8, true><<<n_tiles, 64, 0, s>>>(a, sp.rec, offsets, vals, gk, tend, lp, hdr, io, c->tile_depth_precull);
+  }
   }
   GPS_CHECK_LAUNCH("k_sort_blend");
   return GPS_OK;
@@ -1385,6 +1616,7 @@ gps_status check_render_cfg(const gps_render_config* c) {
   if (c->tile != 8 && c->tile != 16) return invalid("render config: tile must be 8 or 16");
   if (!(c->eps_depth >= 0) || !(c->alpha_min >= 0) || !(c->lowpass >= 0)) return invalid("render config: bad value");
   if (c->max_pairs < 0 || c->max_pairs > 0xFFFFFFFFll) return invalid("render config: bad max_pairs");
+  if (c->sort_free != 0 && c->sort_free != 1) return invalid("render config: sort_free must be 0 or 1");
   return GPS_OK;
 }
 
@@ -1509,12 +1741,20 @@ gps_status gps_refine_step(gps_gaussians* g, gps_adam_state* state, const gps_vi
     const uint32_t* tgt = reinterpret_cast<const uint32_t*>(vw.target_rgba);
     {
     GPS_PROF(K_BACKWARD, s);
-    if (rcfg->tile == 16)
-      k_backward<16><<<n_tiles, 256, 0, s>>>(a, rec, offsets, vals, tend, vw.sdf_depth, cstar, wg, tgt, hdr,
-                                             reinterpret_cast<float*>(grad2d));
-    else
-      k_backward<8><<<n_tiles, 256, 0, s>>>(a, rec, offsets, vals, tend, vw.sdf_depth, cstar, wg, tgt, hdr,
-                                            reinterpret_cast<float*>(grad2d));
+    // sort-free (the paper's renderer, App. B): a thread per (entry, pixel group);
+    // sorted (this build's tile design): a warp per entry with a warp reduction
+    const bool items = rcfg->sort_free != 0;
+    float* g2 = reinterpret_cast<float*>(grad2d);
+    if (items) {
+      if (rcfg->tile == 16)
+        k_backward_items<16><<<n_tiles, 256, 0, s>>>(a, rec, offsets, vals, tend, vw.sdf_depth, cstar, wg, tgt, hdr, g2);
+      else
+        k_backward_items<8><<<n_tiles, 256, 0, s>>>(a, rec, offsets, vals, tend, vw.sdf_depth, cstar, wg, tgt, hdr, g2);
+    } else if (rcfg->tile == 16) {
+      k_backward<16><<<n_tiles, 256, 0, s>>>(a, rec, offsets, vals, tend, vw.sdf_depth, cstar, wg, tgt, hdr, g2);
+    } else {
+      k_backward<8><<<n_tiles, 256, 0, s>>>(a, rec, offsets, vals, tend, vw.sdf_depth, cstar, wg, tgt, hdr, g2);
+    }
     }
     GPS_CHECK_LAUNCH("k_backward");
     if (g->n > 0) {
@@ -1540,7 +1780,7 @@ gps_status gps_refine_step(gps_gaussians* g, gps_adam_state* state, const gps_vi
     src.gout = grad_out ? *grad_out : gps_gaussians{};
     src.has_gout = grad_out != nullptr;
     GPS_PROF(K_GRAD_ADAM, s);
-    k_adam<<<148 * 8, kAdamThreads, 0, s>>>(a, *g, state->m, state->v, src, ad);
+    k_adam<<<adam_total_chunks((uint32_t)g->n, 3u * (uint32_t)a.nc), kAdamThreads, 0, s>>>(a, *g, state->m, state->v, src, ad);
     GPS_CHECK_LAUNCH("k_adam");
   }
   state->step += 1;
@@ -1564,7 +1804,7 @@ gps_status gps_adam_step(gps_gaussians* g, gps_adam_state* state, const gps_gaus
     src.gbuf = *grad;
     src.external = 1;
     GPS_PROF(K_GRAD_ADAM, as_stream(stream));
-    k_adam<<<148 * 8, kAdamThreads, 0, as_stream(stream)>>>(a, *g, state->m, state->v, src, ad);
+    k_adam<<<adam_total_chunks((uint32_t)g->n, 3u * (uint32_t)a.nc), kAdamThreads, 0, as_stream(stream)>>>(a, *g, state->m, state->v, src, ad);
     GPS_CHECK_LAUNCH("k_adam");
   }
   state->step += 1;

@@ -183,15 +183,17 @@ __global__ void __launch_bounds__(256) k_alloc(VolumeView v, FuseParams p,
 // integration (R-INT): grid-stride over the visible list; one CTA per block, 256 threads x 2
 // adjacent voxels (one 16-byte load/store each).  Prescribed fp32, DESIGN.md §4.2.
 // ============================================================================================
-// geometry of one voxel (prescribed fp32): whether it is updated, its pixel and
-// the truncated sample s.  Needs no voxel data, so skipped voxels cost no memory traffic.
-__device__ __forceinline__ bool voxel_sample(const FuseParams& p, int gx, int gy, int gz,
-                                             const uint16_t* __restrict__ depth, uint32_t& pix, float& s) {
+// geometry of one voxel (prescribed fp32), in two halves so that a thread can
+// issue the frame gathers of both its voxels before waiting for either: voxel_project gives the
+// pixel of a voxel in front of the camera, voxel_sample the truncated sample s of its depth
+// (false: not updated).  Needs no voxel data, so skipped voxels cost no voxel traffic.
+__device__ __forceinline__ bool voxel_project(const FuseParams& p, int gx, int gy, int gz, uint32_t& pix,
+                                              float& X2) {
   const float P0 = pmul((float)gx, p.voxel), P1 = pmul((float)gy, p.voxel), P2 = pmul((float)gz, p.voxel);
   const float D0 = psub(P0, p.t[0]), D1 = psub(P1, p.t[1]), D2 = psub(P2, p.t[2]);
   const float X0 = pdot3(p.R[0], D0, p.R[3], D1, p.R[6], D2);
   const float X1 = pdot3(p.R[1], D0, p.R[4], D1, p.R[7], D2);
-  const float X2 = pdot3(p.R[2], D0, p.R[5], D1, p.R[8], D2);
+  X2 = pdot3(p.R[2], D0, p.R[5], D1, p.R[8], D2);
   if (!(X2 > 0.0f)) return false;
   const float iz = __frcp_rn(X2);
   const float uf = padd(pmul(pmul(p.fx, X0), iz), p.cx);
@@ -199,7 +201,10 @@ __device__ __forceinline__ bool voxel_sample(const FuseParams& p, int gx, int gy
   const float ur = floorf(padd(uf, 0.5f)), vr = floorf(padd(vf, 0.5f));
   if (!(ur >= 0.0f && ur <= (float)(p.W - 1) && vr >= 0.0f && vr <= (float)(p.H - 1))) return false;
   pix = (uint32_t)vr * (uint32_t)p.W + (uint32_t)ur;
-  const float d = pmul((float)__ldg(&depth[pix]), p.inv_scale);
+  return true;
+}
+__device__ __forceinline__ bool voxel_sample(const FuseParams& p, uint16_t raw, float X2, float& s) {
+  const float d = pmul((float)raw, p.inv_scale);
   if (!(d >= p.dmin && d <= p.dmax)) return false;
   const float eta = psub(d, X2);
   if (eta < -p.mu) return false;
@@ -207,15 +212,16 @@ __device__ __forceinline__ bool voxel_sample(const FuseParams& p, int gx, int gy
   return true;
 }
 
-// running means (R-INT): tsdf in prescribed fp32 with a correctly rounded reciprocal of (w+1);
-// colour as the exact rational mean with round-half-up, the division by w+1 done as a
-// multiply-high by ceil(2^32/(w+1)) (exact for numerators < 2^17 and w+1 <= 256)
+// running means (R-INT): tsdf in prescribed fp32 with the correctly rounded reciprocal of (w+1)
+// (srcp[w] = __frcp_rn(w + 1), tabulated); colour as the exact rational mean with round-half-up,
+// the division by w+1 done as a multiply-high by ceil(2^32/(w+1)) (exact for numerators < 2^17
+// and w+1 <= 256)
 __device__ __forceinline__ uint2 voxel_update(float tsdf, uint32_t cw, float s, uint32_t c, int wmax,
-                                              const uint32_t* __restrict__ smagic) {
+                                              const uint32_t* __restrict__ smagic, const float* __restrict__ srcp) {
   const uint32_t w = cw >> 24;
   const float wf = (float)w;
   // w = 0: the stored NaN stands for the initial tsdf 1, and (1*0 + s) * (1/1) = s exactly
-  const float t = w == 0 ? s : pmul(padd(pmul(tsdf, wf), s), __frcp_rn(padd(wf, 1.0f)));
+  const float t = w == 0 ? s : pmul(padd(pmul(tsdf, wf), s), srcp[w]);
   const uint32_t w1 = w + 1, half = w1 >> 1, magic = smagic[w];
   uint32_t out;
   if (w == 0) {
@@ -232,64 +238,85 @@ __device__ __forceinline__ uint2 voxel_update(float tsdf, uint32_t cw, float s, 
   return make_uint2(__float_as_uint(t), out);
 }
 
+// Grid-stride over the visible list, software-pipelined two deep: the slot of block q + 2G and
+// the pool index, key and -neighbour row of block q + G are loaded while block q is integrated
+// (G = gridDim.x), so no dependent metadata load is waited for inside the loop.
 __global__ void __launch_bounds__(256) k_integrate(VolumeView v, FuseParams p,
                                                    const uint16_t* __restrict__ depth,
                                                    const uint32_t* __restrict__ rgba) {
   __shared__ uint32_t smagic[256];
+  __shared__ float srcp[256];
   // smagic[w] = ceil(2^32 / (w+1)) for w >= 1 (w = 0 is special-cased in voxel_update)
-  for (int d = threadIdx.x; d < 256; d += blockDim.x) smagic[d] = 0xFFFFFFFFu / (uint32_t)(d + 1) + 1u;
+  for (int d = threadIdx.x; d < 256; d += blockDim.x) {
+    smagic[d] = 0xFFFFFFFFu / (uint32_t)(d + 1) + 1u;
+    srcp[d] = __frcp_rn((float)(d + 1));
+  }
   __syncthreads();
   const uint32_t nvis = min(*(volatile uint32_t*)&v.ctr->n_vis, v.max_blocks);
   if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&v.ctr->vis_total, (unsigned long long)nvis);
   const int e = 2 * threadIdx.x;  // voxel pair (e, e+1): same j,k; i even
   const int li = e & 7, lj = (e >> 3) & 7, lk = e >> 6;
+  const int lane = threadIdx.x & 31;
   __shared__ uint32_t scnt[8];
   uint32_t n_upd = 0;
-  // software pipeline over the CTA's blocks: the next block's (pool index, key) are loaded while
-  // the current one is integrated, and the voxel pair is loaded alongside the depth gather
+  const uint32_t G = gridDim.x;
   uint32_t q = blockIdx.x;
-  int32_t b_next = -1;
-  uint64_t key_next = 0;
+  // pipeline registers: block q (b1, key1, row m0/m1 of b1), and the slot of block q + G
+  int32_t b1 = -1, slot2 = -1;
+  uint64_t key1 = 0;
+  int4 m0 = make_int4(-1, -1, -1, -1), m1 = m0;
   if (q < nvis) {
     const int32_t slot = v.vis[q];
-    b_next = v.vals[slot];
-    key_next = v.keys[slot];
+    b1 = v.vals[slot];
+    key1 = v.keys[slot];
   }
-  for (; q < nvis; q += gridDim.x) {
-    const int32_t b = b_next;
-    const uint64_t key = key_next;
-    const uint32_t qn = q + gridDim.x;
-    if (qn < nvis) {
-      const int32_t slot = v.vis[qn];
-      b_next = v.vals[slot];
-      key_next = v.keys[slot];
+  if (q + G < nvis) slot2 = v.vis[q + G];
+  if (b1 >= 0) {
+    m0 = __ldg(reinterpret_cast<const int4*>(v.nbrm) + 2 * (size_t)b1);
+    m1 = __ldg(reinterpret_cast<const int4*>(v.nbrm) + 2 * (size_t)b1 + 1);
+  }
+  for (; q < nvis; q += G) {
+    const int32_t b = b1;
+    const uint64_t key = key1;
+    const int4 c0r = m0, c1r = m1;
+    // advance the pipeline (all loads below are consumed one iteration later)
+    b1 = -1;
+    if (slot2 >= 0) {
+      b1 = v.vals[slot2];
+      key1 = v.keys[slot2];
     }
+    slot2 = q + 2 * G < nvis ? v.vis[q + 2 * G] : -1;
     if (b < 0) continue;  // uniform across the CTA
-    // the -neighbour row for the apron push, loaded here so its latency overlaps the gather
-    const int4 m0 = __ldg(reinterpret_cast<const int4*>(v.nbrm) + 2 * (size_t)b);
-    const int4 m1 = __ldg(reinterpret_cast<const int4*>(v.nbrm) + 2 * (size_t)b + 1);
     int bx, by, bz;
     unpack_block(key, bx, by, bz);
     float2* tp = reinterpret_cast<float2*>(v.tsdf + (size_t)b * kTsdfBlock + tsdf_index(li, lj, lk));
     uint2* cp = reinterpret_cast<uint2*>(v.rgbw + (size_t)b * 512 + e);
-    float2 ts = *tp;  // speculative: off the dependent chain (bandwidth is not the limit here)
+    float2 ts = *tp;  // speculative: off the dependent chain
     uint2 cw = *cp;
     const int gx = bx * 8 + li, gy = by * 8 + lj, gz = bz * 8 + lk;
     uint32_t pix0 = 0, pix1 = 0;
-    float s0 = 0.f, s1 = 0.f;
-    const bool u0 = voxel_sample(p, gx, gy, gz, depth, pix0, s0);
-    const bool u1 = voxel_sample(p, gx + 1, gy, gz, depth, pix1, s1);
+    float z0 = 0.f, z1 = 0.f, s0 = 0.f, s1 = 0.f;
+    const bool in0 = voxel_project(p, gx, gy, gz, pix0, z0);
+    const bool in1 = voxel_project(p, gx + 1, gy, gz, pix1, z1);
+    // both voxels' depth and colour gathers in flight together (colour speculatively)
+    const uint16_t r0 = in0 ? __ldg(&depth[pix0]) : (uint16_t)0, r1 = in1 ? __ldg(&depth[pix1]) : (uint16_t)0;
+    const uint32_t c0 = in0 ? __ldg(&rgba[pix0]) : 0u, c1 = in1 ? __ldg(&rgba[pix1]) : 0u;
+    if (b1 >= 0) {  // next block's -neighbour row (its pool index arrived last iteration... or now)
+      m0 = __ldg(reinterpret_cast<const int4*>(v.nbrm) + 2 * (size_t)b1);
+      m1 = __ldg(reinterpret_cast<const int4*>(v.nbrm) + 2 * (size_t)b1 + 1);
+    }
+    const bool u0 = in0 && voxel_sample(p, r0, z0, s0);
+    const bool u1 = in1 && voxel_sample(p, r1, z1, s1);
     int dneg0 = 0, dneg1 = 0;  // change of the "tsdf <= 0" indicator of each voxel (NaN: false)
     if (u0 | u1) {
-      const uint32_t c0 = u0 ? __ldg(&rgba[pix0]) : 0u, c1 = u1 ? __ldg(&rgba[pix1]) : 0u;
       const float old0 = ts.x, old1 = ts.y;
       if (u0) {
-        const uint2 r = voxel_update(ts.x, cw.x, s0, c0, p.wmax, smagic);
+        const uint2 r = voxel_update(ts.x, cw.x, s0, c0, p.wmax, smagic, srcp);
         ts.x = __uint_as_float(r.x);
         cw.x = r.y;
       }
       if (u1) {
-        const uint2 r = voxel_update(ts.y, cw.y, s1, c1, p.wmax, smagic);
+        const uint2 r = voxel_update(ts.y, cw.y, s1, c1, p.wmax, smagic, srcp);
         ts.y = __uint_as_float(r.x);
         cw.y = r.y;
       }
@@ -302,7 +329,7 @@ __global__ void __launch_bounds__(256) k_integrate(VolumeView v, FuseParams p,
       // across those faces (k_link's comment)
       const int zyz = (lj == 0 ? 2 : 0) | (lk == 0 ? 4 : 0);
       if (zyz | (li == 0)) {
-        const int32_t mm[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
+        const int32_t mm[8] = {c0r.x, c0r.y, c0r.z, c0r.w, c1r.x, c1r.y, c1r.z, c1r.w};
 #pragma unroll
         for (int k = 1; k < 8; ++k) {
           if (mm[k] < 0) continue;
@@ -312,22 +339,22 @@ __global__ void __launch_bounds__(256) k_integrate(VolumeView v, FuseParams p,
         }
       }
     }
-    // negcnt: the indicator changes of this warp's voxels, for the block itself and (the apron
-    // cell held the owner's old value) for every -neighbour whose apron they feed.  Sign flips
-    // are rare, so the warp first checks for any (b and the -neighbour row are CTA-uniform).
-    if (__any_sync(0xFFFFFFFFu, (dneg0 | dneg1) != 0)) {
-      const int lane = threadIdx.x & 31;
-      const int dsum = __reduce_add_sync(0xFFFFFFFFu, dneg0 + dneg1);
-      if (lane == 0 && dsum) atomicAdd(&v.negcnt[b], dsum);
+    // subneg: the indicator changes of this thread's voxels, for the sub-blocks of the block
+    // itself (row entry 0) that hold them and -- the apron cell held the owner's old value --
+    // for those of every -neighbour whose apron they feed.  Sign flips are rare: one 64-bit
+    // atomic per affected block, each byte's count staying a true count throughout.
+    if (dneg0 | dneg1) {
       const int zyz = (lj == 0 ? 2 : 0) | (lk == 0 ? 4 : 0) | (li == 0 ? 1 : 0);
-      const int32_t mm[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
+      const int32_t mm[8] = {c0r.x, c0r.y, c0r.z, c0r.w, c1r.x, c1r.y, c1r.z, c1r.w};
 #pragma unroll
-      for (int k = 1; k < 8; ++k) {
-        // voxel li feeds -neighbour k iff k's axes are among its zero coordinates; li + 1 never
-        // lies on the x face
-        const int dn = ((k & ~zyz) == 0 ? dneg0 : 0) + ((k & ~(zyz & 6)) == 0 ? dneg1 : 0);
-        const int dk = __reduce_add_sync(0xFFFFFFFFu, dn);
-        if (lane == 0 && dk && mm[k] >= 0) atomicAdd(&v.negcnt[mm[k]], dk);
+      for (int k = 0; k < 8; ++k) {
+        // voxel li feeds -neighbour k iff k's axes are among its zero coordinates (k = 0: the
+        // block itself); li + 1 never lies on the x face
+        const int ox = 8 * (k & 1), oy = 8 * ((k >> 1) & 1), oz = 8 * (k >> 2);
+        uint64_t wd = 0;
+        if ((k & ~zyz) == 0) wd += (uint64_t)(int64_t)dneg0 * cell_subs(li + ox, lj + oy, lk + oz);
+        if ((k & ~(zyz & 6)) == 0) wd += (uint64_t)(int64_t)dneg1 * cell_subs(li + 1 + ox, lj + oy, lk + oz);
+        if (wd && mm[k] >= 0) atomicAdd(reinterpret_cast<unsigned long long*>(&v.subneg[mm[k]]), (unsigned long long)wd);
       }
     }
   }
@@ -387,7 +414,7 @@ __global__ void __launch_bounds__(256) k_link(VolumeView v) {
 #pragma unroll
     for (int k = 0; k < 8; ++k) nb[k] = __shfl_sync(0xFFFFFFFFu, mine, k);
     float* base = v.tsdf + (size_t)b * kTsdfBlock;
-    int nneg = 0;  // the new block's own voxels are unobserved: its count is its apron's
+    uint64_t nneg = 0;  // the new block's own voxels are unobserved: its counts are its apron's
     for (int c = lane; c < 217; c += 32) {
       int ax, ay, az;
       apron_cell(c, ax, ay, az);
@@ -398,10 +425,11 @@ __global__ void __launch_bounds__(256) k_link(VolumeView v) {
       const float val = o >= 0 ? v.tsdf[(size_t)o * kTsdfBlock + tsdf_index(ax & 7, ay & 7, az & 7)]
                                : __uint_as_float(0x7FC00000u);
       base[tsdf_index(ax, ay, az)] = val;
-      nneg += (int)(val <= 0.f);
+      if (val <= 0.f) nneg += cell_subs(ax, ay, az);
     }
-    nneg = __reduce_add_sync(0xFFFFFFFFu, nneg);
-    if (lane == 0) v.negcnt[b] = nneg;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nneg += __shfl_xor_sync(0xFFFFFFFFu, nneg, o);
+    if (lane == 0) v.subneg[b] = nneg;
   }
 }
 
@@ -442,10 +470,55 @@ struct RayParams {
 constexpr int kRangeTile = 16;
 constexpr int kMaxRangeTiles = 256 * 256;  // images up to 4096 x 4096 use the range image
 
+__device__ __forceinline__ void block_tile_range(const VolumeView& v, const RayParams& p, uint32_t b, int tiles_x,
+                                                 int tiles_y, int& otx0, int& otx1, int& oty0, int& oty1,
+                                                 uint32_t& oa0, uint32_t& oa1);
+
 __global__ void __launch_bounds__(256) k_range(VolumeView v, RayParams p, uint32_t* tmin, uint32_t* tmax,
                                                int tiles_x, int tiles_y) {
   const uint32_t nb = min(*(volatile uint32_t*)&v.ctr->n_blocks, v.max_blocks);
-  for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += gridDim.x * blockDim.x) {
+  const uint32_t stride = gridDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31;
+  // warp-uniform trip count: every lane reaches the warp-cooperative tile loop below
+  for (uint32_t b0 = blockIdx.x * blockDim.x; b0 < nb; b0 += stride) {
+    const uint32_t b = b0 + threadIdx.x;
+    int tx0 = 1, tx1 = 0, ty0 = 0, ty1 = 0;
+    uint32_t a0 = 0, a1 = 0;
+    if (b < nb) block_tile_range(v, p, b, tiles_x, tiles_y, tx0, tx1, ty0, ty1, a0, a1);
+    const bool any = tx0 <= tx1 && ty0 <= ty1;
+    const bool big = any && (tx1 - tx0 + 1) * (ty1 - ty0 + 1) > 4;
+    if (any && !big) {
+      for (int ty = ty0; ty <= ty1; ++ty)
+        for (int tx = tx0; tx <= tx1; ++tx) {
+          const int t = ty * tiles_x + tx;
+          if (tmin[t] > a0) atomicMin(&tmin[t], a0);
+          if (tmax[t] < a1) atomicMax(&tmax[t], a1);
+        }
+    }
+    // blocks near the camera cover many tiles: the warp takes them one at a time, a lane per tile
+    uint32_t bm = __ballot_sync(0xFFFFFFFFu, big);
+    while (bm) {
+      const int src = __ffs(bm) - 1;
+      bm &= bm - 1u;
+      const int sx0 = __shfl_sync(0xFFFFFFFFu, tx0, src), sx1 = __shfl_sync(0xFFFFFFFFu, tx1, src);
+      const int sy0 = __shfl_sync(0xFFFFFFFFu, ty0, src), sy1 = __shfl_sync(0xFFFFFFFFu, ty1, src);
+      const uint32_t s0 = __shfl_sync(0xFFFFFFFFu, a0, src), s1 = __shfl_sync(0xFFFFFFFFu, a1, src);
+      const int wx = sx1 - sx0 + 1, cnt = wx * (sy1 - sy0 + 1);
+      for (int k = lane; k < cnt; k += 32) {
+        const int t = (sy0 + k / wx) * tiles_x + sx0 + k % wx;
+        if (tmin[t] > s0) atomicMin(&tmin[t], s0);
+        if (tmax[t] < s1) atomicMax(&tmax[t], s1);
+      }
+    }
+  }
+}
+
+// tile rect [tx0, tx1] x [ty0, ty1] (empty: tx0 > tx1) and the t range (float bits a0, a1) of
+// pool block b for the range image
+__device__ __forceinline__ void block_tile_range(const VolumeView& v, const RayParams& p, uint32_t b, int tiles_x,
+                                                 int tiles_y, int& otx0, int& otx1, int& oty0, int& oty1,
+                                                 uint32_t& oa0, uint32_t& oa1) {
+  {
     int bx, by, bz;
     unpack_block(v.bkeys[b], bx, by, bz);
     const float s = 8.0f * p.voxel;
@@ -497,19 +570,14 @@ __global__ void __launch_bounds__(256) k_range(VolumeView v, RayParams p, uint32
           add(C[c][0] + s * (C[d][0] - C[c][0]), C[c][1] + s * (C[d][1] - C[c][1]), zc);
         }
       }
-    if (!(umin <= umax)) continue;  // entirely nearer than any sample: no ray meets it
-    if (umax < -1.f || vmax < -1.f || umin > p.W || vmin > p.H) continue;
-    const int tx0 = max(0, (int)floorf((fmaxf(umin, -2.f) - 1.f) / kRangeTile));
-    const int tx1 = min(tiles_x - 1, (int)floorf((fminf(umax, (float)p.W + 2.f) + 1.f) / kRangeTile));
-    const int ty0 = max(0, (int)floorf((fmaxf(vmin, -2.f) - 1.f) / kRangeTile));
-    const int ty1 = min(tiles_y - 1, (int)floorf((fminf(vmax, (float)p.H + 2.f) + 1.f) / kRangeTile));
-    const uint32_t a0 = __float_as_uint(t0), a1 = __float_as_uint(t1);
-    for (int ty = ty0; ty <= ty1; ++ty)
-      for (int tx = tx0; tx <= tx1; ++tx) {
-        const int t = ty * tiles_x + tx;
-        if (tmin[t] > a0) atomicMin(&tmin[t], a0);
-        if (tmax[t] < a1) atomicMax(&tmax[t], a1);
-      }
+    if (!(umin <= umax)) return;  // entirely nearer than any sample: no ray meets it
+    if (umax < -1.f || vmax < -1.f || umin > p.W || vmin > p.H) return;
+    otx0 = max(0, (int)floorf((fmaxf(umin, -2.f) - 1.f) / kRangeTile));
+    otx1 = min(tiles_x - 1, (int)floorf((fminf(umax, (float)p.W + 2.f) + 1.f) / kRangeTile));
+    oty0 = max(0, (int)floorf((fmaxf(vmin, -2.f) - 1.f) / kRangeTile));
+    oty1 = min(tiles_y - 1, (int)floorf((fminf(vmax, (float)p.H + 2.f) + 1.f) / kRangeTile));
+    oa0 = __float_as_uint(t0);
+    oa1 = __float_as_uint(t1);
   }
 }
 
@@ -557,6 +625,17 @@ __device__ __forceinline__ void mark_footprint(const VolumeView& v, int32_t b0, 
   }
 }
 
+// the 8 trilinear corners (numbered dx | dy<<1 | dz<<2) of the sample based at cell (lx, ly, lz)
+// of the block plane starting at `pl` (common.cuh layout)
+__device__ __forceinline__ void load_corners(const float* __restrict__ pl, int lx, int ly, int lz, float* tv) {
+  const float* b0 = pl + lx + kTsdfSY * ly + kTsdfSZ * lz;
+  const bool face = lx == 7;
+  const float* b1 = face ? pl + kTsdfFace + ly + 9 * lz : b0 + 1;
+  const int sy = face ? 1 : kTsdfSY, sz = face ? 9 : kTsdfSZ;
+  tv[0] = b0[0]; tv[2] = b0[kTsdfSY]; tv[4] = b0[kTsdfSZ]; tv[6] = b0[kTsdfSY + kTsdfSZ];
+  tv[1] = b1[0]; tv[3] = b1[sy]; tv[5] = b1[sz]; tv[7] = b1[sy + sz];
+}
+
 // tsdf and colour at voxel-unit position p (the hit point); returns validity.  The tsdf corners
 // come from the apron layout, the colour corners from their owner voxels via the +neighbour row.
 __device__ __forceinline__ bool trilinear_color(const VolumeView& v, BlockCache& c0, float px, float py, float pz,
@@ -567,10 +646,8 @@ __device__ __forceinline__ bool trilinear_color(const VolumeView& v, BlockCache&
   const int32_t b0 = cached_find(v, c0, gx >> 3, gy >> 3, gz >> 3);
   if (b0 < 0) return false;
   const int lx = gx & 7, ly = gy & 7, lz = gz & 7;
-  const float* tb = v.tsdf + (size_t)b0 * kTsdfBlock + tsdf_index(lx, ly, lz);
   float tv[8];
-#pragma unroll
-  for (int corner = 0; corner < 8; ++corner) tv[corner] = tb[tsdf_index(corner & 1, (corner >> 1) & 1, (corner >> 2) & 1)];
+  load_corners(v.tsdf + (size_t)b0 * kTsdfBlock, lx, ly, lz, tv);
   float chk = tv[0];
 #pragma unroll
   for (int corner = 1; corner < 8; ++corner) chk += tv[corner];
@@ -637,12 +714,15 @@ __global__ void __launch_bounds__(256, kMinCtas) k_raycast(VolumeView v, RayPara
   const float iqy = qy != 0.f ? 1.f / qy : INFINITY;
   const float iqz = qz != 0.f ? 1.f / qz : INFINITY;
   BlockCache c0{INT_MIN, INT_MIN, INT_MIN, -1};
-  int32_t pb = -1;    // the last allocated block the march entered, and whether its tsdf plane
-  bool ppos = false;  // holds no value <= 0 (negcnt == 0; cleared once its samples are skipped)
+  int32_t pb = -1;   // the last allocated block the march entered, its sub-block counts, and
+  uint64_t pw = 0;   // the sub-block (of pb) whose samples were last skipped
+  int psk = -1;
   bool prev_valid = false, hit = false;
   float prev_f = 0.f, tstar = 0.f;
   int j = jstart;  // samples before jstart (and after jend) meet no allocated block: invalid
   int n_iter = 0, n_skip = 0, n_invalid = 0;
+  // one structured body per grid index (the block lookup, then either the skip or the sample), so
+  // the warp reconverges every iteration
   // one structured body per grid index (the block lookup, then either the skip or the sample), so
   // the warp reconverges every iteration
   while (j <= jend) {
@@ -662,8 +742,11 @@ __global__ void __launch_bounds__(256, kMinCtas) k_raycast(VolumeView v, RayPara
       b0 = cached_find(v, c0, bx, by, bz);
     if (b0 >= 0 && b0 != pb) {
       pb = b0;
-      ppos = __ldg(&v.negcnt[b0]) == 0;
+      pw = __ldg(reinterpret_cast<const unsigned long long*>(&v.subneg[b0]));
+      psk = -1;
     }
+    // all-positive block: every sub-block count is zero (and its samples not skipped yet)
+    const bool ppos = b0 >= 0 && pw == 0ull && psk < 0;
     if (b0 < 0 || ppos) {
       // exit of this block: first grid index at or past it, minus a 0.01-step margin against
       // fp32 error (so jn never exceeds the true first index of the next block)
@@ -671,32 +754,40 @@ __global__ void __launch_bounds__(256, kMinCtas) k_raycast(VolumeView v, RayPara
       const float ey = qy != 0.f ? ((qy > 0.f ? (float)(by + 1) : (float)by) * 8.f - oy) * iqy : INFINITY;
       const float ez = qz != 0.f ? ((qz > 0.f ? (float)(bz + 1) : (float)bz) * 8.f - oz) * iqz : INFINITY;
       const float texit = fminf(ex, fminf(ey, ez));
-      const float jn = ceilf((texit - p.dmin) / p.voxel - 0.01f);
+      const float jn = ceilf((texit - p.dmin) * p.inv_voxel - 0.01f);
       const int jnext = (jn <= (float)(p.J + 1)) ? (int)jn : p.J + 1;
       if (b0 < 0) {  // unallocated: all its samples are invalid
         j = max(j + 1, jnext);
         prev_valid = false;
       } else {
-        // all-positive block: no sample based in it can end the march (a valid sample is a convex
-        // combination of > 0 corners), so only its last sample matters -- as the predecessor of
-        // the next block's first.  Jump there and evaluate it normally.
-        ppos = false;
+        // all-positive block: no sample based in it can end the march (a valid sample is a
+        // convex combination of > 0 corners), so only its last sample matters -- as the
+        // predecessor of the next block's first.  Jump there and evaluate it normally.
+        psk = 0;
         j = max(j, jnext - 1);
       }
       if (kDebug) ++n_skip;
     } else {
-      // the 8 corners at constant offsets in the apron layout (NaN: unallocated or unobserved)
-      const float* tb = v.tsdf + (size_t)b0 * kTsdfBlock + tsdf_index(gx & 7, gy & 7, gz & 7);
-      float tv[8];
-#pragma unroll
-      for (int corner = 0; corner < 8; ++corner)
-        tv[corner] = tb[tsdf_index(corner & 1, (corner >> 1) & 1, (corner >> 2) & 1)];
-      if (kDebug == 2) mark_footprint(v, b0, gx & 7, gy & 7, gz & 7, footprint);
-      float chk = tv[0];
-#pragma unroll
-      for (int corner = 1; corner < 8; ++corner) chk += tv[corner];
-      const bool valid = !isnan(chk);
+      // the 8 corners at constant offsets in the apron layout (NaN: unallocated or unobserved;
+      // a NaN corner makes the nested-lerp value NaN, so validity is "the value is not NaN").
+      // Sample j + 1 is evaluated in the same step when it lies in the same block: its corner
+      // loads are in flight together with sample j's (same arithmetic as its own step would do,
+      // so the result is unchanged; it is discarded if sample j ends the march).
+      const float* pl = v.tsdf + (size_t)b0 * kTsdfBlock;
+      float tv[8], tw[8];
+      load_corners(pl, gx & 7, gy & 7, gz & 7, tv);
+      const float t2 = p.dmin + (float)(j + 1) * p.voxel;
+      const float px2 = fmaf(t2, qx, ox), py2 = fmaf(t2, qy, oy), pz2 = fmaf(t2, qz, oz);
+      const float fx2 = floorf(px2), fy2 = floorf(py2), fz2 = floorf(pz2);
+      const int gx2 = (int)fx2, gy2 = (int)fy2, gz2 = (int)fz2;
+      const bool pair = j + 1 <= jend && (gx2 >> 3) == bx && (gy2 >> 3) == by && (gz2 >> 3) == bz;
+      if (pair) load_corners(pl, gx2 & 7, gy2 & 7, gz2 & 7, tw);
+      if (kDebug == 2) {
+        mark_footprint(v, b0, gx & 7, gy & 7, gz & 7, footprint);
+        if (pair) mark_footprint(v, b0, gx2 & 7, gy2 & 7, gz2 & 7, footprint);
+      }
       const float f = lerp3(tv, px - fx, py - fy, pz - fz);
+      const bool valid = !isnan(f);
       if (kDebug && !valid) ++n_invalid;
       if (j >= 1 && valid && f <= 0.f) {
         if (prev_valid && prev_f > 0.f) {
@@ -708,6 +799,21 @@ __global__ void __launch_bounds__(256, kMinCtas) k_raycast(VolumeView v, RayPara
       prev_valid = valid;
       prev_f = f;
       ++j;
+      if (pair) {
+        const float f2 = lerp3(tw, px2 - fx2, py2 - fy2, pz2 - fz2);
+        const bool valid2 = !isnan(f2);
+        if (kDebug && !valid2) ++n_invalid;
+        if (valid2 && f2 <= 0.f) {  // j >= 1 here
+          if (prev_valid && prev_f > 0.f) {
+            tstar = (p.dmin + (float)(j - 1) * p.voxel) + p.voxel * prev_f / (prev_f - f2);
+            hit = true;
+          }
+          break;
+        }
+        prev_valid = valid2;
+        prev_f = f2;
+        ++j;
+      }
     }
   }
   float D = 0.f, col[3] = {0.f, 0.f, 0.f}, V[3] = {0.f, 0.f, 0.f};
@@ -755,16 +861,20 @@ __global__ void k_apron_check(VolumeView v, unsigned long long* bad) {
   }
 }
 
-// negcnt invariant: recount the <= 0 cells of each allocated block's plane (own + apron)
+// subneg invariant: recount the <= 0 cells of each allocated block's plane (own + apron) per
+// sub-block
 __global__ void k_negcnt_check(VolumeView v, unsigned long long* bad) {
   const uint32_t nb = min(v.ctr->n_blocks, v.max_blocks);
   const int lane = threadIdx.x & 31;
   for (uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < nb; b += (gridDim.x * blockDim.x) >> 5) {
-    int n = 0;
-    for (int c = lane; c < 729; c += 32)
-      n += (int)(v.tsdf[(size_t)b * kTsdfBlock + tsdf_index(c % 9, (c / 9) % 9, c / 81)] <= 0.f);
-    n = __reduce_add_sync(0xFFFFFFFFu, n);
-    if (lane == 0 && n != v.negcnt[b]) atomicAdd(bad, 1ull);
+    uint64_t n = 0;
+    for (int c = lane; c < 729; c += 32) {
+      const int x = c % 9, y = (c / 9) % 9, z = c / 81;
+      if (v.tsdf[(size_t)b * kTsdfBlock + tsdf_index(x, y, z)] <= 0.f) n += cell_subs(x, y, z);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(0xFFFFFFFFu, n, o);
+    if (lane == 0 && n != v.subneg[b]) atomicAdd(bad, 1ull);
   }
 }
 
@@ -846,7 +956,7 @@ gps_status fill_volume(VolumeImpl* v, cudaStream_t s) {
   GPS_CHECK_CUDA(cudaMemsetAsync(v->view.stamp, 0xFF, sizeof(uint32_t) * c.hash_slots, s));
   k_fill_pool<<<1184, 256, 0, s>>>(v->view.tsdf, v->view.rgbw, (size_t)c.max_blocks);
   GPS_CHECK_LAUNCH("k_fill_pool");
-  GPS_CHECK_CUDA(cudaMemsetAsync(v->view.negcnt, 0, sizeof(int32_t) * c.max_blocks, s));
+  GPS_CHECK_CUDA(cudaMemsetAsync(v->view.subneg, 0, sizeof(uint64_t) * c.max_blocks, s));
   GPS_CHECK_CUDA(cudaMemsetAsync(v->view.ctr, 0, sizeof(VolumeCounters), s));
   if (v->view.grid)
     GPS_CHECK_CUDA(cudaMemsetAsync(v->view.grid, 0xFF,
@@ -887,7 +997,7 @@ gps_status gps_volume_create(const gps_volume_config* cfg, gps_stream_t stream, 
             cudaMalloc(&v->view.bkeys, sizeof(uint64_t) * nb) == cudaSuccess &&
             cudaMalloc(&v->view.nbr, sizeof(int32_t) * 8 * nb) == cudaSuccess &&
             cudaMalloc(&v->view.nbrm, sizeof(int32_t) * 8 * nb) == cudaSuccess &&
-            cudaMalloc(&v->view.negcnt, sizeof(int32_t) * nb) == cudaSuccess &&
+            cudaMalloc(&v->view.subneg, sizeof(uint64_t) * nb) == cudaSuccess &&
             cudaMalloc(&v->range, sizeof(uint32_t) * 2 * kMaxRangeTiles) == cudaSuccess &&
             cudaMalloc(&v->view.ctr, sizeof(VolumeCounters)) == cudaSuccess &&
             cudaHostAlloc(&v->flag.host, sizeof(uint32_t), cudaHostAllocMapped) == cudaSuccess &&
@@ -935,7 +1045,7 @@ void gps_volume_destroy(gps_volume* vol) {
   cudaFree(v->view.bkeys);
   cudaFree(v->view.nbr);
   cudaFree(v->view.nbrm);
-  cudaFree(v->view.negcnt);
+  cudaFree(v->view.subneg);
   if (v->view.grid) cudaFree(v->view.grid);
   cudaFree(v->range);
   cudaFree(v->view.ctr);
@@ -961,7 +1071,7 @@ gps_status gps_volume_copy(gps_volume* dst, const gps_volume* src, gps_stream_t 
   GPS_CHECK_CUDA(cp(d->view.bkeys, s->view.bkeys, 8 * nb));
   GPS_CHECK_CUDA(cp(d->view.nbr, s->view.nbr, 32 * nb));
   GPS_CHECK_CUDA(cp(d->view.nbrm, s->view.nbrm, 32 * nb));
-  GPS_CHECK_CUDA(cp(d->view.negcnt, s->view.negcnt, 4 * nb));
+  GPS_CHECK_CUDA(cp(d->view.subneg, s->view.subneg, 8 * nb));
   GPS_CHECK_CUDA(cp(d->view.ctr, s->view.ctr, sizeof(VolumeCounters)));
   if (s->view.grid)
     GPS_CHECK_CUDA(cp(d->view.grid, s->view.grid, 4 * (size_t)s->view.gdx * s->view.gdy * s->view.gdz));

@@ -34,7 +34,7 @@ def test_argument_validation_is_synchronous_and_needs_no_gpu():
     h = ctypes.c_void_p()
     assert lib.gps_volume_create(ctypes.byref(cfg), None, ctypes.byref(h)) == 1
     assert b"bad config" in lib.gps_last_error()
-    rc = N.gps_render_config(0.02, 1 / 255, 0.2, 0.3, 12, 0, 0)  # tile must be 8 or 16
+    rc = N.gps_render_config(0.02, 1 / 255, 0.2, 0.3, 12, 0, 0, 0, 0)  # tile must be 8 or 16
     K = N.gps_intrinsics(60, 60, 31.5, 23.5, 64, 48)
     assert lib.gps_render_workspace_size(10, ctypes.byref(K), ctypes.byref(rc)) == 0
     rc.tile = 16

@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--iters", type=int, default=3)
     ap.add_argument("--only", default="all")
     ap.add_argument("--gaussians", type=int, default=0)
+    ap.add_argument("--sort-free", action="store_true")
     args = ap.parse_args()
     cfg = S.get_config(args.config)
     scene = S.make_scene(cfg)
@@ -40,7 +41,7 @@ def main():
     gd = S.make_gaussians(cfg, n=args.gaussians or None)
     g = G.Gaussians.from_dict(gd)
     st = G.AdamState(g)
-    ras = G.Rasterizer(g.n, cam)
+    ras = G.Rasterizer(g.n, cam, G.RenderConfig(sort_free=int(args.sort_free)))
     D = torch.empty((cfg.height, cfg.width), device="cuda")
     C = torch.empty((cfg.height, cfg.width, 3), device="cuda")
     f = frames[args.history - 1]
