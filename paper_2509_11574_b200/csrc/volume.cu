@@ -1193,8 +1193,8 @@ static gps_status raycast_impl(const gps_volume* vol, const gps_intrinsics* K, c
       k_raycast<1><<<g, 256, 0, s>>>(v->view, p, depth_out, color_out, vertex_out, tmin, tmax);
     else {
       // occupancy variants for tuning (GPS_RAYCAST_CTAS = resident CTAs per SM the register
-      // budget targets; default 6 = 40 registers, no spills)
-      static const int ctas = getenv("GPS_RAYCAST_CTAS") ? atoi(getenv("GPS_RAYCAST_CTAS")) : 6;
+      // budget targets; default 4 = 64 registers, no spills)
+      static const int ctas = getenv("GPS_RAYCAST_CTAS") ? atoi(getenv("GPS_RAYCAST_CTAS")) : 4;
       if (ctas == 8)
         k_raycast<0, 8><<<g, 256, 0, s>>>(v->view, p, depth_out, color_out, vertex_out, tmin, tmax);
       else if (ctas == 4)
