@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-profile", action="store_true", help="time without the per-launch event profiler")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--refine-priority", type=int, default=-1, help="CUDA stream priority of the refinement stream")
     ap.add_argument("--no-overlap", action="store_true",
                     help="refinement on the fusion stream (serial schedule) instead of its own stream")
     ap.add_argument("--cpu-seconds", type=float, default=20.0, help="budget of the cpu_baseline sample")
@@ -168,7 +169,7 @@ def run_ours(args):
     g = G.Gaussians.from_dict(gd)
     rcfg = G.RenderConfig(tile=args.tile, sort_free=int(args.sort_free))
     pipe = MappingPipeline(cam, g, vol, cfg.depth_scale, rcfg, seed=rank,
-                           overlap=not args.no_overlap)
+                           overlap=not args.no_overlap, refine_priority=args.refine_priority)
     k = 0
     for _ in range(args.history):  # build a steady-state volume (untimed, no rounds)
         d, c, R, t = frames[k]
@@ -290,6 +291,8 @@ def run_ours(args):
     per_launch["k_adam"] = n_g * (24 * P + 132)
     # raycast: 16 B of output per pixel + 4 B per distinct tsdf voxel the march reads, the latter
     # measured on device (footprint bitmap) for the last timed frame's pose on the final state
+    if not prof:  # --no-profile: timing only (no per-kernel times, no roofline launch time)
+        prof = {kk: {"ms": 0.0, "launches": 0} for kk in ("k_adam", "k_integrate", "k_raycast")}
     if prof["k_raycast"]["launches"]:
         ray_px = cfg.width * cfg.height
         uniq = vol.raycast_footprint(cam, frames[k - 1][2], frames[k - 1][3])
@@ -300,8 +303,7 @@ def run_ours(args):
     if prof["k_integrate"]["launches"]:
         upd = vstats["updated_total"] - upd0
         per_launch["k_integrate"] = 16 * upd / prof["k_integrate"]["launches"]
-    if not prof:  # --no-profile: timing only
-        prof = {kk: {"ms": 0.0, "launches": 0} for kk in ("k_adam", "k_integrate", "k_raycast")}
+    if not any(v["launches"] for v in prof.values()):
         prof["k_adam"] = {"ms": float("nan"), "launches": 1}
     dominant = max((kk for kk in prof if kk != "memset"), key=lambda kk: prof[kk]["ms"])
     roof_k = dominant if dominant in per_launch else max(per_launch, key=lambda kk: prof[kk]["ms"])

@@ -31,7 +31,7 @@ class MappingPipeline:
                  render_cfg: A.RenderConfig | None = None, adam_cfg: A.AdamConfig | None = None,
                  delta_k: int = Sch.DELTA_K, iterations: int = Sch.ITERATIONS,
                  n_global: int = Sch.N_GLOBAL, n_local: int = Sch.N_LOCAL, seed: int = 0,
-                 overlap: bool = True):
+                 overlap: bool = True, refine_priority: int = -1):
         self.cam, self.g, self.vol = cam, gaussians, volume
         self.depth_scale = float(depth_scale)
         self.rcfg = render_cfg or A.RenderConfig()
@@ -60,7 +60,9 @@ class MappingPipeline:
         self.last_loss = None
         self.copy_stream = torch.cuda.Stream()
         self.overlap = overlap  # may be switched between rounds
-        self.refine_stream = torch.cuda.Stream()
+        # the refinement rounds are the longer of the two streams' work: give them the higher
+        # scheduling priority so fusion and raycasts fill the SMs around them
+        self.refine_stream = torch.cuda.Stream(priority=refine_priority)
         self._set_free = [None] * nsets   # event: the refinement that last read buffer set s is done
         self._refine_done = None
         self.rounds = 0
