@@ -604,7 +604,7 @@ __global__ void __launch_bounds__(TILE* TILE) k_sort_blend(RenderArgs a, const f
                                                           uint64_t* gkeys, uint32_t* tile_end, float* loss_part,
                                                           WsHeader* hdr, BlendIO io, int precull) {
   constexpr int NT = TILE * TILE;
-  __shared__ uint64_t skeys[kMaxList];
+  __shared__ __align__(16) uint64_t skeys[kMaxList + 2];
   __shared__ float4 s0[NT], s1[NT], s2[NT];  // s0 = (px, py, a, 2b); s1 = (c, ln sigma, d, q_max)
   __shared__ float red[NT / 32 + 1];
   __shared__ uint32_t redi[NT / 32 + 1];
@@ -624,9 +624,15 @@ __global__ void __launch_bounds__(TILE* TILE) k_sort_blend(RenderArgs a, const f
       key = ((uint64_t)__float_as_uint(rec[4 * idx + 1].z) << 32) | idx;
       skeys[threadIdx.x] = key;
     }
+    if (threadIdx.x == 0) skeys[n] = ~0ull;  // pad slot of the paired loads below
     __syncthreads();
     int rank = 0;
-    for (int j = 0; j < n; ++j) rank += skeys[j] < key;  // broadcast reads
+    // broadcast reads, two keys per 16-byte load (slot n holds ~0: never smaller)
+    const ulonglong2* k2 = reinterpret_cast<const ulonglong2*>(skeys);
+    for (int j = 0; j < (n + 1) >> 1; ++j) {
+      const ulonglong2 kk = k2[j];
+      rank += (kk.x < key) + (kk.y < key);
+    }
     __syncthreads();
     if ((int)threadIdx.x < n) {
       skeys[rank] = key;
@@ -1304,7 +1310,7 @@ __device__ __forceinline__ void chain3d(const RenderArgs& a, const gps_gaussians
 // gradient record {gx, gls, gq, gop, dcol, Y[16]} and flags it in the (per-iteration zeroed) 2D
 // gradient slot; ACCUM = 1 adds the dense raw gradient into gbuf (multi-view rounds).
 template <int ACCUM>
-__global__ void __launch_bounds__(kChainThreads) k_chain(RenderArgs a, gps_gaussians g, float4* grad2d,
+__global__ void __launch_bounds__(kChainThreads, 4) k_chain(RenderArgs a, gps_gaussians g, float4* grad2d,
                                                          float4* rec3, gps_gaussians gbuf,
                                                          const float4* __restrict__ cgj) {
   const int64_t i = blockIdx.x * (int64_t)kChainThreads + threadIdx.x;
