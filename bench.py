@@ -323,6 +323,14 @@ def run_ours(args):
         roof["note"] = "latency-bound march (dependent voxel loads); bytes = 16 B/px out + 4 B/unique tsdf voxel"
     shares = {kk: {"ms_per_step": round(v["ms"] / args.steps, 4), "launches_per_step": v["launches"] / args.steps,
                    "share": round(v["ms"] / max(ms_prof, 1e-9), 4)} for kk, v in prof.items()}
+    # HBM GB/s per kernel (BASELINE.json metric): algorithmic bytes per launch (from the
+    # run's own counters) / the kernel's average event-timed launch
+    alg = per_kernel_bytes(args, cfg, n_g, P, per_launch, rstats, vstats, upd0, prof)
+    for kk, b in alg.items():
+        if kk in shares and prof[kk]["launches"]:
+            t = prof[kk]["ms"] / prof[kk]["launches"] / 1000.0
+            shares[kk].update({"alg_bytes_per_launch": int(b), "gbs": round(b / t / 1e9, 1),
+                               "hbm_frac": round(b / t / 1e9 / peak, 4)})
     launches = int(sum(v["launches"] for kk, v in prof.items() if kk != "memset"))
     cpu = None
     if not args.no_cpu_baseline:
@@ -348,6 +356,30 @@ def run_ours(args):
     if ws > 1:
         dist.destroy_process_group()
     return line
+
+
+def per_kernel_bytes(args, cfg, n_g, P, per_launch, rstats, vstats, upd0, prof):
+    """Algorithmic bytes per launch of each kernel: one read of every input word
+    and one write of every output word the method needs, times the units one launch processes --
+    N and N_vis Gaussians and K (tile, entry) pairs of the last render, B_vis visible blocks and
+    the updated voxels of the timed fuses, the raycast's distinct voxels and the pixels."""
+    HW = cfg.width * cfg.height
+    nvis = rstats.get("n_visible", 0) or 0
+    K = rstats.get("pairs", 0) or 0
+    nfuse = max(prof.get("k_alloc", {}).get("launches", 0), 1)
+    bvis = vstats.get("n_visible", 0) or 0
+    ntiles = -(-cfg.width // args.tile) * -(-cfg.height // args.tile)
+    out = dict(per_launch)
+    out["k_alloc"] = 2 * HW + 16 * bvis                       # depth + hash entries of the visible blocks
+    out["k_link"] = 0                                          # new blocks only (latency-bound)
+    out["k_range"] = 8 * vstats.get("n_blocks", 0) + 8 * ((cfg.width + 15) // 16) * ((cfg.height + 15) // 16)
+    out["k_preprocess"] = 12 * n_g + (4 * (P - 3) + 64 + 48 + 48 + 16) * nvis   # cull reads, params, record, cgj, grads, ranks
+    out["k_scan"] = 12 * ntiles
+    out["k_emit"] = (32 + 16) * nvis + 4 * K
+    out["k_sort_blend"] = (48 + 8) * K + 36 * HW                # records + values, D_t C_t C_k in, C* W_G out
+    out["k_backward"] = (64 + 4 + 36) * K + 24 * HW             # records, values, 2D-gradient reductions; pixel state
+    out["k_chain"] = (48 + 4 * (P - 3) + 12 + 48 + 128) * nvis  # 2D grads, params, cgj, gradient record
+    return out
 
 
 def workload_config(args, cfg, n_g, ws):
