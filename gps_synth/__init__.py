@@ -500,3 +500,20 @@ def sdf_stage_inputs(cfg: SynthConfig, frame: Frame, seed: int = 0, miss_frac: f
     Ct = np.clip(blur + rng.normal(0, 0.02, size=blur.shape), 0, 1).astype(np.float32)
     Ct[Dt == 0] = 0.0
     return Dt, Ct
+
+
+def adding_stage_inputs(cfg: SynthConfig, frame: Frame, seed: int = 0, miss_frac: float = 0.02):
+    """Seeded stand-ins for the inputs of Gaussian adding, so adding can be
+    tested without consuming any CUDA output: V* = the analytic hit points (a raycast vertex map),
+    D_t = their camera depth with a few misses, C* = the shaded colour perturbed by N(0, 0.04)
+    (a render whose error exceeds delta_c on part of the image), W_G ~ U(0, 8), target C_k =
+    the frame's colour.  No arithmetic of the method: only the scene, noise and masks."""
+    rng = np.random.default_rng(9000 + seed)
+    Dt = frame.depth_m.numpy().astype(np.float32).copy()
+    Dt[rng.random(Dt.shape) < miss_frac] = 0.0
+    V = frame.points.numpy().astype(np.float32).copy()
+    V[Dt == 0] = 0.0
+    rgb = frame.rgb.numpy().astype(np.float64)
+    Cs = np.clip(rgb + rng.normal(0, 0.04, size=rgb.shape), 0, 1).astype(np.float32)
+    WG = rng.uniform(0, 8, size=Dt.shape).astype(np.float32)
+    return {"V": V, "Dt": Dt, "Cstar": Cs, "WG": WG, "target": frame.rgba.numpy()}

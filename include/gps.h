@@ -252,6 +252,67 @@ gps_status gps_adam_step(gps_gaussians* g, gps_adam_state* state /*host struct*/
                          const gps_gaussians* grad, const gps_adam_config* acfg /*host*/,
                          gps_stream_t stream);
 
+/* ---- Gaussian adding and removal (readings R-NORMAL .. R-REMOVE,
+ * DESIGN.md §3) ------------------------------------------------------------------------------ */
+
+/* gps_vertex_normals -- the raycast normal map N* from the raycast vertex map V* (P:106):
+ * N(u,v) = normalise((V(u+1,v) - V(u-1,v)) x (V(u,v+1) - V(u,v-1))) turned towards the camera
+ * centre T.t; 0 where the pixel or one of its 4 neighbours is a miss (sdf_depth = 0), on the
+ * image border, or where the cross product vanishes (R-NORMAL).
+ * vertex f32[H*W*3] (world, as gps_raycast's vertex_out), normal_out f32[H*W*3].              */
+gps_status gps_vertex_normals(const gps_intrinsics* K /*host*/, const gps_pose* T /*host*/,
+                              const float* sdf_depth, const float* vertex, float* normal_out,
+                              gps_stream_t stream);
+
+typedef struct {
+  float delta_c;      /* colour-error threshold of Eq. 6 [0.05]                         */
+  float delta_w;      /* Gaussian-weight threshold of Eq. 6 [4]                         */
+  float sample_frac;  /* fraction of M sampled [0.25]                                   */
+  float opacity_init; /* initial opacity [0.5]                                          */
+  float scale_max;    /* truncation of the kNN scale (App. A) [0.1]                       */
+  float knn_cell;     /* cell edge of the kNN grid, metres (accelerator only) [0.01]            */
+  uint32_t seed;      /* sampling seed (R-SAMPLE): the caller varies it per round               */
+  int32_t reserved;   /* 0                                                                      */
+} gps_add_config;
+
+size_t gps_add_workspace_size(const gps_intrinsics* K /*host*/);
+
+/* gps_add_gaussians_sync -- Gaussian adding (Eq. 6, App. A):
+ * M = {u : sdf_depth > 0, normal != 0, max_ch |C*_ch - C_k,ch| > delta_c, W_G < delta_W}
+ * (fp32 decisions, R-ADD-MASK); a seeded counter hash keeps sample_frac of M (R-SAMPLE); each
+ * kept pixel u, in row-major order, becomes Gaussian n + i with p = V*(u), SH0 = (C_k(u) - 0.5)/C0
+ * (higher SH 0), opacity_init, the rotation taking e_z to N*(u), and log-scales
+ * (s1, s1, 0.1 s1), s1 = min(scale_max, RMS distance to the 3 nearest other vertices of M)
+ * (R-KNN).  Their Adam moments are zeroed (state->step is global and unchanged).
+ * g: caller SoA whose arrays hold `capacity` Gaussians; g->n is updated on the host.
+ * Synchronises once (the counts).  *n_added (host) = Gaussians written; *n_candidates (host,
+ * nullable) = sampled pixels (> n_added only when capacity ran out).                         */
+gps_status gps_add_gaussians_sync(gps_gaussians* g, int64_t capacity, gps_adam_state* state /*host*/,
+                                  const gps_intrinsics* K /*host*/, const float* sdf_depth,
+                                  const float* vertex, const float* normal, const float* cstar,
+                                  const float* weight, const uint8_t* target_rgba,
+                                  const gps_add_config* cfg /*host*/, void* ws, size_t ws_bytes,
+                                  int64_t* n_added /*host*/, int64_t* n_candidates /*host*/,
+                                  gps_stream_t stream);
+
+typedef struct {
+  float sigma_min;  /* delta_sigma of Eq. 8 [0.005]                                    */
+  float scale_max;  /* delta_s_max [0.1]                                                        */
+  float scale_min;  /* delta_s_min [0.003]                                                      */
+  int32_t reserved; /* 0                                                                        */
+} gps_remove_config;
+
+size_t gps_remove_workspace_size(int64_t n, int32_t sh_degree);
+
+/* gps_remove_gaussians_sync -- Gaussian removal (Eq. 8): deletes every Gaussian with
+ * sigmoid(o) < sigma_min, max_k exp(ls_k) > scale_max or max_k exp(ls_k) < scale_min, decided in
+ * fp32 on the raw parameters against thresholds rounded once from double (R-REMOVE).  The
+ * survivors keep their order; their Adam moments move with them.  g->n is updated on the host.
+ * Synchronises once.  *n_removed (host) = Gaussians deleted.                                 */
+gps_status gps_remove_gaussians_sync(gps_gaussians* g, gps_adam_state* state /*host*/,
+                                     const gps_remove_config* cfg /*host*/, void* ws, size_t ws_bytes,
+                                     int64_t* n_removed /*host*/, gps_stream_t stream);
+
 /* Synchronises `stream` and reports the pair count K of the last render held in `ws`, the pair
  * capacity, and the number of Gaussians that survived culling.  Returns
  * GPS_ERR_WORKSPACE_TOO_SMALL if K exceeded the capacity (that render dropped pairs).        */

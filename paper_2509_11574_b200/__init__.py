@@ -5,8 +5,8 @@ package is the thin Python binding (``api``), the host-side round schedule (``sc
 the in-tree build (``build``).  Importing it loads libgps.so and raises if it is missing.
 """
 from . import _native
-from .api import (AdamConfig, AdamState, Camera, Gaussians, Rasterizer, RenderConfig, View, Volume,
-                  adam_step, pose_struct)
+from .api import (AdamConfig, AdamState, AddConfig, Camera, Gaussians, Rasterizer, RemoveConfig, RenderConfig, View,
+                  Volume, adam_step, add_gaussians, pose_struct, remove_gaussians, vertex_normals)
 
-__all__ = ["AdamConfig", "AdamState", "Camera", "Gaussians", "Rasterizer", "RenderConfig", "View", "Volume",
-           "adam_step", "pose_struct"]
+__all__ = ["AdamConfig", "AdamState", "AddConfig", "Camera", "Gaussians", "Rasterizer", "RemoveConfig", "RenderConfig",
+           "View", "Volume", "adam_step", "add_gaussians", "pose_struct", "remove_gaussians", "vertex_normals"]

@@ -63,6 +63,17 @@ class gps_view(C.Structure):
                 ("sdf_color", C.c_void_p), ("target_rgba", C.c_void_p)]
 
 
+class gps_add_config(C.Structure):
+    _fields_ = [("delta_c", C.c_float), ("delta_w", C.c_float), ("sample_frac", C.c_float),
+                ("opacity_init", C.c_float), ("scale_max", C.c_float), ("knn_cell", C.c_float),
+                ("seed", C.c_uint32), ("reserved", C.c_int32)]
+
+
+class gps_remove_config(C.Structure):
+    _fields_ = [("sigma_min", C.c_float), ("scale_max", C.c_float), ("scale_min", C.c_float),
+                ("reserved", C.c_int32)]
+
+
 P = C.POINTER
 vp, i64, i32, f32, sz = C.c_void_p, C.c_int64, C.c_int32, C.c_float, C.c_size_t
 
@@ -84,6 +95,14 @@ PROTOTYPES = {
     "gps_adam_step": (gps_status, [P(gps_gaussians), P(gps_adam_state), P(gps_gaussians),
                                    P(gps_adam_config), gps_stream_t]),
     "gps_render_stats_sync": (gps_status, [vp, gps_stream_t, P(i64), P(i64), P(i64)]),
+    "gps_vertex_normals": (gps_status, [P(gps_intrinsics), P(gps_pose), vp, vp, vp, gps_stream_t]),
+    "gps_add_workspace_size": (sz, [P(gps_intrinsics)]),
+    "gps_add_gaussians_sync": (gps_status, [P(gps_gaussians), i64, P(gps_adam_state), P(gps_intrinsics), vp, vp,
+                                            vp, vp, vp, vp, P(gps_add_config), vp, sz, P(i64), P(i64),
+                                            gps_stream_t]),
+    "gps_remove_workspace_size": (sz, [i64, i32]),
+    "gps_remove_gaussians_sync": (gps_status, [P(gps_gaussians), P(gps_adam_state), P(gps_remove_config), vp, sz,
+                                               P(i64), gps_stream_t]),
     "gps_debug_export_blocks_sync": (gps_status, [vp, gps_stream_t, vp, vp, i64, P(i64)]),
     "gps_debug_export_visible_sync": (gps_status, [vp, gps_stream_t, vp, i64, P(i64)]),
     "gps_debug_apron_check_sync": (gps_status, [vp, gps_stream_t, P(i64)]),

@@ -190,28 +190,43 @@ FIELDS = ("xyz", "log_scale", "rot", "opacity_raw", "sh")
 
 
 class Gaussians:
-    """Caller-owned SoA parameter arrays (float32, contiguous, CUDA)."""
+    """Caller-owned SoA parameter arrays (float32, contiguous, CUDA).  The arrays hold `capacity`
+    Gaussians (default n); the public attributes are views of the first n rows, so Gaussian
+    adding / removal (gps_add_gaussians_sync / gps_remove_gaussians_sync) change n in place."""
 
-    def __init__(self, n: int, sh_degree: int, device="cuda", tensors: dict | None = None):
-        self.n, self.sh_degree = int(n), int(sh_degree)
+    def __init__(self, n: int, sh_degree: int, device="cuda", tensors: dict | None = None,
+                 capacity: int | None = None):
+        self.sh_degree = int(sh_degree)
+        n = int(n)
+        cap = max(int(capacity if capacity is not None else n), n)
         nc = (sh_degree + 1) ** 2
-        shapes = {"xyz": (n, 3), "log_scale": (n, 3), "rot": (n, 4), "opacity_raw": (n,), "sh": (n, nc * 3)}
+        self._shapes = {"xyz": (3,), "log_scale": (3,), "rot": (4,), "opacity_raw": (), "sh": (nc * 3,)}
+        self._store = {}
         for k in FIELDS:
+            buf = torch.zeros((cap,) + self._shapes[k], dtype=torch.float32, device=device)
             if tensors is not None:
-                v = torch.as_tensor(np.asarray(tensors[k], np.float32)).reshape(shapes[k])
-                setattr(self, k, v.to(device).contiguous())
-            else:
-                setattr(self, k, torch.zeros(shapes[k], dtype=torch.float32, device=device))
+                v = torch.as_tensor(np.asarray(tensors[k], np.float32)).reshape((n,) + self._shapes[k])
+                buf[:n].copy_(v.to(device))
+            self._store[k] = buf
+        self.capacity = cap
+        self.set_n(n)
+
+    def set_n(self, n: int):
+        if n > self.capacity:
+            raise ValueError("n exceeds capacity")
+        self.n = int(n)
+        for k in FIELDS:
+            setattr(self, k, self._store[k][:self.n])
 
     @staticmethod
-    def from_dict(d: dict, device="cuda") -> "Gaussians":
-        return Gaussians(int(np.asarray(d["xyz"]).shape[0]), int(d["sh_degree"]), device, d)
+    def from_dict(d: dict, device="cuda", capacity: int | None = None) -> "Gaussians":
+        return Gaussians(int(np.asarray(d["xyz"]).shape[0]), int(d["sh_degree"]), device, d, capacity)
 
     def zeros_like(self) -> "Gaussians":
-        return Gaussians(self.n, self.sh_degree, self.xyz.device)
+        return Gaussians(self.n, self.sh_degree, self.xyz.device, capacity=self.capacity)
 
     def c(self) -> N.gps_gaussians:
-        return N.gps_gaussians(self.n, self.sh_degree, *(C.c_void_p(getattr(self, k).data_ptr()) for k in FIELDS))
+        return N.gps_gaussians(self.n, self.sh_degree, *(C.c_void_p(self._store[k].data_ptr()) for k in FIELDS))
 
     def to_numpy(self) -> dict:
         out = {k: getattr(self, k).detach().cpu().numpy() for k in FIELDS}
@@ -219,7 +234,7 @@ class Gaussians:
         return out
 
     def clone(self) -> "Gaussians":
-        g = Gaussians(self.n, self.sh_degree, self.xyz.device)
+        g = Gaussians(self.n, self.sh_degree, self.xyz.device, capacity=self.capacity)
         for k in FIELDS:
             getattr(g, k).copy_(getattr(self, k))
         return g
@@ -291,6 +306,14 @@ class Rasterizer:
         self.ws = torch.empty(size, dtype=torch.uint8, device="cuda")
         self.loss = torch.zeros(1, dtype=torch.float32, device="cuda")
 
+    def reserve(self, n: int):
+        """Grow the workspace for up to n Gaussians (after Gaussian adding)."""
+        if n <= self.n:
+            return
+        size = _L.gps_refine_workspace_size(n, C.byref(self.cam.c()), C.byref(self.cfg.c()), self.n_views)
+        self.ws = torch.empty(size, dtype=torch.uint8, device="cuda")
+        self.n = n
+
     def render(self, g: Gaussians, cam: Camera, R, t, sdf_depth, sdf_color, target_rgba=None,
                out_color=None, out_weight=None, stream=None):
         if out_color is None:
@@ -344,3 +367,86 @@ def adam_step(g: Gaussians, state: AdamState, grad: Gaussians, adam: AdamConfig 
     N.check("gps_adam_step", _L.gps_adam_step(C.byref(g.c()), C.byref(st), C.byref(grad.c()), C.byref(adam.c()),
                                               _stream(stream)))
     state.step = st.step
+
+
+# ---------------------------------------------------------------------------------------------
+# Gaussian adding and removal
+# ---------------------------------------------------------------------------------------------
+@dataclass
+class AddConfig:
+    delta_c: float = 0.05      # Eq. 6
+    delta_w: float = 4.0       # Eq. 6
+    sample_frac: float = 0.25
+    opacity_init: float = 0.5
+    scale_max: float = 0.1     # App. A
+    knn_cell: float = 0.01     # kNN grid cell (accelerator only)
+    seed: int = 0              # R-SAMPLE
+
+    def c(self) -> N.gps_add_config:
+        return N.gps_add_config(self.delta_c, self.delta_w, self.sample_frac, self.opacity_init, self.scale_max,
+                                self.knn_cell, self.seed & 0xFFFFFFFF, 0)
+
+
+@dataclass
+class RemoveConfig:
+    sigma_min: float = 0.005   # Eq. 8
+    scale_max: float = 0.1
+    scale_min: float = 0.003
+
+    def c(self) -> N.gps_remove_config:
+        return N.gps_remove_config(self.sigma_min, self.scale_max, self.scale_min, 0)
+
+
+def vertex_normals(cam: Camera, R, t, sdf_depth: torch.Tensor, vertex: torch.Tensor, out=None, stream=None):
+    """N* from the raycast vertex map (gps_vertex_normals, R-NORMAL)."""
+    if out is None:
+        out = torch.empty_like(vertex)
+    N.check("gps_vertex_normals", _L.gps_vertex_normals(C.byref(cam.c()), C.byref(pose_struct(R, t)), _ptr(sdf_depth),
+                                                        _ptr(vertex), _ptr(out), _stream(stream)))
+    return out
+
+
+_ws_cache: dict = {}
+
+
+def _ws(key, size):
+    t = _ws_cache.get(key)
+    if t is None or t.numel() < size:
+        t = torch.empty(size, dtype=torch.uint8, device="cuda")
+        _ws_cache[key] = t
+    return t
+
+
+def add_gaussians(g: Gaussians, state: AdamState, cam: Camera, sdf_depth, vertex, normal, cstar, weight,
+                  target_rgba, cfg: AddConfig | None = None, stream=None):
+    """Gaussian adding (gps_add_gaussians_sync): appends to g (up to its capacity) and zeroes
+    the new Gaussians' Adam moments; returns (added, candidates).  Synchronises."""
+    cfg = cfg or AddConfig()
+    ws = _ws("add", _L.gps_add_workspace_size(C.byref(cam.c())))
+    st = N.gps_adam_state(state.m.c(), state.v.c(), state.step)
+    gc = g.c()
+    added, cand = C.c_int64(), C.c_int64()
+    N.check("gps_add_gaussians_sync",
+            _L.gps_add_gaussians_sync(C.byref(gc), g.capacity, C.byref(st), C.byref(cam.c()), _ptr(sdf_depth),
+                                      _ptr(vertex), _ptr(normal), _ptr(cstar), _ptr(weight), _ptr(target_rgba),
+                                      C.byref(cfg.c()), _ptr(ws), ws.numel(), C.byref(added), C.byref(cand),
+                                      _stream(stream)))
+    for x in (g, state.m, state.v):
+        x.set_n(gc.n)
+    return added.value, cand.value
+
+
+def remove_gaussians(g: Gaussians, state: AdamState, cfg: RemoveConfig | None = None, stream=None) -> int:
+    """Gaussian removal (gps_remove_gaussians_sync): stable in-place compaction of g and its Adam
+    moments; returns the number removed.  Synchronises."""
+    cfg = cfg or RemoveConfig()
+    ws = _ws("remove", _L.gps_remove_workspace_size(g.n, g.sh_degree))
+    st = N.gps_adam_state(state.m.c(), state.v.c(), state.step)
+    gc = g.c()
+    removed = C.c_int64()
+    N.check("gps_remove_gaussians_sync",
+            _L.gps_remove_gaussians_sync(C.byref(gc), C.byref(st), C.byref(cfg.c()), _ptr(ws), ws.numel(),
+                                         C.byref(removed), _stream(stream)))
+    for x in (g, state.m, state.v):
+        x.set_n(gc.n)
+    return removed.value

@@ -31,7 +31,8 @@ class MappingPipeline:
                  render_cfg: A.RenderConfig | None = None, adam_cfg: A.AdamConfig | None = None,
                  delta_k: int = Sch.DELTA_K, iterations: int = Sch.ITERATIONS,
                  n_global: int = Sch.N_GLOBAL, n_local: int = Sch.N_LOCAL, seed: int = 0,
-                 overlap: bool = True, refine_priority: int = -1):
+                 overlap: bool = True, refine_priority: int = -1, manage_gaussians: bool = False,
+                 add_cfg: A.AddConfig | None = None, remove_cfg: A.RemoveConfig | None = None):
         self.cam, self.g, self.vol = cam, gaussians, volume
         self.depth_scale = float(depth_scale)
         self.rcfg = render_cfg or A.RenderConfig()
@@ -39,7 +40,15 @@ class MappingPipeline:
         self.delta_k, self.iterations = delta_k, iterations
         self.n_global, self.n_local = n_global, n_local
         self.state = A.AdamState(gaussians)
-        self.ras = A.Rasterizer(gaussians.n, cam, self.rcfg, n_views=1)
+        # workspace sized for the Gaussians' capacity: adding never reallocates it mid-stream
+        self.ras = A.Rasterizer(gaussians.capacity, cam, self.rcfg, n_views=1)
+        # Gaussian adding / removal
+        self.manage = manage_gaussians
+        self.add_cfg = add_cfg or A.AddConfig()
+        self.remove_cfg = remove_cfg or A.RemoveConfig()
+        self.added_total = 0
+        self.removed_total = 0
+        self._removal_pending = False
         self.kf = Sch.KeyframeSelector()
         self.rng = np.random.default_rng(seed)
         H, W = cam.height, cam.width
@@ -49,6 +58,13 @@ class MappingPipeline:
         self._fcolor = torch.empty((H, W, 3), dtype=torch.float32, device=dev)
         self.depth, self.color = self._fdepth, self._fcolor
         nv = n_global + n_local
+        # adding inputs of a round frame (its D_t, C_t, V*, N*) and the second-pass render, one set
+        # per view-buffer set: written by the fusion stream at the round frame, read by the
+        # refinement stream in that round, rewritten two rounds later (after _set_free)
+        mk = lambda *shape: [torch.empty(shape, dtype=torch.float32, device=dev) for _ in range(2)]
+        if manage_gaussians:
+            self.r_depth, self.r_color, self.vertex, self.normal = mk(H, W), mk(H, W, 3), mk(H, W, 3), mk(H, W, 3)
+            self._add_color, self._add_weight = mk(H, W, 3), mk(H, W)
         nsets = 2
         self.view_depth = [[torch.empty((H, W), dtype=torch.float32, device=dev) for _ in range(nv)]
                            for _ in range(nsets)]
@@ -93,17 +109,23 @@ class MappingPipeline:
         round_now = refine and Sch.is_round_frame(k, self.delta_k)
         views_ids = None
         self.depth, self.color = self._fdepth, self._fcolor
+        want_v = round_now and self.manage
         if round_now:
             views_ids = Sch.select_views(self.kf.keyframes, self.interval, self.rng, self.n_global, self.n_local)
             s = self.rounds % len(self.view_depth)
             self._wait_set(s)
-            if k in views_ids:
+            if want_v:
+                # the round frame's raycast also feeds Gaussian adding: into the round's set
+                self.depth, self.color = self.r_depth[s], self.r_color[s]
+            elif k in views_ids:
                 # the frame just fused is a view: its per-frame raycast is the view's
                 j = views_ids.index(k)
                 self.depth, self.color = self.view_depth[s][j], self.view_color[s][j]
-        self.vol.raycast(self.cam, R, t, self.depth, self.color)
+        self.vol.raycast(self.cam, R, t, self.depth, self.color, vertex_out=self.vertex[s] if want_v else None)
+        if want_v:
+            A.vertex_normals(self.cam, R, t, self.depth, self.vertex[s], out=self.normal[s])
         if round_now:
-            self._refine_round(views_ids)
+            self._refine_round(views_ids, add_frame=(k, rgba, R, t, s) if self.manage else None)
         if len(self.interval) >= self.delta_k or Sch.is_round_frame(k, self.delta_k):
             self.interval = []
         # keep device frames only for keyframes and the current interval
@@ -139,11 +161,14 @@ class MappingPipeline:
                 "step": self.state.step, "kf": (list(self.kf.keyframes), copy.deepcopy(self.kf._last)),
                 "frames": dict(self.frames), "interval": list(self.interval), "last_frame": self.last_frame,
                 "rng": copy.deepcopy(self.rng.bit_generator.state), "rounds": self.rounds,
-                "iterations_run": self.iterations_run}
+                "iterations_run": self.iterations_run, "removal_pending": self._removal_pending,
+                "added_total": self.added_total, "removed_total": self.removed_total}
 
     def restore(self, s):
         self.join()
         self.vol.copy_from(s["vol"])
+        for x in (self.g, self.state.m, self.state.v):
+            x.set_n(s["g"].n)
         for k in A.FIELDS:
             getattr(self.g, k).copy_(getattr(s["g"], k))
             getattr(self.state.m, k).copy_(getattr(s["m"], k))
@@ -153,6 +178,8 @@ class MappingPipeline:
         self.frames, self.interval, self.last_frame = dict(s["frames"]), list(s["interval"]), s["last_frame"]
         self.rng.bit_generator.state = s["rng"]
         self.rounds, self.iterations_run = s["rounds"], s["iterations_run"]
+        self._removal_pending = s["removal_pending"]
+        self.added_total, self.removed_total = s["added_total"], s["removed_total"]
         if True:  # the refinement stream must see the restored state
             ev = torch.cuda.Event()
             ev.record(torch.cuda.current_stream())
@@ -165,13 +192,33 @@ class MappingPipeline:
         self._wait_set(self.rounds % len(self.view_depth))
         return self._refine_round(views_ids, reuse_last=False)
 
-    def _refine_round(self, views_ids, reuse_last: bool = True):
+    def _manage(self, rs, add_frame):
+        """On the refinement stream, before the round's iterations: the previous round's Gaussian
+        removal (Eq. 8: "after each Gaussian optimization" -- nothing reads the
+        Gaussians in between, so deferring it to here is the same sequence), then Gaussian adding
+        for the round frame (Eq. 6) from its raycast V*, N* and a second-pass render
+        with the existing Gaussians.  Both synchronise (the new count is host state)."""
+        if self._removal_pending:
+            self.removed_total += A.remove_gaussians(self.g, self.state, self.remove_cfg, stream=rs)
+            self._removal_pending = False
+        k, rgba, R, t, s = add_frame
+        self.ras.render(self.g, self.cam, R, t, self.r_depth[s], self.r_color[s], None, self._add_color[s],
+                        self._add_weight[s], stream=rs)
+        cfg = A.AddConfig(**{**self.add_cfg.__dict__, "seed": (self.add_cfg.seed * 1000003 + k) & 0xFFFFFFFF})
+        added, _ = A.add_gaussians(self.g, self.state, self.cam, self.r_depth[s], self.vertex[s], self.normal[s],
+                                   self._add_color[s], self._add_weight[s], rgba, cfg, stream=rs)
+        self.added_total += added
+
+    def _refine_round(self, views_ids, reuse_last: bool = True, add_frame=None):
         s = self.rounds % len(self.view_depth)
         views = []
         for j, f in enumerate(views_ids):
             rgba, R, t = self.frames[f]
-            if not (reuse_last and f == self.last_frame):
-                self.vol.raycast(self.cam, R, t, self.view_depth[s][j], self.view_color[s][j])
+            if reuse_last and f == self.last_frame:
+                # the frame just fused was raycast against this very volume: same result (P:138)
+                views.append(A.View(self.cam, R, t, self.depth, self.color, rgba))
+                continue
+            self.vol.raycast(self.cam, R, t, self.view_depth[s][j], self.view_color[s][j])
             views.append(A.View(self.cam, R, t, self.view_depth[s][j], self.view_color[s][j], rgba))
         if self.overlap:
             ready = torch.cuda.Event()
@@ -180,15 +227,21 @@ class MappingPipeline:
             rs.wait_event(ready)
             for v in views:
                 v.target_rgba.record_stream(rs)
+            if add_frame is not None:
+                add_frame[1].record_stream(rs)
         else:
             rs = torch.cuda.current_stream()
             self.join(rs)  # after any refinement still running from an overlapped round
         with torch.cuda.stream(rs):
+            if add_frame is not None:
+                self._manage(rs, add_frame)
             for i in range(self.iterations):
                 v = views[Sch.view_for_iteration(i, len(views))]
                 self.last_loss = self.ras.refine_step(self.g, self.state, [v], self.adam, stream=rs)
             done = torch.cuda.Event()
             done.record(rs)
+        if self.manage:
+            self._removal_pending = True
         self._set_free[s] = done
         self._refine_done = done
         self.rounds += 1

@@ -69,3 +69,42 @@ def test_overlapped_rounds_match_serial():
     moved = np.abs(g0["xyz"] - gd["xyz"]).max()
     assert moved > 0
     assert np.median(np.abs(g1["xyz"] - g0["xyz"])) <= 1e-6
+
+
+def test_pipeline_with_gaussian_adding_and_removal():
+    """NEXT-2 inside the mapping step: rounds add Gaussians where Eq. 6 flags colour errors and
+    remove the Eq. 8 set; the overlapped and the serial schedules take the same decisions up to
+    fp32 render-order noise in the add mask (counts within 1%)."""
+    import paper_2509_11574_b200 as G
+    from paper_2509_11574_b200.pipeline import MappingPipeline
+
+    cfg = S.get_config("cfg2")
+    n_frames = 31  # rounds at frames 0, 10, 20, 30
+    scene = S.make_scene(cfg)
+    dc = S.pixel_rays(cfg, "cuda")
+    poses = S.trajectory(cfg, n_frames)
+    frames = []
+    for k in range(n_frames):
+        fr = S.render_frame(cfg, scene, *poses[k], k=k, device="cuda", dc=dc)
+        frames.append((fr.depth.contiguous(), fr.rgba.contiguous(), fr.R, fr.t))
+    gd = S.make_gaussians(cfg, n=5000)
+    res = []
+    for overlap in (False, True):
+        cam = G.Camera(cfg.fx, cfg.fy, cfg.cx, cfg.cy, cfg.width, cfg.height)
+        vol = G.Volume(voxel_size=cfg.voxel_size, max_blocks=cfg.max_blocks, hash_slots=cfg.hash_slots)
+        g = G.Gaussians.from_dict(gd, capacity=400_000)
+        pipe = MappingPipeline(cam, g, vol, cfg.depth_scale, seed=3, overlap=overlap, manage_gaussians=True)
+        for k in range(n_frames):
+            d, c, R, t = frames[k]
+            pipe.process_frame(k, d, c, R, t)
+        pipe.join()
+        torch.cuda.synchronize()
+        assert np.isfinite(pipe.last_loss.item())
+        res.append((g.n, pipe.added_total, pipe.removed_total, pipe.rounds))
+        gn = g.to_numpy()
+        assert np.all(np.isfinite(gn["xyz"])) and np.all(np.isfinite(gn["sh"]))
+    (n0, a0, r0, k0), (n1, a1, r1, k1) = res
+    assert k0 == k1 == 4
+    assert a0 > 100 and r0 >= 0                       # the rounds added (removal: its own test)
+    assert n0 == 5000 + a0 - r0 and n1 == 5000 + a1 - r1
+    assert abs(a1 - a0) <= 0.01 * a0 and abs(n1 - n0) <= 0.01 * n0
