@@ -45,6 +45,10 @@ def parse():
     ap.add_argument("--no-profile", action="store_true", help="time without the per-launch event profiler")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--refine-priority", type=int, default=-1, help="CUDA stream priority of the refinement stream")
+    ap.add_argument("--manage-gaussians", action="store_true",
+                    help="Gaussian adding (Eq. 6) and removal (Eq. 8) every round (NEXT-2)")
+    ap.add_argument("--all-views", action="store_true",
+                    help="every iteration renders all the round's views (SPEC S:471 variant, NEXT-4)")
     ap.add_argument("--no-overlap", action="store_true",
                     help="refinement on the fusion stream (serial schedule) instead of its own stream")
     ap.add_argument("--cpu-seconds", type=float, default=20.0, help="budget of the cpu_baseline sample")
@@ -166,10 +170,11 @@ def run_ours(args):
     cam = G.Camera(cfg.fx, cfg.fy, cfg.cx, cfg.cy, cfg.width, cfg.height)
     vol = G.Volume(voxel_size=cfg.voxel_size, max_blocks=cfg.max_blocks, hash_slots=cfg.hash_slots,
                    dense_bounds=S.scene_bounds(cfg))
-    g = G.Gaussians.from_dict(gd)
+    g = G.Gaussians.from_dict(gd, capacity=4 * n_g if args.manage_gaussians else None)
     rcfg = G.RenderConfig(tile=args.tile, sort_free=int(args.sort_free))
     pipe = MappingPipeline(cam, g, vol, cfg.depth_scale, rcfg, seed=rank,
-                           overlap=not args.no_overlap, refine_priority=args.refine_priority)
+                           overlap=not args.no_overlap, refine_priority=args.refine_priority,
+                           manage_gaussians=args.manage_gaussians, all_views_per_iteration=args.all_views)
     k = 0
     for _ in range(args.history):  # build a steady-state volume (untimed, no rounds)
         d, c, R, t = frames[k]
@@ -351,7 +356,8 @@ def run_ours(args):
                         "per-launch events)",
         "cpu_baseline": cpu,
         "clocks": clk,
-        "stats": {"render": rstats, "volume": vstats, "setup_s": round(t_setup, 1), "rounds": pipe.rounds},
+        "stats": {"render": rstats, "volume": vstats, "setup_s": round(t_setup, 1), "rounds": pipe.rounds,
+                  "gaussians_final": g.n, "added": pipe.added_total, "removed": pipe.removed_total},
     }
     if ws > 1:
         dist.destroy_process_group()
@@ -383,11 +389,14 @@ def per_kernel_bytes(args, cfg, n_g, P, per_launch, rstats, vstats, upd0, prof):
 
 
 def workload_config(args, cfg, n_g, ws):
+    vpi = "all 6 views/iteration (S:471)" if args.all_views else "R-VIEW: 1 view/iteration"
     return {"workload": f"{args.config}: {cfg.width}x{cfg.height} synthetic RGB-D ({cfg.name}), {n_g} Gaussians "
                         f"(SH deg {args.sh_degree}), voxel {cfg.voxel_size} m, delta_k=10, 20 iters/round, "
-                        f"6 views/round (R-VIEW: 1 view/iteration); step = 10 frames",
+                        f"6 views/round ({vpi}); step = 10 frames",
             "frames_per_step": 10, "gaussians": n_g, "sh_degree": args.sh_degree, "tile": args.tile,
             "renderer": "sort-free (P:99-100)" if args.sort_free else "depth-sorted tile lists",
+            "gaussian_management": "adding (Eq. 6) + removal (Eq. 8) every round" if args.manage_gaussians else "off",
+            "views_per_iteration": "all (S:471)" if args.all_views else "one (R-VIEW)",
             "resolution": [cfg.width, cfg.height], "history_frames": args.history,
             "parallelism": f"replicas x{ws} (independent sequences)",
             "streams": "fusion+raycast on one stream, refinement rounds on a second (P:116)"

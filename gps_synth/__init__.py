@@ -70,6 +70,11 @@ CONFIGS = {
                         "room", room=(8.0, 6.0, 2.8), n_objects=10, noise="tof", dropout=0.06,
                         range_min=0.25, range_max=5.5, seed=4, max_blocks=1 << 19,
                         hash_slots=1 << 21),
+    # NEXT-4: ScanNet++-shaped, 1752x1168 ("2.2x ... standard"), a DSLR-like
+    # clean depth (no sensor noise), fx scaled from cfg4's field of view; intrinsics invented
+    "scannetpp": SynthConfig("scannetpp", 1752, 1168, 828.0, 828.0, 875.5, 583.5, 1000.0, 3000, 200_000,
+                             "room", room=(8.0, 6.0, 2.8), n_objects=10, noise="none", dropout=0.0,
+                             range_min=0.25, range_max=8.0, seed=6, max_blocks=1 << 19, hash_slots=1 << 21),
 }
 
 

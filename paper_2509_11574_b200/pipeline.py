@@ -32,7 +32,8 @@ class MappingPipeline:
                  delta_k: int = Sch.DELTA_K, iterations: int = Sch.ITERATIONS,
                  n_global: int = Sch.N_GLOBAL, n_local: int = Sch.N_LOCAL, seed: int = 0,
                  overlap: bool = True, refine_priority: int = -1, manage_gaussians: bool = False,
-                 add_cfg: A.AddConfig | None = None, remove_cfg: A.RemoveConfig | None = None):
+                 add_cfg: A.AddConfig | None = None, remove_cfg: A.RemoveConfig | None = None,
+                 all_views_per_iteration: bool = False):
         self.cam, self.g, self.vol = cam, gaussians, volume
         self.depth_scale = float(depth_scale)
         self.rcfg = render_cfg or A.RenderConfig()
@@ -41,7 +42,11 @@ class MappingPipeline:
         self.n_global, self.n_local = n_global, n_local
         self.state = A.AdamState(gaussians)
         # workspace sized for the Gaussians' capacity: adding never reallocates it mid-stream
-        self.ras = A.Rasterizer(gaussians.capacity, cam, self.rcfg, n_views=1)
+        # R-VIEW: one view per iteration; all_views_per_iteration: every iteration renders all the
+        # round's views and sums their gradients (SPEC S:471 variant)
+        self.all_views = all_views_per_iteration
+        self.ras = A.Rasterizer(gaussians.capacity, cam, self.rcfg,
+                                n_views=(n_global + n_local) if all_views_per_iteration else 1)
         # Gaussian adding / removal
         self.manage = manage_gaussians
         self.add_cfg = add_cfg or A.AddConfig()
@@ -236,8 +241,8 @@ class MappingPipeline:
             if add_frame is not None:
                 self._manage(rs, add_frame)
             for i in range(self.iterations):
-                v = views[Sch.view_for_iteration(i, len(views))]
-                self.last_loss = self.ras.refine_step(self.g, self.state, [v], self.adam, stream=rs)
+                vs = views if self.all_views else [views[Sch.view_for_iteration(i, len(views))]]
+                self.last_loss = self.ras.refine_step(self.g, self.state, vs, self.adam, stream=rs)
             done = torch.cuda.Event()
             done.record(rs)
         if self.manage:
