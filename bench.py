@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--refine-priority", type=int, default=-1, help="CUDA stream priority of the refinement stream")
     ap.add_argument("--manage-gaussians", action="store_true",
                     help="Gaussian adding (Eq. 6) and removal (Eq. 8) every round (NEXT-2)")
+    ap.add_argument("--track", action="store_true",
+                    help="ICP tracking of every frame (Eq. 5, NEXT-3) instead of the given poses")
     ap.add_argument("--all-views", action="store_true",
                     help="every iteration renders all the round's views (SPEC S:471 variant, NEXT-4)")
     ap.add_argument("--no-overlap", action="store_true",
@@ -174,7 +176,9 @@ def run_ours(args):
     rcfg = G.RenderConfig(tile=args.tile, sort_free=int(args.sort_free))
     pipe = MappingPipeline(cam, g, vol, cfg.depth_scale, rcfg, seed=rank,
                            overlap=not args.no_overlap, refine_priority=args.refine_priority,
-                           manage_gaussians=args.manage_gaussians, all_views_per_iteration=args.all_views)
+                           manage_gaussians=args.manage_gaussians, all_views_per_iteration=args.all_views,
+                           track=args.track)
+    ate = []  # (tracked t, ground-truth t) of the timed frames
     k = 0
     for _ in range(args.history):  # build a steady-state volume (untimed, no rounds)
         d, c, R, t = frames[k]
@@ -191,6 +195,8 @@ def run_ours(args):
                     d, c = host[k]
                     R, t = frames[k][2], frames[k][3]
                 pipe.process_frame(k, d, c, R, t)
+                if args.track and host is None:
+                    ate.append((pipe.last_pose[1].astype(np.float64), np.asarray(frames[k][3], np.float64)))
                 k += 1
             if host is not None:  # the step's result read back (D2H) on the refinement stream
                 pipe.loss_to(host["loss"][host["i"]])
@@ -356,6 +362,9 @@ def run_ours(args):
                         "per-launch events)",
         "cpu_baseline": cpu,
         "clocks": clk,
+        "tracking": ({"ate_rmse_m": float(np.sqrt(np.mean([np.sum((a - b) ** 2) for a, b in ate]))),
+                      "frames": len(ate), "converged_frac": float(np.mean([r["converged"] for r in pipe.track_log]))}
+                     if args.track and ate else None),
         "stats": {"render": rstats, "volume": vstats, "setup_s": round(t_setup, 1), "rounds": pipe.rounds,
                   "gaussians_final": g.n, "added": pipe.added_total, "removed": pipe.removed_total},
     }
@@ -397,6 +406,7 @@ def workload_config(args, cfg, n_g, ws):
             "renderer": "sort-free (P:99-100)" if args.sort_free else "depth-sorted tile lists",
             "gaussian_management": "adding (Eq. 6) + removal (Eq. 8) every round" if args.manage_gaussians else "off",
             "views_per_iteration": "all (S:471)" if args.all_views else "one (R-VIEW)",
+            "poses": "ICP-tracked every frame (Eq. 5)" if args.track else "given (ground truth)",
             "resolution": [cfg.width, cfg.height], "history_frames": args.history,
             "parallelism": f"replicas x{ws} (independent sequences)",
             "streams": "fusion+raycast on one stream, refinement rounds on a second (P:116)"

@@ -313,6 +313,44 @@ gps_status gps_remove_gaussians_sync(gps_gaussians* g, gps_adam_state* state /*h
                                      const gps_remove_config* cfg /*host*/, void* ws, size_t ws_bytes,
                                      int64_t* n_removed /*host*/, gps_stream_t stream);
 
+/* ---- camera tracking (readings R-ICP-*) ---------------- */
+typedef struct {
+  int32_t levels;        /* pyramid levels, 1..4 [3] ("a resolution hierarchy")           */
+  int32_t iters[4];      /* Gauss-Newton steps per level, finest first [10, 5, 4]              */
+  float dist_max;        /* correspondence gate, metres [0.1] (R-ICP-GATE)                     */
+  float angle_max_deg;   /* normal-angle gate, degrees [30]                                     */
+  float depth_min, depth_max; /* valid raw depth range, metres [0.1, 10]                         */
+  float eps;             /* a level stops when |xi| < eps [1e-6]                                */
+  float min_inlier_frac; /* converged needs this inlier fraction at the end [0.1]               */
+} gps_icp_config;
+
+typedef struct {
+  gps_pose T;            /* tracked camera -> world pose (fp32 copy of R64, t64)                */
+  double R64[9], t64[3]; /* the pose as iterated on the device (fp64)                           */
+  double energy;         /* sum of squared point-to-plane residuals of the last step's inliers  */
+  int32_t inliers, valid;/* last step's inliers / current pixels with a normal                  */
+  int32_t steps;         /* Gauss-Newton steps taken                                            */
+  int32_t degenerate;    /* a step had < 6 inliers or a rank-deficient system (no update)       */
+  int32_t converged;     /* !degenerate and inliers/valid >= min_inlier_frac                    */
+  float inlier_frac;
+} gps_track_result;
+
+size_t gps_track_workspace_size(const gps_intrinsics* K /*host*/, int32_t levels);
+
+/* gps_track_sync -- Eq. 5: frame-to-model point-to-plane ICP of the depth frame
+ * (u16, raw / depth_scale metres) against the model maps V*_{k-1}, N*_{k-1} (world, f32[H*W*3],
+ * as gps_raycast's vertex_out and gps_vertex_normals) raycast from T_model, starting at T_init.
+ * Coarse to fine over a depth pyramid (R-ICP-PYR); each step associates every current pixel with
+ * the model pixel its point projects to in the T_model camera (R-ICP-ASSOC, the reading of the
+ * garbled projection of P:113), gates it (R-ICP-GATE), and solves the linearised system for a
+ * left-multiplied twist (R-ICP-GN).  The iteration runs on the device (pose in device memory);
+ * synchronises once, at the end.  Degenerate geometry is reported in `out`, not as an error.   */
+gps_status gps_track_sync(const gps_intrinsics* K /*host*/, const uint16_t* depth, float depth_scale,
+                          const float* model_vertex, const float* model_normal,
+                          const gps_pose* T_model /*host*/, const gps_pose* T_init /*host*/,
+                          const gps_icp_config* cfg /*host*/, void* ws, size_t ws_bytes,
+                          gps_track_result* out /*host*/, gps_stream_t stream);
+
 /* Synchronises `stream` and reports the pair count K of the last render held in `ws`, the pair
  * capacity, and the number of Gaussians that survived culling.  Returns
  * GPS_ERR_WORKSPACE_TOO_SMALL if K exceeded the capacity (that render dropped pairs).        */

@@ -6,7 +6,8 @@ the in-tree build (``build``).  Importing it loads libgps.so and raises if it is
 """
 from . import _native
 from .api import (AdamConfig, AdamState, AddConfig, Camera, Gaussians, Rasterizer, RemoveConfig, RenderConfig, View,
-                  Volume, adam_step, add_gaussians, pose_struct, remove_gaussians, vertex_normals)
+                  Volume, adam_step, add_gaussians, pose_struct, remove_gaussians, vertex_normals, IcpConfig, track)
 
 __all__ = ["AdamConfig", "AdamState", "AddConfig", "Camera", "Gaussians", "Rasterizer", "RemoveConfig", "RenderConfig",
-           "View", "Volume", "adam_step", "add_gaussians", "pose_struct", "remove_gaussians", "vertex_normals"]
+           "View", "Volume", "adam_step", "add_gaussians", "pose_struct", "remove_gaussians", "vertex_normals",
+           "IcpConfig", "track"]

@@ -74,6 +74,18 @@ class gps_remove_config(C.Structure):
                 ("reserved", C.c_int32)]
 
 
+class gps_icp_config(C.Structure):
+    _fields_ = [("levels", C.c_int32), ("iters", C.c_int32 * 4), ("dist_max", C.c_float),
+                ("angle_max_deg", C.c_float), ("depth_min", C.c_float), ("depth_max", C.c_float),
+                ("eps", C.c_float), ("min_inlier_frac", C.c_float)]
+
+
+class gps_track_result(C.Structure):
+    _fields_ = [("T", gps_pose), ("R64", C.c_double * 9), ("t64", C.c_double * 3), ("energy", C.c_double),
+                ("inliers", C.c_int32), ("valid", C.c_int32), ("steps", C.c_int32), ("degenerate", C.c_int32),
+                ("converged", C.c_int32), ("inlier_frac", C.c_float)]
+
+
 P = C.POINTER
 vp, i64, i32, f32, sz = C.c_void_p, C.c_int64, C.c_int32, C.c_float, C.c_size_t
 
@@ -101,6 +113,9 @@ PROTOTYPES = {
                                             vp, vp, vp, vp, P(gps_add_config), vp, sz, P(i64), P(i64),
                                             gps_stream_t]),
     "gps_remove_workspace_size": (sz, [i64, i32]),
+    "gps_track_workspace_size": (sz, [P(gps_intrinsics), i32]),
+    "gps_track_sync": (gps_status, [P(gps_intrinsics), vp, f32, vp, vp, P(gps_pose), P(gps_pose), P(gps_icp_config),
+                                    vp, sz, P(gps_track_result), gps_stream_t]),
     "gps_remove_gaussians_sync": (gps_status, [P(gps_gaussians), P(gps_adam_state), P(gps_remove_config), vp, sz,
                                                P(i64), gps_stream_t]),
     "gps_debug_export_blocks_sync": (gps_status, [vp, gps_stream_t, vp, vp, i64, P(i64)]),

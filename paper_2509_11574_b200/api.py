@@ -450,3 +450,41 @@ def remove_gaussians(g: Gaussians, state: AdamState, cfg: RemoveConfig | None = 
     for x in (g, state.m, state.v):
         x.set_n(gc.n)
     return removed.value
+
+
+# ---------------------------------------------------------------------------------------------
+# camera tracking
+# ---------------------------------------------------------------------------------------------
+@dataclass
+class IcpConfig:
+    levels: int = 3
+    iters: tuple = (10, 5, 4)      # finest -> coarsest
+    dist_max: float = 0.1
+    angle_max_deg: float = 30.0
+    depth_min: float = 0.1
+    depth_max: float = 10.0
+    eps: float = 1e-6
+    min_inlier_frac: float = 0.1
+
+    def c(self) -> N.gps_icp_config:
+        it = list(self.iters) + [1] * (4 - len(self.iters))
+        return N.gps_icp_config(self.levels, (C.c_int32 * 4)(*it), self.dist_max, self.angle_max_deg,
+                                self.depth_min, self.depth_max, self.eps, self.min_inlier_frac)
+
+
+def track(cam: Camera, depth: torch.Tensor, depth_scale: float, model_vertex: torch.Tensor,
+          model_normal: torch.Tensor, R_model, t_model, R_init, t_init, cfg: IcpConfig | None = None,
+          stream=None) -> dict:
+    """Frame-to-model ICP (gps_track_sync, Eq. 5): returns {"R", "t" (fp64 numpy), "converged",
+    "degenerate", "inlier_frac", "inliers", "steps", "energy"}.  Synchronises."""
+    cfg = cfg or IcpConfig()
+    ws = _ws("track", _L.gps_track_workspace_size(C.byref(cam.c()), cfg.levels))
+    out = N.gps_track_result()
+    N.check("gps_track_sync",
+            _L.gps_track_sync(C.byref(cam.c()), _ptr(depth), float(depth_scale), _ptr(model_vertex),
+                              _ptr(model_normal), C.byref(pose_struct(R_model, t_model)),
+                              C.byref(pose_struct(R_init, t_init)), C.byref(cfg.c()), _ptr(ws), ws.numel(),
+                              C.byref(out), _stream(stream)))
+    return {"R": np.array(out.R64[:], np.float64).reshape(3, 3), "t": np.array(out.t64[:], np.float64),
+            "converged": bool(out.converged), "degenerate": bool(out.degenerate), "inlier_frac": out.inlier_frac,
+            "inliers": out.inliers, "steps": out.steps, "energy": out.energy}

@@ -1,0 +1,386 @@
+// tracking.cu -- frame-to-model ICP camera tracking for sm_100a:
+// gps_track_sync.
+//
+// Paper: GPS-SLAM (arXiv 2509.11574) Sec. 3.2.1 "Camera tracking", Eq. 5:
+// point-to-plane ICP against the previous frame's raycast vertex and normal maps, over a
+// resolution hierarchy of the depth map.  Readings R-ICP-ASSOC (the garbled projection of
+// P:113), R-ICP-PYR, R-ICP-GATE, R-ICP-GN: DESIGN.md §3.
+//
+// Per frame:  k_icp_depth (u16 -> metres, level 0) -> k_icp_down (levels 1..L-1)
+// per level:  k_icp_maps  (vertex + normal maps of the current frame, camera frame; resets the
+//                          level's stop flag)
+// per step:   k_icp_reduce (per pixel: association, gates, residual and Jacobian; the 27 sums of
+//                          J^T J, J^T r, r^2 and the inlier count per CTA, in double)
+//             k_icp_solve  (one CTA: total the CTA sums, Cholesky-solve the 6x6 system, update the
+//                          pose in device memory -- no host round trip between steps)
+// The pose is read back once, at the end.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <string>
+
+#include "common.cuh"
+
+namespace gps {
+namespace {
+
+constexpr int kIcpMaxLevels = 4;
+constexpr int kIcpThreads = 256;
+constexpr int kIcpSums = 29;  // 21 (upper triangle of J^T J) + 6 (J^T r) + r^2 + count
+
+struct DevPose {
+  double R[9], t[3];
+  double energy;
+  int32_t steps, inliers, valid, degenerate;
+  int32_t stop;  // this level is done (converged or degenerate)
+  int32_t pad;
+};
+
+struct Level {
+  int W, H;
+  float fx, fy, cx, cy;
+  const float* depth;  // this level's depth (metres, 0 = invalid)
+  float* V;            // camera-frame vertex map
+  float* N;            // camera-frame normal map
+  int stride;          // model-map subsampling 2^l
+};
+
+__global__ void k_icp_depth(const uint16_t* __restrict__ raw, int n, float inv_scale, float dmin, float dmax, float* d) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float z = (float)raw[i] * inv_scale;
+  d[i] = (z >= dmin && z <= dmax) ? z : 0.f;
+}
+
+// R-ICP-PYR: mean of the valid children of the 2x2 block
+__global__ void k_icp_down(const float* __restrict__ src, int Ws, float* dst, int Wd, int Hd) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x, v = blockIdx.y;
+  if (u >= Wd || v >= Hd) return;
+  const float* r0 = src + (size_t)(2 * v) * Ws + 2 * u;
+  const float* r1 = r0 + Ws;
+  const float c[4] = {r0[0], r0[1], r1[0], r1[1]};
+  float s = 0.f;
+  int k = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    if (c[j] > 0.f) { s += c[j]; ++k; }
+  dst[(size_t)v * Wd + u] = k ? s / (float)k : 0.f;
+}
+
+__device__ __forceinline__ void bp(const Level& L, int u, int v, float z, float* o) {
+  o[0] = ((float)u - L.cx) / L.fx * z;
+  o[1] = ((float)v - L.cy) / L.fy * z;
+  o[2] = z;
+}
+
+// vertex and normal maps of one level (R-NORMAL in the camera frame)
+__global__ void k_icp_maps(Level L, DevPose* pose) {
+  const int u = blockIdx.x * 16 + (threadIdx.x & 15), v = blockIdx.y * 16 + (threadIdx.x >> 4);
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) pose->stop = 0;
+  if (u >= L.W || v >= L.H) return;
+  const size_t p = (size_t)v * L.W + u;
+  const float z = L.depth[p];
+  float V[3] = {0.f, 0.f, 0.f}, N[3] = {0.f, 0.f, 0.f};
+  if (z > 0.f) bp(L, u, v, z, V);
+  if (z > 0.f && u > 0 && v > 0 && u < L.W - 1 && v < L.H - 1) {
+    const float zl = L.depth[p - 1], zr = L.depth[p + 1], zu = L.depth[p - L.W], zd = L.depth[p + L.W];
+    if (zl > 0.f && zr > 0.f && zu > 0.f && zd > 0.f) {
+      float a[3], b[3], c[3], d[3];
+      bp(L, u + 1, v, zr, a); bp(L, u - 1, v, zl, b); bp(L, u, v + 1, zd, c); bp(L, u, v - 1, zu, d);
+      const float dx0 = a[0] - b[0], dx1 = a[1] - b[1], dx2 = a[2] - b[2];
+      const float dy0 = c[0] - d[0], dy1 = c[1] - d[1], dy2 = c[2] - d[2];
+      float n0 = dx1 * dy2 - dx2 * dy1, n1 = dx2 * dy0 - dx0 * dy2, n2 = dx0 * dy1 - dx1 * dy0;
+      const float nn = sqrtf(n0 * n0 + n1 * n1 + n2 * n2);
+      if (nn > 0.f) {
+        n0 /= nn; n1 /= nn; n2 /= nn;
+        if (n0 * V[0] + n1 * V[1] + n2 * V[2] > 0.f) { n0 = -n0; n1 = -n1; n2 = -n2; }
+        N[0] = n0; N[1] = n1; N[2] = n2;
+      }
+    }
+  }
+  L.V[3 * p] = V[0]; L.V[3 * p + 1] = V[1]; L.V[3 * p + 2] = V[2];
+  L.N[3 * p] = N[0]; L.N[3 * p + 1] = N[1]; L.N[3 * p + 2] = N[2];
+}
+
+struct Assoc {
+  const float* mV;  // full-resolution model maps (world)
+  const float* mN;
+  int mW, mH;       // full resolution
+  float Rp[9], tp[3];  // the camera the model maps were raycast from (camera -> world)
+  float dist_max, cos_max;
+};
+
+// R-ICP-ASSOC / R-ICP-GATE / R-ICP-GN for one pixel: J = [m, p x m], r = (p - q) . m
+__global__ void __launch_bounds__(kIcpThreads) k_icp_reduce(Level L, Assoc a, const DevPose* __restrict__ pose,
+                                                            double* partial) {
+  __shared__ double red[kIcpThreads / 32][kIcpSums];
+  if (pose->stop) return;  // uniform: the level is done
+  float R[9], t[3];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) R[k] = (float)pose->R[k];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) t[k] = (float)pose->t[k];
+  const int Lw = a.mW / L.stride, Lh = a.mH / L.stride;  // this level's model-map size
+  float s[kIcpSums];
+#pragma unroll
+  for (int k = 0; k < kIcpSums; ++k) s[k] = 0.f;
+  const int n = L.W * L.H;
+  const int i = blockIdx.x * kIcpThreads + threadIdx.x;
+  int valid = 0;
+  if (i < n) {
+    const float* Nc = L.N + 3 * (size_t)i;
+    if (Nc[0] != 0.f || Nc[1] != 0.f || Nc[2] != 0.f) {
+      valid = 1;
+      const float* Vc = L.V + 3 * (size_t)i;
+      float p[3], nn[3];
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        p[r] = R[3 * r] * Vc[0] + R[3 * r + 1] * Vc[1] + R[3 * r + 2] * Vc[2] + t[r];
+        nn[r] = R[3 * r] * Nc[0] + R[3 * r + 1] * Nc[1] + R[3 * r + 2] * Nc[2];
+      }
+      const float d0 = p[0] - a.tp[0], d1 = p[1] - a.tp[1], d2 = p[2] - a.tp[2];
+      const float x0 = a.Rp[0] * d0 + a.Rp[3] * d1 + a.Rp[6] * d2;
+      const float x1 = a.Rp[1] * d0 + a.Rp[4] * d1 + a.Rp[7] * d2;
+      const float x2 = a.Rp[2] * d0 + a.Rp[5] * d1 + a.Rp[8] * d2;
+      if (x2 > 1e-9f) {
+        const float uf = floorf(L.fx * x0 / x2 + L.cx + 0.5f), vf = floorf(L.fy * x1 / x2 + L.cy + 0.5f);
+        if (uf >= 0.f && uf <= (float)(Lw - 1) && vf >= 0.f && vf <= (float)(Lh - 1)) {
+          const size_t mp = (size_t)((int)vf * L.stride) * a.mW + (size_t)((int)uf * L.stride);
+          const float q0 = a.mV[3 * mp], q1 = a.mV[3 * mp + 1], q2 = a.mV[3 * mp + 2];
+          const float m0 = a.mN[3 * mp], m1 = a.mN[3 * mp + 1], m2 = a.mN[3 * mp + 2];
+          const float e0 = p[0] - q0, e1 = p[1] - q1, e2 = p[2] - q2;
+          if ((m0 != 0.f || m1 != 0.f || m2 != 0.f) && sqrtf(e0 * e0 + e1 * e1 + e2 * e2) < a.dist_max &&
+              nn[0] * m0 + nn[1] * m1 + nn[2] * m2 > a.cos_max) {
+            const float r = e0 * m0 + e1 * m1 + e2 * m2;
+            const float J[6] = {m0, m1, m2, p[1] * m2 - p[2] * m1, p[2] * m0 - p[0] * m2, p[0] * m1 - p[1] * m0};
+            int k = 0;
+#pragma unroll
+            for (int x = 0; x < 6; ++x)
+#pragma unroll
+              for (int y = x; y < 6; ++y) s[k++] = J[x] * J[y];
+#pragma unroll
+            for (int x = 0; x < 6; ++x) s[21 + x] = J[x] * r;
+            s[27] = r * r;
+            s[28] = 1.f;
+          }
+        }
+      }
+    }
+  }
+  // CTA reduction in double (warp shuffles, then the warps' rows)
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < kIcpSums; ++k) {
+    double x = (double)s[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xFFFFFFFFu, x, o);
+    if (lane == 0) red[w][k] = x;
+  }
+  const int cv = __syncthreads_count(valid);
+  if (threadIdx.x < kIcpSums) {
+    double x = 0.0;
+    for (int j = 0; j < kIcpThreads / 32; ++j) x += red[j][threadIdx.x];
+    partial[(size_t)blockIdx.x * 32 + threadIdx.x] = x;
+  }
+  if (threadIdx.x == 0) partial[(size_t)blockIdx.x * 32 + 29] = (double)cv;
+}
+
+// one CTA: total the CTA sums, solve A xi = -b (Cholesky), pose <- exp(xi) pose
+__global__ void __launch_bounds__(256) k_icp_solve(const double* __restrict__ partial, int nblk, DevPose* pose,
+                                                   double eps) {
+  __shared__ double tot[32];
+  if (pose->stop) return;
+  if (threadIdx.x < 30) {
+    double x = 0.0;
+    for (int b = 0; b < nblk; ++b) x += partial[(size_t)b * 32 + threadIdx.x];
+    tot[threadIdx.x] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  double A[6][6], b[6];
+  int k = 0;
+  for (int x = 0; x < 6; ++x)
+    for (int y = x; y < 6; ++y) { A[x][y] = tot[k]; A[y][x] = tot[k]; ++k; }
+  for (int x = 0; x < 6; ++x) b[x] = tot[21 + x];
+  pose->energy = tot[27];
+  pose->inliers = (int32_t)tot[28];
+  pose->valid = (int32_t)tot[29];
+  if (tot[28] < 6.0) {
+    pose->degenerate = 1;
+    pose->stop = 1;
+    return;
+  }
+  // Cholesky A = L L^T; a pivot below 1e-12 of the largest diagonal: rank deficient (R-ICP-GN)
+  double dmax = 0.0;
+  for (int x = 0; x < 6; ++x) dmax = fmax(dmax, A[x][x]);
+  double Lc[6][6] = {};
+  for (int j = 0; j < 6; ++j) {
+    double d = A[j][j];
+    for (int m = 0; m < j; ++m) d -= Lc[j][m] * Lc[j][m];
+    if (!(d > 1e-12 * dmax)) {
+      pose->degenerate = 1;
+      pose->stop = 1;
+      return;
+    }
+    Lc[j][j] = sqrt(d);
+    for (int i = j + 1; i < 6; ++i) {
+      double s = A[i][j];
+      for (int m = 0; m < j; ++m) s -= Lc[i][m] * Lc[j][m];
+      Lc[i][j] = s / Lc[j][j];
+    }
+  }
+  double y[6], xi[6];
+  for (int i = 0; i < 6; ++i) {
+    double s = -b[i];
+    for (int m = 0; m < i; ++m) s -= Lc[i][m] * y[m];
+    y[i] = s / Lc[i][i];
+  }
+  for (int i = 5; i >= 0; --i) {
+    double s = y[i];
+    for (int m = i + 1; m < 6; ++m) s -= Lc[m][i] * xi[m];
+    xi[i] = s / Lc[i][i];
+  }
+  // exp of the twist (v, w): Rodrigues rotation, translation v (left-multiplied increment)
+  const double w0 = xi[3], w1 = xi[4], w2 = xi[5];
+  const double th = sqrt(w0 * w0 + w1 * w1 + w2 * w2);
+  const double K[9] = {0, -w2, w1, w2, 0, -w0, -w1, w0, 0};
+  double K2[9];
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) K2[3 * r + c] = K[3 * r] * K[c] + K[3 * r + 1] * K[3 + c] + K[3 * r + 2] * K[6 + c];
+  const double ca = th < 1e-12 ? 1.0 : sin(th) / th, cb = th < 1e-12 ? 0.0 : (1.0 - cos(th)) / (th * th);
+  double dR[9];
+  for (int e = 0; e < 9; ++e) dR[e] = (e % 4 == 0 ? 1.0 : 0.0) + ca * K[e] + cb * K2[e];
+  double R[9], t[3];
+  for (int r = 0; r < 3; ++r) {
+    for (int c = 0; c < 3; ++c)
+      R[3 * r + c] = dR[3 * r] * pose->R[c] + dR[3 * r + 1] * pose->R[3 + c] + dR[3 * r + 2] * pose->R[6 + c];
+    t[r] = dR[3 * r] * pose->t[0] + dR[3 * r + 1] * pose->t[1] + dR[3 * r + 2] * pose->t[2] + xi[r];
+  }
+  for (int e = 0; e < 9; ++e) pose->R[e] = R[e];
+  for (int e = 0; e < 3; ++e) pose->t[e] = t[e];
+  pose->steps += 1;
+  double nx = 0.0;
+  for (int e = 0; e < 6; ++e) nx += xi[e] * xi[e];
+  if (sqrt(nx) < eps) pose->stop = 1;
+}
+
+inline size_t up256(size_t x) { return (x + 255) / 256 * 256; }
+
+struct TrackLayout {
+  size_t depth[kIcpMaxLevels], V[kIcpMaxLevels], N[kIcpMaxLevels];
+  size_t partial, pose, total;
+};
+TrackLayout track_layout(int W, int H, int levels) {
+  TrackLayout L{};
+  size_t o = 0;
+  auto take = [&](size_t b) { size_t at = o; o = up256(o + b); return at; };
+  for (int l = 0; l < levels; ++l) {
+    const size_t n = (size_t)(W >> l) * (H >> l);
+    L.depth[l] = take(4 * n);
+    L.V[l] = take(12 * n);
+    L.N[l] = take(12 * n);
+  }
+  L.partial = take(8 * 32 * (((size_t)W * H + kIcpThreads - 1) / kIcpThreads));
+  L.pose = take(sizeof(DevPose));
+  L.total = o;
+  return L;
+}
+
+}  // namespace
+}  // namespace gps
+
+using namespace gps;
+
+extern "C" {
+
+size_t gps_track_workspace_size(const gps_intrinsics* K, int32_t levels) {
+  if (!K || K->width <= 0 || K->height <= 0 || levels < 1 || levels > kIcpMaxLevels) return 0;
+  return track_layout(K->width, K->height, levels).total;
+}
+
+gps_status gps_track_sync(const gps_intrinsics* K, const uint16_t* depth, float depth_scale, const float* model_vertex,
+                          const float* model_normal, const gps_pose* T_model, const gps_pose* T_init,
+                          const gps_icp_config* cfg, void* ws, size_t ws_bytes, gps_track_result* out,
+                          gps_stream_t stream) {
+  if (!K || !depth || !model_vertex || !model_normal || !T_model || !T_init || !cfg || !ws || !out)
+    return invalid("gps_track_sync: null argument");
+  if (K->width <= 0 || K->height <= 0 || !(depth_scale > 0)) return invalid("gps_track_sync: bad intrinsics");
+  if (cfg->levels < 1 || cfg->levels > kIcpMaxLevels || !(cfg->dist_max > 0) || !(cfg->depth_max > cfg->depth_min))
+    return invalid("gps_track_sync: bad config");
+  for (int l = 0; l < cfg->levels; ++l)
+    if (cfg->iters[l] < 1 || (K->width >> l) < 3 || (K->height >> l) < 3) return invalid("gps_track_sync: bad level");
+  if ((reinterpret_cast<uintptr_t>(depth) & 1u) != 0) return invalid("gps_track_sync: depth must be 2-byte aligned");
+  const TrackLayout Lw = track_layout(K->width, K->height, cfg->levels);
+  if (ws_bytes < Lw.total) {
+    set_error("gps_track_sync: workspace too small");
+    return GPS_ERR_WORKSPACE_TOO_SMALL;
+  }
+  cudaStream_t s = as_stream(stream);
+  char* w = static_cast<char*>(ws);
+  DevPose hp{};
+  for (int e = 0; e < 9; ++e) hp.R[e] = T_init->R[e];
+  for (int e = 0; e < 3; ++e) hp.t[e] = T_init->t[e];
+  DevPose* dp = reinterpret_cast<DevPose*>(w + Lw.pose);
+  GPS_CHECK_CUDA(cudaMemcpyAsync(dp, &hp, sizeof(hp), cudaMemcpyHostToDevice, s));
+  const int n0 = K->width * K->height;
+  k_icp_depth<<<(n0 + 255) / 256, 256, 0, s>>>(depth, n0, 1.0f / depth_scale, cfg->depth_min, cfg->depth_max,
+                                               reinterpret_cast<float*>(w + Lw.depth[0]));
+  GPS_CHECK_LAUNCH("k_icp_depth");
+  for (int l = 1; l < cfg->levels; ++l) {
+    const int Wd = K->width >> l, Hd = K->height >> l;
+    k_icp_down<<<dim3((Wd + 127) / 128, Hd), 128, 0, s>>>(reinterpret_cast<const float*>(w + Lw.depth[l - 1]),
+                                                          K->width >> (l - 1), reinterpret_cast<float*>(w + Lw.depth[l]),
+                                                          Wd, Hd);
+    GPS_CHECK_LAUNCH("k_icp_down");
+  }
+  Assoc a;
+  a.mV = model_vertex;
+  a.mN = model_normal;
+  a.mW = K->width;
+  a.mH = K->height;
+  for (int e = 0; e < 9; ++e) a.Rp[e] = T_model->R[e];
+  for (int e = 0; e < 3; ++e) a.tp[e] = T_model->t[e];
+  a.dist_max = cfg->dist_max;
+  a.cos_max = (float)std::cos((double)cfg->angle_max_deg * M_PI / 180.0);
+  double* partial = reinterpret_cast<double*>(w + Lw.partial);
+  for (int l = cfg->levels - 1; l >= 0; --l) {  // coarse -> fine
+    Level L;
+    L.W = K->width >> l;
+    L.H = K->height >> l;
+    const double sc = std::ldexp(1.0, -l);
+    L.fx = (float)(K->fx * sc);
+    L.fy = (float)(K->fy * sc);
+    L.cx = (float)((K->cx + 0.5) * sc - 0.5);
+    L.cy = (float)((K->cy + 0.5) * sc - 0.5);
+    L.depth = reinterpret_cast<const float*>(w + Lw.depth[l]);
+    L.V = reinterpret_cast<float*>(w + Lw.V[l]);
+    L.N = reinterpret_cast<float*>(w + Lw.N[l]);
+    L.stride = 1 << l;
+    k_icp_maps<<<dim3((L.W + 15) / 16, (L.H + 15) / 16), 256, 0, s>>>(L, dp);
+    GPS_CHECK_LAUNCH("k_icp_maps");
+    const int nblk = (L.W * L.H + kIcpThreads - 1) / kIcpThreads;
+    for (int it = 0; it < cfg->iters[l]; ++it) {
+      k_icp_reduce<<<nblk, kIcpThreads, 0, s>>>(L, a, dp, partial);
+      GPS_CHECK_LAUNCH("k_icp_reduce");
+      k_icp_solve<<<1, 256, 0, s>>>(partial, nblk, dp, (double)cfg->eps);
+      GPS_CHECK_LAUNCH("k_icp_solve");
+    }
+  }
+  GPS_CHECK_CUDA(cudaMemcpyAsync(&hp, dp, sizeof(hp), cudaMemcpyDeviceToHost, s));
+  GPS_CHECK_CUDA(cudaStreamSynchronize(s));
+  for (int e = 0; e < 9; ++e) out->T.R[e] = (float)hp.R[e];
+  for (int e = 0; e < 3; ++e) out->T.t[e] = (float)hp.t[e];
+  for (int e = 0; e < 9; ++e) out->R64[e] = hp.R[e];
+  for (int e = 0; e < 3; ++e) out->t64[e] = hp.t[e];
+  out->energy = hp.energy;
+  out->inliers = hp.inliers;
+  out->valid = hp.valid;
+  out->steps = hp.steps;
+  out->degenerate = hp.degenerate;
+  out->inlier_frac = hp.valid > 0 ? (float)hp.inliers / (float)hp.valid : 0.f;
+  out->converged = !hp.degenerate && out->inlier_frac >= cfg->min_inlier_frac;
+  return GPS_OK;
+}
+
+}  // extern "C"

@@ -33,7 +33,8 @@ class MappingPipeline:
                  n_global: int = Sch.N_GLOBAL, n_local: int = Sch.N_LOCAL, seed: int = 0,
                  overlap: bool = True, refine_priority: int = -1, manage_gaussians: bool = False,
                  add_cfg: A.AddConfig | None = None, remove_cfg: A.RemoveConfig | None = None,
-                 all_views_per_iteration: bool = False):
+                 all_views_per_iteration: bool = False, track: bool = False,
+                 icp_cfg: A.IcpConfig | None = None):
         self.cam, self.g, self.vol = cam, gaussians, volume
         self.depth_scale = float(depth_scale)
         self.rcfg = render_cfg or A.RenderConfig()
@@ -47,6 +48,12 @@ class MappingPipeline:
         self.all_views = all_views_per_iteration
         self.ras = A.Rasterizer(gaussians.capacity, cam, self.rcfg,
                                 n_views=(n_global + n_local) if all_views_per_iteration else 1)
+        # camera tracking (Eq. 5): every frame after the first is
+        # tracked against the previous frame's raycast maps, and its tracked pose is the one fused
+        self.tracking = track
+        self.icp_cfg = icp_cfg or A.IcpConfig()
+        self.prev_pose = None
+        self.track_log = []
         # Gaussian adding / removal
         self.manage = manage_gaussians
         self.add_cfg = add_cfg or A.AddConfig()
@@ -67,6 +74,10 @@ class MappingPipeline:
         # per view-buffer set: written by the fusion stream at the round frame, read by the
         # refinement stream in that round, rewritten two rounds later (after _set_free)
         mk = lambda *shape: [torch.empty(shape, dtype=torch.float32, device=dev) for _ in range(2)]
+        if track:
+            self.t_vertex = torch.empty((H, W, 3), dtype=torch.float32, device=dev)
+            self.t_normal = torch.empty((H, W, 3), dtype=torch.float32, device=dev)
+            self._model = None  # (V*, N*) of the previous frame
         if manage_gaussians:
             self.r_depth, self.r_color, self.vertex, self.normal = mk(H, W), mk(H, W, 3), mk(H, W, 3), mk(H, W, 3)
             self._add_color, self._add_weight = mk(H, W, 3), mk(H, W)
@@ -106,8 +117,15 @@ class MappingPipeline:
     def process_frame(self, k: int, depth: torch.Tensor, rgba: torch.Tensor, R, t, refine: bool = True):
         depth = self._device(depth)
         rgba = self._device(rgba)
+        if self.tracking and self._model is not None:
+            Rp, tp = self.prev_pose
+            res = A.track(self.cam, depth, self.depth_scale, self._model[0], self._model[1], Rp, tp, Rp, tp,
+                          self.icp_cfg)
+            R, t = res["R"].astype(np.float32), res["t"].astype(np.float32)
+            self.track_log.append(res)
         self.vol.fuse(self.cam, R, t, depth, self.depth_scale, rgba)
         self.last_frame = k
+        self.last_pose = (np.asarray(R, np.float32), np.asarray(t, np.float32))
         is_kf = self.kf.offer(k, R, t)
         self.interval.append(k)
         self.frames[k] = (rgba, np.asarray(R, np.float32), np.asarray(t, np.float32))
@@ -126,9 +144,17 @@ class MappingPipeline:
                 # the frame just fused is a view: its per-frame raycast is the view's
                 j = views_ids.index(k)
                 self.depth, self.color = self.view_depth[s][j], self.view_color[s][j]
-        self.vol.raycast(self.cam, R, t, self.depth, self.color, vertex_out=self.vertex[s] if want_v else None)
+        vert = self.vertex[s] if want_v else (self.t_vertex if self.tracking else None)
+        self.vol.raycast(self.cam, R, t, self.depth, self.color, vertex_out=vert)
         if want_v:
             A.vertex_normals(self.cam, R, t, self.depth, self.vertex[s], out=self.normal[s])
+            if self.tracking:
+                self._model = (self.vertex[s], self.normal[s])
+        elif self.tracking:
+            A.vertex_normals(self.cam, R, t, self.depth, self.t_vertex, out=self.t_normal)
+            self._model = (self.t_vertex, self.t_normal)
+        if self.tracking:
+            self.prev_pose = (np.asarray(R, np.float32), np.asarray(t, np.float32))
         if round_now:
             self._refine_round(views_ids, add_frame=(k, rgba, R, t, s) if self.manage else None)
         if len(self.interval) >= self.delta_k or Sch.is_round_frame(k, self.delta_k):
@@ -167,7 +193,9 @@ class MappingPipeline:
                 "frames": dict(self.frames), "interval": list(self.interval), "last_frame": self.last_frame,
                 "rng": copy.deepcopy(self.rng.bit_generator.state), "rounds": self.rounds,
                 "iterations_run": self.iterations_run, "removal_pending": self._removal_pending,
-                "added_total": self.added_total, "removed_total": self.removed_total}
+                "added_total": self.added_total, "removed_total": self.removed_total,
+                "track": ((self._model[0].clone(), self._model[1].clone(), self.prev_pose)
+                          if self.tracking and self._model is not None else None)}
 
     def restore(self, s):
         self.join()
@@ -185,6 +213,10 @@ class MappingPipeline:
         self.rounds, self.iterations_run = s["rounds"], s["iterations_run"]
         self._removal_pending = s["removal_pending"]
         self.added_total, self.removed_total = s["added_total"], s["removed_total"]
+        if self.tracking and s["track"] is not None:
+            self.t_vertex.copy_(s["track"][0])
+            self.t_normal.copy_(s["track"][1])
+            self._model, self.prev_pose = (self.t_vertex, self.t_normal), s["track"][2]
         if True:  # the refinement stream must see the restored state
             ev = torch.cuda.Event()
             ev.record(torch.cuda.current_stream())

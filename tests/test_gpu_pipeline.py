@@ -108,3 +108,31 @@ def test_pipeline_with_gaussian_adding_and_removal():
     assert a0 > 100 and r0 >= 0                       # the rounds added (removal: its own test)
     assert n0 == 5000 + a0 - r0 and n1 == 5000 + a1 - r1
     assert abs(a1 - a0) <= 0.01 * a0 and abs(n1 - n0) <= 0.01 * n0
+
+
+def test_pipeline_with_tracking_follows_the_trajectory():
+    """NEXT-3 inside the mapping step: every frame after the first is ICP-tracked against the
+    previous frame's raycast (V*, N*) and fused at its tracked pose; on a noise-free cfg2
+    sequence the tracked trajectory stays within 5 mm of the ground truth over 20 frames."""
+    import paper_2509_11574_b200 as G
+    from paper_2509_11574_b200.pipeline import MappingPipeline
+
+    cfg = S.get_config("cfg2", noise="none", dropout=0.0)
+    n_frames = 21
+    scene = S.make_scene(cfg)
+    dc = S.pixel_rays(cfg, "cuda")
+    poses = S.trajectory(cfg, n_frames)
+    cam = G.Camera(cfg.fx, cfg.fy, cfg.cx, cfg.cy, cfg.width, cfg.height)
+    vol = G.Volume(voxel_size=cfg.voxel_size, max_blocks=cfg.max_blocks, hash_slots=cfg.hash_slots)
+    g = G.Gaussians.from_dict(S.make_gaussians(cfg, n=5000))
+    pipe = MappingPipeline(cam, g, vol, cfg.depth_scale, seed=1, track=True)
+    err = []
+    for k in range(n_frames):
+        fr = S.render_frame(cfg, scene, *poses[k], k=k, device="cuda", dc=dc)
+        pipe.process_frame(k, fr.depth.contiguous(), fr.rgba.contiguous(), fr.R, fr.t)
+        err.append(np.linalg.norm(pipe.last_pose[1].astype(np.float64) - np.asarray(poses[k][1], np.float64)))
+    pipe.join()
+    torch.cuda.synchronize()
+    assert len(pipe.track_log) == n_frames - 1
+    assert all(r["converged"] for r in pipe.track_log)
+    assert err[0] == 0.0 and max(err) < 5e-3
