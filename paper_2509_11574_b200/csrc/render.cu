@@ -326,7 +326,7 @@ __device__ __forceinline__ void preprocess_one(const RenderArgs& a, const gps_ga
 // Per Gaussian: the projection and record (preprocess_one), then, warp-cooperatively, the tile
 // counts of footprints spanning more than 4 tiles (one lane per tile instead of a serial loop)
 // and one aggregated n_visible update per warp.
-__global__ void __launch_bounds__(256) k_preprocess(RenderArgs a, gps_gaussians g, SplatPtrs w) {
+__global__ void __launch_bounds__(256, 3) k_preprocess(RenderArgs a, gps_gaussians g, SplatPtrs w) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   int tr[4] = {1, 0, 0, 0};  // tile rect tx0, tx1, ty0, ty1 of a listed Gaussian (tx0 > tx1: none)
   if (i < a.n) preprocess_one(a, g, w, i, tr);
