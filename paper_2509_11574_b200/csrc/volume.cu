@@ -87,6 +87,41 @@ __device__ void global_insert(const VolumeView& v, uint64_t key, uint32_t frame,
   *(volatile uint32_t*)d_flag = 1u;
 }
 
+// find-or-insert of a block key in the global table; returns its slot (-1: table full or the
+// block budget exceeded, overflow latched).  Does not mark the block visible.
+__device__ int32_t global_find_or_insert(const VolumeView& v, uint64_t key, uint32_t* d_flag) {
+  int x, y, z;
+  unpack_block(key, x, y, z);
+  uint32_t h = hash_block(x, y, z) & v.slot_mask;
+  for (uint32_t probe = 0; probe <= v.slot_mask; ++probe) {
+    const uint64_t k = *(volatile uint64_t*)&v.keys[h];
+    if (k == key) return (int32_t)h;
+    if (k == kEmptyKey) {
+      const unsigned long long old = atomicCAS((unsigned long long*)&v.keys[h], (unsigned long long)kEmptyKey,
+                                               (unsigned long long)key);
+      if (old == kEmptyKey) {
+        const uint32_t b = atomicAdd(&v.ctr->n_blocks, 1u);
+        if (b < v.max_blocks) {
+          v.bkeys[b] = key;
+          v.vals[h] = (int32_t)b;  // the pool block was initialised empty at create/reset
+          const unsigned ix = (unsigned)(x - v.gox), iy = (unsigned)(y - v.goy), iz = (unsigned)(z - v.goz);
+          if (v.grid && ix < (unsigned)v.gdx && iy < (unsigned)v.gdy && iz < (unsigned)v.gdz)
+            v.grid[((size_t)iz * v.gdy + iy) * v.gdx + ix] = (int32_t)b;
+        } else {
+          v.ctr->overflow = 1u;
+          *(volatile uint32_t*)d_flag = 1u;
+        }
+        return (int32_t)h;
+      }
+      if (old == key) return (int32_t)h;
+    }
+    h = (h + 1) & v.slot_mask;
+  }
+  v.ctr->overflow = 1u;  // table full
+  *(volatile uint32_t*)d_flag = 1u;
+  return -1;
+}
+
 __device__ __forceinline__ void set_insert(unsigned long long* set, uint64_t key, const VolumeView& v,
                                            uint32_t frame, uint32_t* d_flag) {
   int x, y, z;
@@ -173,9 +208,31 @@ __global__ void __launch_bounds__(256) k_alloc(VolumeView v, FuseParams p,
       if (x0 + k < p.W && d4[k] != 0) pixel_blocks(p, x0 + k, y, d4[k], set, v, frame, d_flag);
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < kSmemSet; i += blockDim.x) {
-    const uint64_t key = set[i];
-    if (key != kEmptyKey) global_insert(v, key, frame, d_flag);
+  // global phase: find or insert each of the CTA's blocks, then mark the newly visible ones with
+  // ONE append per warp (a single counter for all 65k visible blocks was the kernel's hottest
+  // serialisation point)
+  const int lane = threadIdx.x & 31;
+  for (int i0 = 0; i0 < kSmemSet; i0 += blockDim.x) {
+    const uint64_t key = set[i0 + threadIdx.x];
+    int32_t slot = -1;
+    if (key != kEmptyKey) slot = global_find_or_insert(v, key, d_flag);
+    bool app = false;
+    if (slot >= 0 && v.stamp[slot] != frame) app = atomicExch(&v.stamp[slot], frame) != frame;
+    const unsigned bal = __ballot_sync(0xFFFFFFFFu, app);
+    if (bal) {
+      uint32_t base = 0;
+      if (lane == 0) base = atomicAdd(&v.ctr->n_vis, (uint32_t)__popc(bal));
+      base = __shfl_sync(0xFFFFFFFFu, base, 0);
+      if (app) {
+        const uint32_t idx = base + __popc(bal & ((1u << lane) - 1u));
+        if (idx < v.max_blocks) {
+          v.vis[idx] = slot;
+        } else {
+          v.ctr->overflow = 1u;
+          *(volatile uint32_t*)d_flag = 1u;
+        }
+      }
+    }
   }
 }
 
