@@ -664,6 +664,13 @@ __global__ void __launch_bounds__(TILE* TILE) k_sort_blend(RenderArgs a, const f
   const bool inside = x < a.cam.W && y < a.cam.H;
   const size_t pix = inside ? (size_t)y * a.cam.W + x : 0;
   const float D = inside ? io.sdf_depth[pix] : 0.f;
+  // the composite's inputs, loaded now so their latency hides behind the sort and the blend
+  float ct0 = 0.f, ct1 = 0.f, ct2 = 0.f;
+  uint32_t tgt8 = 0u;
+  if (inside) {
+    ct0 = io.sdf_color[3 * pix]; ct1 = io.sdf_color[3 * pix + 1]; ct2 = io.sdf_color[3 * pix + 2];
+    if (io.target) tgt8 = io.target[pix];
+  }
   const float lim = D > 0.f ? D + a.eps : INFINITY;  // R-MISS: no depth test on an SDF miss
   const float fx = (float)x, fy = (float)y;
   // optional pre-cull: entries at or behind every pixel's limit cannot contribute in this tile
@@ -762,14 +769,13 @@ __global__ void __launch_bounds__(TILE* TILE) k_sort_blend(RenderArgs a, const f
   uint32_t inmask = 0;
   if (inside) {
     const float inv = 1.0f / (1.0f + W);
-    const float ct0 = io.sdf_color[3 * pix], ct1 = io.sdf_color[3 * pix + 1], ct2 = io.sdf_color[3 * pix + 2];
     const float o0 = (ct0 + C0) * inv, o1 = (ct1 + C1) * inv, o2 = (ct2 + C2) * inv;
     io.out_color[3 * pix] = W > 0.f ? o0 : ct0;
     io.out_color[3 * pix + 1] = W > 0.f ? o1 : ct1;
     io.out_color[3 * pix + 2] = W > 0.f ? o2 : ct2;
     io.out_weight[pix] = W;
     if (io.target && (D > 0.f || W > 0.f)) {
-      const uint32_t c = io.target[pix];
+      const uint32_t c = tgt8;
       const float k0 = (float)(c & 0xFFu) * (1.f / 255.f), k1 = (float)((c >> 8) & 0xFFu) * (1.f / 255.f),
                   k2 = (float)((c >> 16) & 0xFFu) * (1.f / 255.f);
       const float r0 = W > 0.f ? o0 : ct0, r1 = W > 0.f ? o1 : ct1, r2 = W > 0.f ? o2 : ct2;
