@@ -830,6 +830,259 @@ __global__ void __launch_bounds__(TILE* TILE) k_sort_blend(RenderArgs a, const f
   }
 }
 
+// --------------------------------------------------------------------------------------------
+// k_sort_blend16x2: the same blend for 16x16 tiles with TWO pixels per thread (128 threads).
+// Warp w covers rows 4w..4w+3 of the tile; lane l holds pixels (l & 15, 4w + (l >> 4)) and the
+// one two rows below.  Against k_sort_blend<16> each (warp, entry) pair now serves 64 pixels:
+// an entry of the median 7-row footprint meets ~2.75 warp strips instead of ~4.5, and the
+// per-entry work of the walk (record loads, compaction) is shared by two pixels.  The sort keeps
+// only 256 + 2 keys in shared memory (longer lists -- none above 252 at cfg4 -- use the global
+// bitonic fallback), so more CTAs stay resident.  Every pixel sees the same entries in the same
+// order as in k_sort_blend, so C* and W_G are bitwise those of the one-pixel-per-thread kernel.
+// --------------------------------------------------------------------------------------------
+template <bool SORTED>
+__global__ void __launch_bounds__(128) k_sort_blend16x2(RenderArgs a, const float4* __restrict__ rec,
+                                                        const uint32_t* __restrict__ offsets, uint32_t* vals,
+                                                        uint64_t* gkeys, uint32_t* tile_end, float* loss_part,
+                                                        WsHeader* hdr, BlendIO io, int precull) {
+  constexpr int NT = 128, NB = 256;  // threads, staged entries per batch (2 per thread)
+  __shared__ __align__(16) uint64_t skeys[NB + 2];
+  __shared__ float4 s0[NB], s1[NB], s2[NB];  // s0 = (px, py, a, 2b); s1 = (c, ln sigma, d, q_max)
+  __shared__ float red[NT / 32 + 1];
+  __shared__ uint32_t redi[NT / 32 + 1];
+  const int t = blockIdx.x;
+  const int tx = t % a.tiles_x, ty = t / a.tiles_x;
+  const uint32_t start = min(offsets[t], a.cap);
+  const uint32_t end = min(offsets[t + 1], a.cap);
+  const int n = (int)(end - start);
+  const bool small = n <= NB;  // keys live in shared memory
+  // ---- per-tile sort by (depth bits, index) ----
+  if (!SORTED) {
+  } else if (small) {
+    // rank sort, two keys per thread
+    uint64_t key[2] = {~0ull, ~0ull};
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int e = threadIdx.x + h * NT;
+      if (e < n) {
+        const uint32_t idx = vals[start + e];
+        key[h] = ((uint64_t)__float_as_uint(rec[4 * idx + 1].z) << 32) | idx;
+        skeys[e] = key[h];
+      }
+    }
+    if (threadIdx.x == 0) skeys[n] = ~0ull;  // pad slot of the paired loads below
+    __syncthreads();
+    int rank[2] = {0, 0};
+    const ulonglong2* k2 = reinterpret_cast<const ulonglong2*>(skeys);
+    for (int j = 0; j < (n + 1) >> 1; ++j) {
+      const ulonglong2 kk = k2[j];
+      rank[0] += (kk.x < key[0]) + (kk.y < key[0]);
+      rank[1] += (kk.x < key[1]) + (kk.y < key[1]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int e = threadIdx.x + h * NT;
+      if (e < n) {
+        skeys[rank[h]] = key[h];
+        vals[start + rank[h]] = (uint32_t)key[h];
+      }
+    }
+  } else {
+    uint64_t* gk = gkeys + start;
+    for (int e = threadIdx.x; e < n; e += NT) {
+      const uint32_t idx = vals[start + e];
+      gk[e] = ((uint64_t)__float_as_uint(rec[4 * idx + 1].z) << 32) | idx;
+    }
+    __syncthreads();
+    bitonic_sort(gk, n);
+    for (int e = threadIdx.x; e < n; e += NT) vals[start + e] = (uint32_t)gk[e];
+  }
+  __syncthreads();
+  // ---- pixel state (two pixels) ----
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int lx = lane & 15, ly0 = 4 * w + (lane >> 4);
+  const int x = tx * 16 + lx;
+  float D[2], lim[2], ct[2][3];
+  uint32_t tgt8[2];
+  bool inside[2];
+  size_t pix[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int y = ty * 16 + ly0 + 2 * h;
+    inside[h] = x < a.cam.W && y < a.cam.H;
+    pix[h] = inside[h] ? (size_t)y * a.cam.W + x : 0;
+    D[h] = inside[h] ? io.sdf_depth[pix[h]] : 0.f;
+    ct[h][0] = ct[h][1] = ct[h][2] = 0.f;
+    tgt8[h] = 0u;
+    if (inside[h]) {
+      ct[h][0] = io.sdf_color[3 * pix[h]]; ct[h][1] = io.sdf_color[3 * pix[h] + 1];
+      ct[h][2] = io.sdf_color[3 * pix[h] + 2];
+      if (io.target) tgt8[h] = io.target[pix[h]];
+    }
+    lim[h] = D[h] > 0.f ? D[h] + a.eps : INFINITY;  // R-MISS: no depth test on an SDF miss
+  }
+  const float fx = (float)x, fy0 = (float)(ty * 16 + ly0), fy1 = fy0 + 2.0f;
+  float wl = fmaxf(inside[0] ? lim[0] : -INFINITY, inside[1] ? lim[1] : -INFINITY);
+  int n_eff = n;
+  if (SORTED && precull) {
+    float m = wl;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+    if (lane == 0) red[w] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) red[NT / 32] = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
+    __syncthreads();
+    const float tmax = red[NT / 32];
+    if (tmax < INFINITY) {  // binary search: first entry with d >= tmax
+      int lo = 0, hi = n;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        const float d = small ? __uint_as_float((uint32_t)(skeys[mid] >> 32)) : rec[4 * vals[start + mid] + 1].z;
+        if (d >= tmax) hi = mid; else lo = mid + 1;
+      }
+      n_eff = lo;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) tile_end[t] = start + n_eff;
+  // ---- blend (per-warp compaction over the warp's 4-row strip, as k_sort_blend) ----
+  const int wy0 = ty * 16 + 4 * w, wy1 = wy0 + 3;
+  float wlim = wl;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) wlim = fmaxf(wlim, __shfl_xor_sync(0xFFFFFFFFu, wlim, o));
+  float W0 = 0.f, A0 = 0.f, B0 = 0.f, G0 = 0.f, W1 = 0.f, A1 = 0.f, B1 = 0.f, G1 = 0.f;
+  bool wdone = !(wlim > -INFINITY);  // warp-uniform
+  for (int base = 0; base < n_eff; base += NB) {
+    const int cnt = min(NB, n_eff - base);
+    __syncthreads();
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int e = threadIdx.x + h * NT;
+      if (e < cnt) {
+        const uint32_t idx = vals[start + base + e];
+        const float4 r0 = rec[4 * idx], r1 = rec[4 * idx + 1];
+        s0[e] = make_float4(r0.x, r0.y, r0.z, pmul(2.0f, r0.w));
+        s1[e] = make_float4(r1.x, r1.y, r1.z, pair_qmax(a.ln_inv_amin, r1.y));
+        s2[e] = rec[4 * idx + 2];
+      }
+    }
+    __syncthreads();
+    for (int kb = 0; kb < cnt && !wdone; kb += 32) {
+      const int k = kb + lane;
+      bool live = false, stop = false;
+      if (k < cnt) {
+        const bool behind = !(s1[k].z < wlim);
+        stop = SORTED && behind;
+        const uint32_t ry = __float_as_uint(s2[k].w);
+        live = !behind && (int)(ry >> 16) >= wy0 && (int)(ry & 0xFFFFu) <= wy1;
+        if (live) {
+          const float4 e0 = s0[k];
+          live = ellipse_meets_strip(e0.x, e0.y, e0.z, e0.w, s1[k].x, s1[k].w, tx * 16, tx * 16 + 15, wy0, wy1);
+        }
+      }
+      uint32_t lm = __ballot_sync(0xFFFFFFFFu, live);
+      const uint32_t sm = __ballot_sync(0xFFFFFFFFu, stop);
+      if (sm) {
+        lm &= (1u << (__ffs(sm) - 1)) - 1u;  // survivors before the first stop
+        wdone = true;
+      }
+      while (lm) {
+        const int kk = kb + __ffs(lm) - 1;
+        lm &= lm - 1u;
+        const float4 r1 = s1[kk];
+        const bool i0 = r1.z < lim[0], i1 = r1.z < lim[1];  // Eq. 1's indicator per pixel
+        if (!(i0 | i1)) continue;
+        const float4 r0 = s0[kk];
+        const float q0 = pair_q(r0.x, r0.y, r0.z, r0.w, r1.x, fx, fy0);
+        const float q1 = pair_q(r0.x, r0.y, r0.z, r0.w, r1.x, fx, fy1);
+        const bool p0 = i0 && q0 <= r1.w, p1 = i1 && q1 <= r1.w;
+        if (!(p0 | p1)) continue;
+        const float4 r2 = s2[kk];
+        if (p0) {
+          const float al = __expf(fmaf(-0.5f, q0, r1.y));  // sigma exp(-q/2), Eq. 3
+          W0 += al;
+          A0 = fmaf(al, r2.x, A0); B0 = fmaf(al, r2.y, B0); G0 = fmaf(al, r2.z, G0);
+        }
+        if (p1) {
+          const float al = __expf(fmaf(-0.5f, q1, r1.y));
+          W1 += al;
+          A1 = fmaf(al, r2.x, A1); B1 = fmaf(al, r2.y, B1); G1 = fmaf(al, r2.z, G1);
+        }
+      }
+    }
+    if (__syncthreads_count(!wdone) == 0) break;
+  }
+  // ---- Eq. 4 composite with W_t = 1, fused L1 ----
+  float l1 = 0.f;
+  uint32_t inmask = 0;
+  const float Ws[2] = {W0, W1}, Cs[2][3] = {{A0, B0, G0}, {A1, B1, G1}};
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    if (!inside[h]) continue;
+    const float W = Ws[h];
+    const float inv = 1.0f / (1.0f + W);
+    const float o0 = (ct[h][0] + Cs[h][0]) * inv, o1 = (ct[h][1] + Cs[h][1]) * inv, o2 = (ct[h][2] + Cs[h][2]) * inv;
+    const float r0 = W > 0.f ? o0 : ct[h][0], r1 = W > 0.f ? o1 : ct[h][1], r2 = W > 0.f ? o2 : ct[h][2];
+    io.out_color[3 * pix[h]] = r0;
+    io.out_color[3 * pix[h] + 1] = r1;
+    io.out_color[3 * pix[h] + 2] = r2;
+    io.out_weight[pix[h]] = W;
+    if (io.target && (D[h] > 0.f || W > 0.f)) {
+      const uint32_t c = tgt8[h];
+      const float k0 = (float)(c & 0xFFu) * (1.f / 255.f), k1 = (float)((c >> 8) & 0xFFu) * (1.f / 255.f),
+                  k2 = (float)((c >> 16) & 0xFFu) * (1.f / 255.f);
+      l1 += fabsf(r0 - k0) + fabsf(r1 - k1) + fabsf(r2 - k2);
+      inmask += 1;
+    }
+  }
+  if (!io.target) return;
+  // deterministic CTA reduction (fixed shuffle tree + fixed smem order)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    l1 += __shfl_xor_sync(0xFFFFFFFFu, l1, o);
+    inmask += __shfl_xor_sync(0xFFFFFFFFu, inmask, o);
+  }
+  __syncthreads();
+  if (lane == 0) {
+    red[w] = l1;
+    redi[w] = inmask;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float sum = 0.f;
+    uint32_t m = 0;
+    for (int k = 0; k < NT / 32; ++k) {
+      sum += red[k];
+      m += redi[k];
+    }
+    loss_part[t] = sum;
+    if (m) atomicAdd(&hdr->mask_count, m);
+    __threadfence();
+    const uint32_t ticket = atomicAdd(&hdr->ticket, 1u);
+    redi[0] = ticket == (uint32_t)(gridDim.x - 1) ? 1u : 0u;
+  }
+  __syncthreads();
+  if (redi[0] == 0u) return;
+  // last CTA: sum the tile partials in tile order (fixed tree) -> mean L1 (R-L1)
+  __threadfence();
+  float sum = 0.f;
+  for (int k = threadIdx.x; k < (int)gridDim.x; k += NT) sum += *(volatile float*)&loss_part[k];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
+  __syncthreads();
+  if (lane == 0) red[w] = sum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float tot = 0.f;
+    for (int k = 0; k < NT / 32; ++k) tot += red[k];
+    const uint32_t m = *(volatile uint32_t*)&hdr->mask_count;
+    const float lv = m ? tot / (3.0f * (float)m) : 0.0f;
+    if (io.loss_out) *io.loss_out = io.accumulate_loss ? *io.loss_out + lv : lv;
+    hdr->ticket = 0u;
+  }
+}
+
 // ============================================================================================
 // k_backward: exact gradient of the L1 loss w.r.t. each listed Gaussian's 2D quantities
 // (p_hat, conic, sigma, colour), R-GRAD.  Order of entries is irrelevant (no transmittance);
@@ -1608,11 +1861,16 @@ gps_status forward_view(const gps_gaussians* g, const View1& v, const gps_render
   float* lp = reinterpret_cast<float*>(ws + L.loss_part);
   {
   GPS_PROF(K_SORT_BLEND, s);
+  static const bool one_px = getenv("GPS_BLEND_1PX") != nullptr;  // the one-pixel-per-thread kernel
   if (c->sort_free) {
-    if (a.tile == 16)
+    if (a.tile == 16 && !one_px)
+      k_sort_blend16x2<false><<<n_tiles, 128, 0, s>>>(a, sp.rec, offsets, vals, gk, tend, lp, hdr, io, 0);
+    else if (a.tile == 16)
       k_sort_blend<16, false><<<n_tiles, 256, 0, s>>>(a, sp.rec, offsets, vals, gk, tend, lp, hdr, io, 0);
     else
       k_sort_blend<8, false><<<n_tiles, 64, 0, s>>>(a, sp.rec, offsets, vals, gk, tend, lp, hdr, io, 0);
+  } else if (a.tile == 16 && !one_px) {
+    k_sort_blend16x2<true><<<n_tiles, 128, 0, s>>>(a, sp.rec, offsets, vals, gk, tend, lp, hdr, io, c->tile_depth_precull);
   } else if (a.tile == 16) {
     k_sort_blend<16, true><<<n_tiles, 256, 0, s>>>(a, sp.rec, offsets, vals, gk, tend, lp, hdr, io, c->tile_depth_precull);
   } else {
