@@ -733,18 +733,20 @@ __device__ __forceinline__ bool trilinear_color(const VolumeView& v, BlockCache&
 // kDebug: 0 = production; 1 = per-pixel march statistics in vertex_out; 2 = mark every tsdf voxel
 // the march reads in `footprint` (the raycast roofline's unique-voxel count)
 template <int kDebug, int kMinCtas = 6>
-__global__ void __launch_bounds__(256, kMinCtas) k_raycast(VolumeView v, RayParams p, float* __restrict__ depth_out,
+__global__ void __launch_bounds__(128, 2 * kMinCtas) k_raycast(VolumeView v, RayParams p, float* __restrict__ depth_out,
                                                  float* __restrict__ color_out,
                                                  float* __restrict__ vertex_out,
                                                  const uint32_t* __restrict__ tmin,
                                                  const uint32_t* __restrict__ tmax,
                                                  uint32_t* footprint = nullptr) {
+  // CTA = 16x8 pixels (128 threads: a small register footprint that co-schedules with the
+  // refinement stream's kernels); two CTAs per 16x16 range tile
   const int u = blockIdx.x * 16 + (threadIdx.x & 15);
-  const int vv = blockIdx.y * 16 + (threadIdx.x >> 4);
+  const int vv = blockIdx.y * 8 + (threadIdx.x >> 4);
   if (u >= p.W || vv >= p.H) return;
   int jstart = 0, jend = p.J;
   if (tmin) {  // the tile's range image entry (CTA == 16x16 range tile)
-    const int tile = blockIdx.y * gridDim.x + blockIdx.x;
+    const int tile = (blockIdx.y >> 1) * gridDim.x + blockIdx.x;
     const uint32_t a0 = tmin[tile], a1 = tmax[tile];
     if (a0 == 0xFFFFFFFFu) {
       jend = -1;  // no allocated block can meet any ray of this tile: miss
@@ -1225,7 +1227,8 @@ static gps_status raycast_impl(const gps_volume* vol, const gps_intrinsics* K, c
     const double ey = std::max(std::fabs(0.0 - K->cy), std::fabs((double)(K->height - 1) - K->cy)) / K->fy;
     p.zc = (float)(0.99 * (double)v->cfg.depth_min / std::sqrt(1.0 + ex * ex + ey * ey));
   }
-  dim3 g((p.W + 15) / 16, (p.H + 15) / 16);
+  dim3 g((p.W + 15) / 16, (p.H + 15) / 16);  // range tiles (16x16); raycast CTAs are 16x8
+  const dim3 gr(g.x, 2 * g.y);
   cudaStream_t s = as_stream(stream);
   const int ntiles = (int)(g.x * g.y);
   uint32_t* tmin = nullptr;
@@ -1245,19 +1248,12 @@ static gps_status raycast_impl(const gps_volume* vol, const gps_intrinsics* K, c
     GPS_PROF(K_RAYCAST, s);
     static const bool dbg = getenv("GPS_RAYCAST_DEBUG") != nullptr;
     if (footprint)
-      k_raycast<2><<<g, 256, 0, s>>>(v->view, p, depth_out, color_out, nullptr, tmin, tmax, footprint);
+      k_raycast<2><<<gr, 128, 0, s>>>(v->view, p, depth_out, color_out, nullptr, tmin, tmax, footprint);
     else if (dbg && vertex_out)
-      k_raycast<1><<<g, 256, 0, s>>>(v->view, p, depth_out, color_out, vertex_out, tmin, tmax);
+      k_raycast<1><<<gr, 128, 0, s>>>(v->view, p, depth_out, color_out, vertex_out, tmin, tmax);
     else {
-      // occupancy variants for tuning (GPS_RAYCAST_CTAS = resident CTAs per SM the register
-      // budget targets; default 4 = 64 registers, no spills)
-      static const int ctas = getenv("GPS_RAYCAST_CTAS") ? atoi(getenv("GPS_RAYCAST_CTAS")) : 4;
-      if (ctas == 8)
-        k_raycast<0, 8><<<g, 256, 0, s>>>(v->view, p, depth_out, color_out, vertex_out, tmin, tmax);
-      else if (ctas == 4)
-        k_raycast<0, 4><<<g, 256, 0, s>>>(v->view, p, depth_out, color_out, vertex_out, tmin, tmax);
-      else
-        k_raycast<0, 6><<<g, 256, 0, s>>>(v->view, p, depth_out, color_out, vertex_out, tmin, tmax);
+      // 8 resident 128-thread CTAs per SM (64 registers, no spills)
+      k_raycast<0, 4><<<gr, 128, 0, s>>>(v->view, p, depth_out, color_out, vertex_out, tmin, tmax);
     }
   }
   GPS_CHECK_LAUNCH("k_raycast");
