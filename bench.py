@@ -342,6 +342,24 @@ def run_ours(args):
             t = prof[kk]["ms"] / prof[kk]["launches"] / 1000.0
             shares[kk].update({"alg_bytes_per_launch": int(b), "gbs": round(b / t / 1e9, 1),
                                "hbm_frac": round(b / t / 1e9 / peak, 4)})
+    # rasteriser work: evaluated / accepted pixel-entry pairs of the last
+    # view, counted by the instrumented forward, and the blend's ALU roofline from the survey's
+    # instruction model (forward ~ 8 E + 20 A thread-instructions) against the issue capacity
+    # 148 SMs x 4 schedulers x 32 lanes x the sampled SM clock
+    raster = None
+    if args.tile == 16 and "k_sort_blend" in shares and prof["k_sort_blend"]["launches"]:
+        v = pipe.last_view
+        E, A_ = pipe.ras.pair_counts(g, cam, v.R, v.t, v.sdf_depth, v.sdf_color)
+        f_sm = 1e6 * (clk.get("sm_mhz") or 1965.0)
+        t_blend = prof["k_sort_blend"]["ms"] / prof["k_sort_blend"]["launches"] / 1000.0
+        instr = 8.0 * E + 20.0 * A_
+        peak_ti = 148 * 4 * 32 * f_sm
+        raster = {"evaluated_pairs": int(E), "accepted_pairs": int(A_), "pairs_K": rstats.get("pairs"),
+                  "blend_alu": {"bound": "alu", "model_thread_instr": int(instr),
+                                "achieved": round(instr / t_blend / 1e12, 2), "peak": round(peak_ti / 1e12, 2),
+                                "unit": "T thread-instr/s", "frac": round(instr / t_blend / peak_ti, 4),
+                                "note": "useful work of the SURVEY §8(d) model over the issue capacity; "
+                                        "ncu's issue-active and lanes/instruction are in profiles/"}}
     launches = int(sum(v["launches"] for kk, v in prof.items() if kk != "memset"))
     cpu = None
     if not args.no_cpu_baseline:
@@ -362,6 +380,7 @@ def run_ours(args):
                         "per-launch events)",
         "cpu_baseline": cpu,
         "clocks": clk,
+        "rasterizer": raster,
         "tracking": ({"ate_rmse_m": float(np.sqrt(np.mean([np.sum((a - b) ** 2) for a, b in ate]))),
                       "frames": len(ate), "converged_frac": float(np.mean([r["converged"] for r in pipe.track_log]))}
                      if args.track and ate else None),

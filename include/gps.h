@@ -371,6 +371,15 @@ gps_status gps_debug_export_blocks_sync(const gps_volume* vol, gps_stream_t stre
  * against a recount; *n_bad (host) = apron cells that differ + blocks whose count is wrong.
  * Debug only.                                                                               */
 gps_status gps_debug_apron_check_sync(const gps_volume* vol, gps_stream_t stream, int64_t* n_bad /*host*/);
+/* Runs the forward of gps_render (16x16 tiles) in its instrumented form and counts, over all
+ * pixels, the pixel-entry pairs whose membership q was evaluated (*evaluated: the entry survived
+ * the warp's strip test and the pixel's Eq. 1 depth indicator) and those accepted (*accepted:
+ * they contribute alpha to Eq. 2).  E and A of SURVEY §8(d).  Debug only; synchronises.      */
+gps_status gps_debug_render_counts_sync(const gps_gaussians* g, const gps_intrinsics* K /*host*/,
+                                        const gps_pose* T /*host*/, const float* sdf_depth,
+                                        const float* sdf_color, const gps_render_config* cfg /*host*/,
+                                        void* ws, size_t ws_bytes, int64_t* evaluated /*host*/,
+                                        int64_t* accepted /*host*/, gps_stream_t stream);
 /* Runs gps_raycast for (K, T) into temporary buffers while marking every tsdf voxel the march
  * reads; *unique_voxels (host) = their number.  Measures the raycast roofline's unit count
  * (4 bytes per unique voxel read + 16 bytes of output per pixel).  Allocates; debug only.     */

@@ -123,6 +123,8 @@ PROTOTYPES = {
     "gps_debug_apron_check_sync": (gps_status, [vp, gps_stream_t, P(i64)]),
     "gps_debug_raycast_footprint_sync": (gps_status, [vp, P(gps_intrinsics), P(gps_pose), gps_stream_t, P(i64)]),
     "gps_debug_render_lists_sync": (gps_status, [vp, gps_stream_t, vp, i64, vp, P(i64)]),
+    "gps_debug_render_counts_sync": (gps_status, [P(gps_gaussians), P(gps_intrinsics), P(gps_pose), vp, vp,
+                                                  P(gps_render_config), vp, sz, P(i64), P(i64), gps_stream_t]),
     "gps_profile_enable": (None, [C.c_int]),
     "gps_profile_read_sync": (C.c_int, [C.c_char_p, C.c_int, P(C.c_double), P(i64), C.c_int]),
     "gps_status_string": (C.c_char_p, [gps_status]),

@@ -346,6 +346,16 @@ class Rasterizer:
         st = _L.gps_render_stats_sync(_ptr(self.ws), _stream(stream), C.byref(K), C.byref(cap), C.byref(nv))
         return {"pairs": K.value, "capacity": cap.value, "n_visible": nv.value, "status": N.STATUS[st]}
 
+    def pair_counts(self, g: Gaussians, cam: Camera, R, t, sdf_depth, sdf_color, stream=None):
+        """(evaluated, accepted) pixel-entry pairs of one instrumented forward (debug; syncs)."""
+        e, a = C.c_int64(), C.c_int64()
+        N.check("gps_debug_render_counts_sync",
+                _L.gps_debug_render_counts_sync(C.byref(g.c()), C.byref(cam.c()), C.byref(pose_struct(R, t)),
+                                                _ptr(sdf_depth), _ptr(sdf_color), C.byref(self.cfg.c()),
+                                                _ptr(self.ws), self.ws.numel(), C.byref(e), C.byref(a),
+                                                _stream(stream)))
+        return e.value, a.value
+
     def lists(self, stream=None):
         """(values u32[K], ranges u32[n_tiles, 2]) of the last render."""
         cam = self.cam

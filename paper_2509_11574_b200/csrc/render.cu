@@ -596,6 +596,7 @@ struct BlendIO {
   float* out_weight;
   float* loss_out;  // nullable
   int accumulate_loss;
+  unsigned long long* counters;  // counting instantiation only: {evaluated, accepted} pairs
 };
 
 template <int TILE, bool SORTED>
@@ -840,7 +841,7 @@ __global__ void __launch_bounds__(TILE* TILE) k_sort_blend(RenderArgs a, const f
 // bitonic fallback), so more CTAs stay resident.  Every pixel sees the same entries in the same
 // order as in k_sort_blend, so C* and W_G are bitwise those of the one-pixel-per-thread kernel.
 // --------------------------------------------------------------------------------------------
-template <bool SORTED>
+template <bool SORTED, bool COUNT = false>
 __global__ void __launch_bounds__(128) k_sort_blend16x2(RenderArgs a, const float4* __restrict__ rec,
                                                         const uint32_t* __restrict__ offsets, uint32_t* vals,
                                                         uint64_t* gkeys, uint32_t* tile_end, float* loss_part,
@@ -952,6 +953,7 @@ __global__ void __launch_bounds__(128) k_sort_blend16x2(RenderArgs a, const floa
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) wlim = fmaxf(wlim, __shfl_xor_sync(0xFFFFFFFFu, wlim, o));
   float W0 = 0.f, A0 = 0.f, B0 = 0.f, G0 = 0.f, W1 = 0.f, A1 = 0.f, B1 = 0.f, G1 = 0.f;
+  uint32_t n_eval = 0, n_acc = 0;  // COUNT: pixel-entry pairs whose q was evaluated / accepted
   bool wdone = !(wlim > -INFINITY);  // warp-uniform
   for (int base = 0; base < n_eff; base += NB) {
     const int cnt = min(NB, n_eff - base);
@@ -997,6 +999,10 @@ __global__ void __launch_bounds__(128) k_sort_blend16x2(RenderArgs a, const floa
         const float q0 = pair_q(r0.x, r0.y, r0.z, r0.w, r1.x, fx, fy0);
         const float q1 = pair_q(r0.x, r0.y, r0.z, r0.w, r1.x, fx, fy1);
         const bool p0 = i0 && q0 <= r1.w, p1 = i1 && q1 <= r1.w;
+        if (COUNT) {
+          n_eval += (uint32_t)(i0 && inside[0]) + (uint32_t)(i1 && inside[1]);
+          n_acc += (uint32_t)(p0 && inside[0]) + (uint32_t)(p1 && inside[1]);
+        }
         if (!(p0 | p1)) continue;
         const float4 r2 = s2[kk];
         if (p0) {
@@ -1012,6 +1018,13 @@ __global__ void __launch_bounds__(128) k_sort_blend16x2(RenderArgs a, const floa
       }
     }
     if (__syncthreads_count(!wdone) == 0) break;
+  }
+  if (COUNT) {
+    const unsigned long long e = __reduce_add_sync(0xFFFFFFFFu, n_eval), c = __reduce_add_sync(0xFFFFFFFFu, n_acc);
+    if (lane == 0) {
+      atomicAdd(io.counters, e);
+      atomicAdd(io.counters + 1, c);
+    }
   }
   // ---- Eq. 4 composite with W_t = 1, fused L1 ----
   float l1 = 0.f;
@@ -1810,7 +1823,8 @@ struct View1 {
 // forward of one view: preprocess .. sort_blend.  ws must follow ws_layout(refine).
 gps_status forward_view(const gps_gaussians* g, const View1& v, const gps_render_config* c, char* ws,
                         const WsLayout& L, int64_t cap, float* out_color, float* out_weight, float* loss_out,
-                        int accumulate_loss, bool zero_grad2d, cudaStream_t s) {
+                        int accumulate_loss, bool zero_grad2d, cudaStream_t s,
+                        unsigned long long* counters = nullptr) {
   RenderArgs a = make_args(g, v.K, v.T, c, cap);
   WsHeader* hdr = reinterpret_cast<WsHeader*>(ws + L.hdr);
   {
@@ -1856,13 +1870,20 @@ gps_status forward_view(const gps_gaussians* g, const View1& v, const gps_render
   io.out_weight = out_weight;
   io.loss_out = loss_out;
   io.accumulate_loss = accumulate_loss;
+  io.counters = counters;
   uint64_t* gk = reinterpret_cast<uint64_t*>(ws + L.keys);
   uint32_t* tend = reinterpret_cast<uint32_t*>(ws + L.tile_end);
   float* lp = reinterpret_cast<float*>(ws + L.loss_part);
   {
   GPS_PROF(K_SORT_BLEND, s);
   static const bool one_px = getenv("GPS_BLEND_1PX") != nullptr;  // the one-pixel-per-thread kernel
-  if (c->sort_free) {
+  if (counters) {  // debug: the instrumented instantiation (16x16 tiles)
+    if (c->sort_free)
+      k_sort_blend16x2<false, true><<<n_tiles, 128, 0, s>>>(a, sp.rec, offsets, vals, gk, tend, lp, hdr, io, 0);
+    else
+      k_sort_blend16x2<true, true><<<n_tiles, 128, 0, s>>>(a, sp.rec, offsets, vals, gk, tend, lp, hdr, io,
+                                                           c->tile_depth_precull);
+  } else if (c->sort_free) {
     if (a.tile == 16 && !one_px)
       k_sort_blend16x2<false><<<n_tiles, 128, 0, s>>>(a, sp.rec, offsets, vals, gk, tend, lp, hdr, io, 0);
     else if (a.tile == 16)
@@ -2095,6 +2116,40 @@ gps_status gps_render_stats_sync(const void* ws, gps_stream_t stream, int64_t* n
     set_error("render pair list overflow: " + std::to_string(h.K) + " pairs > capacity " + std::to_string(h.cap_pairs));
     return GPS_ERR_WORKSPACE_TOO_SMALL;
   }
+  return GPS_OK;
+}
+
+gps_status gps_debug_render_counts_sync(const gps_gaussians* g, const gps_intrinsics* K, const gps_pose* T,
+                                        const float* sdf_depth, const float* sdf_color, const gps_render_config* cfg,
+                                        void* ws, size_t ws_bytes, int64_t* evaluated, int64_t* accepted,
+                                        gps_stream_t stream) {
+  gps_status st = check_gaussians(g, "gps_debug_render_counts_sync");
+  if (st != GPS_OK) return st;
+  if ((st = check_render_cfg(cfg)) != GPS_OK) return st;
+  if (!valid_K(K) || !T || !sdf_depth || !sdf_color || !ws || !evaluated || !accepted || cfg->tile != 16)
+    return invalid("gps_debug_render_counts_sync: bad argument (16x16 tiles only)");
+  const int64_t cap = default_cap(g->n, cfg->max_pairs);
+  const WsLayout L = ws_layout(g->n, K->width, K->height, cfg->tile, cap, 0, false, false);
+  if (ws_bytes < L.total) return invalid("gps_debug_render_counts_sync: workspace too small");
+  cudaStream_t s = as_stream(stream);
+  unsigned long long* cnt = nullptr;
+  float *oc = nullptr, *ow = nullptr;
+  const size_t px = (size_t)K->width * K->height;
+  GPS_CHECK_CUDA(cudaMallocAsync(&cnt, 16, s));
+  GPS_CHECK_CUDA(cudaMallocAsync(&oc, 12 * px, s));
+  GPS_CHECK_CUDA(cudaMallocAsync(&ow, 4 * px, s));
+  GPS_CHECK_CUDA(cudaMemsetAsync(cnt, 0, 16, s));
+  View1 v{K, T, sdf_depth, sdf_color, nullptr};
+  st = forward_view(g, v, cfg, static_cast<char*>(ws), L, cap, oc, ow, nullptr, 0, false, s, cnt);
+  if (st != GPS_OK) return st;
+  unsigned long long h[2] = {0, 0};
+  GPS_CHECK_CUDA(cudaMemcpyAsync(h, cnt, 16, cudaMemcpyDeviceToHost, s));
+  GPS_CHECK_CUDA(cudaFreeAsync(cnt, s));
+  GPS_CHECK_CUDA(cudaFreeAsync(oc, s));
+  GPS_CHECK_CUDA(cudaFreeAsync(ow, s));
+  GPS_CHECK_CUDA(cudaStreamSynchronize(s));
+  *evaluated = (int64_t)h[0];
+  *accepted = (int64_t)h[1];
   return GPS_OK;
 }
 
