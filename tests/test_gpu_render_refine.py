@@ -324,3 +324,40 @@ np.savez(sys.argv[2], **out)
         assert np.array_equal(res["two"][k], res["one"][k]), k
     # sort-free: the bucket order comes from atomics, so only agreement to rounding is expected
     assert np.max(np.abs(res["two"]["C1"] - res["one"]["C1"])) <= 1e-5
+
+
+def test_pair_counters_accepted_matches_an_independent_count():
+    """gps_debug_render_counts_sync's accepted pairs A equal the number of
+    (pixel, Gaussian) pairs passing the exact membership of DESIGN.md §4.3 and the Eq. 1 depth
+    indicator, counted here from the oracle's P32 fields (fp32, FMA emulated through exact fp64
+    products: boundary double-rounding allowed for, 1e-4); the evaluated pairs E bound A."""
+    import paper_2509_11574_b200 as G
+    cfg = S.get_config("cfg2")
+    fr = H.frames(cfg, 1, start=3)[0]
+    gd = S.make_gaussians(cfg, n=20000)
+    Dt, Ct = S.sdf_stage_inputs(cfg, fr, seed=3)
+    gcam, ocam = H.cams(cfg)
+    g = G.Gaussians.from_dict(gd)
+    ras = G.Rasterizer(g.n, gcam, G.RenderConfig(tile_depth_precull=1))
+    E, A = ras.pair_counts(g, gcam, fr.R, fr.t, torch.from_numpy(Dt).cuda(), torch.from_numpy(Ct).cuda())
+    rect, depth, culled, fl = O.project_p32(gd, ocam, fr.R, fr.t, O.RenderCfg(), fields=True)
+    f32 = np.float32
+    L = f32(-np.log(np.float64(f32(1.0 / 255))))
+    eps = f32(0.02)
+    count = 0
+    for i in np.flatnonzero(culled == 0):
+        x0, y0, x1, y1 = rect[i]
+        px, py, a, b, c, lns = fl[i]
+        qmax = min(f32(9.0), f32(f32(2.0) * f32(L + lns)))
+        xs = np.arange(x0, x1 + 1, dtype=f32)
+        ys = np.arange(y0, y1 + 1, dtype=f32)
+        dx = (xs[None, :] - px).astype(f32)
+        dy = (ys[:, None] - py).astype(f32)
+        b2 = f32(f32(2.0) * b)
+        inner = ((b2 * dx).astype(f32).astype(np.float64) * dy + ((c * dy).astype(f32) * dy).astype(f32)).astype(f32)
+        q = ((a * dx).astype(f32).astype(np.float64) * dx + inner).astype(f32)
+        D = Dt[y0:y1 + 1, x0:x1 + 1]
+        ok = (q <= qmax) & ((D == 0) | (depth[i] < (D + eps).astype(f32)))
+        count += int(ok.sum())
+    assert A > 1000 and E >= A
+    assert abs(A - count) <= 1e-4 * count
