@@ -362,7 +362,7 @@ def run_ours(args):
                                         "ncu's issue-active and lanes/instruction are in profiles/"}}
     launches = int(sum(v["launches"] for kk, v in prof.items() if kk != "memset"))
     cpu = None
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and ws == 1:  # the oracle baseline: rank 0 at N = 1 only
         cpu = cpu_baseline(cfg, gd, frames, args.cpu_seconds)
     line = {
         "metric": "mapping frames/sec at 1280x720 (fuse+raycast+refine)",
