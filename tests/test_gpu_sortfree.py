@@ -88,3 +88,21 @@ def test_sortfree_large_gaussians_span_many_tiles():
     ras.refine_step(g, st, [G.View(gcam, R, t, dev["Dt"], dev["Ct"], dev["tgt"])], grad_out=gout)
     oloss, ref, gamb = oracle_grads(gd, c, R, t, Dt, Ct, tgt)
     compare_grads(gout.to_numpy(), ref, gamb, min_checked=20)
+
+
+@pytest.mark.slow
+def test_sortfree_full_size_cfg4():
+    """The sort-free renderer at the bench's full size (1280x720, 200k Gaussians): image, loss and
+    raw-parameter gradients against the oracle."""
+    G, cfg, fr, gd, Dt, Ct, tgt, gcam, ocam, dev = setup("cfg4", start=300)
+    g = G.Gaussians.from_dict(gd)
+    ras = G.Rasterizer(g.n, gcam, G.RenderConfig(sort_free=1))
+    Cs, W, loss = ras.render(g, gcam, fr.R, fr.t, dev["Dt"], dev["Ct"], dev["tgt"])
+    out = O.render(gd, ocam, fr.R, fr.t, Dt, Ct)
+    check_forward(out, Cs.cpu().numpy(), W.cpu().numpy())
+    st = G.AdamState(g)
+    gout = g.zeros_like()
+    ras.refine_step(g, st, [G.View(gcam, fr.R, fr.t, dev["Dt"], dev["Ct"], dev["tgt"])], grad_out=gout)
+    oloss, ref, gamb = oracle_grads(gd, ocam, fr.R, fr.t, Dt, Ct, tgt)
+    assert abs(loss.item() - oloss) <= 1e-5 * oloss
+    compare_grads(gout.to_numpy(), ref, gamb, min_checked=10000)
