@@ -126,12 +126,11 @@ __global__ void __launch_bounds__(kIcpThreads) k_icp_reduce(Level L, Assoc a, co
 #pragma unroll
   for (int k = 0; k < kIcpSums; ++k) s[k] = 0.f;
   const int n = L.W * L.H;
-  const int i = blockIdx.x * kIcpThreads + threadIdx.x;
   int valid = 0;
-  if (i < n) {
+  for (int i = blockIdx.x * kIcpThreads + threadIdx.x; i < n; i += gridDim.x * kIcpThreads) {
     const float* Nc = L.N + 3 * (size_t)i;
     if (Nc[0] != 0.f || Nc[1] != 0.f || Nc[2] != 0.f) {
-      valid = 1;
+      valid += 1;
       const float* Vc = L.V + 3 * (size_t)i;
       float p[3], nn[3];
 #pragma unroll
@@ -158,11 +157,11 @@ __global__ void __launch_bounds__(kIcpThreads) k_icp_reduce(Level L, Assoc a, co
 #pragma unroll
             for (int x = 0; x < 6; ++x)
 #pragma unroll
-              for (int y = x; y < 6; ++y) s[k++] = J[x] * J[y];
+              for (int y = x; y < 6; ++y) s[k++] += J[x] * J[y];
 #pragma unroll
-            for (int x = 0; x < 6; ++x) s[21 + x] = J[x] * r;
-            s[27] = r * r;
-            s[28] = 1.f;
+            for (int x = 0; x < 6; ++x) s[21 + x] += J[x] * r;
+            s[27] += r * r;
+            s[28] += 1.f;
           }
         }
       }
@@ -177,24 +176,40 @@ __global__ void __launch_bounds__(kIcpThreads) k_icp_reduce(Level L, Assoc a, co
     for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xFFFFFFFFu, x, o);
     if (lane == 0) red[w][k] = x;
   }
-  const int cv = __syncthreads_count(valid);
+  __shared__ int svalid[kIcpThreads / 32];
+  const int vw = __reduce_add_sync(0xFFFFFFFFu, valid);
+  if (lane == 0) svalid[w] = vw;
+  __syncthreads();
   if (threadIdx.x < kIcpSums) {
     double x = 0.0;
     for (int j = 0; j < kIcpThreads / 32; ++j) x += red[j][threadIdx.x];
     partial[(size_t)blockIdx.x * 32 + threadIdx.x] = x;
   }
-  if (threadIdx.x == 0) partial[(size_t)blockIdx.x * 32 + 29] = (double)cv;
+  if (threadIdx.x == 0) {
+    int cv = 0;
+    for (int j = 0; j < kIcpThreads / 32; ++j) cv += svalid[j];
+    partial[(size_t)blockIdx.x * 32 + 29] = (double)cv;
+  }
 }
 
 // one CTA: total the CTA sums, solve A xi = -b (Cholesky), pose <- exp(xi) pose
 __global__ void __launch_bounds__(256) k_icp_solve(const double* __restrict__ partial, int nblk, DevPose* pose,
                                                    double eps) {
   __shared__ double tot[32];
+  __shared__ double part[8][32];
   if (pose->stop) return;
-  if (threadIdx.x < 30) {
+  {  // 30 sums x 8 interleaved chunks of the CTA partials, then the 8 chunks per sum
+    const int v = threadIdx.x & 31, c = threadIdx.x >> 5;
     double x = 0.0;
-    for (int b = 0; b < nblk; ++b) x += partial[(size_t)b * 32 + threadIdx.x];
-    tot[threadIdx.x] = x;
+    if (v < 30)
+      for (int b = c; b < nblk; b += 8) x += partial[(size_t)b * 32 + v];
+    part[c][v] = x;
+    __syncthreads();
+    if (threadIdx.x < 30) {
+      double y = 0.0;
+      for (int k = 0; k < 8; ++k) y += part[k][threadIdx.x];
+      tot[threadIdx.x] = y;
+    }
   }
   __syncthreads();
   if (threadIdx.x != 0) return;
@@ -359,7 +374,7 @@ gps_status gps_track_sync(const gps_intrinsics* K, const uint16_t* depth, float 
     L.stride = 1 << l;
     k_icp_maps<<<dim3((L.W + 15) / 16, (L.H + 15) / 16), 256, 0, s>>>(L, dp);
     GPS_CHECK_LAUNCH("k_icp_maps");
-    const int nblk = (L.W * L.H + kIcpThreads - 1) / kIcpThreads;
+    const int nblk = std::min((L.W * L.H + kIcpThreads - 1) / kIcpThreads, 148 * 4);  // grid-stride
     for (int it = 0; it < cfg->iters[l]; ++it) {
       k_icp_reduce<<<nblk, kIcpThreads, 0, s>>>(L, a, dp, partial);
       GPS_CHECK_LAUNCH("k_icp_reduce");
