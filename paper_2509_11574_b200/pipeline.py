@@ -100,23 +100,47 @@ class MappingPipeline:
         self.rounds = 0
         self.iterations_run = 0
 
-    def _device(self, x: torch.Tensor) -> torch.Tensor:
-        """Host frames are uploaded on a dedicated copy stream (pinned memory -> async), so frame
-        k+1's upload overlaps frame k's kernels; the compute stream waits on an event."""
-        if x.is_cuda:
-            return x
-        compute = torch.cuda.current_stream()
+    def _upload(self, x: torch.Tensor):
+        """Start the H2D copy of a pinned host tensor on the copy stream; (device tensor, event)."""
         with torch.cuda.stream(self.copy_stream):
             d = x.to("cuda", non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(self.copy_stream)
+        return d, ev
+
+    def _device(self, x: torch.Tensor) -> torch.Tensor:
+        """Host frames are uploaded on a dedicated copy stream (pinned memory -> async); a frame
+        announced by the previous call's `prefetch` is already in flight.  The compute stream
+        waits on the copy's event."""
+        if x.is_cuda:
+            return x
+        pre = self._prefetched.pop(id(x), None) if hasattr(self, "_prefetched") else None
+        if pre is not None and pre[0] is x:
+            d, ev = pre[1], pre[2]
+        else:
+            d, ev = self._upload(x)
+        compute = torch.cuda.current_stream()
         compute.wait_event(ev)
         d.record_stream(compute)
         return d
 
-    def process_frame(self, k: int, depth: torch.Tensor, rgba: torch.Tensor, R, t, refine: bool = True):
+    def prefetch(self, *host_tensors):
+        """Start uploading the next frame's host tensors now (its process_frame call picks them up)."""
+        if not hasattr(self, "_prefetched"):
+            self._prefetched = {}
+        for x in host_tensors:
+            if x is not None and not x.is_cuda and id(x) not in self._prefetched:
+                d, ev = self._upload(x)
+                self._prefetched[id(x)] = (x, d, ev)
+
+    def process_frame(self, k: int, depth: torch.Tensor, rgba: torch.Tensor, R, t, refine: bool = True,
+                      prefetch=None):
+        """One frame of the mapping step.  `prefetch`: the next frame's (depth, rgba) host tensors,
+        whose upload then overlaps this frame's kernels."""
         depth = self._device(depth)
         rgba = self._device(rgba)
+        if prefetch is not None:
+            self.prefetch(*prefetch)
         if self.tracking and self._model is not None:
             Rp, tp = self.prev_pose
             res = A.track(self.cam, depth, self.depth_scale, self._model[0], self._model[1], Rp, tp, Rp, tp,
