@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define GPS_ABI_VERSION 1
+#define GPS_ABI_VERSION 2  /* 2: gps_render_config.sort_free; adding, removal, tracking entry points */
 
 typedef void* gps_stream_t; /* a cudaStream_t */
 

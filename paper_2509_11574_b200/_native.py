@@ -162,8 +162,13 @@ def load(path: str | None = None):
         fn = getattr(L, name)
         fn.restype = res
         fn.argtypes = args
+    if L.gps_abi_version() != ABI_VERSION:
+        raise OSError(f"libgps.so ABI {L.gps_abi_version()} != binding ABI {ABI_VERSION}: rebuild")
     _lib = L
     return L
+
+
+ABI_VERSION = 2  # must equal GPS_ABI_VERSION of include/gps.h (the struct layouts above)
 
 
 def check(fn: str, status: int):
