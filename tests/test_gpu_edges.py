@@ -1,0 +1,93 @@
+"""Edge cases of the GPU path against the CPU oracle (③: ragged inputs, maximum sizes, degenerate
+cases).
+
+* A ragged 100x75 image (tiles and warps straddle the right and bottom borders, the pixel count
+  is no multiple of any block size) through fuse, raycast, render and the refine gradients.
+* A tile list longer than both shared-memory sorts (> 2048 entries in one tile): the global
+  bitonic fallback keeps the lists bit-exact and the image and gradients equal to the oracle's.
+* An SDF render that missed everywhere (D_t = 0: no depth test, C_t = 0, R-MISS).
+Bars as in test_gpu_fuse_raycast.py / test_gpu_render_refine.py."""
+import numpy as np
+import pytest
+import torch
+
+import gps_synth as S
+import oracle as O
+from tests import gpu_helpers as H
+from tests.test_gpu_fuse_raycast import compare_volumes, raycast_compare
+from tests.test_gpu_render_refine import check_forward, compare_grads, oracle_grads
+
+pytestmark = pytest.mark.gpu
+
+
+def _ragged_cfg():
+    # cfg2's room and noise at a ragged 100x75, intrinsics scaled from cfg2's field of view
+    return S.get_config("cfg2", width=100, height=75, fx=82.0, fy=82.0, cx=49.5, cy=37.0)
+
+
+def test_ragged_image_fuse_and_raycast():
+    cfg = _ragged_cfg()
+    frs = H.frames(cfg, 2)
+    gvol, ovol = H.fuse_both(cfg, frs)
+    compare_volumes(gvol, ovol, 20)
+    raycast_compare(cfg, gvol, ovol, frs[1].R, frs[1].t)
+
+
+@pytest.mark.parametrize("sort_free", [0, 1])
+def test_ragged_image_render_and_gradients(sort_free):
+    import paper_2509_11574_b200 as G
+    cfg = _ragged_cfg()
+    fr = H.frames(cfg, 1)[0]
+    gd = S.make_gaussians(cfg, n=3000, frames=[fr])
+    Dt, Ct = S.sdf_stage_inputs(cfg, fr)
+    tgt = fr.rgba
+    gcam, ocam = H.cams(cfg)
+    dev = dict(Dt=torch.from_numpy(Dt).cuda(), Ct=torch.from_numpy(Ct).cuda(), tgt=tgt.cuda().contiguous())
+    g = G.Gaussians.from_dict(gd)
+    ras = G.Rasterizer(g.n, gcam, G.RenderConfig(sort_free=sort_free))
+    Cs, W, loss = ras.render(g, gcam, fr.R, fr.t, dev["Dt"], dev["Ct"], dev["tgt"])
+    out = O.render(gd, ocam, fr.R, fr.t, Dt, Ct)
+    check_forward(out, Cs.cpu().numpy(), W.cpu().numpy())
+    st = G.AdamState(g)
+    gout = g.zeros_like()
+    ras.refine_step(g, st, [G.View(gcam, fr.R, fr.t, dev["Dt"], dev["Ct"], dev["tgt"])], grad_out=gout)
+    oloss, ref, gamb = oracle_grads(gd, ocam, fr.R, fr.t, Dt, Ct, tgt.numpy())
+    compare_grads(gout.to_numpy(), ref, gamb, min_checked=100)
+
+
+def _crowded(n=2600):
+    """n Gaussians crowding one 16x16 tile of a 96x64 view: that tile's list exceeds both
+    shared-memory sorts (256 for the rank sort, 2048 for the one-pixel kernel's bitonic)."""
+    rng = np.random.default_rng(11)
+    c = O.Camera(80.0, 80.0, 47.5, 31.5, 96, 64)
+    gd = S.random_gaussians(n, 1, rng, center=(0.0, 0.0, 1.0), spread=0.004, scale=(0.002, 0.006))
+    gd["opacity_raw"] = np.full(n, -2.0, np.float32)  # sigma ~ 0.12: many small contributions
+    return c, gd, rng
+
+
+def test_tile_list_beyond_shared_memory_sorts():
+    import paper_2509_11574_b200 as G
+    c, gd, rng = _crowded()
+    gcam = G.Camera(80.0, 80.0, 47.5, 31.5, 96, 64)
+    R, t = np.eye(3, dtype=np.float32), np.zeros(3, np.float32)
+    Dt = np.zeros((64, 96), np.float32)  # no SDF surface: every entry is in front (R-MISS)
+    Ct = rng.random((64, 96, 3)).astype(np.float32)
+    Ct[:] = 0.0
+    tgt = rng.integers(0, 256, (64, 96, 4)).astype(np.uint8)
+    dev = dict(Dt=torch.from_numpy(Dt).cuda(), Ct=torch.from_numpy(Ct).cuda(), tgt=torch.from_numpy(tgt).cuda())
+    g = G.Gaussians.from_dict(gd)
+    ras = G.Rasterizer(g.n, gcam, G.RenderConfig(tile_depth_precull=0))
+    Cs, W, loss = ras.render(g, gcam, R, t, dev["Dt"], dev["Ct"], dev["tgt"])
+    gv, grng = ras.lists()
+    lens = grng[:, 1] - grng[:, 0]
+    assert lens.max() > 2048
+    rect, depth, culled = O.project_p32(gd, c, R, t, O.RenderCfg())
+    ov, orng = O.tile_lists(rect, depth, culled, 96, 64, 16)
+    assert np.array_equal(grng, orng) and np.array_equal(gv, ov)
+    out = O.render(gd, c, R, t, Dt, Ct)
+    check_forward(out, Cs.cpu().numpy(), W.cpu().numpy())
+    st = G.AdamState(g)
+    gout = g.zeros_like()
+    ras.refine_step(g, st, [G.View(gcam, R, t, dev["Dt"], dev["Ct"], dev["tgt"])], grad_out=gout)
+    oloss, ref, gamb = oracle_grads(gd, c, R, t, Dt, Ct, tgt)
+    compare_grads(gout.to_numpy(), ref, gamb, min_checked=500)
