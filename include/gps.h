@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define GPS_ABI_VERSION 2  /* 2: gps_render_config.sort_free; adding, removal, tracking entry points */
+#define GPS_ABI_VERSION 3  /* 2: gps_render_config.sort_free; adding, removal, tracking entry points; 3: device-pose forms */
 
 typedef void* gps_stream_t; /* a cudaStream_t */
 
@@ -145,6 +145,18 @@ gps_status gps_fuse(gps_volume* vol, const gps_intrinsics* K /*host*/, const gps
 gps_status gps_raycast(const gps_volume* vol, const gps_intrinsics* K /*host*/,
                        const gps_pose* T /*host*/, float* depth_out, float* color_out,
                        float* vertex_out, gps_stream_t stream);
+
+/* Device-pose forms (tracking): identical to gps_fuse / gps_raycast --
+ * same kernels, same fp32 sequences, same results for the same pose values -- except that the
+ * pose is read on the device from T_dev (a gps_pose in device memory, 4-byte aligned, e.g. the
+ * output of gps_track_async), so a tracked frame needs no host round trip.  T_dev must stay
+ * valid until the stream has executed the call.                                               */
+gps_status gps_fuse_dpose(gps_volume* vol, const gps_intrinsics* K /*host*/,
+                          const gps_pose* T_dev /*device*/, const uint16_t* depth, float depth_scale,
+                          const uint8_t* rgba, gps_stream_t stream);
+gps_status gps_raycast_dpose(const gps_volume* vol, const gps_intrinsics* K /*host*/,
+                             const gps_pose* T_dev /*device*/, float* depth_out, float* color_out,
+                             float* vertex_out, gps_stream_t stream);
 
 /* ------------------------------------------------------------------------------------------
  * Gaussians ("G = {p_i, sigma_i, r_i, s_i, SH_i} ... following 3DGS").  Caller-owned SoA,
@@ -263,6 +275,10 @@ gps_status gps_adam_step(gps_gaussians* g, gps_adam_state* state /*host struct*/
 gps_status gps_vertex_normals(const gps_intrinsics* K /*host*/, const gps_pose* T /*host*/,
                               const float* sdf_depth, const float* vertex, float* normal_out,
                               gps_stream_t stream);
+/* The same with the camera centre read from a device pose (see gps_fuse_dpose).             */
+gps_status gps_vertex_normals_dpose(const gps_intrinsics* K /*host*/, const gps_pose* T_dev /*device*/,
+                                    const float* sdf_depth, const float* vertex, float* normal_out,
+                                    gps_stream_t stream);
 
 typedef struct {
   float delta_c;      /* colour-error threshold of Eq. 6 [0.05]                         */
@@ -322,16 +338,23 @@ typedef struct {
   float depth_min, depth_max; /* valid raw depth range, metres [0.1, 10]                         */
   float eps;             /* a level stops when |xi| < eps [1e-6]                                */
   float min_inlier_frac; /* converged needs this inlier fraction at the end [0.1]               */
+  int32_t fallback;      /* 1: a frame that does not converge gets T_init (gps_track_async: T_fail
+                          *    if given) as its pose in result.T; R64/t64 still hold the iterate
+                          *    -- R-ICP-FAIL [1]; 0: result.T is the iterate whatever the outcome */
+  float min_inlier_px_frac; /* converged also needs inliers >= this fraction of the frame's
+                             * pixels [0.05] (R-ICP-FAIL: a near-empty depth frame is a failure) */
 } gps_icp_config;
 
 typedef struct {
-  gps_pose T;            /* tracked camera -> world pose (fp32 copy of R64, t64)                */
+  gps_pose T;            /* tracked camera -> world pose: fp32 copy of R64, t64 (or T_init, see
+                          * gps_icp_config.fallback)                                           */
   double R64[9], t64[3]; /* the pose as iterated on the device (fp64)                           */
   double energy;         /* sum of squared point-to-plane residuals of the last step's inliers  */
   int32_t inliers, valid;/* last step's inliers / current pixels with a normal                  */
   int32_t steps;         /* Gauss-Newton steps taken                                            */
   int32_t degenerate;    /* a step had < 6 inliers or a rank-deficient system (no update)       */
-  int32_t converged;     /* !degenerate and inliers/valid >= min_inlier_frac                    */
+  int32_t converged;     /* !degenerate, inliers/valid >= min_inlier_frac and
+                          * inliers >= min_inlier_px_frac * width * height                      */
   float inlier_frac;
 } gps_track_result;
 
@@ -350,6 +373,29 @@ gps_status gps_track_sync(const gps_intrinsics* K /*host*/, const uint16_t* dept
                           const gps_pose* T_model /*host*/, const gps_pose* T_init /*host*/,
                           const gps_icp_config* cfg /*host*/, void* ws, size_t ws_bytes,
                           gps_track_result* out /*host*/, gps_stream_t stream);
+
+/* gps_pose_extrapolate -- constant-velocity prediction of the next pose from the two previous
+ * ones (R-ICP-FAIL): T_out = T_b * (T_a^-1 * T_b), i.e. the relative motion a -> b applied once
+ * more in the camera frame, on the device in double (T_a^-1 = [R^T, -R^T t]), R re-orthonormalised
+ * (Gram-Schmidt on its rows) before rounding to fp32 -- chained predictions would otherwise
+ * amplify the inputs' fp32 departures from orthonormality.
+ * All three poses in device memory; T_out may alias neither input.  The initial pose for the
+ * next frame's gps_track_async.                                                              */
+gps_status gps_pose_extrapolate(const gps_pose* T_a_dev, const gps_pose* T_b_dev, gps_pose* T_out_dev,
+                                gps_stream_t stream);
+
+/* gps_track_async -- gps_track_sync with every pose in device memory and no synchronisation:
+ * the poses T_model_dev, T_init_dev and T_fail_dev (nullable: T_init; the pose a frame that does
+ * not converge gets when cfg->fallback, e.g. gps_pose_extrapolate's prediction) are read on the
+ * device (they may alias each other and T_out_dev); T_out_dev <- the tracked pose (fp32,
+ * = result.T); result_dev (nullable, device) <- the whole gps_track_result.  The same kernels as gps_track_sync: for the same inputs both
+ * produce bit-identical poses.  Errors: argument errors only (returned immediately).           */
+gps_status gps_track_async(const gps_intrinsics* K /*host*/, const uint16_t* depth, float depth_scale,
+                           const float* model_vertex, const float* model_normal,
+                           const gps_pose* T_model_dev, const gps_pose* T_init_dev,
+                           const gps_pose* T_fail_dev, const gps_icp_config* cfg /*host*/, void* ws,
+                           size_t ws_bytes, gps_pose* T_out_dev, gps_track_result* result_dev,
+                           gps_stream_t stream);
 
 /* Synchronises `stream` and reports the pair count K of the last render held in `ws`, the pair
  * capacity, and the number of Gaussians that survived culling.  Returns

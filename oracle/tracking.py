@@ -28,6 +28,7 @@ class IcpCfg:
     depth_max: float = 10.0
     eps: float = 1e-6               # convergence on |xi|
     min_inlier_frac: float = 0.1
+    min_inlier_px_frac: float = 0.05  # R-ICP-FAIL: and inliers >= this fraction of the frame's pixels
 
 
 def depth_pyramid(depth_m: np.ndarray, levels: int, dmin: float, dmax: float):
@@ -156,5 +157,6 @@ def track(depth_u16, depth_scale, K, Vm_full, Nm_full, Rp, tp, R0, t0, cfg: IcpC
             if np.linalg.norm(xi) < cfg.eps:
                 break
     info["inlier_frac"] = info["inliers"] / max(info["valid"], 1)
-    info["converged"] = (not info["degenerate"]) and info["inlier_frac"] >= cfg.min_inlier_frac
+    info["converged"] = ((not info["degenerate"]) and info["inlier_frac"] >= cfg.min_inlier_frac
+                         and info["inliers"] >= cfg.min_inlier_px_frac * np.shape(depth_u16)[0] * np.shape(depth_u16)[1])
     return R, t, info

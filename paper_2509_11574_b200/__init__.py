@@ -6,8 +6,10 @@ the in-tree build (``build``).  Importing it loads libgps.so and raises if it is
 """
 from . import _native
 from .api import (AdamConfig, AdamState, AddConfig, Camera, Gaussians, Rasterizer, RemoveConfig, RenderConfig, View,
-                  Volume, adam_step, add_gaussians, pose_struct, remove_gaussians, vertex_normals, IcpConfig, track)
+                  Volume, adam_step, add_gaussians, pose_struct, remove_gaussians, vertex_normals, IcpConfig, track,
+                  TRACK_RESULT_BYTES, pose_extrapolate, pose_tensor, track_async, track_result, vertex_normals_dpose)
 
 __all__ = ["AdamConfig", "AdamState", "AddConfig", "Camera", "Gaussians", "Rasterizer", "RemoveConfig", "RenderConfig",
            "View", "Volume", "adam_step", "add_gaussians", "pose_struct", "remove_gaussians", "vertex_normals",
-           "IcpConfig", "track"]
+           "IcpConfig", "track", "TRACK_RESULT_BYTES", "pose_extrapolate", "pose_tensor", "track_async", "track_result",
+           "vertex_normals_dpose"]

@@ -77,7 +77,7 @@ class gps_remove_config(C.Structure):
 class gps_icp_config(C.Structure):
     _fields_ = [("levels", C.c_int32), ("iters", C.c_int32 * 4), ("dist_max", C.c_float),
                 ("angle_max_deg", C.c_float), ("depth_min", C.c_float), ("depth_max", C.c_float),
-                ("eps", C.c_float), ("min_inlier_frac", C.c_float)]
+                ("eps", C.c_float), ("min_inlier_frac", C.c_float), ("fallback", C.c_int32), ("min_inlier_px_frac", C.c_float)]
 
 
 class gps_track_result(C.Structure):
@@ -97,6 +97,8 @@ PROTOTYPES = {
     "gps_volume_stats_sync": (gps_status, [vp, gps_stream_t, P(i64), P(i64), P(i64), P(i64), P(i64)]),
     "gps_fuse": (gps_status, [vp, P(gps_intrinsics), P(gps_pose), vp, f32, vp, gps_stream_t]),
     "gps_raycast": (gps_status, [vp, P(gps_intrinsics), P(gps_pose), vp, vp, vp, gps_stream_t]),
+    "gps_fuse_dpose": (gps_status, [vp, P(gps_intrinsics), vp, vp, f32, vp, gps_stream_t]),
+    "gps_raycast_dpose": (gps_status, [vp, P(gps_intrinsics), vp, vp, vp, vp, gps_stream_t]),
     "gps_render_workspace_size": (sz, [i64, P(gps_intrinsics), P(gps_render_config)]),
     "gps_render": (gps_status, [P(gps_gaussians), P(gps_intrinsics), P(gps_pose), vp, vp, vp,
                                 P(gps_render_config), vp, sz, vp, vp, vp, gps_stream_t]),
@@ -108,6 +110,7 @@ PROTOTYPES = {
                                    P(gps_adam_config), gps_stream_t]),
     "gps_render_stats_sync": (gps_status, [vp, gps_stream_t, P(i64), P(i64), P(i64)]),
     "gps_vertex_normals": (gps_status, [P(gps_intrinsics), P(gps_pose), vp, vp, vp, gps_stream_t]),
+    "gps_vertex_normals_dpose": (gps_status, [P(gps_intrinsics), vp, vp, vp, vp, gps_stream_t]),
     "gps_add_workspace_size": (sz, [P(gps_intrinsics)]),
     "gps_add_gaussians_sync": (gps_status, [P(gps_gaussians), i64, P(gps_adam_state), P(gps_intrinsics), vp, vp,
                                             vp, vp, vp, vp, P(gps_add_config), vp, sz, P(i64), P(i64),
@@ -116,6 +119,9 @@ PROTOTYPES = {
     "gps_track_workspace_size": (sz, [P(gps_intrinsics), i32]),
     "gps_track_sync": (gps_status, [P(gps_intrinsics), vp, f32, vp, vp, P(gps_pose), P(gps_pose), P(gps_icp_config),
                                     vp, sz, P(gps_track_result), gps_stream_t]),
+    "gps_pose_extrapolate": (gps_status, [vp, vp, vp, gps_stream_t]),
+    "gps_track_async": (gps_status, [P(gps_intrinsics), vp, f32, vp, vp, vp, vp, vp, P(gps_icp_config), vp, sz, vp,
+                                     vp, gps_stream_t]),
     "gps_remove_gaussians_sync": (gps_status, [P(gps_gaussians), P(gps_adam_state), P(gps_remove_config), vp, sz,
                                                P(i64), gps_stream_t]),
     "gps_debug_export_blocks_sync": (gps_status, [vp, gps_stream_t, vp, vp, i64, P(i64)]),
@@ -168,7 +174,7 @@ def load(path: str | None = None):
     return L
 
 
-ABI_VERSION = 2  # must equal GPS_ABI_VERSION of include/gps.h (the struct layouts above)
+ABI_VERSION = 3  # must equal GPS_ABI_VERSION of include/gps.h (the struct layouts above)
 
 
 def check(fn: str, status: int):

@@ -56,6 +56,20 @@ def pose_struct(R, t) -> N.gps_pose:
     return N.gps_pose((C.c_float * 9)(*R.tolist()), (C.c_float * 3)(*t.tolist()))
 
 
+def pose_tensor(R, t, out: torch.Tensor | None = None) -> torch.Tensor:
+    """A gps_pose in device memory (f32[12]: R row-major, t) for the *_dpose entry points."""
+    h = torch.from_numpy(np.concatenate([np.asarray(R, np.float32).reshape(9), np.asarray(t, np.float32).reshape(3)]))
+    if out is None:
+        return h.cuda()
+    out.copy_(h)
+    return out
+
+
+def _dpose(pose: torch.Tensor) -> int:
+    assert pose.is_cuda and pose.dtype == torch.float32 and pose.numel() == 12 and pose.is_contiguous()
+    return _ptr(pose)
+
+
 # ---------------------------------------------------------------------------------------------
 # volume
 # ---------------------------------------------------------------------------------------------
@@ -122,6 +136,21 @@ class Volume:
         assert rgba.dtype == torch.uint8 and rgba.numel() == 4 * cam.width * cam.height
         N.check("gps_fuse", _L.gps_fuse(self.h, C.byref(cam.c()), C.byref(pose_struct(R, t)), _ptr(depth),
                                         float(depth_scale), _ptr(rgba), _stream(stream)))
+
+    def fuse_dpose(self, cam: Camera, pose: torch.Tensor, depth: torch.Tensor, depth_scale: float,
+                   rgba: torch.Tensor, stream=None):
+        """gps_fuse_dpose: as fuse, the pose read on the device from `pose` (pose_tensor layout)."""
+        assert depth.is_cuda and rgba.is_cuda
+        assert depth.element_size() == 2 and depth.numel() == cam.width * cam.height
+        assert rgba.dtype == torch.uint8 and rgba.numel() == 4 * cam.width * cam.height
+        N.check("gps_fuse_dpose", _L.gps_fuse_dpose(self.h, C.byref(cam.c()), _dpose(pose), _ptr(depth),
+                                                    float(depth_scale), _ptr(rgba), _stream(stream)))
+
+    def raycast_dpose(self, cam: Camera, pose: torch.Tensor, depth_out, color_out, vertex_out=None, stream=None):
+        """gps_raycast_dpose: as raycast, the pose read on the device."""
+        N.check("gps_raycast_dpose", _L.gps_raycast_dpose(self.h, C.byref(cam.c()), _dpose(pose), _ptr(depth_out),
+                                                          _ptr(color_out), _ptr(vertex_out), _stream(stream)))
+        return depth_out, color_out, vertex_out
 
     def raycast(self, cam: Camera, R, t, depth_out=None, color_out=None, vertex_out=None,
                 want_vertex=False, stream=None):
@@ -416,6 +445,15 @@ def vertex_normals(cam: Camera, R, t, sdf_depth: torch.Tensor, vertex: torch.Ten
     return out
 
 
+def vertex_normals_dpose(cam: Camera, pose: torch.Tensor, sdf_depth: torch.Tensor, vertex: torch.Tensor, out,
+                         stream=None):
+    """gps_vertex_normals_dpose: the camera centre read from a device pose."""
+    N.check("gps_vertex_normals_dpose",
+            _L.gps_vertex_normals_dpose(C.byref(cam.c()), _dpose(pose), _ptr(sdf_depth), _ptr(vertex), _ptr(out),
+                                        _stream(stream)))
+    return out
+
+
 _ws_cache: dict = {}
 
 
@@ -475,11 +513,14 @@ class IcpConfig:
     depth_max: float = 10.0
     eps: float = 1e-6
     min_inlier_frac: float = 0.1
+    fallback: bool = True          # R-ICP-FAIL: a frame that does not converge keeps its initial pose
+    min_inlier_px_frac: float = 0.05  # R-ICP-FAIL: converged needs inliers >= this fraction of the pixels
 
     def c(self) -> N.gps_icp_config:
         it = list(self.iters) + [1] * (4 - len(self.iters))
         return N.gps_icp_config(self.levels, (C.c_int32 * 4)(*it), self.dist_max, self.angle_max_deg,
-                                self.depth_min, self.depth_max, self.eps, self.min_inlier_frac)
+                                self.depth_min, self.depth_max, self.eps, self.min_inlier_frac,
+                                int(self.fallback), self.min_inlier_px_frac)
 
 
 def track(cam: Camera, depth: torch.Tensor, depth_scale: float, model_vertex: torch.Tensor,
@@ -496,5 +537,46 @@ def track(cam: Camera, depth: torch.Tensor, depth_scale: float, model_vertex: to
                               C.byref(pose_struct(R_init, t_init)), C.byref(cfg.c()), _ptr(ws), ws.numel(),
                               C.byref(out), _stream(stream)))
     return {"R": np.array(out.R64[:], np.float64).reshape(3, 3), "t": np.array(out.t64[:], np.float64),
+            "T": (np.array(out.T.R[:], np.float32).reshape(3, 3), np.array(out.T.t[:], np.float32)),
+            "converged": bool(out.converged), "degenerate": bool(out.degenerate), "inlier_frac": out.inlier_frac,
+            "inliers": out.inliers, "steps": out.steps, "energy": out.energy}
+
+
+TRACK_RESULT_BYTES = C.sizeof(N.gps_track_result)
+
+
+def track_async(cam: Camera, depth: torch.Tensor, depth_scale: float, model_vertex: torch.Tensor,
+                model_normal: torch.Tensor, pose_model: torch.Tensor, pose_init: torch.Tensor, pose_out: torch.Tensor,
+                result_out: torch.Tensor | None = None, cfg: IcpConfig | None = None, stream=None, ws=None,
+                pose_fail: torch.Tensor | None = None):
+    """gps_track_async: ICP with every pose in device memory (pose_tensor layout) and no
+    synchronisation; result_out (nullable) is a u8[TRACK_RESULT_BYTES] device tensor that
+    receives the gps_track_result (decode with track_result())."""
+    cfg = cfg or IcpConfig()
+    if ws is None:
+        ws = _ws("track", _L.gps_track_workspace_size(C.byref(cam.c()), cfg.levels))
+    if result_out is not None:
+        assert result_out.is_cuda and result_out.numel() >= TRACK_RESULT_BYTES
+    N.check("gps_track_async",
+            _L.gps_track_async(C.byref(cam.c()), _ptr(depth), float(depth_scale), _ptr(model_vertex),
+                               _ptr(model_normal), _dpose(pose_model), _dpose(pose_init),
+                               None if pose_fail is None else _dpose(pose_fail), C.byref(cfg.c()), _ptr(ws),
+                               ws.numel(), _dpose(pose_out), _ptr(result_out), _stream(stream)))
+    return pose_out
+
+
+def pose_extrapolate(pose_a: torch.Tensor, pose_b: torch.Tensor, out: torch.Tensor, stream=None) -> torch.Tensor:
+    """gps_pose_extrapolate: out <- T_b (T_a^-1 T_b), the constant-velocity prediction (device)."""
+    N.check("gps_pose_extrapolate", _L.gps_pose_extrapolate(_dpose(pose_a), _dpose(pose_b), _dpose(out),
+                                                            _stream(stream)))
+    return out
+
+
+def track_result(raw) -> dict:
+    """Decode a gps_track_result copied to the host (bytes / u8 tensor) as track() returns it."""
+    b = bytes(raw.cpu().numpy().tobytes() if isinstance(raw, torch.Tensor) else raw)[:TRACK_RESULT_BYTES]
+    out = N.gps_track_result.from_buffer_copy(b)
+    return {"R": np.array(out.R64[:], np.float64).reshape(3, 3), "t": np.array(out.t64[:], np.float64),
+            "T": (np.array(out.T.R[:], np.float32).reshape(3, 3), np.array(out.T.t[:], np.float32)),
             "converged": bool(out.converged), "degenerate": bool(out.degenerate), "inlier_frac": out.inlier_frac,
             "inliers": out.inliers, "steps": out.steps, "energy": out.energy}

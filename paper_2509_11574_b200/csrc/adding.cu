@@ -48,8 +48,14 @@ uint32_t hash32_host(uint32_t x) {
 
 // ---- normals (R-NORMAL) ----------------------------------------------------------------------
 __global__ void k_vertex_normals(int W, int H, const float* __restrict__ depth, const float* __restrict__ V,
-                                 float cx, float cy, float cz, float* __restrict__ N) {
+                                 float cx, float cy, float cz, float* __restrict__ N,
+                                 const float* __restrict__ dpose = nullptr) {
   const int u = blockIdx.x * 16 + (threadIdx.x & 15), v = blockIdx.y * 16 + (threadIdx.x >> 4);
+  if (dpose) {  // camera centre t from a device pose (gps_vertex_normals_dpose)
+    cx = __ldg(dpose + 9);
+    cy = __ldg(dpose + 10);
+    cz = __ldg(dpose + 11);
+  }
   if (u >= W || v >= H) return;
   const size_t p = (size_t)v * W + u;
   float n0 = 0.f, n1 = 0.f, n2 = 0.f;
@@ -438,6 +444,17 @@ gps_status gps_vertex_normals(const gps_intrinsics* K, const gps_pose* T, const 
   dim3 grid((K->width + 15) / 16, (K->height + 15) / 16);
   k_vertex_normals<<<grid, 256, 0, as_stream(stream)>>>(K->width, K->height, sdf_depth, vertex, T->t[0], T->t[1],
                                                         T->t[2], normal_out);
+  GPS_CHECK_LAUNCH("k_vertex_normals");
+  return GPS_OK;
+}
+
+gps_status gps_vertex_normals_dpose(const gps_intrinsics* K, const gps_pose* T_dev, const float* sdf_depth,
+                                    const float* vertex, float* normal_out, gps_stream_t stream) {
+  if (!K || !T_dev || !sdf_depth || !vertex || !normal_out || K->width <= 0 || K->height <= 0)
+    return invalid("gps_vertex_normals_dpose: bad argument");
+  dim3 grid((K->width + 15) / 16, (K->height + 15) / 16);
+  k_vertex_normals<<<grid, 256, 0, as_stream(stream)>>>(K->width, K->height, sdf_depth, vertex, 0.f, 0.f, 0.f,
+                                                        normal_out, reinterpret_cast<const float*>(T_dev));
   GPS_CHECK_LAUNCH("k_vertex_normals");
   return GPS_OK;
 }

@@ -9,14 +9,16 @@
 // Per frame:  k_icp_depth (u16 -> metres, level 0) -> k_icp_down (levels 1..L-1)
 // per level:  k_icp_maps  (vertex + normal maps of the current frame, camera frame; resets the
 //                          level's stop flag)
-// per step:   k_icp_reduce (per pixel: association, gates, residual and Jacobian; the 27 sums of
-//                          J^T J, J^T r, r^2 and the inlier count per CTA, in double)
-//             k_icp_solve  (one CTA: total the CTA sums, Cholesky-solve the 6x6 system, update the
-//                          pose in device memory -- no host round trip between steps)
-// The pose is read back once, at the end.
+// per step:   k_icp_step   (per pixel: association, gates, residual and Jacobian; the 27 sums of
+//                          J^T J, J^T r, r^2 and the inlier count per CTA, in double; the last CTA
+//                          totals the CTA sums, Cholesky-solves the 6x6 system and updates the pose
+//                          in device memory -- one launch per step, no host round trip)
+// k_icp_init / k_icp_export move the poses in and out: gps_track_sync reads the result back once,
+// gps_track_async leaves it in device memory for gps_fuse_dpose / gps_raycast_dpose.
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <string>
 
@@ -33,8 +35,19 @@ struct DevPose {
   double R[9], t[3];
   double energy;
   int32_t steps, inliers, valid, degenerate;
-  int32_t stop;  // this level is done (converged or degenerate)
-  int32_t pad;
+  int32_t stop;    // this level is done (converged or degenerate)
+  uint32_t ticket; // CTAs of the current k_icp_step that have written their sums
+  float Rp[9], tp[3];  // the camera the model maps were raycast from (camera -> world)
+  gps_pose fail;       // the pose of a frame that does not converge (R-ICP-FAIL): T_fail, else T_init
+};
+
+// the initial, model and failure poses, by value (gps_track_sync) or from device memory
+// (gps_track_async)
+struct PoseSrc {
+  gps_pose init, model;
+  const gps_pose* dinit;
+  const gps_pose* dmodel;
+  const gps_pose* dfail;
 };
 
 struct Level {
@@ -103,24 +116,106 @@ __global__ void k_icp_maps(Level L, DevPose* pose) {
   L.N[3 * p] = N[0]; L.N[3 * p + 1] = N[1]; L.N[3 * p + 2] = N[2];
 }
 
+__global__ void k_icp_init(PoseSrc src, DevPose* pose) {
+  const gps_pose in = src.dinit ? *src.dinit : src.init;
+  const gps_pose mo = src.dmodel ? *src.dmodel : src.model;
+  DevPose d{};
+  for (int e = 0; e < 9; ++e) d.R[e] = in.R[e];
+  for (int e = 0; e < 3; ++e) d.t[e] = in.t[e];
+  for (int e = 0; e < 9; ++e) d.Rp[e] = mo.R[e];
+  for (int e = 0; e < 3; ++e) d.tp[e] = mo.t[e];
+  d.fail = src.dfail ? *src.dfail : in;
+  *pose = d;
+}
+
+// T_out = T_b (T_a^-1 T_b): R = R_b R_a^T R_b, t = R_b R_a^T (t_b - t_a) + t_b, in double, with R
+// re-orthonormalised (Gram-Schmidt on the rows).  Without it the fp32 inputs' departures from
+// orthonormality add up through R_a^T (not R_a^-1 for a non-orthonormal R_a) and grow by ~(1+sqrt 2)
+// per chained prediction.
+__global__ void k_pose_extrapolate(const gps_pose* __restrict__ a, const gps_pose* __restrict__ b, gps_pose* out) {
+  const gps_pose A = *a, B = *b;
+  double Rd[9], td[3], R[9], t[3];
+  for (int r = 0; r < 3; ++r) {
+    for (int c = 0; c < 3; ++c)
+      Rd[3 * r + c] = (double)A.R[r] * B.R[c] + (double)A.R[3 + r] * B.R[3 + c] + (double)A.R[6 + r] * B.R[6 + c];
+    td[r] = (double)A.R[r] * ((double)B.t[0] - A.t[0]) + (double)A.R[3 + r] * ((double)B.t[1] - A.t[1]) +
+            (double)A.R[6 + r] * ((double)B.t[2] - A.t[2]);
+  }
+  for (int r = 0; r < 3; ++r) {
+    for (int c = 0; c < 3; ++c)
+      R[3 * r + c] = (double)B.R[3 * r] * Rd[c] + (double)B.R[3 * r + 1] * Rd[3 + c] + (double)B.R[3 * r + 2] * Rd[6 + c];
+    t[r] = (double)B.R[3 * r] * td[0] + (double)B.R[3 * r + 1] * td[1] + (double)B.R[3 * r + 2] * td[2] + B.t[r];
+  }
+  double* r0 = R;
+  double* r1 = R + 3;
+  double* r2 = R + 6;
+  double n = sqrt(r0[0] * r0[0] + r0[1] * r0[1] + r0[2] * r0[2]);
+  for (int k = 0; k < 3; ++k) r0[k] /= n;
+  const double d = r0[0] * r1[0] + r0[1] * r1[1] + r0[2] * r1[2];
+  for (int k = 0; k < 3; ++k) r1[k] -= d * r0[k];
+  n = sqrt(r1[0] * r1[0] + r1[1] * r1[1] + r1[2] * r1[2]);
+  for (int k = 0; k < 3; ++k) r1[k] /= n;
+  r2[0] = r0[1] * r1[2] - r0[2] * r1[1];
+  r2[1] = r0[2] * r1[0] - r0[0] * r1[2];
+  r2[2] = r0[0] * r1[1] - r0[1] * r1[0];
+  gps_pose o;
+  for (int e = 0; e < 9; ++e) o.R[e] = (float)R[e];
+  for (int e = 0; e < 3; ++e) o.t[e] = (float)t[e];
+  *out = o;
+}
+
+// the tracked pose (fp32, as gps_track_sync rounds it) and, optionally, the whole result
+__global__ void k_icp_export(const DevPose* __restrict__ pose, float min_inlier_frac, double min_inliers, int fallback,
+                             gps_pose* out, gps_track_result* res) {
+  const DevPose d = *pose;
+  gps_track_result r{};
+  for (int e = 0; e < 9; ++e) r.T.R[e] = (float)d.R[e];
+  for (int e = 0; e < 3; ++e) r.T.t[e] = (float)d.t[e];
+  for (int e = 0; e < 9; ++e) r.R64[e] = d.R[e];
+  for (int e = 0; e < 3; ++e) r.t64[e] = d.t[e];
+  r.energy = d.energy;
+  r.inliers = d.inliers;
+  r.valid = d.valid;
+  r.steps = d.steps;
+  r.degenerate = d.degenerate;
+  r.inlier_frac = d.valid > 0 ? (float)d.inliers / (float)d.valid : 0.f;
+  r.converged = !d.degenerate && r.inlier_frac >= min_inlier_frac && (double)d.inliers >= min_inliers;
+  if (fallback && !r.converged) r.T = d.fail;  // R-ICP-FAIL
+  if (out) *out = r.T;
+  if (res) *res = r;
+}
+
 struct Assoc {
   const float* mV;  // full-resolution model maps (world)
   const float* mN;
   int mW, mH;       // full resolution
-  float Rp[9], tp[3];  // the camera the model maps were raycast from (camera -> world)
   float dist_max, cos_max;
+  double eps;       // convergence threshold on |xi|
 };
 
-// R-ICP-ASSOC / R-ICP-GATE / R-ICP-GN for one pixel: J = [m, p x m], r = (p - q) . m
-__global__ void __launch_bounds__(kIcpThreads) k_icp_reduce(Level L, Assoc a, const DevPose* __restrict__ pose,
-                                                            double* partial) {
+__device__ void icp_solve_cta(const double* partial, int nblk, DevPose* pose, double eps);
+
+// One Gauss-Newton step.  Every CTA: R-ICP-ASSOC / R-ICP-GATE / R-ICP-GN per pixel (J = [m, p x m],
+// r = (p - q) . m) and the CTA's sums; the last CTA to finish totals them and solves
+// (icp_solve_cta), so a step is one launch.
+__global__ void __launch_bounds__(kIcpThreads, 3) k_icp_step(Level L, Assoc a, DevPose* pose, double* partial) {
   __shared__ double red[kIcpThreads / 32][kIcpSums];
+  __shared__ bool last;
+  // the current pose (fp32) and the model camera, broadcast from shared memory
+  __shared__ float sR[9], st[3], sRp[9], stp[3];
   if (pose->stop) return;  // uniform: the level is done
-  float R[9], t[3];
-#pragma unroll
-  for (int k = 0; k < 9; ++k) R[k] = (float)pose->R[k];
-#pragma unroll
-  for (int k = 0; k < 3; ++k) t[k] = (float)pose->t[k];
+  if (threadIdx.x < 9) {
+    sR[threadIdx.x] = (float)pose->R[threadIdx.x];
+    sRp[threadIdx.x] = pose->Rp[threadIdx.x];
+  } else if (threadIdx.x < 12) {
+    st[threadIdx.x - 9] = (float)pose->t[threadIdx.x - 9];
+    stp[threadIdx.x - 9] = pose->tp[threadIdx.x - 9];
+  }
+  __syncthreads();
+  const float* R = sR;
+  const float* t = st;
+  const float* Rp = sRp;
+  const float* tp = stp;
   const int Lw = a.mW / L.stride, Lh = a.mH / L.stride;  // this level's model-map size
   float s[kIcpSums];
 #pragma unroll
@@ -138,10 +233,10 @@ __global__ void __launch_bounds__(kIcpThreads) k_icp_reduce(Level L, Assoc a, co
         p[r] = R[3 * r] * Vc[0] + R[3 * r + 1] * Vc[1] + R[3 * r + 2] * Vc[2] + t[r];
         nn[r] = R[3 * r] * Nc[0] + R[3 * r + 1] * Nc[1] + R[3 * r + 2] * Nc[2];
       }
-      const float d0 = p[0] - a.tp[0], d1 = p[1] - a.tp[1], d2 = p[2] - a.tp[2];
-      const float x0 = a.Rp[0] * d0 + a.Rp[3] * d1 + a.Rp[6] * d2;
-      const float x1 = a.Rp[1] * d0 + a.Rp[4] * d1 + a.Rp[7] * d2;
-      const float x2 = a.Rp[2] * d0 + a.Rp[5] * d1 + a.Rp[8] * d2;
+      const float d0 = p[0] - tp[0], d1 = p[1] - tp[1], d2 = p[2] - tp[2];
+      const float x0 = Rp[0] * d0 + Rp[3] * d1 + Rp[6] * d2;
+      const float x1 = Rp[1] * d0 + Rp[4] * d1 + Rp[7] * d2;
+      const float x2 = Rp[2] * d0 + Rp[5] * d1 + Rp[8] * d2;
       if (x2 > 1e-9f) {
         const float uf = floorf(L.fx * x0 / x2 + L.cx + 0.5f), vf = floorf(L.fy * x1 / x2 + L.cy + 0.5f);
         if (uf >= 0.f && uf <= (float)(Lw - 1) && vf >= 0.f && vf <= (float)(Lh - 1)) {
@@ -190,19 +285,26 @@ __global__ void __launch_bounds__(kIcpThreads) k_icp_reduce(Level L, Assoc a, co
     for (int j = 0; j < kIcpThreads / 32; ++j) cv += svalid[j];
     partial[(size_t)blockIdx.x * 32 + 29] = (double)cv;
   }
+  // last-CTA election: the sums are visible device-wide before the ticket is taken
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(&pose->ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  icp_solve_cta(partial, gridDim.x, pose, a.eps);
+  if (threadIdx.x == 0) pose->ticket = 0;  // for the next step (stream-ordered)
 }
 
-// one CTA: total the CTA sums, solve A xi = -b (Cholesky), pose <- exp(xi) pose
-__global__ void __launch_bounds__(256) k_icp_solve(const double* __restrict__ partial, int nblk, DevPose* pose,
-                                                   double eps) {
+// one CTA (256 threads): total the CTA sums, solve A xi = -b (Cholesky), pose <- exp(xi) pose
+__device__ void icp_solve_cta(const double* partial, int nblk, DevPose* pose, double eps) {
   __shared__ double tot[32];
   __shared__ double part[8][32];
-  if (pose->stop) return;
   {  // 30 sums x 8 interleaved chunks of the CTA partials, then the 8 chunks per sum
     const int v = threadIdx.x & 31, c = threadIdx.x >> 5;
     double x = 0.0;
     if (v < 30)
-      for (int b = c; b < nblk; b += 8) x += partial[(size_t)b * 32 + v];
+      for (int b = c; b < nblk; b += 8) x += __ldcg(partial + (size_t)b * 32 + v);
     part[c][v] = x;
     __syncthreads();
     if (threadIdx.x < 30) {
@@ -314,30 +416,31 @@ size_t gps_track_workspace_size(const gps_intrinsics* K, int32_t levels) {
   return track_layout(K->width, K->height, levels).total;
 }
 
-gps_status gps_track_sync(const gps_intrinsics* K, const uint16_t* depth, float depth_scale, const float* model_vertex,
-                          const float* model_normal, const gps_pose* T_model, const gps_pose* T_init,
-                          const gps_icp_config* cfg, void* ws, size_t ws_bytes, gps_track_result* out,
-                          gps_stream_t stream) {
-  if (!K || !depth || !model_vertex || !model_normal || !T_model || !T_init || !cfg || !ws || !out)
-    return invalid("gps_track_sync: null argument");
-  if (K->width <= 0 || K->height <= 0 || !(depth_scale > 0)) return invalid("gps_track_sync: bad intrinsics");
-  if (cfg->levels < 1 || cfg->levels > kIcpMaxLevels || !(cfg->dist_max > 0) || !(cfg->depth_max > cfg->depth_min))
-    return invalid("gps_track_sync: bad config");
+}  // extern "C"
+
+static gps_status track_impl(const gps_intrinsics* K, const uint16_t* depth, float depth_scale,
+                             const float* model_vertex, const float* model_normal, const PoseSrc& src,
+                             const gps_icp_config* cfg, void* ws, size_t ws_bytes, gps_pose* out_pose,
+                             gps_track_result* out_res, gps_stream_t stream, const char* who) {
+  const std::string w_(who);
+  if (!K || !depth || !model_vertex || !model_normal || !cfg || !ws) return invalid(w_ + ": null argument");
+  if (K->width <= 0 || K->height <= 0 || !(depth_scale > 0)) return invalid(w_ + ": bad intrinsics");
+  if (cfg->levels < 1 || cfg->levels > kIcpMaxLevels || !(cfg->dist_max > 0) || !(cfg->depth_max > cfg->depth_min) ||
+      cfg->fallback < 0 || cfg->fallback > 1 || !(cfg->min_inlier_px_frac >= 0.f && cfg->min_inlier_px_frac <= 1.f))
+    return invalid(w_ + ": bad config");
   for (int l = 0; l < cfg->levels; ++l)
-    if (cfg->iters[l] < 1 || (K->width >> l) < 3 || (K->height >> l) < 3) return invalid("gps_track_sync: bad level");
-  if ((reinterpret_cast<uintptr_t>(depth) & 1u) != 0) return invalid("gps_track_sync: depth must be 2-byte aligned");
+    if (cfg->iters[l] < 1 || (K->width >> l) < 3 || (K->height >> l) < 3) return invalid(w_ + ": bad level");
+  if ((reinterpret_cast<uintptr_t>(depth) & 1u) != 0) return invalid(w_ + ": depth must be 2-byte aligned");
   const TrackLayout Lw = track_layout(K->width, K->height, cfg->levels);
   if (ws_bytes < Lw.total) {
-    set_error("gps_track_sync: workspace too small");
+    set_error(w_ + ": workspace too small");
     return GPS_ERR_WORKSPACE_TOO_SMALL;
   }
   cudaStream_t s = as_stream(stream);
   char* w = static_cast<char*>(ws);
-  DevPose hp{};
-  for (int e = 0; e < 9; ++e) hp.R[e] = T_init->R[e];
-  for (int e = 0; e < 3; ++e) hp.t[e] = T_init->t[e];
   DevPose* dp = reinterpret_cast<DevPose*>(w + Lw.pose);
-  GPS_CHECK_CUDA(cudaMemcpyAsync(dp, &hp, sizeof(hp), cudaMemcpyHostToDevice, s));
+  k_icp_init<<<1, 1, 0, s>>>(src, dp);
+  GPS_CHECK_LAUNCH("k_icp_init");
   const int n0 = K->width * K->height;
   k_icp_depth<<<(n0 + 255) / 256, 256, 0, s>>>(depth, n0, 1.0f / depth_scale, cfg->depth_min, cfg->depth_max,
                                                reinterpret_cast<float*>(w + Lw.depth[0]));
@@ -354,10 +457,9 @@ gps_status gps_track_sync(const gps_intrinsics* K, const uint16_t* depth, float 
   a.mN = model_normal;
   a.mW = K->width;
   a.mH = K->height;
-  for (int e = 0; e < 9; ++e) a.Rp[e] = T_model->R[e];
-  for (int e = 0; e < 3; ++e) a.tp[e] = T_model->t[e];
   a.dist_max = cfg->dist_max;
   a.cos_max = (float)std::cos((double)cfg->angle_max_deg * M_PI / 180.0);
+  a.eps = (double)cfg->eps;
   double* partial = reinterpret_cast<double*>(w + Lw.partial);
   for (int l = cfg->levels - 1; l >= 0; --l) {  // coarse -> fine
     Level L;
@@ -374,28 +476,62 @@ gps_status gps_track_sync(const gps_intrinsics* K, const uint16_t* depth, float 
     L.stride = 1 << l;
     k_icp_maps<<<dim3((L.W + 15) / 16, (L.H + 15) / 16), 256, 0, s>>>(L, dp);
     GPS_CHECK_LAUNCH("k_icp_maps");
-    const int nblk = std::min((L.W * L.H + kIcpThreads - 1) / kIcpThreads, 148 * 4);  // grid-stride
+    static const int ctas = getenv("GPS_ICP_CTAS") ? atoi(getenv("GPS_ICP_CTAS")) : 148 * 3;
+    const int nblk = std::min((L.W * L.H + kIcpThreads - 1) / kIcpThreads, ctas);  // grid-stride, one wave at 3 CTAs/SM
     for (int it = 0; it < cfg->iters[l]; ++it) {
-      k_icp_reduce<<<nblk, kIcpThreads, 0, s>>>(L, a, dp, partial);
-      GPS_CHECK_LAUNCH("k_icp_reduce");
-      k_icp_solve<<<1, 256, 0, s>>>(partial, nblk, dp, (double)cfg->eps);
-      GPS_CHECK_LAUNCH("k_icp_solve");
+      k_icp_step<<<nblk, kIcpThreads, 0, s>>>(L, a, dp, partial);
+      GPS_CHECK_LAUNCH("k_icp_step");
     }
   }
-  GPS_CHECK_CUDA(cudaMemcpyAsync(&hp, dp, sizeof(hp), cudaMemcpyDeviceToHost, s));
-  GPS_CHECK_CUDA(cudaStreamSynchronize(s));
-  for (int e = 0; e < 9; ++e) out->T.R[e] = (float)hp.R[e];
-  for (int e = 0; e < 3; ++e) out->T.t[e] = (float)hp.t[e];
-  for (int e = 0; e < 9; ++e) out->R64[e] = hp.R[e];
-  for (int e = 0; e < 3; ++e) out->t64[e] = hp.t[e];
-  out->energy = hp.energy;
-  out->inliers = hp.inliers;
-  out->valid = hp.valid;
-  out->steps = hp.steps;
-  out->degenerate = hp.degenerate;
-  out->inlier_frac = hp.valid > 0 ? (float)hp.inliers / (float)hp.valid : 0.f;
-  out->converged = !hp.degenerate && out->inlier_frac >= cfg->min_inlier_frac;
+  k_icp_export<<<1, 1, 0, s>>>(dp, cfg->min_inlier_frac,
+                               (double)cfg->min_inlier_px_frac * (double)K->width * (double)K->height, cfg->fallback,
+                               out_pose, out_res);
+  GPS_CHECK_LAUNCH("k_icp_export");
   return GPS_OK;
+}
+
+extern "C" {
+
+gps_status gps_track_sync(const gps_intrinsics* K, const uint16_t* depth, float depth_scale, const float* model_vertex,
+                          const float* model_normal, const gps_pose* T_model, const gps_pose* T_init,
+                          const gps_icp_config* cfg, void* ws, size_t ws_bytes, gps_track_result* out,
+                          gps_stream_t stream) {
+  if (!T_model || !T_init || !out) return invalid("gps_track_sync: null argument");
+  PoseSrc src{};
+  src.init = *T_init;
+  src.model = *T_model;
+  gps_track_result* dres = nullptr;
+  cudaStream_t s = as_stream(stream);
+  GPS_CHECK_CUDA(cudaMallocAsync(&dres, sizeof(gps_track_result), s));
+  gps_status st = track_impl(K, depth, depth_scale, model_vertex, model_normal, src, cfg, ws, ws_bytes, nullptr,
+                             dres, stream, "gps_track_sync");
+  if (st == GPS_OK) GPS_CHECK_CUDA(cudaMemcpyAsync(out, dres, sizeof(*out), cudaMemcpyDeviceToHost, s));
+  GPS_CHECK_CUDA(cudaFreeAsync(dres, s));
+  GPS_CHECK_CUDA(cudaStreamSynchronize(s));
+  return st;
+}
+
+gps_status gps_pose_extrapolate(const gps_pose* T_a_dev, const gps_pose* T_b_dev, gps_pose* T_out_dev,
+                                gps_stream_t stream) {
+  if (!T_a_dev || !T_b_dev || !T_out_dev) return invalid("gps_pose_extrapolate: null argument");
+  if (T_out_dev == T_a_dev || T_out_dev == T_b_dev) return invalid("gps_pose_extrapolate: output aliases an input");
+  k_pose_extrapolate<<<1, 1, 0, as_stream(stream)>>>(T_a_dev, T_b_dev, T_out_dev);
+  GPS_CHECK_LAUNCH("k_pose_extrapolate");
+  return GPS_OK;
+}
+
+gps_status gps_track_async(const gps_intrinsics* K, const uint16_t* depth, float depth_scale,
+                           const float* model_vertex, const float* model_normal, const gps_pose* T_model_dev,
+                           const gps_pose* T_init_dev, const gps_pose* T_fail_dev, const gps_icp_config* cfg,
+                           void* ws, size_t ws_bytes, gps_pose* T_out_dev, gps_track_result* result_dev,
+                           gps_stream_t stream) {
+  if (!T_model_dev || !T_init_dev || !T_out_dev) return invalid("gps_track_async: null argument");
+  PoseSrc src{};
+  src.dinit = T_init_dev;
+  src.dmodel = T_model_dev;
+  src.dfail = T_fail_dev;
+  return track_impl(K, depth, depth_scale, model_vertex, model_normal, src, cfg, ws, ws_bytes, T_out_dev, result_dev,
+                    stream, "gps_track_async");
 }
 
 }  // extern "C"

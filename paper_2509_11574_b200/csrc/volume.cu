@@ -33,7 +33,20 @@ struct FuseParams {
   float scale, mu, voxel, bs, dmin, dmax;
   float inv_scale, inv_mu;  // fl(1/depth_scale), fl(1/mu): host fp32 divisions
   int wmax;
+  const float* dpose;  // device pose (R row-major, t) for the *_dpose entry points, else null
 };
+
+// the device-pose instantiations read R, t from device memory once per thread (the same fp32
+// values the host would pass, so every prescribed sequence is unchanged)
+template <bool DPOSE, class P>
+__device__ __forceinline__ void apply_dpose(P& p) {
+  if (DPOSE) {
+#pragma unroll
+    for (int k = 0; k < 9; ++k) p.R[k] = __ldg(p.dpose + k);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) p.t[k] = __ldg(p.dpose + 9 + k);
+  }
+}
 
 __device__ __forceinline__ void mark_visible(const VolumeView& v, uint32_t slot, uint32_t frame,
                                              uint32_t* d_flag) {
@@ -184,9 +197,12 @@ __device__ __forceinline__ void pixel_blocks(const FuseParams& p, int u, int vv,
   }
 }
 
-__global__ void __launch_bounds__(256) k_alloc(VolumeView v, FuseParams p,
+template <bool DPOSE = false>
+__global__ void __launch_bounds__(256) k_alloc(VolumeView v, FuseParams p_in,
                                                const uint16_t* __restrict__ depth, uint32_t frame,
                                                uint32_t* d_flag) {
+  FuseParams p = p_in;
+  apply_dpose<DPOSE>(p);
   __shared__ unsigned long long set[kSmemSet];
   for (int i = threadIdx.x; i < kSmemSet; i += blockDim.x) set[i] = kEmptyKey;
   __syncthreads();
@@ -298,9 +314,12 @@ __device__ __forceinline__ uint2 voxel_update(float tsdf, uint32_t cw, float s, 
 // Grid-stride over the visible list, software-pipelined two deep: the slot of block q + 2G and
 // the pool index, key and -neighbour row of block q + G are loaded while block q is integrated
 // (G = gridDim.x), so no dependent metadata load is waited for inside the loop.
-__global__ void __launch_bounds__(256) k_integrate(VolumeView v, FuseParams p,
+template <bool DPOSE = false>
+__global__ void __launch_bounds__(256) k_integrate(VolumeView v, FuseParams p_in,
                                                    const uint16_t* __restrict__ depth,
                                                    const uint32_t* __restrict__ rgba) {
+  FuseParams p = p_in;
+  apply_dpose<DPOSE>(p);
   __shared__ uint32_t smagic[256];
   __shared__ float srcp[256];
   // smagic[w] = ceil(2^32 / (w+1)) for w >= 1 (w = 0 is special-cased in voxel_update)
@@ -514,6 +533,7 @@ struct RayParams {
   float voxel, inv_voxel, dmin;
   float zc;  // smallest camera z of any ray sample: dmin * min over pixels of the unit ray's z
   int J;  // last grid index
+  const float* dpose;  // device pose for gps_raycast_dpose, else null
 };
 
 // --------------------------------------------------------------------------------------------
@@ -531,8 +551,11 @@ __device__ __forceinline__ void block_tile_range(const VolumeView& v, const RayP
                                                  int tiles_y, int& otx0, int& otx1, int& oty0, int& oty1,
                                                  uint32_t& oa0, uint32_t& oa1);
 
-__global__ void __launch_bounds__(256) k_range(VolumeView v, RayParams p, uint32_t* tmin, uint32_t* tmax,
+template <bool DPOSE = false>
+__global__ void __launch_bounds__(256) k_range(VolumeView v, RayParams p_in, uint32_t* tmin, uint32_t* tmax,
                                                int tiles_x, int tiles_y) {
+  RayParams p = p_in;
+  apply_dpose<DPOSE>(p);
   const uint32_t nb = min(*(volatile uint32_t*)&v.ctr->n_blocks, v.max_blocks);
   const uint32_t stride = gridDim.x * blockDim.x;
   const int lane = threadIdx.x & 31;
@@ -732,13 +755,15 @@ __device__ __forceinline__ bool trilinear_color(const VolumeView& v, BlockCache&
 
 // kDebug: 0 = production; 1 = per-pixel march statistics in vertex_out; 2 = mark every tsdf voxel
 // the march reads in `footprint` (the raycast roofline's unique-voxel count)
-template <int kDebug, int kMinCtas = 6>
-__global__ void __launch_bounds__(128, 2 * kMinCtas) k_raycast(VolumeView v, RayParams p, float* __restrict__ depth_out,
+template <int kDebug, int kMinCtas = 6, bool DPOSE = false>
+__global__ void __launch_bounds__(128, 2 * kMinCtas) k_raycast(VolumeView v, RayParams p_in, float* __restrict__ depth_out,
                                                  float* __restrict__ color_out,
                                                  float* __restrict__ vertex_out,
                                                  const uint32_t* __restrict__ tmin,
                                                  const uint32_t* __restrict__ tmax,
                                                  uint32_t* footprint = nullptr) {
+  RayParams p = p_in;
+  apply_dpose<DPOSE>(p);
   // CTA = 16x8 pixels (128 threads: a small register footprint that co-schedules with the
   // refinement stream's kernels); two CTAs per 16x16 range tile
   const int u = blockIdx.x * 16 + (threadIdx.x & 15);
@@ -1163,21 +1188,24 @@ gps_status gps_volume_stats_sync(gps_volume* vol, gps_stream_t stream, int64_t* 
   return GPS_OK;
 }
 
-gps_status gps_fuse(gps_volume* vol, const gps_intrinsics* K, const gps_pose* T, const uint16_t* depth,
-                    float depth_scale, const uint8_t* rgba, gps_stream_t stream) {
-  if (!vol || !T || !depth || !rgba) return invalid("gps_fuse: null argument");
-  if (!valid_intrinsics(K)) return invalid("gps_fuse: bad intrinsics");
-  if (!(depth_scale > 0)) return invalid("gps_fuse: depth_scale must be > 0");
-  if ((reinterpret_cast<uintptr_t>(rgba) & 3u) != 0) return invalid("gps_fuse: rgba must be 4-byte aligned");
-  if ((reinterpret_cast<uintptr_t>(depth) & 1u) != 0) return invalid("gps_fuse: depth must be 2-byte aligned");
+static gps_status fuse_impl(gps_volume* vol, const gps_intrinsics* K, const gps_pose* T, const gps_pose* dT,
+                            const uint16_t* depth, float depth_scale, const uint8_t* rgba, gps_stream_t stream,
+                            const char* who) {
+  if (!vol || !(T || dT) || !depth || !rgba) return invalid(std::string(who) + ": null argument");
+  if (!valid_intrinsics(K)) return invalid(std::string(who) + ": bad intrinsics");
+  if (!(depth_scale > 0)) return invalid(std::string(who) + ": depth_scale must be > 0");
+  if ((reinterpret_cast<uintptr_t>(rgba) & 3u) != 0) return invalid(std::string(who) + ": rgba must be 4-byte aligned");
+  if ((reinterpret_cast<uintptr_t>(depth) & 1u) != 0) return invalid(std::string(who) + ": depth must be 2-byte aligned");
+  if (dT && (reinterpret_cast<uintptr_t>(dT) & 3u) != 0) return invalid(std::string(who) + ": pose must be 4-byte aligned");
   gps_status st = check_sticky(vol);
   if (st != GPS_OK) return st;
   VolumeImpl* v = static_cast<VolumeImpl*>(vol);
   cudaStream_t s = as_stream(stream);
   FuseParams p;
   p.fx = K->fx; p.fy = K->fy; p.cx = K->cx; p.cy = K->cy; p.W = K->width; p.H = K->height;
-  for (int i = 0; i < 9; ++i) p.R[i] = T->R[i];
-  for (int i = 0; i < 3; ++i) p.t[i] = T->t[i];
+  for (int i = 0; i < 9; ++i) p.R[i] = T ? T->R[i] : 0.f;
+  for (int i = 0; i < 3; ++i) p.t[i] = T ? T->t[i] : 0.f;
+  p.dpose = dT ? reinterpret_cast<const float*>(dT) : nullptr;
   p.scale = depth_scale;
   p.mu = v->cfg.mu;
   p.inv_scale = 1.0f / depth_scale;
@@ -1193,7 +1221,10 @@ gps_status gps_fuse(gps_volume* vol, const gps_intrinsics* K, const gps_pose* T,
   dim3 ga((p.W + kAllocPatch - 1) / kAllocPatch, (p.H + kAllocPatch - 1) / kAllocPatch);
   {
     GPS_PROF(K_ALLOC, s);
-    k_alloc<<<ga, 256, 0, s>>>(v->view, p, depth, frame, v->flag.dev);
+    if (dT)
+      k_alloc<true><<<ga, 256, 0, s>>>(v->view, p, depth, frame, v->flag.dev);
+    else
+      k_alloc<<<ga, 256, 0, s>>>(v->view, p, depth, frame, v->flag.dev);
   }
   GPS_CHECK_LAUNCH("k_alloc");
   {
@@ -1204,19 +1235,36 @@ gps_status gps_fuse(gps_volume* vol, const gps_intrinsics* K, const gps_pose* T,
   // persistent-style grid: 148 SMs x 8 resident 256-thread CTAs, striding over the visible list
   {
     GPS_PROF(K_INTEGRATE, s);
-    k_integrate<<<148 * 8, 256, 0, s>>>(v->view, p, depth, reinterpret_cast<const uint32_t*>(rgba));
+    if (dT)
+      k_integrate<true><<<148 * 8, 256, 0, s>>>(v->view, p, depth, reinterpret_cast<const uint32_t*>(rgba));
+    else
+      k_integrate<<<148 * 8, 256, 0, s>>>(v->view, p, depth, reinterpret_cast<const uint32_t*>(rgba));
   }
   GPS_CHECK_LAUNCH("k_integrate");
   return GPS_OK;
 }
 
+gps_status gps_fuse(gps_volume* vol, const gps_intrinsics* K, const gps_pose* T, const uint16_t* depth,
+                    float depth_scale, const uint8_t* rgba, gps_stream_t stream) {
+  if (!T) return invalid("gps_fuse: null argument");
+  return fuse_impl(vol, K, T, nullptr, depth, depth_scale, rgba, stream, "gps_fuse");
+}
+
+gps_status gps_fuse_dpose(gps_volume* vol, const gps_intrinsics* K, const gps_pose* T_dev, const uint16_t* depth,
+                          float depth_scale, const uint8_t* rgba, gps_stream_t stream) {
+  if (!T_dev) return invalid("gps_fuse_dpose: null argument");
+  return fuse_impl(vol, K, nullptr, T_dev, depth, depth_scale, rgba, stream, "gps_fuse_dpose");
+}
+
 static gps_status raycast_impl(const gps_volume* vol, const gps_intrinsics* K, const gps_pose* T, float* depth_out,
-                               float* color_out, float* vertex_out, uint32_t* footprint, gps_stream_t stream) {
+                               float* color_out, float* vertex_out, uint32_t* footprint, gps_stream_t stream,
+                               const gps_pose* dT = nullptr) {
   const VolumeImpl* v = static_cast<const VolumeImpl*>(vol);
   RayParams p;
   p.fx = K->fx; p.fy = K->fy; p.cx = K->cx; p.cy = K->cy; p.W = K->width; p.H = K->height;
-  for (int i = 0; i < 9; ++i) p.R[i] = T->R[i];
-  for (int i = 0; i < 3; ++i) p.t[i] = T->t[i];
+  for (int i = 0; i < 9; ++i) p.R[i] = T ? T->R[i] : 0.f;
+  for (int i = 0; i < 3; ++i) p.t[i] = T ? T->t[i] : 0.f;
+  p.dpose = dT ? reinterpret_cast<const float*>(dT) : nullptr;
   p.voxel = v->cfg.voxel_size;
   p.inv_voxel = 1.0f / v->cfg.voxel_size;
   p.dmin = v->cfg.depth_min;
@@ -1240,7 +1288,10 @@ static gps_status raycast_impl(const gps_volume* vol, const gps_intrinsics* K, c
     GPS_CHECK_CUDA(cudaMemsetAsync(tmax, 0x00, sizeof(uint32_t) * ntiles, s));
     {
       GPS_PROF(K_RANGE, s);
-      k_range<<<148 * 4, 256, 0, s>>>(v->view, p, tmin, tmax, (int)g.x, (int)g.y);
+      if (dT)
+        k_range<true><<<148 * 4, 256, 0, s>>>(v->view, p, tmin, tmax, (int)g.x, (int)g.y);
+      else
+        k_range<<<148 * 4, 256, 0, s>>>(v->view, p, tmin, tmax, (int)g.x, (int)g.y);
     }
     GPS_CHECK_LAUNCH("k_range");
   }
@@ -1249,8 +1300,10 @@ static gps_status raycast_impl(const gps_volume* vol, const gps_intrinsics* K, c
     static const bool dbg = getenv("GPS_RAYCAST_DEBUG") != nullptr;
     if (footprint)
       k_raycast<2><<<gr, 128, 0, s>>>(v->view, p, depth_out, color_out, nullptr, tmin, tmax, footprint);
-    else if (dbg && vertex_out)
+    else if (dbg && vertex_out && !dT)
       k_raycast<1><<<gr, 128, 0, s>>>(v->view, p, depth_out, color_out, vertex_out, tmin, tmax);
+    else if (dT)
+      k_raycast<0, 4, true><<<gr, 128, 0, s>>>(v->view, p, depth_out, color_out, vertex_out, tmin, tmax);
     else {
       // 8 resident 128-thread CTAs per SM (64 registers, no spills)
       k_raycast<0, 4><<<gr, 128, 0, s>>>(v->view, p, depth_out, color_out, vertex_out, tmin, tmax);
@@ -1267,6 +1320,16 @@ gps_status gps_raycast(const gps_volume* vol, const gps_intrinsics* K, const gps
   gps_status st = check_sticky(vol);
   if (st != GPS_OK) return st;
   return raycast_impl(vol, K, T, depth_out, color_out, vertex_out, nullptr, stream);
+}
+
+gps_status gps_raycast_dpose(const gps_volume* vol, const gps_intrinsics* K, const gps_pose* T_dev, float* depth_out,
+                             float* color_out, float* vertex_out, gps_stream_t stream) {
+  if (!vol || !T_dev || !depth_out || !color_out) return invalid("gps_raycast_dpose: null argument");
+  if (!valid_intrinsics(K)) return invalid("gps_raycast_dpose: bad intrinsics");
+  if ((reinterpret_cast<uintptr_t>(T_dev) & 3u) != 0) return invalid("gps_raycast_dpose: pose must be 4-byte aligned");
+  gps_status st = check_sticky(vol);
+  if (st != GPS_OK) return st;
+  return raycast_impl(vol, K, nullptr, depth_out, color_out, vertex_out, nullptr, stream, T_dev);
 }
 
 gps_status gps_debug_apron_check_sync(const gps_volume* vol, gps_stream_t stream, int64_t* n_bad) {

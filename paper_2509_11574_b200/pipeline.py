@@ -10,6 +10,9 @@ end-to-end path).
 """
 from __future__ import annotations
 
+import ctypes as C
+import dataclasses
+
 import numpy as np
 import torch
 
@@ -50,10 +53,18 @@ class MappingPipeline:
                                 n_views=(n_global + n_local) if all_views_per_iteration else 1)
         # camera tracking (Eq. 5): every frame after the first is
         # tracked against the previous frame's raycast maps, and its tracked pose is the one fused
+        # The tracked pose stays on the device: ICP writes it (gps_track_async) into a ring slot
+        # that fusion, raycast and normals read (the *_dpose forms) and the next frame's ICP
+        # starts from; a copy goes to pinned host memory, read lazily (keyframe selection and the
+        # round's views need it only at round frames), so a frame costs no host round trip.
         self.tracking = track
         self.icp_cfg = icp_cfg or A.IcpConfig()
-        self.prev_pose = None
-        self.track_log = []
+        self._track_log = []
+        self._pending = []       # frames whose keyframe offer waits for their host pose, in order
+        self._last_pose = None
+        self._pose_dev = None    # device pose (f32[12]) of the last fused frame, tracking mode
+        self._pose_prev = None   # ... and of the frame before it (constant-velocity prediction)
+        self.poses = {}          # frame -> host (R, t) as fused, tracking mode (filled by _resolve)
         # Gaussian adding / removal
         self.manage = manage_gaussians
         self.add_cfg = add_cfg or A.AddConfig()
@@ -78,6 +89,14 @@ class MappingPipeline:
             self.t_vertex = torch.empty((H, W, 3), dtype=torch.float32, device=dev)
             self.t_normal = torch.empty((H, W, 3), dtype=torch.float32, device=dev)
             self._model = None  # (V*, N*) of the previous frame
+            rb = (A.TRACK_RESULT_BYTES + 15) // 16 * 16
+            self._ring = 64
+            self._res_dev = torch.zeros((self._ring, rb), dtype=torch.uint8, device=dev)
+            self._res_host = torch.zeros((self._ring, rb), dtype=torch.uint8, pin_memory=True)
+            self._slot = 0
+            self._pred = torch.empty(12, dtype=torch.float32, device=dev)
+            self._track_ws = torch.empty(A._L.gps_track_workspace_size(C.byref(cam.c()), self.icp_cfg.levels),
+                                         dtype=torch.uint8, device=dev)
         if manage_gaussians:
             self.r_depth, self.r_color, self.vertex, self.normal = mk(H, W), mk(H, W, 3), mk(H, W, 3), mk(H, W, 3)
             self._add_color, self._add_weight = mk(H, W, 3), mk(H, W)
@@ -141,19 +160,27 @@ class MappingPipeline:
         rgba = self._device(rgba)
         if prefetch is not None:
             self.prefetch(*prefetch)
-        if self.tracking and self._model is not None:
-            Rp, tp = self.prev_pose
-            res = A.track(self.cam, depth, self.depth_scale, self._model[0], self._model[1], Rp, tp, Rp, tp,
-                          self.icp_cfg)
-            R, t = res["R"].astype(np.float32), res["t"].astype(np.float32)
-            self.track_log.append(res)
-        self.vol.fuse(self.cam, R, t, depth, self.depth_scale, rgba)
+        dpose = None
+        if self.tracking:
+            if self._model is not None:
+                dpose = self._track(k, depth)
+            else:  # the first frame: its given pose starts the trajectory
+                dpose = self._pose_dev = A.pose_tensor(R, t)
+                self._pending.append((k, None, (np.asarray(R, np.float32), np.asarray(t, np.float32))))
+            self.vol.fuse_dpose(self.cam, dpose, depth, self.depth_scale, rgba)
+            is_kf = None  # decided when the pose is read back (_resolve)
+            self.frames[k] = (rgba, None, None)
+        else:
+            self.vol.fuse(self.cam, R, t, depth, self.depth_scale, rgba)
+            self._last_pose = (np.asarray(R, np.float32), np.asarray(t, np.float32))
+            is_kf = self.kf.offer(k, R, t)
+            self.frames[k] = (rgba, np.asarray(R, np.float32), np.asarray(t, np.float32))
         self.last_frame = k
-        self.last_pose = (np.asarray(R, np.float32), np.asarray(t, np.float32))
-        is_kf = self.kf.offer(k, R, t)
         self.interval.append(k)
-        self.frames[k] = (rgba, np.asarray(R, np.float32), np.asarray(t, np.float32))
         round_now = refine and Sch.is_round_frame(k, self.delta_k)
+        if round_now and self.tracking:
+            self._resolve()  # the keyframes and the views' host poses (waits for this frame's ICP)
+            R, t = self._last_pose
         views_ids = None
         self.depth, self.color = self._fdepth, self._fcolor
         want_v = round_now and self.manage
@@ -169,25 +196,88 @@ class MappingPipeline:
                 j = views_ids.index(k)
                 self.depth, self.color = self.view_depth[s][j], self.view_color[s][j]
         vert = self.vertex[s] if want_v else (self.t_vertex if self.tracking else None)
-        self.vol.raycast(self.cam, R, t, self.depth, self.color, vertex_out=vert)
-        if want_v:
-            A.vertex_normals(self.cam, R, t, self.depth, self.vertex[s], out=self.normal[s])
-            if self.tracking:
-                self._model = (self.vertex[s], self.normal[s])
-        elif self.tracking:
-            A.vertex_normals(self.cam, R, t, self.depth, self.t_vertex, out=self.t_normal)
-            self._model = (self.t_vertex, self.t_normal)
         if self.tracking:
-            self.prev_pose = (np.asarray(R, np.float32), np.asarray(t, np.float32))
+            self.vol.raycast_dpose(self.cam, dpose, self.depth, self.color, vert)
+            nrm = self.normal[s] if want_v else self.t_normal
+            A.vertex_normals_dpose(self.cam, dpose, self.depth, vert, nrm)
+            self._model = (vert, nrm)
+        else:
+            self.vol.raycast(self.cam, R, t, self.depth, self.color, vertex_out=vert)
+            if want_v:
+                A.vertex_normals(self.cam, R, t, self.depth, self.vertex[s], out=self.normal[s])
         if round_now:
             self._refine_round(views_ids, add_frame=(k, rgba, R, t, s) if self.manage else None)
         if len(self.interval) >= self.delta_k or Sch.is_round_frame(k, self.delta_k):
             self.interval = []
-        # keep device frames only for keyframes and the current interval
+        if not self._pending:
+            self._drop_frames()
+        return is_kf
+
+    def _drop_frames(self):
+        """Keep device frames only for keyframes and the current interval."""
         keep = set(self.kf.keyframes) | set(self.interval)
         for f in [f for f in self.frames if f not in keep]:
             del self.frames[f]
-        return is_kf
+
+    def _track(self, k, depth):
+        """ICP of frame k against the previous frame's maps, from the previous frame's device pose
+        (gps_track_async); the result record is copied to pinned memory for _resolve."""
+        if len(self._pending) >= self._ring - 1:
+            self._resolve()  # the oldest pending slot is about to be reused
+        i = self._slot
+        self._slot = (i + 1) % self._ring
+        raw = self._res_dev[i]
+        pose = raw[:48].view(torch.float32)  # gps_track_result.T is its first member
+        # the ICP starts from the previous frame's pose, whose camera is also the association's (Eq. 5);
+        # a frame whose ICP fails gets the constant-velocity prediction from the two previous
+        # frames instead (R-ICP-FAIL); with no prediction yet (the second frame) the iterate stands
+        cfg = self.icp_cfg
+        fail = None
+        if self._pose_prev is not None:
+            fail = A.pose_extrapolate(self._pose_prev, self._pose_dev, self._pred)
+        elif cfg.fallback:
+            cfg = dataclasses.replace(cfg, fallback=False)
+        A.track_async(self.cam, depth, self.depth_scale, self._model[0], self._model[1], self._pose_dev,
+                      self._pose_dev, pose, raw, cfg, ws=self._track_ws, pose_fail=fail)
+        self._pose_prev = self._pose_dev
+        self._res_host[i].copy_(raw, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream())
+        self._pending.append((k, (i, ev), None))
+        self._pose_dev = pose
+        return pose
+
+    def _resolve(self):
+        """Read back the pending tracked poses (waiting only for the last one's ICP), and make the
+        deferred keyframe offers in frame order."""
+        if not self._pending:
+            return
+        for k, dev, host in self._pending:
+            if dev is not None:
+                i, ev = dev
+                ev.synchronize()
+                res = A.track_result(self._res_host[i])
+                self._track_log.append(res)
+                host = res["T"]  # the fused pose (the iterate, or the prediction on failure)
+            R, t = host
+            self.poses[k] = host
+            self.kf.offer(k, R, t)
+            if k in self.frames:
+                self.frames[k] = (self.frames[k][0], R, t)
+            self._last_pose = host
+        self._pending = []
+        self._drop_frames()
+
+    @property
+    def last_pose(self):
+        """Host (R, t) of the last fused frame (tracking mode: waits for its ICP)."""
+        self._resolve()
+        return self._last_pose
+
+    @property
+    def track_log(self):
+        self._resolve()
+        return self._track_log
 
     def _wait_set(self, s: int):
         ev = self._set_free[s]
@@ -212,17 +302,20 @@ class MappingPipeline:
         the host bookkeeping) for replaying a window of the sequence."""
         import copy
         self.join()
+        self._resolve()
         return {"vol": self.vol.clone(), "g": self.g.clone(), "m": self.state.m.clone(), "v": self.state.v.clone(),
                 "step": self.state.step, "kf": (list(self.kf.keyframes), copy.deepcopy(self.kf._last)),
                 "frames": dict(self.frames), "interval": list(self.interval), "last_frame": self.last_frame,
                 "rng": copy.deepcopy(self.rng.bit_generator.state), "rounds": self.rounds,
                 "iterations_run": self.iterations_run, "removal_pending": self._removal_pending,
                 "added_total": self.added_total, "removed_total": self.removed_total,
-                "track": ((self._model[0].clone(), self._model[1].clone(), self.prev_pose)
+                "track": ((self._model[0].clone(), self._model[1].clone(), self._pose_dev.clone(), self._last_pose,
+                           None if self._pose_prev is None else self._pose_prev.clone())
                           if self.tracking and self._model is not None else None)}
 
     def restore(self, s):
         self.join()
+        self._resolve()
         self.vol.copy_from(s["vol"])
         for x in (self.g, self.state.m, self.state.v):
             x.set_n(s["g"].n)
@@ -238,9 +331,13 @@ class MappingPipeline:
         self._removal_pending = s["removal_pending"]
         self.added_total, self.removed_total = s["added_total"], s["removed_total"]
         if self.tracking and s["track"] is not None:
+            self._pending = []
             self.t_vertex.copy_(s["track"][0])
             self.t_normal.copy_(s["track"][1])
-            self._model, self.prev_pose = (self.t_vertex, self.t_normal), s["track"][2]
+            self._model = (self.t_vertex, self.t_normal)
+            self._pose_dev = s["track"][2].clone()
+            self._pose_prev = None if s["track"][4] is None else s["track"][4].clone()
+            self._last_pose = s["track"][3]
         if True:  # the refinement stream must see the restored state
             ev = torch.cuda.Event()
             ev.record(torch.cuda.current_stream())
@@ -249,6 +346,7 @@ class MappingPipeline:
     def refine_round(self):
         """A round at the current point of the sequence (views chosen now; the last frame's
         raycast is recomputed into the round's buffers)."""
+        self._resolve()
         views_ids = Sch.select_views(self.kf.keyframes, self.interval, self.rng, self.n_global, self.n_local)
         self._wait_set(self.rounds % len(self.view_depth))
         return self._refine_round(views_ids, reuse_last=False)
