@@ -301,10 +301,22 @@ __device__ void icp_solve_cta(const double* partial, int nblk, DevPose* pose, do
   __shared__ double tot[32];
   __shared__ double part[8][32];
   {  // 30 sums x 8 interleaved chunks of the CTA partials, then the 8 chunks per sum
+    // 8 independent accumulators keep 8 loads in flight per thread (the partials are L2-resident;
+    // a dependent chain of ~nblk/8 L2 round trips would dominate small levels)
     const int v = threadIdx.x & 31, c = threadIdx.x >> 5;
     double x = 0.0;
-    if (v < 30)
-      for (int b = c; b < nblk; b += 8) x += __ldcg(partial + (size_t)b * 32 + v);
+    if (v < 30) {
+      double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      int b = c;
+      for (; b + 56 < nblk; b += 64) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] += __ldcg(partial + (size_t)(b + 8 * j) * 32 + v);
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (b + 8 * j < nblk) acc[j] += __ldcg(partial + (size_t)(b + 8 * j) * 32 + v);
+      x = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+    }
     part[c][v] = x;
     __syncthreads();
     if (threadIdx.x < 30) {
@@ -315,6 +327,9 @@ __device__ void icp_solve_cta(const double* partial, int nblk, DevPose* pose, do
   }
   __syncthreads();
   if (threadIdx.x != 0) return;
+  double R0[9], t0[3];  // the current pose, loaded while the system is assembled
+  for (int e = 0; e < 9; ++e) R0[e] = pose->R[e];
+  for (int e = 0; e < 3; ++e) t0[e] = pose->t[e];
   double A[6][6], b[6];
   int k = 0;
   for (int x = 0; x < 6; ++x)
@@ -332,6 +347,7 @@ __device__ void icp_solve_cta(const double* partial, int nblk, DevPose* pose, do
   double dmax = 0.0;
   for (int x = 0; x < 6; ++x) dmax = fmax(dmax, A[x][x]);
   double Lc[6][6] = {};
+  double inv[6];
   for (int j = 0; j < 6; ++j) {
     double d = A[j][j];
     for (int m = 0; m < j; ++m) d -= Lc[j][m] * Lc[j][m];
@@ -341,22 +357,23 @@ __device__ void icp_solve_cta(const double* partial, int nblk, DevPose* pose, do
       return;
     }
     Lc[j][j] = sqrt(d);
+    inv[j] = 1.0 / Lc[j][j];  // one division per pivot (a serial single-thread chain: keep it short)
     for (int i = j + 1; i < 6; ++i) {
       double s = A[i][j];
       for (int m = 0; m < j; ++m) s -= Lc[i][m] * Lc[j][m];
-      Lc[i][j] = s / Lc[j][j];
+      Lc[i][j] = s * inv[j];
     }
   }
   double y[6], xi[6];
   for (int i = 0; i < 6; ++i) {
     double s = -b[i];
     for (int m = 0; m < i; ++m) s -= Lc[i][m] * y[m];
-    y[i] = s / Lc[i][i];
+    y[i] = s * inv[i];
   }
   for (int i = 5; i >= 0; --i) {
     double s = y[i];
     for (int m = i + 1; m < 6; ++m) s -= Lc[m][i] * xi[m];
-    xi[i] = s / Lc[i][i];
+    xi[i] = s * inv[i];
   }
   // exp of the twist (v, w): Rodrigues rotation, translation v (left-multiplied increment)
   const double w0 = xi[3], w1 = xi[4], w2 = xi[5];
@@ -365,14 +382,23 @@ __device__ void icp_solve_cta(const double* partial, int nblk, DevPose* pose, do
   double K2[9];
   for (int r = 0; r < 3; ++r)
     for (int c = 0; c < 3; ++c) K2[3 * r + c] = K[3 * r] * K[c] + K[3 * r + 1] * K[3 + c] + K[3 * r + 2] * K[6 + c];
-  const double ca = th < 1e-12 ? 1.0 : sin(th) / th, cb = th < 1e-12 ? 0.0 : (1.0 - cos(th)) / (th * th);
+  // sin(th)/th and (1-cos th)/th^2: their Taylor series for th < 1e-2 (the first omitted terms,
+  // th^8/9! and th^8/10!, are below 1e-21), else the closed forms
+  double ca, cb;
+  const double th2 = th * th;
+  if (th < 1e-2) {
+    ca = 1.0 - th2 / 6.0 * (1.0 - th2 / 20.0 * (1.0 - th2 / 42.0));
+    cb = 0.5 - th2 / 24.0 * (1.0 - th2 / 30.0 * (1.0 - th2 / 56.0));
+  } else {
+    ca = sin(th) / th;
+    cb = (1.0 - cos(th)) / th2;
+  }
   double dR[9];
   for (int e = 0; e < 9; ++e) dR[e] = (e % 4 == 0 ? 1.0 : 0.0) + ca * K[e] + cb * K2[e];
   double R[9], t[3];
   for (int r = 0; r < 3; ++r) {
-    for (int c = 0; c < 3; ++c)
-      R[3 * r + c] = dR[3 * r] * pose->R[c] + dR[3 * r + 1] * pose->R[3 + c] + dR[3 * r + 2] * pose->R[6 + c];
-    t[r] = dR[3 * r] * pose->t[0] + dR[3 * r + 1] * pose->t[1] + dR[3 * r + 2] * pose->t[2] + xi[r];
+    for (int c = 0; c < 3; ++c) R[3 * r + c] = dR[3 * r] * R0[c] + dR[3 * r + 1] * R0[3 + c] + dR[3 * r + 2] * R0[6 + c];
+    t[r] = dR[3 * r] * t0[0] + dR[3 * r + 1] * t0[1] + dR[3 * r + 2] * t0[2] + xi[r];
   }
   for (int e = 0; e < 9; ++e) pose->R[e] = R[e];
   for (int e = 0; e < 3; ++e) pose->t[e] = t[e];
