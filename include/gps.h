@@ -356,6 +356,10 @@ typedef struct {
   int32_t converged;     /* !degenerate, inliers/valid >= min_inlier_frac and
                           * inliers >= min_inlier_px_frac * width * height                      */
   float inlier_frac;
+  float pivot_ratio;     /* smallest Cholesky pivot / largest diagonal of the last step's system
+                          * (conditioning: ~1 well constrained, -> 0 sliding along a degenerate
+                          * direction)                                                        */
+  int32_t reserved;
 } gps_track_result;
 
 size_t gps_track_workspace_size(const gps_intrinsics* K /*host*/, int32_t levels);

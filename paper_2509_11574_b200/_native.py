@@ -83,7 +83,8 @@ class gps_icp_config(C.Structure):
 class gps_track_result(C.Structure):
     _fields_ = [("T", gps_pose), ("R64", C.c_double * 9), ("t64", C.c_double * 3), ("energy", C.c_double),
                 ("inliers", C.c_int32), ("valid", C.c_int32), ("steps", C.c_int32), ("degenerate", C.c_int32),
-                ("converged", C.c_int32), ("inlier_frac", C.c_float)]
+                ("converged", C.c_int32), ("inlier_frac", C.c_float), ("pivot_ratio", C.c_float),
+                ("reserved", C.c_int32)]
 
 
 P = C.POINTER

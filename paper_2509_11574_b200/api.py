@@ -539,7 +539,7 @@ def track(cam: Camera, depth: torch.Tensor, depth_scale: float, model_vertex: to
     return {"R": np.array(out.R64[:], np.float64).reshape(3, 3), "t": np.array(out.t64[:], np.float64),
             "T": (np.array(out.T.R[:], np.float32).reshape(3, 3), np.array(out.T.t[:], np.float32)),
             "converged": bool(out.converged), "degenerate": bool(out.degenerate), "inlier_frac": out.inlier_frac,
-            "inliers": out.inliers, "steps": out.steps, "energy": out.energy}
+            "inliers": out.inliers, "steps": out.steps, "energy": out.energy, "pivot_ratio": out.pivot_ratio}
 
 
 TRACK_RESULT_BYTES = C.sizeof(N.gps_track_result)
@@ -579,4 +579,4 @@ def track_result(raw) -> dict:
     return {"R": np.array(out.R64[:], np.float64).reshape(3, 3), "t": np.array(out.t64[:], np.float64),
             "T": (np.array(out.T.R[:], np.float32).reshape(3, 3), np.array(out.T.t[:], np.float32)),
             "converged": bool(out.converged), "degenerate": bool(out.degenerate), "inlier_frac": out.inlier_frac,
-            "inliers": out.inliers, "steps": out.steps, "energy": out.energy}
+            "inliers": out.inliers, "steps": out.steps, "energy": out.energy, "pivot_ratio": out.pivot_ratio}

@@ -35,6 +35,7 @@ struct DevPose {
   double R[9], t[3];
   double energy;
   int32_t steps, inliers, valid, degenerate;
+  double pivot;    // smallest Cholesky pivot / largest diagonal of the last system
   int32_t stop;    // this level is done (converged or degenerate)
   uint32_t ticket; // CTAs of the current k_icp_step that have written their sums
   float Rp[9], tp[3];  // the camera the model maps were raycast from (camera -> world)
@@ -179,6 +180,7 @@ __global__ void k_icp_export(const DevPose* __restrict__ pose, float min_inlier_
   r.steps = d.steps;
   r.degenerate = d.degenerate;
   r.inlier_frac = d.valid > 0 ? (float)d.inliers / (float)d.valid : 0.f;
+  r.pivot_ratio = (float)d.pivot;
   r.converged = !d.degenerate && r.inlier_frac >= min_inlier_frac && (double)d.inliers >= min_inliers;
   if (fallback && !r.converged) r.T = d.fail;  // R-ICP-FAIL
   if (out) *out = r.T;
@@ -348,10 +350,13 @@ __device__ void icp_solve_cta(const double* partial, int nblk, DevPose* pose, do
   for (int x = 0; x < 6; ++x) dmax = fmax(dmax, A[x][x]);
   double Lc[6][6] = {};
   double inv[6];
+  double pmin = 1.0;
   for (int j = 0; j < 6; ++j) {
     double d = A[j][j];
     for (int m = 0; m < j; ++m) d -= Lc[j][m] * Lc[j][m];
+    pmin = fmin(pmin, d / dmax);
     if (!(d > 1e-12 * dmax)) {
+      pose->pivot = pmin;
       pose->degenerate = 1;
       pose->stop = 1;
       return;
@@ -364,6 +369,7 @@ __device__ void icp_solve_cta(const double* partial, int nblk, DevPose* pose, do
       Lc[i][j] = s * inv[j];
     }
   }
+  pose->pivot = pmin;
   double y[6], xi[6];
   for (int i = 0; i < 6; ++i) {
     double s = -b[i];

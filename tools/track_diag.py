@@ -15,12 +15,12 @@ import paper_2509_11574_b200 as G  # noqa: E402
 from paper_2509_11574_b200.pipeline import MappingPipeline  # noqa: E402
 
 
-def run(cfg, frames, history, eager, n_g, watch=None):
+def run(cfg, frames, history, eager, n_g, watch=None, icp=None):
     cam = G.Camera(cfg.fx, cfg.fy, cfg.cx, cfg.cy, cfg.width, cfg.height)
     vol = G.Volume(voxel_size=cfg.voxel_size, max_blocks=cfg.max_blocks, hash_slots=cfg.hash_slots,
                    dense_bounds=S.scene_bounds(cfg))
     g = G.Gaussians.from_dict(S.make_gaussians(cfg, n=n_g))
-    pipe = MappingPipeline(cam, g, vol, cfg.depth_scale, seed=0, track=True)
+    pipe = MappingPipeline(cam, g, vol, cfg.depth_scale, seed=0, track=True, icp_cfg=icp)
     for k, (d, c, R, t) in enumerate(frames):
         pipe.process_frame(k, d, c, R, t, refine=k >= history)
         if eager and watch and watch[0] <= k <= watch[1]:
@@ -47,6 +47,8 @@ def main():
     ap.add_argument("--gaussians", type=int, default=20000)
     ap.add_argument("--detail", type=int, default=0, help="print ICP records of this many frames before failure")
     ap.add_argument("--watch", type=int, nargs=2, default=None, help="print model-map stats for these frames")
+    ap.add_argument("--angle", type=float, default=30.0)
+    ap.add_argument("--dist", type=float, default=0.1)
     ap.add_argument("--clean", action="store_true", help="noise-free depth")
     ap.add_argument("--both", action="store_true", help="also the deferred read-back")
     a = ap.parse_args()
@@ -59,7 +61,8 @@ def main():
         fr = S.render_frame(cfg, scene, *poses[k], k=k, device="cuda", dc=dc)
         frames.append((fr.depth.contiguous(), fr.rgba.contiguous(), fr.R, fr.t))
     for eager in (True, False):
-        err, nb, log = run(cfg, frames, a.history, eager, a.gaussians, watch=a.watch)
+        icp = G.IcpConfig(angle_max_deg=a.angle, dist_max=a.dist)
+        err, nb, log = run(cfg, frames, a.history, eager, a.gaussians, watch=a.watch, icp=icp)
         bad = np.nonzero(err > 0.02)[0]
         print(f"eager={eager}: max err {err.max():.4f} m, rmse {np.sqrt(np.mean(err ** 2)):.4f}, blocks {nb}, "
               f"first frame > 2 cm: {bad[0] if len(bad) else None}")
@@ -72,7 +75,7 @@ def main():
                 ang = np.degrees(np.arccos(np.clip((np.trace(dR) - 1) / 2, -1, 1)))
                 mv = np.linalg.norm(np.asarray(frames[f][3], np.float64) - np.asarray(frames[f - 1][3], np.float64))
                 print(f"  frame {f}: err {err[f]:.4f} true step {mv * 1000:.1f} mm {ang:.2f} deg | steps {r['steps']} "
-                      f"inl {r['inlier_frac']:.3f} n {r['inliers']} conv {r['converged']} degen {r['degenerate']} energy {r['energy']:.3g}")
+                      f"inl {r['inlier_frac']:.3f} n {r['inliers']} conv {r['converged']} piv {r['pivot_ratio']:.2e} degen {r['degenerate']} energy {r['energy']:.3g}")
         if not a.both:
             break
 
