@@ -343,6 +343,13 @@ typedef struct {
                           *    -- R-ICP-FAIL [1]; 0: result.T is the iterate whatever the outcome */
   float min_inlier_px_frac; /* converged also needs inliers >= this fraction of the frame's
                              * pixels [0.05] (R-ICP-FAIL: a near-empty depth frame is a failure) */
+  float min_pivot_ratio; /* ... and the last system's pivot_ratio >= this [1e-3] (R-ICP-FAIL:
+                          * an ill-conditioned system slides along its weak direction)         */
+  int32_t filter_radius; /* bilateral pre-filter of the depth used for tracking (KinectFusion's
+                          * measurement filter; fusion keeps the raw depth), window radius in
+                          * pixels, 0 = off [0; the mapping pipeline tracks with 3] (R-ICP-FILT) */
+  float filter_sigma_s;  /* spatial sigma, pixels [4.5]                                         */
+  float filter_sigma_r;  /* range sigma, metres [0.03]                                          */
 } gps_icp_config;
 
 typedef struct {
@@ -353,8 +360,9 @@ typedef struct {
   int32_t inliers, valid;/* last step's inliers / current pixels with a normal                  */
   int32_t steps;         /* Gauss-Newton steps taken                                            */
   int32_t degenerate;    /* a step had < 6 inliers or a rank-deficient system (no update)       */
-  int32_t converged;     /* !degenerate, inliers/valid >= min_inlier_frac and
-                          * inliers >= min_inlier_px_frac * width * height                      */
+  int32_t converged;     /* !degenerate, inliers/valid >= min_inlier_frac,
+                          * inliers >= min_inlier_px_frac * width * height and
+                          * pivot_ratio >= min_pivot_ratio                                      */
   float inlier_frac;
   float pivot_ratio;     /* smallest Cholesky pivot / largest diagonal of the last step's system
                           * (conditioning: ~1 well constrained, -> 0 sliding along a degenerate

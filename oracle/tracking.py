@@ -29,6 +29,31 @@ class IcpCfg:
     eps: float = 1e-6               # convergence on |xi|
     min_inlier_frac: float = 0.1
     min_inlier_px_frac: float = 0.05  # R-ICP-FAIL: and inliers >= this fraction of the frame's pixels
+    min_pivot_ratio: float = 1e-3     # R-ICP-FAIL: and the last system's smallest Cholesky pivot /
+                                      # largest diagonal >= this
+    filter_radius: int = 0            # R-ICP-FILT: bilateral pre-filter radius (0 = off)
+    filter_sigma_s: float = 4.5
+    filter_sigma_r: float = 0.03
+
+
+def bilateral(d: np.ndarray, r: int, sigma_s: float, sigma_r: float) -> np.ndarray:
+    """R-ICP-FILT (KinectFusion's measurement filter), written out: for every valid pixel (d > 0),
+    sum_q w_q d_q / sum_q w_q over the valid pixels q of the (2r+1)^2 window inside the image,
+    w_q = exp(-|q - p|^2 / (2 sigma_s^2) - (d_q - d_p)^2 / (2 sigma_r^2)); invalid pixels stay 0."""
+    d = np.asarray(d, np.float64)
+    H, W = d.shape
+    sw = np.zeros_like(d)
+    sz = np.zeros_like(d)
+    for dy in range(-r, r + 1):
+        for dx in range(-r, r + 1):
+            q = np.zeros_like(d)  # d shifted so that q[y, x] = d[y + dy, x + dx] (0 outside)
+            ys, yd = slice(max(dy, 0), H + min(dy, 0)), slice(max(-dy, 0), H + min(-dy, 0))
+            xs, xd = slice(max(dx, 0), W + min(dx, 0)), slice(max(-dx, 0), W + min(-dx, 0))
+            q[yd, xd] = d[ys, xs]
+            w = np.exp(-(dx * dx + dy * dy) / (2 * sigma_s ** 2) - (q - d) ** 2 / (2 * sigma_r ** 2)) * (q > 0)
+            sw += w
+            sz += w * q
+    return np.where(d > 0, sz / np.maximum(sw, 1e-300), 0.0)
 
 
 def depth_pyramid(depth_m: np.ndarray, levels: int, dmin: float, dmax: float):
@@ -131,10 +156,14 @@ def track(depth_u16, depth_scale, K, Vm_full, Nm_full, Rp, tp, R0, t0, cfg: IcpC
     steps at level l (stopping early when |xi| < eps).  Returns (R, t, info)."""
     fx, fy, cx, cy = K
     d = np.asarray(depth_u16, np.float64) * np.float64(np.float32(1.0 / depth_scale))
+    if cfg.filter_radius > 0:  # R-ICP-FILT on the in-range level-0 depth, before the pyramid
+        d0 = d.copy()
+        d0[(d0 < cfg.depth_min) | (d0 > cfg.depth_max)] = 0.0
+        d = bilateral(d0, cfg.filter_radius, cfg.filter_sigma_s, cfg.filter_sigma_r)
     pyr = depth_pyramid(d, cfg.levels, cfg.depth_min, cfg.depth_max)
     R, t = np.asarray(R0, np.float64).copy(), np.asarray(t0, np.float64).copy()
     Rp, tp = np.asarray(Rp, np.float64), np.asarray(tp, np.float64)
-    info = {"steps": 0, "inliers": 0, "valid": 0, "degenerate": False}
+    info = {"steps": 0, "inliers": 0, "valid": 0, "degenerate": False, "pivot_ratio": 0.0}
     for lev in reversed(range(cfg.levels)):
         intr = level_intrinsics(fx, fy, cx, cy, lev)
         Vc = backproject(pyr[lev], *intr)
@@ -150,6 +179,8 @@ def track(depth_u16, depth_scale, K, Vm_full, Nm_full, Rp, tp, R0, t0, cfg: IcpC
             if ev[0] <= 1e-12 * max(ev[-1], 1e-300):
                 info["degenerate"] = True
                 break
+            Lc = np.linalg.cholesky(A)
+            info["pivot_ratio"] = float((np.diag(Lc) ** 2).min() / np.diag(A).max())
             xi = -np.linalg.solve(A, b)
             dR, dt = exp_se3(xi)
             R, t = dR @ R, dR @ t + dt
@@ -158,5 +189,6 @@ def track(depth_u16, depth_scale, K, Vm_full, Nm_full, Rp, tp, R0, t0, cfg: IcpC
                 break
     info["inlier_frac"] = info["inliers"] / max(info["valid"], 1)
     info["converged"] = ((not info["degenerate"]) and info["inlier_frac"] >= cfg.min_inlier_frac
-                         and info["inliers"] >= cfg.min_inlier_px_frac * np.shape(depth_u16)[0] * np.shape(depth_u16)[1])
+                         and info["inliers"] >= cfg.min_inlier_px_frac * np.shape(depth_u16)[0] * np.shape(depth_u16)[1]
+                         and info["pivot_ratio"] >= cfg.min_pivot_ratio)
     return R, t, info

@@ -77,7 +77,8 @@ class gps_remove_config(C.Structure):
 class gps_icp_config(C.Structure):
     _fields_ = [("levels", C.c_int32), ("iters", C.c_int32 * 4), ("dist_max", C.c_float),
                 ("angle_max_deg", C.c_float), ("depth_min", C.c_float), ("depth_max", C.c_float),
-                ("eps", C.c_float), ("min_inlier_frac", C.c_float), ("fallback", C.c_int32), ("min_inlier_px_frac", C.c_float)]
+                ("eps", C.c_float), ("min_inlier_frac", C.c_float), ("fallback", C.c_int32), ("min_inlier_px_frac", C.c_float), ("min_pivot_ratio", C.c_float),
+                ("filter_radius", C.c_int32), ("filter_sigma_s", C.c_float), ("filter_sigma_r", C.c_float)]
 
 
 class gps_track_result(C.Structure):

@@ -515,12 +515,18 @@ class IcpConfig:
     min_inlier_frac: float = 0.1
     fallback: bool = True          # R-ICP-FAIL: a frame that does not converge keeps its initial pose
     min_inlier_px_frac: float = 0.05  # R-ICP-FAIL: converged needs inliers >= this fraction of the pixels
+    min_pivot_ratio: float = 1e-3     # R-ICP-FAIL: ... and a well-conditioned last system
+    filter_radius: int = 0            # R-ICP-FILT: bilateral pre-filter of the tracking depth (0 = off;
+                                      # MappingPipeline tracks with 3)
+    filter_sigma_s: float = 4.5
+    filter_sigma_r: float = 0.03
 
     def c(self) -> N.gps_icp_config:
         it = list(self.iters) + [1] * (4 - len(self.iters))
         return N.gps_icp_config(self.levels, (C.c_int32 * 4)(*it), self.dist_max, self.angle_max_deg,
                                 self.depth_min, self.depth_max, self.eps, self.min_inlier_frac,
-                                int(self.fallback), self.min_inlier_px_frac)
+                                int(self.fallback), self.min_inlier_px_frac, self.min_pivot_ratio,
+                                int(self.filter_radius), self.filter_sigma_s, self.filter_sigma_r)
 
 
 def track(cam: Camera, depth: torch.Tensor, depth_scale: float, model_vertex: torch.Tensor,

@@ -67,6 +67,41 @@ __global__ void k_icp_depth(const uint16_t* __restrict__ raw, int n, float inv_s
   d[i] = (z >= dmin && z <= dmax) ? z : 0.f;
 }
 
+// R-ICP-FILT: bilateral filter of the level-0 depth (metres, 0 = invalid), over the valid
+// pixels of the (2r+1)^2 window: sum w z / sum w, w = exp(-(dx^2 + dy^2) / (2 s_s^2)
+// - (z - z0)^2 / (2 s_r^2)); invalid pixels stay 0
+__global__ void k_icp_bilateral(const uint16_t* __restrict__ raw, int W, int H, float inv_scale, float dmin,
+                                float dmax, int r, float inv2ss, float inv2sr, float* __restrict__ out) {
+  const int u = blockIdx.x * 32 + (threadIdx.x & 31), v = blockIdx.y * 8 + (threadIdx.x >> 5);
+  if (u >= W || v >= H) return;
+  auto depth_at = [&](int x, int y) {
+    const float z = (float)raw[(size_t)y * W + x] * inv_scale;
+    return (z >= dmin && z <= dmax) ? z : 0.f;
+  };
+  const float z0 = depth_at(u, v);
+  float res = 0.f;
+  if (z0 > 0.f) {
+    float sw = 0.f, sz = 0.f;
+    for (int dy = -r; dy <= r; ++dy) {
+      const int y = v + dy;
+      if (y < 0 || y >= H) continue;
+      for (int dx = -r; dx <= r; ++dx) {
+        const int x = u + dx;
+        if (x < 0 || x >= W) continue;
+        const float z = depth_at(x, y);
+        if (z > 0.f) {
+          const float dz = z - z0;
+          const float w = __expf(-(float)(dx * dx + dy * dy) * inv2ss - dz * dz * inv2sr);
+          sw += w;
+          sz += w * z;
+        }
+      }
+    }
+    res = sz / sw;  // sw >= 1 (the centre)
+  }
+  out[(size_t)v * W + u] = res;
+}
+
 // R-ICP-PYR: mean of the valid children of the 2x2 block
 __global__ void k_icp_down(const float* __restrict__ src, int Ws, float* dst, int Wd, int Hd) {
   const int u = blockIdx.x * blockDim.x + threadIdx.x, v = blockIdx.y;
@@ -166,8 +201,8 @@ __global__ void k_pose_extrapolate(const gps_pose* __restrict__ a, const gps_pos
 }
 
 // the tracked pose (fp32, as gps_track_sync rounds it) and, optionally, the whole result
-__global__ void k_icp_export(const DevPose* __restrict__ pose, float min_inlier_frac, double min_inliers, int fallback,
-                             gps_pose* out, gps_track_result* res) {
+__global__ void k_icp_export(const DevPose* __restrict__ pose, float min_inlier_frac, double min_inliers,
+                             float min_pivot, int fallback, gps_pose* out, gps_track_result* res) {
   const DevPose d = *pose;
   gps_track_result r{};
   for (int e = 0; e < 9; ++e) r.T.R[e] = (float)d.R[e];
@@ -181,7 +216,8 @@ __global__ void k_icp_export(const DevPose* __restrict__ pose, float min_inlier_
   r.degenerate = d.degenerate;
   r.inlier_frac = d.valid > 0 ? (float)d.inliers / (float)d.valid : 0.f;
   r.pivot_ratio = (float)d.pivot;
-  r.converged = !d.degenerate && r.inlier_frac >= min_inlier_frac && (double)d.inliers >= min_inliers;
+  r.converged = !d.degenerate && r.inlier_frac >= min_inlier_frac && (double)d.inliers >= min_inliers &&
+                d.pivot >= (double)min_pivot;
   if (fallback && !r.converged) r.T = d.fail;  // R-ICP-FAIL
   if (out) *out = r.T;
   if (res) *res = r;
@@ -458,7 +494,9 @@ static gps_status track_impl(const gps_intrinsics* K, const uint16_t* depth, flo
   if (!K || !depth || !model_vertex || !model_normal || !cfg || !ws) return invalid(w_ + ": null argument");
   if (K->width <= 0 || K->height <= 0 || !(depth_scale > 0)) return invalid(w_ + ": bad intrinsics");
   if (cfg->levels < 1 || cfg->levels > kIcpMaxLevels || !(cfg->dist_max > 0) || !(cfg->depth_max > cfg->depth_min) ||
-      cfg->fallback < 0 || cfg->fallback > 1 || !(cfg->min_inlier_px_frac >= 0.f && cfg->min_inlier_px_frac <= 1.f))
+      cfg->fallback < 0 || cfg->fallback > 1 || !(cfg->min_inlier_px_frac >= 0.f && cfg->min_inlier_px_frac <= 1.f) ||
+      !(cfg->min_pivot_ratio >= 0.f) || cfg->filter_radius < 0 || cfg->filter_radius > 7 ||
+      (cfg->filter_radius > 0 && !(cfg->filter_sigma_s > 0.f && cfg->filter_sigma_r > 0.f)))
     return invalid(w_ + ": bad config");
   for (int l = 0; l < cfg->levels; ++l)
     if (cfg->iters[l] < 1 || (K->width >> l) < 3 || (K->height >> l) < 3) return invalid(w_ + ": bad level");
@@ -474,9 +512,17 @@ static gps_status track_impl(const gps_intrinsics* K, const uint16_t* depth, flo
   k_icp_init<<<1, 1, 0, s>>>(src, dp);
   GPS_CHECK_LAUNCH("k_icp_init");
   const int n0 = K->width * K->height;
-  k_icp_depth<<<(n0 + 255) / 256, 256, 0, s>>>(depth, n0, 1.0f / depth_scale, cfg->depth_min, cfg->depth_max,
-                                               reinterpret_cast<float*>(w + Lw.depth[0]));
-  GPS_CHECK_LAUNCH("k_icp_depth");
+  if (cfg->filter_radius > 0) {
+    const double ss = cfg->filter_sigma_s, sr = cfg->filter_sigma_r;
+    k_icp_bilateral<<<dim3((K->width + 31) / 32, (K->height + 7) / 8), 256, 0, s>>>(
+        depth, K->width, K->height, 1.0f / depth_scale, cfg->depth_min, cfg->depth_max, cfg->filter_radius,
+        (float)(1.0 / (2.0 * ss * ss)), (float)(1.0 / (2.0 * sr * sr)), reinterpret_cast<float*>(w + Lw.depth[0]));
+    GPS_CHECK_LAUNCH("k_icp_bilateral");
+  } else {
+    k_icp_depth<<<(n0 + 255) / 256, 256, 0, s>>>(depth, n0, 1.0f / depth_scale, cfg->depth_min, cfg->depth_max,
+                                                 reinterpret_cast<float*>(w + Lw.depth[0]));
+    GPS_CHECK_LAUNCH("k_icp_depth");
+  }
   for (int l = 1; l < cfg->levels; ++l) {
     const int Wd = K->width >> l, Hd = K->height >> l;
     k_icp_down<<<dim3((Wd + 127) / 128, Hd), 128, 0, s>>>(reinterpret_cast<const float*>(w + Lw.depth[l - 1]),
@@ -516,8 +562,8 @@ static gps_status track_impl(const gps_intrinsics* K, const uint16_t* depth, flo
     }
   }
   k_icp_export<<<1, 1, 0, s>>>(dp, cfg->min_inlier_frac,
-                               (double)cfg->min_inlier_px_frac * (double)K->width * (double)K->height, cfg->fallback,
-                               out_pose, out_res);
+                               (double)cfg->min_inlier_px_frac * (double)K->width * (double)K->height,
+                               cfg->min_pivot_ratio, cfg->fallback, out_pose, out_res);
   GPS_CHECK_LAUNCH("k_icp_export");
   return GPS_OK;
 }

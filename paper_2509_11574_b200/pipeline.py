@@ -58,7 +58,7 @@ class MappingPipeline:
         # starts from; a copy goes to pinned host memory, read lazily (keyframe selection and the
         # round's views need it only at round frames), so a frame costs no host round trip.
         self.tracking = track
-        self.icp_cfg = icp_cfg or A.IcpConfig()
+        self.icp_cfg = icp_cfg or A.IcpConfig(filter_radius=3)  # R-ICP-FILT on the tracking depth
         self._track_log = []
         self._pending = []       # frames whose keyframe offer waits for their host pose, in order
         self._last_pose = None

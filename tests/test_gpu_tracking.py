@@ -207,3 +207,24 @@ def test_chained_pose_predictions_stay_rigid():
     R = o[:9].reshape(3, 3)
     assert np.abs(R @ R.T - np.eye(3)).max() < 1e-6
     assert np.abs(R - ref[:3, :3]).max() < 1e-4 and np.abs(o[9:] - ref[:3, 3]).max() < 1e-4
+
+
+def test_filtered_track_matches_oracle():
+    """R-ICP-FILT (bilateral pre-filter of the tracking depth, k_icp_bilateral) on ToF-noisy cfg2:
+    GPU pose = oracle pose within the tracking bars; the same convergence decision."""
+    import paper_2509_11574_b200 as G
+    cfg = S.get_config("cfg2", noise="tof", dropout=0.03)
+    R0, t0 = S.trajectory(cfg, 1)[0]
+    R0, t0 = np.asarray(R0, np.float64), np.asarray(t0, np.float64)
+    R1 = _rot([0.3, 1.0, 0.2], 0.5) @ R0
+    t1 = t0 + np.array([0.004, -0.003, 0.002])
+    f0, f1 = _frame(S.get_config("cfg2", noise="none", dropout=0.0), R0, t0), _frame(cfg, R1, t1)
+    V, N = _model(f0)
+    depth = f1.depth.numpy().view(np.uint16)
+    K = (cfg.fx, cfg.fy, cfg.cx, cfg.cy)
+    Ro, to, info = OT.track(depth, cfg.depth_scale, K, V, N, R0, t0, R0, t0, OT.IcpCfg(filter_radius=3))
+    res = _gpu_track(G, cfg, depth, V, N, R0, t0, R0, t0, G.IcpConfig(filter_radius=3))
+    assert res["converged"] and info["converged"]
+    assert np.linalg.norm(res["t"] - to) < 2e-5 and _angle_deg(res["R"], Ro) < 2e-3
+    assert abs(res["inlier_frac"] - info["inlier_frac"]) < 2e-3
+    assert abs(res["pivot_ratio"] - info["pivot_ratio"]) < 1e-3 * info["pivot_ratio"] + 1e-6

@@ -111,3 +111,62 @@ def test_pyramid_averages_valid_children_only():
     assert np.allclose(pyr[1], [[2.0, 2.0]])  # (1+3)/2 ; 20 m is out of range
     fx, fy, cx, cy = T.level_intrinsics(600, 600, 319.5, 239.5, 1)
     assert (fx, cx, cy) == (300, 159.5, 119.5)
+
+
+def _bilateral_brute(d, r, ss, sr):
+    """The R-ICP-FILT definition with plain loops (tiny inputs only)."""
+    H, W = d.shape
+    out = np.zeros_like(d)
+    for y in range(H):
+        for x in range(W):
+            if d[y, x] <= 0:
+                continue
+            sw = sz = 0.0
+            for yy in range(max(0, y - r), min(H, y + r + 1)):
+                for xx in range(max(0, x - r), min(W, x + r + 1)):
+                    if d[yy, xx] > 0:
+                        w = np.exp(-((xx - x) ** 2 + (yy - y) ** 2) / (2 * ss * ss)
+                                   - (d[yy, xx] - d[y, x]) ** 2 / (2 * sr * sr))
+                        sw += w
+                        sz += w * d[yy, xx]
+            out[y, x] = sz / sw
+    return out
+
+
+def test_bilateral_matches_its_definition_and_special_cases():
+    rng = np.random.default_rng(3)
+    d = 2.0 + 0.02 * rng.standard_normal((9, 11))
+    d[rng.random(d.shape) < 0.2] = 0.0  # invalid pixels
+    assert np.allclose(T.bilateral(d, 2, 1.5, 0.03), _bilateral_brute(d, 2, 1.5, 0.03), rtol=0, atol=1e-14)
+    # constant depth is a fixed point; invalid pixels stay invalid, valid ones stay valid
+    c = np.full((6, 7), 1.7)
+    c[2, 3] = 0.0
+    f = T.bilateral(c, 3, 4.5, 0.03)
+    assert f[2, 3] == 0.0 and np.allclose(np.delete(f.ravel(), 2 * 7 + 3), 1.7, rtol=0, atol=1e-15)
+    # a 1 m step is preserved (range weight exp(-1 / (2 * 0.03^2)) underflows)
+    s = np.ones((5, 8))
+    s[:, 4:] = 2.0
+    assert np.array_equal(T.bilateral(s, 3, 4.5, 0.03), s)
+    # noise is reduced on a plane
+    n = 2.0 + 0.01 * rng.standard_normal((40, 40))
+    assert np.std(T.bilateral(n, 3, 4.5, 0.03)[5:-5, 5:-5] - 2.0) < 0.5 * np.std(n - 2.0)
+
+
+def test_filtered_track_recovers_a_known_motion():
+    """R-ICP-FILT on ToF-noisy depth (cfg2): the filtered ICP recovers the true motion, closer
+    than the unfiltered one, with most valid pixels kept as inliers."""
+    cfg = S.get_config("cfg2", noise="tof", dropout=0.0)
+    R0, t0 = S.trajectory(cfg, 1)[0]
+    R0, t0 = np.asarray(R0, np.float64), np.asarray(t0, np.float64)
+    R1 = _rot([0.3, 1.0, 0.2], 0.5) @ R0
+    t1 = t0 + np.array([0.004, -0.003, 0.002])
+    f0 = _frame(S.get_config("cfg2", noise="none", dropout=0.0), R0, t0)
+    f1 = _frame(cfg, R1, t1)
+    V, N = _model(f0)
+    K = (cfg.fx, cfg.fy, cfg.cx, cfg.cy)
+    d = f1.depth.numpy().view(np.uint16)
+    R, t, info = T.track(d, cfg.depth_scale, K, V, N, R0, t0, R0, t0, T.IcpCfg(filter_radius=3))
+    Ru, tu, _ = T.track(d, cfg.depth_scale, K, V, N, R0, t0, R0, t0, T.IcpCfg(filter_radius=0))
+    assert info["converged"] and info["inlier_frac"] > 0.9 and info["pivot_ratio"] > 1e-3
+    assert np.linalg.norm(t - t1) < 2e-4 and _angle_deg(R, R1) < 0.01
+    assert np.linalg.norm(t - t1) < np.linalg.norm(tu - t1)

@@ -39,6 +39,21 @@ def run(cfg, frames, history, eager, n_g, watch=None, icp=None):
     return np.array(err), vol.stats()["n_blocks"], pipe.track_log
 
 
+def bilateral(d_u16: torch.Tensor, scale: float, r=3, sig_s=4.5, sig_r=0.03) -> torch.Tensor:
+    """Diagnostic-only depth pre-filter (KinectFusion-style bilateral), torch ops."""
+    z = (d_u16.view(torch.int16).to(torch.int32) & 0xFFFF).to(torch.float32) / scale
+    H, W = z.shape
+    zp = torch.nn.functional.pad(z[None, None], (r, r, r, r))
+    patches = torch.nn.functional.unfold(zp, 2 * r + 1).view((2 * r + 1) ** 2, H, W)
+    yy, xx = torch.meshgrid(torch.arange(-r, r + 1), torch.arange(-r, r + 1), indexing="ij")
+    ws = torch.exp(-(xx ** 2 + yy ** 2).float() / (2 * sig_s ** 2)).reshape(-1, 1, 1).to(z.device)
+    wr = torch.exp(-((patches - z[None]) ** 2) / (2 * sig_r ** 2)) * (patches > 0)
+    w = ws * wr
+    out = (w * patches).sum(0) / w.sum(0).clamp_min(1e-12)
+    out = torch.where(z > 0, out, torch.zeros_like(out))
+    return torch.round(out * scale).to(torch.int32).to(torch.int16).contiguous()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="cfg4")
@@ -48,7 +63,9 @@ def main():
     ap.add_argument("--detail", type=int, default=0, help="print ICP records of this many frames before failure")
     ap.add_argument("--watch", type=int, nargs=2, default=None, help="print model-map stats for these frames")
     ap.add_argument("--angle", type=float, default=30.0)
+    ap.add_argument("--filter", type=int, default=3, help="R-ICP-FILT radius (0 = off)")
     ap.add_argument("--dist", type=float, default=0.1)
+    ap.add_argument("--prefilter", action="store_true", help="bilateral-filter the depth frames first")
     ap.add_argument("--clean", action="store_true", help="noise-free depth")
     ap.add_argument("--both", action="store_true", help="also the deferred read-back")
     a = ap.parse_args()
@@ -59,9 +76,10 @@ def main():
     frames = []
     for k in range(a.frames):
         fr = S.render_frame(cfg, scene, *poses[k], k=k, device="cuda", dc=dc)
-        frames.append((fr.depth.contiguous(), fr.rgba.contiguous(), fr.R, fr.t))
+        dep = bilateral(fr.depth, cfg.depth_scale) if a.prefilter else fr.depth.contiguous()
+        frames.append((dep, fr.rgba.contiguous(), fr.R, fr.t))
     for eager in (True, False):
-        icp = G.IcpConfig(angle_max_deg=a.angle, dist_max=a.dist)
+        icp = G.IcpConfig(angle_max_deg=a.angle, dist_max=a.dist, filter_radius=a.filter)
         err, nb, log = run(cfg, frames, a.history, eager, a.gaussians, watch=a.watch, icp=icp)
         bad = np.nonzero(err > 0.02)[0]
         print(f"eager={eager}: max err {err.max():.4f} m, rmse {np.sqrt(np.mean(err ** 2)):.4f}, blocks {nb}, "
