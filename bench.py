@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--tile", type=int, default=16)
     ap.add_argument("--sort-free", action="store_true",
                     help="the paper's sort-free renderer (P:99-100) instead of the depth-sorted tile lists")
+    ap.add_argument("--backward", type=int, default=0, choices=[0, 1, 2],
+                    help="gradient scheme: 0 the renderer's own, 1 warp per entry, 2 thread per (entry, pixel group)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-profile", action="store_true", help="time without the per-launch event profiler")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -173,7 +175,7 @@ def run_ours(args):
     vol = G.Volume(voxel_size=cfg.voxel_size, max_blocks=cfg.max_blocks, hash_slots=cfg.hash_slots,
                    dense_bounds=S.scene_bounds(cfg))
     g = G.Gaussians.from_dict(gd, capacity=4 * n_g if args.manage_gaussians else None)
-    rcfg = G.RenderConfig(tile=args.tile, sort_free=int(args.sort_free))
+    rcfg = G.RenderConfig(tile=args.tile, sort_free=int(args.sort_free), backward=args.backward)
     pipe = MappingPipeline(cam, g, vol, cfg.depth_scale, rcfg, seed=rank,
                            overlap=not args.no_overlap, refine_priority=args.refine_priority,
                            manage_gaussians=args.manage_gaussians, all_views_per_iteration=args.all_views,
@@ -426,7 +428,8 @@ def workload_config(args, cfg, n_g, ws):
                         f"(SH deg {args.sh_degree}), voxel {cfg.voxel_size} m, delta_k=10, 20 iters/round, "
                         f"6 views/round ({vpi}); step = 10 frames",
             "frames_per_step": 10, "gaussians": n_g, "sh_degree": args.sh_degree, "tile": args.tile,
-            "renderer": "sort-free (P:99-100)" if args.sort_free else "depth-sorted tile lists",
+            "renderer": ("sort-free (P:99-100)" if args.sort_free else "depth-sorted tile lists")
+                        + {0: "", 1: ", warp-per-entry backward", 2: ", thread-per-group backward"}[args.backward],
             "gaussian_management": "adding (Eq. 6) + removal (Eq. 8) every round" if args.manage_gaussians else "off",
             "views_per_iteration": "all (S:471)" if args.all_views else "one (R-VIEW)",
             "poses": "ICP-tracked every frame (Eq. 5)" if args.track else "given (ground truth)",

@@ -190,7 +190,10 @@ typedef struct {
                       * 1: the paper's sort-free rendering (Table 7): lists
                       *    stay unsorted -- Eqs. 1-2 are order-free sums -- and every entry is
                       *    depth-tested; same C*, W_G up to fp32 summation order               */
-  int32_t reserved;  /* 0                                                                     */
+  int32_t backward;  /* gradient scheme of gps_refine_step (same gradients up to fp32 summation
+                      * order): 0 = the renderer's own (sorted: a warp per list entry with a
+                      * warp reduction; sort-free: the paper's thread per (entry, 32-pixel
+                      * group), App. B), 1 = warp per entry, 2 = thread per group   */
 } gps_render_config;
 
 size_t gps_render_workspace_size(int64_t n, const gps_intrinsics* K /*host*/,

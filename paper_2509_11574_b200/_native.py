@@ -45,7 +45,7 @@ class gps_gaussians(C.Structure):
 class gps_render_config(C.Structure):
     _fields_ = [("eps_depth", C.c_float), ("alpha_min", C.c_float), ("near_z", C.c_float),
                 ("lowpass", C.c_float), ("tile", C.c_int32), ("tile_depth_precull", C.c_int32),
-                ("max_pairs", C.c_int64), ("sort_free", C.c_int32), ("reserved", C.c_int32)]
+                ("max_pairs", C.c_int64), ("sort_free", C.c_int32), ("backward", C.c_int32)]
 
 
 class gps_adam_config(C.Structure):

@@ -286,10 +286,11 @@ class RenderConfig:
     tile_depth_precull: int = 1
     max_pairs: int = 0
     sort_free: int = 0               # 1: the paper's sort-free rendering
+    backward: int = 0                # 0: the renderer's own scheme, 1: warp per entry, 2: thread per group
 
     def c(self) -> N.gps_render_config:
         return N.gps_render_config(self.eps_depth, self.alpha_min, self.near_z, self.lowpass, self.tile,
-                                   self.tile_depth_precull, self.max_pairs, self.sort_free, 0)
+                                   self.tile_depth_precull, self.max_pairs, self.sort_free, self.backward)
 
 
 @dataclass

@@ -1908,6 +1908,7 @@ gps_status check_render_cfg(const gps_render_config* c) {
   if (!(c->eps_depth >= 0) || !(c->alpha_min >= 0) || !(c->lowpass >= 0)) return invalid("render config: bad value");
   if (c->max_pairs < 0 || c->max_pairs > 0xFFFFFFFFll) return invalid("render config: bad max_pairs");
   if (c->sort_free != 0 && c->sort_free != 1) return invalid("render config: sort_free must be 0 or 1");
+  if (c->backward < 0 || c->backward > 2) return invalid("render config: backward must be 0, 1 or 2");
   return GPS_OK;
 }
 
@@ -2034,7 +2035,7 @@ gps_status gps_refine_step(gps_gaussians* g, gps_adam_state* state, const gps_vi
     GPS_PROF(K_BACKWARD, s);
     // sort-free (the paper's renderer, App. B): a thread per (entry, pixel group);
     // sorted (this build's tile design): a warp per entry with a warp reduction
-    const bool items = rcfg->sort_free != 0;
+    const bool items = rcfg->backward == 2 || (rcfg->backward == 0 && rcfg->sort_free != 0);
     float* g2 = reinterpret_cast<float*>(grad2d);
     if (items) {
       if (rcfg->tile == 16)

@@ -53,13 +53,15 @@ def test_sortfree_and_sorted_images_agree():
     assert abs(l1 - l0) <= 1e-5 * l0
 
 
-@pytest.mark.parametrize("tile", [16, 8])
-def test_sortfree_refine_gradients_match_oracle(tile):
+@pytest.mark.parametrize("tile,backward", [(16, 0), (8, 0), (16, 1), (8, 1)])
+def test_sortfree_refine_gradients_match_oracle(tile, backward):
+    """backward 0: the paper's thread-per-group scheme; 1: the warp-per-entry backward on the
+    unsorted lists (order-free: no transmittance)."""
     G, cfg, fr, gd, Dt, Ct, tgt, gcam, ocam, dev = setup()
     g = G.Gaussians.from_dict(gd)
     st = G.AdamState(g)
     gout = g.zeros_like()
-    ras = G.Rasterizer(g.n, gcam, G.RenderConfig(tile=tile, sort_free=1))
+    ras = G.Rasterizer(g.n, gcam, G.RenderConfig(tile=tile, sort_free=1, backward=backward))
     ras.refine_step(g, st, [G.View(gcam, fr.R, fr.t, dev["Dt"], dev["Ct"], dev["tgt"])], grad_out=gout)
     oloss, ref, gamb = oracle_grads(gd, ocam, fr.R, fr.t, Dt, Ct, tgt)
     compare_grads(gout.to_numpy(), ref, gamb)
