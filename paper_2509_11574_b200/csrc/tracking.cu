@@ -554,8 +554,7 @@ static gps_status track_impl(const gps_intrinsics* K, const uint16_t* depth, flo
     L.stride = 1 << l;
     k_icp_maps<<<dim3((L.W + 15) / 16, (L.H + 15) / 16), 256, 0, s>>>(L, dp);
     GPS_CHECK_LAUNCH("k_icp_maps");
-    static const int ctas = getenv("GPS_ICP_CTAS") ? atoi(getenv("GPS_ICP_CTAS")) : 148 * 3;
-    const int nblk = std::min((L.W * L.H + kIcpThreads - 1) / kIcpThreads, ctas);  // grid-stride, one wave at 3 CTAs/SM
+    const int nblk = std::min((L.W * L.H + kIcpThreads - 1) / kIcpThreads, 148 * 3);  // grid-stride, one wave at 3 CTAs/SM
     for (int it = 0; it < cfg->iters[l]; ++it) {
       k_icp_step<<<nblk, kIcpThreads, 0, s>>>(L, a, dp, partial);
       GPS_CHECK_LAUNCH("k_icp_step");

@@ -228,3 +228,23 @@ def test_filtered_track_matches_oracle():
     assert np.linalg.norm(res["t"] - to) < 2e-5 and _angle_deg(res["R"], Ro) < 2e-3
     assert abs(res["inlier_frac"] - info["inlier_frac"]) < 2e-3
     assert abs(res["pivot_ratio"] - info["pivot_ratio"]) < 1e-3 * info["pivot_ratio"] + 1e-6
+
+
+def test_track_full_size_cfg4():
+    """The pipeline's tracking configuration (R-ICP-FILT on) at the bench's full 1280x720 on the
+    ToF-noisy cfg4 sensor model: GPU pose = oracle pose within the tracking bars."""
+    import paper_2509_11574_b200 as G
+    cfg = S.get_config("cfg4")
+    R0, t0 = S.trajectory(cfg, 1)[0]
+    R0, t0 = np.asarray(R0, np.float64), np.asarray(t0, np.float64)
+    R1 = _rot([0.2, 1.0, -0.1], 0.4) @ R0
+    t1 = t0 + np.array([0.005, 0.002, -0.004])
+    f0, f1 = _frame(S.get_config("cfg4", noise="none", dropout=0.0), R0, t0), _frame(cfg, R1, t1)
+    V, N = _model(f0)
+    depth = f1.depth.numpy().view(np.uint16)
+    K = (cfg.fx, cfg.fy, cfg.cx, cfg.cy)
+    Ro, to, info = OT.track(depth, cfg.depth_scale, K, V, N, R0, t0, R0, t0, OT.IcpCfg(filter_radius=3))
+    res = _gpu_track(G, cfg, depth, V, N, R0, t0, R0, t0, G.IcpConfig(filter_radius=3))
+    assert res["converged"] == info["converged"] and res["converged"]
+    assert np.linalg.norm(res["t"] - to) < 2e-5 and _angle_deg(res["R"], Ro) < 2e-3
+    assert np.linalg.norm(res["t"] - t1) < 2e-3 and _angle_deg(res["R"], R1) < 0.1
