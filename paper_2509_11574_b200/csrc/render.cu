@@ -848,6 +848,7 @@ __global__ void __launch_bounds__(128) k_sort_blend16x2(RenderArgs a, const floa
                                                         WsHeader* hdr, BlendIO io, int precull) {
   constexpr int NT = 128, NB = 256;  // threads, staged entries per batch (2 per thread)
   __shared__ __align__(16) uint64_t skeys[NB + 2];
+  __shared__ __align__(16) uint32_t sdep[NB + 4];
   __shared__ float4 s0[NB], s1[NB], s2[NB];  // s0 = (px, py, a, 2b); s1 = (c, ln sigma, d, q_max)
   __shared__ float red[NT / 32 + 1];
   __shared__ uint32_t redi[NT / 32 + 1];
@@ -860,35 +861,66 @@ __global__ void __launch_bounds__(128) k_sort_blend16x2(RenderArgs a, const floa
   // ---- per-tile sort by (depth bits, index) ----
   if (!SORTED) {
   } else if (small) {
-    // rank sort, two keys per thread
+    // rank sort, two keys per thread.  The rank is first counted on the 32-bit depth bits alone
+    // (four per 16-byte shared load); it equals the (depth bits, index) rank unless two entries
+    // share a depth, which shows as a slot left unwritten by the scatter -- then the tile is
+    // re-ranked on the full 64-bit keys.
     uint64_t key[2] = {~0ull, ~0ull};
+    uint32_t dk[2] = {~0u, ~0u};
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int e = threadIdx.x + h * NT;
       if (e < n) {
         const uint32_t idx = vals[start + e];
-        key[h] = ((uint64_t)__float_as_uint(rec[4 * idx + 1].z) << 32) | idx;
-        skeys[e] = key[h];
+        dk[h] = __float_as_uint(rec[4 * idx + 1].z);
+        key[h] = ((uint64_t)dk[h] << 32) | idx;
+        sdep[e] = dk[h];
       }
     }
-    if (threadIdx.x == 0) skeys[n] = ~0ull;  // pad slot of the paired loads below
+    if (threadIdx.x < 4) sdep[n + threadIdx.x] = ~0u;  // pad of the 4-wide loads (never < a depth)
     __syncthreads();
     int rank[2] = {0, 0};
-    const ulonglong2* k2 = reinterpret_cast<const ulonglong2*>(skeys);
-    for (int j = 0; j < (n + 1) >> 1; ++j) {
-      const ulonglong2 kk = k2[j];
-      rank[0] += (kk.x < key[0]) + (kk.y < key[0]);
-      rank[1] += (kk.x < key[1]) + (kk.y < key[1]);
-    }
-    __syncthreads();
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int e = threadIdx.x + h * NT;
-      if (e < n) {
-        skeys[rank[h]] = key[h];
-        vals[start + rank[h]] = (uint32_t)key[h];
+    {
+      const uint4* d4 = reinterpret_cast<const uint4*>(sdep);
+      for (int j = 0; j < (n + 3) >> 2; ++j) {
+        const uint4 q = d4[j];
+        rank[0] += (q.x < dk[0]) + (q.y < dk[0]) + (q.z < dk[0]) + (q.w < dk[0]);
+        rank[1] += (q.x < dk[1]) + (q.y < dk[1]) + (q.z < dk[1]) + (q.w < dk[1]);
       }
     }
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      if (threadIdx.x + h * NT < n) skeys[threadIdx.x + h * NT] = ~0ull;  // "unwritten"
+    __syncthreads();
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      if (threadIdx.x + h * NT < n) skeys[rank[h]] = key[h];
+    __syncthreads();
+    bool hole = false;
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      if (threadIdx.x + h * NT < n) hole |= skeys[threadIdx.x + h * NT] == ~0ull;
+    if (__syncthreads_or(hole)) {  // equal depths: rank on the full keys
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        if (threadIdx.x + h * NT < n) skeys[threadIdx.x + h * NT] = key[h];
+      if (threadIdx.x == 0) skeys[n] = ~0ull;  // pad slot of the paired loads below
+      __syncthreads();
+      rank[0] = rank[1] = 0;
+      const ulonglong2* k2 = reinterpret_cast<const ulonglong2*>(skeys);
+      for (int j = 0; j < (n + 1) >> 1; ++j) {
+        const ulonglong2 kk = k2[j];
+        rank[0] += (kk.x < key[0]) + (kk.y < key[0]);
+        rank[1] += (kk.x < key[1]) + (kk.y < key[1]);
+      }
+      __syncthreads();
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        if (threadIdx.x + h * NT < n) skeys[rank[h]] = key[h];
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      if (threadIdx.x + h * NT < n) vals[start + rank[h]] = (uint32_t)key[h];
   } else {
     uint64_t* gk = gkeys + start;
     for (int e = threadIdx.x; e < n; e += NT) {
