@@ -2050,7 +2050,6 @@ gps_status gps_refine_step(gps_gaussians* g, gps_adam_state* state, const gps_vi
     GPS_CHECK_CUDA(cudaMemsetAsync(w + L.gbuf, 0, sizeof(float) * gbuf_floats(g), s));
   if (loss_out) GPS_CHECK_CUDA(cudaMemsetAsync(loss_out, 0, sizeof(float), s));
   AdamArgs ad = make_adam(acfg, state->step + 1);
-  const gps_gaussians gout = grad_out ? *grad_out : gps_gaussians{};
   for (int v = 0; v < n_views; ++v) {
     const gps_view& vw = views[v];
     View1 v1{&vw.K, &vw.T, vw.sdf_depth, vw.sdf_color, vw.target_rgba};

@@ -332,7 +332,6 @@ __global__ void __launch_bounds__(256) k_integrate(VolumeView v, FuseParams p_in
   if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&v.ctr->vis_total, (unsigned long long)nvis);
   const int e = 2 * threadIdx.x;  // voxel pair (e, e+1): same j,k; i even
   const int li = e & 7, lj = (e >> 3) & 7, lk = e >> 6;
-  const int lane = threadIdx.x & 31;
   __shared__ uint32_t scnt[8];
   uint32_t n_upd = 0;
   const uint32_t G = gridDim.x;
