@@ -91,3 +91,46 @@ def test_tile_list_beyond_shared_memory_sorts():
     ras.refine_step(g, st, [G.View(gcam, R, t, dev["Dt"], dev["Ct"], dev["tgt"])], grad_out=gout)
     oloss, ref, gamb = oracle_grads(gd, c, R, t, Dt, Ct, tgt)
     compare_grads(gout.to_numpy(), ref, gamb, min_checked=500)
+
+
+def test_pair_capacity_overflow_is_reported_and_contained():
+    """max_pairs below the frame's (tile, entry) count: the render reports
+    GPS_ERR_WORKSPACE_TOO_SMALL through gps_render_stats_sync, writes nothing past the pair
+    capacity (a guard region after the workspace stays intact), and a render with enough
+    capacity on the same Gaussians still matches the oracle."""
+    import paper_2509_11574_b200 as G
+    cfg = _ragged_cfg()
+    fr = H.frames(cfg, 1)[0]
+    gd = S.make_gaussians(cfg, n=3000, frames=[fr])
+    Dt, Ct = S.sdf_stage_inputs(cfg, fr)
+    gcam, ocam = H.cams(cfg)
+    dev = dict(Dt=torch.from_numpy(Dt).cuda(), Ct=torch.from_numpy(Ct).cuda(), tgt=fr.rgba.cuda().contiguous())
+    g = G.Gaussians.from_dict(gd)
+    ras = G.Rasterizer(g.n, gcam, G.RenderConfig(max_pairs=64))
+    n_ws = ras.ws.numel()
+    guard = torch.full((1 << 16,), 0xA5, dtype=torch.uint8, device="cuda")
+    big = torch.cat([ras.ws, guard])  # the workspace followed by a guard region
+    ras.ws = big[:n_ws]
+    ras.render(g, gcam, fr.R, fr.t, dev["Dt"], dev["Ct"], dev["tgt"])
+    st = ras.stats()
+    assert st["status"] == "GPS_ERR_WORKSPACE_TOO_SMALL" and st["pairs"] > st["capacity"] == 64
+    assert bool((big[n_ws:] == 0xA5).all())
+    ok = G.Rasterizer(g.n, gcam, G.RenderConfig())
+    Cs, W, _ = ok.render(g, gcam, fr.R, fr.t, dev["Dt"], dev["Ct"], dev["tgt"])
+    assert ok.stats()["status"] == "GPS_OK"
+    check_forward(O.render(gd, ocam, fr.R, fr.t, Dt, Ct), Cs.cpu().numpy(), W.cpu().numpy())
+
+
+def test_tracking_rejects_bad_configs():
+    import paper_2509_11574_b200 as G
+    from paper_2509_11574_b200 import _native as N
+    cfg = _ragged_cfg()
+    fr = H.frames(cfg, 1)[0]
+    cam = G.Camera(cfg.fx, cfg.fy, cfg.cx, cfg.cy, cfg.width, cfg.height)
+    V = torch.zeros((cfg.height, cfg.width, 3), dtype=torch.float32, device="cuda")
+    eye = np.eye(3, dtype=np.float32)
+    for bad in (dict(levels=0), dict(levels=5), dict(filter_radius=9), dict(min_pivot_ratio=-1.0),
+                dict(filter_radius=2, filter_sigma_r=0.0)):
+        with pytest.raises(N.GPSError):
+            G.track(cam, fr.depth.cuda(), cfg.depth_scale, V, V, eye, np.zeros(3), eye, np.zeros(3),
+                    G.IcpConfig(**bad))
