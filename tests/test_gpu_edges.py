@@ -134,3 +134,28 @@ def test_tracking_rejects_bad_configs():
         with pytest.raises(N.GPSError):
             G.track(cam, fr.depth.cuda(), cfg.depth_scale, V, V, eye, np.zeros(3), eye, np.zeros(3),
                     G.IcpConfig(**bad))
+
+
+def test_empty_gaussian_set():
+    """N = 0 (no preprocess launch): the render is the SDF image itself (C* = C_t, W_G = 0, no
+    pairs), the loss is the oracle's, and a refine step is a no-op that still counts the step."""
+    import paper_2509_11574_b200 as G
+    cfg = _ragged_cfg()
+    fr = H.frames(cfg, 1)[0]
+    gd = S.make_gaussians(cfg, n=0, frames=[fr])
+    Dt, Ct = S.sdf_stage_inputs(cfg, fr)
+    gcam, ocam = H.cams(cfg)
+    tgt = fr.rgba.numpy()
+    dev = dict(Dt=torch.from_numpy(Dt).cuda(), Ct=torch.from_numpy(Ct).cuda(), tgt=fr.rgba.cuda().contiguous())
+    g = G.Gaussians.from_dict(gd)
+    assert g.n == 0
+    ras = G.Rasterizer(max(g.n, 1), gcam, G.RenderConfig())
+    Cs, W, loss = ras.render(g, gcam, fr.R, fr.t, dev["Dt"], dev["Ct"], dev["tgt"])
+    assert np.array_equal(Cs.cpu().numpy(), Ct) and not W.cpu().numpy().any()
+    assert ras.stats()["pairs"] == 0
+    out = O.render(gd, ocam, fr.R, fr.t, Dt, Ct)
+    ol, _, _, _ = O.l1_loss(out["Cstar"], out["WG"], Dt, tgt)
+    assert abs(loss.item() - ol) <= 1e-5 * max(ol, 1e-6)
+    st = G.AdamState(g)
+    ras.refine_step(g, st, [G.View(gcam, fr.R, fr.t, dev["Dt"], dev["Ct"], dev["tgt"])])
+    assert st.step == 1
