@@ -120,7 +120,8 @@ gps_status gps_volume_stats_sync(gps_volume* vol, gps_stream_t stream, int64_t* 
  *     block is inserted into the hash (R-BAND) and marked visible for this frame.
  * (2) Integration: every voxel of every visible block is projected to its nearest pixel; with
  *     eta = depth - z: skipped if eta < -mu, else s = min(1, eta/mu),
- *     tsdf <- (tsdf*w + s)/(w+1), rgb <- integer rounded running mean, w <- min(w+1, w_max)
+ *     tsdf <- (tsdf*w + s)*fl(1/(w+1)) (one correctly rounded reciprocal, then a multiply),
+ *     rgb <- the exact rational running mean rounded half up, w <- min(w+1, w_max)
  *     (R-INT).  Allocation and tsdf use the prescribed fp32 sequences of DESIGN.md §4 (no FMA
  *     contraction) so that they are bit-reproducible.
  * depth: u16[height*width] row-major; metres = depth/depth_scale; 0 = invalid.

@@ -159,9 +159,12 @@ def test_colour_running_mean_worked_example():
 
 
 def test_first_observation_copies_sample():
-    """with w = 0 the update gives exactly s = min(1, eta/mu) (no averaging)."""
+    """with w = 0 the update gives s = min(1, eta/mu) (no averaging).  Checked against
+    the fp64 closed form (Z0 - z)/mu of a fronto-parallel plane, independent of the oracle's
+    fp32 evaluation order (fp32 rounding of voxel position, depth and sample: <= 5e-6)."""
     c = cam()
-    depth, rgba = const_frame(c, 0.30)
+    Z0 = 0.30
+    depth, rgba = const_frame(c, Z0)
     v = O.Volume()
     v.fuse(c, np.eye(3), np.zeros(3), depth, 1e4, rgba)
     co, ts, cw = v.blocks()
@@ -169,11 +172,98 @@ def test_first_observation_copies_sample():
     # on the optical axis column of voxels (x = y = 0) the pixel is the principal point area
     sel = (np.abs(P[..., 0]) < 1e-9) & (np.abs(P[..., 1]) < 1e-9) & (cw[..., 3] == 1)
     assert sel.sum() >= 5
-    z = P[..., 2][sel].astype(np.float32)
-    # the sample s of DESIGN.md §4.2: d = raw * fl(1/scale), s = min(1, (d - z) * fl(1/mu))
-    d = np.float32(3000) * (np.float32(1.0) / np.float32(1e4))
-    expect = np.minimum(np.float32(1.0), (d - z) * (np.float32(1.0) / np.float32(MU)))
-    assert np.max(np.abs(ts[sel] - expect)) == 0.0
+    z = P[..., 2][sel]
+    expect = np.minimum(1.0, (Z0 - z) / MU)
+    assert np.any(expect < 0) and np.any((expect > 0) & (expect < 1)) and np.any(expect == 1.0)
+    assert np.max(np.abs(ts[sel] - expect)) <= 5e-6
+
+
+def _plane_frames_pin(c, depths, rgbs, w_max=100):
+    """Fuse fronto-parallel planes at the given depths (identity pose) and return, per voxel,
+    (tsdf, rgbw, world z, clear mask): voxels away from the pixel-rounding boundaries that
+    project inside the image, away from every frame's -mu decision boundary."""
+    v = O.Volume(w_max=w_max)
+    for Z, rgb in zip(depths, rgbs):
+        d, col = const_frame(c, Z, rgb)
+        v.fuse(c, np.eye(3), np.zeros(3), d, 1e4, col)
+    co, ts, cw = v.blocks()
+    P = voxel_world(co)
+    z = P[..., 2]
+    u = c.fx * P[..., 0] / np.where(z > 0, z, 1) + c.cx
+    vv = c.fy * P[..., 1] / np.where(z > 0, z, 1) + c.cy
+    ui, vi = np.floor(u + 0.5), np.floor(vv + 0.5)
+    inside = (z > 0) & (ui >= 0) & (ui <= c.width - 1) & (vi >= 0) & (vi <= c.height - 1) \
+        & (np.abs(u + 0.5 - np.round(u + 0.5)) > 1e-3) & (np.abs(vv + 0.5 - np.round(vv + 0.5)) > 1e-3)
+    clear = inside.copy()
+    for Z in depths:
+        clear &= np.abs((Z - z) + MU) > 1e-4
+    return ts, cw, z, clear
+
+
+def test_tsdf_is_the_weighted_mean_of_the_samples():
+    """P:60 / P:106 "standard SDF fusion" (reading R-INT): after frames at DISTINCT depths the
+    voxel's tsdf is the mean of the samples s_k = min(1, (Z_k - z)/mu) of the frames that
+    updated it (eta_k >= -mu), w = their number; a voxel no frame updated keeps tsdf 1, w 0.
+    fp64 closed form; an update rule that ignores the weight (e.g. (tsdf + s)/2) fails it."""
+    c = cam()
+    depths = (0.30, 0.315, 0.33)
+    ts, cw, z, clear = _plane_frames_pin(c, depths, [(9, 9, 9)] * 3)
+    S = np.stack([np.minimum(1.0, (Z - z) / MU) for Z in depths])           # (3, n, 512)
+    upd = np.stack([(Z - z) >= -MU for Z in depths])
+    n_upd = upd.sum(0)
+    mean = np.where(n_upd > 0, (S * upd).sum(0) / np.maximum(n_upd, 1), 1.0)
+    w = cw[..., 3]
+    assert np.all(w[clear] == n_upd[clear])
+    for k in (1, 2, 3):
+        sel = clear & (n_upd == k)
+        assert sel.sum() >= 20, (k, sel.sum())
+        assert np.max(np.abs(ts[sel] - mean[sel])) <= 5e-6, k
+    # voxels whose samples differ across frames (not all clamped to 1): the mean is informative
+    informative = clear & (n_upd == 3) & (np.ptp(np.where(upd, S, 0), axis=0) > 0.1)
+    assert informative.sum() >= 20
+    assert np.all(ts[clear & (n_upd == 0)] == 1.0)
+
+
+def test_weight_cap_running_mean_closed_form():
+    """R-WMAX with distinct samples: w_max = 2, three frames.  The third update weighs the
+    stored mean by the capped weight: tsdf = (2*mean(s1, s2) + s3)/3, w = 2."""
+    c = cam()
+    depths = (0.30, 0.31, 0.32)
+    ts, cw, z, clear = _plane_frames_pin(c, depths, [(9, 9, 9)] * 3, w_max=2)
+    s = [np.minimum(1.0, (Z - z) / MU) for Z in depths]
+    all3 = clear & np.all(np.stack([(Z - z) >= -MU for Z in depths]), 0)
+    assert all3.sum() >= 20
+    exp = (2.0 * (s[0] + s[1]) / 2.0 + s[2]) / 3.0
+    assert np.max(np.abs(ts[all3] - exp[all3])) <= 5e-6
+    assert np.all(cw[..., 3][all3] == 2)
+
+
+def _round_half_up_mean(values):
+    """the exact rational running mean of u8 observations, rounded half up at each update
+    (R-INT), computed with exact fractions: floor(mean + 1/2) -- never the integer formula."""
+    from fractions import Fraction
+    c, w = 0, 0
+    for x in values:
+        m = Fraction(c * w + x, w + 1)
+        c = int(np.floor(m + Fraction(1, 2)))
+        w += 1
+    return c
+
+
+@pytest.mark.parametrize("seq", [(51, 154), (10, 20, 32), (200, 3, 101, 7), (255, 0), (0, 255)])
+def test_colour_mean_rounds_half_up(seq):
+    """R-INT colour: the per-channel running mean is the exact rational mean rounded half up
+    (51, 154 -> 102.5 -> 103; 10, 20, 32 -> 15 then 62/3 + ... -> 21).  A truncating mean
+    fails the .5 and the w = 2 cases."""
+    c = cam()
+    v = O.Volume()
+    for x in seq:
+        d, col = const_frame(c, 0.5, (x, x, x))
+        v.fuse(c, np.eye(3), np.zeros(3), d, 1e4, col)
+    _, _, cw = v.blocks()
+    seen = cw[..., 3] == len(seq)
+    assert seen.sum() > 100
+    assert np.all(cw[..., :3][seen] == _round_half_up_mean(seq))
 
 
 def test_budget_overflow_flag():

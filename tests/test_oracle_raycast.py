@@ -117,3 +117,25 @@ def test_sphere_rmse_below_voxel():
     rmse = np.sqrt(np.mean((D[both] - z[both]) ** 2))
     assert rmse < 0.005, rmse
     assert np.max(np.abs(col[both] - 180 / 255.0)) < 1e-9
+
+
+def test_negative_region_entered_from_unobserved_space_is_a_miss():
+    """R-RAY "invalid predecessor => miss" ("find the zero crossing": a crossing needs a
+    valid positive sample before the first valid non-positive one).  A plane fused from the
+    front (Z0 = 0.4 m) and raycast from BEHIND it: the rays come from unobserved voxels (w = 0,
+    invalid) straight into the negative band behind the surface, so no +/- crossing exists and
+    every pixel is a miss.  Seen from the front the same volume is hit everywhere."""
+    c = cam()
+    Z0 = 0.4
+    depth = np.full((c.height, c.width), 4000, np.uint16)
+    rgba = np.full((c.height, c.width, 4), 77, np.uint8)
+    v = O.Volume()
+    v.fuse(c, np.eye(3), np.zeros(3), depth, 1e4, rgba)
+    Rb = np.array([[-1, 0, 0], [0, 1, 0], [0, 0, -1]], np.float32)   # looking along -z
+    tb = np.array([0.0, 0.0, 0.8], np.float32)                       # 0.4 m behind the plane
+    D, col, _, margin = v.raycast(c, Rb, tb)
+    assert np.all(D == 0) and np.all(col == 0)
+    # the rays do reach valid, negative samples (so the miss is the predecessor rule, not range)
+    assert np.sum(margin < 1.0) > 0.5 * D.size
+    Df, _, _, _ = v.raycast(c, np.eye(3), np.zeros(3))
+    assert np.mean(Df > 0) > 0.8

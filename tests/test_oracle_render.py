@@ -178,6 +178,22 @@ def test_l1_worked_example():
     assert l0 == 0 and c0 == 0 and np.all(g0 == 0)
 
 
+def test_l1_mask_includes_gaussian_only_pixels():
+    """R-L1 mask M = {D_t > 0 or W_G > 0} (P:15 Gaussians fill "missing data"): a pixel
+    the SDF missed (D_t = 0) but a Gaussian covers (W_G > 0) is in the loss and gets a
+    gradient; a pixel with neither is not.  Three pixels, hand-computed:
+    |C* - C_k| sums 0.3 (SDF hit) + 1.2 (Gaussian only) over |M| = 2 -> L = 1.5/6 = 0.25."""
+    tgt = np.zeros((1, 3, 4), np.uint8)
+    Cs = np.array([[[0.1] * 3, [0.4] * 3, [0.9] * 3]])
+    Dt = np.array([[0.5, 0.0, 0.0]])
+    WG = np.array([[0.0, 0.3, 0.0]])
+    loss, grad, cnt, _ = O.l1_loss(Cs, WG, Dt, tgt)
+    assert cnt == 2
+    assert abs(loss - 0.25) < 1e-15
+    assert np.allclose(grad[0, 0], 1 / 6) and np.allclose(grad[0, 1], 1 / 6)
+    assert np.all(grad[0, 2] == 0)
+
+
 GROUPS = ("xyz", "log_scale", "rot", "opacity_raw", "sh")
 
 
