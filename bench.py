@@ -55,6 +55,10 @@ def parse():
                     help="every iteration renders all the round's views (SPEC S:471 variant, NEXT-4)")
     ap.add_argument("--no-overlap", action="store_true",
                     help="refinement on the fusion stream (serial schedule) instead of its own stream")
+    ap.add_argument("--dense-grid", default="workspace", choices=["none", "workspace", "scene"],
+                    help="dense block-index grid (an accelerator; results do not depend on it): none (hash "
+                         "only); workspace (a fixed 25.6 m cube centred on the first camera position, the hash "
+                         "beyond it; no scene knowledge); scene (the synthetic room's ground-truth bounds)")
     ap.add_argument("--cpu-seconds", type=float, default=20.0, help="budget of the cpu_baseline sample")
     return ap.parse_args()
 
@@ -68,10 +72,23 @@ def dist_env():
 
 
 def rank_config(name: str, rank: int, world: int):
-    """Config 5: with several GPUs every rank maps its own independent sequence
-    (seed 40 + rank: a different room and trajectory); a single GPU runs the config's own seed."""
+    """Config 5: with several GPUs every rank maps its own independent sequence.
+    Rank 0 runs the config's own seed at every N (so N = 1 and rank 0 of N > 1 map the same room
+    and trajectory); rank r > 0 runs seed 40 + r (a different room and trajectory)."""
     import gps_synth as S
-    return S.get_config(name, seed=40 + rank) if world > 1 else S.get_config(name)
+    return S.get_config(name) if rank == 0 else S.get_config(name, seed=40 + rank)
+
+
+WORKSPACE_HALF = 12.8  # metres: half the edge of the dense grid's cube (640^3 blocks of 4 cm, 1 GiB)
+
+
+def dense_bounds(args, S, cfg, poses):
+    if args.dense_grid == "scene":
+        return S.scene_bounds(cfg)
+    if args.dense_grid == "workspace":
+        c = np.asarray(poses[0][1], np.float64)
+        return (tuple(c - WORKSPACE_HALF), tuple(c + WORKSPACE_HALF))
+    return None
 
 
 def max_over_ranks(ms: float, device) -> float:
@@ -173,7 +190,7 @@ def run_ours(args):
     t_setup = time.time() - t0
     cam = G.Camera(cfg.fx, cfg.fy, cfg.cx, cfg.cy, cfg.width, cfg.height)
     vol = G.Volume(voxel_size=cfg.voxel_size, max_blocks=cfg.max_blocks, hash_slots=cfg.hash_slots,
-                   dense_bounds=S.scene_bounds(cfg))
+                   dense_bounds=dense_bounds(args, S, cfg, poses))
     g = G.Gaussians.from_dict(gd, capacity=4 * n_g if args.manage_gaussians else None)
     rcfg = G.RenderConfig(tile=args.tile, sort_free=int(args.sort_free), backward=args.backward)
     pipe = MappingPipeline(cam, g, vol, cfg.depth_scale, rcfg, seed=rank,
@@ -261,6 +278,7 @@ def run_ours(args):
         pipe.overlap = not args.no_overlap
     rstats = pipe.ras.stats()
     vstats = vol.stats()
+    check_status("timed window", rstats, vstats)
     ms_max = max_over_ranks(ms, "cuda")
     frames_timed = args.steps * dk
     value = job_rate(frames_timed, ws, ms_max)
@@ -284,6 +302,7 @@ def run_ours(args):
         pipe.join(stream)
         e1.record(stream)
         torch.cuda.synchronize()
+        check_status("end-to-end window", pipe.ras.stats(), vol.stats())
         ems = max_over_ranks(e0.elapsed_time(e1), "cuda")
         e2e = {"value": round(job_rate(frames_timed, ws, ems), 2), "unit": "frames/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 4,
@@ -351,18 +370,7 @@ def run_ours(args):
     # 148 SMs x 4 schedulers x 32 lanes x the sampled SM clock
     raster = None
     if args.tile == 16 and "k_sort_blend" in shares and prof["k_sort_blend"]["launches"]:
-        v = pipe.last_view
-        E, A_ = pipe.ras.pair_counts(g, cam, v.R, v.t, v.sdf_depth, v.sdf_color)
-        f_sm = 1e6 * (clk.get("sm_mhz") or 1965.0)
-        t_blend = prof["k_sort_blend"]["ms"] / prof["k_sort_blend"]["launches"] / 1000.0
-        instr = 8.0 * E + 20.0 * A_
-        peak_ti = 148 * 4 * 32 * f_sm
-        raster = {"evaluated_pairs": int(E), "accepted_pairs": int(A_), "pairs_K": rstats.get("pairs"),
-                  "blend_alu": {"bound": "alu", "model_thread_instr": int(instr),
-                                "achieved": round(instr / t_blend / 1e12, 2), "peak": round(peak_ti / 1e12, 2),
-                                "unit": "T thread-instr/s", "frac": round(instr / t_blend / peak_ti, 4),
-                                "note": "useful work of the SURVEY §8(d) model over the issue capacity; "
-                                        "ncu's issue-active and lanes/instruction are in profiles/"}}
+        raster = blend_alu(N, pipe, g, cam, clk, rstats)
     launches = int(sum(v["launches"] for kk, v in prof.items() if kk != "memset"))
     cpu = None
     if not args.no_cpu_baseline and ws == 1:  # the oracle baseline: rank 0 at N = 1 only
@@ -396,6 +404,46 @@ def run_ours(args):
     if ws > 1:
         dist.destroy_process_group()
     return line
+
+
+def blend_alu(N, pipe, g, cam, clk, rstats):
+    """Rasteriser work and the blend's ALU roofline, each view's counts over the
+    SAME view's blend time: for every view of the last round, one forward with the event profiler
+    (its k_sort_blend time) and one instrumented forward counting evaluated (E) and accepted (A)
+    pixel-entry pairs.  Model: forward ~ 8 E + 20 A thread-instructions against the issue
+    capacity 148 SMs x 4 schedulers x 32 lanes x the sampled SM clock."""
+    import torch
+    f_sm = 1e6 * (clk.get("sm_mhz") or 1965.0)
+    peak_ti = 148 * 4 * 32 * f_sm
+    E_tot = A_tot = 0
+    t_tot = 0.0
+    for v in pipe.last_views:
+        torch.cuda.synchronize()
+        N._lib.gps_profile_enable(1)
+        pipe.ras.render(g, cam, v.R, v.t, v.sdf_depth, v.sdf_color)
+        torch.cuda.synchronize()
+        t_tot += read_profile(N)["k_sort_blend"]["ms"] / 1000.0
+        N._lib.gps_profile_enable(0)
+        E, A_ = pipe.ras.pair_counts(g, cam, v.R, v.t, v.sdf_depth, v.sdf_color)
+        E_tot += E
+        A_tot += A_
+    nv = len(pipe.last_views)
+    instr = 8.0 * E_tot + 20.0 * A_tot
+    return {"views": nv, "evaluated_pairs_per_view": int(E_tot / nv), "accepted_pairs_per_view": int(A_tot / nv),
+            "pairs_K_last_render": rstats.get("pairs"),
+            "blend_alu": {"bound": "alu", "model_thread_instr_per_view": int(instr / nv),
+                          "blend_ms_per_view": round(1000 * t_tot / nv, 4),
+                          "achieved": round(instr / t_tot / 1e12, 2), "peak": round(peak_ti / 1e12, 2),
+                          "unit": "T thread-instr/s", "frac": round(instr / t_tot / peak_ti, 4),
+                          "note": "each view's E/A over the same view's blend time (the last round's views, "
+                                  "rendered alone after the timed window); ncu's issue-active and lanes per "
+                                  "instruction are in profiles/"}}
+
+
+def check_status(where, rstats, vstats):
+    """a window whose render dropped pairs or whose volume ran out of blocks is not a valid run"""
+    if rstats["status"] != "GPS_OK" or vstats["status"] != "GPS_OK":
+        raise RuntimeError(f"{where}: render {rstats['status']}, volume {vstats['status']}")
 
 
 def per_kernel_bytes(args, cfg, n_g, P, per_launch, rstats, vstats, upd0, prof):
@@ -437,7 +485,11 @@ def workload_config(args, cfg, n_g, ws):
             "parallelism": f"replicas x{ws} (independent sequences)",
             "streams": "fusion+raycast on one stream, refinement rounds on a second (P:116)"
                        if not args.no_overlap else "one stream (serial schedule)",
-            "l2": "inputs larger than L2 (per-step state > 126 MB: params+Adam 283 MB, volume)"}
+            "l2": "inputs larger than L2 (per-step state > 126 MB: params+Adam 283 MB, volume)",
+            "dense_grid": {"none": "off (hash lookups only)",
+                           "workspace": f"{2 * WORKSPACE_HALF} m cube centred on the first camera position "
+                                        "(fixed size, no scene knowledge; hash beyond it)",
+                           "scene": "the synthetic room's ground-truth bounds"}[args.dense_grid]}
 
 
 def read_profile(N):

@@ -142,8 +142,11 @@ gps_status gps_fuse(gps_volume* vol, const gps_intrinsics* K /*host*/, const gps
  * Unallocated blocks are skipped without changing the result.
  * depth_out:  f32[height*width], camera z of V* in metres; 0 = miss.
  * color_out:  f32[height*width*3], RGB in [0,1]; 0 on a miss.
- * vertex_out: nullable f32[height*width*3], V* in world metres; 0 on a miss.                 */
-gps_status gps_raycast(const gps_volume* vol, const gps_intrinsics* K /*host*/,
+ * vertex_out: nullable f32[height*width*3], V* in world metres; 0 on a miss.
+ * The call writes the volume's per-volume range-image scratch (the result does not depend on
+ * it): two raycasts of the same volume, or a raycast and a gps_fuse of it, must not run
+ * concurrently on different streams -- order them on one stream or with events.             */
+gps_status gps_raycast(gps_volume* vol, const gps_intrinsics* K /*host*/,
                        const gps_pose* T /*host*/, float* depth_out, float* color_out,
                        float* vertex_out, gps_stream_t stream);
 
@@ -155,7 +158,7 @@ gps_status gps_raycast(const gps_volume* vol, const gps_intrinsics* K /*host*/,
 gps_status gps_fuse_dpose(gps_volume* vol, const gps_intrinsics* K /*host*/,
                           const gps_pose* T_dev /*device*/, const uint16_t* depth, float depth_scale,
                           const uint8_t* rgba, gps_stream_t stream);
-gps_status gps_raycast_dpose(const gps_volume* vol, const gps_intrinsics* K /*host*/,
+gps_status gps_raycast_dpose(gps_volume* vol, const gps_intrinsics* K /*host*/,
                              const gps_pose* T_dev /*device*/, float* depth_out, float* color_out,
                              float* vertex_out, gps_stream_t stream);
 

@@ -298,8 +298,9 @@ int orc_fuse(orc_volume* v, const float* K4, int W, int H, const float* R, const
 /* ---- O4 raycast (reading R-RAY), F64 ----------------------------------------- */
 
 /* Trilinear sample at world point P (metres).  Valid iff all 8 corners are allocated with
- * w > 0 (R-RAY).  Returns validity; writes tsdf and (if col) colour in [0,255].           */
-static int tri_sample(const orc_volume* v, const double P[3], double* f, double col[3]) {
+ * w > 0 (R-RAY).  Returns validity; writes tsdf, (if col) colour in [0,255] and (if grad) the
+ * trilinear gradient in tsdf units per voxel (test diagnostics only).                       */
+static int tri_sample_g(const orc_volume* v, const double P[3], double* f, double col[3], double grad[3]) {
   double vs = (double)v->voxel;
   double p[3], fr[3];
   int32_t base[3];
@@ -309,7 +310,7 @@ static int tri_sample(const orc_volume* v, const double P[3], double* f, double 
     base[c] = (int32_t)b;
     fr[c] = p[c] - b;
   }
-  double acc = 0.0, acol[3] = {0, 0, 0};
+  double acc = 0.0, acol[3] = {0, 0, 0}, ag[3] = {0, 0, 0};
   for (int corner = 0; corner < 8; ++corner) {
     int dx = corner & 1, dy = (corner >> 1) & 1, dz = (corner >> 2) & 1;
     int32_t g[3] = {base[0] + dx, base[1] + dy, base[2] + dz};
@@ -319,21 +320,56 @@ static int tri_sample(const orc_volume* v, const double P[3], double* f, double 
     int idx = (g[0] - 8 * b[0]) + 8 * (g[1] - 8 * b[1]) + 64 * (g[2] - 8 * b[2]);
     const uint8_t* cw = v->rgbw + 2048 * bi + 4 * idx;
     if (cw[3] == 0) return 0;
-    double wgt = (dx ? fr[0] : 1.0 - fr[0]) * (dy ? fr[1] : 1.0 - fr[1]) * (dz ? fr[2] : 1.0 - fr[2]);
-    acc += wgt * (double)v->tsdf[512 * bi + idx];
+    double wx = dx ? fr[0] : 1.0 - fr[0], wy = dy ? fr[1] : 1.0 - fr[1], wz = dz ? fr[2] : 1.0 - fr[2];
+    double wgt = wx * wy * wz;
+    double val = (double)v->tsdf[512 * bi + idx];
+    acc += wgt * val;
+    ag[0] += (dx ? 1.0 : -1.0) * wy * wz * val;
+    ag[1] += (dy ? 1.0 : -1.0) * wx * wz * val;
+    ag[2] += (dz ? 1.0 : -1.0) * wx * wy * val;
     if (col)
       for (int c = 0; c < 3; ++c) acol[c] += wgt * (double)cw[c];
   }
   *f = acc;
   if (col)
     for (int c = 0; c < 3; ++c) col[c] = acol[c];
+  if (grad)
+    for (int c = 0; c < 3; ++c) grad[c] = ag[c];
   return 1;
+}
+static int tri_sample(const orc_volume* v, const double P[3], double* f, double col[3]) {
+  return tri_sample_g(v, P, f, col, NULL);
+}
+
+/* Decision margin of one sample, in voxel units of position (test diagnostics only): how far
+ * the sample point may move before a decision the march takes on it can change.  (i) sign:
+ * |f| / |grad f|_1 for a valid sample; (ii) validity: the distance to a cell face across which
+ * the validity differs (the 8-corner set changes there).  An implementation that evaluates the
+ * sample position with an error below the margin takes the same decisions.                  */
+static double sample_margin(const orc_volume* v, const double P[3], int valid, double f, const double g[3]) {
+  double m = INFINITY;
+  if (valid) {
+    double gl1 = fabs(g[0]) + fabs(g[1]) + fabs(g[2]);
+    m = fabs(f) == 0.0 ? 0.0 : (gl1 > 0.0 ? fabs(f) / gl1 : INFINITY);
+  }
+  double vs = (double)v->voxel;
+  for (int a = 0; a < 3; ++a) {
+    double pa = P[a] / vs, fa = pa - floor(pa);
+    double dist = fa < 0.5 ? fa : 1.0 - fa;
+    if (dist >= 0.05 || dist >= m) continue;
+    double Q[3] = {P[0], P[1], P[2]};
+    Q[a] = (fa < 0.5 ? floor(pa) - 1e-7 : floor(pa) + 1.0 + 1e-7) * vs; /* just across the face */
+    double fq;
+    if (tri_sample(v, Q, &fq, NULL) != valid) m = dist;
+  }
+  return m;
 }
 
 /* Raycast the listed pixels (pix = n*2 (u,v) pairs; NULL = all pixels in row-major order).
  * Outputs per listed pixel: depth (0 = miss), color (3, in [0,1]), vertex (3, nullable),
- * and `margin` (nullable): the smallest |f| over the sign decisions taken on the ray, used by
- * the tests to recognise rays where fp32 and fp64 may legitimately decide differently.     */
+ * and `margin` (nullable): the smallest sample_margin (voxel units of position) over the
+ * samples the march evaluated and the colour sample at V*, used by the tests to recognise
+ * rays where an fp32 evaluation may legitimately decide differently.                        */
 void orc_raycast(const orc_volume* v, const float* K4, int W, int H, const float* Rf,
                  const float* tf, const int32_t* pix, int64_t n, double* depth, double* color,
                  double* vertex, double* margin) {
@@ -357,9 +393,12 @@ void orc_raycast(const orc_volume* v, const float* K4, int W, int H, const float
     for (int64_t j = 0; j <= J; ++j) {
       double tj = tmin + (double)j * vs;
       double P[3] = {t[0] + tj * r[0], t[1] + tj * r[1], t[2] + tj * r[2]};
-      double f;
-      int valid = tri_sample(v, P, &f, NULL);
-      if (valid && fabs(f) < mg) mg = fabs(f);
+      double f, g[3];
+      int valid = tri_sample_g(v, P, &f, NULL, g);
+      if (margin) {
+        double ms = sample_margin(v, P, valid, f, g);
+        if (ms < mg) mg = ms;
+      }
       if (j >= 1 && valid && f <= 0.0) {
         if (prev_valid && prev_f > 0.0) {
           tstar = (tmin + (double)(j - 1) * vs) + vs * prev_f / (prev_f - f);
@@ -373,8 +412,13 @@ void orc_raycast(const orc_volume* v, const float* K4, int W, int H, const float
     double col[3] = {0, 0, 0}, V[3] = {0, 0, 0}, D = 0.0;
     if (hit) {
       for (int a = 0; a < 3; ++a) V[a] = t[a] + tstar * r[a];
-      double fdummy;
-      if (tri_sample(v, V, &fdummy, col)) {
+      double fdummy, gd[3];
+      int cv = tri_sample_g(v, V, &fdummy, col, gd);
+      if (margin) {
+        double ms = sample_margin(v, V, cv, INFINITY, gd); /* validity of the colour sample only */
+        if (ms < mg) mg = ms;
+      }
+      if (cv) {
         D = tstar / nrm; /* camera z of V*: t* times the z component of the unit ray */
         for (int a = 0; a < 3; ++a) col[a] /= 255.0;
       } else {

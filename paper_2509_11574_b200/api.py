@@ -128,10 +128,20 @@ class Volume:
              stream=None):
         """depth: u16/i16 [H,W] raw sensor units; rgba: u8 [H,W,4].  CPU tensors are copied to
         the device first (that copy is part of an end-to-end measurement)."""
-        if not depth.is_cuda:
-            depth = depth.cuda(non_blocking=True)
-        if not rgba.is_cuda:
-            rgba = rgba.cuda(non_blocking=True)
+        if not depth.is_cuda or not rgba.is_cuda:
+            # the copies run on the stream the fuse runs on, so the caching allocator cannot
+            # hand the temporaries to another stream before the kernels have read them
+            if stream is None:
+                s = torch.cuda.current_stream()
+            elif isinstance(stream, torch.cuda.Stream):
+                s = stream
+            else:
+                s = torch.cuda.ExternalStream(_stream(stream))
+            with torch.cuda.stream(s):
+                if not depth.is_cuda:
+                    depth = depth.cuda(non_blocking=True)
+                if not rgba.is_cuda:
+                    rgba = rgba.cuda(non_blocking=True)
         assert depth.element_size() == 2 and depth.numel() == cam.width * cam.height
         assert rgba.dtype == torch.uint8 and rgba.numel() == 4 * cam.width * cam.height
         N.check("gps_fuse", _L.gps_fuse(self.h, C.byref(cam.c()), C.byref(pose_struct(R, t)), _ptr(depth),

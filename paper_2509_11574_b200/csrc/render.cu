@@ -36,6 +36,31 @@ namespace gps {
 constexpr int kMaxList = 2048;  // entries a tile sorts in shared memory (16 KB of keys)
 constexpr uint32_t kWsMagic = 0x47505357u;  // "GPSW"
 
+// Pair-list overflow (K > capacity: pairs were dropped) is latched in a process-wide host-mapped
+// flag that k_scan sets; the next gps_render / gps_refine_step / gps_render_stats_sync call sees
+// it without synchronising, returns GPS_ERR_WORKSPACE_TOO_SMALL and clears it.
+struct OverflowFlag {
+  uint32_t* host = nullptr;
+  uint32_t* dev = nullptr;
+};
+OverflowFlag& overflow_flag() {
+  static OverflowFlag f = [] {
+    OverflowFlag o;
+    if (cudaHostAlloc(reinterpret_cast<void**>(&o.host), sizeof(uint32_t), cudaHostAllocMapped | cudaHostAllocPortable) ==
+            cudaSuccess &&
+        cudaHostGetDevicePointer(reinterpret_cast<void**>(&o.dev), o.host, 0) == cudaSuccess) {
+      *o.host = 0;
+    } else {
+      o.host = nullptr;
+      o.dev = nullptr;
+    }
+    return o;
+  }();
+  return f;
+}
+
+uint32_t* overflow_flag_dev() { return overflow_flag().dev; }
+
 struct WsHeader {
   uint32_t magic, tile, tiles_x, tiles_y;
   uint32_t width, height, n_tiles, pad0;
@@ -51,6 +76,7 @@ struct WsHeader {
   // ---- static: where this render's lists live (refine and render layouts differ) ----
   uint64_t off_vals, off_offsets, off_tile_end;
 };
+
 
 struct WsLayout {
   size_t hdr, counts, cursor, bigcounts, offsets, tile_end, loss_part, records, ranks, grad2d, rec3, cgj, vals, keys,
@@ -445,7 +471,8 @@ __device__ __forceinline__ void preprocess_one(const RenderArgs& a, const gps_ga
 // ============================================================================================
 __global__ void __launch_bounds__(1024) k_scan(const uint32_t* __restrict__ counts,
                                                const uint32_t* __restrict__ bigcounts, uint32_t* offsets,
-                                               int n_tiles, WsHeader* hdr, WsHeader stat) {
+                                               int n_tiles, WsHeader* hdr, WsHeader stat,
+                                               uint32_t* sticky_overflow) {
   __shared__ uint32_t warp_sums[32];
   __shared__ uint32_t carry;
   if (threadIdx.x == 0) carry = 0;
@@ -493,6 +520,10 @@ __global__ void __launch_bounds__(1024) k_scan(const uint32_t* __restrict__ coun
     hdr->off_vals = stat.off_vals; hdr->off_offsets = stat.off_offsets; hdr->off_tile_end = stat.off_tile_end;
     hdr->K = carry;
     hdr->overflow = carry > stat.cap_pairs ? 1u : 0u;
+    if (carry > stat.cap_pairs) {  // host-mapped and sticky: reported by the next call
+      *reinterpret_cast<volatile uint32_t*>(sticky_overflow) = 1u;
+      __threadfence_system();
+    }
   }
 }
 
@@ -1884,7 +1915,7 @@ gps_status forward_view(const gps_gaussians* g, const View1& v, const gps_render
   uint32_t* offsets = reinterpret_cast<uint32_t*>(ws + L.offsets);
   {
     GPS_PROF(K_SCAN, s);
-    k_scan<<<1, 1024, 0, s>>>(sp.counts, sp.bigcounts, offsets, n_tiles, hdr, stat);
+    k_scan<<<1, 1024, 0, s>>>(sp.counts, sp.bigcounts, offsets, n_tiles, hdr, stat, overflow_flag_dev());
   }
   GPS_CHECK_LAUNCH("k_scan");
   uint32_t* vals = reinterpret_cast<uint32_t*>(ws + L.vals);
@@ -1931,6 +1962,23 @@ gps_status forward_view(const gps_gaussians* g, const View1& v, const gps_render
   }
   }
   GPS_CHECK_LAUNCH("k_sort_blend");
+  return GPS_OK;
+}
+
+
+// returns GPS_ERR_WORKSPACE_TOO_SMALL (and clears the flag) if an earlier render overflowed
+gps_status check_render_overflow(const char* who) {
+  OverflowFlag& f = overflow_flag();
+  if (!f.host) {
+    set_error(std::string(who) + ": could not allocate the host-mapped overflow flag");
+    return GPS_ERR_CUDA;
+  }
+  if (*reinterpret_cast<volatile uint32_t*>(f.host)) {
+    *reinterpret_cast<volatile uint32_t*>(f.host) = 0;
+    set_error(std::string(who) + ": an earlier render's (tile, Gaussian) pair list exceeded its capacity "
+              "(pairs were dropped); raise max_pairs");
+    return GPS_ERR_WORKSPACE_TOO_SMALL;
+  }
   return GPS_OK;
 }
 
@@ -1991,6 +2039,7 @@ gps_status gps_render(const gps_gaussians* g, const gps_intrinsics* K, const gps
                       size_t ws_bytes, float* out_color, float* out_weight, float* loss_out, gps_stream_t stream) {
   gps_status st = check_gaussians(g, "gps_render");
   if (st != GPS_OK) return st;
+  if ((st = check_render_overflow("gps_render")) != GPS_OK) return st;
   if ((st = check_render_cfg(cfg)) != GPS_OK) return st;
   if (!valid_K(K) || !T || !sdf_depth || !sdf_color || !ws || !out_color || !out_weight)
     return invalid("gps_render: null or bad argument");
@@ -2013,6 +2062,7 @@ gps_status gps_refine_step(gps_gaussians* g, gps_adam_state* state, const gps_vi
                            float* loss_out, const gps_gaussians* grad_out, gps_stream_t stream) {
   gps_status st = check_gaussians(g, "gps_refine_step");
   if (st != GPS_OK) return st;
+  if ((st = check_render_overflow("gps_refine_step")) != GPS_OK) return st;
   if ((st = check_render_cfg(rcfg)) != GPS_OK) return st;
   if ((st = check_adam_state(g, state)) != GPS_OK) return st;
   if (!views || n_views < 1 || !acfg || !ws) return invalid("gps_refine_step: bad argument");
@@ -2144,11 +2194,12 @@ gps_status gps_render_stats_sync(const void* ws, gps_stream_t stream, int64_t* n
   if (n_pairs) *n_pairs = h.K;
   if (capacity) *capacity = (int64_t)h.cap_pairs;
   if (n_visible) *n_visible = h.n_visible;
+  const gps_status sticky = check_render_overflow("gps_render_stats_sync");
   if (h.overflow) {
     set_error("render pair list overflow: " + std::to_string(h.K) + " pairs > capacity " + std::to_string(h.cap_pairs));
     return GPS_ERR_WORKSPACE_TOO_SMALL;
   }
-  return GPS_OK;
+  return sticky;
 }
 
 gps_status gps_debug_render_counts_sync(const gps_gaussians* g, const gps_intrinsics* K, const gps_pose* T,

@@ -1312,7 +1312,7 @@ static gps_status raycast_impl(const gps_volume* vol, const gps_intrinsics* K, c
   return GPS_OK;
 }
 
-gps_status gps_raycast(const gps_volume* vol, const gps_intrinsics* K, const gps_pose* T, float* depth_out,
+gps_status gps_raycast(gps_volume* vol, const gps_intrinsics* K, const gps_pose* T, float* depth_out,
                        float* color_out, float* vertex_out, gps_stream_t stream) {
   if (!vol || !T || !depth_out || !color_out) return invalid("gps_raycast: null argument");
   if (!valid_intrinsics(K)) return invalid("gps_raycast: bad intrinsics");
@@ -1321,7 +1321,7 @@ gps_status gps_raycast(const gps_volume* vol, const gps_intrinsics* K, const gps
   return raycast_impl(vol, K, T, depth_out, color_out, vertex_out, nullptr, stream);
 }
 
-gps_status gps_raycast_dpose(const gps_volume* vol, const gps_intrinsics* K, const gps_pose* T_dev, float* depth_out,
+gps_status gps_raycast_dpose(gps_volume* vol, const gps_intrinsics* K, const gps_pose* T_dev, float* depth_out,
                              float* color_out, float* vertex_out, gps_stream_t stream) {
   if (!vol || !T_dev || !depth_out || !color_out) return invalid("gps_raycast_dpose: null argument");
   if (!valid_intrinsics(K)) return invalid("gps_raycast_dpose: bad intrinsics");

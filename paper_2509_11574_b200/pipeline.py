@@ -395,6 +395,7 @@ class MappingPipeline:
             if add_frame is not None:
                 self._manage(rs, add_frame)
             self.last_view = views[-1]
+            self.last_views = list(views)
             for i in range(self.iterations):
                 vs = views if self.all_views else [views[Sch.view_for_iteration(i, len(views))]]
                 self.last_loss = self.ras.refine_step(self.g, self.state, vs, self.adam, stream=rs)

@@ -121,6 +121,33 @@ def test_pair_capacity_overflow_is_reported_and_contained():
     check_forward(O.render(gd, ocam, fr.R, fr.t, Dt, Ct), Cs.cpu().numpy(), W.cpu().numpy())
 
 
+def test_pair_overflow_in_an_earlier_view_is_sticky():
+    """an overflow in the FIRST view of a multi-view refine step is not lost when a
+    later view fits: the host-mapped sticky flag makes the next render / refine call return
+    GPS_ERR_WORKSPACE_TOO_SMALL (once), after which calls succeed again."""
+    import paper_2509_11574_b200 as G
+    cfg = _ragged_cfg()
+    fr = H.frames(cfg, 1)[0]
+    gd = S.make_gaussians(cfg, n=3000, frames=[fr])
+    Dt, Ct = S.sdf_stage_inputs(cfg, fr)
+    gcam, _ = H.cams(cfg)
+    dev = dict(Dt=torch.from_numpy(Dt).cuda(), Ct=torch.from_numpy(Ct).cuda(), tgt=fr.rgba.cuda().contiguous())
+    g = G.Gaussians.from_dict(gd)
+    # view 1 sees the Gaussians (overflows 64 pairs), view 2 looks away (0 pairs)
+    Rb = np.array([[-1, 0, 0], [0, 1, 0], [0, 0, -1]], np.float32) @ np.asarray(fr.R, np.float32)
+    views = [G.View(gcam, fr.R, fr.t, dev["Dt"], dev["Ct"], dev["tgt"]),
+             G.View(gcam, Rb, fr.t, dev["Dt"], dev["Ct"], dev["tgt"])]
+    ras = G.Rasterizer(g.n, gcam, G.RenderConfig(max_pairs=64), n_views=2)
+    st = G.AdamState(g)
+    ras.refine_step(g, st, views)
+    torch.cuda.synchronize()
+    with pytest.raises(G._native.GPSError) as e:
+        ras.refine_step(g, st, views[1:])
+    assert e.value.status == 3
+    ras.refine_step(g, st, views[1:])  # reported once: the next call runs
+    torch.cuda.synchronize()
+
+
 def test_tracking_rejects_bad_configs():
     import paper_2509_11574_b200 as G
     from paper_2509_11574_b200 import _native as N

@@ -87,7 +87,17 @@ def test_fuse_empty_frame_and_budget_overflow():
     assert e.value.status == 2
 
 
-def raycast_compare(cfg, gvol, ovol, R, t, pixels=None):
+# Near-tie margin, in voxel units of sample position (oracle.c sample_margin): the CUDA march
+# evaluates p = t*(r/v) + o/v in fp32 with |p| < 2^11 voxels (world coordinates < 10 m): one
+# rounding of o/v, of the product and of the sum (<= 3 * 2^-13 voxel) plus the unit ray's
+# relative error (~6 roundings, 4e-7) times t*|r|/v <= 2000 voxels (8e-4 voxel) -- <= 1.2e-3.
+TIE_VOXELS = 2e-3
+
+
+def raycast_compare(cfg, gvol, ovol, R, t, pixels=None, label=""):
+    """hit masks equal and |dD| <= 1e-4 m on >= 99.99% of the pixels whose
+    decisions are not fp32 near-ties (margin < TIE_VOXELS); C_t <= 1e-3 where both hit.  Every
+    exception and the near-tie count are printed."""
     gcam, ocam = H.cams(cfg)
     D, Ct, V = gvol.raycast(gcam, R, t, want_vertex=True)
     torch.cuda.synchronize()
@@ -99,11 +109,17 @@ def raycast_compare(cfg, gvol, ovol, R, t, pixels=None):
     od, oc, ov, margin = ovol.raycast(ocam, R, t, pixels)
     hit_g, hit_o = D > 0, od > 0
     mism = (hit_g != hit_o) | (hit_g & hit_o & (np.abs(D - od) > 1e-4))
-    # a disagreement is legitimate only where an fp32/fp64 sign decision is a near-tie
-    bad = mism & (margin > 1e-3)
+    tie = margin < TIE_VOXELS
+    bad = mism & ~tie
     n = len(D)
-    assert mism.sum() <= max(1, int(1e-4 * n)) + int(0.002 * n), f"{mism.sum()} of {n} pixels differ"
-    assert bad.sum() <= max(1, int(1e-4 * n)), f"{bad.sum()} unexplained mismatches"
+    print(f"raycast {label}: {n} px, {int(hit_o.sum())} oracle hits, {int(mism.sum())} differ "
+          f"({int((mism & tie).sum())} at near-ties, {int(bad.sum())} not), {int(tie.sum())} near-tie px")
+    for k in np.nonzero(bad)[0][:10]:
+        print(f"   px {k}: gpu D={D[k]:.6f} oracle D={od[k]:.6f} margin={margin[k]:.3g} vox")
+    assert bad.sum() <= int(1e-4 * n), f"{bad.sum()} of {n} pixels differ outside fp32 near-ties"
+    # near-ties are common on cfg1's lattice-aligned plane (depth 0.30 m = 60 voxels), but the
+    # two sides rarely take different decisions at them
+    assert (mism & tie).sum() <= max(2, int(1e-3 * n))
     both = hit_g & hit_o & ~mism
     assert both.sum() > 0.3 * n
     assert np.max(np.abs(Ct[both] - oc[both])) <= 1e-3
@@ -114,7 +130,7 @@ def test_raycast_cfg1():
     cfg = S.get_config("cfg1")
     frs = H.frames(cfg, 1)
     gvol, ovol = H.fuse_both(cfg, frs)
-    raycast_compare(cfg, gvol, ovol, frs[0].R, frs[0].t)
+    raycast_compare(cfg, gvol, ovol, frs[0].R, frs[0].t, label="cfg1")
 
 
 def test_raycast_cfg2_other_pose_sampled():
@@ -125,7 +141,7 @@ def test_raycast_cfg2_other_pose_sampled():
     R, t = S.trajectory(cfg, 1, start=5)[0]
     rng = np.random.default_rng(0)
     pix = np.stack([rng.integers(0, cfg.width, 4000), rng.integers(0, cfg.height, 4000)], 1).astype(np.int32)
-    raycast_compare(cfg, gvol, ovol, R, t, pix)
+    raycast_compare(cfg, gvol, ovol, R, t, pix, label="cfg2 other pose")
 
 
 @pytest.mark.slow
@@ -135,7 +151,7 @@ def test_raycast_full_size_cfg4_sampled():
     gvol, ovol = H.fuse_both(cfg, frs)
     rng = np.random.default_rng(1)
     pix = np.stack([rng.integers(0, cfg.width, 3000), rng.integers(0, cfg.height, 3000)], 1).astype(np.int32)
-    raycast_compare(cfg, gvol, ovol, frs[1].R, frs[1].t, pix)
+    raycast_compare(cfg, gvol, ovol, frs[1].R, frs[1].t, pix, label="cfg4")
 
 
 def test_raycast_empty_volume_misses():

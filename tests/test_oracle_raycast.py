@@ -136,6 +136,6 @@ def test_negative_region_entered_from_unobserved_space_is_a_miss():
     D, col, _, margin = v.raycast(c, Rb, tb)
     assert np.all(D == 0) and np.all(col == 0)
     # the rays do reach valid, negative samples (so the miss is the predecessor rule, not range)
-    assert np.sum(margin < 1.0) > 0.5 * D.size
+    assert np.sum(np.isfinite(margin)) > 0.5 * D.size
     Df, _, _, _ = v.raycast(c, np.eye(3), np.zeros(3))
     assert np.mean(Df > 0) > 0.8
