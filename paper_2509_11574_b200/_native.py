@@ -162,7 +162,7 @@ def load(path: str | None = None):
     global _lib
     if _lib is not None:
         return _lib
-    p = path or LIB_PATH
+    p = path or os.environ.get("GPS_LIB") or LIB_PATH  # GPS_LIB: A/B builds (tools/ab.sh) only
     if not os.path.exists(p):
         raise OSError(f"libgps.so not built at {p}: run `python paper_2509_11574_b200/build.py`")
     L = C.CDLL(p)

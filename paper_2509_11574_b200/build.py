@@ -34,8 +34,8 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(d) <= t for d in deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, out: str | None = None) -> str:
+    if out is None and not force and up_to_date():
         return LIB
     objs = []
     bdir = os.path.join(HERE, "build")
@@ -51,12 +51,16 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for p in procs:
         if p.wait() != 0:
             raise subprocess.CalledProcessError(p.returncode, p.args)
-    tmp = LIB + f".tmp{os.getpid()}"
+    dst = out or LIB
+    os.makedirs(os.path.dirname(os.path.abspath(dst)), exist_ok=True)
+    tmp = dst + f".tmp{os.getpid()}"
     subprocess.check_call([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", *objs,
                            "-o", tmp, "-lcudart"])
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, dst)
+    return dst
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    # --out PATH: build the current tree into PATH (A/B experiments, tools/ab.sh) instead of libgps.so
+    o = sys.argv[sys.argv.index("--out") + 1] if "--out" in sys.argv else None
+    print(build(force="--force" in sys.argv, verbose=True, out=o))

@@ -17,7 +17,7 @@ import gps_synth as S
 import oracle as O
 from tests import gpu_helpers as H
 from tests.test_gpu_fuse_raycast import TIE_VOXELS, compare_volumes
-from tests.test_gpu_render_refine import GROUPS, compare_grads
+from tests.test_gpu_render_refine import GROUPS, compare_grads, grad_sensitivity
 
 pytestmark = pytest.mark.gpu
 
@@ -38,6 +38,20 @@ def depth_test_ties(gd, ocam, R, t, Dg, Do, excl):
         sl = (slice(y0, y1 + 1), slice(x0, x1 + 1))
         out[sl] |= np.abs(float(d[i]) - thr[sl]) <= tol[sl]
     return out
+
+
+def report_grads(label, gg, ref, gamb):
+    keep = ~gamb
+    msg = []
+    for k in GROUPS:
+        a = gg[k].reshape(len(keep), -1)[keep]
+        b = ref[k].reshape(len(keep), -1)[keep]
+        tau = 1e-3 * np.max(np.abs(b))
+        err = np.abs(a - b) / np.maximum(np.abs(b), tau)
+        i = np.unravel_index(np.argmax(err), err.shape)
+        gi = np.nonzero(keep)[0][i[0]]
+        msg.append(f"{k}: max {err.max():.2e} (Gaussian {gi}, gpu {a[i]:.4e} ref {b[i]:.4e} tau {tau:.3e})")
+    print(f"grads {label}: {int(keep.sum())} compared; " + "; ".join(msg))
 
 
 def run_chain(cfg_name, n_frames, n_gauss=None):
@@ -94,7 +108,10 @@ def run_chain(cfg_name, n_frames, n_gauss=None):
     l2 = ras.refine_step(g, st, [gview], grad_out=gout).item()
     assert abs(l2 - lg) <= 1e-6 * lg
     ref, gamb = O.backward(gd, ocam, R, t, Do, out["Cstar"], out["WG"], OG, pix_amb=(samb | excl))
-    compare_grads(gout.to_numpy(), ref, gamb)
+    gg = gout.to_numpy()
+    report_grads("chained", gg, ref, gamb)
+    sens = grad_sensitivity(gd, ocam, R, t, Do, out["Cstar"], out["WG"], OG, samb | excl)
+    compare_grads(gg, ref, gamb, sens=sens)
     m0 = {k: np.zeros_like(np.asarray(p0[k], np.float64)) for k in GROUPS}
     P1, _, _ = O.adam_step(p0, m0, m0, ref, 0)
     p1 = g.to_numpy()

@@ -111,16 +111,51 @@ def oracle_grads(gd, ocam, R, t, Dt, Ct, tgt):
     return loss, grads, gamb
 
 
-def compare_grads(gg, ref, gamb, min_checked=50):
+def grad_sensitivity(gd, ocam, R, t, Dt, Cstar, WG, G, pix_amb, rel=5e-7, prel=2e-7, seed=0):
+    """How much the oracle's own gradient moves under fp32-rounding-level perturbations of what
+    the CUDA path computes in fp32: C* scaled by (1 +- 5e-7) (8 fp32 ulps, coherent over the
+    image), and every Gaussian position scaled by (1 + 2e-7 r), r = +-1 per Gaussian (the fp32
+    projection's error of p_hat).  Elementwise max of |change|: the scale of the legitimate fp32
+    error of a gradient that sums cancelling terms (dL/dalpha ~ c - C* small, or symmetric
+    footprints cancelling dL/dp_hat; R-GRAD)."""
+    rng = np.random.default_rng(seed)
+    base, _ = O.backward(gd, ocam, R, t, Dt, Cstar, WG, G, pix_amb=pix_amb)
+    out = {k: np.zeros_like(v) for k, v in base.items()}
+    C = np.asarray(Cstar, np.float64)
+    gp = dict(gd, xyz=(np.asarray(gd["xyz"], np.float64)
+                       * (1.0 + prel * rng.choice([-1.0, 1.0], size=(len(gd["xyz"]), 1)))))
+    for args in ((gd, C * (1.0 + rel)), (gd, C * (1.0 - rel)), (gp, C)):
+        g2, _ = O.backward(args[0], ocam, R, t, Dt, args[1], WG, G, pix_amb=pix_amb)
+        for k in GROUPS:
+            out[k] = np.maximum(out[k], np.abs(g2[k] - base[k]))
+    return out
+
+
+def compare_grads(gg, ref, gamb, min_checked=50, sens=None):
+    """O9: |g_gpu - g_ref| <= 1e-3 max(|g_ref|, tau), tau = 1e-3 max|g_ref| per parameter block.
+    With `sens` (grad_sensitivity), a value may instead be within 4x the gradient's sensitivity
+    to fp32 rounding of C* (an ill-conditioned dL/dalpha); such values are counted and must be
+    <= 1e-3 of those compared."""
     keep = ~gamb
     assert keep.sum() >= min_checked
+    n_sens = n_tot = 0
     for k in GROUPS:
         a = gg[k].reshape(len(keep), -1)[keep]
         b = ref[k].reshape(len(keep), -1)[keep]
         tau = 1e-3 * np.max(np.abs(b))
         assert tau > 0, k
         err = np.abs(a - b) / np.maximum(np.abs(b), tau)
-        assert err.max() <= 1e-3, (k, float(err.max()))
+        bad = err > 1e-3
+        if sens is not None:
+            sk = sens[k].reshape(len(keep), -1)[keep]
+            explained = bad & (np.abs(a - b) <= 4.0 * sk)
+            n_sens += int(explained.sum())
+            bad &= ~explained
+        n_tot += err.size
+        assert not bad.any(), (k, float(err[bad].max()), int(bad.sum()))
+    if sens is not None:
+        print(f"gradients: {n_tot} values compared, {n_sens} within 4x their fp32 C* sensitivity only")
+        assert n_sens <= max(2, 1e-3 * n_tot)
 
 
 def test_refine_gradients_and_adam_cfg1():
