@@ -211,36 +211,42 @@ static void merge_blocks(orc_volume* v, const int32_t* add, int64_t na) {
 }
 
 /* ---- O3 integration (reading R-INT), P32 prescribed, DESIGN.md §4.2 ---------- */
+/* The world->camera map of a voxel as one affine map of its integer index g (R-POSE: X = R^T
+ * (g v - t)), scaled by the focal lengths: (fx X, fy Y, Z) = A g + b.  Its coefficients are
+ * computed in double from the fp32 inputs and rounded once to fp32:
+ *   A[c][k] = fl((s_c * v) * R[k][c]),   b[c] = fl(-(s_c * ((R[0][c] t0 + R[1][c] t1) + R[2][c] t2))),
+ * s = (fx, fy, 1); each coordinate is then fmaf(A[c][2], gz, fmaf(A[c][1], gy, fmaf(A[c][0], gx, b[c]))). */
+static void affine_cam(const float* K4, const float* R, const float* t, float voxel, float A[3][3], float b[3]) {
+  const double sc[3] = {(double)K4[0], (double)K4[1], 1.0};
+  for (int c = 0; c < 3; ++c) {
+    const double sv = sc[c] * (double)voxel;
+    for (int k = 0; k < 3; ++k) A[c][k] = (float)(sv * (double)R[3 * k + c]);
+    double acc = (double)R[c] * (double)t[0];
+    acc = acc + (double)R[3 + c] * (double)t[1];
+    acc = acc + (double)R[6 + c] * (double)t[2];
+    b[c] = (float)(-(sc[c] * acc));
+  }
+}
+
 static void integrate_block(orc_volume* v, int64_t bi, const float* K4, int W, int H,
                             const float* R, const float* t, const uint16_t* depth, float scale,
                             const uint8_t* rgba) {
   const int32_t* bc = v->coords + 3 * bi;
-  float fx = K4[0], fy = K4[1], cx = K4[2], cy = K4[3];
+  float cx = K4[2], cy = K4[3];
   float inv_scale = 1.0f / scale, inv_mu = 1.0f / v->mu;
+  float A[3][3], b[3];
+  affine_cam(K4, R, t, v->voxel, A, b);
   for (int k = 0; k < 8; ++k)
     for (int j = 0; j < 8; ++j)
       for (int i = 0; i < 8; ++i) {
         int32_t g[3] = {bc[0] * 8 + i, bc[1] * 8 + j, bc[2] * 8 + k};
-        float P[3], D[3], X[3];
-        for (int c = 0; c < 3; ++c) {
-          P[c] = (float)g[c] * v->voxel;
-          D[c] = P[c] - t[c];
-        }
-        for (int c = 0; c < 3; ++c) { /* X = R^T D */
-          float acc = R[0 * 3 + c] * D[0];
-          float p1 = R[1 * 3 + c] * D[1];
-          acc = acc + p1;
-          float p2 = R[2 * 3 + c] * D[2];
-          X[c] = acc + p2;
-        }
+        float X[3]; /* (fx X_c, fy Y_c, Z_c) */
+        for (int c = 0; c < 3; ++c)
+          X[c] = fmaf(A[c][2], (float)g[2], fmaf(A[c][1], (float)g[1], fmaf(A[c][0], (float)g[0], b[c])));
         if (!(X[2] > 0.0f)) continue;
         float iz = 1.0f / X[2];
-        float ux = fx * X[0];
-        float uf = ux * iz;
-        uf = uf + cx;
-        float vy = fy * X[1];
-        float vf = vy * iz;
-        vf = vf + cy;
+        float uf = fmaf(X[0], iz, cx);
+        float vf = fmaf(X[1], iz, cy);
         float ur = floorf(uf + 0.5f), vr = floorf(vf + 0.5f);
         if (!(ur >= 0.0f && ur <= (float)(W - 1) && vr >= 0.0f && vr <= (float)(H - 1))) continue;
         int64_t pix = (int64_t)vr * W + (int64_t)ur;
