@@ -503,44 +503,66 @@ def read_profile(N):
 
 
 # ----------------------------------------------------------------------------------------------
-def cpu_baseline(cfg, gd, frames, budget_s):
-    """The oracle as it stands (single-threaded C + numpy, fp64 render), on a bounded sample of
-    the same workload: fuse of 2 full frames, raycast of a pixel sample (scaled to a full frame),
-    one refine iteration on a sampled subset of Gaussians (scaled to all).  Frame time is
-    assembled like the step: t = t_fuse + 1.6 t_raycast + 2 t_iter."""
-    import oracle as O
-    import torch
+def cpu_model() -> str:
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
 
-    ocam = O.Camera(cfg.fx, cfg.fy, cfg.cx, cfg.cy, cfg.width, cfg.height)
-    vol = O.Volume(voxel_size=cfg.voxel_size, mu=4 * cfg.voxel_size)
-    t0 = time.time()
-    nf = 0
-    for k in range(2):
-        d, c, R, t = frames[k]
-        vol.fuse(ocam, R, t, d.cpu().numpy().view(np.uint16), cfg.depth_scale, c.cpu().numpy())
-        nf += 1
-    t_fuse = (time.time() - t0) / nf
-    rng = np.random.default_rng(0)
-    npx = 400
-    pix = np.stack([rng.integers(0, cfg.width, npx), rng.integers(0, cfg.height, npx)], 1).astype(np.int32)
-    t0 = time.time()
-    vol.raycast(ocam, frames[1][2], frames[1][3], pix)
-    t_ray = (time.time() - t0) * (cfg.width * cfg.height / npx)
-    n = gd["xyz"].shape[0]
-    m = min(n, 20000)
-    sub = {k: (v[:m] if isinstance(v, np.ndarray) else v) for k, v in gd.items()}
-    Dt = np.zeros((cfg.height, cfg.width), np.float32)
-    Ct = np.zeros((cfg.height, cfg.width, 3), np.float32)
-    tgt = frames[1][1].cpu().numpy()
-    t0 = time.time()
-    out = O.render(sub, ocam, frames[1][2], frames[1][3], Dt, Ct)
-    loss, Gr, cnt, _ = O.l1_loss(out["Cstar"], out["WG"], Dt, tgt)
-    grads, _ = O.backward(sub, ocam, frames[1][2], frames[1][3], Dt, out["Cstar"], out["WG"], Gr)
-    zero = {k: np.zeros_like(np.asarray(v, np.float64)) for k, v in grads.items()}
-    O.adam_step(sub, zero, zero, grads, 0)
-    t_iter = (time.time() - t0) * (n / m)
+
+def cpu_baseline(cfg, gd, frames, budget_s):
+    """The oracle as it stands (C + numpy, fp64 render), in its OpenMP build on all host cores
+    (pixel, block, Gaussian and row-band loops in parallel), on a bounded sample of the same
+    workload: fuse of 2 full frames, raycast of a pixel sample (scaled to a full frame), one
+    refine iteration on a sampled subset of Gaussians (scaled to all).  Frame time is assembled
+    like the step: t = t_fuse + 1.6 t_raycast + 2 t_iter."""
+    import oracle as O
+
+    threads = O.use_openmp(True)
+    try:
+        ocam = O.Camera(cfg.fx, cfg.fy, cfg.cx, cfg.cy, cfg.width, cfg.height)
+        vol = O.Volume(voxel_size=cfg.voxel_size, mu=4 * cfg.voxel_size)
+        t0 = time.time()
+        nf = 0
+        for k in range(2):
+            d, c, R, t = frames[k]
+            vol.fuse(ocam, R, t, d.cpu().numpy().view(np.uint16), cfg.depth_scale, c.cpu().numpy())
+            nf += 1
+        t_fuse = (time.time() - t0) / nf
+        rng = np.random.default_rng(0)
+        npx = min(cfg.width * cfg.height, 400 * max(1, threads))
+        pix = np.stack([rng.integers(0, cfg.width, npx), rng.integers(0, cfg.height, npx)], 1).astype(np.int32)
+        t0 = time.time()
+        vol.raycast(ocam, frames[1][2], frames[1][3], pix)
+        t_ray = (time.time() - t0) * (cfg.width * cfg.height / npx)
+        n = gd["xyz"].shape[0]
+        m = min(n, 20000 * max(1, threads // 4))
+        sub = {k: (v[:m] if isinstance(v, np.ndarray) else v) for k, v in gd.items()}
+        Dt = np.zeros((cfg.height, cfg.width), np.float32)
+        Ct = np.zeros((cfg.height, cfg.width, 3), np.float32)
+        tgt = frames[1][1].cpu().numpy()
+        t0 = time.time()
+        out = O.render(sub, ocam, frames[1][2], frames[1][3], Dt, Ct)
+        loss, Gr, cnt, _ = O.l1_loss(out["Cstar"], out["WG"], Dt, tgt)
+        grads, _ = O.backward(sub, ocam, frames[1][2], frames[1][3], Dt, out["Cstar"], out["WG"], Gr)
+        zero = {k: np.zeros_like(np.asarray(v, np.float64)) for k, v in grads.items()}
+        O.adam_step(sub, zero, zero, grads, 0)
+        t_iter = (time.time() - t0) * (n / m)
+    finally:
+        O.use_openmp(False)
     t_frame = t_fuse + 1.6 * t_ray + 2.0 * t_iter
-    return {"value": round(1.0 / t_frame, 6), "unit": "frames/s", "cores": 1, "kind": "oracle",
+    return {"value": round(1.0 / t_frame, 6), "unit": "frames/s", "cores": threads, "kind": "oracle",
+            "cpu_model": cpu_model(), "build": "oracle.c with -fopenmp (all host cores)",
             "sample": f"fuse 2 full frames; raycast {npx} px scaled to {cfg.width}x{cfg.height}; one refine "
                       f"iteration on {m} of {n} Gaussians scaled x{n / m:.1f}; t_frame = t_fuse + 1.6 t_ray + 2 t_iter",
             "t_fuse_s": round(t_fuse, 3), "t_raycast_s": round(t_ray, 2), "t_iter_s": round(t_iter, 2)}

@@ -31,23 +31,40 @@ _CFLAGS = ["-O2", "-std=c99", "-ffp-contract=off", "-fno-fast-math", "-fno-math-
            "-shared", "-fPIC"]
 
 
+_LIB_OMP_PATH = os.path.join(_HERE, "liboracle_omp.so")
+
+
 def build(force: bool = False) -> str:
-    """Compile oracle.c into liboracle.so (gcc, -ffp-contract=off)."""
-    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
-        tmp = _LIB_PATH + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", *_CFLAGS, _SRC, "-o", tmp, "-lm"])
-        os.replace(tmp, _LIB_PATH)
+    """Compile oracle.c into liboracle.so (gcc, -ffp-contract=off) and, for the CPU timing
+    baseline only, liboracle_omp.so (the same source with -fopenmp: pixel, block, Gaussian and
+    row-band loops in parallel; each pixel still sums in index order)."""
+    for path, extra in ((_LIB_PATH, []), (_LIB_OMP_PATH, ["-fopenmp"])):
+        if force or not os.path.exists(path) or os.path.getmtime(path) < os.path.getmtime(_SRC):
+            tmp = path + f".tmp{os.getpid()}"
+            subprocess.check_call(["gcc", *_CFLAGS, *extra, _SRC, "-o", tmp, "-lm"])
+            os.replace(tmp, path)
     return _LIB_PATH
 
 
 _lib = None
+_use_omp = False
+
+
+def use_openmp(on: bool = True) -> int:
+    """Switch this process to the OpenMP build (bench.py's cpu_baseline only; tests never call
+    it).  Returns the number of threads it will use."""
+    global _use_omp, _lib
+    if on != _use_omp:
+        _use_omp = on
+        _lib = None
+    return int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1)) if on else 1
 
 
 def lib():
     global _lib
     if _lib is None:
         build()
-        L = C.CDLL(_LIB_PATH)
+        L = C.CDLL(_LIB_OMP_PATH if _use_omp else _LIB_PATH)
         vp, i64, i32, f32, f64 = C.c_void_p, C.c_int64, C.c_int, C.c_float, C.c_double
         L.orc_volume_new.restype = vp
         L.orc_volume_new.argtypes = [f32, f32, i32, f32, f32, i64]

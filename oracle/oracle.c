@@ -24,6 +24,9 @@
  */
 #include <math.h>
 #include <stdint.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 #include <stdlib.h>
 #include <string.h>
 
@@ -294,6 +297,8 @@ int orc_fuse(orc_volume* v, const float* K4, int W, int H, const float* R, const
   merge_blocks(v, samples, u);
   free(samples);
   if (v->n > v->budget) v->overflow = 1;
+  /* blocks are disjoint: the OpenMP build (timing baseline only) integrates them in parallel */
+#pragma omp parallel for schedule(dynamic, 16)
   for (int64_t i = 0; i < v->nvis; ++i) {
     int64_t bi = find_block(v, v->vis + 3 * i);
     integrate_block(v, bi, K4, W, H, R, t, depth, scale, rgba);
@@ -386,6 +391,7 @@ void orc_raycast(const orc_volume* v, const float* K4, int W, int H, const float
   double vs = (double)v->voxel, tmin = (double)v->dmin;
   int64_t J = (int64_t)floor(((double)v->dmax - (double)v->dmin) / vs);
   int64_t count = pix ? n : (int64_t)W * H;
+#pragma omp parallel for schedule(dynamic, 64)
   for (int64_t q = 0; q < count; ++q) {
     int u = pix ? pix[2 * q] : (int)(q % W);
     int vv = pix ? pix[2 * q + 1] : (int)(q / W);
@@ -834,33 +840,48 @@ void orc_render(int64_t n, int deg, const double* xyz, const double* ls, const d
   double* cg = (double*)calloc(HW * 3, sizeof(double));
   memset(WG, 0, sizeof(double) * HW);
   if (amb) memset(amb, 0, HW);
-  for (int64_t i = 0; i < n; ++i) {
-    float pf[3], lf[3], qf[4], of;
-    f32_params(xyz + 3 * i, ls + 3 * i, rot + 4 * i, op[i], pf, lf, qf, &of);
-    p32 h;
-    proj32(pf, lf, qf, of, K4f, W, H, Rf, tf, (float)near_z, (float)lowpass, &h);
-    gproj g;
-    project_f64(&cam, deg, xyz + 3 * i, ls + 3 * i, rot + 4 * i, op[i], sh + 3 * nc * i, &g);
-    int gam = gauss_amb(&g, near_z);
-    if (h.culled || !(g.det > 0) || !(g.X[2] > 0)) {
-      if (amb && gam && g.det > 0 && g.X[2] > 0) { /* fp64 might keep it: flag its footprint */
-        double rx = 3.0 * sqrt(g.cxx) + 1.0, ry = 3.0 * sqrt(g.cyy) + 1.0;
-        int x0 = (int)fmax(0, floor(g.px - rx)), x1 = (int)fmin(W - 1, ceil(g.px + rx));
-        int y0 = (int)fmax(0, floor(g.py - ry)), y1 = (int)fmin(H - 1, ceil(g.py + ry));
-        for (int y = y0; y <= y1; ++y)
-          for (int x = x0; x <= x1; ++x) amb[(int64_t)y * W + x] = 1;
+  /* One band of image rows per task; every pixel still sums its Gaussians in index order, so the
+   * result does not depend on the band count (1 in the serial build the tests use; the OpenMP
+   * build, a timing baseline only, runs bands in parallel). */
+  int nbands = 1;
+#ifdef _OPENMP
+  nbands = 4 * omp_get_max_threads();
+  if (nbands > H) nbands = H;
+#endif
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int band = 0; band < nbands; ++band) {
+    const int by0 = (int)((int64_t)band * H / nbands), by1 = (int)((int64_t)(band + 1) * H / nbands) - 1;
+    for (int64_t i = 0; i < n; ++i) {
+      float pf[3], lf[3], qf[4], of;
+      f32_params(xyz + 3 * i, ls + 3 * i, rot + 4 * i, op[i], pf, lf, qf, &of);
+      p32 h;
+      proj32(pf, lf, qf, of, K4f, W, H, Rf, tf, (float)near_z, (float)lowpass, &h);
+      if (h.culled && !amb) continue; /* contributes nothing; only the ambiguity map needs it */
+      if (nbands > 1 && !h.culled && (h.rect[3] < by0 || h.rect[1] > by1)) continue;
+      gproj g;
+      project_f64(&cam, deg, xyz + 3 * i, ls + 3 * i, rot + 4 * i, op[i], sh + 3 * nc * i, &g);
+      int gam = gauss_amb(&g, near_z);
+      if (h.culled || !(g.det > 0) || !(g.X[2] > 0)) {
+        if (amb && gam && g.det > 0 && g.X[2] > 0) { /* fp64 might keep it: flag its footprint */
+          double rx = 3.0 * sqrt(g.cxx) + 1.0, ry = 3.0 * sqrt(g.cyy) + 1.0;
+          int x0 = (int)fmax(0, floor(g.px - rx)), x1 = (int)fmin(W - 1, ceil(g.px + rx));
+          int y0 = (int)fmax(by0, floor(g.py - ry)), y1 = (int)fmin(by1, ceil(g.py + ry));
+          for (int y = y0; y <= y1; ++y)
+            for (int x = x0; x <= x1; ++x) amb[(int64_t)y * W + x] = 1;
+        }
+        continue;
       }
-      continue;
+      const int ry0 = h.rect[1] > by0 ? h.rect[1] : by0, ry1 = h.rect[3] < by1 ? h.rect[3] : by1;
+      for (int y = ry0; y <= ry1; ++y)
+        for (int x = h.rect[0]; x <= h.rect[2]; ++x) {
+          int64_t pi = (int64_t)y * W + x;
+          pairv pv = eval_pair(&g, &h, x, y, Dt[pi], eps, alpha_min);
+          if (amb && (pv.amb || (gam && pv.in))) amb[pi] = 1;
+          if (!pv.in) continue;
+          for (int ch = 0; ch < 3; ++ch) cg[3 * pi + ch] += pv.alpha * g.col[ch];
+          WG[pi] += pv.alpha;
+        }
     }
-    for (int y = h.rect[1]; y <= h.rect[3]; ++y)
-      for (int x = h.rect[0]; x <= h.rect[2]; ++x) {
-        int64_t pi = (int64_t)y * W + x;
-        pairv pv = eval_pair(&g, &h, x, y, Dt[pi], eps, alpha_min);
-        if (amb && (pv.amb || (gam && pv.in))) amb[pi] = 1;
-        if (!pv.in) continue;
-        for (int ch = 0; ch < 3; ++ch) cg[3 * pi + ch] += pv.alpha * g.col[ch];
-        WG[pi] += pv.alpha;
-      }
   }
   for (int64_t pi = 0; pi < HW; ++pi)
     for (int ch = 0; ch < 3; ++ch) Cstar[3 * pi + ch] = (Ct[3 * pi + ch] + cg[3 * pi + ch]) / (1.0 + WG[pi]);
@@ -884,6 +905,7 @@ void orc_backward(int64_t n, int deg, const double* xyz, const double* ls, const
   float K4f[4], Rf[9], tf[3];
   cam32(K4, R, t, K4f, Rf, tf);
   int nc = (deg + 1) * (deg + 1);
+#pragma omp parallel for schedule(dynamic, 64)
   for (int64_t i = 0; i < n; ++i) {
     double* dp = gxyz + 3 * i;
     double* dls = gls + 3 * i;
