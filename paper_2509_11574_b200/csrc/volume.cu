@@ -32,9 +32,41 @@ struct FuseParams {
   float R[9], t[3];
   float scale, mu, voxel, bs, dmin, dmax;
   float inv_scale, inv_mu;  // fl(1/depth_scale), fl(1/mu): host fp32 divisions
+  float A[9], b[3];  // integration's affine voxel -> (fx X, fy Y, Z) map, row c = A[3c..3c+2] (§4.2)
   int wmax;
   const float* dpose;  // device pose (R row-major, t) for the *_dpose entry points, else null
 };
+
+// A[c][k] = fl((s_c v) R[k][c]), b[c] = fl(-(s_c ((R[0][c] t0 + R[1][c] t1) + R[2][c] t2))),
+// s = (fx, fy, 1), in double with every operation rounded separately (no contraction), then once
+// to fp32 -- the host computes it for host poses, the device for device poses (same values)
+__host__ __device__ __forceinline__ double dmul(double a, double b) {
+#ifdef __CUDA_ARCH__
+  return __dmul_rn(a, b);
+#else
+  return a * b;
+#endif
+}
+__host__ __device__ __forceinline__ double dadd(double a, double b) {
+#ifdef __CUDA_ARCH__
+  return __dadd_rn(a, b);
+#else
+  return a + b;
+#endif
+}
+__host__ __device__ __forceinline__ void affine_cam(FuseParams& p) {
+  const double sc[3] = {(double)p.fx, (double)p.fy, 1.0};
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const double sv = dmul(sc[c], (double)p.voxel);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) p.A[3 * c + k] = (float)dmul(sv, (double)p.R[3 * k + c]);
+    double acc = dmul((double)p.R[c], (double)p.t[0]);
+    acc = dadd(acc, dmul((double)p.R[3 + c], (double)p.t[1]));
+    acc = dadd(acc, dmul((double)p.R[6 + c], (double)p.t[2]));
+    p.b[c] = (float)(-dmul(sc[c], acc));
+  }
+}
 
 // the device-pose instantiations read R, t from device memory once per thread (the same fp32
 // values the host would pass, so every prescribed sequence is unchanged)
@@ -262,15 +294,14 @@ __global__ void __launch_bounds__(256) k_alloc(VolumeView v, FuseParams p_in,
 // (false: not updated).  Needs no voxel data, so skipped voxels cost no voxel traffic.
 __device__ __forceinline__ bool voxel_project(const FuseParams& p, int gx, int gy, int gz, uint32_t& pix,
                                               float& X2) {
-  const float P0 = pmul((float)gx, p.voxel), P1 = pmul((float)gy, p.voxel), P2 = pmul((float)gz, p.voxel);
-  const float D0 = psub(P0, p.t[0]), D1 = psub(P1, p.t[1]), D2 = psub(P2, p.t[2]);
-  const float X0 = pdot3(p.R[0], D0, p.R[3], D1, p.R[6], D2);
-  const float X1 = pdot3(p.R[1], D0, p.R[4], D1, p.R[7], D2);
-  X2 = pdot3(p.R[2], D0, p.R[5], D1, p.R[8], D2);
+  const float fgx = (float)gx, fgy = (float)gy, fgz = (float)gz;  // exact (|g| < 2^24)
+  const float U = __fmaf_rn(p.A[2], fgz, __fmaf_rn(p.A[1], fgy, __fmaf_rn(p.A[0], fgx, p.b[0])));
+  const float V = __fmaf_rn(p.A[5], fgz, __fmaf_rn(p.A[4], fgy, __fmaf_rn(p.A[3], fgx, p.b[1])));
+  X2 = __fmaf_rn(p.A[8], fgz, __fmaf_rn(p.A[7], fgy, __fmaf_rn(p.A[6], fgx, p.b[2])));
   if (!(X2 > 0.0f)) return false;
   const float iz = __frcp_rn(X2);
-  const float uf = padd(pmul(pmul(p.fx, X0), iz), p.cx);
-  const float vf = padd(pmul(pmul(p.fy, X1), iz), p.cy);
+  const float uf = __fmaf_rn(U, iz, p.cx);
+  const float vf = __fmaf_rn(V, iz, p.cy);
   const float ur = floorf(padd(uf, 0.5f)), vr = floorf(padd(vf, 0.5f));
   if (!(ur >= 0.0f && ur <= (float)(p.W - 1) && vr >= 0.0f && vr <= (float)(p.H - 1))) return false;
   pix = (uint32_t)vr * (uint32_t)p.W + (uint32_t)ur;
@@ -320,6 +351,7 @@ __global__ void __launch_bounds__(256) k_integrate(VolumeView v, FuseParams p_in
                                                    const uint32_t* __restrict__ rgba) {
   FuseParams p = p_in;
   apply_dpose<DPOSE>(p);
+  if (DPOSE) affine_cam(p);  // host poses: computed on the host (identical values)
   __shared__ uint32_t smagic[256];
   __shared__ float srcp[256];
   // smagic[w] = ceil(2^32 / (w+1)) for w >= 1 (w = 0 is special-cased in voxel_update)
@@ -1214,6 +1246,7 @@ static gps_status fuse_impl(gps_volume* vol, const gps_intrinsics* K, const gps_
   p.dmin = v->cfg.depth_min;
   p.dmax = v->cfg.depth_max;
   p.wmax = v->cfg.w_max;
+  if (T) affine_cam(p);  // device poses: k_integrate computes it from the pose it reads
   const uint32_t frame = v->frame++;
   k_reset_frame<<<1, 1, 0, s>>>(v->view.ctr);
   GPS_CHECK_LAUNCH("k_reset_frame");
