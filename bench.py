@@ -59,6 +59,8 @@ def parse():
                     help="dense block-index grid (an accelerator; results do not depend on it): none (hash "
                          "only); workspace (a fixed 25.6 m cube centred on the first camera position, the hash "
                          "beyond it; no scene knowledge); scene (the synthetic room's ground-truth bounds)")
+    ap.add_argument("--workspace-m", type=float, default=25.6,
+                    help="edge of the workspace grid's cube in metres (25.6 m: 640^3 blocks of 4 cm, 1 GiB)")
     ap.add_argument("--cpu-seconds", type=float, default=20.0, help="budget of the cpu_baseline sample")
     return ap.parse_args()
 
@@ -79,7 +81,6 @@ def rank_config(name: str, rank: int, world: int):
     return S.get_config(name) if rank == 0 else S.get_config(name, seed=40 + rank)
 
 
-WORKSPACE_HALF = 12.8  # metres: half the edge of the dense grid's cube (640^3 blocks of 4 cm, 1 GiB)
 
 
 def dense_bounds(args, S, cfg, poses):
@@ -87,7 +88,8 @@ def dense_bounds(args, S, cfg, poses):
         return S.scene_bounds(cfg)
     if args.dense_grid == "workspace":
         c = np.asarray(poses[0][1], np.float64)
-        return (tuple(c - WORKSPACE_HALF), tuple(c + WORKSPACE_HALF))
+        h = 0.5 * args.workspace_m
+        return (tuple(c - h), tuple(c + h))
     return None
 
 
@@ -234,9 +236,9 @@ def run_ours(args):
     if st["status"] != "GPS_OK":
         raise RuntimeError(f"volume overflow during warm-up: {st}")
     # Three passes over the SAME window from the SAME state (device snapshot of volume, Gaussians,
-    # Adam moments + host bookkeeping): (1) the timed device-resident run (value); (2) an
-    # event-profiled replay, every library launch bracketed by CUDA events on its stream (kernel
-    # shares, launch count, the roofline's launch time); (3) the end-to-end replay (e2e).
+    # Adam moments + host bookkeeping): (1) the timed device-resident run (value); (2) the
+    # end-to-end replay (e2e); (3) an event-profiled replay, every library launch bracketed by CUDA
+    # events on its stream (kernel shares, launch count, the roofline's launch time).
     snap = pipe.snapshot()
     k0 = k
     torch.cuda.synchronize()
@@ -256,6 +258,50 @@ def run_ours(args):
         dist.barrier()
     clk = clocks.stop()
     ms = ev0.elapsed_time(ev1)
+    rstats = pipe.ras.stats()
+    vstats = vol.stats()
+    check_status("timed window", rstats, vstats)
+    ms_max = max_over_ranks(ms, "cuda")
+    frames_timed = args.steps * dk
+    value = job_rate(frames_timed, ws, ms_max)
+    # ---------------- end-to-end leg: host (pinned) frames, result read back ----------------
+    e2e = None
+    if not args.no_e2e:
+        pipe.restore(snap)
+        k = k0
+        host = {}
+        for j in range(k, k + dk * args.steps):
+            host[j] = (frames[j][0].cpu().pin_memory(), frames[j][1].cpu().pin_memory())
+        host["loss"] = [torch.empty(1, dtype=torch.float32).pin_memory() for _ in range(args.steps)]
+        host["i"] = 0
+        # warm the freshly pinned buffers (first-use DMA mappings) with one untimed H2D copy each,
+        # as a reused host frame pool would be; their data is copied again inside the timed region
+        scratch_d = torch.empty_like(frames[k0][0])
+        scratch_c = torch.empty_like(frames[k0][1])
+        for j in range(k, k + dk * args.steps):
+            scratch_d.copy_(host[j][0], non_blocking=True)
+            scratch_c.copy_(host[j][1], non_blocking=True)
+        torch.cuda.synchronize()
+        del scratch_d, scratch_c
+        h2d = dk * (frames[k][0].numel() * 2 + frames[k][1].numel())
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        run_steps(args.steps, host)
+        pipe.join(stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        check_status("end-to-end window", pipe.ras.stats(), vol.stats())
+        ems = max_over_ranks(e0.elapsed_time(e1), "cuda")
+        e2e = {"value": round(job_rate(frames_timed, ws, ems), 2), "unit": "frames/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 4,
+               "ms_per_step": round(ems / args.steps, 4),
+               "path": "MappingPipeline.process_frame with pinned-host depth/RGBA (H2D on a copy stream, the next frame's started one frame ahead) + "
+                       "loss D2H per step; same frames and starting state as the device-resident window"}
+    # ---------------- event-profiled replay (after the e2e leg: it leaves the pipeline serial
+    # for a window and the profiler's events behind, which must not touch the e2e timing) ----------
     prof = {}
     upd0 = 0
     ms_prof = float("nan")
@@ -276,39 +322,6 @@ def run_ours(args):
         prof = read_profile(N)
         N._lib.gps_profile_enable(0)
         pipe.overlap = not args.no_overlap
-    rstats = pipe.ras.stats()
-    vstats = vol.stats()
-    check_status("timed window", rstats, vstats)
-    ms_max = max_over_ranks(ms, "cuda")
-    frames_timed = args.steps * dk
-    value = job_rate(frames_timed, ws, ms_max)
-    # ---------------- end-to-end leg: host (pinned) frames, result read back ----------------
-    e2e = None
-    if not args.no_e2e:
-        pipe.restore(snap)
-        k = k0
-        host = {}
-        for j in range(k, k + dk * args.steps):
-            host[j] = (frames[j][0].cpu().pin_memory(), frames[j][1].cpu().pin_memory())
-        host["loss"] = [torch.empty(1, dtype=torch.float32).pin_memory() for _ in range(args.steps)]
-        host["i"] = 0
-        h2d = dk * (frames[k][0].numel() * 2 + frames[k][1].numel())
-        if ws > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        run_steps(args.steps, host)
-        pipe.join(stream)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        check_status("end-to-end window", pipe.ras.stats(), vol.stats())
-        ems = max_over_ranks(e0.elapsed_time(e1), "cuda")
-        e2e = {"value": round(job_rate(frames_timed, ws, ems), 2), "unit": "frames/s",
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 4,
-               "ms_per_step": round(ems / args.steps, 4),
-               "path": "MappingPipeline.process_frame with pinned-host depth/RGBA (H2D on a copy stream, the next frame's started one frame ahead) + "
-                       "loss D2H per step; same frames and starting state as the device-resident window"}
     if ws > 1:
         dist.barrier()
     if rank != 0:
@@ -487,7 +500,7 @@ def workload_config(args, cfg, n_g, ws):
                        if not args.no_overlap else "one stream (serial schedule)",
             "l2": "inputs larger than L2 (per-step state > 126 MB: params+Adam 283 MB, volume)",
             "dense_grid": {"none": "off (hash lookups only)",
-                           "workspace": f"{2 * WORKSPACE_HALF} m cube centred on the first camera position "
+                           "workspace": f"{args.workspace_m} m cube centred on the first camera position "
                                         "(fixed size, no scene knowledge; hash beyond it)",
                            "scene": "the synthetic room's ground-truth bounds"}[args.dense_grid]}
 

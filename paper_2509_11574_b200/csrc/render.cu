@@ -72,7 +72,9 @@ struct WsHeader {
   uint32_t n_visible;  // Gaussians surviving culls
   uint32_t mask_count; // |M| of the L1 mask
   uint32_t ticket;     // last-CTA election for the loss
-  uint32_t pad1[3];
+  uint32_t n_extra;    // work items beyond one per tile (lists longer than 256 entries)
+  uint32_t n_part;     // partial slots handed to long lists (the blend's split)
+  uint32_t pad1;
   // ---- static: where this render's lists live (refine and render layouts differ) ----
   uint64_t off_vals, off_offsets, off_tile_end;
 };
@@ -80,7 +82,8 @@ struct WsHeader {
 
 struct WsLayout {
   size_t hdr, counts, cursor, bigcounts, offsets, tile_end, loss_part, records, ranks, grad2d, rec3, cgj, vals, keys,
-      cstar, wg, gbuf, total;
+      cstar, wg, gbuf, extra, pbase, tick, part, total;
+  uint32_t extra_cap, part_cap;
   size_t zero_begin, zero_bytes;
 };
 
@@ -99,8 +102,9 @@ WsLayout ws_layout(int64_t n, int W, int H, int tile, int64_t cap, int64_t n_par
   L.counts = take(4 * tiles);     // per tile: entries of Gaussians spanning <= 4 tiles
   L.cursor = take(4 * tiles);     // per tile: scatter cursor of the others
   L.bigcounts = take(4 * tiles);  // per tile: entries of Gaussians spanning > 4 tiles
+  L.tick = take(4 * tiles);       // per tile: chunks of a split long list finished by the blend
   L.zero_begin = L.hdr + offsetof(WsHeader, K);
-  L.zero_bytes = L.bigcounts + 4 * tiles - L.zero_begin;
+  L.zero_bytes = L.tick + 4 * tiles - L.zero_begin;
   L.offsets = take(4 * (tiles + 1));
   L.tile_end = take(4 * tiles);
   L.loss_part = take(4 * tiles);
@@ -111,6 +115,11 @@ WsLayout ws_layout(int64_t n, int W, int H, int tile, int64_t cap, int64_t n_par
   L.cgj = refine ? take(48 * (size_t)std::max<int64_t>(n, 1)) : 0;
   L.vals = take(4 * (size_t)cap);
   L.keys = take(8 * (size_t)cap);
+  L.extra_cap = (uint32_t)std::min<int64_t>(cap / 256 + 1, 0x7FFFFFFF);
+  L.extra = take(8 * (size_t)L.extra_cap);  // {tile, chunk} work items of long lists
+  L.pbase = take(4 * tiles);                 // per long list: its first partial slot (or ~0)
+  L.part_cap = 2048;                         // 2048 chunks of 256 entries (8 MB) per render
+  L.part = take(16 * 256 * (size_t)L.part_cap);
   L.cstar = refine ? take(12 * (size_t)W * H) : 0;
   L.wg = refine ? take(4 * (size_t)W * H) : 0;
   L.gbuf = gbuf ? take(4 * (size_t)n_params) : 0;
@@ -472,7 +481,8 @@ __device__ __forceinline__ void preprocess_one(const RenderArgs& a, const gps_ga
 __global__ void __launch_bounds__(1024) k_scan(const uint32_t* __restrict__ counts,
                                                const uint32_t* __restrict__ bigcounts, uint32_t* offsets,
                                                int n_tiles, WsHeader* hdr, WsHeader stat,
-                                               uint32_t* sticky_overflow) {
+                                               uint32_t* sticky_overflow, uint2* extra, uint32_t extra_cap,
+                                               uint32_t* pbase, uint32_t part_cap) {
   __shared__ uint32_t warp_sums[32];
   __shared__ uint32_t carry;
   if (threadIdx.x == 0) carry = 0;
@@ -507,6 +517,16 @@ __global__ void __launch_bounds__(1024) k_scan(const uint32_t* __restrict__ coun
     for (int k = 0; k < 4; ++k) {
       if (i0 + k < n_tiles) offsets[i0 + k] = excl;
       excl += c[k];
+      // a list longer than 256 entries gives the backward one work item per further 256 (rare:
+      // their order is irrelevant, the gradients are sums)
+      if (c[k] > 256u && extra) {
+        const uint32_t more = (c[k] + 255u) / 256u - 1u;
+        const uint32_t at = atomicAdd(&hdr->n_extra, more);
+        for (uint32_t q = 0; q < more && at + q < extra_cap; ++q) extra[at + q] = make_uint2((uint32_t)(i0 + k), q + 1u);
+        // the blend splits the list only when all its chunks have work items and partial slots
+        const uint32_t pb = atomicAdd(&hdr->n_part, more + 1u);
+        pbase[i0 + k] = (at + more <= extra_cap && pb + more + 1u <= part_cap) ? pb : ~0u;
+      }
     }
     __syncthreads();
     if (threadIdx.x == 1023) carry = excl;
@@ -617,6 +637,45 @@ __device__ __forceinline__ void bitonic_sort(Keys keys, int n) {
 }
 
 // ============================================================================================
+// k_sort_long: tiles whose list is longer than kShortList entries are sorted here, by (depth bits,
+// index) keys, one 1024-thread CTA per tile (grid-stride over the tiles): a bitonic network in
+// shared memory up to kLongSmem keys, in the global key buffer beyond.  The blend kernels rank-
+// sort the short lists themselves and take the long ones as they are.  (A 128-thread blend CTA
+// sorting a 6000-entry list in global memory was the whole kernel's tail: late cfg4 frames see
+// ~50 such tiles where thousands of small Gaussians stack along a wall at grazing angles.)
+// ============================================================================================
+constexpr int kShortList = 256;
+constexpr int kLongSmem = 8192;  // 64 KB of dynamic shared memory
+
+__global__ void __launch_bounds__(1024) k_sort_long(const float4* __restrict__ rec, const uint32_t* __restrict__ offsets,
+                                                   uint32_t* vals, uint64_t* gkeys, int n_tiles, uint32_t cap) {
+  extern __shared__ __align__(16) uint64_t sk[];
+  for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    const uint32_t start = min(offsets[t], cap), end = min(offsets[t + 1], cap);
+    const int n = (int)(end - start);
+    if (n <= kShortList) continue;  // uniform across the CTA
+    uint64_t* keys = n <= kLongSmem ? sk : gkeys + start;
+    for (int e = threadIdx.x; e < n; e += blockDim.x) {
+      const uint32_t idx = vals[start + e];
+      keys[e] = ((uint64_t)__float_as_uint(rec[4 * idx + 1].z) << 32) | idx;
+    }
+    __syncthreads();
+    if (n <= (int)blockDim.x) {
+      // one key per thread: its rank is the number of smaller keys (keys are unique)
+      uint64_t mine = threadIdx.x < (unsigned)n ? keys[threadIdx.x] : ~0ull;
+      int rank = 0;
+      for (int j = 0; j < n; ++j) rank += keys[j] < mine;
+      __syncthreads();
+      if (threadIdx.x < (unsigned)n) vals[start + rank] = (uint32_t)mine;
+    } else {
+      bitonic_sort(keys, n);
+      for (int e = threadIdx.x; e < n; e += blockDim.x) vals[start + e] = (uint32_t)keys[e];
+    }
+    __syncthreads();
+  }
+}
+
+// ============================================================================================
 // k_sort_blend
 // ============================================================================================
 struct BlendIO {
@@ -636,7 +695,7 @@ __global__ void __launch_bounds__(TILE* TILE) k_sort_blend(RenderArgs a, const f
                                                           uint64_t* gkeys, uint32_t* tile_end, float* loss_part,
                                                           WsHeader* hdr, BlendIO io, int precull) {
   constexpr int NT = TILE * TILE;
-  __shared__ __align__(16) uint64_t skeys[kMaxList + 2];
+  __shared__ __align__(16) uint64_t skeys[kShortList + 2];
   __shared__ float4 s0[NT], s1[NT], s2[NT];  // s0 = (px, py, a, 2b); s1 = (c, ln sigma, d, q_max)
   __shared__ float red[NT / 32 + 1];
   __shared__ uint32_t redi[NT / 32 + 1];
@@ -670,7 +729,7 @@ __global__ void __launch_bounds__(TILE* TILE) k_sort_blend(RenderArgs a, const f
       skeys[rank] = key;
       vals[start + rank] = (uint32_t)key;
     }
-  } else if (n <= kMaxList) {
+  } else if (n <= kShortList) {
     for (int e = threadIdx.x; e < n; e += NT) {
       const uint32_t idx = vals[start + e];
       const float d = rec[4 * idx + 1].z;
@@ -679,16 +738,7 @@ __global__ void __launch_bounds__(TILE* TILE) k_sort_blend(RenderArgs a, const f
     __syncthreads();
     bitonic_sort(skeys, n);
     for (int e = threadIdx.x; e < n; e += NT) vals[start + e] = (uint32_t)skeys[e];
-  } else {
-    uint64_t* gk = gkeys + start;
-    for (int e = threadIdx.x; e < n; e += NT) {
-      const uint32_t idx = vals[start + e];
-      gk[e] = ((uint64_t)__float_as_uint(rec[4 * idx + 1].z) << 32) | idx;
-    }
-    __syncthreads();
-    bitonic_sort(gk, n);
-    for (int e = threadIdx.x; e < n; e += NT) vals[start + e] = (uint32_t)gk[e];
-  }
+  }  // longer lists: sorted by k_sort_long
   __syncthreads();
   // ---- pixel state ----
   const int lx = threadIdx.x % TILE, ly = threadIdx.x / TILE;
@@ -724,7 +774,7 @@ __global__ void __launch_bounds__(TILE* TILE) k_sort_blend(RenderArgs a, const f
       int lo = 0, hi = n;
       while (lo < hi) {
         const int mid = (lo + hi) >> 1;
-        const float d = n <= kMaxList ? __uint_as_float((uint32_t)(skeys[mid] >> 32)) : rec[4 * vals[start + mid] + 1].z;
+        const float d = n <= kShortList ? __uint_as_float((uint32_t)(skeys[mid] >> 32)) : rec[4 * vals[start + mid] + 1].z;
         if (d >= tmax) hi = mid; else lo = mid + 1;
       }
       n_eff = lo;
@@ -872,24 +922,54 @@ __global__ void __launch_bounds__(TILE* TILE) k_sort_blend(RenderArgs a, const f
 // bitonic fallback), so more CTAs stay resident.  Every pixel sees the same entries in the same
 // order as in k_sort_blend, so C* and W_G are bitwise those of the one-pixel-per-thread kernel.
 // --------------------------------------------------------------------------------------------
+// Long lists (more than NB entries; sorted by k_sort_long) are split into work items of NB
+// entries: CTA t takes (tile t, chunk 0), then the further chunks k_scan listed (extra[e] for
+// e = t, t + grid, ...).  Each chunk accumulates its entries' W and C per pixel and stores them
+// in its partial slot; the tile's last chunk to finish (a per-tile ticket) sums the partials in
+// chunk order -- a fixed order, so the image stays bit-reproducible -- and composites.  (One
+// 128-thread CTA walking a 6000-entry list was the kernel's tail in late cfg4 frames.)
+struct SplitIO {
+  const uint2* extra;     // {tile, chunk >= 1} work items of long lists (k_scan)
+  uint32_t extra_cap;
+  const uint32_t* pbase;  // per long tile: its first partial slot, ~0 = not split (no room)
+  uint32_t* tick;         // per tile: chunks finished (zeroed per render)
+  float4* part;           // partial slots, 256 pixels each: (W, C0, C1, C2)
+};
+
 template <bool SORTED, bool COUNT = false>
-__global__ void __launch_bounds__(128) k_sort_blend16x2(RenderArgs a, const float4* __restrict__ rec,
+__global__ void __launch_bounds__(128, 8) k_sort_blend16x2(RenderArgs a, const float4* __restrict__ rec,
                                                         const uint32_t* __restrict__ offsets, uint32_t* vals,
                                                         uint64_t* gkeys, uint32_t* tile_end, float* loss_part,
-                                                        WsHeader* hdr, BlendIO io, int precull) {
+                                                        WsHeader* hdr, BlendIO io, int precull, SplitIO spl) {
   constexpr int NT = 128, NB = 256;  // threads, staged entries per batch (2 per thread)
   __shared__ __align__(16) uint64_t skeys[NB + 2];
   __shared__ __align__(16) uint32_t sdep[NB + 4];
   __shared__ float4 s0[NB], s1[NB], s2[NB];  // s0 = (px, py, a, 2b); s1 = (c, ln sigma, d, q_max)
   __shared__ float red[NT / 32 + 1];
   __shared__ uint32_t redi[NT / 32 + 1];
-  const int t = blockIdx.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t n_extra = (SORTED && spl.extra) ? min(hdr->n_extra, spl.extra_cap) : 0u;
+  for (uint32_t item = blockIdx.x; item < gridDim.x + n_extra; item += gridDim.x) {
+  int t;
+  uint32_t chunk;
+  if (item < gridDim.x) {
+    t = (int)item;
+    chunk = 0;
+  } else {
+    const uint2 wi = spl.extra[item - gridDim.x];
+    t = (int)wi.x;
+    chunk = wi.y;
+  }
   const int tx = t % a.tiles_x, ty = t / a.tiles_x;
   const uint32_t start = min(offsets[t], a.cap);
   const uint32_t end = min(offsets[t + 1], a.cap);
   const int n = (int)(end - start);
   const bool small = n <= NB;  // keys live in shared memory
-  // ---- per-tile sort by (depth bits, index) ----
+  const int nch = (SORTED && spl.extra && !small) ? (n + NB - 1) / NB : 1;
+  const bool split = nch > 1 && spl.pbase[t] != ~0u;
+  if (!split && chunk > 0) continue;  // a long list that could not be split: chunk 0 walks it all
+  __syncthreads();  // shared memory of the previous item is free
+  // ---- per-tile sort by (depth bits, index) (lists longer than NB: sorted by k_sort_long) ----
   if (!SORTED) {
   } else if (small) {
     // rank sort, two keys per thread.  The rank is first counted on the 32-bit depth bits alone
@@ -952,19 +1032,9 @@ __global__ void __launch_bounds__(128) k_sort_blend16x2(RenderArgs a, const floa
 #pragma unroll
     for (int h = 0; h < 2; ++h)
       if (threadIdx.x + h * NT < n) vals[start + rank[h]] = (uint32_t)key[h];
-  } else {
-    uint64_t* gk = gkeys + start;
-    for (int e = threadIdx.x; e < n; e += NT) {
-      const uint32_t idx = vals[start + e];
-      gk[e] = ((uint64_t)__float_as_uint(rec[4 * idx + 1].z) << 32) | idx;
-    }
-    __syncthreads();
-    bitonic_sort(gk, n);
-    for (int e = threadIdx.x; e < n; e += NT) vals[start + e] = (uint32_t)gk[e];
   }
   __syncthreads();
   // ---- pixel state (two pixels) ----
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int lx = lane & 15, ly0 = 4 * w + (lane >> 4);
   const int x = tx * 16 + lx;
   float D[2], lim[2], ct[2][3];
@@ -1009,8 +1079,9 @@ __global__ void __launch_bounds__(128) k_sort_blend16x2(RenderArgs a, const floa
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) tile_end[t] = start + n_eff;
+  if (threadIdx.x == 0 && chunk == 0) tile_end[t] = start + n_eff;
   // ---- blend (per-warp compaction over the warp's 4-row strip, as k_sort_blend) ----
+  const int b_lo = split ? NB * (int)chunk : 0, b_hi = split ? min(b_lo + NB, n_eff) : n_eff;
   const int wy0 = ty * 16 + 4 * w, wy1 = wy0 + 3;
   float wlim = wl;
 #pragma unroll
@@ -1018,8 +1089,8 @@ __global__ void __launch_bounds__(128) k_sort_blend16x2(RenderArgs a, const floa
   float W0 = 0.f, A0 = 0.f, B0 = 0.f, G0 = 0.f, W1 = 0.f, A1 = 0.f, B1 = 0.f, G1 = 0.f;
   uint32_t n_eval = 0, n_acc = 0;  // COUNT: pixel-entry pairs whose q was evaluated / accepted
   bool wdone = !(wlim > -INFINITY);  // warp-uniform
-  for (int base = 0; base < n_eff; base += NB) {
-    const int cnt = min(NB, n_eff - base);
+  for (int base = b_lo; base < b_hi; base += NB) {
+    const int cnt = min(NB, b_hi - base);
     __syncthreads();
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -1089,6 +1160,27 @@ __global__ void __launch_bounds__(128) k_sort_blend16x2(RenderArgs a, const floa
       atomicAdd(io.counters + 1, c);
     }
   }
+  if (split) {
+    // this chunk's partial sums into its slot; the tile's last chunk combines them in order
+    const uint32_t slot = spl.pbase[t] + chunk;
+    const int p0i = ly0 * 16 + lx, p1i = (ly0 + 2) * 16 + lx;
+    spl.part[256 * (size_t)slot + p0i] = make_float4(W0, A0, B0, G0);
+    spl.part[256 * (size_t)slot + p1i] = make_float4(W1, A1, B1, G1);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) redi[0] = atomicAdd(&spl.tick[t], 1u) == (uint32_t)(nch - 1) ? 1u : 0u;
+    __syncthreads();
+    if (redi[0] == 0u) continue;  // another chunk of this tile finishes it
+    __threadfence();
+    W0 = A0 = B0 = G0 = W1 = A1 = B1 = G1 = 0.f;
+    const uint32_t b0s = spl.pbase[t];
+    for (int c = 0; c < nch; ++c) {
+      const float4 q0 = __ldcg(&spl.part[256 * (size_t)(b0s + c) + p0i]);
+      const float4 q1 = __ldcg(&spl.part[256 * (size_t)(b0s + c) + p1i]);
+      W0 += q0.x; A0 += q0.y; B0 += q0.z; G0 += q0.w;
+      W1 += q1.x; A1 += q1.y; B1 += q1.z; G1 += q1.w;
+    }
+  }
   // ---- Eq. 4 composite with W_t = 1, fused L1 ----
   float l1 = 0.f;
   uint32_t inmask = 0;
@@ -1112,7 +1204,7 @@ __global__ void __launch_bounds__(128) k_sort_blend16x2(RenderArgs a, const floa
       inmask += 1;
     }
   }
-  if (!io.target) return;
+  if (!io.target) continue;
   // deterministic CTA reduction (fixed shuffle tree + fixed smem order)
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -1135,12 +1227,12 @@ __global__ void __launch_bounds__(128) k_sort_blend16x2(RenderArgs a, const floa
     loss_part[t] = sum;
     if (m) atomicAdd(&hdr->mask_count, m);
     __threadfence();
-    const uint32_t ticket = atomicAdd(&hdr->ticket, 1u);
+    const uint32_t ticket = atomicAdd(&hdr->ticket, 1u);  // one per finished tile
     redi[0] = ticket == (uint32_t)(gridDim.x - 1) ? 1u : 0u;
   }
   __syncthreads();
-  if (redi[0] == 0u) return;
-  // last CTA: sum the tile partials in tile order (fixed tree) -> mean L1 (R-L1)
+  if (redi[0] == 0u) continue;
+  // last tile: sum the tile partials in tile order (fixed tree) -> mean L1 (R-L1)
   __threadfence();
   float sum = 0.f;
   for (int k = threadIdx.x; k < (int)gridDim.x; k += NT) sum += *(volatile float*)&loss_part[k];
@@ -1157,6 +1249,7 @@ __global__ void __launch_bounds__(128) k_sort_blend16x2(RenderArgs a, const floa
     if (io.loss_out) *io.loss_out = io.accumulate_loss ? *io.loss_out + lv : lv;
     hdr->ticket = 0u;
   }
+  }  // work items
 }
 
 // ============================================================================================
@@ -1230,21 +1323,13 @@ __global__ void __launch_bounds__(256) k_backward(RenderArgs a, const float4* __
                                                   const float* __restrict__ sdf_depth,
                                                   const float* __restrict__ cstar, const float* __restrict__ wg,
                                                   const uint32_t* __restrict__ target, const WsHeader* hdr,
-                                                  float* grad2d) {
+                                                  float* grad2d, const uint2* __restrict__ extra, uint32_t extra_cap) {
   constexpr int NP = TILE * TILE;
   __shared__ float4 sgs[NP];  // per pixel (g0, g1, g2, s): A * dL/dC*_ch and A * sum_ch g_ch C*_ch
   __shared__ float slim[NP];
   __shared__ uint32_t smagic[TILE + 1];  // ceil(65536 / w), w = 1..TILE
   if (threadIdx.x <= TILE) smagic[threadIdx.x] = threadIdx.x ? (65536u + threadIdx.x - 1u) / threadIdx.x : 0u;
-  const int t = blockIdx.x;
-  const int tx = t % a.tiles_x, ty = t / a.tiles_x;
-  const uint32_t m = backward_pixel_state<TILE>(a, t, sdf_depth, cstar, wg, target, hdr, sgs, slim);
-  __syncthreads();
-  if (!m) return;
-  const uint32_t start = min(offsets[t], a.cap);
-  const uint32_t end = min(tile_end[t], a.cap);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int tx0 = tx * TILE, ty0 = ty * TILE;
   // the lane that ends up holding each reduced value (reduce-scatter below), and which value
   int vidx;
   {
@@ -1254,13 +1339,38 @@ __global__ void __launch_bounds__(256) k_backward(RenderArgs a, const float4* __
     const int ka = kb < 0 ? -1 : (b3 ? (3 + kb < 5 ? 3 + kb : -1) : kb);
     vidx = (ka < 0 || (lane & 1)) ? -1 : (b4 ? (ka < 4 ? 5 + ka : -1) : ka);
   }
-  // entries are staged 256 at a time into shared memory by the whole CTA (independent loads),
-  // then each warp takes entries j = warp, warp + nw, ... of the batch
   __shared__ float4 se0[256], se1[256], se2[256], se3[256];
   __shared__ uint32_t sidx[256];
-  for (uint32_t base = start; base < end; base += 256) {
-    const int cnt_e = (int)min(256u, end - base);
-    __syncthreads();
+  // Work items of 256 list entries: CTA b takes (tile b, entries 0-255), then the further chunks
+  // of long lists that k_scan listed, extra[e] for e = b, b + grid, ... (the pixel state is
+  // loaded once per item; in the common case every tile is one item).
+  const uint32_t n_extra = min(hdr->n_extra, extra_cap);
+  int cur_tile = -1;
+  uint32_t m = 0;
+  for (uint32_t item = blockIdx.x; item < gridDim.x + n_extra; item += gridDim.x) {
+    int t;
+    uint32_t chunk;
+    if (item < gridDim.x) {
+      t = (int)item;
+      chunk = 0;
+    } else {
+      const uint2 w = extra[item - gridDim.x];
+      t = (int)w.x;
+      chunk = w.y;
+    }
+    const int tx = t % a.tiles_x, ty = t / a.tiles_x;
+    if (t != cur_tile) {
+      __syncthreads();  // the previous item's readers of the pixel state are done
+      m = backward_pixel_state<TILE>(a, t, sdf_depth, cstar, wg, target, hdr, sgs, slim);
+      cur_tile = t;
+    }
+    if (!m) return;  // empty loss mask: no gradient anywhere (uniform)
+    const uint32_t start = min(offsets[t], a.cap);
+    const uint32_t end = min(tile_end[t], a.cap);
+    const int tx0 = tx * TILE, ty0 = ty * TILE;
+    const uint32_t base = start + 256u * chunk;
+    const int cnt_e = base < end ? (int)min(256u, end - base) : 0;
+    __syncthreads();  // pixel state visible; the previous batch's readers are done
     for (int j = threadIdx.x; j < cnt_e; j += blockDim.x) {
       const uint32_t id = vals[base + j];
       sidx[j] = id;
@@ -1915,7 +2025,9 @@ gps_status forward_view(const gps_gaussians* g, const View1& v, const gps_render
   uint32_t* offsets = reinterpret_cast<uint32_t*>(ws + L.offsets);
   {
     GPS_PROF(K_SCAN, s);
-    k_scan<<<1, 1024, 0, s>>>(sp.counts, sp.bigcounts, offsets, n_tiles, hdr, stat, overflow_flag_dev());
+    k_scan<<<1, 1024, 0, s>>>(sp.counts, sp.bigcounts, offsets, n_tiles, hdr, stat, overflow_flag_dev(),
+                              reinterpret_cast<uint2*>(ws + L.extra), L.extra_cap,
+                              reinterpret_cast<uint32_t*>(ws + L.pbase), L.part_cap);
   }
   GPS_CHECK_LAUNCH("k_scan");
   uint32_t* vals = reinterpret_cast<uint32_t*>(ws + L.vals);
@@ -1935,6 +2047,16 @@ gps_status forward_view(const gps_gaussians* g, const View1& v, const gps_render
   io.accumulate_loss = accumulate_loss;
   io.counters = counters;
   uint64_t* gk = reinterpret_cast<uint64_t*>(ws + L.keys);
+  SplitIO spl{reinterpret_cast<const uint2*>(ws + L.extra), L.extra_cap, reinterpret_cast<const uint32_t*>(ws + L.pbase),
+              reinterpret_cast<uint32_t*>(ws + L.tick), reinterpret_cast<float4*>(ws + L.part)};
+  if (!c->sort_free && g->n > 0) {
+    GPS_PROF(K_SORT_LONG, s);
+    static const bool attr = cudaFuncSetAttribute(k_sort_long, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  8 * kLongSmem) == cudaSuccess;
+    if (!attr) return cuda_fail("cudaFuncSetAttribute(k_sort_long)", cudaGetLastError());
+    k_sort_long<<<148, 1024, 8 * kLongSmem, s>>>(sp.rec, offsets, vals, gk, n_tiles, (uint32_t)a.cap);
+    GPS_CHECK_LAUNCH("k_sort_long");
+  }
   uint32_t* tend = reinterpret_cast<uint32_t*>(ws + L.tile_end);
   float* lp = reinterpret_cast<float*>(ws + L.loss_part);
   {
@@ -1942,19 +2064,20 @@ gps_status forward_view(const gps_gaussians* g, const View1& v, const gps_render
   static const bool one_px = getenv("GPS_BLEND_1PX") != nullptr;  // the one-pixel-per-thread kernel
   if (counters) {  // debug: the instrumented instantiation (16x16 tiles)
     if (c->sort_free)
-      k_sort_blend16x2<false, true><<<n_tiles, 128, 0, s>>>(a, sp.rec, offsets, vals, gk, tend, lp, hdr, io, 0);
+      k_sort_blend16x2<false, true><<<n_tiles, 128, 0, s>>>(a, sp.rec, offsets, vals, gk, tend, lp, hdr, io, 0, spl);
     else
       k_sort_blend16x2<true, true><<<n_tiles, 128, 0, s>>>(a, sp.rec, offsets, vals, gk, tend, lp, hdr, io,
-                                                           c->tile_depth_precull);
+                                                           c->tile_depth_precull, spl);
   } else if (c->sort_free) {
     if (a.tile == 16 && !one_px)
-      k_sort_blend16x2<false><<<n_tiles, 128, 0, s>>>(a, sp.rec, offsets, vals, gk, tend, lp, hdr, io, 0);
+      k_sort_blend16x2<false><<<n_tiles, 128, 0, s>>>(a, sp.rec, offsets, vals, gk, tend, lp, hdr, io, 0, spl);
     else if (a.tile == 16)
       k_sort_blend<16, false><<<n_tiles, 256, 0, s>>>(a, sp.rec, offsets, vals, gk, tend, lp, hdr, io, 0);
     else
       k_sort_blend<8, false><<<n_tiles, 64, 0, s>>>(a, sp.rec, offsets, vals, gk, tend, lp, hdr, io, 0);
   } else if (a.tile == 16 && !one_px) {
-    k_sort_blend16x2<true><<<n_tiles, 128, 0, s>>>(a, sp.rec, offsets, vals, gk, tend, lp, hdr, io, c->tile_depth_precull);
+    k_sort_blend16x2<true><<<n_tiles, 128, 0, s>>>(a, sp.rec, offsets, vals, gk, tend, lp, hdr, io, c->tile_depth_precull,
+                                                    spl);
   } else if (a.tile == 16) {
     k_sort_blend<16, true><<<n_tiles, 256, 0, s>>>(a, sp.rec, offsets, vals, gk, tend, lp, hdr, io, c->tile_depth_precull);
   } else {
@@ -2118,15 +2241,18 @@ gps_status gps_refine_step(gps_gaussians* g, gps_adam_state* state, const gps_vi
     // sorted (this build's tile design): a warp per entry with a warp reduction
     const bool items = rcfg->backward == 2 || (rcfg->backward == 0 && rcfg->sort_free != 0);
     float* g2 = reinterpret_cast<float*>(grad2d);
+    const uint2* xtra = reinterpret_cast<const uint2*>(w + L.extra);
     if (items) {
       if (rcfg->tile == 16)
         k_backward_items<16><<<n_tiles, 256, 0, s>>>(a, rec, offsets, vals, tend, vw.sdf_depth, cstar, wg, tgt, hdr, g2);
       else
         k_backward_items<8><<<n_tiles, 256, 0, s>>>(a, rec, offsets, vals, tend, vw.sdf_depth, cstar, wg, tgt, hdr, g2);
     } else if (rcfg->tile == 16) {
-      k_backward<16><<<n_tiles, 256, 0, s>>>(a, rec, offsets, vals, tend, vw.sdf_depth, cstar, wg, tgt, hdr, g2);
+      k_backward<16><<<n_tiles, 256, 0, s>>>(a, rec, offsets, vals, tend, vw.sdf_depth, cstar, wg, tgt, hdr, g2,
+                                             xtra, L.extra_cap);
     } else {
-      k_backward<8><<<n_tiles, 256, 0, s>>>(a, rec, offsets, vals, tend, vw.sdf_depth, cstar, wg, tgt, hdr, g2);
+      k_backward<8><<<n_tiles, 256, 0, s>>>(a, rec, offsets, vals, tend, vw.sdf_depth, cstar, wg, tgt, hdr, g2,
+                                            xtra, L.extra_cap);
     }
     }
     GPS_CHECK_LAUNCH("k_backward");

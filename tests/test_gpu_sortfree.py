@@ -105,6 +105,6 @@ def test_sortfree_full_size_cfg4():
     st = G.AdamState(g)
     gout = g.zeros_like()
     ras.refine_step(g, st, [G.View(gcam, fr.R, fr.t, dev["Dt"], dev["Ct"], dev["tgt"])], grad_out=gout)
-    oloss, ref, gamb = oracle_grads(gd, ocam, fr.R, fr.t, Dt, Ct, tgt)
+    oloss, ref, gamb, sens = oracle_grads(gd, ocam, fr.R, fr.t, Dt, Ct, tgt, with_sens=True)
     assert abs(loss.item() - oloss) <= 1e-5 * oloss
-    compare_grads(gout.to_numpy(), ref, gamb, min_checked=10000)
+    compare_grads(gout.to_numpy(), ref, gamb, min_checked=10000, sens=sens)
