@@ -660,17 +660,8 @@ __global__ void __launch_bounds__(1024) k_sort_long(const float4* __restrict__ r
       keys[e] = ((uint64_t)__float_as_uint(rec[4 * idx + 1].z) << 32) | idx;
     }
     __syncthreads();
-    if (n <= (int)blockDim.x) {
-      // one key per thread: its rank is the number of smaller keys (keys are unique)
-      uint64_t mine = threadIdx.x < (unsigned)n ? keys[threadIdx.x] : ~0ull;
-      int rank = 0;
-      for (int j = 0; j < n; ++j) rank += keys[j] < mine;
-      __syncthreads();
-      if (threadIdx.x < (unsigned)n) vals[start + rank] = (uint32_t)mine;
-    } else {
-      bitonic_sort(keys, n);
-      for (int e = threadIdx.x; e < n; e += blockDim.x) vals[start + e] = (uint32_t)keys[e];
-    }
+    bitonic_sort(keys, n);
+    for (int e = threadIdx.x; e < n; e += blockDim.x) vals[start + e] = (uint32_t)keys[e];
     __syncthreads();
   }
 }
