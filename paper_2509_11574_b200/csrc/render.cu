@@ -74,7 +74,7 @@ struct WsHeader {
   uint32_t ticket;     // last-CTA election for the loss
   uint32_t n_extra;    // work items beyond one per tile (lists longer than 256 entries)
   uint32_t n_part;     // partial slots handed to long lists (the blend's split)
-  uint32_t pad1;
+  uint32_t n_long;     // tiles whose list is longer than 256 entries (k_sort_long's work)
   // ---- static: where this render's lists live (refine and render layouts differ) ----
   uint64_t off_vals, off_offsets, off_tile_end;
 };
@@ -82,7 +82,7 @@ struct WsHeader {
 
 struct WsLayout {
   size_t hdr, counts, cursor, bigcounts, offsets, tile_end, loss_part, records, ranks, grad2d, rec3, cgj, vals, keys,
-      cstar, wg, gbuf, extra, pbase, tick, part, total;
+      cstar, wg, gbuf, extra, pbase, tick, part, longl, total;
   uint32_t extra_cap, part_cap;
   size_t zero_begin, zero_bytes;
 };
@@ -118,8 +118,9 @@ WsLayout ws_layout(int64_t n, int W, int H, int tile, int64_t cap, int64_t n_par
   L.extra_cap = (uint32_t)std::min<int64_t>(cap / 256 + 1, 0x7FFFFFFF);
   L.extra = take(8 * (size_t)L.extra_cap);  // {tile, chunk} work items of long lists
   L.pbase = take(4 * tiles);                 // per long list: its first partial slot (or ~0)
-  L.part_cap = 2048;                         // 2048 chunks of 256 entries (8 MB) per render
+  L.part_cap = 8192;                         // 8192 chunks of 256 entries (32 MB) per render
   L.part = take(16 * 256 * (size_t)L.part_cap);
+  L.longl = take(4 * tiles);                 // the tiles with long lists
   L.cstar = refine ? take(12 * (size_t)W * H) : 0;
   L.wg = refine ? take(4 * (size_t)W * H) : 0;
   L.gbuf = gbuf ? take(4 * (size_t)n_params) : 0;
@@ -482,7 +483,7 @@ __global__ void __launch_bounds__(1024) k_scan(const uint32_t* __restrict__ coun
                                                const uint32_t* __restrict__ bigcounts, uint32_t* offsets,
                                                int n_tiles, WsHeader* hdr, WsHeader stat,
                                                uint32_t* sticky_overflow, uint2* extra, uint32_t extra_cap,
-                                               uint32_t* pbase, uint32_t part_cap) {
+                                               uint32_t* pbase, uint32_t part_cap, uint32_t* longl) {
   __shared__ uint32_t warp_sums[32];
   __shared__ uint32_t carry;
   if (threadIdx.x == 0) carry = 0;
@@ -524,6 +525,7 @@ __global__ void __launch_bounds__(1024) k_scan(const uint32_t* __restrict__ coun
         const uint32_t at = atomicAdd(&hdr->n_extra, more);
         for (uint32_t q = 0; q < more && at + q < extra_cap; ++q) extra[at + q] = make_uint2((uint32_t)(i0 + k), q + 1u);
         // the blend splits the list only when all its chunks have work items and partial slots
+        longl[atomicAdd(&hdr->n_long, 1u)] = (uint32_t)(i0 + k);
         const uint32_t pb = atomicAdd(&hdr->n_part, more + 1u);
         pbase[i0 + k] = (at + more <= extra_cap && pb + more + 1u <= part_cap) ? pb : ~0u;
       }
@@ -638,7 +640,7 @@ __device__ __forceinline__ void bitonic_sort(Keys keys, int n) {
 
 // ============================================================================================
 // k_sort_long: tiles whose list is longer than kShortList entries are sorted here, by (depth bits,
-// index) keys, one 1024-thread CTA per tile (grid-stride over the tiles): a bitonic network in
+// index) keys, one 512-thread CTA per tile (grid-stride over k_scan's list): a bitonic network in
 // shared memory up to kLongSmem keys, in the global key buffer beyond.  The blend kernels rank-
 // sort the short lists themselves and take the long ones as they are.  (A 128-thread blend CTA
 // sorting a 6000-entry list in global memory was the whole kernel's tail: late cfg4 frames see
@@ -647,13 +649,15 @@ __device__ __forceinline__ void bitonic_sort(Keys keys, int n) {
 constexpr int kShortList = 256;
 constexpr int kLongSmem = 8192;  // 64 KB of dynamic shared memory
 
-__global__ void __launch_bounds__(1024) k_sort_long(const float4* __restrict__ rec, const uint32_t* __restrict__ offsets,
-                                                   uint32_t* vals, uint64_t* gkeys, int n_tiles, uint32_t cap) {
+__global__ void __launch_bounds__(512) k_sort_long(const float4* __restrict__ rec, const uint32_t* __restrict__ offsets,
+                                                  uint32_t* vals, uint64_t* gkeys, const uint32_t* __restrict__ longl,
+                                                  const WsHeader* hdr, uint32_t cap) {
   extern __shared__ __align__(16) uint64_t sk[];
-  for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+  const uint32_t n_long = hdr->n_long;  // k_scan listed the tiles longer than kShortList
+  for (uint32_t li = blockIdx.x; li < n_long; li += gridDim.x) {
+    const int t = (int)longl[li];
     const uint32_t start = min(offsets[t], cap), end = min(offsets[t + 1], cap);
     const int n = (int)(end - start);
-    if (n <= kShortList) continue;  // uniform across the CTA
     uint64_t* keys = n <= kLongSmem ? sk : gkeys + start;
     for (int e = threadIdx.x; e < n; e += blockDim.x) {
       const uint32_t idx = vals[start + e];
@@ -2018,7 +2022,8 @@ gps_status forward_view(const gps_gaussians* g, const View1& v, const gps_render
     GPS_PROF(K_SCAN, s);
     k_scan<<<1, 1024, 0, s>>>(sp.counts, sp.bigcounts, offsets, n_tiles, hdr, stat, overflow_flag_dev(),
                               reinterpret_cast<uint2*>(ws + L.extra), L.extra_cap,
-                              reinterpret_cast<uint32_t*>(ws + L.pbase), L.part_cap);
+                              reinterpret_cast<uint32_t*>(ws + L.pbase), L.part_cap,
+                              reinterpret_cast<uint32_t*>(ws + L.longl));
   }
   GPS_CHECK_LAUNCH("k_scan");
   uint32_t* vals = reinterpret_cast<uint32_t*>(ws + L.vals);
@@ -2045,7 +2050,11 @@ gps_status forward_view(const gps_gaussians* g, const View1& v, const gps_render
     static const bool attr = cudaFuncSetAttribute(k_sort_long, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                   8 * kLongSmem) == cudaSuccess;
     if (!attr) return cuda_fail("cudaFuncSetAttribute(k_sort_long)", cudaGetLastError());
-    k_sort_long<<<148, 1024, 8 * kLongSmem, s>>>(sp.rec, offsets, vals, gk, n_tiles, (uint32_t)a.cap);
+    // 3 CTAs of 512 threads per SM (64 KB of keys each): parts of the cfg4 trajectory have
+    // hundreds of long lists per view, each a ~55-stage network
+    k_sort_long<<<148 * 3, 512, 8 * kLongSmem, s>>>(sp.rec, offsets, vals, gk,
+                                                     reinterpret_cast<const uint32_t*>(ws + L.longl), hdr,
+                                                     (uint32_t)a.cap);
     GPS_CHECK_LAUNCH("k_sort_long");
   }
   uint32_t* tend = reinterpret_cast<uint32_t*>(ws + L.tile_end);
