@@ -1,10 +1,5 @@
 #!/bin/bash
 # scratch GPU session script (gpurun)
-for r in 1 2 3 4 5; do
-  python bench.py --steps 20 --warmup 5 --no-cpu-baseline --no-profile > gpurun_out/g.json 2> gpurun_out/g.err
-  python -c "
-import json
-d=json.load(open('gpurun_out/g.json'))
-print('run $r', d['value'], d['ms_per_step'], d['host_enqueue_ms_per_step'], 'e2e', d['e2e']['value'], d['e2e']['ms_per_step'], d['e2e']['host_enqueue_ms_per_step'], d['e2e']['allocator'])
-" || tail -3 gpurun_out/g.err
-done
+python -m pytest tests/test_gpu_render_refine.py tests/test_gpu_edges.py tests/test_gpu_sortfree.py tests/test_gpu_pipeline.py -m gpu -x -q 2>&1 | tail -3
+bash tools/ab.sh "--steps 20 --warmup 5 --no-cpu-baseline --no-e2e" base pdl > gpurun_out/ab.log 2>&1
+cat gpurun_out/ab.log

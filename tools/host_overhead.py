@@ -23,6 +23,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--history", type=int, default=30)
+    ap.add_argument("--cprofile", action="store_true", help="cProfile the enqueue loop (host hot spots)")
     args = ap.parse_args()
     cfg = S.get_config("cfg4")
     scene = S.make_scene(cfg)
@@ -52,12 +53,21 @@ def main():
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
+    prof = None
+    if args.cprofile:
+        import cProfile
+        prof = cProfile.Profile()
+        prof.enable()
     h0 = time.perf_counter()
     for _ in range(10 * args.steps):
         f = frames[k]
         pipe.process_frame(k, f.depth, f.rgba, f.R, f.t)
         k += 1
     h1 = time.perf_counter()
+    if prof is not None:
+        prof.disable()
+        import pstats
+        pstats.Stats(prof).sort_stats("tottime").print_stats(25)
     pipe.join()
     e1.record()
     torch.cuda.synchronize()
