@@ -505,6 +505,9 @@ def per_kernel_bytes(args, cfg, n_g, P, per_launch, rstats, vstats, upd0, prof):
     out["k_sort_blend"] = (48 + 8) * K + 36 * HW                # records + values, D_t C_t C_k in, C* W_G out
     out["k_backward"] = (64 + 4 + 36) * K + 24 * HW             # records, values, 2D-gradient reductions; pixel state
     out["k_chain"] = (48 + 4 * (P - 3) + 12 + 48 + 128) * nvis  # 2D grads, params, cgj, gradient record
+    # fused chain + Adam: p, m, v read and written (24 P), every Gaussian's 2D-gradient slot (48),
+    # the visible ones' colour Jacobian (48); the chain's parameter reads are the update's own
+    out["k_chain_adam"] = (24 * P + 48) * n_g + 48 * nvis
     return out
 
 

@@ -11,7 +11,7 @@ namespace gps {
 bool g_prof_on = false;
 namespace {
 const char* kNames[K_COUNT] = {"k_alloc",      "k_integrate", "k_raycast",  "k_preprocess", "k_scan",
-                               "k_emit",       "k_sort_blend", "k_backward", "k_adam", "memset", "k_range", "k_link", "k_chain", "k_sort_long"};
+                               "k_emit",       "k_sort_blend", "k_backward", "k_adam", "memset", "k_range", "k_link", "k_chain", "k_sort_long", "k_chain_adam"};
 struct Pair {
   cudaEvent_t a, b;
   int id;

@@ -7,7 +7,7 @@
 namespace gps {
 enum KernelId {
   K_ALLOC = 0, K_INTEGRATE, K_RAYCAST, K_PREPROCESS, K_SCAN, K_EMIT, K_SORT_BLEND, K_BACKWARD, K_GRAD_ADAM,
-  K_MEMSET, K_RANGE, K_LINK, K_CHAIN, K_SORT_LONG, K_COUNT
+  K_MEMSET, K_RANGE, K_LINK, K_CHAIN, K_SORT_LONG, K_CHAIN_ADAM, K_COUNT
 };
 extern bool g_prof_on;
 void prof_begin(int id, cudaStream_t s);

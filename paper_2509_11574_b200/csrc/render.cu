@@ -1816,6 +1816,14 @@ __device__ __forceinline__ float sqrt_approx(float x) {
   return r;
 }
 
+// R-ADAM for one element, in explicit rounding steps (no contraction left to the compiler), so
+// that every kernel applying it -- k_adam and the fused k_chain_adam -- produces the same bits
+__device__ __forceinline__ void adam_elem(float& p, float& m, float& v, float gr, float st, const AdamArgs& ad) {
+  m = __fmaf_rn(ad.b1, m, __fmul_rn(1.0f - ad.b1, gr));
+  v = __fmaf_rn(ad.b2, v, __fmul_rn(__fmul_rn(1.0f - ad.b2, gr), gr));
+  p = __fsub_rn(p, __fdividef(__fmul_rn(st, m), __fmaf_rn(sqrt_approx(v), ad.inv_sqrt_bc2, ad.eps)));
+}
+
 template <int GRP, int DIM>
 __device__ __forceinline__ void adam_unit(float* __restrict__ P, float* __restrict__ M, float* __restrict__ V,
                                           const float* __restrict__ E, float* __restrict__ O, uint32_t len,
@@ -1869,9 +1877,7 @@ __device__ __forceinline__ void adam_unit(float* __restrict__ P, float* __restri
     if (src.has_gout && (uint32_t)k < cnt) O[e0 + k] = gr;
     const uint32_t comp = (e0 + k) % DIM;
     const float st = (GRP == 4 && comp < 3u) ? ad.step_sh0 : step;
-    m[k] = ad.b1 * m[k] + (1.0f - ad.b1) * gr;
-    v[k] = ad.b2 * v[k] + (1.0f - ad.b2) * gr * gr;
-    p[k] -= __fdividef(st * m[k], sqrt_approx(v[k]) * ad.inv_sqrt_bc2 + ad.eps);
+    adam_elem(p[k], m[k], v[k], gr, st, ad);
   }
   if (cnt == 4u) {
     *reinterpret_cast<float4*>(P + e0) = make_float4(p[0], p[1], p[2], p[3]);
@@ -1919,6 +1925,180 @@ __global__ void __launch_bounds__(kAdamThreads) k_adam(RenderArgs a, gps_gaussia
       case 12: adam_unit<4, 12>(g.sh, gm.sh, gv.sh, src.gbuf.sh, src.gout.sh, nsh * n, u, src, ad, ad.step_shr); break;
       case 27: adam_unit<4, 27>(g.sh, gm.sh, gv.sh, src.gbuf.sh, src.gout.sh, nsh * n, u, src, ad, ad.step_shr); break;
       default: adam_unit<4, 48>(g.sh, gm.sh, gv.sh, src.gbuf.sh, src.gout.sh, nsh * n, u, src, ad, ad.step_shr); break;
+    }
+  }
+}
+
+// --------------------------------------------------------------------------------------------
+// k_chain_adam (a11 fused, single-view refine steps): one CTA per chunk of kCaG Gaussians.
+//  phase A: a thread per Gaussian runs the R-GRAD chain (chain3d, as k_chain) when its 2D
+//           gradient is non-zero and leaves the raw gradient terms in shared memory
+//           {gx[3], gls[3], gq[4], gop, dcol[3], Y[16]} (zeros otherwise: R-ADAM's dense update
+//           with a zero gradient, as k_adam's unflagged record);
+//  phase B: the CTA streams the chunk's slices of the five parameter groups (p, m, v as float4
+//           units, 4 units per thread in flight) and applies adam_elem with the gradient read
+//           from shared memory (SH: Y[k] * dcol[ch], the product k_adam forms from the record).
+// Same arithmetic as k_chain<0> + k_adam, so the same bits (tests/test_gpu_render_refine.py),
+// without the 128-byte record round trip and one launch; CTAs of an SM in different phases
+// overlap the latency-bound chain with the streaming update.
+// --------------------------------------------------------------------------------------------
+constexpr int kCaG = 128;      // Gaussians per CTA (= threads)
+constexpr int kCaStride = 31;  // floats per Gaussian in shared memory (odd: conflict-free columns)
+
+struct CaGroup {
+  float* P;
+  float* M;
+  float* V;
+  float* O;
+};
+
+__global__ void __launch_bounds__(kCaG, 4) k_chain_adam(RenderArgs a, gps_gaussians g, gps_gaussians gm,
+                                                      gps_gaussians gv, const float4* __restrict__ grad2d,
+                                                      const float4* __restrict__ cgj, gps_gaussians gout,
+                                                      int has_gout, AdamArgs ad) {
+  __shared__ float sg[kCaG * kCaStride];
+  const int64_t g0 = (int64_t)blockIdx.x * kCaG;
+  const int cg = (int)(a.n - g0 < (int64_t)kCaG ? a.n - g0 : (int64_t)kCaG);
+  // ---- phase A ----
+  {
+    const int t = threadIdx.x;
+    float* o = sg + t * kCaStride;
+#pragma unroll
+    for (int k = 0; k < 30; ++k) o[k] = 0.f;
+    if (t < cg) {
+      const int64_t i = g0 + t;
+      const float4 q0 = grad2d[3 * i], q1 = grad2d[3 * i + 1], q2 = grad2d[3 * i + 2];
+      float dcol[3] = {q1.z, q1.w, q2.x};
+      const bool nz = (q0.x != 0.f) | (q0.y != 0.f) | (q0.z != 0.f) | (q0.w != 0.f) | (q1.x != 0.f) |
+                      (q1.y != 0.f) | (dcol[0] != 0.f) | (dcol[1] != 0.f) | (dcol[2] != 0.f);
+      if (nz) {
+        float gx[3], gls[3], gq[4], gop, Y[16];
+        chain3d(a, g, i, q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, dcol, gx, gls, gq, gop, Y, cgj);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          o[k] = gx[k];
+          o[3 + k] = gls[k];
+          o[11 + k] = dcol[k];
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) o[6 + k] = gq[k];
+        o[10] = gop;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) o[14 + k] = Y[k];
+      }
+    }
+  }
+  __syncthreads();
+  // ---- phase B: units of the chunk's group slices, concatenated (group table in shared memory:
+  // dynamically indexed, it would otherwise live on the stack) ----
+  __shared__ CaGroup grp[5];
+  __shared__ uint32_t len[5], dims[5], ub[6];
+  __shared__ float idim[5], steps[5];
+  __shared__ int soff[5];
+  const uint32_t nsh = 3u * (uint32_t)a.nc;
+  if (threadIdx.x == 0) {
+    const uint32_t ln[5] = {3u * cg, 3u * cg, 4u * cg, (uint32_t)cg, nsh * cg};
+    const uint32_t dm[5] = {3u, 3u, 4u, 1u, nsh};
+    const int so[5] = {0, 3, 6, 10, 14};
+    const float st[5] = {ad.step_xyz, ad.step_ls, ad.step_rot, ad.step_op, ad.step_shr};
+    float* const Ps[5] = {g.xyz + 3 * g0, g.log_scale + 3 * g0, g.rot + 4 * g0, g.opacity_raw + g0, g.sh + nsh * g0};
+    float* const Ms[5] = {gm.xyz + 3 * g0, gm.log_scale + 3 * g0, gm.rot + 4 * g0, gm.opacity_raw + g0, gm.sh + nsh * g0};
+    float* const Vs[5] = {gv.xyz + 3 * g0, gv.log_scale + 3 * g0, gv.rot + 4 * g0, gv.opacity_raw + g0, gv.sh + nsh * g0};
+    ub[0] = 0;
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+      len[q] = ln[q];
+      dims[q] = dm[q];
+      idim[q] = 1.0f / (float)dm[q];
+      steps[q] = st[q];
+      soff[q] = so[q];
+      ub[q + 1] = ub[q] + (ln[q] + 3u) / 4u;
+      grp[q].P = Ps[q];
+      grp[q].M = Ms[q];
+      grp[q].V = Vs[q];
+    }
+    grp[0].O = has_gout ? gout.xyz + 3 * g0 : nullptr;
+    grp[1].O = has_gout ? gout.log_scale + 3 * g0 : nullptr;
+    grp[2].O = has_gout ? gout.rot + 4 * g0 : nullptr;
+    grp[3].O = has_gout ? gout.opacity_raw + g0 : nullptr;
+    grp[4].O = has_gout ? gout.sh + nsh * g0 : nullptr;
+  }
+  __syncthreads();
+  constexpr int kU = 4;  // units per thread in flight
+  for (uint32_t U0 = threadIdx.x; U0 < ub[5]; U0 += kU * kCaG) {
+    float p[kU][4], m[kU][4], v[kU][4];
+    int gq[kU];
+    uint32_t e0[kU], cnt[kU];
+#pragma unroll
+    for (int j = 0; j < kU; ++j) {
+      const uint32_t U = U0 + j * kCaG;
+      int q = 0;
+#pragma unroll
+      for (int r = 1; r < 5; ++r) q += U >= ub[r];
+      gq[j] = q;
+      cnt[j] = 0;
+      e0[j] = 0;
+      if (U < ub[5]) {
+        e0[j] = 4u * (U - ub[q]);
+        cnt[j] = min(4u, len[q] - e0[j]);
+      }
+      const CaGroup G = grp[q];
+      if (cnt[j] == 4u) {
+        const float4 p4 = *reinterpret_cast<const float4*>(G.P + e0[j]);
+        const float4 m4 = *reinterpret_cast<const float4*>(G.M + e0[j]);
+        const float4 v4 = *reinterpret_cast<const float4*>(G.V + e0[j]);
+        p[j][0] = p4.x; p[j][1] = p4.y; p[j][2] = p4.z; p[j][3] = p4.w;
+        m[j][0] = m4.x; m[j][1] = m4.y; m[j][2] = m4.z; m[j][3] = m4.w;
+        v[j][0] = v4.x; v[j][1] = v4.y; v[j][2] = v4.z; v[j][3] = v4.w;
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const bool in = (uint32_t)k < cnt[j];
+          p[j][k] = in ? G.P[e0[j] + k] : 0.f;
+          m[j][k] = in ? G.M[e0[j] + k] : 0.f;
+          v[j][k] = in ? G.V[e0[j] + k] : 0.f;
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kU; ++j) {
+      if (cnt[j] == 0u) continue;
+      const int q = gq[j];
+      const uint32_t dim = dims[q];
+      const CaGroup G = grp[q];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t e = e0[j] + k;
+        // e / dim for e < 48 * kCaG: (e + 1/2) / dim is >= 1/(2 dim) from an integer, far beyond
+        // the fp32 error of the product
+        const uint32_t gl = __float2uint_rz(((float)e + 0.5f) * idim[q]), comp = e - gl * dim;
+        const float* o = sg + gl * kCaStride;
+        float gr, st = steps[q];
+        if (q == 4) {
+          gr = o[14 + comp / 3u] * o[11 + comp % 3u];
+          if (comp < 3u) st = ad.step_sh0;
+        } else {
+          gr = o[soff[q] + comp];
+        }
+        if ((uint32_t)k < cnt[j]) {
+          if (has_gout) G.O[e] = gr;
+          adam_elem(p[j][k], m[j][k], v[j][k], gr, st, ad);
+        }
+      }
+      if (cnt[j] == 4u) {
+        *reinterpret_cast<float4*>(G.P + e0[j]) = make_float4(p[j][0], p[j][1], p[j][2], p[j][3]);
+        *reinterpret_cast<float4*>(G.M + e0[j]) = make_float4(m[j][0], m[j][1], m[j][2], m[j][3]);
+        *reinterpret_cast<float4*>(G.V + e0[j]) = make_float4(v[j][0], v[j][1], v[j][2], v[j][3]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if ((uint32_t)k < cnt[j]) {
+            G.P[e0[j] + k] = p[j][k];
+            G.M[e0[j] + k] = m[j][k];
+            G.V[e0[j] + k] = v[j][k];
+          }
+        }
+      }
     }
   }
 }
@@ -2223,6 +2403,8 @@ gps_status gps_refine_step(gps_gaussians* g, gps_adam_state* state, const gps_vi
     GPS_CHECK_CUDA(cudaMemsetAsync(w + L.gbuf, 0, sizeof(float) * gbuf_floats(g), s));
   if (loss_out) GPS_CHECK_CUDA(cudaMemsetAsync(loss_out, 0, sizeof(float), s));
   AdamArgs ad = make_adam(acfg, state->step + 1);
+  // GPS_UNFUSED_ADAM=1: k_chain + k_adam instead of k_chain_adam (A/B and the bitwise test)
+  const bool fused = n_views == 1 && getenv("GPS_UNFUSED_ADAM") == nullptr;
   for (int v = 0; v < n_views; ++v) {
     const gps_view& vw = views[v];
     View1 v1{&vw.K, &vw.T, vw.sdf_depth, vw.sdf_color, vw.target_rgba};
@@ -2256,7 +2438,15 @@ gps_status gps_refine_step(gps_gaussians* g, gps_adam_state* state, const gps_vi
     }
     }
     GPS_CHECK_LAUNCH("k_backward");
-    if (g->n > 0) {
+    if (g->n > 0 && fused) {
+      // single view: chain rule and Adam in one kernel (a11), same bits as the two below
+      RenderArgs a0 = make_args(g, &views[0].K, &views[0].T, rcfg, cap);
+      GPS_PROF(K_CHAIN_ADAM, s);
+      k_chain_adam<<<(unsigned)((g->n + kCaG - 1) / kCaG), kCaG, 0, s>>>(
+          a0, *g, state->m, state->v, grad2d, reinterpret_cast<const float4*>(w + L.cgj),
+          grad_out ? *grad_out : gps_gaussians{}, grad_out != nullptr, ad);
+      GPS_CHECK_LAUNCH("k_chain_adam");
+    } else if (g->n > 0) {
       const unsigned cgrid = (unsigned)((g->n + kChainThreads - 1) / kChainThreads);
       float4* rec3 = reinterpret_cast<float4*>(w + L.rec3);
       GPS_PROF(K_CHAIN, s);
@@ -2268,7 +2458,7 @@ gps_status gps_refine_step(gps_gaussians* g, gps_adam_state* state, const gps_vi
       GPS_CHECK_LAUNCH("k_chain");
     }
   }
-  if (g->n > 0) {
+  if (g->n > 0 && !fused) {
     RenderArgs a = make_args(g, &views[0].K, &views[0].T, rcfg, cap);
     AdamSrc src{};
     src.grad2d = grad2d;

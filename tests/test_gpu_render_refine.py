@@ -420,3 +420,43 @@ def test_tile_lists_with_equal_depths_bit_exact():
     gv, grng = ras.lists()
     assert np.array_equal(grng, orng) and np.array_equal(gv, ov)
     check_forward(O.render(gd, ocam, fr.R, fr.t, Dt, Ct), Cs, W)
+
+
+@pytest.mark.parametrize("deg,n", [(3, 50001), (1, 1001)])
+def test_fused_chain_adam_matches_the_unfused_pair(deg, n, monkeypatch):
+    """k_chain_adam (single-view refine steps) applies the same chain rule and the same Adam
+    arithmetic as k_chain + k_adam (GPS_UNFUSED_ADAM=1, read per call).  The backward's 2D
+    gradient totals arrive by fp32 atomics (order-dependent in the last bits), so two runs agree
+    to rounding, not bitwise: raw gradients and moments within 1e-4 relative (plus 1e-6 of the
+    group's largest), parameters within 2 lr (Adam's first step is ~lr sign(g)).  n not a multiple
+    of the 128-Gaussian chunk, 3n not a multiple of 4 (ragged chunk and float4 units)."""
+    import paper_2509_11574_b200 as G
+    cfg = S.get_config("cfg2")
+    fr = H.frames(cfg, 1, start=5)[0]
+    gd = S.make_gaussians(cfg, n=n, sh_degree=deg)
+    Dt, Ct = S.sdf_stage_inputs(cfg, fr, seed=5)
+    tgt = S.target_rgba(cfg, fr).cuda().contiguous()
+    gcam, _ = H.cams(cfg)
+    view = G.View(gcam, fr.R, fr.t, torch.from_numpy(Dt).cuda(), torch.from_numpy(Ct).cuda(), tgt)
+    res = {}
+    for mode in ("fused", "unfused"):
+        if mode == "unfused":
+            monkeypatch.setenv("GPS_UNFUSED_ADAM", "1")
+        else:
+            monkeypatch.delenv("GPS_UNFUSED_ADAM", raising=False)
+        g = G.Gaussians.from_dict(gd)
+        st = G.AdamState(g)
+        gout = g.zeros_like()
+        ras = G.Rasterizer(g.n, gcam, G.RenderConfig())
+        loss = ras.refine_step(g, st, [view], grad_out=gout).item()
+        torch.cuda.synchronize()
+        res[mode] = (loss, g.to_numpy(), st.m.to_numpy(), st.v.to_numpy(), gout.to_numpy())
+    fl, fu = res["fused"], res["unfused"]
+    assert fl[0] == fu[0]  # the forward is bit-reproducible
+    lr = {"xyz": 1.6e-4, "log_scale": 5e-3, "rot": 1e-3, "opacity_raw": 5e-2, "sh": 2.5e-3}
+    for k in GROUPS:
+        for a, b in ((fl[4][k], fu[4][k]), (fl[2][k], fu[2][k]), (fl[3][k], fu[3][k])):
+            a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+            assert np.all(np.abs(a - b) <= 1e-4 * np.abs(b) + 1e-6 * np.abs(b).max()), k
+            assert np.count_nonzero(b) > 0 and np.array_equal(a != 0, b != 0), k
+        assert np.max(np.abs(np.asarray(fl[1][k], np.float64) - fu[1][k])) <= 2 * lr[k], k
