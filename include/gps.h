@@ -436,6 +436,26 @@ gps_status gps_debug_export_blocks_sync(const gps_volume* vol, gps_stream_t stre
  * against a recount; *n_bad (host) = apron cells that differ + blocks whose count is wrong.
  * Debug only.                                                                               */
 gps_status gps_debug_apron_check_sync(const gps_volume* vol, gps_stream_t stream, int64_t* n_bad /*host*/);
+/* Checks the hash table, pool and neighbour tables (the lock-free insert of gps_fuse and the
+ * neighbour linking): every occupied slot's pool block carries the slot's key,
+ * every pool block is found at its key, each block's 8 +neighbour and 8 -neighbour entries equal
+ * a fresh lookup, dense-grid cells of allocated blocks hold their pool index, and the occupied
+ * slots number exactly the pool blocks (no key inserted twice).  *n_bad (host) = violations.
+ * Debug only (synchronises).                                                                */
+gps_status gps_debug_hash_check_sync(const gps_volume* vol, gps_stream_t stream, int64_t* n_bad /*host*/);
+/* Checked build (libgps_checked.so, compiled with -DGPS_CHECKED): the hot
+ * kernels evaluate their index bounds and record each failed kind as one bit of a device word
+ * without stopping: bit 0 pool block index, 1 plane offset, 2 pixel, 3 hash slot / grid cell,
+ * 4 visible list, 5 range tile, 6 neighbour entry, 7 sub-block count byte leaving [0, 125],
+ * 16 pair index, 17 tile, 18 Gaussian index, 19 a list entry outside its tile's range,
+ * 20 shared-memory staging index, 21 fused-Adam element, 22 long-list partial slot,
+ * 24 adding / removal index, 28 tracking index.  Synchronises the device, then *word (host)
+ * receives the OR of the bits since the last call (which clears them) and *checked (host,
+ * nullable) 1 for the checked build, 0 for the production build (whose word stays 0).       */
+gps_status gps_debug_check_word_sync(int64_t* word /*host*/, int32_t* checked /*host*/);
+/* Enqueues one kernel whose bound check fails for bit `bit` (0..63): in the checked build the next
+ * gps_debug_check_word_sync reports that bit (the mechanism's self-test); a no-op otherwise.  */
+gps_status gps_debug_check_selftest(int32_t bit, gps_stream_t stream);
 /* Runs the forward of gps_render (16x16 tiles) in its instrumented form and counts, over all
  * pixels, the pixel-entry pairs whose membership q was evaluated (*evaluated: the entry survived
  * the warp's strip test and the pixel's Eq. 1 depth indicator) and those accepted (*accepted:

@@ -129,6 +129,9 @@ PROTOTYPES = {
     "gps_debug_export_blocks_sync": (gps_status, [vp, gps_stream_t, vp, vp, i64, P(i64)]),
     "gps_debug_export_visible_sync": (gps_status, [vp, gps_stream_t, vp, i64, P(i64)]),
     "gps_debug_apron_check_sync": (gps_status, [vp, gps_stream_t, P(i64)]),
+    "gps_debug_hash_check_sync": (gps_status, [vp, gps_stream_t, P(i64)]),
+    "gps_debug_check_word_sync": (gps_status, [P(i64), P(C.c_int32)]),
+    "gps_debug_check_selftest": (gps_status, [C.c_int32, gps_stream_t]),
     "gps_debug_raycast_footprint_sync": (gps_status, [vp, P(gps_intrinsics), P(gps_pose), gps_stream_t, P(i64)]),
     "gps_debug_render_lists_sync": (gps_status, [vp, gps_stream_t, vp, i64, vp, P(i64)]),
     "gps_debug_render_counts_sync": (gps_status, [P(gps_gaussians), P(gps_intrinsics), P(gps_pose), vp, vp,
@@ -167,6 +170,8 @@ def load(path: str | None = None):
         raise OSError(f"libgps.so not built at {p}: run `python paper_2509_11574_b200/build.py`")
     L = C.CDLL(p)
     for name, (res, args) in PROTOTYPES.items():
+        if name.startswith("gps_debug_") and not hasattr(L, name):
+            continue  # an older A/B build without a later debug hook
         fn = getattr(L, name)
         fn.restype = res
         fn.argtypes = args

@@ -205,6 +205,13 @@ class Volume:
         N.check("gps_debug_apron_check_sync", _L.gps_debug_apron_check_sync(self.h, _stream(stream), C.byref(n)))
         return n.value
 
+    def hash_mismatches(self, stream=None) -> int:
+        """Violations of the hash / pool / neighbour-table invariants (gps_debug_hash_check_sync);
+        0 after every fuse (debug; synchronises)."""
+        n = C.c_int64()
+        N.check("gps_debug_hash_check_sync", _L.gps_debug_hash_check_sync(self.h, _stream(stream), C.byref(n)))
+        return n.value
+
     def raycast_footprint(self, cam: Camera, R, t, stream=None) -> int:
         """Number of distinct tsdf voxels a raycast from (R, t) reads (debug; synchronises)."""
         n = C.c_int64()
@@ -597,3 +604,11 @@ def track_result(raw) -> dict:
             "T": (np.array(out.T.R[:], np.float32).reshape(3, 3), np.array(out.T.t[:], np.float32)),
             "converged": bool(out.converged), "degenerate": bool(out.degenerate), "inlier_frac": out.inlier_frac,
             "inliers": out.inliers, "steps": out.steps, "energy": out.energy, "pivot_ratio": out.pivot_ratio}
+
+
+def check_word() -> tuple[int, bool]:
+    """(OR of the checked build's failed-bound bits since the last call, whether the loaded library
+    is the checked build); synchronises the device (gps_debug_check_word_sync)."""
+    w, c = C.c_int64(), C.c_int32()
+    N.check("gps_debug_check_word_sync", _L.gps_debug_check_word_sync(C.byref(w), C.byref(c)))
+    return w.value, bool(c.value)

@@ -34,16 +34,23 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(d) <= t for d in deps())
 
 
-def build(force: bool = False, verbose: bool = False, out: str | None = None) -> str:
+LIB_CHECKED = os.path.join(HERE, "libgps_checked.so")
+
+
+def build(force: bool = False, verbose: bool = False, out: str | None = None, checked: bool = False) -> str:
+    """checked=True: the bounds-checked variant (-DGPS_CHECKED) into
+    libgps_checked.so (or `out`); the production library is never replaced by it."""
+    if checked and out is None:
+        out = LIB_CHECKED
     if out is None and not force and up_to_date():
         return LIB
     objs = []
-    bdir = os.path.join(HERE, "build")
+    bdir = os.path.join(HERE, "build_checked" if checked else "build")
     os.makedirs(bdir, exist_ok=True)
     procs = []
     for src in sources():
         obj = os.path.join(bdir, os.path.basename(src)[:-3] + ".o")
-        cmd = [NVCC, *FLAGS, "-c", src, "-o", obj]
+        cmd = [NVCC, *FLAGS, *(["-DGPS_CHECKED"] if checked else []), "-c", src, "-o", obj]
         if verbose:
             print(" ".join(cmd))
         procs.append(subprocess.Popen(cmd))
@@ -63,4 +70,4 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None) ->
 if __name__ == "__main__":
     # --out PATH: build the current tree into PATH (A/B experiments, tools/ab.sh) instead of libgps.so
     o = sys.argv[sys.argv.index("--out") + 1] if "--out" in sys.argv else None
-    print(build(force="--force" in sys.argv, verbose=True, out=o))
+    print(build(force="--force" in sys.argv, verbose=True, out=o, checked="--checked" in sys.argv))

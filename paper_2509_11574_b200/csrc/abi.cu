@@ -34,4 +34,19 @@ const char* gps_status_string(gps_status s) {
 }
 const char* gps_last_error(void) { return gps::g_last_error.c_str(); }
 int gps_abi_version(void) { return GPS_ABI_VERSION; }
+
+gps_status gps_debug_check_word_sync(int64_t* word, int32_t* checked) {
+  if (!word) return gps::invalid("gps_debug_check_word_sync: null argument");
+  GPS_CHECK_CUDA(cudaDeviceSynchronize());
+  const unsigned long long w = gps::check_word_take_volume() | gps::check_word_take_render() |
+                               gps::check_word_take_adding() | gps::check_word_take_tracking();
+  GPS_CHECK_CUDA(cudaGetLastError());
+  *word = (int64_t)w;
+#ifdef GPS_CHECKED
+  if (checked) *checked = 1;
+#else
+  if (checked) *checked = 0;
+#endif
+  return GPS_OK;
+}
 }

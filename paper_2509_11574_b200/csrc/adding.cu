@@ -20,9 +20,17 @@
 #include <cmath>
 #include <string>
 
+#define GPS_CHK_VAR g_chk_adding
 #include "common.cuh"
 
 namespace gps {
+__device__ unsigned long long g_chk_adding = 0ull;
+unsigned long long check_word_take_adding() {
+  unsigned long long w = 0ull, z = 0ull;
+  cudaMemcpyFromSymbol(&w, g_chk_adding, sizeof(w));
+  cudaMemcpyToSymbol(g_chk_adding, &z, sizeof(z));
+  return w;
+}
 namespace {
 
 constexpr int kBlk = 1024;                // items per CTA of the flag / compaction passes
@@ -198,9 +206,11 @@ __global__ void __launch_bounds__(kBlk) k_add_compact(AddArgs a, const uint8_t* 
   uint32_t tm, ts;
   const uint32_t rm = cta_rank(f & 1, sw, tm);
   const uint32_t rs = cta_rank((f >> 1) & 1, sw, ts);
+  GPS_DCHECK(!(f & 1) || boff[blockIdx.x] + rm < n, CHK_ADD);
   if (f & 1) mpix[boff[blockIdx.x] + rm] = p;
   if (f & 2) {
     const uint32_t at = boff[a.nblk + blockIdx.x] + rs;
+    GPS_DCHECK(at <= boff[blockIdx.x] + rm && at < n, CHK_ADD);
     spix[at] = p;
     smi[at] = boff[blockIdx.x] + rm;
   }
@@ -361,6 +371,7 @@ __global__ void __launch_bounds__(kBlk) k_remove_scatter(gps_gaussians g, gps_ga
   const uint32_t r = cta_rank(k, sw, tot);
   if (!k) return;
   const int64_t j = boff[blockIdx.x] + r;
+  GPS_DCHECK(j <= i, CHK_ADD);  // a stable compaction never moves a row forward
   copy_row(g, sp, i, j, nsh);
   copy_row(gm, sm, i, j, nsh);
   copy_row(gv, sv, i, j, nsh);

@@ -27,6 +27,46 @@ gps_status cuda_fail(const char* where, cudaError_t e);
 gps_status invalid(const std::string& msg);
 
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// ---- checked build (the bounds/race evidence compute-sanitizer cannot give on this pool) -----
+// Built with -DGPS_CHECKED (build.py --checked -> libgps_checked.so), every GPS_DCHECK(cond, bit)
+// in a hot kernel evaluates its bound and, when it fails, sets `bit` in the translation unit's
+// device check word (GPS_CHK_VAR, one per .cu: no relocatable device code needed) without
+// stopping the kernel; gps_debug_check_word_sync ORs and clears the words.  In the production
+// build the macro is empty.  Bits: include/gps.h (gps_debug_check_word_sync).
+#ifdef GPS_CHECKED
+#define GPS_DCHECK(cond, bit)                                                      \
+  do {                                                                             \
+    if (!(cond)) atomicOr(&GPS_CHK_VAR, 1ull << (bit));                            \
+  } while (0)
+#else
+#define GPS_DCHECK(cond, bit) \
+  do {                        \
+  } while (0)
+#endif
+enum CheckBit {
+  CHK_POOL = 0,       // a pool block index outside [0, n_blocks)
+  CHK_PLANE = 1,      // a tsdf/rgbw plane offset outside its block
+  CHK_PIXEL = 2,      // a pixel index outside the image
+  CHK_SLOT = 3,       // a hash slot or dense-grid cell outside its table
+  CHK_VISLIST = 4,    // a visible-list index at or beyond max_blocks
+  CHK_RANGE_TILE = 5, // a range-image tile outside the image's tiles
+  CHK_NBR = 6,        // a neighbour-table entry outside [-1, n_blocks)
+  CHK_SUBNEG = 7,     // a sub-block count leaving [0, 125] (byte borrow)
+  CHK_PAIR = 16,      // a (tile, Gaussian) pair index at or beyond the capacity
+  CHK_TILE = 17,      // a tile index outside the image's tiles
+  CHK_GAUSS = 18,     // a Gaussian index at or beyond n
+  CHK_LIST = 19,      // a tile list range that is not ordered / inside the pair array
+  CHK_SMEM = 20,      // a shared-memory staging index beyond its array
+  CHK_ADAM = 21,      // a fused-Adam element outside its chunk slice
+  CHK_SPLIT = 22,     // a long-list partial slot or chunk outside its table
+  CHK_ADD = 24,       // adding / removal: an index outside its array
+  CHK_TRACK = 28      // tracking: a pixel or partial-sum index outside its array
+};
+unsigned long long check_word_take_volume();
+unsigned long long check_word_take_render();
+unsigned long long check_word_take_adding();
+unsigned long long check_word_take_tracking();
 inline cudaStream_t as_stream(gps_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
 
 // ---- prescribed fp32 arithmetic: never contracted into FMA ------------------

@@ -28,10 +28,18 @@
 #include <string>
 #include <vector>
 
+#define GPS_CHK_VAR g_chk_render
 #include "common.cuh"
 #include "prof.cuh"
 
 namespace gps {
+__device__ unsigned long long g_chk_render = 0ull;
+unsigned long long check_word_take_render() {
+  unsigned long long w = 0ull, z = 0ull;
+  cudaMemcpyFromSymbol(&w, g_chk_render, sizeof(w));
+  cudaMemcpyToSymbol(g_chk_render, &z, sizeof(z));
+  return w;
+}
 
 constexpr int kMaxList = 2048;  // entries a tile sorts in shared memory (16 KB of keys)
 constexpr uint32_t kWsMagic = 0x47505357u;  // "GPSW"
@@ -577,6 +585,8 @@ __global__ void __launch_bounds__(256) k_emit(RenderArgs a, const float4* __rest
     for (int ty = ty0; ty <= ty1; ++ty)
       for (int tx = tx0; tx <= tx1; ++tx) {
         const uint32_t pos = offsets[ty * a.tiles_x + tx] + rk[k++];
+        GPS_DCHECK(ty * a.tiles_x + tx < a.tiles_x * a.tiles_y, CHK_TILE);
+        GPS_DCHECK(pos < offsets[ty * a.tiles_x + tx + 1], CHK_LIST);  // inside its tile's range
         if (pos < a.cap) vals[pos] = (uint32_t)i;
       }
   }
@@ -595,6 +605,8 @@ __global__ void __launch_bounds__(256) k_emit(RenderArgs a, const float4* __rest
     for (int k = lane; k < cnt; k += 32) {
       const int t = (sy0 + k / wx) * a.tiles_x + sx0 + k % wx;
       const uint32_t pos = offsets[t] + counts[t] + atomicAdd(&cursor[t], 1u);
+      GPS_DCHECK(t >= 0 && t < a.tiles_x * a.tiles_y, CHK_TILE);
+      GPS_DCHECK(pos < offsets[t + 1], CHK_LIST);
       if (pos < a.cap) vals[pos] = gi;
     }
   }
@@ -659,8 +671,10 @@ __global__ void __launch_bounds__(512) k_sort_long(const float4* __restrict__ re
     const uint32_t start = min(offsets[t], cap), end = min(offsets[t + 1], cap);
     const int n = (int)(end - start);
     uint64_t* keys = n <= kLongSmem ? sk : gkeys + start;
+    GPS_DCHECK(start <= end, CHK_LIST);
     for (int e = threadIdx.x; e < n; e += blockDim.x) {
       const uint32_t idx = vals[start + e];
+      GPS_DCHECK((int64_t)idx < hdr->n, CHK_GAUSS);
       keys[e] = ((uint64_t)__float_as_uint(rec[4 * idx + 1].z) << 32) | idx;
     }
     __syncthreads();
@@ -978,6 +992,7 @@ __global__ void __launch_bounds__(128, 8) k_sort_blend16x2(RenderArgs a, const f
       const int e = threadIdx.x + h * NT;
       if (e < n) {
         const uint32_t idx = vals[start + e];
+        GPS_DCHECK((int64_t)idx < a.n, CHK_GAUSS);
         dk[h] = __float_as_uint(rec[4 * idx + 1].z);
         key[h] = ((uint64_t)dk[h] << 32) | idx;
         sdep[e] = dk[h];
@@ -999,8 +1014,10 @@ __global__ void __launch_bounds__(128, 8) k_sort_blend16x2(RenderArgs a, const f
       if (threadIdx.x + h * NT < n) skeys[threadIdx.x + h * NT] = ~0ull;  // "unwritten"
     __syncthreads();
 #pragma unroll
-    for (int h = 0; h < 2; ++h)
+    for (int h = 0; h < 2; ++h) {
+      GPS_DCHECK(threadIdx.x + h * NT >= n || rank[h] < n, CHK_SMEM);
       if (threadIdx.x + h * NT < n) skeys[rank[h]] = key[h];
+    }
     __syncthreads();
     bool hole = false;
 #pragma unroll
@@ -1092,6 +1109,7 @@ __global__ void __launch_bounds__(128, 8) k_sort_blend16x2(RenderArgs a, const f
       const int e = threadIdx.x + h * NT;
       if (e < cnt) {
         const uint32_t idx = vals[start + base + e];
+        GPS_DCHECK((int64_t)idx < a.n && start + base + e < end, CHK_GAUSS);
         const float4 r0 = rec[4 * idx], r1 = rec[4 * idx + 1];
         s0[e] = make_float4(r0.x, r0.y, r0.z, pmul(2.0f, r0.w));
         s1[e] = make_float4(r1.x, r1.y, r1.z, pair_qmax(a.ln_inv_amin, r1.y));
@@ -1158,6 +1176,7 @@ __global__ void __launch_bounds__(128, 8) k_sort_blend16x2(RenderArgs a, const f
   if (split) {
     // this chunk's partial sums into its slot; the tile's last chunk combines them in order
     const uint32_t slot = spl.pbase[t] + chunk;
+    GPS_DCHECK(chunk < (uint32_t)nch && slot < hdr->n_part, CHK_SPLIT);
     const int p0i = ly0 * 16 + lx, p1i = (ly0 + 2) * 16 + lx;
     spl.part[256 * (size_t)slot + p0i] = make_float4(W0, A0, B0, G0);
     spl.part[256 * (size_t)slot + p1i] = make_float4(W1, A1, B1, G1);
@@ -1366,8 +1385,10 @@ __global__ void __launch_bounds__(256) k_backward(RenderArgs a, const float4* __
     const uint32_t base = start + 256u * chunk;
     const int cnt_e = base < end ? (int)min(256u, end - base) : 0;
     __syncthreads();  // pixel state visible; the previous batch's readers are done
+    GPS_DCHECK(cnt_e <= 256 && t < a.tiles_x * a.tiles_y, CHK_SMEM);
     for (int j = threadIdx.x; j < cnt_e; j += blockDim.x) {
       const uint32_t id = vals[base + j];
+      GPS_DCHECK((int64_t)id < a.n, CHK_GAUSS);
       sidx[j] = id;
       const float4 q0 = rec[4 * id], q1 = rec[4 * id + 1], q2 = rec[4 * id + 2], q3 = rec[4 * id + 3];
       se0[j] = q0;
@@ -1395,6 +1416,7 @@ __global__ void __launch_bounds__(256) k_backward(RenderArgs a, const float4* __
       const int row = (int)(((uint32_t)k * magic) >> 16);
       const int x = x0 + (k - row * wx), y = y0 + row;
       const int p = (y - ty0) * TILE + (x - tx0);
+      GPS_DCHECK(p >= 0 && p < NP, CHK_SMEM);
       if (!(r1.z < slim[p])) continue;  // Eq. 1 indicator (and inactive pixels)
       const float q = pair_q(r0.x, r0.y, r0.z, b2, r1.x, (float)x, (float)y);
       if (!(q <= qmax)) continue;
@@ -2072,6 +2094,7 @@ __global__ void __launch_bounds__(kCaG, 4) k_chain_adam(RenderArgs a, gps_gaussi
         // e / dim for e < 48 * kCaG: (e + 1/2) / dim is >= 1/(2 dim) from an integer, far beyond
         // the fp32 error of the product
         const uint32_t gl = __float2uint_rz(((float)e + 0.5f) * idim[q]), comp = e - gl * dim;
+        GPS_DCHECK((uint32_t)k >= cnt[j] || (gl < (uint32_t)cg && comp < dim && e < len[q]), CHK_ADAM);
         const float* o = sg + gl * kCaStride;
         float gr, st = steps[q];
         if (q == 4) {

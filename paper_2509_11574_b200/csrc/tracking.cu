@@ -22,9 +22,17 @@
 #include <cmath>
 #include <string>
 
+#define GPS_CHK_VAR g_chk_tracking
 #include "common.cuh"
 
 namespace gps {
+__device__ unsigned long long g_chk_tracking = 0ull;
+unsigned long long check_word_take_tracking() {
+  unsigned long long w = 0ull, z = 0ull;
+  cudaMemcpyFromSymbol(&w, g_chk_tracking, sizeof(w));
+  cudaMemcpyToSymbol(g_chk_tracking, &z, sizeof(z));
+  return w;
+}
 namespace {
 
 constexpr int kIcpMaxLevels = 4;

@@ -13,10 +13,18 @@
 #include <cstring>
 #include <vector>
 
+#define GPS_CHK_VAR g_chk_volume
 #include "common.cuh"
 #include "prof.cuh"
 
 namespace gps {
+__device__ unsigned long long g_chk_volume = 0ull;
+unsigned long long check_word_take_volume() {
+  unsigned long long w = 0ull, z = 0ull;
+  cudaMemcpyFromSymbol(&w, g_chk_volume, sizeof(w));
+  cudaMemcpyToSymbol(g_chk_volume, &z, sizeof(z));
+  return w;
+}
 
 // ============================================================================================
 // allocation: one CTA per 32x32 pixel patch, 256 threads x 4 pixels (one 8-byte depth load
@@ -85,6 +93,7 @@ __device__ __forceinline__ void mark_visible(const VolumeView& v, uint32_t slot,
   if (v.stamp[slot] == frame) return;
   if (atomicExch(&v.stamp[slot], frame) == frame) return;
   const uint32_t idx = atomicAdd(&v.ctr->n_vis, 1u);
+  GPS_DCHECK(slot <= v.slot_mask, CHK_SLOT);
   if (idx < v.max_blocks) {
     v.vis[idx] = (int32_t)slot;
   } else {
@@ -273,6 +282,7 @@ __global__ void __launch_bounds__(256) k_alloc(VolumeView v, FuseParams p_in,
       base = __shfl_sync(0xFFFFFFFFu, base, 0);
       if (app) {
         const uint32_t idx = base + __popc(bal & ((1u << lane) - 1u));
+        GPS_DCHECK((uint32_t)slot <= v.slot_mask, CHK_SLOT);
         if (idx < v.max_blocks) {
           v.vis[idx] = slot;
         } else {
@@ -394,6 +404,7 @@ __global__ void __launch_bounds__(256) k_integrate(VolumeView v, FuseParams p_in
     }
     slot2 = q + 2 * G < nvis ? v.vis[q + 2 * G] : -1;
     if (b < 0) continue;  // uniform across the CTA
+    GPS_DCHECK((uint32_t)b < min(v.ctr->n_blocks, v.max_blocks), CHK_POOL);
     int bx, by, bz;
     unpack_block(key, bx, by, bz);
     float2* tp = reinterpret_cast<float2*>(v.tsdf + (size_t)b * kTsdfBlock + tsdf_index(li, lj, lk));
@@ -406,6 +417,8 @@ __global__ void __launch_bounds__(256) k_integrate(VolumeView v, FuseParams p_in
     const bool in0 = voxel_project(p, gx, gy, gz, pix0, z0);
     const bool in1 = voxel_project(p, gx + 1, gy, gz, pix1, z1);
     // both voxels' depth and colour gathers in flight together (colour speculatively)
+    GPS_DCHECK(!in0 || pix0 < (uint32_t)(p.W * p.H), CHK_PIXEL);
+    GPS_DCHECK(!in1 || pix1 < (uint32_t)(p.W * p.H), CHK_PIXEL);
     const uint16_t r0 = in0 ? __ldg(&depth[pix0]) : (uint16_t)0, r1 = in1 ? __ldg(&depth[pix1]) : (uint16_t)0;
     const uint32_t c0 = in0 ? __ldg(&rgba[pix0]) : 0u, c1 = in1 ? __ldg(&rgba[pix1]) : 0u;
     if (b1 >= 0) {  // next block's -neighbour row (its pool index arrived last iteration... or now)
@@ -440,9 +453,17 @@ __global__ void __launch_bounds__(256) k_integrate(VolumeView v, FuseParams p_in
 #pragma unroll
         for (int k = 1; k < 8; ++k) {
           if (mm[k] < 0) continue;
-          float* dst = v.tsdf + (size_t)mm[k] * kTsdfBlock + tsdf_index(li + 8 * (k & 1), lj + 8 * ((k >> 1) & 1), lk + 8 * (k >> 2));
-          if (u0 && (k & ~(zyz | (li == 0 ? 1 : 0))) == 0) dst[0] = ts.x;
-          if (u1 && (k & ~zyz) == 0) dst[1] = ts.y;   // voxel li+1 >= 1: never on the x face
+          GPS_DCHECK((uint32_t)mm[k] < min(v.ctr->n_blocks, v.max_blocks), CHK_NBR);
+          const int di = tsdf_index(li + 8 * (k & 1), lj + 8 * ((k >> 1) & 1), lk + 8 * (k >> 2));
+          float* dst = v.tsdf + (size_t)mm[k] * kTsdfBlock + di;
+          if (u0 && (k & ~(zyz | (li == 0 ? 1 : 0))) == 0) {
+            GPS_DCHECK(di >= 0 && di < kTsdfBlock, CHK_PLANE);
+            dst[0] = ts.x;
+          }
+          if (u1 && (k & ~zyz) == 0) {  // voxel li+1 >= 1: never on the x face
+            GPS_DCHECK(di >= 0 && di + 1 < kTsdfFace, CHK_PLANE);
+            dst[1] = ts.y;
+          }
         }
       }
     }
@@ -461,7 +482,20 @@ __global__ void __launch_bounds__(256) k_integrate(VolumeView v, FuseParams p_in
         uint64_t wd = 0;
         if ((k & ~zyz) == 0) wd += (uint64_t)(int64_t)dneg0 * cell_subs(li + ox, lj + oy, lk + oz);
         if ((k & ~(zyz & 6)) == 0) wd += (uint64_t)(int64_t)dneg1 * cell_subs(li + 1 + ox, lj + oy, lk + oz);
-        if (wd && mm[k] >= 0) atomicAdd(reinterpret_cast<unsigned long long*>(&v.subneg[mm[k]]), (unsigned long long)wd);
+        if (wd && mm[k] >= 0) {
+          GPS_DCHECK((uint32_t)mm[k] < min(v.ctr->n_blocks, v.max_blocks), CHK_NBR);
+#ifdef GPS_CHECKED
+          // no byte of the packed counts may leave [0, 125] (a borrow would corrupt its neighbour)
+          const unsigned long long nw =
+              atomicAdd(reinterpret_cast<unsigned long long*>(&v.subneg[mm[k]]), (unsigned long long)wd) + wd;
+          bool okb = true;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) okb &= ((nw >> (8 * q)) & 0xFFull) <= 125ull;
+          GPS_DCHECK(okb, CHK_SUBNEG);
+#else
+          atomicAdd(reinterpret_cast<unsigned long long*>(&v.subneg[mm[k]]), (unsigned long long)wd);
+#endif
+        }
       }
     }
   }
@@ -512,6 +546,7 @@ __global__ void __launch_bounds__(256) k_link(VolumeView v) {
       const int dx = k & 1, dy = (k >> 1) & 1, dz = (k >> 2) & 1;
       if (k) {
         mine = find_block_fast(v, x + sg * dx, y + sg * dy, z + sg * dz);
+        GPS_DCHECK(mine < (int32_t)hi, CHK_NBR);
         // the existing neighbour's opposite table gets b
         if (mine >= 0) (lane < 8 ? v.nbrm : v.nbr)[8 * (size_t)mine + k] = (int32_t)b;
       }
@@ -602,6 +637,7 @@ __global__ void __launch_bounds__(256) k_range(VolumeView v, RayParams p_in, uin
       for (int ty = ty0; ty <= ty1; ++ty)
         for (int tx = tx0; tx <= tx1; ++tx) {
           const int t = ty * tiles_x + tx;
+          GPS_DCHECK(t >= 0 && t < tiles_x * tiles_y, CHK_RANGE_TILE);
           if (tmin[t] > a0) atomicMin(&tmin[t], a0);
           if (tmax[t] < a1) atomicMax(&tmax[t], a1);
         }
@@ -617,6 +653,7 @@ __global__ void __launch_bounds__(256) k_range(VolumeView v, RayParams p_in, uin
       const int wx = sx1 - sx0 + 1, cnt = wx * (sy1 - sy0 + 1);
       for (int k = lane; k < cnt; k += 32) {
         const int t = (sy0 + k / wx) * tiles_x + sx0 + k % wx;
+        GPS_DCHECK(t >= 0 && t < tiles_x * tiles_y, CHK_RANGE_TILE);
         if (tmin[t] > s0) atomicMin(&tmin[t], s0);
         if (tmax[t] < s1) atomicMax(&tmax[t], s1);
       }
@@ -772,6 +809,7 @@ __device__ __forceinline__ bool trilinear_color(const VolumeView& v, BlockCache&
     const int dx = corner & 1, dy = (corner >> 1) & 1, dz = (corner >> 2) & 1;
     const int k = (dx && lx == 7) | ((dy && ly == 7) << 1) | ((dz && lz == 7) << 2);
     // every corner's block is allocated here (its tsdf apron entry is not NaN)
+    GPS_DCHECK(nbr_entry(b0, n0, n1, k) >= 0 && nbr_entry(b0, n0, n1, k) < (int32_t)min(v.ctr->n_blocks, v.max_blocks), CHK_NBR);
     cw[corner] = v.rgbw[(size_t)nbr_entry(b0, n0, n1, k) * 512 + ((lx + dx) & 7) + 8 * ((ly + dy) & 7) + 64 * ((lz + dz) & 7)];
   }
 #pragma unroll
@@ -855,6 +893,7 @@ __global__ void __launch_bounds__(128, 2 * kMinCtas) k_raycast(VolumeView v, Ray
       b0 = __ldg(&v.grid[(iz * (unsigned)v.gdy + iy) * (unsigned)v.gdx + ix]);
     else
       b0 = cached_find(v, c0, bx, by, bz);
+    GPS_DCHECK(b0 < (int32_t)min(v.ctr->n_blocks, v.max_blocks), CHK_POOL);
     if (b0 >= 0 && b0 != pb) {
       pb = b0;
       pw = __ldg(reinterpret_cast<const unsigned long long*>(&v.subneg[b0]));
@@ -961,6 +1000,11 @@ __global__ void __launch_bounds__(128, 2 * kMinCtas) k_raycast(VolumeView v, Ray
   }
 }
 
+// a deliberately failing check (the checked build's self-test: its bit must reach the word)
+__global__ void k_check_selftest(int bit) {
+  GPS_DCHECK(threadIdx.x != 7, bit);
+}
+
 __global__ void k_apron_check(VolumeView v, unsigned long long* bad) {
   const uint32_t nb = min(v.ctr->n_blocks, v.max_blocks);
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < (size_t)nb * 217; i += (size_t)gridDim.x * blockDim.x) {
@@ -974,6 +1018,43 @@ __global__ void k_apron_check(VolumeView v, unsigned long long* bad) {
     const float got = v.tsdf[(size_t)b * kTsdfBlock + tsdf_index(x, y, z)];
     if (!((isnan(want) && isnan(got)) || __float_as_uint(want) == __float_as_uint(got))) atomicAdd(bad, 1ull);
   }
+}
+
+// hash / pool / neighbour-table invariants (the checked build's race evidence for the lock-free
+// insert and k_link): every occupied slot maps to a pool block whose key is the slot's key; every
+// pool block is found at its own key; each block's 8 + and 8 - neighbour entries equal a fresh
+// lookup of those neighbours; dense-grid cells of allocated blocks hold their pool index; the
+// number of occupied slots equals the number of pool blocks (no duplicate key was inserted).
+__global__ void k_hash_check(VolumeView v, unsigned long long* bad, unsigned long long* occupied) {
+  const uint32_t nb = min(v.ctr->n_blocks, v.max_blocks);
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  const size_t i0 = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  unsigned long long nbad = 0, nocc = 0;
+  for (size_t h = i0; h <= v.slot_mask; h += stride) {
+    const uint64_t k = v.keys[h];
+    if (k == kEmptyKey) continue;
+    ++nocc;
+    const int32_t b = v.vals[h];
+    if (b < 0 || (uint32_t)b >= nb || v.bkeys[b] != k) ++nbad;
+  }
+  for (size_t b = i0; b < nb; b += stride) {
+    int x, y, z;
+    unpack_block(v.bkeys[b], x, y, z);
+    if (find_block(v, x, y, z) != (int32_t)b) ++nbad;
+    for (int q = 0; q < 8; ++q) {
+      const int dx = q & 1, dy = (q >> 1) & 1, dz = (q >> 2) & 1;
+      if (v.nbr[8 * b + q] != find_block(v, x + dx, y + dy, z + dz)) ++nbad;
+      if (v.nbrm[8 * b + q] != find_block(v, x - dx, y - dy, z - dz)) ++nbad;
+    }
+    if (v.grid) {
+      const unsigned ix = (unsigned)(x - v.gox), iy = (unsigned)(y - v.goy), iz = (unsigned)(z - v.goz);
+      if (ix < (unsigned)v.gdx && iy < (unsigned)v.gdy && iz < (unsigned)v.gdz &&
+          v.grid[((size_t)iz * v.gdy + iy) * v.gdx + ix] != (int32_t)b)
+        ++nbad;
+    }
+  }
+  if (nbad) atomicAdd(bad, nbad);
+  if (nocc) atomicAdd(occupied, nocc);
 }
 
 // subneg invariant: recount the <= 0 cells of each allocated block's plane (own + apron) per
@@ -1313,7 +1394,8 @@ static gps_status raycast_impl(const gps_volume* vol, const gps_intrinsics* K, c
   const int ntiles = (int)(g.x * g.y);
   uint32_t* tmin = nullptr;
   uint32_t* tmax = nullptr;
-  if (ntiles <= kMaxRangeTiles) {
+  static const bool no_range = getenv("GPS_NO_RANGE") != nullptr;  // A/B: march from dmin
+  if (ntiles <= kMaxRangeTiles && !no_range) {
     tmin = v->range;
     tmax = v->range + kMaxRangeTiles;
     GPS_CHECK_CUDA(cudaMemsetAsync(tmin, 0xFF, sizeof(uint32_t) * ntiles, s));
@@ -1380,6 +1462,33 @@ gps_status gps_debug_apron_check_sync(const gps_volume* vol, gps_stream_t stream
   GPS_CHECK_CUDA(cudaFreeAsync(cnt, s));
   GPS_CHECK_CUDA(cudaStreamSynchronize(s));
   *n_bad = (int64_t)h;
+  return GPS_OK;
+}
+
+gps_status gps_debug_check_selftest(int32_t bit, gps_stream_t stream) {
+  if (bit < 0 || bit > 63) return invalid("gps_debug_check_selftest: bit must be in [0, 63]");
+  k_check_selftest<<<1, 32, 0, as_stream(stream)>>>(bit);
+  GPS_CHECK_LAUNCH("k_check_selftest");
+  return GPS_OK;
+}
+
+gps_status gps_debug_hash_check_sync(const gps_volume* vol, gps_stream_t stream, int64_t* n_bad) {
+  if (!vol || !n_bad) return invalid("gps_debug_hash_check_sync: bad argument");
+  const VolumeImpl* v = static_cast<const VolumeImpl*>(vol);
+  cudaStream_t s = as_stream(stream);
+  unsigned long long* cnt = nullptr;
+  GPS_CHECK_CUDA(cudaMallocAsync(&cnt, 16, s));
+  GPS_CHECK_CUDA(cudaMemsetAsync(cnt, 0, 16, s));
+  k_hash_check<<<592, 256, 0, s>>>(v->view, cnt, cnt + 1);
+  GPS_CHECK_LAUNCH("k_hash_check");
+  unsigned long long h[2] = {0, 0};
+  VolumeCounters c{};
+  GPS_CHECK_CUDA(cudaMemcpyAsync(h, cnt, 16, cudaMemcpyDeviceToHost, s));
+  GPS_CHECK_CUDA(cudaMemcpyAsync(&c, v->view.ctr, sizeof(c), cudaMemcpyDeviceToHost, s));
+  GPS_CHECK_CUDA(cudaFreeAsync(cnt, s));
+  GPS_CHECK_CUDA(cudaStreamSynchronize(s));
+  const unsigned long long nb = std::min<unsigned long long>(c.n_blocks, v->view.max_blocks);
+  *n_bad = (int64_t)(h[0] + (h[1] > nb ? h[1] - nb : nb - h[1]));
   return GPS_OK;
 }
 

@@ -50,7 +50,7 @@ def main():
     if bench and os.path.exists(bench):
         d = json.load(open(bench))
         lines += [f"Bench line (`{os.path.basename(bench)}`): value **{d['value']} {d['unit']}**, "
-                  f"{d['ms_per_step']} ms/step (10 frames), e2e {d['e2e']['value']} frames/s, "
+                  f"{d['ms_per_step']} ms/step (10 frames), e2e {(d.get('e2e') or {}).get('value')} frames/s, "
                   f"gpu_launches {d['gpu_launches']}, clocks {d['clocks']}", "",
                   f"Roofline: `{json.dumps(d['roofline'])}`", "",
                   "Live CUDA-event shares of the timed region (bench):", "",
