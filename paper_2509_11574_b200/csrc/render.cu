@@ -945,7 +945,7 @@ struct SplitIO {
   float4* part;           // partial slots, 256 pixels each: (W, C0, C1, C2)
 };
 
-template <bool SORTED, bool COUNT = false>
+template <bool SORTED, bool COUNT = false, bool WW = true>
 __global__ void __launch_bounds__(128, 8) k_sort_blend16x2(RenderArgs a, const float4* __restrict__ rec,
                                                         const uint32_t* __restrict__ offsets, uint32_t* vals,
                                                         uint64_t* gkeys, uint32_t* tile_end, float* loss_part,
@@ -953,7 +953,8 @@ __global__ void __launch_bounds__(128, 8) k_sort_blend16x2(RenderArgs a, const f
   constexpr int NT = 128, NB = 256;  // threads, staged entries per batch (2 per thread)
   __shared__ __align__(16) uint64_t skeys[NB + 2];
   __shared__ __align__(16) uint32_t sdep[NB + 4];
-  __shared__ float4 s0[NB], s1[NB], s2[NB];  // s0 = (px, py, a, 2b); s1 = (c, ln sigma, d, q_max)
+  __shared__ float4 s0[WW ? 1 : NB], s1[WW ? 1 : NB], s2[WW ? 1 : NB];  // s0 = (px, py, a, 2b); s1 = (c, ln sigma, d, q_max)
+  __shared__ float4 ws0[WW ? 4 : 1][32], ws1[WW ? 4 : 1][32], ws2[WW ? 4 : 1][32];  // per-warp chunk (WW)
   __shared__ float red[NT / 32 + 1];
   __shared__ uint32_t redi[NT / 32 + 1];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -1101,7 +1102,77 @@ __global__ void __launch_bounds__(128, 8) k_sort_blend16x2(RenderArgs a, const f
   float W0 = 0.f, A0 = 0.f, B0 = 0.f, G0 = 0.f, W1 = 0.f, A1 = 0.f, B1 = 0.f, G1 = 0.f;
   uint32_t n_eval = 0, n_acc = 0;  // COUNT: pixel-entry pairs whose q was evaluated / accepted
   bool wdone = !(wlim > -INFINITY);  // warp-uniform
-  for (int base = b_lo; base < b_hi; base += NB) {
+  if (WW) {
+    // Warp walk: each warp stages its own 32-entry chunks (a lane per entry, from the sorted
+    // keys in shared memory or the list) into a per-warp buffer and walks them without any CTA
+    // barrier -- the four warps of a tile no longer wait for each other at every 256-entry
+    // batch.  Per live entry the two pixels (rows y, y + 2) are evaluated together in packed
+    // f32x2 arithmetic (FFMA2/FMUL2/FADD2: per component the same rounding as the scalar
+    // sequence, so the image is bitwise unchanged) and accumulated branch-free (a rejected
+    // pixel adds alpha = 0, which leaves every sum bitwise unchanged).
+    float4* const e0s = ws0[WW ? w : 0];
+    float4* const e1s = ws1[WW ? w : 0];
+    float4* const e2s = ws2[WW ? w : 0];
+    float2 Wv = make_float2(0.f, 0.f), Av = Wv, Bv = Wv, Gv = Wv;
+    const float2 fyv = make_float2(fy0, fy1), limv = make_float2(lim[0], lim[1]);
+    for (int kb = b_lo; kb < b_hi && !wdone; kb += 32) {
+      const int k = kb + lane;
+      bool live = false, stop = false;
+      if (k < b_hi) {
+        const uint32_t idx = (SORTED && small) ? (uint32_t)skeys[k] : vals[start + k];
+        GPS_DCHECK((int64_t)idx < a.n && start + k < end, CHK_GAUSS);
+        const float4 r0 = rec[4 * idx], r1 = rec[4 * idx + 1], r2 = rec[4 * idx + 2];
+        const float4 e0 = make_float4(r0.x, r0.y, r0.z, pmul(2.0f, r0.w));
+        const float4 e1 = make_float4(r1.x, r1.y, r1.z, pair_qmax(a.ln_inv_amin, r1.y));
+        e0s[lane] = e0;
+        e1s[lane] = e1;
+        e2s[lane] = r2;
+        const bool behind = !(e1.z < wlim);
+        stop = SORTED && behind;
+        const uint32_t ry = __float_as_uint(r2.w);
+        live = !behind && (int)(ry >> 16) >= wy0 && (int)(ry & 0xFFFFu) <= wy1;
+        if (live) live = ellipse_meets_strip(e0.x, e0.y, e0.z, e0.w, e1.x, e1.w, tx * 16, tx * 16 + 15, wy0, wy1);
+      }
+      uint32_t lm = __ballot_sync(0xFFFFFFFFu, live);
+      const uint32_t sm = __ballot_sync(0xFFFFFFFFu, stop);
+      if (sm) {
+        lm &= (1u << (__ffs(sm) - 1)) - 1u;  // survivors before the first stop
+        wdone = true;
+      }
+      __syncwarp();
+      while (lm) {
+        const int kk = __ffs(lm) - 1;
+        lm &= lm - 1u;
+        const float4 r1 = e1s[kk];
+        const bool i0 = r1.z < limv.x, i1 = r1.z < limv.y;  // Eq. 1's indicator per pixel
+        if (!(i0 | i1)) continue;
+        const float4 r0 = e0s[kk];
+        // pair_q at (x, y) and (x, y + 2): dx and its products are shared
+        const float dx = fx - r0.x;
+        const float bdx = pmul(r0.w, dx), adx = pmul(r0.z, dx);
+        const float2 dy = __fadd2_rn(fyv, make_float2(-r0.y, -r0.y));
+        const float2 cdy2 = __fmul2_rn(__fmul2_rn(make_float2(r1.x, r1.x), dy), dy);
+        const float2 q = __ffma2_rn(make_float2(adx, adx), make_float2(dx, dx),
+                                    __ffma2_rn(make_float2(bdx, bdx), dy, cdy2));
+        const bool p0 = i0 && q.x <= r1.w, p1 = i1 && q.y <= r1.w;
+        if (COUNT) {
+          n_eval += (uint32_t)(i0 && inside[0]) + (uint32_t)(i1 && inside[1]);
+          n_acc += (uint32_t)(p0 && inside[0]) + (uint32_t)(p1 && inside[1]);
+        }
+        if (!(p0 | p1)) continue;
+        const float4 r2 = e2s[kk];
+        const float2 arg = __ffma2_rn(make_float2(-0.5f, -0.5f), q, make_float2(r1.y, r1.y));
+        const float2 al = make_float2(p0 ? __expf(arg.x) : 0.f, p1 ? __expf(arg.y) : 0.f);  // Eq. 3
+        Wv = __fadd2_rn(Wv, al);
+        Av = __ffma2_rn(al, make_float2(r2.x, r2.x), Av);
+        Bv = __ffma2_rn(al, make_float2(r2.y, r2.y), Bv);
+        Gv = __ffma2_rn(al, make_float2(r2.z, r2.z), Gv);
+      }
+      __syncwarp();
+    }
+    W0 = Wv.x; W1 = Wv.y; A0 = Av.x; A1 = Av.y; B0 = Bv.x; B1 = Bv.y; G0 = Gv.x; G1 = Gv.y;
+  }
+  for (int base = b_lo; !WW && base < b_hi; base += NB) {
     const int cnt = min(NB, b_hi - base);
     __syncthreads();
 #pragma unroll
@@ -2265,6 +2336,7 @@ gps_status forward_view(const gps_gaussians* g, const View1& v, const gps_render
   {
   GPS_PROF(K_SORT_BLEND, s);
   static const bool one_px = getenv("GPS_BLEND_1PX") != nullptr;  // the one-pixel-per-thread kernel
+  static const bool staged = getenv("GPS_BLEND_STAGED") != nullptr;  // the CTA-staged 16x2 loop (A/B)
   if (counters) {  // debug: the instrumented instantiation (16x16 tiles)
     if (c->sort_free)
       k_sort_blend16x2<false, true><<<n_tiles, 128, 0, s>>>(a, sp.rec, offsets, vals, gk, tend, lp, hdr, io, 0, spl);
@@ -2278,6 +2350,9 @@ gps_status forward_view(const gps_gaussians* g, const View1& v, const gps_render
       k_sort_blend<16, false><<<n_tiles, 256, 0, s>>>(a, sp.rec, offsets, vals, gk, tend, lp, hdr, io, 0);
     else
       k_sort_blend<8, false><<<n_tiles, 64, 0, s>>>(a, sp.rec, offsets, vals, gk, tend, lp, hdr, io, 0);
+  } else if (a.tile == 16 && !one_px && staged) {
+    k_sort_blend16x2<true, false, false><<<n_tiles, 128, 0, s>>>(a, sp.rec, offsets, vals, gk, tend, lp, hdr, io,
+                                                                 c->tile_depth_precull, spl);
   } else if (a.tile == 16 && !one_px) {
     k_sort_blend16x2<true><<<n_tiles, 128, 0, s>>>(a, sp.rec, offsets, vals, gk, tend, lp, hdr, io, c->tile_depth_precull,
                                                     spl);

@@ -324,9 +324,10 @@ def test_large_gaussians_span_many_tiles():
 
 
 def test_two_pixel_blend_is_bitwise_the_one_pixel_blend(tmp_path):
-    """k_sort_blend16x2 (default for 16x16 tiles) processes, per pixel, the same entries in the
-    same order as k_sort_blend<16> (GPS_BLEND_1PX=1, read once per process): C*, W_G and the loss
-    are bitwise equal.  cfg2-sized frame, 50k Gaussians, sorted and sort-free."""
+    """k_sort_blend16x2 (default for 16x16 tiles: per-warp walk, packed f32x2) processes, per
+    pixel, the same entries in the same order with the same roundings as k_sort_blend<16>
+    (GPS_BLEND_1PX=1) and as its CTA-staged scalar form (GPS_BLEND_STAGED=1; both read once per
+    process): C*, W_G and the loss are bitwise equal.  cfg2-sized frame, 50k Gaussians, sorted and sort-free."""
     import os
     import subprocess
     import sys
@@ -351,14 +352,15 @@ np.savez(sys.argv[2], **out)
 '''
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     res = {}
-    for name, env in (("two", {}), ("one", {"GPS_BLEND_1PX": "1"})):
+    for name, env in (("two", {}), ("one", {"GPS_BLEND_1PX": "1"}), ("staged", {"GPS_BLEND_STAGED": "1"})):
         path = str(tmp_path / f"{name}.npz")
-        e = dict(os.environ, **env)
-        e.pop("GPS_BLEND_1PX", None) if not env else None
+        e = {k: v for k, v in os.environ.items() if k not in ("GPS_BLEND_1PX", "GPS_BLEND_STAGED")}
+        e.update(env)
         subprocess.run([sys.executable, "-c", code, root, path], check=True, env=e, timeout=600)
         res[name] = np.load(path)
     for k in ("C0", "W0", "l0"):
         assert np.array_equal(res["two"][k], res["one"][k]), k
+        assert np.array_equal(res["two"][k], res["staged"][k]), k  # warp walk + f32x2 vs CTA-staged
     # sort-free: the bucket order comes from atomics, so only agreement to rounding is expected
     assert np.max(np.abs(res["two"]["C1"] - res["one"]["C1"])) <= 1e-5
 
