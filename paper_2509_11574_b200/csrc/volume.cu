@@ -510,6 +510,188 @@ __global__ void __launch_bounds__(256) k_integrate(VolumeView v, FuseParams p_in
   }
 }
 
+// --------------------------------------------------------------------------------------------
+// k_integrate_rows: the same integration (R-INT: voxel_project / voxel_sample /
+// voxel_update, so the volume is bitwise that of k_integrate and the oracle), one THREAD per
+// 8-voxel x-row.  A warp covers half a block (32 rows), so the block's metadata is warp-uniform
+// (one broadcast load per warp, pipelined two blocks ahead as in k_integrate); the row's tsdf
+// and colour are one 32-byte sector each (2 x 16-byte loads / stores); the frame gathers are
+// issued four voxels at a time; the apron pushes become row stores into the -y / -z / -yz
+// neighbours' apron rows (32-byte aligned) plus the x-face cells of voxel 0, written only for
+// rows with an update (an unchanged voxel rewrites the value its apron already holds: the
+// apron invariant makes that a no-op); sign changes (rare) take a per-voxel path.  Against one
+// thread per voxel pair this amortises the per-block and per-iteration work over 8 voxels.
+// --------------------------------------------------------------------------------------------
+template <bool DPOSE = false>
+__global__ void __launch_bounds__(256, 4) k_integrate_rows(VolumeView v, FuseParams p_in,
+                                                        const uint16_t* __restrict__ depth,
+                                                        const uint32_t* __restrict__ rgba) {
+  FuseParams p = p_in;
+  apply_dpose<DPOSE>(p);
+  if (DPOSE) affine_cam(p);
+  __shared__ uint32_t smagic[256];
+  __shared__ float srcp[256];
+  for (int d = threadIdx.x; d < 256; d += blockDim.x) {
+    smagic[d] = 0xFFFFFFFFu / (uint32_t)(d + 1) + 1u;
+    srcp[d] = __frcp_rn((float)(d + 1));
+  }
+  __syncthreads();
+  const uint32_t nvis = min(*(volatile uint32_t*)&v.ctr->n_vis, v.max_blocks);
+  if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&v.ctr->vis_total, (unsigned long long)nvis);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int row = (warp & 1) * 32 + lane;  // row (lj, lk) of this thread's block
+  const int lj = row & 7, lk = row >> 3;
+  const uint32_t sub = (uint32_t)(warp >> 1);  // block of the CTA's group of 4
+  __shared__ uint32_t scnt[8];
+  uint32_t n_upd = 0;
+  const uint32_t G = 4u * gridDim.x;  // blocks per grid step
+  uint32_t q = 4u * blockIdx.x + sub;
+  int32_t b1 = -1, slot2 = -1;
+  uint64_t key1 = 0;
+  int4 m0 = make_int4(-1, -1, -1, -1), m1 = m0;
+  if (q < nvis) {
+    const int32_t slot = v.vis[q];
+    b1 = v.vals[slot];
+    key1 = v.keys[slot];
+  }
+  if (q + G < nvis) slot2 = v.vis[q + G];
+  if (b1 >= 0) {
+    m0 = __ldg(reinterpret_cast<const int4*>(v.nbrm) + 2 * (size_t)b1);
+    m1 = __ldg(reinterpret_cast<const int4*>(v.nbrm) + 2 * (size_t)b1 + 1);
+  }
+  for (; q < nvis; q += G) {
+    const int32_t b = b1;
+    const uint64_t key = key1;
+    const int4 c0r = m0, c1r = m1;
+    b1 = -1;
+    if (slot2 >= 0) {
+      b1 = v.vals[slot2];
+      key1 = v.keys[slot2];
+    }
+    slot2 = q + 2 * G < nvis ? v.vis[q + 2 * G] : -1;
+    if (b < 0) continue;  // uniform across the warp
+    GPS_DCHECK((uint32_t)b < min(v.ctr->n_blocks, v.max_blocks), CHK_POOL);
+    int bx, by, bz;
+    unpack_block(key, bx, by, bz);
+    float* trow = v.tsdf + (size_t)b * kTsdfBlock + kTsdfSY * lj + kTsdfSZ * lk;
+    uint32_t* crow = v.rgbw + (size_t)b * 512 + 8 * lj + 64 * lk;
+    const float4 ta = reinterpret_cast<const float4*>(trow)[0], tb = reinterpret_cast<const float4*>(trow)[1];
+    const uint4 ca = reinterpret_cast<const uint4*>(crow)[0], cb = reinterpret_cast<const uint4*>(crow)[1];
+    float ts[8] = {ta.x, ta.y, ta.z, ta.w, tb.x, tb.y, tb.z, tb.w};
+    uint32_t cw[8] = {ca.x, ca.y, ca.z, ca.w, cb.x, cb.y, cb.z, cb.w};
+    if (b1 >= 0) {  // next block's -neighbour row
+      m0 = __ldg(reinterpret_cast<const int4*>(v.nbrm) + 2 * (size_t)b1);
+      m1 = __ldg(reinterpret_cast<const int4*>(v.nbrm) + 2 * (size_t)b1 + 1);
+    }
+    const int gx0 = bx * 8, gy = by * 8 + lj, gz = bz * 8 + lk;
+    uint32_t upd = 0, up = 0, dn = 0;  // updated voxels; indicator "tsdf <= 0" turned on / off
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      uint32_t pix[4];
+      float z[4];
+      bool in[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        pix[i] = 0;
+        z[i] = 0.f;
+        in[i] = voxel_project(p, gx0 + 4 * h + i, gy, gz, pix[i], z[i]);
+        GPS_DCHECK(!in[i] || pix[i] < (uint32_t)(p.W * p.H), CHK_PIXEL);
+      }
+      uint16_t raw[4];
+      uint32_t col[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        raw[i] = in[i] ? __ldg(&depth[pix[i]]) : (uint16_t)0;
+        col[i] = in[i] ? __ldg(&rgba[pix[i]]) : 0u;
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        float smp = 0.f;
+        if (in[i] && voxel_sample(p, raw[i], z[i], smp)) {
+          const int x = 4 * h + i;
+          const float old = ts[x];
+          const uint2 r = voxel_update(old, cw[x], smp, col[i], p.wmax, smagic, srcp);
+          ts[x] = __uint_as_float(r.x);
+          cw[x] = r.y;
+          upd |= 1u << x;
+          const bool nowneg = ts[x] <= 0.f, wasneg = old <= 0.f;  // NaN: false
+          up |= (uint32_t)(nowneg && !wasneg) << x;
+          dn |= (uint32_t)(!nowneg && wasneg) << x;
+        }
+      }
+    }
+    if (upd) {
+      reinterpret_cast<float4*>(trow)[0] = make_float4(ts[0], ts[1], ts[2], ts[3]);
+      reinterpret_cast<float4*>(trow)[1] = make_float4(ts[4], ts[5], ts[6], ts[7]);
+      reinterpret_cast<uint4*>(crow)[0] = make_uint4(cw[0], cw[1], cw[2], cw[3]);
+      reinterpret_cast<uint4*>(crow)[1] = make_uint4(cw[4], cw[5], cw[6], cw[7]);
+      n_upd += __popc(upd);
+      // apron pushes: the row is the y = 8 row of the -y neighbour (lj = 0), the z = 8 row of the
+      // -z neighbour (lk = 0), the (y, z) = (8, 8) row of the -yz neighbour (both); voxel 0 is
+      // the x = 8 face cell of the -x, -xy, -xz, -xyz neighbours (same conditions)
+      const int32_t mm[8] = {c0r.x, c0r.y, c0r.z, c0r.w, c1r.x, c1r.y, c1r.z, c1r.w};
+      const float4 va = make_float4(ts[0], ts[1], ts[2], ts[3]), vb = make_float4(ts[4], ts[5], ts[6], ts[7]);
+#pragma unroll
+      for (int k = 2; k < 8; k += 2) {  // k = dy<<1 | dz<<2 (no x bit): whole-row pushes
+        const bool feeds = (k & 2 ? lj == 0 : true) && (k & 4 ? lk == 0 : true);
+        if (!feeds || mm[k] < 0) continue;
+        GPS_DCHECK((uint32_t)mm[k] < min(v.ctr->n_blocks, v.max_blocks), CHK_NBR);
+        float* dst = v.tsdf + (size_t)mm[k] * kTsdfBlock + tsdf_index(0, lj + 8 * ((k >> 1) & 1), lk + 8 * (k >> 2));
+        reinterpret_cast<float4*>(dst)[0] = va;
+        reinterpret_cast<float4*>(dst)[1] = vb;
+      }
+      if (upd & 1u) {
+#pragma unroll
+        for (int k = 1; k < 8; k += 2) {  // x face cells of voxel 0
+          const bool feeds = (k & 2 ? lj == 0 : true) && (k & 4 ? lk == 0 : true);
+          if (!feeds || mm[k] < 0) continue;
+          GPS_DCHECK((uint32_t)mm[k] < min(v.ctr->n_blocks, v.max_blocks), CHK_NBR);
+          v.tsdf[(size_t)mm[k] * kTsdfBlock + tsdf_index(8, lj + 8 * ((k >> 1) & 1), lk + 8 * (k >> 2))] = ts[0];
+        }
+      }
+    }
+    // subneg (rare): each voxel whose indicator changed adjusts the counts of the sub-blocks that
+    // hold it, in the block itself and in every -neighbour whose apron it feeds
+    if (up | dn) {
+      const int32_t mm[8] = {c0r.x, c0r.y, c0r.z, c0r.w, c1r.x, c1r.y, c1r.z, c1r.w};
+      uint64_t wd[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      for (int x = 0; x < 8; ++x) {
+        const int d = (int)((up >> x) & 1u) - (int)((dn >> x) & 1u);
+        if (!d) continue;
+        const int zyz = (x == 0 ? 1 : 0) | (lj == 0 ? 2 : 0) | (lk == 0 ? 4 : 0);
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if ((k & ~zyz) == 0)
+            wd[k] += (uint64_t)(int64_t)d * cell_subs(x + 8 * (k & 1), lj + 8 * ((k >> 1) & 1), lk + 8 * (k >> 2));
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (!wd[k] || mm[k] < 0) continue;
+        GPS_DCHECK((uint32_t)mm[k] < min(v.ctr->n_blocks, v.max_blocks), CHK_NBR);
+#ifdef GPS_CHECKED
+        const unsigned long long nw =
+            atomicAdd(reinterpret_cast<unsigned long long*>(&v.subneg[mm[k]]), (unsigned long long)wd[k]) + wd[k];
+        bool okb = true;
+#pragma unroll
+        for (int qb = 0; qb < 8; ++qb) okb &= ((nw >> (8 * qb)) & 0xFFull) <= 125ull;
+        GPS_DCHECK(okb, CHK_SUBNEG);
+#else
+        atomicAdd(reinterpret_cast<unsigned long long*>(&v.subneg[mm[k]]), (unsigned long long)wd[k]);
+#endif
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) n_upd += __shfl_xor_sync(0xFFFFFFFFu, n_upd, o);
+  if (lane == 0) scnt[warp] = n_upd;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long sm = 0;
+    for (int k = 0; k < 8; ++k) sm += scnt[k];
+    if (sm) atomicAdd(&v.ctr->upd_total, sm);
+  }
+}
+
 __global__ void k_reset_frame(VolumeCounters* ctr) {
   ctr->n_vis = 0u;
   ctr->n_prev = ctr->n_blocks;
@@ -1348,10 +1530,16 @@ static gps_status fuse_impl(gps_volume* vol, const gps_intrinsics* K, const gps_
   // persistent-style grid: 148 SMs x 8 resident 256-thread CTAs, striding over the visible list
   {
     GPS_PROF(K_INTEGRATE, s);
-    if (dT)
-      k_integrate<true><<<148 * 8, 256, 0, s>>>(v->view, p, depth, reinterpret_cast<const uint32_t*>(rgba));
+    static const bool pairs = getenv("GPS_INTEGRATE_PAIRS") != nullptr;  // A/B: thread per voxel pair
+    const uint32_t* c4 = reinterpret_cast<const uint32_t*>(rgba);
+    if (pairs && dT)
+      k_integrate<true><<<148 * 8, 256, 0, s>>>(v->view, p, depth, c4);
+    else if (pairs)
+      k_integrate<<<148 * 8, 256, 0, s>>>(v->view, p, depth, c4);
+    else if (dT)
+      k_integrate_rows<true><<<148 * 8, 256, 0, s>>>(v->view, p, depth, c4);
     else
-      k_integrate<<<148 * 8, 256, 0, s>>>(v->view, p, depth, reinterpret_cast<const uint32_t*>(rgba));
+      k_integrate_rows<<<148 * 8, 256, 0, s>>>(v->view, p, depth, c4);
   }
   GPS_CHECK_LAUNCH("k_integrate");
   return GPS_OK;
