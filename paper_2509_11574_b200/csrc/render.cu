@@ -2045,86 +2045,96 @@ struct CaGroup {
   float* O;
 };
 
-__global__ void __launch_bounds__(kCaG, 4) k_chain_adam(RenderArgs a, gps_gaussians g, gps_gaussians gm,
-                                                      gps_gaussians gv, const float4* __restrict__ grad2d,
-                                                      const float4* __restrict__ cgj, gps_gaussians gout,
-                                                      int has_gout, AdamArgs ad) {
-  __shared__ float sg[kCaG * kCaStride];
-  const int64_t g0 = (int64_t)blockIdx.x * kCaG;
-  const int cg = (int)(a.n - g0 < (int64_t)kCaG ? a.n - g0 : (int64_t)kCaG);
-  // ---- phase A ----
-  {
-    const int t = threadIdx.x;
-    float* o = sg + t * kCaStride;
+// phase A for Gaussian t of the chunk starting at g0 (cg Gaussians): its raw gradient terms into
+// sgb[t * kCaStride ...] (zeros without a 2D gradient)
+__device__ __forceinline__ void ca_phase_a(const RenderArgs& a, const gps_gaussians& g,
+                                           const float4* __restrict__ grad2d, const float4* __restrict__ cgj,
+                                           int64_t g0, int cg, int t, float* sgb) {
+  float* o = sgb + t * kCaStride;
 #pragma unroll
-    for (int k = 0; k < 30; ++k) o[k] = 0.f;
-    if (t < cg) {
-      const int64_t i = g0 + t;
-      const float4 q0 = grad2d[3 * i], q1 = grad2d[3 * i + 1], q2 = grad2d[3 * i + 2];
-      float dcol[3] = {q1.z, q1.w, q2.x};
-      const bool nz = (q0.x != 0.f) | (q0.y != 0.f) | (q0.z != 0.f) | (q0.w != 0.f) | (q1.x != 0.f) |
-                      (q1.y != 0.f) | (dcol[0] != 0.f) | (dcol[1] != 0.f) | (dcol[2] != 0.f);
-      if (nz) {
-        float gx[3], gls[3], gq[4], gop, Y[16];
-        chain3d(a, g, i, q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, dcol, gx, gls, gq, gop, Y, cgj);
+  for (int k = 0; k < 30; ++k) o[k] = 0.f;
+  if (t >= cg) return;
+  const int64_t i = g0 + t;
+  const float4 q0 = grad2d[3 * i], q1 = grad2d[3 * i + 1], q2 = grad2d[3 * i + 2];
+  float dcol[3] = {q1.z, q1.w, q2.x};
+  const bool nz = (q0.x != 0.f) | (q0.y != 0.f) | (q0.z != 0.f) | (q0.w != 0.f) | (q1.x != 0.f) | (q1.y != 0.f) |
+                  (dcol[0] != 0.f) | (dcol[1] != 0.f) | (dcol[2] != 0.f);
+  if (!nz) return;
+  float gx[3], gls[3], gq[4], gop, Y[16];
+  chain3d(a, g, i, q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, dcol, gx, gls, gq, gop, Y, cgj);
 #pragma unroll
-        for (int k = 0; k < 3; ++k) {
-          o[k] = gx[k];
-          o[3 + k] = gls[k];
-          o[11 + k] = dcol[k];
-        }
-#pragma unroll
-        for (int k = 0; k < 4; ++k) o[6 + k] = gq[k];
-        o[10] = gop;
-#pragma unroll
-        for (int k = 0; k < 16; ++k) o[14 + k] = Y[k];
-      }
-    }
+  for (int k = 0; k < 3; ++k) {
+    o[k] = gx[k];
+    o[3 + k] = gls[k];
+    o[11 + k] = dcol[k];
   }
-  __syncthreads();
-  // ---- phase B: units of the chunk's group slices, concatenated (group table in shared memory:
-  // dynamically indexed, it would otherwise live on the stack) ----
-  __shared__ CaGroup grp[5];
-  __shared__ uint32_t len[5], dims[5], ub[6];
-  __shared__ float idim[5], steps[5];
-  __shared__ int soff[5];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) o[6 + k] = gq[k];
+  o[10] = gop;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) o[14 + k] = Y[k];
+}
+
+// the chunk's five group slices (pointers, lengths, float4-unit ranges, floats per Gaussian, step
+// sizes, gradient offsets): built by one thread into shared memory (dynamically indexed per unit)
+struct CaTable {
+  CaGroup grp[5];
+  uint32_t len[5], dims[5], ub[6];
+  float idim[5], steps[5];
+  int soff[5];
+  int cg;
+};
+__device__ __forceinline__ void ca_table(CaTable& T, const RenderArgs& a, const gps_gaussians& g,
+                                         const gps_gaussians& gm, const gps_gaussians& gv, const gps_gaussians& gout,
+                                         int has_gout, const AdamArgs& ad, int64_t g0, int cg) {
   const uint32_t nsh = 3u * (uint32_t)a.nc;
-  if (threadIdx.x == 0) {
-    const uint32_t ln[5] = {3u * cg, 3u * cg, 4u * cg, (uint32_t)cg, nsh * cg};
-    const uint32_t dm[5] = {3u, 3u, 4u, 1u, nsh};
-    const int so[5] = {0, 3, 6, 10, 14};
-    const float st[5] = {ad.step_xyz, ad.step_ls, ad.step_rot, ad.step_op, ad.step_shr};
-    float* const Ps[5] = {g.xyz + 3 * g0, g.log_scale + 3 * g0, g.rot + 4 * g0, g.opacity_raw + g0, g.sh + nsh * g0};
-    float* const Ms[5] = {gm.xyz + 3 * g0, gm.log_scale + 3 * g0, gm.rot + 4 * g0, gm.opacity_raw + g0, gm.sh + nsh * g0};
-    float* const Vs[5] = {gv.xyz + 3 * g0, gv.log_scale + 3 * g0, gv.rot + 4 * g0, gv.opacity_raw + g0, gv.sh + nsh * g0};
-    ub[0] = 0;
+  const uint32_t ln[5] = {3u * cg, 3u * cg, 4u * cg, (uint32_t)cg, nsh * cg};
+  const uint32_t dm[5] = {3u, 3u, 4u, 1u, nsh};
+  const int so[5] = {0, 3, 6, 10, 14};
+  const float st[5] = {ad.step_xyz, ad.step_ls, ad.step_rot, ad.step_op, ad.step_shr};
+  float* const Ps[5] = {g.xyz + 3 * g0, g.log_scale + 3 * g0, g.rot + 4 * g0, g.opacity_raw + g0, g.sh + nsh * g0};
+  float* const Ms[5] = {gm.xyz + 3 * g0, gm.log_scale + 3 * g0, gm.rot + 4 * g0, gm.opacity_raw + g0, gm.sh + nsh * g0};
+  float* const Vs[5] = {gv.xyz + 3 * g0, gv.log_scale + 3 * g0, gv.rot + 4 * g0, gv.opacity_raw + g0, gv.sh + nsh * g0};
+  T.ub[0] = 0;
+  T.cg = cg;
 #pragma unroll
-    for (int q = 0; q < 5; ++q) {
-      len[q] = ln[q];
-      dims[q] = dm[q];
-      idim[q] = 1.0f / (float)dm[q];
-      steps[q] = st[q];
-      soff[q] = so[q];
-      ub[q + 1] = ub[q] + (ln[q] + 3u) / 4u;
-      grp[q].P = Ps[q];
-      grp[q].M = Ms[q];
-      grp[q].V = Vs[q];
-    }
-    grp[0].O = has_gout ? gout.xyz + 3 * g0 : nullptr;
-    grp[1].O = has_gout ? gout.log_scale + 3 * g0 : nullptr;
-    grp[2].O = has_gout ? gout.rot + 4 * g0 : nullptr;
-    grp[3].O = has_gout ? gout.opacity_raw + g0 : nullptr;
-    grp[4].O = has_gout ? gout.sh + nsh * g0 : nullptr;
+  for (int q = 0; q < 5; ++q) {
+    T.len[q] = ln[q];
+    T.dims[q] = dm[q];
+    T.idim[q] = 1.0f / (float)dm[q];
+    T.steps[q] = st[q];
+    T.soff[q] = so[q];
+    T.ub[q + 1] = T.ub[q] + (ln[q] + 3u) / 4u;
+    T.grp[q].P = Ps[q];
+    T.grp[q].M = Ms[q];
+    T.grp[q].V = Vs[q];
   }
-  __syncthreads();
+  T.grp[0].O = has_gout ? gout.xyz + 3 * g0 : nullptr;
+  T.grp[1].O = has_gout ? gout.log_scale + 3 * g0 : nullptr;
+  T.grp[2].O = has_gout ? gout.rot + 4 * g0 : nullptr;
+  T.grp[3].O = has_gout ? gout.opacity_raw + g0 : nullptr;
+  T.grp[4].O = has_gout ? gout.sh + nsh * g0 : nullptr;
+}
+
+// phase B by threads tid = 0 .. nthr-1: the chunk's units, kU per thread in flight
+__device__ __forceinline__ void ca_phase_b(const CaTable& T, const float* sg, int tid, int nthr, int has_gout,
+                                           const AdamArgs& ad) {
+  const int cg = T.cg;
+  const uint32_t* ub = T.ub;
+  const uint32_t* len = T.len;
+  const uint32_t* dims = T.dims;
+  const float* idim = T.idim;
+  const float* steps = T.steps;
+  const int* soff = T.soff;
+  const CaGroup* grp = T.grp;
   constexpr int kU = 4;  // units per thread in flight
-  for (uint32_t U0 = threadIdx.x; U0 < ub[5]; U0 += kU * kCaG) {
+  for (uint32_t U0 = tid; U0 < ub[5]; U0 += kU * nthr) {
     float p[kU][4], m[kU][4], v[kU][4];
     int gq[kU];
     uint32_t e0[kU], cnt[kU];
 #pragma unroll
     for (int j = 0; j < kU; ++j) {
-      const uint32_t U = U0 + j * kCaG;
+      const uint32_t U = U0 + j * nthr;
       int q = 0;
 #pragma unroll
       for (int r = 1; r < 5; ++r) q += U >= ub[r];
@@ -2195,6 +2205,20 @@ __global__ void __launch_bounds__(kCaG, 4) k_chain_adam(RenderArgs a, gps_gaussi
       }
     }
   }
+}
+
+__global__ void __launch_bounds__(kCaG, 4) k_chain_adam(RenderArgs a, gps_gaussians g, gps_gaussians gm,
+                                                      gps_gaussians gv, const float4* __restrict__ grad2d,
+                                                      const float4* __restrict__ cgj, gps_gaussians gout,
+                                                      int has_gout, AdamArgs ad) {
+  __shared__ float sg[kCaG * kCaStride];
+  __shared__ CaTable tab;
+  const int64_t g0 = (int64_t)blockIdx.x * kCaG;
+  const int cg = (int)(a.n - g0 < (int64_t)kCaG ? a.n - g0 : (int64_t)kCaG);
+  ca_phase_a(a, g, grad2d, cgj, g0, cg, threadIdx.x, sg);
+  if (threadIdx.x == 0) ca_table(tab, a, g, gm, gv, gout, has_gout, ad, g0, cg);
+  __syncthreads();
+  ca_phase_b(tab, sg, threadIdx.x, kCaG, has_gout, ad);
 }
 
 }  // namespace gps
