@@ -843,6 +843,71 @@ __global__ void __launch_bounds__(256) k_range(VolumeView v, RayParams p_in, uin
   }
 }
 
+// k_range_smem: the same range image, reduced first in shared memory.  Every block hits 1-16
+// tiles and ~100 blocks share a tile, so the global form serialises on ~3600 hot addresses; here
+// each CTA folds a contiguous slice of the pool (blocks allocated together lie together) into its
+// own copy of the image with shared atomics, then merges only the tiles it touched.  Same min/max
+// of the same values: the image is identical.  Images up to kRangeSmemTiles tiles.
+constexpr int kRangeSmemTiles = 6144;  // 48 KB of dynamic shared memory (1280x720 at 16x16: 3600)
+
+template <bool DPOSE = false>
+__global__ void __launch_bounds__(512) k_range_smem(VolumeView v, RayParams p_in, uint32_t* tmin, uint32_t* tmax,
+                                                    int tiles_x, int tiles_y) {
+  extern __shared__ uint32_t srange[];  // [ntiles] min, then [ntiles] max
+  RayParams p = p_in;
+  apply_dpose<DPOSE>(p);
+  const int ntiles = tiles_x * tiles_y;
+  uint32_t* smin = srange;
+  uint32_t* smax = srange + ntiles;
+  for (int t = threadIdx.x; t < ntiles; t += blockDim.x) {
+    smin[t] = 0xFFFFFFFFu;
+    smax[t] = 0u;
+  }
+  __syncthreads();
+  const uint32_t nb = min(*(volatile uint32_t*)&v.ctr->n_blocks, v.max_blocks);
+  const uint32_t per = (nb + gridDim.x - 1) / gridDim.x;
+  const uint32_t lo = blockIdx.x * per, hi = min(nb, lo + per);
+  const int lane = threadIdx.x & 31;
+  for (uint32_t b0 = lo; b0 < hi; b0 += blockDim.x) {  // warp-uniform trip count
+    const uint32_t b = b0 + threadIdx.x;
+    int tx0 = 1, tx1 = 0, ty0 = 0, ty1 = 0;
+    uint32_t a0 = 0, a1 = 0;
+    if (b < hi) block_tile_range(v, p, b, tiles_x, tiles_y, tx0, tx1, ty0, ty1, a0, a1);
+    const bool any = tx0 <= tx1 && ty0 <= ty1;
+    const bool big = any && (tx1 - tx0 + 1) * (ty1 - ty0 + 1) > 4;
+    if (any && !big) {
+      for (int ty = ty0; ty <= ty1; ++ty)
+        for (int tx = tx0; tx <= tx1; ++tx) {
+          const int t = ty * tiles_x + tx;
+          GPS_DCHECK(t >= 0 && t < ntiles, CHK_RANGE_TILE);
+          atomicMin(&smin[t], a0);
+          atomicMax(&smax[t], a1);
+        }
+    }
+    uint32_t bm = __ballot_sync(0xFFFFFFFFu, big);
+    while (bm) {
+      const int src = __ffs(bm) - 1;
+      bm &= bm - 1u;
+      const int sx0 = __shfl_sync(0xFFFFFFFFu, tx0, src), sx1 = __shfl_sync(0xFFFFFFFFu, tx1, src);
+      const int sy0 = __shfl_sync(0xFFFFFFFFu, ty0, src), sy1 = __shfl_sync(0xFFFFFFFFu, ty1, src);
+      const uint32_t s0 = __shfl_sync(0xFFFFFFFFu, a0, src), s1 = __shfl_sync(0xFFFFFFFFu, a1, src);
+      const int wx = sx1 - sx0 + 1, cnt = wx * (sy1 - sy0 + 1);
+      for (int k = lane; k < cnt; k += 32) {
+        const int t = (sy0 + k / wx) * tiles_x + sx0 + k % wx;
+        GPS_DCHECK(t >= 0 && t < ntiles, CHK_RANGE_TILE);
+        atomicMin(&smin[t], s0);
+        atomicMax(&smax[t], s1);
+      }
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < ntiles; t += blockDim.x) {
+    const uint32_t m0 = smin[t], m1 = smax[t];
+    if (m0 != 0xFFFFFFFFu && tmin[t] > m0) atomicMin(&tmin[t], m0);
+    if (m1 != 0u && tmax[t] < m1) atomicMax(&tmax[t], m1);
+  }
+}
+
 // tile rect [tx0, tx1] x [ty0, ty1] (empty: tx0 > tx1) and the t range (float bits a0, a1) of
 // pool block b for the range image
 __device__ __forceinline__ void block_tile_range(const VolumeView& v, const RayParams& p, uint32_t b, int tiles_x,
@@ -1590,10 +1655,23 @@ static gps_status raycast_impl(const gps_volume* vol, const gps_intrinsics* K, c
     GPS_CHECK_CUDA(cudaMemsetAsync(tmax, 0x00, sizeof(uint32_t) * ntiles, s));
     {
       GPS_PROF(K_RANGE, s);
-      if (dT)
+      const bool global_range = getenv("GPS_RANGE_GLOBAL") != nullptr;  // A/B and the test: global atomics only
+      const size_t smem = 8 * (size_t)ntiles;
+      if (ntiles <= kRangeSmemTiles && !global_range) {
+        static const bool attr = cudaFuncSetAttribute(k_range_smem<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                      8 * kRangeSmemTiles) == cudaSuccess &&
+                                 cudaFuncSetAttribute(k_range_smem<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                      8 * kRangeSmemTiles) == cudaSuccess;
+        if (!attr) return cuda_fail("cudaFuncSetAttribute(k_range_smem)", cudaGetLastError());
+        if (dT)
+          k_range_smem<true><<<148 * 2, 512, smem, s>>>(v->view, p, tmin, tmax, (int)g.x, (int)g.y);
+        else
+          k_range_smem<<<148 * 2, 512, smem, s>>>(v->view, p, tmin, tmax, (int)g.x, (int)g.y);
+      } else if (dT) {
         k_range<true><<<148 * 4, 256, 0, s>>>(v->view, p, tmin, tmax, (int)g.x, (int)g.y);
-      else
+      } else {
         k_range<<<148 * 4, 256, 0, s>>>(v->view, p, tmin, tmax, (int)g.x, (int)g.y);
+      }
     }
     GPS_CHECK_LAUNCH("k_range");
   }

@@ -181,3 +181,23 @@ def test_dense_grid_changes_nothing():
     Da, Ca, _ = a.raycast(gcam, R, t)
     Db, Cb, _ = b.raycast(gcam, R, t)
     assert torch.equal(Da, Db) and torch.equal(Ca, Cb)
+
+
+def test_shared_memory_range_image_changes_nothing(monkeypatch):
+    """k_range_smem (per-CTA range image in shared memory, merged per touched tile) computes the
+    same min/max of the same per-block values as the global-atomics k_range (GPS_RANGE_GLOBAL=1,
+    read per call): the raycast -- depth, colour and vertices -- is bitwise identical (cfg4 after
+    40 frames: ~60k blocks; a pose inside the room and one whose near blocks span many tiles)."""
+    cfg = S.get_config("cfg4")
+    vol = H.gpu_volume(cfg)
+    gcam, _ = H.cams(cfg)
+    for fr in H.frames(cfg, 40):
+        d, c = H.to_dev(fr)
+        vol.fuse(gcam, fr.R, fr.t, d, cfg.depth_scale, c)
+    for R, t in (S.trajectory(cfg, 1, start=45)[0], S.trajectory(cfg, 1, start=0)[0]):
+        monkeypatch.delenv("GPS_RANGE_GLOBAL", raising=False)
+        D0, C0, V0 = vol.raycast(gcam, R, t, want_vertex=True)
+        monkeypatch.setenv("GPS_RANGE_GLOBAL", "1")
+        D1, C1, V1 = vol.raycast(gcam, R, t, want_vertex=True)
+        assert int((D0 > 0).sum()) > 100000
+        assert torch.equal(D0, D1) and torch.equal(C0, C1) and torch.equal(V0, V1)
