@@ -651,32 +651,38 @@ __global__ void __launch_bounds__(256, 4) k_integrate_rows(VolumeView v, FusePar
       }
     }
     // subneg (rare): each voxel whose indicator changed adjusts the counts of the sub-blocks that
-    // hold it, in the block itself and in every -neighbour whose apron it feeds
+    // hold it, in the block itself and in every -neighbour whose apron it feeds.  A cell x of the
+    // row lies in x-half 0 if x <= 4 and in x-half 1 if x >= 4 (cell 4 in both), so per target
+    // block the row's change is Dlo * (its half-0 sub-blocks) + Dhi * (its half-1 sub-blocks);
+    // voxel 0 alone feeds the x-face (x = 8: half 1) of the -x neighbours
     if (up | dn) {
       const int32_t mm[8] = {c0r.x, c0r.y, c0r.z, c0r.w, c1r.x, c1r.y, c1r.z, c1r.w};
-      uint64_t wd[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      for (int x = 0; x < 8; ++x) {
-        const int d = (int)((up >> x) & 1u) - (int)((dn >> x) & 1u);
-        if (!d) continue;
-        const int zyz = (x == 0 ? 1 : 0) | (lj == 0 ? 2 : 0) | (lk == 0 ? 4 : 0);
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-          if ((k & ~zyz) == 0)
-            wd[k] += (uint64_t)(int64_t)d * cell_subs(x + 8 * (k & 1), lj + 8 * ((k >> 1) & 1), lk + 8 * (k >> 2));
-      }
+      const int Dlo = __popc(up & 0x1Fu) - __popc(dn & 0x1Fu), Dhi = __popc(up & 0xF0u) - __popc(dn & 0xF0u);
+      const int d0 = (int)(up & 1u) - (int)(dn & 1u);
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        if (!wd[k] || mm[k] < 0) continue;
+        const bool feeds = (k & 2 ? lj == 0 : true) && (k & 4 ? lk == 0 : true);
+        if (!feeds || mm[k] < 0) continue;
+        const int yy = lj + 8 * ((k >> 1) & 1), zz = lk + 8 * (k >> 2);
+        uint64_t wd;
+        if (k & 1) {
+          if (!d0) continue;
+          wd = (uint64_t)(int64_t)d0 * cell_subs(8, yy, zz);
+        } else {
+          // cell_subs(0, ..) = the half-0 sub-blocks, cell_subs(7, ..) = the half-1 ones
+          wd = (uint64_t)(int64_t)Dlo * cell_subs(0, yy, zz) + (uint64_t)(int64_t)Dhi * cell_subs(7, yy, zz);
+        }
+        if (!wd) continue;
         GPS_DCHECK((uint32_t)mm[k] < min(v.ctr->n_blocks, v.max_blocks), CHK_NBR);
 #ifdef GPS_CHECKED
         const unsigned long long nw =
-            atomicAdd(reinterpret_cast<unsigned long long*>(&v.subneg[mm[k]]), (unsigned long long)wd[k]) + wd[k];
+            atomicAdd(reinterpret_cast<unsigned long long*>(&v.subneg[mm[k]]), (unsigned long long)wd) + wd;
         bool okb = true;
 #pragma unroll
         for (int qb = 0; qb < 8; ++qb) okb &= ((nw >> (8 * qb)) & 0xFFull) <= 125ull;
         GPS_DCHECK(okb, CHK_SUBNEG);
 #else
-        atomicAdd(reinterpret_cast<unsigned long long*>(&v.subneg[mm[k]]), (unsigned long long)wd[k]);
+        atomicAdd(reinterpret_cast<unsigned long long*>(&v.subneg[mm[k]]), (unsigned long long)wd);
 #endif
       }
     }
