@@ -62,6 +62,8 @@ def parse():
                          "beyond it; no scene knowledge); scene (the synthetic room's ground-truth bounds)")
     ap.add_argument("--workspace-m", type=float, default=25.6,
                     help="edge of the workspace grid's cube in metres (25.6 m: 640^3 blocks of 4 cm, 1 GiB)")
+    ap.add_argument("--timeline", default="", help="diagnostic: write the overlapped schedule's per-launch "
+                    "timeline (JSON) after the measurements")
     ap.add_argument("--cpu-seconds", type=float, default=20.0, help="budget of the cpu_baseline sample")
     return ap.parse_args()
 
@@ -346,6 +348,18 @@ def run_ours(args):
         prof = read_profile(N)
         N._lib.gps_profile_enable(0)
         pipe.overlap = not args.no_overlap
+    if args.timeline and rank == 0:
+        # diagnostic: the overlapped schedule with every launch bracketed by events on its stream
+        # (the per-launch start/end show which stream waits where); never a timed value
+        pipe.restore(snap)
+        k = k0
+        torch.cuda.synchronize()
+        N._lib.gps_profile_enable(1)
+        run_steps(args.steps)
+        pipe.join(stream)
+        torch.cuda.synchronize()
+        write_timeline(N, args.timeline)
+        N._lib.gps_profile_enable(0)
     if ws > 1:
         dist.barrier()
     if rank != 0:
@@ -531,6 +545,59 @@ def workload_config(args, cfg, n_g, ws):
                            "workspace": f"{args.workspace_m} m cube centred on the first camera position "
                                         "(fixed size, no scene knowledge; hash beyond it)",
                            "scene": "the synthetic room's ground-truth bounds"}[args.dense_grid]}
+
+
+def write_timeline(N, path):
+    """Per-launch (kernel, start, end) of the last profiled session as JSON (ms from its first
+    event), plus per-stream-family busy time and the refinement stream's idle gaps."""
+    import ctypes as C
+    cap = 1 << 16
+    ids = (C.c_int32 * cap)()
+    t0 = (C.c_double * cap)()
+    t1 = (C.c_double * cap)()
+    n = min(N._lib.gps_profile_timeline_sync(ids, t0, t1, cap), cap)
+    names = C.create_string_buffer(512)
+    tot = (C.c_double * 32)()
+    cnt = (C.c_int64 * 32)()
+    m = N._lib.gps_profile_read_sync(names, 512, tot, cnt, 32)
+    kn = names.value.decode().split(";")[:m]
+    ev = [(kn[ids[i]], t0[i], t1[i]) for i in range(n)]
+    fusion = {"k_alloc", "k_link", "k_integrate", "k_range", "k_raycast"}
+
+    def union(iv):
+        iv = sorted(iv)
+        tot_, cur0, cur1 = 0.0, None, None
+        gaps = []
+        for a, b in iv:
+            if cur1 is None or a > cur1:
+                if cur1 is not None:
+                    tot_ += cur1 - cur0
+                    gaps.append(a - cur1)
+                cur0, cur1 = a, b
+            else:
+                cur1 = max(cur1, b)
+        if cur1 is not None:
+            tot_ += cur1 - cur0
+        return tot_, gaps
+    span = max(e[2] for e in ev) - min(e[1] for e in ev) if ev else 0.0
+    fb, _ = union([(a, b) for k_, a, b in ev if k_ in fusion])
+    rb, rg = union([(a, b) for k_, a, b in ev if k_ not in fusion])
+    both = 0.0
+    fi = sorted((a, b) for k_, a, b in ev if k_ in fusion)
+    ri = sorted((a, b) for k_, a, b in ev if k_ not in fusion)
+    j = 0
+    for a, b in ri:  # overlap of the two families (intervals within a family do not overlap)
+        while j < len(fi) and fi[j][1] <= a:
+            j += 1
+        jj = j
+        while jj < len(fi) and fi[jj][0] < b:
+            both += max(0.0, min(b, fi[jj][1]) - max(a, fi[jj][0]))
+            jj += 1
+    summary = {"span_ms": span, "fusion_busy_ms": fb, "refine_busy_ms": rb, "both_busy_ms": both,
+               "refine_gaps_over_50us_ms": sum(g for g in rg if g > 0.05), "n_launches": n}
+    with open(path, "w") as f:
+        json.dump({"summary": summary, "launches": ev}, f)
+    print("timeline:", json.dumps(summary), file=sys.stderr)
 
 
 def read_profile(N):

@@ -491,6 +491,12 @@ gps_status gps_debug_render_lists_sync(const void* ws, gps_stream_t stream, uint
 void gps_profile_enable(int on);
 int gps_profile_read_sync(char* names /*host*/, int names_cap, double* total_ms /*host*/,
                           int64_t* launches /*host*/, int cap);
+/* The session's per-launch timeline: for each launch in enqueue order its kernel id (the index
+ * into gps_profile_read_sync's names) and its start / end in ms from the session's first event
+ * (host arrays of `cap`); returns the number of launches (synchronises).  Concurrent streams'
+ * launches overlap in this timeline as they did on the device (debug).                      */
+int64_t gps_profile_timeline_sync(int32_t* ids /*host*/, double* t0_ms /*host*/, double* t1_ms /*host*/,
+                                  int64_t cap);
 
 const char* gps_status_string(gps_status s);
 const char* gps_last_error(void); /* thread-local; "" if none */

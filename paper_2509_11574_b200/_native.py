@@ -138,6 +138,7 @@ PROTOTYPES = {
                                                   P(gps_render_config), vp, sz, P(i64), P(i64), gps_stream_t]),
     "gps_profile_enable": (None, [C.c_int]),
     "gps_profile_read_sync": (C.c_int, [C.c_char_p, C.c_int, P(C.c_double), P(i64), C.c_int]),
+    "gps_profile_timeline_sync": (i64, [P(C.c_int32), P(C.c_double), P(C.c_double), i64]),
     "gps_status_string": (C.c_char_p, [gps_status]),
     "gps_last_error": (C.c_char_p, []),
     "gps_abi_version": (C.c_int, []),

@@ -89,4 +89,25 @@ int gps_profile_read_sync(char* names, int names_cap, double* total_ms, int64_t*
   }
   return gps::K_COUNT;
 }
+
+// per-launch timeline of the session: kernel id and start / end in ms from the session's first
+// event (all launches, in enqueue order); returns the number of launches recorded
+int64_t gps_profile_timeline_sync(int32_t* ids, double* t0_ms, double* t1_ms, int64_t cap) {
+  std::lock_guard<std::mutex> l(gps::g_mu);
+  if (gps::g_pairs.empty()) return 0;
+  cudaEvent_t base = gps::g_pairs.front().a;
+  int64_t n = 0;
+  for (auto& p : gps::g_pairs) {
+    if (cudaEventSynchronize(p.b) != cudaSuccess) continue;
+    float a = 0.f, b = 0.f;
+    if (cudaEventElapsedTime(&a, base, p.a) != cudaSuccess || cudaEventElapsedTime(&b, base, p.b) != cudaSuccess) continue;
+    if (n < cap) {
+      ids[n] = p.id;
+      t0_ms[n] = a;
+      t1_ms[n] = b;
+    }
+    ++n;
+  }
+  return n;
+}
 }
