@@ -261,6 +261,7 @@ class Gaussians:
         if n > self.capacity:
             raise ValueError("n exceeds capacity")
         self.n = int(n)
+        self._c = None  # the cached C struct carries n
         for k in FIELDS:
             setattr(self, k, self._store[k][:self.n])
 
@@ -272,7 +273,10 @@ class Gaussians:
         return Gaussians(self.n, self.sh_degree, self.xyz.device, capacity=self.capacity)
 
     def c(self) -> N.gps_gaussians:
-        return N.gps_gaussians(self.n, self.sh_degree, *(C.c_void_p(self._store[k].data_ptr()) for k in FIELDS))
+        # cached: the storage never moves and n changes only through set_n (host cost per call)
+        if getattr(self, "_c", None) is None:
+            self._c = N.gps_gaussians(self.n, self.sh_degree, *(C.c_void_p(self._store[k].data_ptr()) for k in FIELDS))
+        return self._c
 
     def to_numpy(self) -> dict:
         out = {k: getattr(self, k).detach().cpu().numpy() for k in FIELDS}
@@ -337,8 +341,11 @@ class View:
     target_rgba: torch.Tensor
 
     def c(self) -> N.gps_view:
-        return N.gps_view(self.cam.c(), pose_struct(self.R, self.t), _ptr(self.sdf_depth), _ptr(self.sdf_color),
-                          _ptr(self.target_rgba))
+        # built once: a View is not modified after its first use (the pipeline makes new ones)
+        if getattr(self, "_c", None) is None:
+            self._c = N.gps_view(self.cam.c(), pose_struct(self.R, self.t), _ptr(self.sdf_depth),
+                                 _ptr(self.sdf_color), _ptr(self.target_rgba))
+        return self._c
 
 
 class Rasterizer:
@@ -381,9 +388,12 @@ class Rasterizer:
         st = N.gps_adam_state(state.m.c(), state.v.c(), state.step)
         gc = g.c()
         go = grad_out.c() if grad_out is not None else None
+        key = (id(adam), tuple(adam.__dict__.values()), tuple(self.cfg.__dict__.values()))
+        if getattr(self, "_ckey", None) != key:  # the config structs, rebuilt only when they change
+            self._ckey, self._cc = key, (self.cfg.c(), adam.c())
         N.check("gps_refine_step",
-                _L.gps_refine_step(C.byref(gc), C.byref(st), arr, len(views), C.byref(self.cfg.c()),
-                                   C.byref(adam.c()), _ptr(self.ws), self.ws.numel(), _ptr(self.loss),
+                _L.gps_refine_step(C.byref(gc), C.byref(st), arr, len(views), C.byref(self._cc[0]),
+                                   C.byref(self._cc[1]), _ptr(self.ws), self.ws.numel(), _ptr(self.loss),
                                    C.byref(go) if go is not None else None, _stream(stream)))
         state.step = st.step
         return self.loss

@@ -174,3 +174,64 @@ def test_tracking_pose_readback_is_deferred_not_changed():
     # fusion is bit-exact, so the same poses give the same volume (the refinement's float
     # atomics are not order-deterministic, so the Gaussians are not compared bitwise)
     assert np.array_equal(ca, cb) and np.array_equal(va.view(np.uint8), vb.view(np.uint8))
+
+
+def test_host_frames_through_the_upload_pool_match_device_frames():
+    """The end-to-end path: pinned host frames uploaded on the copy stream (one frame ahead) give
+    the volume bitwise and the losses of the same frames passed as device tensors; 42 frames (4
+    rounds, keyframes kept across rounds), then a snapshot / restore / replay of the last 10
+    frames from host frames reproduces the volume again."""
+    import paper_2509_11574_b200 as G
+    from paper_2509_11574_b200.pipeline import MappingPipeline
+
+    cfg = S.get_config("cfg2")
+    n_frames = 42
+    scene = S.make_scene(cfg)
+    dc = S.pixel_rays(cfg, "cuda")
+    poses = S.trajectory(cfg, n_frames)
+    frames = []
+    for k in range(n_frames):
+        fr = S.render_frame(cfg, scene, *poses[k], k=k, device="cuda", dc=dc)
+        frames.append((fr.depth.contiguous(), fr.rgba.contiguous(), fr.R, fr.t))
+    host = [(d.cpu().pin_memory(), c.cpu().pin_memory()) for d, c, _, _ in frames]
+    gd = S.make_gaussians(cfg, n=10000)
+    out = []
+    for mode in ("device", "host"):
+        cam = G.Camera(cfg.fx, cfg.fy, cfg.cx, cfg.cy, cfg.width, cfg.height)
+        vol = G.Volume(voxel_size=cfg.voxel_size, max_blocks=cfg.max_blocks, hash_slots=cfg.hash_slots)
+        g = G.Gaussians.from_dict(gd)
+        pipe = MappingPipeline(cam, g, vol, cfg.depth_scale, seed=5)
+        losses, snap = [], None
+        for k in range(n_frames):
+            if k == 31:
+                snap = pipe.snapshot()
+            d, c, R, t = frames[k]
+            if mode == "host":
+                d, c = host[k]
+            nxt = host[k + 1] if mode == "host" and k + 1 < n_frames else None
+            pipe.process_frame(k, d, c, R, t, prefetch=nxt)
+            if k % 10 == 0:
+                pipe.join()
+                losses.append(pipe.last_loss.item())
+        pipe.join()
+        torch.cuda.synchronize()
+        coords, vox = vol.export_blocks()
+        order = np.lexsort((coords[:, 2], coords[:, 1], coords[:, 0]))
+        res = [coords[order], vox[order], losses]
+        if mode == "host":  # replay frames 31..41 from the snapshot
+            pipe.restore(snap)
+            for k in range(31, n_frames):
+                d, c = host[k]
+                pipe.process_frame(k, d, c, frames[k][2], frames[k][3],
+                                   prefetch=host[k + 1] if k + 1 < n_frames else None)
+            pipe.join()
+            torch.cuda.synchronize()
+            c2, v2 = vol.export_blocks()
+            o2 = np.lexsort((c2[:, 2], c2[:, 1], c2[:, 0]))
+            res += [c2[o2], v2[o2]]
+        out.append(res)
+    (c0, v0, l0), (c1, v1, l1, c2, v2) = out[0], out[1]
+    assert np.array_equal(c0, c1) and np.array_equal(v0.view(np.uint8), v1.view(np.uint8))
+    assert np.array_equal(c0, c2) and np.array_equal(v0.view(np.uint8), v2.view(np.uint8))
+    assert len(l0) == 5 and all(x > 0 for x in l0)
+    np.testing.assert_allclose(l1, l0, rtol=2e-3)
