@@ -198,6 +198,17 @@ def run_ours(args):
                    dense_bounds=dense_bounds(args, S, cfg, poses))
     g = G.Gaussians.from_dict(gd, capacity=4 * n_g if args.manage_gaussians else None)
     rcfg = G.RenderConfig(tile=args.tile, sort_free=int(args.sort_free), backward=args.backward)
+    slow = float(os.environ.get("GPS_BENCH_HOST_DELAY_US", "0"))  # diagnostic: emulate a slower host
+    if slow > 0:
+        _pf = MappingPipeline.process_frame
+
+        def _slow_pf(self, *a, **kw):
+            r = _pf(self, *a, **kw)
+            t_end = time.perf_counter() + slow * 1e-6
+            while time.perf_counter() < t_end:
+                pass
+            return r
+        MappingPipeline.process_frame = _slow_pf
     pipe = MappingPipeline(cam, g, vol, cfg.depth_scale, rcfg, seed=rank,
                            overlap=not args.no_overlap, refine_priority=args.refine_priority,
                            manage_gaussians=args.manage_gaussians, all_views_per_iteration=args.all_views,
