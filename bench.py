@@ -384,14 +384,15 @@ def run_ours(args):
     # algorithmic bytes per launch: dense Adam reads and writes p, m, v (24 P B per
     # Gaussian) and reads each Gaussian's gradient record + flag (132 B)
     per_launch["k_adam"] = n_g * (24 * P + 132)
-    # raycast: 16 B of output per pixel + 4 B per distinct tsdf voxel the march reads, the latter
+    # raycast: 16 B of output per pixel + 8 B (the voxel's state: tsdf + colour
+    # word) per distinct voxel the march touches, the latter
     # measured on device (footprint bitmap) for the last timed frame's pose on the final state
     if not prof:  # --no-profile: timing only (no per-kernel times, no roofline launch time)
         prof = {kk: {"ms": 0.0, "launches": 0} for kk in ("k_adam", "k_integrate", "k_raycast")}
     if prof["k_raycast"]["launches"]:
         ray_px = cfg.width * cfg.height
         uniq = vol.raycast_footprint(cam, frames[k - 1][2], frames[k - 1][3])
-        per_launch["k_raycast"] = 16 * ray_px + 4 * uniq
+        per_launch["k_raycast"] = 16 * ray_px + 8 * uniq
         ray_note = {"unique_voxels": uniq, "pixels": ray_px}
     # integration reads + writes each voxel it updates (eta >= -mu): 16 B per updated voxel,
     # counted on device over the timed region (updated_total delta)
@@ -415,7 +416,9 @@ def run_ours(args):
             "algorithmic_bytes_per_launch": int(per_launch[roof_k]), "avg_launch_ms": round(avg, 5)}
     if roof_k == "k_raycast":
         roof["units"] = ray_note
-        roof["note"] = "latency-bound march (dependent voxel loads); bytes = 16 B/px out + 4 B/unique tsdf voxel"
+        roof["note"] = ("latency-bound march (dependent L1 corner loads); bytes = SURVEY 8(d) a4: 16 B/px out + "
+                        "8 B per distinct voxel touched (this build's march reads the 4-byte tsdf plane, and "
+                        "colour only at the hit)")
     shares = {kk: {"ms_per_step": round(v["ms"] / args.steps, 4), "launches_per_step": v["launches"] / args.steps,
                    "share": round(v["ms"] / max(ms_prof, 1e-9), 4)} for kk, v in prof.items()}
     # HBM GB/s per kernel (BASELINE.json metric): algorithmic bytes per launch (from the
