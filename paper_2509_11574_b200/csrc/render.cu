@@ -659,7 +659,7 @@ __device__ __forceinline__ void bitonic_sort(Keys keys, int n) {
 // ~50 such tiles where thousands of small Gaussians stack along a wall at grazing angles.)
 // ============================================================================================
 constexpr int kShortList = 256;
-constexpr int kLongSmem = 8192;  // 64 KB of dynamic shared memory
+constexpr int kLongSmem = 2048;  // 16 KB of dynamic shared memory (longer lists sort in global memory)
 
 __global__ void __launch_bounds__(512) k_sort_long(const float4* __restrict__ rec, const uint32_t* __restrict__ offsets,
                                                   uint32_t* vals, uint64_t* gkeys, const uint32_t* __restrict__ longl,
