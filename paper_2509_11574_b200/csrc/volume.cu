@@ -267,12 +267,24 @@ __global__ void __launch_bounds__(256) k_alloc(VolumeView v, FuseParams p_in,
   __syncthreads();
   // global phase: find or insert each of the CTA's blocks, then mark the newly visible ones with
   // ONE append per warp (a single counter for all 65k visible blocks was the kernel's hottest
-  // serialisation point)
-  const int lane = threadIdx.x & 31;
-  for (int i0 = 0; i0 < kSmemSet; i0 += blockDim.x) {
-    const uint64_t key = set[i0 + threadIdx.x];
+  // serialisation point).  Each warp first compacts the occupied slots of its 256-slot share of
+  // the set (ballots, no barrier), so its dependent global chain (probe, stamp, append) runs once
+  // per 32 keys instead of once per 32 slots that hold any key.
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __shared__ uint16_t wlist[8][256];
+  uint32_t nk = 0;
+  for (int r = 0; r < 256; r += 32) {
+    const int slot = w * 256 + r + lane;
+    const bool occ = set[slot] != kEmptyKey;
+    const unsigned b = __ballot_sync(0xFFFFFFFFu, occ);
+    if (occ) wlist[w][nk + __popc(b & ((1u << lane) - 1u))] = (uint16_t)slot;
+    nk += __popc(b);
+  }
+  __syncwarp();
+  for (uint32_t i0 = 0; i0 < nk; i0 += 32) {
+    const uint32_t i = i0 + lane;
     int32_t slot = -1;
-    if (key != kEmptyKey) slot = global_find_or_insert(v, key, d_flag);
+    if (i < nk) slot = global_find_or_insert(v, set[wlist[w][i]], d_flag);
     bool app = false;
     if (slot >= 0 && v.stamp[slot] != frame) app = atomicExch(&v.stamp[slot], frame) != frame;
     const unsigned bal = __ballot_sync(0xFFFFFFFFu, app);
