@@ -54,6 +54,8 @@ def parse():
                     help="ICP tracking of every frame (Eq. 5, NEXT-3) instead of the given poses")
     ap.add_argument("--all-views", action="store_true",
                     help="every iteration renders all the round's views (SPEC S:471 variant, NEXT-4)")
+    ap.add_argument("--no-graphs", action="store_true",
+                    help="launch each refinement iteration directly instead of one CUDA graph per round")
     ap.add_argument("--no-overlap", action="store_true",
                     help="refinement on the fusion stream (serial schedule) instead of its own stream")
     ap.add_argument("--dense-grid", default="workspace", choices=["none", "workspace", "scene"],
@@ -212,7 +214,7 @@ def run_ours(args):
     pipe = MappingPipeline(cam, g, vol, cfg.depth_scale, rcfg, seed=rank,
                            overlap=not args.no_overlap, refine_priority=args.refine_priority,
                            manage_gaussians=args.manage_gaussians, all_views_per_iteration=args.all_views,
-                           track=args.track)
+                           track=args.track, graphs=not args.no_graphs)
     ate = []  # the timed frames (their tracked poses are compared with the truth after timing)
     k = 0
     for _ in range(args.history):  # build a steady-state volume (untimed, no rounds)
@@ -554,6 +556,8 @@ def workload_config(args, cfg, n_g, ws):
             "parallelism": f"replicas x{ws} (independent sequences)",
             "streams": "fusion+raycast on one stream, refinement rounds on a second (P:116)"
                        if not args.no_overlap else "one stream (serial schedule)",
+            "round_graphs": "each round's 20 iterations one CUDA graph (gps_refine_round)"
+                            if not args.no_graphs else "off (one gps_refine_step call per iteration)",
             "l2": "inputs larger than L2 (per-step state > 126 MB: params+Adam 283 MB, volume)",
             "dense_grid": {"none": "off (hash lookups only)",
                            "workspace": f"{args.workspace_m} m cube centred on the first camera position "

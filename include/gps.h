@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define GPS_ABI_VERSION 3  /* 2: gps_render_config.sort_free; adding, removal, tracking entry points; 3: device-pose forms */
+#define GPS_ABI_VERSION 4  /* 2: gps_render_config.sort_free; adding, removal, tracking entry points; 3: device-pose forms; 4: gps_refine_round */
 
 typedef void* gps_stream_t; /* a cudaStream_t */
 
@@ -264,6 +264,23 @@ gps_status gps_refine_step(gps_gaussians* g, gps_adam_state* state /*host struct
                            const gps_render_config* rcfg /*host*/,
                            const gps_adam_config* acfg /*host*/, void* ws, size_t ws_bytes,
                            float* loss_out, const gps_gaussians* grad_out, gps_stream_t stream);
+
+/* gps_refine_round -- a refinement round: n_iter gps_refine_step calls in
+ * one host call, iteration i over the views_per_iter views views[iter_views[i*views_per_iter + j]]
+ * (iter_views: host array of n_iter*views_per_iter indices into views; out-of-range -> error,
+ * nothing launched).  Same kernels, same order, same results as the n_iter calls; state->step
+ * += n_iter; loss_out <- the last iteration's loss.  use_graph != 0: the round's launches are
+ * stream-captured and replayed as one CUDA graph (one executable graph per workspace, updated in
+ * place while the round's launch structure is unchanged; freed at process exit).  Graphs are
+ * skipped on the legacy/per-thread default streams, inside a caller's own capture and while the
+ * event profiler is enabled.  On an error no iteration is launched and state->step is unchanged
+ * (with use_graph; without it, the iterations before the failing one have been enqueued).     */
+gps_status gps_refine_round(gps_gaussians* g, gps_adam_state* state /*host struct*/,
+                            const gps_view* views /*host array*/, int32_t n_views,
+                            const int32_t* iter_views /*host*/, int32_t views_per_iter, int32_t n_iter,
+                            const gps_render_config* rcfg /*host*/, const gps_adam_config* acfg /*host*/,
+                            void* ws, size_t ws_bytes, float* loss_out, int32_t use_graph,
+                            gps_stream_t stream);
 
 /* gps_adam_step -- the Adam update of gps_refine_step alone, on caller-given gradients
  * `grad` (parameter SoA layout).  Used to test the optimiser on identical gradients.          */

@@ -108,6 +108,8 @@ PROTOTYPES = {
     "gps_refine_step": (gps_status, [P(gps_gaussians), P(gps_adam_state), P(gps_view), i32,
                                      P(gps_render_config), P(gps_adam_config), vp, sz, vp,
                                      P(gps_gaussians), gps_stream_t]),
+    "gps_refine_round": (gps_status, [P(gps_gaussians), P(gps_adam_state), P(gps_view), i32, P(i32), i32, i32,
+                                      P(gps_render_config), P(gps_adam_config), vp, sz, vp, i32, gps_stream_t]),
     "gps_adam_step": (gps_status, [P(gps_gaussians), P(gps_adam_state), P(gps_gaussians),
                                    P(gps_adam_config), gps_stream_t]),
     "gps_render_stats_sync": (gps_status, [vp, gps_stream_t, P(i64), P(i64), P(i64)]),
@@ -182,7 +184,7 @@ def load(path: str | None = None):
     return L
 
 
-ABI_VERSION = 3  # must equal GPS_ABI_VERSION of include/gps.h (the struct layouts above)
+ABI_VERSION = 4  # must equal GPS_ABI_VERSION of include/gps.h (the struct layouts above)
 
 
 def check(fn: str, status: int):

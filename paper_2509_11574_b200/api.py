@@ -398,6 +398,31 @@ class Rasterizer:
         state.step = st.step
         return self.loss
 
+    def refine_round(self, g: Gaussians, state: AdamState, views: list[View], iter_views,
+                     adam: AdamConfig | None = None, graph: bool = True, stream=None):
+        """n_iter refine_step iterations in one call (gps_refine_round): iteration i uses the views
+        views[j] for j in iter_views[i] (a sequence of index sequences of equal length); with
+        graph=True the round runs as one CUDA graph (on a created stream)."""
+        adam = adam or AdamConfig()
+        rows = [list(r) for r in iter_views]
+        per = len(rows[0]) if rows else 1
+        if any(len(r) != per for r in rows):
+            raise ValueError("every iteration must use the same number of views")
+        flat = [j for r in rows for j in r]
+        idx = (C.c_int32 * max(len(flat), 1))(*flat)
+        arr = (N.gps_view * len(views))(*[v.c() for v in views])
+        st = N.gps_adam_state(state.m.c(), state.v.c(), state.step)
+        gc = g.c()
+        key = (id(adam), tuple(adam.__dict__.values()), tuple(self.cfg.__dict__.values()))
+        if getattr(self, "_ckey", None) != key:
+            self._ckey, self._cc = key, (self.cfg.c(), adam.c())
+        N.check("gps_refine_round",
+                _L.gps_refine_round(C.byref(gc), C.byref(st), arr, len(views), idx, per, len(rows),
+                                    C.byref(self._cc[0]), C.byref(self._cc[1]), _ptr(self.ws), self.ws.numel(),
+                                    _ptr(self.loss), int(graph), _stream(stream)))
+        state.step = st.step
+        return self.loss
+
     def stats(self, stream=None):
         K, cap, nv = C.c_int64(), C.c_int64(), C.c_int64()
         st = _L.gps_render_stats_sync(_ptr(self.ws), _stream(stream), C.byref(K), C.byref(cap), C.byref(nv))

@@ -24,7 +24,9 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -2278,6 +2280,12 @@ int64_t gbuf_floats(const gps_gaussians* g) {
   return (int64_t)align_up(11 * g->n, 4) + 3 * g->n * (g->sh_degree + 1) * (g->sh_degree + 1);
 }
 
+bool sort_long_ready() {  // once per process (before any stream capture: see gps_refine_round)
+  static const bool ok = cudaFuncSetAttribute(k_sort_long, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              8 * kLongSmem) == cudaSuccess;
+  return ok;
+}
+
 struct View1 {
   const gps_intrinsics* K;
   const gps_pose* T;
@@ -2345,9 +2353,7 @@ gps_status forward_view(const gps_gaussians* g, const View1& v, const gps_render
               reinterpret_cast<uint32_t*>(ws + L.tick), reinterpret_cast<float4*>(ws + L.part)};
   if (!c->sort_free && g->n > 0) {
     GPS_PROF(K_SORT_LONG, s);
-    static const bool attr = cudaFuncSetAttribute(k_sort_long, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                  8 * kLongSmem) == cudaSuccess;
-    if (!attr) return cuda_fail("cudaFuncSetAttribute(k_sort_long)", cudaGetLastError());
+    if (!sort_long_ready()) return cuda_fail("cudaFuncSetAttribute(k_sort_long)", cudaGetLastError());
     // 3 CTAs of 512 threads per SM (64 KB of keys each): parts of the cfg4 trajectory have
     // hundreds of long lists per view, each a ~55-stage network
     k_sort_long<<<148 * 3, 512, 8 * kLongSmem, s>>>(sp.rec, offsets, vals, gk,
@@ -2595,6 +2601,103 @@ gps_status gps_refine_step(gps_gaussians* g, gps_adam_state* state, const gps_vi
     GPS_CHECK_LAUNCH("k_adam");
   }
   state->step += 1;
+  return GPS_OK;
+}
+
+// gps_refine_round: n_iter gps_refine_step calls in one host call; with use_graph the round's
+// launches are captured once per call and replayed as one CUDA graph (the executable graph of
+// this workspace is updated in place when the round has the same launch structure as the last)
+namespace {
+// a ring of executable graphs per workspace: updating a graph whose last launch is still in flight
+// can stall the host until that launch completes, so a round updates the graph of three rounds ago
+constexpr int kRoundRing = 3;
+struct RoundGraph {
+  const void* ws;
+  cudaGraphExec_t exec[kRoundRing];
+  int next;
+};
+std::mutex g_round_mu;
+std::vector<RoundGraph> g_round_graphs;
+bool capturing(cudaStream_t s) {  // inside a caller's own capture the launches join that graph
+  cudaStreamCaptureStatus c = cudaStreamCaptureStatusNone;
+  return cudaStreamIsCapturing(s, &c) != cudaSuccess || c != cudaStreamCaptureStatusNone;
+}
+}  // namespace
+
+gps_status gps_refine_round(gps_gaussians* g, gps_adam_state* state, const gps_view* views, int32_t n_views,
+                            const int32_t* iter_views, int32_t views_per_iter, int32_t n_iter,
+                            const gps_render_config* rcfg, const gps_adam_config* acfg, void* ws, size_t ws_bytes,
+                            float* loss_out, int32_t use_graph, gps_stream_t stream) {
+  if (!g || !state || !views || n_views < 1 || !iter_views || views_per_iter < 1 || n_iter < 0)
+    return invalid("gps_refine_round: bad argument");
+  for (int64_t i = 0; i < (int64_t)n_iter * views_per_iter; ++i)
+    if (iter_views[i] < 0 || iter_views[i] >= n_views) return invalid("gps_refine_round: view index out of range");
+  if (n_iter == 0) return GPS_OK;
+  cudaStream_t s = as_stream(stream);
+  // capture needs a created stream; the event profiler's per-launch events stay outside graphs
+  const bool graph = use_graph != 0 && s != nullptr && s != cudaStreamLegacy && s != cudaStreamPerThread && !g_prof_on &&
+                     !capturing(s);
+  std::vector<gps_view> sel(views_per_iter);
+  const int64_t step0 = state->step;
+  if (graph) {
+    // the once-per-process setup (host-mapped flag allocation, kernel attributes) must not run
+    // inside a capture
+    if (!overflow_flag().host) return check_render_overflow("gps_refine_round");
+    if (!sort_long_ready()) return cuda_fail("cudaFuncSetAttribute(k_sort_long)", cudaGetLastError());
+    GPS_CHECK_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  }
+  gps_status st = GPS_OK;
+  for (int32_t i = 0; i < n_iter && st == GPS_OK; ++i) {
+    for (int32_t j = 0; j < views_per_iter; ++j) sel[j] = views[iter_views[(int64_t)i * views_per_iter + j]];
+    st = gps_refine_step(g, state, sel.data(), views_per_iter, rcfg, acfg, ws, ws_bytes, loss_out, nullptr, stream);
+  }
+  if (!graph) return st;
+  cudaGraph_t gr = nullptr;
+  const cudaError_t ec = cudaStreamEndCapture(s, &gr);
+  if (st != GPS_OK || ec != cudaSuccess) {  // nothing was launched
+    if (gr) cudaGraphDestroy(gr);
+    cudaGetLastError();
+    state->step = step0;
+    return st != GPS_OK ? st : cuda_fail("cudaStreamEndCapture", ec);
+  }
+  std::lock_guard<std::mutex> lock(g_round_mu);
+  RoundGraph* rg = nullptr;
+  for (RoundGraph& r : g_round_graphs)
+    if (r.ws == ws) rg = &r;
+  if (!rg) {
+    g_round_graphs.push_back(RoundGraph{ws, {}, 0});
+    rg = &g_round_graphs.back();
+  }
+  cudaGraphExec_t& exec = rg->exec[rg->next];
+  rg->next = (rg->next + 1) % kRoundRing;
+  if (exec) {
+    // same topology (same n_iter, views per iteration, configuration): parameters updated in
+    // place for future launches; else a new executable graph (an in-flight one is freed on completion)
+    cudaGraphExecUpdateResultInfo info;
+    if (cudaGraphExecUpdate(exec, gr, &info) != cudaSuccess) {
+      cudaGetLastError();
+      cudaGraphExecDestroy(exec);
+      exec = nullptr;
+    }
+  }
+  cudaError_t e = cudaSuccess;
+  static const bool verbose = getenv("GPS_GRAPH_VERBOSE") != nullptr;
+  if (!exec) {
+    e = cudaGraphInstantiate(&exec, gr, 0);
+    if (verbose) fprintf(stderr, "gps_refine_round: instantiated a graph of %d iterations (ws %p)\n", n_iter, ws);
+  }
+  cudaGraphDestroy(gr);
+  if (e != cudaSuccess) {
+    exec = nullptr;
+    state->step = step0;
+    return cuda_fail("cudaGraphInstantiate", e);
+  }
+  // the graph's kernels run at the priority of the stream it is launched into
+  e = cudaGraphLaunch(exec, s);
+  if (e != cudaSuccess) {
+    state->step = step0;
+    return cuda_fail("cudaGraphLaunch", e);
+  }
   return GPS_OK;
 }
 

@@ -37,8 +37,9 @@ class MappingPipeline:
                  overlap: bool = True, refine_priority: int = -1, manage_gaussians: bool = False,
                  add_cfg: A.AddConfig | None = None, remove_cfg: A.RemoveConfig | None = None,
                  all_views_per_iteration: bool = False, track: bool = False,
-                 icp_cfg: A.IcpConfig | None = None):
+                 icp_cfg: A.IcpConfig | None = None, graphs: bool = True):
         self.cam, self.g, self.vol = cam, gaussians, volume
+        self.graphs = graphs  # each refinement round as one CUDA graph (gps_refine_round)
         self.depth_scale = float(depth_scale)
         self.rcfg = render_cfg or A.RenderConfig()
         self.adam = adam_cfg or A.AdamConfig()
@@ -396,9 +397,13 @@ class MappingPipeline:
                 self._manage(rs, add_frame)
             self.last_view = views[-1]
             self.last_views = list(views)
-            for i in range(self.iterations):
-                vs = views if self.all_views else [views[Sch.view_for_iteration(i, len(views))]]
-                self.last_loss = self.ras.refine_step(self.g, self.state, vs, self.adam, stream=rs)
+            if self.all_views:
+                order = [list(range(len(views)))] * self.iterations
+            else:
+                order = [[Sch.view_for_iteration(i, len(views))] for i in range(self.iterations)]
+            # the round's iterations in one library call, replayed as one CUDA graph
+            self.last_loss = self.ras.refine_round(self.g, self.state, views, order, self.adam,
+                                                   graph=self.graphs, stream=rs)
             done = torch.cuda.Event()
             done.record(rs)
         if self.manage:

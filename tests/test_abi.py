@@ -19,7 +19,7 @@ def test_library_exports_every_declared_symbol():
     for s in N.declared_symbols():
         assert hasattr(lib, s), s
     assert set(N.PROTOTYPES) == set(N.declared_symbols())
-    assert lib.gps_abi_version() == 3
+    assert lib.gps_abi_version() == 4
     assert lib.gps_status_string(2) == b"GPS_ERR_OUT_OF_BLOCKS"
 
 

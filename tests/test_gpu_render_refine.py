@@ -464,3 +464,124 @@ def test_fused_chain_adam_matches_the_unfused_pair(deg, n, monkeypatch):
                 # the gradient's support is exact; m and v may underflow (denormal v) differently
                 assert j > 0 or (np.count_nonzero(b) > 0 and np.array_equal(a != 0, b != 0)), k
             assert np.max(np.abs(np.asarray(fl[1][k], np.float64) - fu[1][k])) <= 2 * lr[k], k
+
+
+def _round_views(G, cfg, frs, window):
+    """Views of frames frs through a (x0, y0, w, h) window of the camera (a crop: same rays)."""
+    x0, y0, w, h = window
+    cam = G.Camera(cfg.fx, cfg.fy, cfg.cx - x0, cfg.cy - y0, w, h)
+    views = []
+    for i, fr in enumerate(frs):
+        Dt, Ct = S.sdf_stage_inputs(cfg, fr, seed=11 + i)
+        tgt = S.target_rgba(cfg, fr)
+        crop = (slice(y0, y0 + h), slice(x0, x0 + w))
+        views.append(G.View(cam, fr.R, fr.t, torch.from_numpy(np.ascontiguousarray(Dt[crop])).cuda(),
+                            torch.from_numpy(np.ascontiguousarray(Ct[crop])).cuda(),
+                            tgt[crop].contiguous().cuda()))
+    return cam, views
+
+
+def _run_round(G, gd, cam, views, plan, mode, stream):
+    """plan: list of rounds, each a list of per-iteration view-index lists."""
+    g = G.Gaussians.from_dict(gd)
+    st = G.AdamState(g)
+    ras = G.Rasterizer(g.n, cam, G.RenderConfig())
+    losses = []
+    with torch.cuda.stream(stream):
+        for order in plan:
+            if mode.startswith("steps"):
+                for vi in order:
+                    ras.refine_step(g, st, [views[j] for j in vi], stream=stream)
+            else:
+                ras.refine_round(g, st, views, order, graph=(mode == "graph"), stream=stream)
+            torch.cuda.synchronize()
+            losses.append(ras.loss.item())
+    return st.step, losses, g.to_numpy(), st.m.to_numpy(), st.v.to_numpy()
+
+
+def test_refine_round_graph_is_bitwise_the_refine_steps():
+    """gps_refine_round (one call per round; use_graph: the round captured and replayed as one
+    CUDA graph, updated in place for the next round of the same shape, re-instantiated for a
+    round of another length) launches the same kernels in the same order as the per-iteration
+    gps_refine_step calls.  On a single 16x16 tile every Gaussian's 2D gradient arrives in one
+    atomic per view (deterministic), so the three schedules are compared bitwise: parameters,
+    moments, step counts and each round's last loss."""
+    import paper_2509_11574_b200 as G
+    cfg = S.get_config("cfg2")
+    frs = H.frames(cfg, 3, start=4)
+    cam, views = _round_views(G, cfg, frs, (312, 232, 16, 16))
+    gd = S.make_gaussians(cfg, n=3000, sh_degree=3)
+    plan = [[[i % 3] for i in range(7)], [[(i + 1) % 3] for i in range(7)], [[2], [0], [1]],
+            [[0], [0], [2]]]
+    s = torch.cuda.Stream()
+    res = {m: _run_round(G, gd, cam, views, plan, m, s) for m in ("steps", "steps2", "direct", "graph")}
+    ref = res["steps"]
+    assert ref[0] == 7 + 7 + 3 + 3 and all(l > 0 for l in ref[1])
+    for m in ("steps2", "direct", "graph"):  # steps2: the schedule is reproducible at all
+        r = res[m]
+        assert r[0] == ref[0] and r[1] == ref[1], m
+        for a, b in zip(r[2:], ref[2:]):
+            for k in GROUPS:
+                assert np.array_equal(a[k], b[k]), (m, k)
+    # the parameters did move (the window sees Gaussians)
+    g0 = G.Gaussians.from_dict(gd).to_numpy()
+    assert any(not np.array_equal(ref[2][k], g0[k]) for k in GROUPS)
+
+
+def test_refine_round_full_size_graph_matches_direct():
+    """The same at cfg4 size (3600 tiles; gradients arrive by fp32 atomics from many tiles, so
+    the two schedules agree to rounding): losses within 1e-5 relative, parameters within
+    2 lr per iteration."""
+    import paper_2509_11574_b200 as G
+    cfg = S.get_config("cfg4")
+    frs = H.frames(cfg, 2, start=30)
+    cam, views = _round_views(G, cfg, frs, (0, 0, cfg.width, cfg.height))
+    gd = S.make_gaussians(cfg, n=40000, sh_degree=3)
+    plan = [[[i % 2] for i in range(4)]] * 2
+    s = torch.cuda.Stream()
+    a = _run_round(G, gd, cam, views, plan, "graph", s)
+    b = _run_round(G, gd, cam, views, plan, "direct", s)
+    assert a[0] == b[0] == 8
+    assert np.allclose(a[1], b[1], rtol=1e-5, atol=0)
+    lr = {"xyz": 1.6e-4, "log_scale": 5e-3, "rot": 1e-3, "opacity_raw": 5e-2, "sh": 2.5e-3}
+    for k in GROUPS:
+        assert np.max(np.abs(np.asarray(a[2][k], np.float64) - b[2][k])) <= 2 * 8 * lr[k], k
+
+
+def test_refine_round_rejects_bad_view_index_and_keeps_state():
+    import paper_2509_11574_b200 as G
+    cfg = S.get_config("cfg2")
+    frs = H.frames(cfg, 1, start=4)
+    cam, views = _round_views(G, cfg, frs, (312, 232, 16, 16))
+    g = G.Gaussians.from_dict(S.make_gaussians(cfg, n=500))
+    st = G.AdamState(g)
+    ras = G.Rasterizer(g.n, cam, G.RenderConfig())
+    s = torch.cuda.Stream()
+    for graph in (True, False):
+        with pytest.raises(G._native.GPSError):
+            ras.refine_round(g, st, views, [[0], [1]], graph=graph, stream=s)
+        assert st.step == 0
+    ras.refine_round(g, st, views, [], graph=True, stream=s)  # an empty round is a no-op
+    assert st.step == 0
+
+
+def test_refine_round_graph_as_the_first_call_of_a_process():
+    """The library's once-per-process setup (the host-mapped overflow flag, kernel attributes)
+    happens before the capture even when a graph round is the process's first render call."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import torch, numpy as np, gps_synth as S, paper_2509_11574_b200 as G\n"
+        "from tests.test_gpu_render_refine import _round_views\n"
+        "cfg = S.get_config('cfg2'); frs = S.make_frames(cfg, 2, start=4, device='cpu')\n"
+        "cam, views = _round_views(G, cfg, frs, (0, 0, cfg.width, cfg.height))\n"
+        "g = G.Gaussians.from_dict(S.make_gaussians(cfg, n=5000)); st = G.AdamState(g)\n"
+        "ras = G.Rasterizer(g.n, cam, G.RenderConfig()); s = torch.cuda.Stream()\n"
+        "for r in range(3):\n"
+        "    ras.refine_round(g, st, views, [[0], [1], [0]], graph=True, stream=s)\n"
+        "torch.cuda.synchronize(); assert st.step == 9 and ras.loss.item() > 0\n"
+        "print('OK')\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and "OK" in out.stdout, out.stderr[-2000:]
