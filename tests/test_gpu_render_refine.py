@@ -485,8 +485,9 @@ def _run_round(G, gd, cam, views, plan, mode, stream):
     """plan: list of rounds, each a list of per-iteration view-index lists."""
     g = G.Gaussians.from_dict(gd)
     st = G.AdamState(g)
-    ras = G.Rasterizer(g.n, cam, G.RenderConfig())
+    ras = G.Rasterizer(g.n, cam, G.RenderConfig(), n_views=max(len(it) for r in plan for it in r))
     losses = []
+    stream.wait_stream(torch.cuda.current_stream())  # the parameters and moments are initialised
     with torch.cuda.stream(stream):
         for order in plan:
             if mode.startswith("steps"):
@@ -494,9 +495,11 @@ def _run_round(G, gd, cam, views, plan, mode, stream):
                     ras.refine_step(g, st, [views[j] for j in vi], stream=stream)
             else:
                 ras.refine_round(g, st, views, order, graph=(mode == "graph"), stream=stream)
-            torch.cuda.synchronize()
-            losses.append(ras.loss.item())
-    return st.step, losses, g.to_numpy(), st.m.to_numpy(), st.v.to_numpy()
+            # no synchronisation between rounds: a graph round may be updated while an earlier
+            # one is still in flight
+            losses.append(ras.loss.clone())
+    torch.cuda.synchronize()
+    return st.step, [x.item() for x in losses], g.to_numpy(), st.m.to_numpy(), st.v.to_numpy()
 
 
 def test_refine_round_graph_is_bitwise_the_refine_steps():
@@ -512,17 +515,24 @@ def test_refine_round_graph_is_bitwise_the_refine_steps():
     cam, views = _round_views(G, cfg, frs, (312, 232, 16, 16))
     gd = S.make_gaussians(cfg, n=3000, sh_degree=3)
     plan = [[[i % 3] for i in range(7)], [[(i + 1) % 3] for i in range(7)], [[2], [0], [1]],
-            [[0], [0], [2]]]
+            [[0], [0], [2]], [[1], [2], [0]], [[i % 3] for i in range(7)], [[2], [2], [1]]]
     s = torch.cuda.Stream()
     res = {m: _run_round(G, gd, cam, views, plan, m, s) for m in ("steps", "steps2", "direct", "graph")}
     ref = res["steps"]
-    assert ref[0] == 7 + 7 + 3 + 3 and all(l > 0 for l in ref[1])
+    assert ref[0] == 7 + 7 + 3 + 3 + 3 + 7 + 3 and all(l > 0 for l in ref[1])
     for m in ("steps2", "direct", "graph"):  # steps2: the schedule is reproducible at all
         r = res[m]
         assert r[0] == ref[0] and r[1] == ref[1], m
         for a, b in zip(r[2:], ref[2:]):
             for k in GROUPS:
                 assert np.array_equal(a[k], b[k]), (m, k)
+    # several views per iteration (the all-views variant: gradients summed, k_chain + k_adam)
+    plan2 = [[[0, 1], [1, 2], [2, 0]], [[1, 2], [0, 1], [0, 2]]]
+    r2 = {m: _run_round(G, gd, cam, views, plan2, m, s) for m in ("steps", "graph")}
+    assert r2["graph"][0] == r2["steps"][0] == 6 and r2["graph"][1] == r2["steps"][1]
+    for a, b in zip(r2["graph"][2:], r2["steps"][2:]):
+        for k in GROUPS:
+            assert np.array_equal(a[k], b[k]), ("multi-view", k)
     # the parameters did move (the window sees Gaussians)
     g0 = G.Gaussians.from_dict(gd).to_numpy()
     assert any(not np.array_equal(ref[2][k], g0[k]) for k in GROUPS)
