@@ -54,6 +54,8 @@ def parse():
                     help="ICP tracking of every frame (Eq. 5, NEXT-3) instead of the given poses")
     ap.add_argument("--all-views", action="store_true",
                     help="every iteration renders all the round's views (SPEC S:471 variant, NEXT-4)")
+    ap.add_argument("--frames-ahead", type=int, default=0,
+                    help="the host enqueues at most this many frames ahead of the fusion stream (0: unbounded)")
     ap.add_argument("--no-graphs", action="store_true",
                     help="launch each refinement iteration directly instead of one CUDA graph per round")
     ap.add_argument("--no-overlap", action="store_true",
@@ -214,7 +216,8 @@ def run_ours(args):
     pipe = MappingPipeline(cam, g, vol, cfg.depth_scale, rcfg, seed=rank,
                            overlap=not args.no_overlap, refine_priority=args.refine_priority,
                            manage_gaussians=args.manage_gaussians, all_views_per_iteration=args.all_views,
-                           track=args.track, graphs=not args.no_graphs)
+                           track=args.track, graphs=not args.no_graphs,
+                           max_frames_ahead=args.frames_ahead)
     ate = []  # the timed frames (their tracked poses are compared with the truth after timing)
     k = 0
     for _ in range(args.history):  # build a steady-state volume (untimed, no rounds)
@@ -556,6 +559,7 @@ def workload_config(args, cfg, n_g, ws):
             "parallelism": f"replicas x{ws} (independent sequences)",
             "streams": "fusion+raycast on one stream, refinement rounds on a second (P:116)"
                        if not args.no_overlap else "one stream (serial schedule)",
+            "frames_ahead": args.frames_ahead,
             "round_graphs": "each round's 20 iterations one CUDA graph (gps_refine_round)"
                             if not args.no_graphs else "off (one gps_refine_step call per iteration)",
             "l2": "inputs larger than L2 (per-step state > 126 MB: params+Adam 283 MB, volume)",

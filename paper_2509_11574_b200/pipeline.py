@@ -10,6 +10,7 @@ end-to-end path).
 """
 from __future__ import annotations
 
+import collections
 import ctypes as C
 import dataclasses
 
@@ -37,9 +38,13 @@ class MappingPipeline:
                  overlap: bool = True, refine_priority: int = -1, manage_gaussians: bool = False,
                  add_cfg: A.AddConfig | None = None, remove_cfg: A.RemoveConfig | None = None,
                  all_views_per_iteration: bool = False, track: bool = False,
-                 icp_cfg: A.IcpConfig | None = None, graphs: bool = True):
+                 icp_cfg: A.IcpConfig | None = None, graphs: bool = True, max_frames_ahead: int = 0):
         self.cam, self.g, self.vol = cam, gaussians, volume
         self.graphs = graphs  # each refinement round as one CUDA graph (gps_refine_round)
+        # the host enqueues at most max_frames_ahead frames beyond the device's fusion stream (0:
+        # unbounded): bounds the frames in flight, so the caching allocator stops growing
+        self.max_ahead = max_frames_ahead
+        self._inflight = collections.deque()
         self.depth_scale = float(depth_scale)
         self.rcfg = render_cfg or A.RenderConfig()
         self.adam = adam_cfg or A.AdamConfig()
@@ -157,6 +162,8 @@ class MappingPipeline:
                       prefetch=None):
         """One frame of the mapping step.  `prefetch`: the next frame's (depth, rgba) host tensors,
         whose upload then overlaps this frame's kernels."""
+        if self.max_ahead and len(self._inflight) >= self.max_ahead:
+            self._inflight.popleft().synchronize()
         depth = self._device(depth)
         rgba = self._device(rgba)
         if prefetch is not None:
@@ -212,6 +219,10 @@ class MappingPipeline:
             self.interval = []
         if not self._pending:
             self._drop_frames()
+        if self.max_ahead:
+            ev = torch.cuda.Event()
+            ev.record(torch.cuda.current_stream())
+            self._inflight.append(ev)
         return is_kf
 
     def _drop_frames(self):
