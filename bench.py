@@ -56,6 +56,8 @@ def parse():
                     help="every iteration renders all the round's views (SPEC S:471 variant, NEXT-4)")
     ap.add_argument("--frames-ahead", type=int, default=0,
                     help="the host enqueues at most this many frames ahead of the fusion stream (0: unbounded)")
+    ap.add_argument("--no-frame-graphs", action="store_true",
+                    help="launch each frame's fuse + raycast directly (the rounds stay graphs unless --no-graphs)")
     ap.add_argument("--no-graphs", action="store_true",
                     help="launch each refinement iteration directly instead of one CUDA graph per round")
     ap.add_argument("--no-overlap", action="store_true",
@@ -177,6 +179,9 @@ def run_ours(args):
     torch.cuda.set_device(local)
     if ws > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    # the fusion work runs on a created stream (stream capture, hence the per-frame CUDA graphs of
+    # gps_fuse_raycast, is not possible on the legacy default stream)
+    torch.cuda.set_stream(torch.cuda.Stream())
     import gps_synth as S
     import paper_2509_11574_b200 as G
     from paper_2509_11574_b200 import _native as N
@@ -217,7 +222,8 @@ def run_ours(args):
                            overlap=not args.no_overlap, refine_priority=args.refine_priority,
                            manage_gaussians=args.manage_gaussians, all_views_per_iteration=args.all_views,
                            track=args.track, graphs=not args.no_graphs,
-                           max_frames_ahead=args.frames_ahead)
+                           max_frames_ahead=args.frames_ahead,
+                           frame_graphs=not (args.no_graphs or args.no_frame_graphs))
     ate = []  # the timed frames (their tracked poses are compared with the truth after timing)
     k = 0
     for _ in range(args.history):  # build a steady-state volume (untimed, no rounds)
@@ -562,6 +568,8 @@ def workload_config(args, cfg, n_g, ws):
             "frames_ahead": args.frames_ahead,
             "round_graphs": "each round's 20 iterations one CUDA graph (gps_refine_round)"
                             if not args.no_graphs else "off (one gps_refine_step call per iteration)",
+            "frame_graphs": "each frame's fuse + raycast one CUDA graph (gps_fuse_raycast)"
+                            if not (args.no_graphs or args.no_frame_graphs) else "off",
             "l2": "inputs larger than L2 (per-step state > 126 MB: params+Adam 283 MB, volume)",
             "dense_grid": {"none": "off (hash lookups only)",
                            "workspace": f"{args.workspace_m} m cube centred on the first camera position "

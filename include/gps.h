@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define GPS_ABI_VERSION 4  /* 2: gps_render_config.sort_free; adding, removal, tracking entry points; 3: device-pose forms; 4: gps_refine_round */
+#define GPS_ABI_VERSION 4  /* 2: gps_render_config.sort_free; adding, removal, tracking entry points; 3: device-pose forms; 4: gps_refine_round, gps_fuse_raycast */
 
 typedef void* gps_stream_t; /* a cudaStream_t */
 
@@ -149,6 +149,18 @@ gps_status gps_fuse(gps_volume* vol, const gps_intrinsics* K /*host*/, const gps
 gps_status gps_raycast(gps_volume* vol, const gps_intrinsics* K /*host*/,
                        const gps_pose* T /*host*/, float* depth_out, float* color_out,
                        float* vertex_out, gps_stream_t stream);
+
+/* gps_fuse_raycast -- gps_fuse of a frame followed by gps_raycast from the same pose (each
+ * frame is fused, then raycast), in one call; same kernels, same order, same results as the two
+ * calls.  use_graph != 0: the frame's launches are stream-captured and replayed as one CUDA graph
+ * (one ring of executable graphs per volume, updated in place; skipped on the legacy/per-thread
+ * default streams, inside a caller's own capture and while the event profiler is enabled).
+ * Arguments and errors as gps_fuse and gps_raycast; on an error nothing is launched (with
+ * use_graph; without it, a failing raycast leaves the fuse enqueued).                        */
+gps_status gps_fuse_raycast(gps_volume* vol, const gps_intrinsics* K /*host*/, const gps_pose* T /*host*/,
+                            const uint16_t* depth, float depth_scale, const uint8_t* rgba,
+                            float* depth_out, float* color_out, float* vertex_out /*nullable*/,
+                            int32_t use_graph, gps_stream_t stream);
 
 /* Device-pose forms (tracking): identical to gps_fuse / gps_raycast --
  * same kernels, same fp32 sequences, same results for the same pose values -- except that the

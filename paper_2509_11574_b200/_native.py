@@ -99,6 +99,8 @@ PROTOTYPES = {
     "gps_volume_stats_sync": (gps_status, [vp, gps_stream_t, P(i64), P(i64), P(i64), P(i64), P(i64)]),
     "gps_fuse": (gps_status, [vp, P(gps_intrinsics), P(gps_pose), vp, f32, vp, gps_stream_t]),
     "gps_raycast": (gps_status, [vp, P(gps_intrinsics), P(gps_pose), vp, vp, vp, gps_stream_t]),
+    "gps_fuse_raycast": (gps_status, [vp, P(gps_intrinsics), P(gps_pose), vp, f32, vp, vp, vp, vp, i32,
+                                      gps_stream_t]),
     "gps_fuse_dpose": (gps_status, [vp, P(gps_intrinsics), vp, vp, f32, vp, gps_stream_t]),
     "gps_raycast_dpose": (gps_status, [vp, P(gps_intrinsics), vp, vp, vp, vp, gps_stream_t]),
     "gps_render_workspace_size": (sz, [i64, P(gps_intrinsics), P(gps_render_config)]),

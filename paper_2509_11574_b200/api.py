@@ -176,6 +176,19 @@ class Volume:
                                               _stream(stream)))
         return depth_out, color_out, vertex_out
 
+    def fuse_raycast(self, cam: Camera, R, t, depth: torch.Tensor, depth_scale: float, rgba: torch.Tensor,
+                     depth_out, color_out, vertex_out=None, graph: bool = True, stream=None):
+        """gps_fuse_raycast: fuse the frame, then raycast it from the same pose, in one call (one
+        CUDA graph with graph=True on a created stream).  Device frames only."""
+        assert depth.is_cuda and rgba.is_cuda
+        assert depth.element_size() == 2 and depth.numel() == cam.width * cam.height
+        assert rgba.dtype == torch.uint8 and rgba.numel() == 4 * cam.width * cam.height
+        N.check("gps_fuse_raycast",
+                _L.gps_fuse_raycast(self.h, C.byref(cam.c()), C.byref(pose_struct(R, t)), _ptr(depth),
+                                    float(depth_scale), _ptr(rgba), _ptr(depth_out), _ptr(color_out),
+                                    _ptr(vertex_out), int(graph), _stream(stream)))
+        return depth_out, color_out, vertex_out
+
     def stats(self, stream=None):
         nb, bud, nv, vt, ut = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
         st = _L.gps_volume_stats_sync(self.h, _stream(stream), C.byref(nb), C.byref(bud), C.byref(nv), C.byref(vt),

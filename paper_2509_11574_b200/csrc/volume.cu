@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #define GPS_CHK_VAR g_chk_volume
@@ -1640,6 +1641,14 @@ gps_status gps_fuse_dpose(gps_volume* vol, const gps_intrinsics* K, const gps_po
   return fuse_impl(vol, K, nullptr, T_dev, depth, depth_scale, rgba, stream, "gps_fuse_dpose");
 }
 
+static bool range_smem_ready() {  // once per process (before any stream capture: gps_fuse_raycast)
+  static const bool ok = cudaFuncSetAttribute(k_range_smem<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              8 * kRangeSmemTiles) == cudaSuccess &&
+                         cudaFuncSetAttribute(k_range_smem<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              8 * kRangeSmemTiles) == cudaSuccess;
+  return ok;
+}
+
 static gps_status raycast_impl(const gps_volume* vol, const gps_intrinsics* K, const gps_pose* T, float* depth_out,
                                float* color_out, float* vertex_out, uint32_t* footprint, gps_stream_t stream,
                                const gps_pose* dT = nullptr) {
@@ -1676,11 +1685,7 @@ static gps_status raycast_impl(const gps_volume* vol, const gps_intrinsics* K, c
       const bool global_range = getenv("GPS_RANGE_GLOBAL") != nullptr;  // A/B and the test: global atomics only
       const size_t smem = 8 * (size_t)ntiles;
       if (ntiles <= kRangeSmemTiles && !global_range) {
-        static const bool attr = cudaFuncSetAttribute(k_range_smem<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                      8 * kRangeSmemTiles) == cudaSuccess &&
-                                 cudaFuncSetAttribute(k_range_smem<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                      8 * kRangeSmemTiles) == cudaSuccess;
-        if (!attr) return cuda_fail("cudaFuncSetAttribute(k_range_smem)", cudaGetLastError());
+        if (!range_smem_ready()) return cuda_fail("cudaFuncSetAttribute(k_range_smem)", cudaGetLastError());
         if (dT)
           k_range_smem<true><<<148 * 2, 512, smem, s>>>(v->view, p, tmin, tmax, (int)g.x, (int)g.y);
         else
@@ -1728,6 +1733,80 @@ gps_status gps_raycast_dpose(gps_volume* vol, const gps_intrinsics* K, const gps
   gps_status st = check_sticky(vol);
   if (st != GPS_OK) return st;
   return raycast_impl(vol, K, nullptr, depth_out, color_out, vertex_out, nullptr, stream, T_dev);
+}
+
+// gps_fuse_raycast: gps_fuse then gps_raycast of the same frame in one call; with use_graph the
+// frame's launches are captured and replayed as one CUDA graph (a ring of executable graphs per
+// volume, updated in place: see gps_refine_round in render.cu)
+namespace {
+constexpr int kFrameRing = 3;
+struct FrameGraph {
+  const void* vol;
+  cudaGraphExec_t exec[kFrameRing];
+  int next;
+};
+std::mutex g_frame_mu;
+std::vector<FrameGraph> g_frame_graphs;
+}  // namespace
+
+gps_status gps_fuse_raycast(gps_volume* vol, const gps_intrinsics* K, const gps_pose* T, const uint16_t* depth,
+                            float depth_scale, const uint8_t* rgba, float* depth_out, float* color_out,
+                            float* vertex_out, int32_t use_graph, gps_stream_t stream) {
+  if (!vol || !T || !depth_out || !color_out) return invalid("gps_fuse_raycast: null argument");
+  if (!valid_intrinsics(K)) return invalid("gps_fuse_raycast: bad intrinsics");
+  cudaStream_t s = as_stream(stream);
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  const bool graph = use_graph != 0 && s != nullptr && s != cudaStreamLegacy && s != cudaStreamPerThread &&
+                     !g_prof_on && cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone;
+  VolumeImpl* v = static_cast<VolumeImpl*>(vol);
+  const uint32_t frame0 = v->frame;
+  if (graph) {
+    if (!range_smem_ready()) return cuda_fail("cudaFuncSetAttribute(k_range_smem)", cudaGetLastError());
+    GPS_CHECK_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  }
+  gps_status st = fuse_impl(vol, K, T, nullptr, depth, depth_scale, rgba, stream, "gps_fuse_raycast");
+  if (st == GPS_OK) st = raycast_impl(vol, K, T, depth_out, color_out, vertex_out, nullptr, stream);
+  if (!graph) return st;
+  cudaGraph_t gr = nullptr;
+  const cudaError_t ec = cudaStreamEndCapture(s, &gr);
+  if (st != GPS_OK || ec != cudaSuccess) {  // nothing was launched
+    if (gr) cudaGraphDestroy(gr);
+    cudaGetLastError();
+    v->frame = frame0;
+    return st != GPS_OK ? st : cuda_fail("cudaStreamEndCapture", ec);
+  }
+  std::lock_guard<std::mutex> lock(g_frame_mu);
+  FrameGraph* fg = nullptr;
+  for (FrameGraph& f : g_frame_graphs)
+    if (f.vol == vol) fg = &f;
+  if (!fg) {
+    g_frame_graphs.push_back(FrameGraph{vol, {}, 0});
+    fg = &g_frame_graphs.back();
+  }
+  cudaGraphExec_t& exec = fg->exec[fg->next];
+  fg->next = (fg->next + 1) % kFrameRing;
+  if (exec) {
+    cudaGraphExecUpdateResultInfo info;
+    if (cudaGraphExecUpdate(exec, gr, &info) != cudaSuccess) {
+      cudaGetLastError();
+      cudaGraphExecDestroy(exec);
+      exec = nullptr;
+    }
+  }
+  cudaError_t e = cudaSuccess;
+  if (!exec) e = cudaGraphInstantiate(&exec, gr, 0);
+  cudaGraphDestroy(gr);
+  if (e != cudaSuccess) {
+    exec = nullptr;
+    v->frame = frame0;
+    return cuda_fail("cudaGraphInstantiate", e);
+  }
+  e = cudaGraphLaunch(exec, s);
+  if (e != cudaSuccess) {
+    v->frame = frame0;
+    return cuda_fail("cudaGraphLaunch", e);
+  }
+  return GPS_OK;
 }
 
 gps_status gps_debug_apron_check_sync(const gps_volume* vol, gps_stream_t stream, int64_t* n_bad) {

@@ -38,9 +38,12 @@ class MappingPipeline:
                  overlap: bool = True, refine_priority: int = -1, manage_gaussians: bool = False,
                  add_cfg: A.AddConfig | None = None, remove_cfg: A.RemoveConfig | None = None,
                  all_views_per_iteration: bool = False, track: bool = False,
-                 icp_cfg: A.IcpConfig | None = None, graphs: bool = True, max_frames_ahead: int = 0):
+                 icp_cfg: A.IcpConfig | None = None, graphs: bool = True, max_frames_ahead: int = 0,
+                 frame_graphs: bool | None = None):
         self.cam, self.g, self.vol = cam, gaussians, volume
         self.graphs = graphs  # each refinement round as one CUDA graph (gps_refine_round)
+        # each frame's fuse + raycast as one CUDA graph (gps_fuse_raycast; default: as `graphs`)
+        self.frame_graphs = graphs if frame_graphs is None else frame_graphs
         # the host enqueues at most max_frames_ahead frames beyond the device's fusion stream (0:
         # unbounded): bounds the frames in flight, so the caching allocator stops growing
         self.max_ahead = max_frames_ahead
@@ -179,7 +182,7 @@ class MappingPipeline:
             is_kf = None  # decided when the pose is read back (_resolve)
             self.frames[k] = (rgba, None, None)
         else:
-            self.vol.fuse(self.cam, R, t, depth, self.depth_scale, rgba)
+            # fused together with its raycast below (gps_fuse_raycast: one CUDA graph per frame)
             self._last_pose = (np.asarray(R, np.float32), np.asarray(t, np.float32))
             is_kf = self.kf.offer(k, R, t)
             self.frames[k] = (rgba, np.asarray(R, np.float32), np.asarray(t, np.float32))
@@ -210,7 +213,8 @@ class MappingPipeline:
             A.vertex_normals_dpose(self.cam, dpose, self.depth, vert, nrm)
             self._model = (vert, nrm)
         else:
-            self.vol.raycast(self.cam, R, t, self.depth, self.color, vertex_out=vert)
+            self.vol.fuse_raycast(self.cam, R, t, depth, self.depth_scale, rgba, self.depth, self.color,
+                                  vertex_out=vert, graph=self.frame_graphs)
             if want_v:
                 A.vertex_normals(self.cam, R, t, self.depth, self.vertex[s], out=self.normal[s])
         if round_now:

@@ -201,3 +201,42 @@ def test_shared_memory_range_image_changes_nothing(monkeypatch):
         D1, C1, V1 = vol.raycast(gcam, R, t, want_vertex=True)
         assert int((D0 > 0).sum()) > 100000
         assert torch.equal(D0, D1) and torch.equal(C0, C1) and torch.equal(V0, V1)
+
+
+def test_fuse_raycast_graph_is_bitwise_the_two_calls():
+    """gps_fuse_raycast (the frame's fuse then its raycast in one call; use_graph: captured and
+    replayed as one CUDA graph, a ring of executable graphs per volume updated in place) gives
+    the volume and the maps of gps_fuse + gps_raycast bitwise (cfg2, 8 frames, no synchronisation
+    between frames, vertex map on every other frame so the graph topology changes)."""
+    cfg = S.get_config("cfg2")
+    frs = H.frames(cfg, 8)
+    gcam, _ = H.cams(cfg)
+    dev = [H.to_dev(fr) for fr in frs]
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    out = {}
+    for mode in ("calls", "direct", "graph"):
+        vol = H.gpu_volume(cfg)
+        maps = []
+        with torch.cuda.stream(s):
+            for i, (fr, (d, c)) in enumerate(zip(frs, dev)):
+                D = torch.empty((cfg.height, cfg.width), device="cuda")
+                C = torch.empty((cfg.height, cfg.width, 3), device="cuda")
+                V = torch.empty((cfg.height, cfg.width, 3), device="cuda") if i % 2 else None
+                if mode == "calls":
+                    vol.fuse(gcam, fr.R, fr.t, d, cfg.depth_scale, c, stream=s)
+                    vol.raycast(gcam, fr.R, fr.t, D, C, vertex_out=V, stream=s)
+                else:
+                    vol.fuse_raycast(gcam, fr.R, fr.t, d, cfg.depth_scale, c, D, C, vertex_out=V,
+                                     graph=(mode == "graph"), stream=s)
+                maps.append((D, C, V))
+        torch.cuda.synchronize()
+        out[mode] = (H.sorted_blocks(*vol.export_blocks()), maps)
+    (c0, v0), m0 = out["calls"]
+    assert int((m0[-1][0] > 0).sum()) > 100000
+    for mode in ("direct", "graph"):
+        (c1, v1), m1 = out[mode]
+        assert np.array_equal(c0, c1) and np.array_equal(v0.view(np.uint8), v1.view(np.uint8)), mode
+        for a, b in zip(m0, m1):
+            for x, y in zip(a, b):
+                assert (x is None and y is None) or torch.equal(x, y), mode
