@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--no-profile", action="store_true", help="time without the per-launch event profiler")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--refine-priority", type=int, default=-1, help="CUDA stream priority of the refinement stream")
+    ap.add_argument("--fusion-priority", type=int, default=0, help="CUDA stream priority of the fusion stream")
     ap.add_argument("--manage-gaussians", action="store_true",
                     help="Gaussian adding (Eq. 6) and removal (Eq. 8) every round (NEXT-2)")
     ap.add_argument("--track", action="store_true",
@@ -181,7 +182,7 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     # the fusion work runs on a created stream (stream capture, hence the per-frame CUDA graphs of
     # gps_fuse_raycast, is not possible on the legacy default stream)
-    torch.cuda.set_stream(torch.cuda.Stream())
+    torch.cuda.set_stream(torch.cuda.Stream(priority=args.fusion_priority))
     import gps_synth as S
     import paper_2509_11574_b200 as G
     from paper_2509_11574_b200 import _native as N
