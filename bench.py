@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--refine-priority", type=int, default=-1, help="CUDA stream priority of the refinement stream")
     ap.add_argument("--fusion-priority", type=int, default=0, help="CUDA stream priority of the fusion stream")
+    ap.add_argument("--view-priority", type=int, default=None,
+                    help="run the round's view raycasts on a third stream of this priority (default: the fusion stream)")
     ap.add_argument("--manage-gaussians", action="store_true",
                     help="Gaussian adding (Eq. 6) and removal (Eq. 8) every round (NEXT-2)")
     ap.add_argument("--track", action="store_true",
@@ -224,7 +226,8 @@ def run_ours(args):
                            manage_gaussians=args.manage_gaussians, all_views_per_iteration=args.all_views,
                            track=args.track, graphs=not args.no_graphs,
                            max_frames_ahead=args.frames_ahead,
-                           frame_graphs=not (args.no_graphs or args.no_frame_graphs))
+                           frame_graphs=not (args.no_graphs or args.no_frame_graphs),
+                           view_priority=args.view_priority)
     ate = []  # the timed frames (their tracked poses are compared with the truth after timing)
     k = 0
     for _ in range(args.history):  # build a steady-state volume (untimed, no rounds)

@@ -11,6 +11,7 @@ end-to-end path).
 from __future__ import annotations
 
 import collections
+import contextlib
 import ctypes as C
 import dataclasses
 
@@ -39,7 +40,7 @@ class MappingPipeline:
                  add_cfg: A.AddConfig | None = None, remove_cfg: A.RemoveConfig | None = None,
                  all_views_per_iteration: bool = False, track: bool = False,
                  icp_cfg: A.IcpConfig | None = None, graphs: bool = True, max_frames_ahead: int = 0,
-                 frame_graphs: bool | None = None):
+                 frame_graphs: bool | None = None, view_priority: int | None = None):
         self.cam, self.g, self.vol = cam, gaussians, volume
         self.graphs = graphs  # each refinement round as one CUDA graph (gps_refine_round)
         # each frame's fuse + raycast as one CUDA graph (gps_fuse_raycast; default: as `graphs`)
@@ -123,6 +124,9 @@ class MappingPipeline:
         # the refinement rounds are the longer of the two streams' work: give them the higher
         # scheduling priority so fusion and raycasts fill the SMs around them
         self.refine_stream = torch.cuda.Stream(priority=refine_priority)
+        # view_priority: the round's view raycasts on a third stream of that priority (ordered after
+        # the round frame's fusion; the next frames' fusion waits for them), else on the fusion stream
+        self.view_stream = torch.cuda.Stream(priority=view_priority) if view_priority is not None else None
         self._set_free = [None] * nsets   # event: the refinement that last read buffer set s is done
         self._refine_done = None
         self.rounds = 0
@@ -387,14 +391,21 @@ class MappingPipeline:
     def _refine_round(self, views_ids, reuse_last: bool = True, add_frame=None):
         s = self.rounds % len(self.view_depth)
         views = []
-        for j, f in enumerate(views_ids):
-            rgba, R, t = self.frames[f]
-            if reuse_last and f == self.last_frame:
-                # the frame just fused was raycast against this very volume: same result
-                views.append(A.View(self.cam, R, t, self.depth, self.color, rgba))
-                continue
-            self.vol.raycast(self.cam, R, t, self.view_depth[s][j], self.view_color[s][j])
-            views.append(A.View(self.cam, R, t, self.view_depth[s][j], self.view_color[s][j], rgba))
+        cur = torch.cuda.current_stream()
+        vs = self.view_stream if self.overlap else None
+        if vs is not None:
+            vs.wait_stream(cur)  # after the round frame's fusion
+        with torch.cuda.stream(vs) if vs is not None else contextlib.nullcontext():
+            for j, f in enumerate(views_ids):
+                rgba, R, t = self.frames[f]
+                if reuse_last and f == self.last_frame:
+                    # the frame just fused was raycast against this very volume: same result
+                    views.append(A.View(self.cam, R, t, self.depth, self.color, rgba))
+                    continue
+                self.vol.raycast(self.cam, R, t, self.view_depth[s][j], self.view_color[s][j])
+                views.append(A.View(self.cam, R, t, self.view_depth[s][j], self.view_color[s][j], rgba))
+        if vs is not None:
+            cur.wait_stream(vs)  # the next frames' fusion writes the volume the raycasts read
         if self.overlap:
             ready = torch.cuda.Event()
             ready.record(torch.cuda.current_stream())
