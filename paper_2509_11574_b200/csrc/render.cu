@@ -1418,13 +1418,13 @@ __global__ void __launch_bounds__(256) k_backward(RenderArgs a, const float4* __
   if (threadIdx.x <= TILE) smagic[threadIdx.x] = threadIdx.x ? (65536u + threadIdx.x - 1u) / threadIdx.x : 0u;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   // the lane that ends up holding each reduced value (reduce-scatter below), and which value
-  int vidx;
+  int vidx;  // within the lane's half-warp (levels xor 8, 4, 2, 1 below)
   {
-    const int b4 = (lane >> 4) & 1, b3 = (lane >> 3) & 1, b2 = (lane >> 2) & 1, b1 = (lane >> 1) & 1;
-    const int kc = b1;
-    const int kb = b2 ? (2 + kc < 3 ? 2 + kc : -1) : kc;
-    const int ka = kb < 0 ? -1 : (b3 ? (3 + kb < 5 ? 3 + kb : -1) : kb);
-    vidx = (ka < 0 || (lane & 1)) ? -1 : (b4 ? (ka < 4 ? 5 + ka : -1) : ka);
+    const int b3 = (lane >> 3) & 1, b2 = (lane >> 2) & 1, b1 = (lane >> 1) & 1, b0 = lane & 1;
+    const int kc = b0;
+    const int kb = b1 ? (2 + kc < 3 ? 2 + kc : -1) : kc;
+    const int ka = kb < 0 ? -1 : (b2 ? (3 + kb < 5 ? 3 + kb : -1) : kb);
+    vidx = ka < 0 ? -1 : (b3 ? (ka < 4 ? 5 + ka : -1) : ka);
   }
   __shared__ float4 se0[256], se1[256], se2[256], se3[256];
   __shared__ uint32_t sidx[256];
@@ -1470,22 +1470,27 @@ __global__ void __launch_bounds__(256) k_backward(RenderArgs a, const float4* __
       se3[j] = make_float4(q3.x, q3.y, q1.w, q2.w);  // exact offsets, packed rect x / y ranges
     }
     __syncthreads();
-  for (int j = warp; j < cnt_e; j += nw) {
-    const uint32_t idx = sidx[j];
-    const float4 r0 = se0[j], r1 = se1[j], r2 = se2[j], r3 = se3[j];
+  // a half-warp per list entry: the two entries of a warp share its setup and reduction
+  // instructions (small footprints leave most of a full warp idle)
+  for (int jb = 2 * warp; jb < cnt_e; jb += 2 * nw) {
+    const int j = jb + (lane >> 4);
+    const bool valid = j < cnt_e;
+    const int jj = valid ? j : jb;
+    const uint32_t idx = sidx[jj];
+    const float4 r0 = se0[jj], r1 = se1[jj], r2 = se2[jj], r3 = se3[jj];
     const float b2 = pmul(2.0f, r0.w), qmax = r1.w;
     const float sig = r2.w;
     const uint32_t rx = __float_as_uint(r3.z), ry = __float_as_uint(r3.w);
     const int x0 = max((int)(rx & 0xFFFF), tx0), x1 = min((int)(rx >> 16), tx0 + TILE - 1);
     const int y0 = max((int)(ry & 0xFFFF), ty0), y1 = min((int)(ry >> 16), ty0 + TILE - 1);
-    const int wx = x1 - x0 + 1, cnt = wx * (y1 - y0 + 1);
+    const int wx = x1 - x0 + 1, cnt = valid ? wx * (y1 - y0 + 1) : 0;
     // k / wx for k < 256, wx <= 16 as a multiply-high (exact; tests/test_abi.py)
     const uint32_t magic = smagic[wx];
     float acc[9];
 #pragma unroll
     for (int k = 0; k < 9; ++k) acc[k] = 0.f;
     bool any = false;
-    for (int k = lane; k < cnt; k += 32) {
+    for (int k = lane & 15; k < cnt; k += 16) {
       const int row = (int)(((uint32_t)k * magic) >> 16);
       const int x = x0 + (k - row * wx), y = y0 + row;
       const int p = (y - ty0) * TILE + (x - tx0);
@@ -1513,16 +1518,16 @@ __global__ void __launch_bounds__(256) k_backward(RenderArgs a, const float4* __
       acc[8] = fmaf(gA2, al, acc[8]);
       any = true;
     }
-    if (!__any_sync(0xFFFFFFFFu, any)) continue;
-    // warp reduce-scatter: 12 shuffles instead of 45; value k ends on one even lane
+    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, any);
+    if (!bal) continue;
+    // half-warp reduce-scatter: 12 shuffles for the two entries; value k ends on one lane
     float l1[5], l2[3], l3[2], l4[1];
-    rs_level<9, 5>(acc, l1, lane, 16);
-    rs_level<5, 3>(l1, l2, lane, 8);
-    rs_level<3, 2>(l2, l3, lane, 4);
-    rs_level<2, 1>(l3, l4, lane, 2);
-    const float tot = l4[0] + __shfl_xor_sync(0xFFFFFFFFu, l4[0], 1);
+    rs_level<9, 5>(acc, l1, lane, 8);
+    rs_level<5, 3>(l1, l2, lane, 4);
+    rs_level<3, 2>(l2, l3, lane, 2);
+    rs_level<2, 1>(l3, l4, lane, 1);
     // 2D gradient slot layout: [px, py, a, b | c, sigma, r, g | b, flag, -, -]
-    if (vidx >= 0) atomicAdd(grad2d + 12 * (size_t)idx + vidx, tot);
+    if (vidx >= 0 && ((bal >> (lane & 16)) & 0xFFFFu)) atomicAdd(grad2d + 12 * (size_t)idx + vidx, l4[0]);
   }
   }
 }
