@@ -14,9 +14,9 @@
 //   k_sort_blend  one CTA per tile: sort the bucket by (depth bits, index) in shared memory,
 //                 front-to-back blend with early termination at the SDF depth, composite,
 //                 fused L1 partials; the last CTA finalises the loss deterministically
-//   k_backward    one CTA per tile: a warp per list entry walks the entry's footprint inside the
-//                 tile, accumulates the 9 2D gradients in registers, warp-reduces, and issues
-//                 three vector reductions (red.global.add.v4.f32)
+//   k_backward    one CTA per tile: a half-warp per list entry walks the entry's footprint inside
+//                 the tile, accumulates the 9 2D gradients in registers, reduce-scatters them over
+//                 its 16 lanes and adds each total to the entry's 2D gradient slot (one atomic each)
 //   k_chain       per Gaussian with a gradient: 2D -> raw-parameter chain rule into a 128-B
 //                 record (11 raw gradients, clamped colour gradient, SH basis)
 //   k_adam        dense Adam streamed over float4 units of every parameter array
