@@ -57,7 +57,7 @@ def parse():
                     help="ICP tracking of every frame (Eq. 5, NEXT-3) instead of the given poses")
     ap.add_argument("--all-views", action="store_true",
                     help="every iteration renders all the round's views (SPEC S:471 variant, NEXT-4)")
-    ap.add_argument("--frames-ahead", type=int, default=0,
+    ap.add_argument("--frames-ahead", type=int, default=20,
                     help="the host enqueues at most this many frames ahead of the fusion stream (0: unbounded)")
     ap.add_argument("--no-frame-graphs", action="store_true",
                     help="launch each frame's fuse + raycast directly (the rounds stay graphs unless --no-graphs)")

@@ -39,7 +39,7 @@ class MappingPipeline:
                  overlap: bool = True, refine_priority: int = -1, manage_gaussians: bool = False,
                  add_cfg: A.AddConfig | None = None, remove_cfg: A.RemoveConfig | None = None,
                  all_views_per_iteration: bool = False, track: bool = False,
-                 icp_cfg: A.IcpConfig | None = None, graphs: bool = True, max_frames_ahead: int = 0,
+                 icp_cfg: A.IcpConfig | None = None, graphs: bool = True, max_frames_ahead: int = 20,
                  frame_graphs: bool | None = None, view_priority: int | None = None):
         self.cam, self.g, self.vol = cam, gaussians, volume
         self.graphs = graphs  # each refinement round as one CUDA graph (gps_refine_round)
