@@ -14,6 +14,7 @@ import collections
 import contextlib
 import ctypes as C
 import dataclasses
+import time
 
 import numpy as np
 import torch
@@ -49,6 +50,7 @@ class MappingPipeline:
         # unbounded): bounds the frames in flight, so the caching allocator stops growing
         self.max_ahead = max_frames_ahead
         self._inflight = collections.deque()
+        self.host_wait_s = 0.0  # host time spent waiting on that bound
         self.depth_scale = float(depth_scale)
         self.rcfg = render_cfg or A.RenderConfig()
         self.adam = adam_cfg or A.AdamConfig()
@@ -170,7 +172,9 @@ class MappingPipeline:
         """One frame of the mapping step.  `prefetch`: the next frame's (depth, rgba) host tensors,
         whose upload then overlaps this frame's kernels."""
         if self.max_ahead and len(self._inflight) >= self.max_ahead:
+            t0 = time.perf_counter()
             self._inflight.popleft().synchronize()
+            self.host_wait_s += time.perf_counter() - t0
         depth = self._device(depth)
         rgba = self._device(rgba)
         if prefetch is not None:
