@@ -41,7 +41,8 @@ class MappingPipeline:
                  add_cfg: A.AddConfig | None = None, remove_cfg: A.RemoveConfig | None = None,
                  all_views_per_iteration: bool = False, track: bool = False,
                  icp_cfg: A.IcpConfig | None = None, graphs: bool = True, max_frames_ahead: int = 20,
-                 frame_graphs: bool | None = None, view_priority: int | None = None):
+                 frame_graphs: bool | None = None, view_priority: int | None = None,
+                 upload_reserve_mb: int = 1024):
         self.cam, self.g, self.vol = cam, gaussians, volume
         self.graphs = graphs  # each refinement round as one CUDA graph (gps_refine_round)
         # each frame's fuse + raycast as one CUDA graph (gps_fuse_raycast; default: as `graphs`)
@@ -51,6 +52,11 @@ class MappingPipeline:
         self.max_ahead = max_frames_ahead
         self._inflight = collections.deque()
         self.host_wait_s = 0.0  # host time spent waiting on that bound
+        # device memory for the host-frame uploads, reserved in the copy stream's allocator pool
+        # at the first upload: a cudaMalloc while the GPU is busy blocked the host for 14-85 ms
+        # (measured), so the uploads must be served from cached blocks
+        self.upload_reserve_mb = upload_reserve_mb
+        self._reserved = False
         self.depth_scale = float(depth_scale)
         self.rcfg = render_cfg or A.RenderConfig()
         self.adam = adam_cfg or A.AdamConfig()
@@ -136,6 +142,11 @@ class MappingPipeline:
 
     def _upload(self, x: torch.Tensor):
         """Start the H2D copy of a pinned host tensor on the copy stream; (device tensor, event)."""
+        if not self._reserved:
+            self._reserved = True
+            if self.upload_reserve_mb > 0:
+                with torch.cuda.stream(self.copy_stream):
+                    torch.empty(self.upload_reserve_mb << 20, dtype=torch.uint8, device="cuda")
         with torch.cuda.stream(self.copy_stream):
             d = x.to("cuda", non_blocking=True)
             ev = torch.cuda.Event()
