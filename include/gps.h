@@ -10,7 +10,10 @@
  * estimated camera pose T_{g,k} ... update the SDF and color values in a global hash table;
  * afterwards the raycast is performed", then render with Eqs. 1-4 (Sec. 3.1) and
  * optimise with the L1 loss of Eq. 7 using Adam (App. C).
- * The four hot entry points are gps_fuse, gps_raycast, gps_render and gps_refine_step.
+ * The four hot entry points are gps_fuse, gps_raycast, gps_render and gps_refine_step;
+ * gps_fuse_raycast (a frame) and gps_refine_round (a round of iterations) run the same kernels
+ * in one call each, replayed as CUDA graphs (graph objects are the library's only host-side
+ * per-workspace / per-volume state; the executable graphs are created on first use).
  *
  * General conventions (apply to every function below)
  *  - Every pointer is a DEVICE pointer unless marked (host).  Device buffers are caller-owned,
