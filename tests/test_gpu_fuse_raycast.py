@@ -240,3 +240,33 @@ def test_fuse_raycast_graph_is_bitwise_the_two_calls():
         for a, b in zip(m0, m1):
             for x, y in zip(a, b):
                 assert (x is None and y is None) or torch.equal(x, y), mode
+
+
+def test_fuse_raycast_graph_error_leaves_stream_and_volume_usable():
+    """An argument error found inside the capture (depth_scale <= 0) ends the capture, launches
+    nothing and leaves the frame counter alone: the next frame on the same stream gives the
+    result of a volume that never saw the failed call."""
+    cfg = S.get_config("cfg2")
+    frs = H.frames(cfg, 2)
+    gcam, _ = H.cams(cfg)
+    (d0, c0), (d1, c1) = H.to_dev(frs[0]), H.to_dev(frs[1])
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    D = torch.empty((cfg.height, cfg.width), device="cuda")
+    C = torch.empty((cfg.height, cfg.width, 3), device="cuda")
+    a = H.gpu_volume(cfg)
+    b = H.gpu_volume(cfg)
+    import paper_2509_11574_b200 as G
+    with torch.cuda.stream(s):
+        a.fuse_raycast(gcam, frs[0].R, frs[0].t, d0, cfg.depth_scale, c0, D, C, graph=True, stream=s)
+        with pytest.raises(G._native.GPSError):
+            a.fuse_raycast(gcam, frs[1].R, frs[1].t, d1, 0.0, c1, D, C, graph=True, stream=s)
+        a.fuse_raycast(gcam, frs[1].R, frs[1].t, d1, cfg.depth_scale, c1, D, C, graph=True, stream=s)
+        b.fuse(gcam, frs[0].R, frs[0].t, d0, cfg.depth_scale, c0, stream=s)
+        b.fuse(gcam, frs[1].R, frs[1].t, d1, cfg.depth_scale, c1, stream=s)
+        Db, Cb, _ = b.raycast(gcam, frs[1].R, frs[1].t, stream=s)
+    torch.cuda.synchronize()
+    ca, va = H.sorted_blocks(*a.export_blocks())
+    cb, vb = H.sorted_blocks(*b.export_blocks())
+    assert np.array_equal(ca, cb) and np.array_equal(va.view(np.uint8), vb.view(np.uint8))
+    assert torch.equal(D, Db) and torch.equal(C, Cb)

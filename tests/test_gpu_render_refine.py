@@ -595,3 +595,26 @@ def test_refine_round_graph_as_the_first_call_of_a_process():
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and "OK" in out.stdout, out.stderr[-2000:]
+
+
+def test_refine_round_graph_error_inside_capture_leaves_stream_usable():
+    """A workspace too small for the round is found inside the capture: the capture ends, nothing
+    is launched, the step count is unchanged, and the next round on the same stream runs."""
+    import paper_2509_11574_b200 as G
+    cfg = S.get_config("cfg2")
+    frs = H.frames(cfg, 2, start=4)
+    cam, views = _round_views(G, cfg, frs, (0, 0, cfg.width, cfg.height))
+    g = G.Gaussians.from_dict(S.make_gaussians(cfg, n=4000))
+    st = G.AdamState(g)
+    ras = G.Rasterizer(g.n, cam, G.RenderConfig())
+    good = ras.ws
+    ras.ws = good[: good.numel() // 4]  # too small
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with pytest.raises(G._native.GPSError):
+        ras.refine_round(g, st, views, [[0], [1]], graph=True, stream=s)
+    assert st.step == 0
+    ras.ws = good
+    ras.refine_round(g, st, views, [[0], [1]], graph=True, stream=s)
+    torch.cuda.synchronize()
+    assert st.step == 2 and ras.loss.item() > 0
