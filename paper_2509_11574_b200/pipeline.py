@@ -6,7 +6,9 @@ PAPER.md P:106 (per-frame fusion then raycast), P:138 (views raycast once per ro
 All compute is in libgps's kernels (fusion and raycasts on the caller's stream, refinement on a
 second stream when overlap=True); this class only sequences calls and keeps the device buffers.
 Frames may be device tensors, or host tensors (copied in on a copy stream -- that is the
-end-to-end path).
+end-to-end path).  On a created (non-default) stream each frame's fuse + raycast and each round's
+iterations run as CUDA graphs (gps_fuse_raycast, gps_refine_round; graphs=False: direct
+launches); the host is held at most max_frames_ahead frames ahead of the device.
 """
 from __future__ import annotations
 
