@@ -60,3 +60,17 @@ def test_footprint_walk_division_is_exact():
         magic = (65536 + w - 1) // w
         for k in range(256):
             assert (k * magic) >> 16 == k // w, (w, k)
+
+
+def test_refine_round_rejects_uneven_view_lists_before_any_launch():
+    """The binding checks the round's per-iteration view lists (all the same length) on the host,
+    before it builds any argument for the library."""
+    from paper_2509_11574_b200 import api as A
+    ras = A.Rasterizer.__new__(A.Rasterizer)  # no workspace: the check comes first
+    with pytest.raises(ValueError):
+        ras.refine_round(None, None, [], [[0], [0, 1]])
+
+
+def test_graph_entry_points_are_declared():
+    syms = N.declared_symbols()
+    assert "gps_refine_round" in syms and "gps_fuse_raycast" in syms
