@@ -1,5 +1,3 @@
-GPS_LIB=ab/ca64/libgps.so timeout 900 python -m pytest tests/test_gpu_render_refine.py -q -x -k "fused or adam or round" 2>&1 | tail -1
-GPS_LIB=ab/pp128/libgps.so timeout 900 python -m pytest tests/test_gpu_render_refine.py -q -x -k "cfg1 or round" 2>&1 | tail -1
 for r in 1 2; do
-bash tools/ab.sh "--gpus 1 --steps 20 --warmup 5 --no-e2e --no-cpu-baseline" base pp128 ca64
+bash tools/ab.sh "--gpus 1 --steps 20 --warmup 5 --no-e2e --no-cpu-baseline" base ig4 ig12 ig16
 done
